@@ -1,0 +1,349 @@
+#!/usr/bin/env python
+"""Headline benchmark: batched DCF evaluation, 32-bit domain (BASELINE config 2).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Workload (BASELINE.json configs[1]): 2^24 independent DCF keys over a 32-bit
+domain, random thresholds, one random uint32 point per key; a step evaluates
+every key at its point (src/fss.py:288 dcf_eval == _walk_eval).  Synthetic,
+seeded inputs (keys generated on the device by ogm_fss_gen from seeded roots).
+
+* ``value``  -- evals/s with keys resident in HBM (9.1 GB > the 126 MB L2, so
+  no flush is needed between steps), device-timed with CUDA events.
+* ``e2e``    -- the same metric through the C ABI's host-buffer entry point
+  (ogm_fss_eval_points_host): pinned host keys -> H2D -> eval -> D2H bits,
+  every step, wall-clocked around the synchronous call.
+* ``roofline`` -- integer-ALU bound: algorithmic work is
+  2 int ops per AES table lookup of the minimal T-table walk (DCF: 31 levels x
+  (160 + 133) + 133 = 9216 lookups/eval), against the measured LOP3 issue
+  rate of this GPU (ogm_measure_int_peak).
+* ``cpu_baseline`` -- the CPU oracle port (oracle/, C, all host threads) on a
+  bounded sample of the same workload, rank 0 only.
+
+Multi-GPU: the key batch partitions (independent keys), so each rank
+evaluates its own 2^24 keys with no data-path collective: weak scaling,
+value = all ranks' evals / max-over-ranks time.
+
+``--impl reference`` times the reference algorithm's CPU implementation
+(the oracle port, all host threads) on the same config and prints the same
+JSON line with "impl": "reference".
+"""
+
+from __future__ import annotations
+
+import argparse
+import ctypes
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "dcf_evals_per_sec_32bit"
+UNIT = "evals/s"
+BITS = 32
+DEFAULT_KEYS = 1 << 24
+LOOKUPS = {"dcf": 31 * (160 + 133) + 133, "dpf": 32 * (160 + 133)}
+OPS_PER_LOOKUP = 2
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=10)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    p.add_argument("--kind", choices=["dcf", "dpf"], default="dcf")
+    p.add_argument("--keys", type=int, default=DEFAULT_KEYS)
+    p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-cpu", action="store_true")
+    p.add_argument("--cpu-seconds", type=float, default=10.0)
+    return p.parse_args()
+
+
+# ---------------------------------------------------------------------------
+# clocks
+# ---------------------------------------------------------------------------
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines: list[str] = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except OSError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        sms, maxes, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sms.append(float(parts[0]))
+                maxes.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, val in zip(names, parts[4:8]):
+                if val.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sms) if sms else None,
+                "sm_max_mhz": max(maxes) if maxes else None,
+                "reasons": sorted(reasons), "samples": len(sms)}
+
+
+# ---------------------------------------------------------------------------
+# CPU legs (oracle port; only here and in tests)
+# ---------------------------------------------------------------------------
+
+
+def cpu_keys(kind: str, n: int, seed: int):
+    import oracle
+    rng = np.random.default_rng(seed)
+    alphas = rng.integers(0, 1 << BITS, size=n, dtype=np.uint64)
+    pts = rng.integers(0, 1 << BITS, size=n, dtype=np.uint64)
+    r0 = rng.integers(0, 256, (n, 16), dtype=np.uint8)
+    r1 = rng.integers(0, 256, (n, 16), dtype=np.uint8)
+    k0, _ = oracle.tree_gen_batch(alphas, BITS, r0, r1, kind == "dcf")
+    return k0, pts
+
+
+def cpu_eval_rate(kind: str, target_seconds: float, threads: int):
+    """evals/s of the oracle port on a bounded sample sized to ~target_seconds."""
+    import oracle
+    k0, pts = cpu_keys(kind, 4096, 1)
+    t = time.perf_counter()
+    oracle.eval_points(k0, pts, nthreads=threads)
+    rate = 4096 / max(time.perf_counter() - t, 1e-6)
+    n = int(min(max(rate * target_seconds, 4096), 1 << 22)) // 32 * 32
+    k0, pts = cpu_keys(kind, n, 2)
+    t = time.perf_counter()
+    oracle.eval_points(k0, pts, nthreads=threads)
+    dt = time.perf_counter() - t
+    return n / dt, n, dt
+
+
+def cpu_model() -> str:
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import oracle
+    oracle.build()
+    threads = os.cpu_count() or 1
+    sample = 1 << 16
+    k0, pts = cpu_keys(args.kind, sample, 3)
+    for _ in range(args.warmup):
+        oracle.eval_points(k0, pts, nthreads=threads)
+    times = []
+    for _ in range(args.steps):
+        t = time.perf_counter()
+        oracle.eval_points(k0, pts, nthreads=threads)
+        times.append(time.perf_counter() - t)
+    tot = sum(times)
+    value = sample * args.steps / tot
+    desc = (f"{sample} of the {args.keys} keys per step ({args.kind.upper()}, 32-bit domain), "
+            f"oracle/ C port of src/fss.py:257-281, {threads} threads on {cpu_model()}")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32",
+        "data": "synthetic", "config": {"workload": f"C2 batched {args.kind.upper()} micro",
+                                        "keys": args.keys, "domain_bits": BITS, "points_per_key": 1},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port", "sample": desc},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# GPU leg
+# ---------------------------------------------------------------------------
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+    import torch
+    import torch.distributed as dist
+
+    from paper_2209_03526_b200 import _lib, fss
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    lib = _lib.load()
+    _lib.check(lib.ogm_init())
+
+    K = args.keys
+    comparison = args.kind == "dcf"
+    gen = torch.Generator(device="cuda").manual_seed(1234 + rank)
+    alphas = torch.randint(-(1 << 31), 1 << 31, (K,), dtype=torch.int32, device="cuda", generator=gen)
+    pts = torch.randint(-(1 << 31), 1 << 31, (K,), dtype=torch.int32, device="cuda", generator=gen)
+    r0 = torch.randint(0, 256, (K, 16), dtype=torch.uint8, device="cuda", generator=gen)
+    r1 = torch.randint(0, 256, (K, 16), dtype=torch.uint8, device="cuda", generator=gen)
+    b0, b1 = fss.gen_batch(comparison, BITS, alphas, r0, r1)
+    del r1
+    out = torch.empty(((K + 31) // 32,), dtype=torch.int32, device="cuda")
+    torch.cuda.synchronize()
+
+    # correctness gate on the bench inputs: pair XOR == indicator
+    o1 = torch.empty_like(out)
+    fss.eval_points(b0, pts, out)
+    fss.eval_points(b1, pts, o1)
+    x = (out ^ o1).cpu().numpy().view(np.uint8)
+    got = np.unpackbits(x, bitorder="little")[:K]
+    a = alphas.cpu().numpy().view(np.uint32)
+    p = pts.cpu().numpy().view(np.uint32)
+    want = (p < a) if comparison else (p == a)
+    if not np.array_equal(got, want.astype(np.uint8)):
+        raise SystemExit("bench correctness gate failed: pair XOR != indicator")
+    del o1, b1
+
+    peak = ctypes.c_double()
+    secs = ctypes.c_double()
+    _lib.check(lib.ogm_measure_int_peak(ctypes.byref(peak), ctypes.byref(secs)))
+
+    stream = torch.cuda.current_stream()
+    for _ in range(args.warmup):
+        fss.eval_points(b0, pts, out)
+    torch.cuda.synchronize()
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.3)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
+    ev[0].record(stream)
+    for s in range(args.steps):
+        fss.eval_points(b0, pts, out)
+        ev[s + 1].record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clk = clocks.stop()
+    per_launch = [ev[i].elapsed_time(ev[i + 1]) for i in range(args.steps)]
+    total_ms = ev[0].elapsed_time(ev[-1])
+    t = torch.tensor([total_ms], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    max_ms = float(t.item())
+    ms_per_step = max_ms / args.steps
+    value = world * K * args.steps / (max_ms * 1e-3)
+    avg_launch_s = statistics.mean(per_launch) * 1e-3
+    ops_per_eval = OPS_PER_LOOKUP * LOOKUPS[args.kind]
+    achieved = K * ops_per_eval / avg_launch_s
+    roofline = {"bound": "int_alu", "achieved": achieved / 1e12, "peak": peak.value / 1e12,
+                "unit": "Tops/s", "frac": achieved / peak.value, "traffic": None,
+                "ops_per_eval": ops_per_eval, "aes_lookups_per_eval": LOOKUPS[args.kind],
+                "peak_source": "ogm_measure_int_peak (LOP3 issue rate, this run)",
+                "key_bytes_per_eval": 16 + 16 * (BITS - (1 if comparison else 0)) + 12 + 1 + 4}
+
+    # end-to-end through the C ABI from pinned host buffers
+    e2e = None
+    if not args.no_e2e:
+        host = [t_.cpu().pin_memory() for t_ in (b0.root, b0.seed_cw, b0.ctrl, b0.flags, pts)]
+        hout = torch.zeros(((K + 31) // 32,), dtype=torch.int32).pin_memory()
+        kind = _lib.KIND_DCF if comparison else _lib.KIND_DPF
+        fn = lib.ogm_fss_eval_points_host
+        argv = [kind, BITS, K, *(_lib.ptr(h) for h in host), _lib.ptr(hout)]
+        _lib.check(fn(*argv))  # warm-up (allocates the staging buffers)
+        if not np.array_equal(hout.numpy(), out.cpu().numpy()):
+            raise SystemExit("e2e result differs from the device-resident result")
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            _lib.check(fn(*argv))
+        el = time.perf_counter() - t0
+        tt = torch.tensor([el], dtype=torch.float64, device="cuda")
+        if world > 1:
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        h2d = sum(h.numel() * h.element_size() for h in host)
+        e2e = {"value": world * K * args.steps / float(tt.item()), "unit": UNIT,
+               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": hout.numel() * 4,
+               "ms_per_step": 1e3 * float(tt.item()) / args.steps}
+        del host, hout
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        import oracle
+        oracle.build()
+        threads = os.cpu_count() or 1
+        rate, n, dt = cpu_eval_rate(args.kind, args.cpu_seconds, threads)
+        cpu = {"value": rate, "unit": UNIT, "cores": threads, "kind": "port",
+               "sample": f"{n} keys x 1 point ({args.kind.upper()}, 32-bit) in {dt:.1f}s, "
+                         f"oracle/ C port of src/fss.py:257-281 on {cpu_model()}"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
+            "config": {"workload": f"C2 batched {args.kind.upper()} micro (BASELINE configs[1])",
+                       "keys_per_gpu": K, "domain_bits": BITS, "points_per_key": 1,
+                       "parallelism": f"key-sharded x{world}",
+                       "l2": "inputs (9.1 GB of keys) larger than L2; no flush"},
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+            "gpu_launches": args.steps, "clocks": clk,
+            "launch_ms": {"mean": statistics.mean(per_launch), "min": min(per_launch),
+                          "max": max(per_launch)},
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

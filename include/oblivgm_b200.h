@@ -1,0 +1,138 @@
+/*
+ * oblivgm_b200.h -- C ABI of the B200-native OblivGM hot path (libogm_b200.so).
+ *
+ * The reference (oblivgm 0.1.0, /root/reference/pkg/src/oblivgm, abbreviated
+ * src/) is pure Python and has no FFI of its own: its "operator interface" is
+ * a set of module-level functions over numpy arrays.  Every entry point below
+ * replaces one of those functions (cited per entry); the Python package
+ * paper_2209_03526_b200 keeps the reference names and signatures and binds
+ * these symbols with ctypes (see INTEGRATION.md for the binding a maintainer
+ * of the reference would add).
+ *
+ * Conventions
+ *  - Plain pointers and sizes only.  Pointers are DEVICE pointers unless the
+ *    entry point name ends in _host.  `stream` is a cudaStream_t (NULL =
+ *    legacy default stream).  Calls are asynchronous on `stream` unless
+ *    documented otherwise; the library holds no global mutable state besides
+ *    per-device constant tables, so distinct host threads may drive distinct
+ *    streams concurrently (one per logical party, src/net.py:320-351).
+ *  - Return value: 0 on success, a negative OGM_ERR_* code otherwise; the
+ *    message is available from ogm_last_error() (thread-local).  The Python
+ *    shim maps OGM_ERR_DOMAIN to fss.DomainError (src/fss.py:44-45),
+ *    OGM_ERR_ARG to ValueError, OGM_ERR_PROTOCOL to net.ProtocolError
+ *    (src/net.py:38-39).
+ *  - Bit vectors: bit i lives at bit i%32 of uint32 word i/32, bits past the
+ *    logical length are zero (src/bits.py:1-8).  Share matrices are row-major
+ *    (rows, pitch) uint32 with pitch >= ceil(width/32) words.
+ *  - 16-byte seeds are the little-endian image of (lo, hi) uint64
+ *    (src/prf.py:60-67).
+ *  - FSS key batches are structure-of-arrays, level-major, so that thread k
+ *    of a warp reads key k with coalesced 128-bit loads:
+ *        root    [K][16 B]
+ *        seed_cw [bits][K][16 B]       (src/fss.py:62 seed_cw[lvl])
+ *        ctrl    [3][K] uint32         word 0 bit lvl = tau_L, word 1 = tau_R,
+ *                                      word 2 = value bit (src/fss.py:63)
+ *        flags   [K] uint8             bit0 root_t, bit1 final_cw,
+ *                                      bit2 add_const (src/fss.py:59-65)
+ *    so domain_bits is limited to 1..32 (graph dictionaries and BASELINE
+ *    config 2 are all <= 32 bits).
+ */
+#ifndef OBLIVGM_B200_H
+#define OBLIVGM_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define OGM_OK 0
+#define OGM_ERR_ARG -1      /* ValueError: length / width / party mismatch   */
+#define OGM_ERR_DOMAIN -2   /* fss.DomainError: point or threshold outside    */
+#define OGM_ERR_CUDA -3     /* CUDA runtime failure                           */
+#define OGM_ERR_PROTOCOL -4 /* net.ProtocolError: label / table id mismatch   */
+#define OGM_ERR_NOMEM -5    /* device allocation failure                      */
+
+#define OGM_KIND_DPF 0 /* point function, src/fss.py:160-164      */
+#define OGM_KIND_DCF 1 /* comparison function, src/fss.py:167-171 */
+
+/* ---- library ----------------------------------------------------------- */
+
+/* Thread-local message of the last failing call. */
+const char* ogm_last_error(void);
+/* ABI version (bumped on any signature change). */
+int ogm_abi_version(void);
+/* Upload the AES tables and fixed PRG round keys to the current device.
+ * Idempotent per device; every other entry point calls it lazily. */
+int ogm_init(void);
+
+/* ---- L0 randomness (src/prf.py) ----------------------------------------- */
+
+/* src/prf.py:41-57 prg_expand.  seeds/left/right: n x 16 B; t_left, t_right,
+ * value: n bytes (0/1). */
+int ogm_prg_expand(const void* seeds, int64_t n, void* left, void* right, uint8_t* t_left,
+                   uint8_t* t_right, uint8_t* value, void* stream);
+
+/* src/prf.py:70-92 prf_stream / prf_words: AES-128-CTR keystream of
+ * (key, label, index) as uint32 LE words, starting at word `first_word`
+ * (random access by block).  key/label are HOST pointers (16 / 4 bytes). */
+int ogm_prf_words(const uint8_t* key, const uint8_t* label, uint64_t index, uint64_t first_word,
+                  int64_t nwords, uint32_t* out, void* stream);
+
+/* src/rss.py:143-148 ZeroShareContext.next_share at counter `counter`:
+ * out = F(key_own, "ZSHR", counter) ^ F(key_prev, "ZSHR", counter), masked to
+ * nbits.  If `xor_into` is non-NULL the share is XORed into it instead
+ * (out may equal xor_into).  Keys are HOST pointers. */
+int ogm_zero_share(const uint8_t* key_own, const uint8_t* key_prev, uint64_t counter,
+                   int64_t nbits, const uint32_t* xor_into, uint32_t* out, void* stream);
+
+/* src/prf.py:95-105 seeded_permutation: Fisher-Yates driven by
+ * prf_stream(key, label, index, 8(n-1)); bit-exact, computed on the device by
+ * deterministic reservations.  perm: n int32 (gather semantics, M[perm]).
+ * workspace: >= ogm_perm_workspace_bytes(n) bytes of device memory. */
+int64_t ogm_perm_workspace_bytes(int64_t n);
+int ogm_seeded_permutation(const uint8_t* key, const uint8_t* label, uint64_t index, int64_t n,
+                           int32_t* perm, void* workspace, void* stream);
+
+/* ---- L1 function secret sharing (src/fss.py) ---------------------------- */
+
+/* src/fss.py:116-157 _tree_gen, batched over K independent keys with
+ * injected roots (the reference draws root0, root1 with rng.bytes(16),
+ * src/fss.py:117-118).  alphas: K uint32 (< 2^bits).  Writes the shared
+ * correction words (seed_cw [bits][K][16 B], ctrl [3][K]) and final_cw [K]. */
+int ogm_fss_gen(int kind, int bits, int64_t K, const uint32_t* alphas, const void* roots0,
+                const void* roots1, void* seed_cw, uint32_t* ctrl, uint8_t* final_cw,
+                void* stream);
+
+/* src/fss.py:257-299 _walk_eval / dpf_eval / dcf_eval: one point per key,
+ * one thread per (key, point).  out_bits: ceil(K/32) words, bit k = key k. */
+int ogm_fss_eval_points(int kind, int bits, int64_t K, const void* root, const void* seed_cw,
+                        const uint32_t* ctrl, const uint8_t* flags, const uint32_t* points,
+                        uint32_t* out_bits, void* stream);
+
+/* Same computation from HOST buffers (the end-to-end call a CPU caller
+ * makes): copies keys/points in, evaluates, copies the packed bits out and
+ * synchronizes.  Host buffers should be pinned for full PCIe bandwidth.
+ * The transfer is chunked and overlapped with evaluation on two streams. */
+int ogm_fss_eval_points_host(int kind, int bits, int64_t K, const void* root_h,
+                             const void* seed_cw_h, const uint32_t* ctrl_h, const uint8_t* flags_h,
+                             const uint32_t* points_h, uint32_t* out_bits_h);
+
+/* src/fss.py:302-344 _full_domain_tree / full_domain_eval for `nkeys` keys
+ * of one batch (layout above with K = nkeys), each over points [0, n).
+ * out_words: nkeys x pitch words (pitch >= ceil(n/32)), row k = key k. */
+int ogm_fss_full_domain(int kind, int bits, int nkeys, const void* root, const void* seed_cw,
+                        const uint32_t* ctrl, const uint8_t* flags, int64_t n, uint32_t* out_words,
+                        int64_t pitch, void* stream);
+
+/* ---- measurement -------------------------------------------------------- */
+
+/* Roofline denominator for the integer-ALU-bound kernels: issue rate of
+ * independent LOP3 chains over the whole device (32-bit lane-ops per second),
+ * timed with CUDA events on the legacy stream.  Synchronous. */
+int ogm_measure_int_peak(double* ops_per_sec, double* seconds);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,98 @@
+"""ctypes binding of libogm_b200.so (the C ABI in include/oblivgm_b200.h).
+
+The product path has no CPU fallback: if the shared library is missing, or no
+CUDA device is visible, every call raises.  Return codes map to the
+reference's exception types (src/fss.py:44-45 DomainError, src/net.py:38-39
+ProtocolError, ValueError for shape/length errors).
+"""
+
+from __future__ import annotations
+
+import ctypes
+from pathlib import Path
+
+import torch
+
+from .errors import DomainError, ProtocolError
+
+LIB_PATH = Path(__file__).resolve().parent / "libogm_b200.so"
+
+OGM_ERR_ARG = -1
+OGM_ERR_DOMAIN = -2
+OGM_ERR_CUDA = -3
+OGM_ERR_PROTOCOL = -4
+OGM_ERR_NOMEM = -5
+
+KIND_DPF = 0
+KIND_DCF = 1
+
+_vp = ctypes.c_void_p
+_i64 = ctypes.c_int64
+_u64 = ctypes.c_uint64
+_int = ctypes.c_int
+_cp = ctypes.c_char_p
+
+# name -> argtypes (every symbol declared in include/oblivgm_b200.h)
+SIGNATURES = {
+    "ogm_last_error": ([], ctypes.c_char_p),
+    "ogm_abi_version": ([], _int),
+    "ogm_init": ([], _int),
+    "ogm_prg_expand": ([_vp, _i64, _vp, _vp, _vp, _vp, _vp, _vp], _int),
+    "ogm_prf_words": ([_cp, _cp, _u64, _u64, _i64, _vp, _vp], _int),
+    "ogm_zero_share": ([_cp, _cp, _u64, _i64, _vp, _vp, _vp], _int),
+    "ogm_perm_workspace_bytes": ([_i64], _i64),
+    "ogm_seeded_permutation": ([_cp, _cp, _u64, _i64, _vp, _vp, _vp], _int),
+    "ogm_fss_gen": ([_int, _int, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp], _int),
+    "ogm_fss_eval_points": ([_int, _int, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp], _int),
+    "ogm_fss_eval_points_host": ([_int, _int, _i64, _vp, _vp, _vp, _vp, _vp, _vp], _int),
+    "ogm_fss_full_domain": ([_int, _int, _int, _vp, _vp, _vp, _vp, _i64, _vp, _i64, _vp], _int),
+    "ogm_measure_int_peak": ([ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double)], _int),
+}
+
+_lib = None
+
+
+def load(require_device: bool = True):
+    """Load the library (and, by default, insist on a CUDA device)."""
+    global _lib
+    if _lib is None:
+        if not LIB_PATH.exists():
+            raise RuntimeError(
+                f"{LIB_PATH} is missing: build it with `python -m paper_2209_03526_b200.build` "
+                "(there is no CPU fallback)")
+        lib = ctypes.CDLL(str(LIB_PATH))
+        for name, (args, res) in SIGNATURES.items():
+            fn = getattr(lib, name)
+            fn.argtypes = args
+            fn.restype = res
+        _lib = lib
+    if require_device and not torch.cuda.is_available():
+        raise RuntimeError("paper_2209_03526_b200 needs a CUDA device (no CPU fallback)")
+    return _lib
+
+
+def check(rc: int) -> None:
+    if rc == 0:
+        return
+    msg = (_lib.ogm_last_error() or b"").decode(errors="replace")
+    if rc == OGM_ERR_DOMAIN:
+        raise DomainError(msg)
+    if rc == OGM_ERR_PROTOCOL:
+        raise ProtocolError(msg)
+    if rc == OGM_ERR_ARG:
+        raise ValueError(msg)
+    raise RuntimeError(f"libogm_b200 error {rc}: {msg}")
+
+
+def call(name: str, *args) -> None:
+    lib = load()
+    check(getattr(lib, name)(*args))
+
+
+def ptr(t: torch.Tensor | None):
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def stream_ptr(stream: torch.cuda.Stream | None = None):
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return ctypes.c_void_p(s.cuda_stream)
