@@ -125,6 +125,91 @@ int ogm_fss_full_domain(int kind, int bits, int nkeys, const void* root, const v
                         const uint32_t* ctrl, const uint8_t* flags, int64_t n, uint32_t* out_words,
                         int64_t pitch, void* stream);
 
+/* ---- L1 replicated secret sharing (src/rss.py) ---------------------------- */
+
+/* src/rss.py:143-148 for all three co-resident parties at once:
+ * out[q] = F(key_q) ^ F(key_{q-1}) (^ xor_into[q]), keys k1, k2, k3 as held
+ * by src/net.py:221-233.  xor_into may be NULL (or have NULL entries). */
+int ogm_zero_share_trio(const uint8_t* k1, const uint8_t* k2, const uint8_t* k3, uint64_t counter,
+                        int64_t nbits, const uint32_t* const* xor_into, uint32_t* const* out,
+                        void* stream);
+
+/* src/rss.py:115-126 and_terms for nparty (1..3) parties: out[q] =
+ * a_a[q]&b_a[q] ^ a_a[q]&b_b[q] ^ a_b[q]&b_a[q] over nwords words. */
+int ogm_and_terms(int64_t nwords, int nparty, const uint32_t* const* a_a, const uint32_t* const* a_b,
+                  const uint32_t* const* b_a, const uint32_t* const* b_b, uint32_t* const* out,
+                  void* stream);
+
+/* Word-wise out = a ^ b (^ c if non-NULL): the local XOR of shares
+ * (src/rss.py:53-59, src/engine.py:164,182,188). */
+int ogm_xor_words(int64_t nwords, const uint32_t* a, const uint32_t* b, const uint32_t* c,
+                  uint32_t* out, void* stream);
+
+/* ---- L3 protocol engine (src/engine.py) ---------------------------------- */
+
+/* src/engine.py:76-80 + :162 (secEval's local step, both interval passes
+ * in one read of the shares).  nparty = 1: comps = {A, B} (the party's two
+ * share matrices); nparty = 3: comps = {x1, x2, x3} and party q reads
+ * (x_q, x_{q+1}).  a_idx/b_idx must state that mapping.  ind[(p*nparty+q)*2
+ * + {0,1}] = full-domain indicator words of pass p's first / second key
+ * (src/engine.py:160-161); out[p*nparty+q] = ceil(rows/32) words. */
+int ogm_masked_parity(int64_t rows, int64_t words, int64_t pitch, int ncomp, const uint32_t* const* comps,
+                      int nparty, const int32_t* a_idx, const int32_t* b_idx, int npass,
+                      const uint32_t* const* ind, uint32_t* const* out, void* stream);
+
+/* src/engine.py:95-102 _select_one_additive for nparty parties (Case I
+ * fetch, src/engine.py:197-217, and the posting fold of sec_access,
+ * src/engine.py:309-311): out[q] (words) = XOR over rows c of
+ * fa_q(c)(A_q[c]^B_q[c]) ^ fb_q(c) A_q[c], with fa/fb bit vectors. */
+int ogm_select_fold(int64_t rows, int64_t words, int64_t pitch, int nparty, const uint32_t* const* A,
+                    const uint32_t* const* B, const uint32_t* const* fa, const uint32_t* const* fb,
+                    uint32_t* const* out, void* stream);
+
+/* src/engine.py:105-120 _select_many_additive: out (K, opitch) =
+ * sel_a (K x X one-hot rows) * (A ^ B) ^ sel_b * A over GF(2), A/B (X, pitch).
+ * workspace: >= 8*X bytes. */
+int ogm_select_many(int64_t K, int64_t X, int64_t words, int64_t pitch, const uint32_t* sel_a,
+                    const uint32_t* sel_b, int64_t spitch, const uint32_t* A, const uint32_t* B,
+                    uint32_t* out, int64_t opitch, void* workspace, void* stream);
+
+/* src/engine.py:227-233 / :317-318 row building: out row r = flag(r) ||
+ * field_0[r] || ... (bit-concatenated at their logical widths, LE, clean
+ * tail).  flag_bits (rows bits) may be NULL. */
+int ogm_pack_fields(int64_t rows, const uint32_t* flag_bits, int nfields, const uint32_t* const* fields,
+                    const int64_t* fpitch, const int64_t* fwidth, uint32_t* out, int64_t opitch,
+                    void* stream);
+
+/* src/engine.py:249-269 / :331-334 field slicing: out[k] = bits
+ * [bit_offset, bit_offset+width) of src row idx[k] (idx NULL = identity). */
+int ogm_extract_field(const uint32_t* src, int64_t spitch, const int32_t* idx, int64_t n,
+                      int64_t bit_offset, int64_t width, uint32_t* out, int64_t opitch, void* stream);
+
+/* src/engine.py:241-245: bit r of out_bits = mat[r][0] & 1 (flag column). */
+int ogm_column_bits(const uint32_t* mat, int64_t pitch, int64_t rows, uint32_t* out_bits, void* stream);
+
+/* src/engine.py:252 / :327 np.nonzero of an opened mask: indices of set
+ * bits in order, count to *out_count (device int64). */
+int64_t ogm_compact_workspace_bytes(int64_t n);
+int ogm_compact_bits(int64_t n, const uint32_t* bits, int32_t* out_idx, int64_t* out_count,
+                     void* workspace, int64_t workspace_bytes, void* stream);
+
+/* ---- L1 shuffle (src/shuffle.py) ------------------------------------------ */
+
+/* One party-local step of sec_shuffle (src/shuffle.py:106-143):
+ *   k2 = perm_outer ? perm_outer[i] : i;  k1 = perm_inner ? perm_inner[k2] : k2
+ *   out[i] = m1[k1] ^ m2[k1] ^ T1[k1] ^ T2[k2] ^ m3[i] ^ R[i]
+ * Each blinding table term is either a precomputed matrix (*_mat) or an
+ * AES-CTR table generated on the fly from (key, label, index) with
+ * src/shuffle.py:69-73 layout; all-NULL = absent.  Rows are `words` words
+ * wide (= ceil(width_bits/32)), densely packed. */
+int ogm_shuffle_gather(int64_t rows, int64_t words, int64_t width_bits, const int32_t* perm_outer,
+                       const int32_t* perm_inner, const uint32_t* m1, const uint32_t* m2,
+                       const uint32_t* m3, const uint8_t* t1_key, const uint8_t* t1_label,
+                       uint64_t t1_index, const uint32_t* t1_mat, const uint8_t* t2_key,
+                       const uint8_t* t2_label, uint64_t t2_index, const uint32_t* t2_mat,
+                       const uint8_t* r_key, const uint8_t* r_label, uint64_t r_index,
+                       const uint32_t* r_mat, uint32_t* out, void* stream);
+
 /* ---- measurement -------------------------------------------------------- */
 
 /* Roofline denominator for the integer-ALU-bound kernels: issue rate of

@@ -46,6 +46,19 @@ SIGNATURES = {
     "ogm_fss_eval_points": ([_int, _int, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp], _int),
     "ogm_fss_eval_points_host": ([_int, _int, _i64, _vp, _vp, _vp, _vp, _vp, _vp], _int),
     "ogm_fss_full_domain": ([_int, _int, _int, _vp, _vp, _vp, _vp, _i64, _vp, _i64, _vp], _int),
+    "ogm_zero_share_trio": ([_cp, _cp, _cp, _u64, _i64, _vp, _vp, _vp], _int),
+    "ogm_and_terms": ([_i64, _int, _vp, _vp, _vp, _vp, _vp, _vp], _int),
+    "ogm_xor_words": ([_i64, _vp, _vp, _vp, _vp, _vp], _int),
+    "ogm_masked_parity": ([_i64, _i64, _i64, _int, _vp, _int, _vp, _vp, _int, _vp, _vp, _vp], _int),
+    "ogm_select_fold": ([_i64, _i64, _i64, _int, _vp, _vp, _vp, _vp, _vp, _vp], _int),
+    "ogm_select_many": ([_i64, _i64, _i64, _i64, _vp, _vp, _i64, _vp, _vp, _vp, _i64, _vp, _vp], _int),
+    "ogm_pack_fields": ([_i64, _vp, _int, _vp, _vp, _vp, _vp, _i64, _vp], _int),
+    "ogm_extract_field": ([_vp, _i64, _vp, _i64, _i64, _i64, _vp, _i64, _vp], _int),
+    "ogm_column_bits": ([_vp, _i64, _i64, _vp, _vp], _int),
+    "ogm_compact_workspace_bytes": ([_i64], _i64),
+    "ogm_compact_bits": ([_i64, _vp, _vp, _vp, _vp, _i64, _vp], _int),
+    "ogm_shuffle_gather": ([_i64, _i64, _i64, _vp, _vp, _vp, _vp, _vp, _cp, _cp, _u64, _vp, _cp, _cp, _u64,
+                            _vp, _cp, _cp, _u64, _vp, _vp, _vp], _int),
     "ogm_measure_int_peak": ([ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double)], _int),
 }
 
@@ -91,6 +104,28 @@ def call(name: str, *args) -> None:
 
 def ptr(t: torch.Tensor | None):
     return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def ptr_array(tensors) -> ctypes.Array:
+    """Host array of device pointers (NULL for None) for the const T* const* args."""
+    arr = (ctypes.c_void_p * max(1, len(tensors)))()
+    for i, t in enumerate(tensors):
+        arr[i] = None if t is None else t.data_ptr()
+    return arr
+
+
+def int_array(vals) -> ctypes.Array:
+    arr = (ctypes.c_int32 * max(1, len(vals)))()
+    for i, v in enumerate(vals):
+        arr[i] = int(v)
+    return arr
+
+
+def i64_array(vals) -> ctypes.Array:
+    arr = (ctypes.c_int64 * max(1, len(vals)))()
+    for i, v in enumerate(vals):
+        arr[i] = int(v)
+    return arr
 
 
 def stream_ptr(stream: torch.cuda.Stream | None = None):

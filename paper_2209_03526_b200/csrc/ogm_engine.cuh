@@ -1,6 +1,642 @@
-// ogm_engine.cuh -- secEval / combine / fetch kernels (src/engine.py, src/rss.py).
+// ogm_engine.cuh -- secEval / combine / fetch / access kernels for sm_100a
+// (src/engine.py, src/rss.py).  These are HBM-bound streaming kernels over
+// row-major (rows, pitch) uint32 share matrices; no tensor cores, no FP.
+//
+// Party mapping: with the three logical servers co-resident on one GPU, each
+// share component x_j is stored once; party q holds (x_q, x_{q+1})
+// (src/graphs.py:382-399).  Kernels take component pointers plus per-party
+// component indices, so a "trio" launch reads every component once for all
+// three parties while a per-party launch (the drop-in path, one CUDA stream
+// per party thread) reads only its own two.
 #pragma once
+
+#include <cub/cub.cuh>
+
+#include "ogm_aes.cuh"
 #include "ogm_common.cuh"
+#include "ogm_host.cuh"
+
 namespace ogm {
-int engine_init() { return OGM_OK; }
+
+constexpr int kMaxComp = 3;
+constexpr int kMaxParty = 3;
+constexpr int kMaxPass = 2;
+
+// ---------------------------------------------------------------------------
+// src/engine.py:76-80 + :162 (interval passes :147-164): per candidate row c,
+// additive bit = parity((A[c] & IA) ^ (B[c] & IB)) for every (pass, party).
+// G lanes cooperate on a row (G chosen on the host from the row length), a
+// warp owns 32 consecutive rows so every output word is assembled from
+// ballots.  Indicator vectors are re-read through L1 (__ldg), share rows are
+// streamed once from HBM with 128-bit loads when aligned.
+// ---------------------------------------------------------------------------
+struct ParityArgs {
+    const uint32_t* comp[kMaxComp];
+    const uint32_t* ind[kMaxPass * kMaxParty * 2];
+    uint32_t* out[kMaxPass * kMaxParty];
+    int a_idx[kMaxParty], b_idx[kMaxParty];
+    int ncomp, nparty, npass, G;
+    int64_t rows, words, pitch;
+};
+
+template <bool VEC4, int NPARTY, int NPASS>
+__global__ void __launch_bounds__(256) masked_parity_kernel(const ParityArgs p) {
+    constexpr int NJ = NPARTY * NPASS;
+    constexpr int NCOMP = NPARTY == 1 ? 2 : 3;  // per party: (A, B); trio: x1, x2, x3
+    const int lane = threadIdx.x & 31;
+    const int G = p.G;
+    const int rows_per_pass = 32 / G;
+    const int sub = lane % G;
+    const int64_t tiles = (p.rows + 31) >> 5;
+    const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+    const int64_t nvec = VEC4 ? (p.words >> 2) : 0;
+    const int64_t tail0 = nvec << 2;
+    for (int64_t tile = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); tile < tiles;
+         tile += warps) {
+        uint32_t outw[NJ];
+#pragma unroll
+        for (int j = 0; j < NJ; j++) outw[j] = 0;
+        for (int ps = 0; ps < G; ps++) {
+            const int64_t row = (tile << 5) + ps * rows_per_pass + lane / G;
+            uint32_t acc[NJ];
+#pragma unroll
+            for (int j = 0; j < NJ; j++) acc[j] = 0;
+            if (row < p.rows) {
+                const uint32_t* rp[NCOMP];
+#pragma unroll
+                for (int c = 0; c < NCOMP; c++) rp[c] = p.comp[c] + row * p.pitch;
+                if (VEC4) {
+                    for (int64_t u = sub; u < nvec; u += G) {
+                        uint4 cv[NCOMP];
+#pragma unroll
+                        for (int c = 0; c < NCOMP; c++) cv[c] = __ldcs(reinterpret_cast<const uint4*>(rp[c]) + u);
+#pragma unroll
+                        for (int ps2 = 0; ps2 < NPASS; ps2++) {
+#pragma unroll
+                            for (int q = 0; q < NPARTY; q++) {
+                                const int j = ps2 * NPARTY + q;
+                                const uint4 ia = __ldg(reinterpret_cast<const uint4*>(p.ind[2 * j]) + u);
+                                const uint4 ib = __ldg(reinterpret_cast<const uint4*>(p.ind[2 * j + 1]) + u);
+                                const uint4 A = cv[q], B = cv[(q + 1) % NCOMP];
+                                acc[j] ^= ((A.x & ia.x) ^ (B.x & ib.x)) ^ ((A.y & ia.y) ^ (B.y & ib.y)) ^
+                                          ((A.z & ia.z) ^ (B.z & ib.z)) ^ ((A.w & ia.w) ^ (B.w & ib.w));
+                            }
+                        }
+                    }
+                }
+                for (int64_t w = tail0 + sub; w < p.words; w += G) {
+                    uint32_t cv[NCOMP];
+#pragma unroll
+                    for (int c = 0; c < NCOMP; c++) cv[c] = __ldcs(rp[c] + w);
+#pragma unroll
+                    for (int ps2 = 0; ps2 < NPASS; ps2++) {
+#pragma unroll
+                        for (int q = 0; q < NPARTY; q++) {
+                            const int j = ps2 * NPARTY + q;
+                            acc[j] ^= (cv[q] & __ldg(p.ind[2 * j] + w)) ^
+                                      (cv[(q + 1) % NCOMP] & __ldg(p.ind[2 * j + 1] + w));
+                        }
+                    }
+                }
+            }
+            // XOR-reduce each row's G lanes (aligned groups), then ballot.
+#pragma unroll
+            for (int j = 0; j < NJ; j++) {
+                uint32_t a = acc[j];
+                for (int off = G >> 1; off > 0; off >>= 1) a ^= __shfl_xor_sync(0xffffffffu, a, off);
+                const bool leader = sub == 0 && row < p.rows;
+                const uint32_t b = __ballot_sync(0xffffffffu, leader && (__popc(a) & 1));
+                if (G == 1) {
+                    outw[j] = b;
+                } else {
+                    uint32_t packed = 0;
+                    for (int g = 0; g < rows_per_pass; g++) packed |= ((b >> (g * G)) & 1u) << g;
+                    outw[j] |= packed << (ps * rows_per_pass);
+                }
+            }
+        }
+        if (lane == 0) {
+#pragma unroll
+            for (int j = 0; j < NJ; j++) p.out[j][tile] = outw[j];
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// src/rss.py:143-148 for all three parties at once: alpha_q = F(k_q) ^
+// F(k_{q-1}) (party q holds its own key and its predecessor's,
+// src/net.py:229-232), optionally XORed into per-party buffers.  3 AES per
+// 16-byte block instead of 6.
+// ---------------------------------------------------------------------------
+struct Zs3Args {
+    AesKeySched k[3];
+    const uint32_t* xin[3];
+    uint32_t* out[3];
+};
+
+__global__ void __launch_bounds__(kAesThreads) zero_share3_kernel(const Zs3Args a, uint32_t label_be,
+                                                                   uint64_t counter, int64_t nwords,
+                                                                   int64_t nbits) {
+    extern __shared__ __align__(128) uint8_t smem_raw[];
+    aes_fill_tables(smem_raw);
+    __syncthreads();
+    const AesTab T(smem_raw);
+    const int64_t nblk = (nwords + 3) >> 2;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b < nblk; b += stride) {
+        const uint4 ctr = ctr_block(label_be, counter, (uint64_t)b);
+        uint4 f[3];
+#pragma unroll
+        for (int q = 0; q < 3; q++) f[q] = aes128_enc(T, ctr, ParamKey{a.k[q].rk});
+#pragma unroll
+        for (int q = 0; q < 3; q++) {
+            const uint4 z = xor4(f[q], f[(q + 2) % 3]);
+            const uint32_t zw[4] = {z.x, z.y, z.z, z.w};
+#pragma unroll
+            for (int j = 0; j < 4; j++) {
+                const int64_t o = b * 4 + j;
+                if (o >= nwords) break;
+                uint32_t v = zw[j];
+                if (o == nwords - 1 && (nbits & 31)) v &= (1u << (nbits & 31)) - 1u;
+                if (a.xin[q]) v ^= a.xin[q][o];
+                a.out[q][o] = v;
+            }
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// src/rss.py:115-126 and_terms (per party), src/engine.py:174-189 XOR folds.
+// ---------------------------------------------------------------------------
+struct AndArgs {
+    const uint32_t* aa[kMaxParty];
+    const uint32_t* ab[kMaxParty];
+    const uint32_t* ba[kMaxParty];
+    const uint32_t* bb[kMaxParty];
+    uint32_t* out[kMaxParty];
+    int nparty;
+};
+
+__global__ void and_terms_kernel(const AndArgs a, int64_t nwords) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nwords; i += stride) {
+#pragma unroll
+        for (int q = 0; q < kMaxParty; q++) {
+            if (q >= a.nparty) break;
+            const uint32_t x = a.aa[q][i], y = a.ab[q][i], u = a.ba[q][i], v = a.bb[q][i];
+            a.out[q][i] = (x & u) ^ (x & v) ^ (y & u);
+        }
+    }
+}
+
+__global__ void xor3_kernel(const uint32_t* __restrict__ a, const uint32_t* __restrict__ b,
+                            const uint32_t* __restrict__ c, uint32_t* __restrict__ out, int64_t nwords) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nwords; i += stride)
+        out[i] = a[i] ^ b[i] ^ (c ? c[i] : 0u);
+}
+
+// ---------------------------------------------------------------------------
+// src/engine.py:95-102 _select_one_additive: out_q = XOR_c [fa_q(c) (A_q[c] ^
+// B_q[c]) ^ fb_q(c) A_q[c]] (flag bits are the party's two flag shares).
+// Column-parallel partial folds, combined with atomicXor (out pre-zeroed).
+// ---------------------------------------------------------------------------
+struct FoldArgs {
+    const uint32_t* A[kMaxParty];
+    const uint32_t* B[kMaxParty];
+    const uint32_t* fa[kMaxParty];
+    const uint32_t* fb[kMaxParty];
+    uint32_t* out[kMaxParty];
+    int nparty;
+    int64_t rows, words, pitch;
+};
+
+__global__ void select_fold_kernel(const FoldArgs a) {
+    const int64_t T = (int64_t)gridDim.x * blockDim.x;
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t w = t % a.words;
+    const int64_t rstride = T / a.words;
+    const int64_t r0 = t / a.words;
+    if (r0 >= rstride) return;  // trailing threads of an incomplete column set
+    uint32_t acc[kMaxParty] = {0, 0, 0};
+    for (int64_t r = r0; r < a.rows; r += rstride) {
+#pragma unroll
+        for (int q = 0; q < kMaxParty; q++) {
+            if (q >= a.nparty) break;
+            const uint32_t fa = (__ldg(a.fa[q] + (r >> 5)) >> (r & 31)) & 1u;
+            const uint32_t fb = (__ldg(a.fb[q] + (r >> 5)) >> (r & 31)) & 1u;
+            const uint32_t x = a.A[q][r * a.pitch + w], y = a.B[q][r * a.pitch + w];
+            acc[q] ^= ((x ^ y) & (0u - fa)) ^ (x & (0u - fb));
+        }
+    }
+#pragma unroll
+    for (int q = 0; q < kMaxParty; q++) {
+        if (q >= a.nparty) break;
+        if (acc[q]) atomicXor(a.out[q] + w, acc[q]);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Bit-granular row packing (src/engine.py:227-233, 317-318): row r of the
+// output is flag(r) || field_0[r] || field_1[r] ... with each field's
+// logical width, packed LE with a clean tail.  Thread per (row, out word).
+// ---------------------------------------------------------------------------
+constexpr int kMaxFields = 8;
+
+struct PackArgs {
+    const uint32_t* flag;  // bit vector (rows bits) for bit 0, or null
+    const uint32_t* f[kMaxFields];
+    int64_t fpitch[kMaxFields];
+    int64_t fwidth[kMaxFields];
+    int64_t foff[kMaxFields];
+    int nfields;
+    uint32_t* out;
+    int64_t opitch, owidth, rows;
+};
+
+__device__ __forceinline__ uint32_t field_bits32(const uint32_t* row, int64_t width, int64_t s) {
+    // 32 bits of a width-bit field starting at (possibly negative) position s
+    uint32_t lo = 0, hi = 0;
+    const int64_t wi = s >= 0 ? (s >> 5) : -1;
+    const int sh = (int)(s & 31);
+    const int64_t nw = (width + 31) >> 5;
+    if (wi >= 0 && wi < nw) lo = row[wi];
+    if (wi + 1 >= 0 && wi + 1 < nw) hi = row[wi + 1];
+    return sh ? __funnelshift_r(lo, hi, sh) : lo;
+}
+
+__global__ void pack_fields_kernel(const PackArgs a) {
+    const int64_t total = a.rows * a.opitch;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    const int64_t ow = (a.owidth + 31) >> 5;
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += stride) {
+        const int64_t r = t / a.opitch, k = t % a.opitch;
+        uint32_t v = 0;
+        if (k < ow) {
+            const int64_t lo = k * 32;
+            if (a.flag && lo == 0) v |= (a.flag[r >> 5] >> (r & 31)) & 1u;
+            for (int f = 0; f < a.nfields; f++) {
+                const int64_t o = a.foff[f], wdt = a.fwidth[f];
+                if (o >= lo + 32 || o + wdt <= lo) continue;
+                uint32_t bits = field_bits32(a.f[f] + r * a.fpitch[f], wdt, lo - o);
+                // keep only positions inside [o, o+wdt) of this word
+                const int64_t b0 = o > lo ? o - lo : 0;
+                const int64_t b1 = (o + wdt < lo + 32) ? o + wdt - lo : 32;
+                uint32_t m = (b1 - b0 >= 32) ? 0xffffffffu : (((1u << (b1 - b0)) - 1u) << b0);
+                v |= bits & m;
+            }
+        }
+        a.out[r * a.opitch + k] = v;
+    }
+}
+
+// out[k] = bits [off, off+width) of row idx[k] (idx null -> identity).
+__global__ void extract_field_kernel(const uint32_t* __restrict__ src, int64_t spitch,
+                                     const int32_t* __restrict__ idx, int64_t n, int64_t off, int64_t width,
+                                     uint32_t* __restrict__ out, int64_t opitch) {
+    const int64_t ow = (width + 31) >> 5;
+    const int64_t total = n * opitch;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    const int64_t sw = (off + width + 31) >> 5;  // words of the source row that are read
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += stride) {
+        const int64_t k = t / opitch, j = t % opitch;
+        uint32_t v = 0;
+        if (j < ow) {
+            const int64_t r = idx ? idx[k] : k;
+            v = field_bits32(src + r * spitch, sw * 32, off + j * 32);
+            if (j == ow - 1 && (width & 31)) v &= (1u << (width & 31)) - 1u;
+        }
+        out[k * opitch + j] = v;
+    }
+}
+
+// bit r of out = mat[r][0] & 1 (the flag column, src/engine.py:241-245).
+__global__ void column_bit_kernel(const uint32_t* __restrict__ mat, int64_t pitch, int64_t rows,
+                                  uint32_t* __restrict__ out) {
+    const int64_t nw = (rows + 31) >> 5;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; w < nw; w += stride) {
+        uint32_t v = 0;
+        const int64_t r0 = w << 5;
+        const int n = (int)min((int64_t)32, rows - r0);
+        for (int i = 0; i < n; i++) v |= (mat[(r0 + i) * pitch] & 1u) << i;
+        out[w] = v;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// src/engine.py:105-120 _select_many_additive: GF(2) product of K one-hot
+// selector rows (K, X) with (X, W) share rows.  Selectors are transposed to
+// one 32-bit mask per x per chunk of 32 selectors; a thread owns one word
+// column and a range of x, folding into 32 accumulators.
+// ---------------------------------------------------------------------------
+__global__ void transpose_sel_kernel(const uint32_t* __restrict__ sel, int64_t spitch, int64_t K,
+                                     int64_t k0, int64_t X, uint32_t* __restrict__ tmask) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    const int kn = (int)min((int64_t)32, K - k0);
+    for (int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; x < X; x += stride) {
+        uint32_t m = 0;
+        for (int k = 0; k < kn; k++) m |= ((sel[(k0 + k) * spitch + (x >> 5)] >> (x & 31)) & 1u) << k;
+        tmask[x] = m;
+    }
+}
+
+__global__ void select_many_kernel(const uint32_t* __restrict__ ta, const uint32_t* __restrict__ tb,
+                                   const uint32_t* __restrict__ A, const uint32_t* __restrict__ B,
+                                   int64_t X, int64_t words, int64_t pitch, int kn,
+                                   uint32_t* __restrict__ out, int64_t opitch) {
+    const int64_t T = (int64_t)gridDim.x * blockDim.x;
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t w = t % words;
+    const int64_t xs = T / words;
+    const int64_t x0 = t / words;
+    if (x0 >= xs) return;
+    uint32_t acc[32];
+#pragma unroll
+    for (int k = 0; k < 32; k++) acc[k] = 0;
+    for (int64_t x = x0; x < X; x += xs) {
+        const uint32_t ma = __ldg(ta + x), mb = __ldg(tb + x);
+        if (!(ma | mb)) continue;
+        const uint32_t a = A[x * pitch + w], b = B[x * pitch + w];
+        const uint32_t ab = a ^ b;
+#pragma unroll
+        for (int k = 0; k < 32; k++) acc[k] ^= (ab & (0u - ((ma >> k) & 1u))) ^ (a & (0u - ((mb >> k) & 1u)));
+    }
+#pragma unroll
+    for (int k = 0; k < 32; k++)
+        if (k < kn && acc[k]) atomicXor(out + k * opitch + w, acc[k]);
+}
+
+// rows whose bit is set, in order (public compaction after an open).
+struct FlagIter {
+    const uint32_t* bits;
+    __host__ __device__ bool operator()(int64_t i) const { return (bits[i >> 5] >> (i & 31)) & 1u; }
+};
+
+int engine_init() {
+    OGM_CUDA_TRY(allow_big_smem(zero_share3_kernel, kAesTableBytes));
+    return OGM_OK;
+}
+
+static int grid_for(int64_t work, int threads = 256) {
+    int64_t g = (work + threads - 1) / threads;
+    int64_t cap = (int64_t)sm_count() * 16;
+    if (g > cap) g = cap;
+    if (g < 1) g = 1;
+    return (int)g;
+}
+
 }  // namespace ogm
+
+// ===========================================================================
+// C ABI
+// ===========================================================================
+extern "C" {
+
+int ogm_masked_parity(int64_t rows, int64_t words, int64_t pitch, int ncomp, const uint32_t* const* comps,
+                      int nparty, const int32_t* a_idx, const int32_t* b_idx, int npass,
+                      const uint32_t* const* ind, uint32_t* const* out, void* stream) {
+    using namespace ogm;
+    OGM_CHECK_ARG(rows >= 0 && words >= 0 && pitch >= words, OGM_ERR_ARG, "bad matrix shape");
+    OGM_CHECK_ARG((nparty == 1 && ncomp == 2) || (nparty == 3 && ncomp == 3), OGM_ERR_ARG,
+                  "need nparty=1 with 2 components (A, B) or nparty=3 with 3 components");
+    OGM_CHECK_ARG(npass == 1 || npass == 2, OGM_ERR_ARG, "npass must be 1 or 2");
+    if (rows == 0) return OGM_OK;
+    ParityArgs p{};
+    bool aligned = (pitch % 4) == 0;
+    for (int c = 0; c < ncomp; c++) {
+        p.comp[c] = comps[c];
+        aligned = aligned && (((uintptr_t)comps[c]) & 15) == 0;
+    }
+    for (int q = 0; q < nparty; q++) {
+        // party q reads (x_q, x_{q+1}) (src/graphs.py:382-399): fixed mapping
+        OGM_CHECK_ARG(a_idx[q] == q && b_idx[q] == (q + 1) % ncomp, OGM_ERR_ARG,
+                      "party %d must read components (%d, %d)", q, q, (q + 1) % ncomp);
+        p.a_idx[q] = a_idx[q];
+        p.b_idx[q] = b_idx[q];
+    }
+    for (int j = 0; j < npass * nparty; j++) {
+        p.ind[2 * j] = ind[2 * j];
+        p.ind[2 * j + 1] = ind[2 * j + 1];
+        aligned = aligned && ((((uintptr_t)ind[2 * j]) | ((uintptr_t)ind[2 * j + 1])) & 15) == 0;
+        p.out[j] = out[j];
+    }
+    p.ncomp = ncomp;
+    p.nparty = nparty;
+    p.npass = npass;
+    p.rows = rows;
+    p.words = words;
+    p.pitch = pitch;
+    const int64_t units = aligned ? (words + 3) / 4 : words;
+    int G = 1;
+    while (G < 32 && G * 4 < units) G <<= 1;  // >= ~4 loads per lane per row
+    p.G = G;
+    const int64_t tiles = (rows + 31) / 32;
+    int64_t grid = (tiles + 7) / 8;
+    int64_t cap = (int64_t)sm_count() * 8;
+    if (grid > cap) grid = cap;
+    if (grid < 1) grid = 1;
+    cudaStream_t st = as_stream(stream);
+#define OGM_PARITY_LAUNCH(V, NP, NS) masked_parity_kernel<V, NP, NS><<<(int)grid, 256, 0, st>>>(p)
+    if (aligned) {
+        if (nparty == 1 && npass == 1) OGM_PARITY_LAUNCH(true, 1, 1);
+        else if (nparty == 1) OGM_PARITY_LAUNCH(true, 1, 2);
+        else if (npass == 1) OGM_PARITY_LAUNCH(true, 3, 1);
+        else OGM_PARITY_LAUNCH(true, 3, 2);
+    } else {
+        if (nparty == 1 && npass == 1) OGM_PARITY_LAUNCH(false, 1, 1);
+        else if (nparty == 1) OGM_PARITY_LAUNCH(false, 1, 2);
+        else if (npass == 1) OGM_PARITY_LAUNCH(false, 3, 1);
+        else OGM_PARITY_LAUNCH(false, 3, 2);
+    }
+#undef OGM_PARITY_LAUNCH
+    OGM_LAUNCH_CHECK();
+    return OGM_OK;
+}
+
+int ogm_zero_share_trio(const uint8_t* k1, const uint8_t* k2, const uint8_t* k3, uint64_t counter,
+                        int64_t nbits, const uint32_t* const* xor_into, uint32_t* const* out, void* stream) {
+    using namespace ogm;
+    OGM_CHECK_ARG(k1 && k2 && k3 && out, OGM_ERR_ARG, "zero-share keys and outputs are required");
+    OGM_CHECK_ARG(nbits >= 0, OGM_ERR_ARG, "negative bit count");
+    if (nbits == 0) return OGM_OK;
+    OGM_ENSURE_INIT();
+    static const uint8_t kZshr[4] = {'Z', 'S', 'H', 'R'};
+    Zs3Args a{};
+    a.k[0] = make_sched(k1);
+    a.k[1] = make_sched(k2);
+    a.k[2] = make_sched(k3);
+    for (int q = 0; q < 3; q++) {
+        a.xin[q] = xor_into ? xor_into[q] : nullptr;
+        a.out[q] = out[q];
+    }
+    const int64_t nwords = (nbits + 31) / 32;
+    zero_share3_kernel<<<aes_grid((nwords + 3) / 4), kAesThreads, kAesTableBytes, as_stream(stream)>>>(
+        a, label_be(kZshr), counter, nwords, nbits);
+    OGM_LAUNCH_CHECK();
+    return OGM_OK;
+}
+
+int ogm_and_terms(int64_t nwords, int nparty, const uint32_t* const* a_a, const uint32_t* const* a_b,
+                  const uint32_t* const* b_a, const uint32_t* const* b_b, uint32_t* const* out, void* stream) {
+    using namespace ogm;
+    OGM_CHECK_ARG(nparty >= 1 && nparty <= kMaxParty, OGM_ERR_ARG, "nparty must be 1..3");
+    OGM_CHECK_ARG(nwords >= 0, OGM_ERR_ARG, "negative length");
+    if (nwords == 0) return OGM_OK;
+    AndArgs a{};
+    for (int q = 0; q < nparty; q++) {
+        a.aa[q] = a_a[q];
+        a.ab[q] = a_b[q];
+        a.ba[q] = b_a[q];
+        a.bb[q] = b_b[q];
+        a.out[q] = out[q];
+    }
+    a.nparty = nparty;
+    and_terms_kernel<<<grid_for(nwords), 256, 0, as_stream(stream)>>>(a, nwords);
+    OGM_LAUNCH_CHECK();
+    return OGM_OK;
+}
+
+int ogm_xor_words(int64_t nwords, const uint32_t* a, const uint32_t* b, const uint32_t* c, uint32_t* out,
+                  void* stream) {
+    using namespace ogm;
+    OGM_CHECK_ARG(nwords >= 0, OGM_ERR_ARG, "negative length");
+    if (nwords == 0) return OGM_OK;
+    xor3_kernel<<<grid_for(nwords), 256, 0, as_stream(stream)>>>(a, b, c, out, nwords);
+    OGM_LAUNCH_CHECK();
+    return OGM_OK;
+}
+
+int ogm_select_fold(int64_t rows, int64_t words, int64_t pitch, int nparty, const uint32_t* const* A,
+                    const uint32_t* const* B, const uint32_t* const* fa, const uint32_t* const* fb,
+                    uint32_t* const* out, void* stream) {
+    using namespace ogm;
+    OGM_CHECK_ARG(nparty >= 1 && nparty <= kMaxParty, OGM_ERR_ARG, "nparty must be 1..3");
+    OGM_CHECK_ARG(rows >= 0 && words >= 0 && pitch >= words, OGM_ERR_ARG, "bad matrix shape");
+    cudaStream_t st = as_stream(stream);
+    FoldArgs a{};
+    for (int q = 0; q < nparty; q++) {
+        a.A[q] = A[q];
+        a.B[q] = B[q];
+        a.fa[q] = fa[q];
+        a.fb[q] = fb[q];
+        a.out[q] = out[q];
+        if (words) OGM_CUDA_TRY(cudaMemsetAsync(out[q], 0, 4 * words, st));
+    }
+    if (rows == 0 || words == 0) return OGM_OK;
+    a.nparty = nparty;
+    a.rows = rows;
+    a.words = words;
+    a.pitch = pitch;
+    int64_t threads_total = words * rows;
+    int64_t cap = (int64_t)sm_count() * 2048;
+    if (threads_total > cap) threads_total = cap;
+    if (threads_total < words) threads_total = words;
+    int grid = (int)((threads_total + 255) / 256);
+    select_fold_kernel<<<grid, 256, 0, st>>>(a);
+    OGM_LAUNCH_CHECK();
+    return OGM_OK;
+}
+
+int ogm_pack_fields(int64_t rows, const uint32_t* flag_bits, int nfields, const uint32_t* const* fields,
+                    const int64_t* fpitch, const int64_t* fwidth, uint32_t* out, int64_t opitch,
+                    void* stream) {
+    using namespace ogm;
+    OGM_CHECK_ARG(nfields >= 0 && nfields <= kMaxFields, OGM_ERR_ARG, "at most %d fields", kMaxFields);
+    PackArgs a{};
+    int64_t off = flag_bits ? 1 : 0;
+    for (int f = 0; f < nfields; f++) {
+        a.f[f] = fields[f];
+        a.fpitch[f] = fpitch[f];
+        a.fwidth[f] = fwidth[f];
+        a.foff[f] = off;
+        off += fwidth[f];
+    }
+    OGM_CHECK_ARG(opitch >= (off + 31) / 32, OGM_ERR_ARG, "output pitch too small for %lld bits",
+                  (long long)off);
+    if (rows == 0) return OGM_OK;
+    a.flag = flag_bits;
+    a.nfields = nfields;
+    a.out = out;
+    a.opitch = opitch;
+    a.owidth = off;
+    a.rows = rows;
+    pack_fields_kernel<<<grid_for(rows * opitch), 256, 0, as_stream(stream)>>>(a);
+    OGM_LAUNCH_CHECK();
+    return OGM_OK;
+}
+
+int ogm_extract_field(const uint32_t* src, int64_t spitch, const int32_t* idx, int64_t n, int64_t bit_offset,
+                      int64_t width, uint32_t* out, int64_t opitch, void* stream) {
+    using namespace ogm;
+    OGM_CHECK_ARG(n >= 0 && width >= 0 && bit_offset >= 0, OGM_ERR_ARG, "bad extract arguments");
+    OGM_CHECK_ARG(opitch >= (width + 31) / 32, OGM_ERR_ARG, "output pitch too small");
+    if (n == 0 || opitch == 0) return OGM_OK;
+    extract_field_kernel<<<grid_for(n * opitch), 256, 0, as_stream(stream)>>>(src, spitch, idx, n, bit_offset,
+                                                                               width, out, opitch);
+    OGM_LAUNCH_CHECK();
+    return OGM_OK;
+}
+
+int ogm_column_bits(const uint32_t* mat, int64_t pitch, int64_t rows, uint32_t* out_bits, void* stream) {
+    using namespace ogm;
+    OGM_CHECK_ARG(rows >= 0, OGM_ERR_ARG, "negative rows");
+    if (rows == 0) return OGM_OK;
+    column_bit_kernel<<<grid_for((rows + 31) / 32), 256, 0, as_stream(stream)>>>(mat, pitch, rows, out_bits);
+    OGM_LAUNCH_CHECK();
+    return OGM_OK;
+}
+
+int64_t ogm_compact_workspace_bytes(int64_t n) {
+    size_t bytes = 0;
+    cub::CountingInputIterator<int64_t> it(0);
+    cub::TransformInputIterator<bool, ogm::FlagIter, cub::CountingInputIterator<int64_t>> flags(
+        it, ogm::FlagIter{nullptr});
+    cub::DeviceSelect::Flagged(nullptr, bytes, it, flags, (int32_t*)nullptr, (int64_t*)nullptr, n);
+    return (int64_t)bytes + 256;
+}
+
+int ogm_compact_bits(int64_t n, const uint32_t* bits, int32_t* out_idx, int64_t* out_count, void* workspace,
+                     int64_t workspace_bytes, void* stream) {
+    using namespace ogm;
+    OGM_CHECK_ARG(n >= 0, OGM_ERR_ARG, "negative length");
+    if (n == 0) {
+        OGM_CUDA_TRY(cudaMemsetAsync(out_count, 0, 8, as_stream(stream)));
+        return OGM_OK;
+    }
+    cub::CountingInputIterator<int64_t> it(0);
+    cub::TransformInputIterator<bool, FlagIter, cub::CountingInputIterator<int64_t>> flags(it, FlagIter{bits});
+    size_t bytes = (size_t)workspace_bytes;
+    OGM_CUDA_TRY(cub::DeviceSelect::Flagged(workspace, bytes, it, flags, out_idx, out_count, n,
+                                            as_stream(stream)));
+    return OGM_OK;
+}
+
+int ogm_select_many(int64_t K, int64_t X, int64_t words, int64_t pitch, const uint32_t* sel_a,
+                    const uint32_t* sel_b, int64_t spitch, const uint32_t* A, const uint32_t* B, uint32_t* out,
+                    int64_t opitch, void* workspace, void* stream) {
+    using namespace ogm;
+    OGM_CHECK_ARG(K >= 0 && X >= 0 && words >= 0 && pitch >= words && opitch >= words, OGM_ERR_ARG,
+                  "bad select-many shape");
+    cudaStream_t st = as_stream(stream);
+    if (K == 0) return OGM_OK;
+    OGM_CUDA_TRY(cudaMemsetAsync(out, 0, 4 * K * opitch, st));
+    if (X == 0 || words == 0) return OGM_OK;
+    uint32_t* ta = (uint32_t*)workspace;
+    uint32_t* tb = ta + X;
+    int64_t threads_total = words * X;
+    int64_t cap = (int64_t)sm_count() * 1024;
+    if (threads_total > cap) threads_total = cap;
+    if (threads_total < words) threads_total = words;
+    for (int64_t k0 = 0; k0 < K; k0 += 32) {
+        transpose_sel_kernel<<<grid_for(X), 256, 0, st>>>(sel_a, spitch, K, k0, X, ta);
+        transpose_sel_kernel<<<grid_for(X), 256, 0, st>>>(sel_b, spitch, K, k0, X, tb);
+        const int kn = (int)((K - k0) < 32 ? (K - k0) : 32);
+        select_many_kernel<<<(int)((threads_total + 127) / 128), 128, 0, st>>>(ta, tb, A, B, X, words, pitch, kn,
+                                                                              out + k0 * opitch, opitch);
+    }
+    OGM_LAUNCH_CHECK();
+    return OGM_OK;
+}
+
+}  // extern "C"

@@ -91,8 +91,119 @@ __global__ void perm_reset_kernel(const int32_t* __restrict__ live, const int32_
     }
 }
 
+
+// ---------------------------------------------------------------------------
+// One step of the 3-party shuffle (src/shuffle.py:106-143), as a gather:
+//
+//   k2 = P2 ? P2[i] : i          k1 = P1 ? P1[k2] : k2
+//   out[i] = M1[k1] ^ M2[k1] ^ T1[k1] ^ T2[k2] ^ M3[i] ^ R[i]
+//
+// with every term optional.  T1/T2/R are blinding tables: either
+// precomputed matrices (offline phase) or generated on the fly from
+// AES-CTR (label, table id), row r = stream words [r*W, r*W + W) with the
+// row tail masked to `width` (src/shuffle.py:69-73).  `_apply(p, M) = M[p]`
+// (src/shuffle.py:76-77), so nested applications compose as index lookups:
+//   P1: x1 = pi31(pi12(a^b^T12) ^ T31):  P2=pi31, P1=pi12, M1=a, M2=b, T1=T12, T2=T31
+//   P2: y1 = pi12(b^T12):                 P1=pi12, M1=b, T1=T12
+//   P2: c1 = pi23(x1^T23) ^ R2:           P1=pi23, M1=x1, T1=T23, R=R2
+//   P3: R3 = c1 ^ pi23(pi31(y1^T31)^T23) ^ R1:
+//                                          P2=pi23, P1=pi31, M1=y1, T1=T31, T2=T23, M3=c1, R=R1
+// A thread owns a 4-word chunk of one output row.
+// ---------------------------------------------------------------------------
+struct GatherTerm {
+    AesKeySched key;
+    const uint32_t* mat;  // precomputed table (row-major, W words) or null
+    uint32_t label_be;
+    uint64_t index;
+    int on;  // 0 absent, 1 online PRF, 2 matrix
+};
+
+struct GatherArgs {
+    const int32_t* P1;
+    const int32_t* P2;
+    const uint32_t* M1;
+    const uint32_t* M2;
+    const uint32_t* M3;
+    GatherTerm t1, t2, r;
+    uint32_t* out;
+    int64_t rows, W, width;
+};
+
+__device__ __forceinline__ void prf_row_chunk(const AesTab& T, const GatherTerm& g, int64_t row, int64_t W,
+                                              int64_t c, int nw, uint32_t v[4]) {
+    const uint64_t g0 = (uint64_t)row * (uint64_t)W + 4 * (uint64_t)c;
+    const uint64_t b0 = g0 >> 2;
+    const int off = (int)(g0 & 3);
+    const uint4 k0 = aes128_enc(T, ctr_block(g.label_be, g.index, b0), ParamKey{g.key.rk});
+    uint32_t w8[8] = {k0.x, k0.y, k0.z, k0.w, 0, 0, 0, 0};
+    if (off + nw > 4) {
+        const uint4 k1 = aes128_enc(T, ctr_block(g.label_be, g.index, b0 + 1), ParamKey{g.key.rk});
+        w8[4] = k1.x; w8[5] = k1.y; w8[6] = k1.z; w8[7] = k1.w;
+    }
+#pragma unroll
+    for (int j = 0; j < 4; j++) v[j] = w8[(off + j) & 7];
+}
+
+template <bool ONLINE>
+__global__ void __launch_bounds__(kAesThreads) shuffle_gather_kernel(const GatherArgs a) {
+    extern __shared__ __align__(128) uint8_t smem_raw[];
+    if (ONLINE) {
+        aes_fill_tables(smem_raw);
+        __syncthreads();
+    }
+    const AesTab T(smem_raw);
+    const int64_t nch = (a.W + 3) >> 2;
+    const int64_t total = a.rows * nch;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    const uint32_t tail = (a.width & 31) ? ((1u << (a.width & 31)) - 1u) : 0xffffffffu;
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += stride) {
+        const int64_t i = t / nch, c = t % nch;
+        const int nw = (int)min((int64_t)4, a.W - 4 * c);
+        const int64_t k2 = a.P2 ? (int64_t)__ldg(a.P2 + i) : i;
+        const int64_t k1 = a.P1 ? (int64_t)__ldg(a.P1 + k2) : k2;
+        uint32_t acc[4] = {0, 0, 0, 0};
+        const GatherTerm* terms[3] = {&a.t1, &a.t2, &a.r};
+        const int64_t trow[3] = {k1, k2, i};
+#pragma unroll
+        for (int q = 0; q < 3; q++) {
+            const GatherTerm& g = *terms[q];
+            if (g.on == 0) continue;
+            uint32_t v[4] = {0, 0, 0, 0};
+            if (ONLINE && g.on == 1) {
+                prf_row_chunk(T, g, trow[q], a.W, c, nw, v);
+                if (4 * c + nw == a.W) v[nw - 1] &= tail;
+            } else {
+                const uint32_t* src = g.mat + trow[q] * a.W + 4 * c;
+                for (int j = 0; j < nw; j++) v[j] = src[j];
+            }
+#pragma unroll
+            for (int j = 0; j < 4; j++) acc[j] ^= v[j];
+        }
+        const uint32_t* m1 = a.M1 ? a.M1 + k1 * a.W + 4 * c : nullptr;
+        const uint32_t* m2 = a.M2 ? a.M2 + k1 * a.W + 4 * c : nullptr;
+        const uint32_t* m3 = a.M3 ? a.M3 + i * a.W + 4 * c : nullptr;
+        uint32_t* o = a.out + i * a.W + 4 * c;
+        if (nw == 4 && ((a.W & 3) == 0)) {
+            uint4 x = make_uint4(acc[0], acc[1], acc[2], acc[3]);
+            if (m1) x = xor4(x, *reinterpret_cast<const uint4*>(m1));
+            if (m2) x = xor4(x, *reinterpret_cast<const uint4*>(m2));
+            if (m3) x = xor4(x, *reinterpret_cast<const uint4*>(m3));
+            *reinterpret_cast<uint4*>(o) = x;
+        } else {
+            for (int j = 0; j < nw; j++) {
+                uint32_t x = acc[j];
+                if (m1) x ^= m1[j];
+                if (m2) x ^= m2[j];
+                if (m3) x ^= m3[j];
+                o[j] = x;
+            }
+        }
+    }
+}
+
 int shuffle_init() {
     OGM_CUDA_TRY(allow_big_smem(perm_draws_kernel, kAesTableBytes));
+    OGM_CUDA_TRY(allow_big_smem(shuffle_gather_kernel<true>, kAesTableBytes));
     return OGM_OK;
 }
 
@@ -153,6 +264,63 @@ int ogm_seeded_permutation(const uint8_t* key, const uint8_t* label, uint64_t in
     OGM_CHECK_ARG(n == 0 || workspace, OGM_ERR_ARG, "permutation workspace is required");
     OGM_ENSURE_INIT();
     return ogm::seeded_permutation_impl(key, label, index, n, perm, workspace, ogm::as_stream(stream));
+}
+
+static int set_term(ogm::GatherTerm& g, const uint8_t* key, const uint8_t* label, uint64_t index,
+                    const uint32_t* mat) {
+    if (mat) {
+        g.on = 2;
+        g.mat = mat;
+    } else if (key) {
+        OGM_CHECK_ARG(label, OGM_ERR_ARG, "PRF table label is required");
+        g.on = 1;
+        g.key = ogm::make_sched(key);
+        g.label_be = ogm::label_be(label);
+        g.index = index;
+    }
+    return OGM_OK;
+}
+
+int ogm_shuffle_gather(int64_t rows, int64_t words, int64_t width_bits, const int32_t* perm_outer,
+                       const int32_t* perm_inner, const uint32_t* m1, const uint32_t* m2, const uint32_t* m3,
+                       const uint8_t* t1_key, const uint8_t* t1_label, uint64_t t1_index, const uint32_t* t1_mat,
+                       const uint8_t* t2_key, const uint8_t* t2_label, uint64_t t2_index, const uint32_t* t2_mat,
+                       const uint8_t* r_key, const uint8_t* r_label, uint64_t r_index, const uint32_t* r_mat,
+                       uint32_t* out, void* stream) {
+    using namespace ogm;
+    OGM_CHECK_ARG(rows >= 0 && words >= 0 && width_bits >= 0 && (width_bits + 31) / 32 == words, OGM_ERR_ARG,
+                  "table shares must have %lld words per row for width %lld", (long long)((width_bits + 31) / 32),
+                  (long long)width_bits);
+    OGM_CHECK_ARG(out, OGM_ERR_ARG, "output is required");
+    if (rows == 0 || words == 0) return OGM_OK;
+    OGM_ENSURE_INIT();
+    GatherArgs a{};
+    a.P1 = perm_inner;
+    a.P2 = perm_outer;
+    a.M1 = m1;
+    a.M2 = m2;
+    a.M3 = m3;
+    int rc = set_term(a.t1, t1_key, t1_label, t1_index, t1_mat);
+    if (!rc) rc = set_term(a.t2, t2_key, t2_label, t2_index, t2_mat);
+    if (!rc) rc = set_term(a.r, r_key, r_label, r_index, r_mat);
+    if (rc) return rc;
+    a.out = out;
+    a.rows = rows;
+    a.W = words;
+    a.width = width_bits;
+    const bool online = a.t1.on == 1 || a.t2.on == 1 || a.r.on == 1;
+    const int64_t work = rows * ((words + 3) / 4);
+    cudaStream_t st = as_stream(stream);
+    if (online) {
+        shuffle_gather_kernel<true><<<aes_grid(work), kAesThreads, kAesTableBytes, st>>>(a);
+    } else {
+        int64_t g = (work + kAesThreads - 1) / kAesThreads;
+        const int64_t cap = (int64_t)sm_count() * 8;
+        if (g > cap) g = cap;
+        shuffle_gather_kernel<false><<<(int)(g < 1 ? 1 : g), kAesThreads, 0, st>>>(a);
+    }
+    OGM_LAUNCH_CHECK();
+    return OGM_OK;
 }
 
 }  // extern "C"
