@@ -81,8 +81,9 @@ int ogm_prf_words(const uint8_t* key, const uint8_t* label, uint64_t index, uint
 
 /* src/rss.py:143-148 ZeroShareContext.next_share at counter `counter`:
  * out = F(key_own, "ZSHR", counter) ^ F(key_prev, "ZSHR", counter), masked to
- * nbits.  If `xor_into` is non-NULL the share is XORed into it instead
- * (out may equal xor_into).  Keys are HOST pointers. */
+ * nbits.  If `xor_into` is non-NULL the share is XORed into it and the
+ * tail is masked after the fold, as BitVector(additive ^ share, nbits) does
+ * in src/rss.py:171 (out may equal xor_into).  Keys are HOST pointers. */
 int ogm_zero_share(const uint8_t* key_own, const uint8_t* key_prev, uint64_t counter,
                    int64_t nbits, const uint32_t* xor_into, uint32_t* out, void* stream);
 

@@ -157,8 +157,8 @@ __global__ void __launch_bounds__(kAesThreads) zero_share3_kernel(const Zs3Args 
                 const int64_t o = b * 4 + j;
                 if (o >= nwords) break;
                 uint32_t v = zw[j];
-                if (o == nwords - 1 && (nbits & 31)) v &= (1u << (nbits & 31)) - 1u;
                 if (a.xin[q]) v ^= a.xin[q][o];
+                if (o == nwords - 1 && (nbits & 31)) v &= (1u << (nbits & 31)) - 1u;
                 a.out[q][o] = v;
             }
         }

@@ -257,8 +257,9 @@ __global__ void __launch_bounds__(kFssThreads) prf_words_kernel(
             if (o < 0 || o >= nwords) continue;
             uint32_t v = kw[j];
             if (ZERO) {
-                if (o == nwords - 1 && (nbits & 31)) v &= (1u << (nbits & 31)) - 1u;
+                // BitVector(additive ^ share, n) semantics: tail masked after the fold
                 if (xor_into) v ^= xor_into[o];
+                if (o == nwords - 1 && (nbits & 31)) v &= (1u << (nbits & 31)) - 1u;
             }
             out[o] = v;
         }

@@ -71,10 +71,13 @@ def test_zero_shares(golden):
         for p in range(3):
             got = host_u32(prf.zero_share_device(*pairs[p], ctr, nbits))
             assert np.array_equal(got, g[f"zs{j}_p{p}"])
-        # fold mode: out = base ^ share
+        # fold mode: BitVector(base ^ share, nbits) -- tail masked after the XOR
         base = np.arange(len(g[f"zs{j}_p0"]), dtype=np.uint32) * np.uint32(2654435761)
         folded = host_u32(prf.zero_share_device(*pairs[0], ctr, nbits, xor_into=dev_u32(base)))
-        assert np.array_equal(folded, base ^ g[f"zs{j}_p0"])
+        want = base ^ g[f"zs{j}_p0"]
+        if nbits % 32:
+            want[-1] &= np.uint32((1 << (nbits % 32)) - 1)
+        assert np.array_equal(folded, want)
         j += 1
 
 
