@@ -1,0 +1,296 @@
+#!/usr/bin/env python
+"""Secondary benchmarks for BASELINE configs 1, 3 and 5 (bench.py covers config 2).
+
+    python bench_configs.py c1 [--steps K]      tiny end-to-end query latency
+    python bench_configs.py c3 [--rows X]       root-slot secEval (HBM-bound)
+    python bench_configs.py c5 [--max-log 28]   shuffle / fetch bandwidth sweep
+
+Each prints one JSON line per measurement.  Device times use CUDA events on
+the launching stream(s) after warm-up; wall-clock is used only for the
+three-thread end-to-end protocol runs, as the reference does
+(src/bench.py:47-49).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import statistics
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+import torch
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+from paper_2209_03526_b200 import _lib, fss  # noqa: E402
+from paper_2209_03526_b200.bits import words_for  # noqa: E402
+from paper_2209_03526_b200.engine import CandidateGroup, EngineConfig, open_results, sec_eval, sec_match  # noqa: E402
+from paper_2209_03526_b200.graphs import device_trio, encrypt_graph  # noqa: E402
+from paper_2209_03526_b200.net import local_runtimes, make_session_configs, run_trio  # noqa: E402
+from paper_2209_03526_b200.query import gen_token, load_query  # noqa: E402
+from paper_2209_03526_b200.shuffle import ShuffleOffline, blind_table, gather  # noqa: E402
+from paper_2209_03526_b200.prf import seeded_permutation_device  # noqa: E402
+from paper_2209_03526_b200 import workloads  # noqa: E402
+
+HBM_PEAK = 6553.0  # GB/s, MEASURED_PEAKS.json (copy benchmark on this pool)
+
+
+def emit(d):
+    print(json.dumps(d), flush=True)
+
+
+def events(n):
+    return [torch.cuda.Event(enable_timing=True) for _ in range(n)]
+
+
+# ---------------------------------------------------------------------------
+# C1: tiny end-to-end
+# ---------------------------------------------------------------------------
+
+
+def run_c1(args):
+    import oracle.matcher as om
+
+    graph = workloads.tiny_graph(args.seed)
+    qtext = workloads.tiny_query(graph, args.seed)
+    rng = np.random.default_rng(args.seed)
+    t0 = time.perf_counter()
+    schema, shares = encrypt_graph(graph, 2, rng)
+    t_enc = time.perf_counter() - t0
+    dshares = device_trio(shares)
+    query = load_query(qtext, schema)
+    t0 = time.perf_counter()
+    tokens = gen_token(query, schema, rng)
+    t_tok = time.perf_counter() - t0
+    want = om.oracle_match(graph, query, schema)
+    master = b"\x5a" * 16
+
+    def one():
+        rts = local_runtimes(make_session_configs(master))
+        res = run_trio(lambda rt: sec_match(rt, tokens[rt.index - 1], dshares[rt.index - 1], EngineConfig()), rts)
+        matches, _ = open_results(res[:2], schema)
+        return set(matches), rts
+
+    for _ in range(args.warmup):
+        got, _ = one()
+    if got != want:
+        raise SystemExit(f"C1 result differs from the plaintext oracle: {got} vs {want}")
+    lat = []
+    for _ in range(args.steps):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        got, rts = one()
+        lat.append(time.perf_counter() - t0)
+    phases = {ph: st.bytes_sent for ph, st in rts[0].meter.phases.items()}
+    emit({"config": "C1 tiny (1000 vertices, 3 types, 3-vertex path, k=2)", "metric": "query_latency_ms",
+          "value": 1e3 * statistics.median(lat), "unit": "ms", "higher_is_better": False,
+          "min_ms": 1e3 * min(lat), "max_ms": 1e3 * max(lat), "steps": args.steps, "matches": len(got),
+          "oracle_equal": got == want, "bytes_per_party_by_phase": phases,
+          "offline": {"encrypt_graph_s": t_enc, "gen_token_s": t_tok},
+          "path": "per-party drop-in API: 3 party threads, device messages, run_trio + sec_match + open_results"})
+
+
+# ---------------------------------------------------------------------------
+# C3: root-slot secEval on the medium graph shapes
+# ---------------------------------------------------------------------------
+
+
+def run_c3(args):
+    X = args.rows
+    dev = torch.device("cuda")
+    rng = np.random.default_rng(args.seed)
+    for name, n in (("uniform", 182083), ("zipf", 8969)):
+        vals = torch.from_numpy(rng.integers(0, n, size=X).astype(np.int32)).to(dev)
+        c1, c2, c3 = workloads.shared_one_hot(vals, n, args.seed, 10)
+        comps = [c1, c2, c3]
+        w = words_for(n)
+        lo = int(rng.integers(0, n // 2))
+        pairs = [fss.ic_gen(lo, lo + n // 10, n, rng) for _ in range(3)]
+        (k11, k21), (k12, k22), (k13, k23) = pairs
+        keys = [(k11, k12), (k22, k13), (k23, k21)]
+        # full-domain indicators once (cached per key in sec_match)
+        inds = []
+        for p in range(3):
+            row = []
+            for pi in range(2):
+                ka = fss.key_parts_for_engine(keys[p][0])[pi]
+                kb = fss.key_parts_for_engine(keys[p][1])[pi]
+                row.append((fss.full_domain(fss.KeyBatch.from_keys([ka]), n)[0],
+                            fss.full_domain(fss.KeyBatch.from_keys([kb]), n)[0]))
+            inds.append(row)
+        outs = [torch.empty(words_for(X), dtype=torch.int32, device=dev) for _ in range(6)]
+        A = _lib.ptr_array
+
+        def per_party(p):
+            ind = [inds[p][0][0], inds[p][0][1], inds[p][1][0], inds[p][1][1]]
+            _lib.call("ogm_masked_parity", X, w, comps[0].stride(0), 2, A([comps[p], comps[(p + 1) % 3]]), 1, _lib.int_array([0]),
+                      _lib.int_array([1]), 2, A(ind), A(outs[2 * p:2 * p + 2]), _lib.stream_ptr())
+
+        def trio():
+            ind = []
+            for pi in range(2):
+                for p in range(3):
+                    ind += [inds[p][pi][0], inds[p][pi][1]]
+            _lib.call("ogm_masked_parity", X, w, comps[0].stride(0), 3, A(comps), 3, _lib.int_array([0, 1, 2]),
+                      _lib.int_array([1, 2, 0]), 2, A(ind), A(outs), _lib.stream_ptr())
+
+        # parity check: trio == per-party results
+        for p in range(3):
+            per_party(p)
+        ref = [o.clone() for o in outs]
+        trio()
+        ok = all(torch.equal(ref[2 * p + pi], outs[pi * 3 + p]) for p in range(3) for pi in range(2))
+        for mode, fn, nbytes in (("per-party (3 launches)", lambda: [per_party(p) for p in range(3)], 3 * 2 * X * w * 4),
+                                 ("trio-fused", trio, 3 * X * w * 4)):
+            for _ in range(args.warmup):
+                fn()
+            ev = events(args.steps + 1)
+            ev[0].record()
+            for s in range(args.steps):
+                fn()
+                ev[s + 1].record()
+            torch.cuda.synchronize()
+            ms = statistics.median(ev[i].elapsed_time(ev[i + 1]) for i in range(args.steps))
+            emit({"config": f"C3 root secEval, {X} candidates, {name} attr n={n} (w={w} words), interval "
+                            "(2 passes fused)", "metric": "secEval_local_GBps", "mode": mode,
+                  "value": nbytes / (ms * 1e-3) / 1e9, "unit": "GB/s", "ms": ms,
+                  "hbm_frac": nbytes / (ms * 1e-3) / 1e9 / HBM_PEAK, "algorithmic_bytes": nbytes,
+                  "trio_equals_per_party": ok})
+        # the full protocol step (3 threads, fused passes + 2 reshares per party)
+        group = [CandidateGroup(None, None, X, X, comps[p][:, :1], comps[(p + 1) % 3][:, :1],
+                                {"a": (comps[p], comps[(p + 1) % 3])}, {"a": n}) for p in range(3)]
+        caches = [dict() for _ in range(3)]
+        lat = []
+        for it in range(args.warmup + args.steps):
+            rts = local_runtimes(make_session_configs(b"\x33" * 16))
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            run_trio(lambda rt: sec_eval(rt, group[rt.index - 1], keys[rt.index - 1], "a", n,
+                                         caches[rt.index - 1]), rts)
+            if it >= args.warmup:
+                lat.append(time.perf_counter() - t0)
+        emit({"config": f"C3 root secEval {name}", "metric": "secEval_protocol_ms", "value": 1e3 * statistics.median(lat),
+              "unit": "ms", "path": "per-party drop-in sec_eval x3 threads (indicators cached)"})
+        del c1, c2, c3, comps, group
+        torch.cuda.empty_cache()
+
+
+# ---------------------------------------------------------------------------
+# C5: shuffle / fetch sweep
+# ---------------------------------------------------------------------------
+
+
+def run_c5(args):
+    dev = torch.device("cuda")
+    cfg = make_session_configs(b"\x77" * 16)
+    s12, s23, s31 = cfg[0].seed_with_next, cfg[1].seed_with_next, cfg[2].seed_with_next
+    width = 128
+    W = 4
+    for lg in range(args.min_log, args.max_log + 1, args.log_step):
+        rows = 1 << lg
+        comps = [workloads.device_random_words(rows * W, args.seed, 20 + c).reshape(rows, W) for c in range(3)]
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        perms = {s: seeded_permutation_device(s, b"SHPI", 0, rows) for s in (s12, s23, s31)}
+        torch.cuda.synchronize()
+        t_perm = time.perf_counter() - t0
+        t0 = time.perf_counter()
+        blinds = {
+            "T12": blind_table(s12, b"SHTB", 0, rows, width), "T23": blind_table(s23, b"SHTB", 0, rows, width),
+            "T31": blind_table(s31, b"SHTB", 0, rows, width), "R1": blind_table(s31, b"SHRD", 0, rows, width),
+            "R2": blind_table(s12, b"SHRD", 0, rows, width)}
+        torch.cuda.synchronize()
+        t_blind = time.perf_counter() - t0
+        pi12, pi23, pi31 = perms[s12], perms[s23], perms[s31]
+        x1 = torch.empty_like(comps[0])
+        y1 = torch.empty_like(comps[0])
+        c1 = torch.empty_like(comps[0])
+        r3 = torch.empty_like(comps[0])
+        # offline phase per party (ShuffleOffline): composed perms + permuted, combined blinds
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        pc = {(s, 0, rows): perms[s] for s in perms}
+        off = [ShuffleOffline(p + 1, cfg[p].seed_with_next, cfg[p].seed_with_prev, 0, rows, width, perm_cache=pc)
+               for p in range(3)]
+        torch.cuda.synchronize()
+        t_off = time.perf_counter() - t0
+
+        def online(pre: bool):
+            # the four party-local steps of src/shuffle.py:106-143 in protocol order
+            if pre:
+                gather(rows, width, x1, inner=off[0].k1, m1=comps[0], m2=comps[1], r=off[0].u)
+                gather(rows, width, y1, inner=off[1].pi12, m1=comps[2], r=off[1].v)
+                gather(rows, width, c1, inner=off[1].pi23, m1=x1, r=off[1].w)
+                gather(rows, width, r3, inner=off[2].k3, m1=y1, m3=c1, r=off[2].z)
+                return
+            gather(rows, width, x1, outer=pi31, inner=pi12, m1=comps[0], m2=comps[1],
+                   t1=(s12, b"SHTB", 0), t2=(s31, b"SHTB", 0))
+            gather(rows, width, y1, inner=pi12, m1=comps[2], t1=(s12, b"SHTB", 0))
+            gather(rows, width, c1, inner=pi23, m1=x1, t1=(s23, b"SHTB", 0), r=(s12, b"SHRD", 0))
+            gather(rows, width, r3, outer=pi23, inner=pi31, m1=y1, t1=(s31, b"SHTB", 0),
+                   t2=(s23, b"SHTB", 0), m3=c1, r=(s31, b"SHRD", 0))
+
+        # correctness: R1 ^ R2 ^ R3 == composed-permuted plaintext (size-independent check)
+        online(True)
+        perm = pi12.long()[pi31.long()[pi23.long()]]
+        plain = comps[0] ^ comps[1] ^ comps[2]
+        ok = bool(torch.equal(blinds["R1"] ^ blinds["R2"] ^ r3, plain[perm]))
+        r3_pre = r3.clone()
+        online(False)
+        ok = ok and bool(torch.equal(r3, r3_pre))
+        del perm, plain
+        for pre in (True, False):
+            for _ in range(args.warmup):
+                online(pre)
+            ev = events(args.steps + 1)
+            ev[0].record()
+            for s in range(args.steps):
+                online(pre)
+                ev[s + 1].record()
+            torch.cuda.synchronize()
+            ms = statistics.median(ev[i].elapsed_time(ev[i + 1]) for i in range(args.steps))
+            if pre:
+                # x1: 2 gathers + U1 + write; y1: gather + V + write; c1: gather + W + write;
+                # R3: gather + c1 + Z + write  = 14 row moves (16 B) + 4 coalesced index reads
+                nbytes = rows * (14 * 16 + 4 * 4)
+            else:
+                # 10 row moves + 6 index reads (2 of them dependent/random); blinds by AES
+                nbytes = rows * (10 * 16 + 6 * 4)
+            emit({"config": f"C5 shuffle 2^{lg} rows x 128-bit", "metric": "shuffle_online_GBps",
+                  "blinds": "offline (ShuffleOffline: composed perms + permuted combined blinds)" if pre
+                  else "AES-CTR on the fly, nested permutation lookups",
+                  "value": nbytes / (ms * 1e-3) / 1e9, "unit": "GB/s", "ms": ms,
+                  "hbm_frac": nbytes / (ms * 1e-3) / 1e9 / HBM_PEAK, "algorithmic_bytes_per_row": nbytes // rows,
+                  "rows_per_s": rows / (ms * 1e-3), "offline_perm_s": t_perm, "offline_blinds_s": t_blind,
+                  "offline_party_material_s": t_off, "bit_exact_recombination": ok})
+        del off, pc
+        del comps, perms, blinds, x1, y1, c1, r3, r3_pre
+        torch.cuda.empty_cache()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("which", choices=["c1", "c3", "c5", "all"])
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--seed", type=int, default=1)
+    ap.add_argument("--rows", type=int, default=200_000)
+    ap.add_argument("--min-log", type=int, default=16)
+    ap.add_argument("--max-log", type=int, default=28)
+    ap.add_argument("--log-step", type=int, default=2)
+    args = ap.parse_args()
+    _lib.check(_lib.load().ogm_init())
+    if args.which in ("c1", "all"):
+        run_c1(args)
+    if args.which in ("c3", "all"):
+        run_c3(args)
+    if args.which in ("c5", "all"):
+        run_c5(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -211,6 +211,10 @@ int ogm_shuffle_gather(int64_t rows, int64_t words, int64_t width_bits, const in
                        const uint8_t* r_key, const uint8_t* r_label, uint64_t r_index,
                        const uint32_t* r_mat, uint32_t* out, void* stream);
 
+/* Offline composition of two known permutations: out[i] = inner[outer[i]]
+ * (gather semantics, so M[out] = M[inner][outer] as in src/shuffle.py:76-77). */
+int ogm_perm_compose(int64_t n, const int32_t* outer, const int32_t* inner, int32_t* out, void* stream);
+
 /* ---- measurement -------------------------------------------------------- */
 
 /* Roofline denominator for the integer-ALU-bound kernels: issue rate of

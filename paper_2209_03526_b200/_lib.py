@@ -59,6 +59,7 @@ SIGNATURES = {
     "ogm_compact_bits": ([_i64, _vp, _vp, _vp, _vp, _i64, _vp], _int),
     "ogm_shuffle_gather": ([_i64, _i64, _i64, _vp, _vp, _vp, _vp, _vp, _cp, _cp, _u64, _vp, _cp, _cp, _u64,
                             _vp, _cp, _cp, _u64, _vp, _vp, _vp], _int),
+    "ogm_perm_compose": ([_i64, _vp, _vp, _vp, _vp], _int),
     "ogm_measure_int_peak": ([ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double)], _int),
 }
 

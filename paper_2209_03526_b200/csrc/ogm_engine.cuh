@@ -122,6 +122,83 @@ __global__ void __launch_bounds__(256) masked_parity_kernel(const ParityArgs p) 
     }
 }
 
+
+// ---------------------------------------------------------------------------
+// Masked parity, register-resident indicators (the bandwidth path).
+//
+// The indicator vectors are identical for every candidate row, so a CTA owns
+// a chunk of columns and keeps its slice of all 2*NPARTY*NPASS indicators in
+// registers (one uint4 per vector per lane); warps then stream rows through
+// it.  For each row a lane folds its 4 words into a 32-bit partial per
+// (pass, party); the row's partial parity over the warp's 128 columns is
+// popc(ballot(popc(partial) & 1)) & 1.  32 rows make an output word, which is
+// XORed into the (pre-zeroed) result -- parity is XOR-linear, so column
+// chunks and warps combine with atomicXor.  Shares are read exactly once,
+// with 128-bit loads, and the indicator traffic is paid once per CTA.
+// ---------------------------------------------------------------------------
+template <int NPARTY, int NPASS>
+__global__ void __launch_bounds__(256) masked_parity_v2_kernel(const ParityArgs p, int CW, int64_t tiles_per_block) {
+    constexpr int NJ = NPARTY * NPASS;
+    constexpr int NCOMP = NPARTY == 1 ? 2 : 3;
+    const int lane = threadIdx.x & 31;
+    const int warp = threadIdx.x >> 5;
+    const int RG = 8 / CW;
+    const int rg = warp / CW, wc = warp % CW;
+    const int64_t col0 = ((int64_t)blockIdx.x * CW + wc) * 128 + lane * 4;  // first word of this lane
+    uint4 ia[NJ], ib[NJ];
+#pragma unroll
+    for (int j = 0; j < NJ; j++) {
+        uint32_t a4[4], b4[4];
+#pragma unroll
+        for (int e = 0; e < 4; e++) {
+            const bool in = col0 + e < p.words;
+            a4[e] = in ? __ldg(p.ind[2 * j] + col0 + e) : 0u;
+            b4[e] = in ? __ldg(p.ind[2 * j + 1] + col0 + e) : 0u;
+        }
+        ia[j] = make_uint4(a4[0], a4[1], a4[2], a4[3]);
+        ib[j] = make_uint4(b4[0], b4[1], b4[2], b4[3]);
+    }
+    const bool lane_live = col0 < p.words;
+    const int64_t ntiles = (p.rows + 31) >> 5;
+    const int64_t t0 = (int64_t)blockIdx.y * tiles_per_block;
+    const int64_t t1 = min(ntiles, t0 + tiles_per_block);
+    for (int64_t tile = t0 + rg; tile < t1; tile += RG) {
+        uint32_t word[NJ];
+#pragma unroll
+        for (int j = 0; j < NJ; j++) word[j] = 0;
+        const int64_t rbase = tile << 5;
+        const int nrow = (int)min((int64_t)32, p.rows - rbase);
+#pragma unroll 4
+        for (int i = 0; i < nrow; i++) {
+            const int64_t row = rbase + i;
+            uint4 cv[NCOMP];
+#pragma unroll
+            for (int c = 0; c < NCOMP; c++)
+                cv[c] = lane_live ? __ldcs(reinterpret_cast<const uint4*>(p.comp[c] + row * p.pitch + col0))
+                                  : make_uint4(0, 0, 0, 0);
+#pragma unroll
+            for (int ps = 0; ps < NPASS; ps++) {
+#pragma unroll
+                for (int q = 0; q < NPARTY; q++) {
+                    const int j = ps * NPARTY + q;
+                    const uint4 A = cv[q], B = cv[(q + 1) % NCOMP];
+                    const uint32_t part = ((A.x & ia[j].x) ^ (B.x & ib[j].x)) ^ ((A.y & ia[j].y) ^ (B.y & ib[j].y)) ^
+                                          ((A.z & ia[j].z) ^ (B.z & ib[j].z)) ^ ((A.w & ia[j].w) ^ (B.w & ib[j].w));
+                    const uint32_t bal = __ballot_sync(0xffffffffu, __popc(part) & 1);
+                    word[j] |= (uint32_t)(__popc(bal) & 1) << i;
+                }
+            }
+        }
+        if (lane < NJ) {
+            uint32_t v = 0;
+#pragma unroll
+            for (int j = 0; j < NJ; j++)
+                if (j == lane) v = word[j];
+            if (v) atomicXor(p.out[lane] + tile, v);
+        }
+    }
+}
+
 // ---------------------------------------------------------------------------
 // src/rss.py:143-148 for all three parties at once: alpha_q = F(k_q) ^
 // F(k_{q-1}) (party q holds its own key and its predecessor's,
@@ -427,6 +504,33 @@ int ogm_masked_parity(int64_t rows, int64_t words, int64_t pitch, int ncomp, con
     p.rows = rows;
     p.words = words;
     p.pitch = pitch;
+    cudaStream_t st = as_stream(stream);
+    if (aligned && words >= 64) {
+        // register-resident indicators; CW warps (x128 columns) per row group
+        int CW = 1;
+        while (CW < 8 && CW * 128 < words) CW <<= 1;
+        const int64_t col_chunks = (words + CW * 128 - 1) / (CW * 128);
+        const int64_t ntiles = (rows + 31) / 32;
+        const int64_t want_blocks = (int64_t)sm_count() * 6;
+        int64_t row_blocks = want_blocks / col_chunks;
+        if (row_blocks < 1) row_blocks = 1;
+        if (row_blocks > 65535) row_blocks = 65535;
+        const int RG = 8 / CW;
+        int64_t tpb = (ntiles + row_blocks - 1) / row_blocks;
+        tpb = (tpb + RG - 1) / RG * RG;
+        row_blocks = (ntiles + tpb - 1) / tpb;
+        for (int j = 0; j < npass * nparty; j++)
+            OGM_CUDA_TRY(cudaMemsetAsync(out[j], 0, 4 * ntiles, st));
+        dim3 grid((unsigned)col_chunks, (unsigned)row_blocks);
+#define OGM_PARITY2(NP, NS) masked_parity_v2_kernel<NP, NS><<<grid, 256, 0, st>>>(p, CW, tpb)
+        if (nparty == 1 && npass == 1) OGM_PARITY2(1, 1);
+        else if (nparty == 1) OGM_PARITY2(1, 2);
+        else if (npass == 1) OGM_PARITY2(3, 1);
+        else OGM_PARITY2(3, 2);
+#undef OGM_PARITY2
+        OGM_LAUNCH_CHECK();
+        return OGM_OK;
+    }
     const int64_t units = aligned ? (words + 3) / 4 : words;
     int G = 1;
     while (G < 32 && G * 4 < units) G <<= 1;  // >= ~4 loads per lane per row
@@ -436,7 +540,6 @@ int ogm_masked_parity(int64_t rows, int64_t words, int64_t pitch, int ncomp, con
     int64_t cap = (int64_t)sm_count() * 8;
     if (grid > cap) grid = cap;
     if (grid < 1) grid = 1;
-    cudaStream_t st = as_stream(stream);
 #define OGM_PARITY_LAUNCH(V, NP, NS) masked_parity_kernel<V, NP, NS><<<(int)grid, 256, 0, st>>>(p)
     if (aligned) {
         if (nparty == 1 && npass == 1) OGM_PARITY_LAUNCH(true, 1, 1);

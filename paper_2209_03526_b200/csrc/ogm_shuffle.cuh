@@ -201,6 +201,15 @@ __global__ void __launch_bounds__(kAesThreads) shuffle_gather_kernel(const Gathe
     }
 }
 
+// out[i] = inner[outer[i]]: the composition a party precomputes offline for
+// the two permutations it knows (pi12 o pi31 at P1, pi31 o pi23 at P3).
+__global__ void perm_compose_kernel(const int32_t* __restrict__ outer, const int32_t* __restrict__ inner,
+                                    int64_t n, int32_t* __restrict__ out) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
+        out[i] = __ldg(inner + __ldg(outer + i));
+}
+
 int shuffle_init() {
     OGM_CUDA_TRY(allow_big_smem(perm_draws_kernel, kAesTableBytes));
     OGM_CUDA_TRY(allow_big_smem(shuffle_gather_kernel<true>, kAesTableBytes));
@@ -264,6 +273,17 @@ int ogm_seeded_permutation(const uint8_t* key, const uint8_t* label, uint64_t in
     OGM_CHECK_ARG(n == 0 || workspace, OGM_ERR_ARG, "permutation workspace is required");
     OGM_ENSURE_INIT();
     return ogm::seeded_permutation_impl(key, label, index, n, perm, workspace, ogm::as_stream(stream));
+}
+
+int ogm_perm_compose(int64_t n, const int32_t* outer, const int32_t* inner, int32_t* out, void* stream) {
+    OGM_CHECK_ARG(n >= 0, OGM_ERR_ARG, "negative length");
+    if (n == 0) return OGM_OK;
+    int64_t g = (n + 255) / 256;
+    const int64_t cap = (int64_t)ogm::sm_count() * 16;
+    if (g > cap) g = cap;
+    ogm::perm_compose_kernel<<<(int)g, 256, 0, ogm::as_stream(stream)>>>(outer, inner, n, out);
+    OGM_LAUNCH_CHECK();
+    return OGM_OK;
 }
 
 static int set_term(ogm::GatherTerm& g, const uint8_t* key, const uint8_t* label, uint64_t index,

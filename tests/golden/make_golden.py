@@ -192,11 +192,14 @@ def engine_fixture(ref):
     # --- sec_eval: per-party output shares + transcripts (src/engine.py:139-165)
     ev_cases = [("eq", (5,), 16, [5, 7, 5, 0]), ("ge", (0,), 8, [None, 2, None]),
                 ("lt", (40,), 128, list(range(0, 128, 3))), ("iv", (30, 40), 128, None),
-                ("iv", (3, 200), 333, None), ("le", (63,), 64, None)]
+                ("iv", (3, 200), 333, None), ("le", (63,), 64, None),
+                ("iv", (100, 3000), 4000, None), ("eq", (77,), 2500, None)]
     for ci, (kind, ops, domain, values) in enumerate(ev_cases):
         rng = np.random.default_rng(100 + ci)
         if values is None:
-            values = rng.integers(0, domain, size=97).tolist()
+            values = rng.integers(0, domain, size=97 if domain < 1000 else 203).tolist()
+            if kind == "eq":
+                values[::7] = [ops[0]] * len(values[::7])
         comps = _group_shares(values, domain, rng)
         groups = _groups(ref, comps, len(values), domain)
         if kind == "iv":

@@ -38,8 +38,9 @@ def digest(g, key):
     return bytes(g[key]).hex()
 
 
-def make_groups(g, tag, count, domain, with_ids=True):
-    attr = [dev(g[f"{tag}_attr{c}"]) for c in range(3)]
+def make_groups(g, tag, count, domain, with_ids=True, padded=False):
+    from paper_2209_03526_b200.graphs import padded_device_matrix
+    attr = [padded_device_matrix(g[f"{tag}_attr{c}"]) if padded else dev(g[f"{tag}_attr{c}"]) for c in range(3)]
     if with_ids and f"{tag}_id0" in g:
         ids = [dev(g[f"{tag}_id{c}"]) for c in range(3)]
     else:
@@ -49,11 +50,12 @@ def make_groups(g, tag, count, domain, with_ids=True):
                            {"a": (attr[p], attr[(p + 1) % 3])}, {"a": domain}) for p in range(3)]
 
 
-def test_sec_eval_matches_reference(golden):
+@pytest.mark.parametrize("padded", [False, True])
+def test_sec_eval_matches_reference(golden, padded):
     g = golden("engine")
     for tag in g["ev_cases"]:
         count, domain = int(g[f"{tag}_count"]), int(g[f"{tag}_domain"])
-        groups = make_groups(g, tag, count, domain, with_ids=False)
+        groups = make_groups(g, tag, count, domain, with_ids=False, padded=padded)
         keys = [(fss.parse_key(g[f"{tag}_key{p}_0"].tobytes()), fss.parse_key(g[f"{tag}_key{p}_1"].tobytes()))
                 for p in range(3)]
         rts = local_runtimes(make_session_configs(g[f"{tag}_master"].tobytes()), transcript=True)
@@ -191,3 +193,36 @@ def test_open_label_guard_and_and_gate():
     z = run_trio(lambda rt: rss.and_gate(rt, sa[rt.index - 1], sb[rt.index - 1]),
                  local_runtimes(make_session_configs(b"\x02" * 16)))
     assert rss.reconstruct(z) == (a & b)
+
+
+@pytest.mark.parametrize("words,rows", [(11, 70), (64, 1000), (100, 333), (5691, 2048)])
+@pytest.mark.parametrize("npass", [1, 2])
+def test_masked_parity_kernels_vs_oracle(words, rows, npass):
+    """Both kernel paths (unaligned G-lane, aligned register-indicator) for
+    per-party and trio launches against the oracle's src/engine.py:76-80."""
+    import oracle
+    from paper_2209_03526_b200 import _lib
+    from paper_2209_03526_b200.graphs import padded_device_matrix
+    rng = np.random.default_rng(words * 7 + rows + npass)
+    comps_h = [rng.integers(0, 1 << 32, (rows, words), dtype=np.uint32) for _ in range(3)]
+    inds_h = [[rng.integers(0, 1 << 32, words, dtype=np.uint32) for _ in range(2)] for _ in range(3 * npass)]
+    A = _lib.ptr_array
+    for padded in (False, True):
+        comps = [padded_device_matrix(c) if padded else dev(c) for c in comps_h]
+        inds = [[dev(x) for x in pair] for pair in inds_h]
+        pitch = comps[0].stride(0)
+        # trio: j = pass*3 + party
+        outs = [torch.empty(((rows + 31) // 32,), dtype=torch.int32, device="cuda") for _ in range(3 * npass)]
+        _lib.call("ogm_masked_parity", rows, words, pitch, 3, A(comps), 3, _lib.int_array([0, 1, 2]),
+                  _lib.int_array([1, 2, 0]), npass, A([t for pair in inds for t in pair]), A(outs), _lib.stream_ptr())
+        for ps in range(npass):
+            for q in range(3):
+                j = ps * 3 + q
+                want = oracle.masked_parity(comps_h[q], comps_h[(q + 1) % 3], inds_h[j][0], inds_h[j][1])
+                got = np.unpackbits(host(outs[j]).view(np.uint8), bitorder="little")[:rows]
+                assert np.array_equal(got, want), (words, rows, npass, padded, j)
+                # per-party launch of the same party/pass
+                o1 = torch.empty_like(outs[j])
+                _lib.call("ogm_masked_parity", rows, words, pitch, 2, A([comps[q], comps[(q + 1) % 3]]), 1,
+                          _lib.int_array([0]), _lib.int_array([1]), 1, A(inds[j]), A([o1]), _lib.stream_ptr())
+                assert torch.equal(o1, outs[j])
