@@ -272,9 +272,78 @@ def run_c5(args):
         torch.cuda.empty_cache()
 
 
+# ---------------------------------------------------------------------------
+# C4: large graph, root-slot secEval on the Zipf attribute, rows sharded
+# across ranks (torchrun, one process per GPU; NCCL all-gather of match bits)
+# ---------------------------------------------------------------------------
+
+
+def run_c4(args):
+    import os
+
+    import torch.distributed as dist
+
+    from paper_2209_03526_b200.sharding import ShardPlan, sharded_sec_eval_trio
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    rows, n = args.c4_rows, 10_000  # 2M vertices of the root type; Zipf(1.1) over 10^4 values
+    plan = ShardPlan(rows, world)
+    lo, hi = plan.bounds(rank)
+    rng = np.random.default_rng(args.seed)
+    ranks = np.arange(1, n + 1)
+    p = 1.0 / ranks ** 1.1
+    vals_all = rng.choice(n, size=rows, p=p / p.sum()).astype(np.int32)
+    vals = torch.from_numpy(vals_all[lo:hi]).cuda()
+    c1, c2, c3 = workloads.shared_one_hot(vals, n, args.seed + rank, 40)
+    comps = [c1, c2, c3]
+    w = words_for(n)
+    krng = np.random.default_rng(args.seed + 1)  # identical keys on every rank
+    pairs = [fss.ic_gen(100, 4000, n, krng) for _ in range(3)]
+    (k11, k21), (k12, k22), (k13, k23) = pairs
+    keys = [(k11, k12), (k22, k13), (k23, k21)]
+    inds = [[(fss.full_domain(fss.KeyBatch.from_keys([fss.key_parts_for_engine(keys[q][0])[ps]]), n)[0],
+              fss.full_domain(fss.KeyBatch.from_keys([fss.key_parts_for_engine(keys[q][1])[ps]]), n)[0])
+             for q in range(3)] for ps in range(2)]
+    cfg = make_session_configs(b"\x44" * 16)
+    zk = [(c.zero_key_own, c.zero_key_prev) for c in cfg]
+    step = lambda: sharded_sec_eval_trio(comps, w, plan, rank, inds, zk, [0, 1])  # noqa: E731
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ev = events(2)
+    ev[0].record()
+    for _ in range(args.steps):
+        res = step()
+    ev[1].record()
+    torch.cuda.synchronize()
+    ms = ev[0].elapsed_time(ev[1]) / args.steps
+    t = torch.tensor([ms], device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    if rank == 0:
+        nbytes_local = 3 * (hi - lo) * w * 4
+        emit({"config": f"C4 root secEval, {rows} candidates (Zipf attr n={n}, w={w}), interval, "
+                        f"rows sharded x{world}", "metric": "secEval_candidates_per_s",
+              "value": rows / (ms * 1e-3), "unit": "candidates/s", "ms_per_step": ms, "n_gpus": world,
+              "scaling": "strong", "rank0_hbm_GBps": nbytes_local / (ms * 1e-3) / 1e9,
+              "collective": "NCCL all_gather of packed blinded match bits" if world > 1 else "none",
+              "result_words": int(res[0][0].numel())})
+    if world > 1:
+        dist.destroy_process_group()
+
+
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("which", choices=["c1", "c3", "c5", "all"])
+    ap.add_argument("which", choices=["c1", "c3", "c4", "c5", "all"])
+    ap.add_argument("--c4-rows", type=int, default=2_000_000)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--seed", type=int, default=1)
@@ -290,6 +359,8 @@ def main():
         run_c3(args)
     if args.which in ("c5", "all"):
         run_c5(args)
+    if args.which == "c4":
+        run_c4(args)
 
 
 if __name__ == "__main__":

@@ -87,6 +87,14 @@ int ogm_prf_words(const uint8_t* key, const uint8_t* label, uint64_t index, uint
 int ogm_zero_share(const uint8_t* key_own, const uint8_t* key_prev, uint64_t counter,
                    int64_t nbits, const uint32_t* xor_into, uint32_t* out, void* stream);
 
+/* Words [first_word, first_word + nwords) of the same zero share (random
+ * access by CTR block): the slice a rank owns when candidate rows are
+ * sharded across GPUs; concatenated slices equal the
+ * unsharded share bit for bit. */
+int ogm_zero_share_slice(const uint8_t* key_own, const uint8_t* key_prev, uint64_t counter,
+                         int64_t total_nbits, uint64_t first_word, int64_t nwords,
+                         const uint32_t* xor_into, uint32_t* out, void* stream);
+
 /* src/prf.py:95-105 seeded_permutation: Fisher-Yates driven by
  * prf_stream(key, label, index, 8(n-1)); bit-exact, computed on the device by
  * deterministic reservations.  perm: n int32 (gather semantics, M[perm]).

@@ -40,6 +40,7 @@ SIGNATURES = {
     "ogm_prg_expand": ([_vp, _i64, _vp, _vp, _vp, _vp, _vp, _vp], _int),
     "ogm_prf_words": ([_cp, _cp, _u64, _u64, _i64, _vp, _vp], _int),
     "ogm_zero_share": ([_cp, _cp, _u64, _i64, _vp, _vp, _vp], _int),
+    "ogm_zero_share_slice": ([_cp, _cp, _u64, _i64, _u64, _i64, _vp, _vp, _vp], _int),
     "ogm_perm_workspace_bytes": ([_i64], _i64),
     "ogm_seeded_permutation": ([_cp, _cp, _u64, _i64, _vp, _vp, _vp], _int),
     "ogm_fss_gen": ([_int, _int, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp], _int),

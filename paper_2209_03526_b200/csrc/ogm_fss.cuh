@@ -259,7 +259,7 @@ __global__ void __launch_bounds__(kFssThreads) prf_words_kernel(
             if (ZERO) {
                 // BitVector(additive ^ share, n) semantics: tail masked after the fold
                 if (xor_into) v ^= xor_into[o];
-                if (o == nwords - 1 && (nbits & 31)) v &= (1u << (nbits & 31)) - 1u;
+                if ((nbits & 31) && (int64_t)(blk * 4 + j) == ((nbits + 31) >> 5) - 1) v &= (1u << (nbits & 31)) - 1u;
             }
             out[o] = v;
         }

@@ -71,6 +71,25 @@ int ogm_zero_share(const uint8_t* key_own, const uint8_t* key_prev, uint64_t cou
     return OGM_OK;
 }
 
+int ogm_zero_share_slice(const uint8_t* key_own, const uint8_t* key_prev, uint64_t counter, int64_t total_nbits,
+                         uint64_t first_word, int64_t nwords, const uint32_t* xor_into, uint32_t* out,
+                         void* stream) {
+    OGM_CHECK_ARG(key_own && key_prev, OGM_ERR_ARG, "zero-share keys are required");
+    OGM_CHECK_ARG(total_nbits >= 0 && nwords >= 0, OGM_ERR_ARG, "negative length");
+    OGM_CHECK_ARG((int64_t)first_word + nwords <= (total_nbits + 31) / 32, OGM_ERR_ARG,
+                  "slice [%llu, +%lld) outside the %lld-bit share", (unsigned long long)first_word,
+                  (long long)nwords, (long long)total_nbits);
+    if (nwords == 0) return OGM_OK;
+    OGM_ENSURE_INIT();
+    static const uint8_t kZshr[4] = {'Z', 'S', 'H', 'R'};
+    AesKeySched k1 = make_sched(key_own), k2 = make_sched(key_prev);
+    int64_t nblk = (int64_t)(((first_word + nwords + 3) >> 2) - (first_word >> 2));
+    prf_words_kernel<true><<<aes_grid(nblk), kFssThreads, kAesTableBytes, as_stream(stream)>>>(
+        k1, k2, label_be(kZshr), counter, first_word, nwords, total_nbits, xor_into, out);
+    OGM_LAUNCH_CHECK();
+    return OGM_OK;
+}
+
 int ogm_fss_gen(int kind, int bits, int64_t K, const uint32_t* alphas, const void* roots0,
                 const void* roots1, void* seed_cw, uint32_t* ctrl, uint8_t* final_cw, void* stream) {
     OGM_CHECK_ARG(kind == OGM_KIND_DPF || kind == OGM_KIND_DCF, OGM_ERR_ARG, "unknown key kind %d", kind);

@@ -226,3 +226,58 @@ def test_masked_parity_kernels_vs_oracle(words, rows, npass):
                 _lib.call("ogm_masked_parity", rows, words, pitch, 2, A([comps[q], comps[(q + 1) % 3]]), 1,
                           _lib.int_array([0]), _lib.int_array([1]), 1, A(inds[j]), A([o1]), _lib.stream_ptr())
                 assert torch.equal(o1, outs[j])
+
+
+@pytest.mark.parametrize("world", [1, 2, 3, 8])
+def test_sharded_sec_eval_slices_equal_unsharded(world):
+    """Per-rank shards (masked parity on the row slice + zero-share slice by
+    CTR-block offset), concatenated in rank order, equal the single-GPU
+    blinded vectors -- what sharded_sec_eval_trio all-gathers."""
+    import oracle
+    from paper_2209_03526_b200 import _lib
+    from paper_2209_03526_b200.graphs import padded_device_matrix
+    from paper_2209_03526_b200.sharding import ShardPlan, assemble, pad_slice, sharded_sec_eval_trio
+    rows, words, counters = 5000, 70, [7, 8]
+    rng = np.random.default_rng(world)
+    comps_h = [rng.integers(0, 1 << 32, (rows, words), dtype=np.uint32) for _ in range(3)]
+    inds_h = [[(rng.integers(0, 1 << 32, words, dtype=np.uint32), rng.integers(0, 1 << 32, words, dtype=np.uint32))
+               for _ in range(3)] for _ in range(2)]
+    keys = [bytes([9 + i]) * 16 for i in range(3)]
+    zk = [(keys[0], keys[2]), (keys[1], keys[0]), (keys[2], keys[1])]
+    comps = [padded_device_matrix(c) for c in comps_h]
+    inds = [[(dev(a), dev(b)) for a, b in ps] for ps in inds_h]
+    plan = ShardPlan(rows, world)
+    chunks = [[[] for _ in range(3)] for _ in range(2)]
+    for r in range(world):
+        lo, hi = plan.bounds(r)
+        local = [c[lo:hi] for c in comps]
+        res = sharded_sec_eval_trio(local, words, ShardPlan(rows, 1) if world == 1 else plan, r, inds, zk,
+                                    counters) if world == 1 else None
+        if world > 1:
+            # same steps as sharded_sec_eval_trio minus the collective
+            nloc = hi - lo
+            outs = [torch.empty((max((nloc + 31) // 32, 1),), dtype=torch.int32, device="cuda") for _ in range(6)]
+            A = _lib.ptr_array
+            if nloc:
+                flat = [t for ps in range(2) for q in range(3) for t in inds[ps][q]]
+                _lib.call("ogm_masked_parity", nloc, words, local[0].stride(0), 3, A(local), 3,
+                          _lib.int_array([0, 1, 2]), _lib.int_array([1, 2, 0]), 2, A(flat), A(outs),
+                          _lib.stream_ptr())
+            w0, w1 = plan.word_bounds(r)
+            for ps in range(2):
+                for q in range(3):
+                    add = outs[ps * 3 + q][: w1 - w0]
+                    if w1 > w0:
+                        _lib.call("ogm_zero_share_slice", zk[q][0], zk[q][1], counters[ps], rows, w0, w1 - w0,
+                                  _lib.ptr(add), _lib.ptr(add), _lib.stream_ptr())
+                    chunks[ps][q].append(pad_slice(add, plan))
+        else:
+            for ps in range(2):
+                for q in range(3):
+                    chunks[ps][q] = [res[ps][q]]
+    for ps in range(2):
+        for q in range(3):
+            got = chunks[ps][q][0] if world == 1 else assemble(torch.cat(chunks[ps][q]), plan)
+            want = oracle.pack_bits(oracle.masked_parity(comps_h[q], comps_h[(q + 1) % 3], *inds_h[ps][q]))
+            want = want ^ oracle.zero_share(*zk[q], counters[ps], rows)
+            assert np.array_equal(host(got), want), (world, ps, q)

@@ -1,0 +1,99 @@
+"""Multi-rank secEval host logic on CPU: world_size-2 gloo all-gather of
+row-sharded, zero-share-blinded match bits must equal the unsharded result
+bit for bit.  The per-shard arithmetic is the CPU oracle
+(tests may call it); the shard plan, CTR-block-aligned slicing, padding and
+assembly are the product's (paper_2209_03526_b200.sharding)."""
+
+import os
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+import oracle
+from paper_2209_03526_b200.sharding import ALIGN_ROWS, ShardPlan, all_gather_bits
+
+ROWS, WORDS, COUNTER = 1000, 9, 5
+KEYS = [bytes([i + 1]) * 16 for i in range(3)]
+PAIRS = [(KEYS[0], KEYS[2]), (KEYS[1], KEYS[0]), (KEYS[2], KEYS[1])]
+
+
+def _inputs():
+    rng = np.random.default_rng(42)
+    comps = [rng.integers(0, 1 << 32, (ROWS, WORDS), dtype=np.uint32) for _ in range(3)]
+    inds = [(rng.integers(0, 1 << 32, WORDS, dtype=np.uint32), rng.integers(0, 1 << 32, WORDS, dtype=np.uint32))
+            for _ in range(3)]
+    return comps, inds
+
+
+def _blinded_reference():
+    comps, inds = _inputs()
+    out = []
+    for q in range(3):
+        bits = oracle.masked_parity(comps[q], comps[(q + 1) % 3], *inds[q])
+        out.append(oracle.pack_bits(bits) ^ oracle.zero_share(*PAIRS[q], COUNTER, ROWS))
+    return out
+
+
+def _zero_share_slice(q, w0, nwords):
+    """Words [w0, w0+nwords) of the share via CTR block offsets (oracle)."""
+    blk0 = w0 // 4
+    raw = [np.frombuffer(oracle.prf_stream(k, b"ZSHR", COUNTER, 16 * (-(-nwords // 4)), block_offset=blk0),
+                         np.uint32) for k in PAIRS[q]]
+    w = (raw[0] ^ raw[1])[:nwords].copy()
+    total = -(-ROWS // 32)
+    if ROWS % 32 and w0 + nwords == total:
+        w[-1] &= np.uint32((1 << (ROWS % 32)) - 1)
+    return w
+
+
+def _worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    comps, inds = _inputs()
+    plan = ShardPlan(ROWS, world)
+    lo, hi = plan.bounds(rank)
+    w0, w1 = plan.word_bounds(rank)
+    outs = []
+    for party in range(3):
+        bits = oracle.masked_parity(comps[party][lo:hi], comps[(party + 1) % 3][lo:hi], *inds[party])
+        local = oracle.pack_bits(bits) if hi > lo else np.zeros(0, np.uint32)
+        local = local ^ _zero_share_slice(party, w0, w1 - w0)
+        full = all_gather_bits(torch.from_numpy(local.view(np.int32).copy()), plan)
+        outs.append(full.numpy().view(np.uint32).copy())
+    q.put((rank, outs))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_sharded_sec_eval_equals_unsharded(world):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = 29500 + world * 7 + os.getpid() % 1000
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    got = dict(q.get(timeout=120) for _ in range(world))
+    for p in procs:
+        p.join(60)
+        assert p.exitcode == 0
+    want = _blinded_reference()
+    for r in range(world):
+        for party in range(3):
+            assert np.array_equal(got[r][party], want[party]), (world, r, party)
+
+
+def test_plan_alignment_and_coverage():
+    for rows in (1, 31, 128, 1000, 200_000, 2_000_001):
+        for world in (1, 2, 4, 8):
+            plan = ShardPlan(rows, world)
+            covered = []
+            for r in range(world):
+                lo, hi = plan.bounds(r)
+                assert lo % ALIGN_ROWS == 0 or lo == rows
+                covered.extend(range(lo, hi)) if rows < 5000 else None
+            if rows < 5000:
+                assert covered == list(range(rows))
+            assert plan.bounds(world - 1)[1] == rows
