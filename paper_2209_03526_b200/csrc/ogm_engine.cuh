@@ -168,24 +168,33 @@ __global__ void __launch_bounds__(256) masked_parity_v2_kernel(const ParityArgs 
         for (int j = 0; j < NJ; j++) word[j] = 0;
         const int64_t rbase = tile << 5;
         const int nrow = (int)min((int64_t)32, p.rows - rbase);
-#pragma unroll 4
-        for (int i = 0; i < nrow; i++) {
-            const int64_t row = rbase + i;
-            uint4 cv[NCOMP];
+        // rows in batches of RB: issue all RB x NCOMP 128-bit loads before the
+        // first ballot so each lane keeps RB*NCOMP*16 B in flight.
+        constexpr int RB = NPARTY == 1 ? 8 : 4;
+        for (int i0 = 0; i0 < nrow; i0 += RB) {
+            uint4 cv[RB][NCOMP];
 #pragma unroll
-            for (int c = 0; c < NCOMP; c++)
-                cv[c] = lane_live ? __ldcs(reinterpret_cast<const uint4*>(p.comp[c] + row * p.pitch + col0))
+            for (int r = 0; r < RB; r++) {
+                const int64_t row = rbase + i0 + r;
+                const bool ok = lane_live && (i0 + r) < nrow;
+#pragma unroll
+                for (int c = 0; c < NCOMP; c++)
+                    cv[r][c] = ok ? __ldcs(reinterpret_cast<const uint4*>(p.comp[c] + row * p.pitch + col0))
                                   : make_uint4(0, 0, 0, 0);
+            }
 #pragma unroll
-            for (int ps = 0; ps < NPASS; ps++) {
+            for (int r = 0; r < RB; r++) {
 #pragma unroll
-                for (int q = 0; q < NPARTY; q++) {
-                    const int j = ps * NPARTY + q;
-                    const uint4 A = cv[q], B = cv[(q + 1) % NCOMP];
-                    const uint32_t part = ((A.x & ia[j].x) ^ (B.x & ib[j].x)) ^ ((A.y & ia[j].y) ^ (B.y & ib[j].y)) ^
-                                          ((A.z & ia[j].z) ^ (B.z & ib[j].z)) ^ ((A.w & ia[j].w) ^ (B.w & ib[j].w));
-                    const uint32_t bal = __ballot_sync(0xffffffffu, __popc(part) & 1);
-                    word[j] |= (uint32_t)(__popc(bal) & 1) << i;
+                for (int ps = 0; ps < NPASS; ps++) {
+#pragma unroll
+                    for (int q = 0; q < NPARTY; q++) {
+                        const int j = ps * NPARTY + q;
+                        const uint4 A = cv[r][q], B = cv[r][(q + 1) % NCOMP];
+                        const uint32_t part = ((A.x & ia[j].x) ^ (B.x & ib[j].x)) ^ ((A.y & ia[j].y) ^ (B.y & ib[j].y)) ^
+                                              ((A.z & ia[j].z) ^ (B.z & ib[j].z)) ^ ((A.w & ia[j].w) ^ (B.w & ib[j].w));
+                        const uint32_t bal = __ballot_sync(0xffffffffu, __popc(part) & 1);
+                        word[j] |= (uint32_t)(__popc(bal) & 1) << (i0 + r);
+                    }
                 }
             }
         }

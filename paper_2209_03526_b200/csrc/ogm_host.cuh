@@ -137,6 +137,11 @@ static int device_init() {
     OGM_CUDA_TRY(cudaMemcpyToSymbol(c_T0, h.t0, sizeof h.t0));
     OGM_CUDA_TRY(cudaMemcpyToSymbol(c_prg_rk, rk, sizeof rk));
     OGM_CUDA_TRY(cudaMemcpyToSymbol(c_prg_dlr, dlr, sizeof dlr));
+    // Random 16-byte row gathers (shuffle) otherwise pull a whole 128-byte
+    // line per miss; streaming kernels request full lines anyway.
+    size_t gran = 0;
+    if (cudaDeviceGetLimit(&gran, cudaLimitMaxL2FetchGranularity) == cudaSuccess && gran > 32)
+        OGM_CUDA_TRY(cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, 32));
     int rc = fss_init();
     if (rc) return rc;
     rc = engine_init();
