@@ -222,10 +222,10 @@ def run_c5(args):
         def online(pre: bool):
             # the four party-local steps of src/shuffle.py:106-143 in protocol order
             if pre:
-                gather(rows, width, x1, inner=off[0].k1, m1=comps[0], m2=comps[1], r=off[0].u)
-                gather(rows, width, y1, inner=off[1].pi12, m1=comps[2], r=off[1].v)
-                gather(rows, width, c1, inner=off[1].pi23, m1=x1, r=off[1].w)
-                gather(rows, width, r3, inner=off[2].k3, m1=y1, m3=c1, r=off[2].z)
+                off[0].step_x1(comps[0], comps[1], x1)
+                off[1].step_y1(comps[2], y1)
+                off[1].step_c1(x1, c1)
+                off[2].step_r3(y1, c1, r3)
                 return
             gather(rows, width, x1, outer=pi31, inner=pi12, m1=comps[0], m2=comps[1],
                    t1=(s12, b"SHTB", 0), t2=(s31, b"SHTB", 0))
@@ -254,14 +254,17 @@ def run_c5(args):
             torch.cuda.synchronize()
             ms = statistics.median(ev[i].elapsed_time(ev[i + 1]) for i in range(args.steps))
             if pre:
-                # x1: 2 gathers + U1 + write; y1: gather + V + write; c1: gather + W + write;
-                # R3: gather + c1 + Z + write  = 14 row moves (16 B) + 4 coalesced index reads
+                # algorithmic (protocol) bytes: x1: 2 gathers + U1 + write; y1: gather + V + write;
+                # c1: gather + W + write; R3: gather + c1 + Z + write = 14 row moves (16 B) + 4 index
+                # reads.  The planned two-pass execution moves more bytes physically (scratch pass).
                 nbytes = rows * (14 * 16 + 4 * 4)
             else:
                 # 10 row moves + 6 index reads (2 of them dependent/random); blinds by AES
                 nbytes = rows * (10 * 16 + 6 * 4)
             emit({"config": f"C5 shuffle 2^{lg} rows x 128-bit", "metric": "shuffle_online_GBps",
-                  "blinds": "offline (ShuffleOffline: composed perms + permuted combined blinds)" if pre
+                  "blinds": ("offline (ShuffleOffline: composed perms + permuted combined blinds"
+                             + (", planned two-pass gathers)" if off[1].plan_y1 is not None else ", direct gathers)"))
+                  if pre
                   else "AES-CTR on the fly, nested permutation lookups",
                   "value": nbytes / (ms * 1e-3) / 1e9, "unit": "GB/s", "ms": ms,
                   "hbm_frac": nbytes / (ms * 1e-3) / 1e9 / HBM_PEAK, "algorithmic_bytes_per_row": nbytes // rows,

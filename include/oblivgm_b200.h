@@ -223,6 +223,19 @@ int ogm_shuffle_gather(int64_t rows, int64_t words, int64_t width_bits, const in
  * (gather semantics, so M[out] = M[inner][outer] as in src/shuffle.py:76-77). */
 int ogm_perm_compose(int64_t n, const int32_t* outer, const int32_t* inner, int32_t* out, void* stream);
 
+/* Planned two-pass gather (offline plan for a data-independent permutation):
+ * out[i] = (m1 ^ m2)[idx[i]] ^ r_mat[i] ^ m3[i] computed as a bucket scatter
+ * into `inter` (rows x words scratch) followed by a shared-memory tile
+ * gather, both streaming.  ogm_gather_tile_rows(words) gives the tile size;
+ * ogm_gather_plan derives pos1/q2 (n int32 each) from idx. */
+int64_t ogm_gather_tile_rows(int64_t words);
+int64_t ogm_gather_plan_workspace_bytes(int64_t n);
+int ogm_gather_plan(int64_t n, const int32_t* idx, int64_t tile_rows, int32_t* pos1, int32_t* q2,
+                    void* workspace, int64_t workspace_bytes, void* stream);
+int ogm_gather_planned(int64_t rows, int64_t words, int64_t tile_rows, const int32_t* pos1,
+                       const int32_t* q2, const uint32_t* m1, const uint32_t* m2, const uint32_t* m3,
+                       const uint32_t* r_mat, uint32_t* inter, uint32_t* out, void* stream);
+
 /* ---- measurement -------------------------------------------------------- */
 
 /* Roofline denominator for the integer-ALU-bound kernels: issue rate of

@@ -278,8 +278,21 @@ __global__ void and_terms_kernel(const AndArgs a, int64_t nwords) {
 __global__ void xor3_kernel(const uint32_t* __restrict__ a, const uint32_t* __restrict__ b,
                             const uint32_t* __restrict__ c, uint32_t* __restrict__ out, int64_t nwords) {
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nwords; i += stride)
-        out[i] = a[i] ^ b[i] ^ (c ? c[i] : 0u);
+    const int64_t t0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const bool vec = ((((uintptr_t)a) | ((uintptr_t)b) | ((uintptr_t)c) | ((uintptr_t)out)) & 15) == 0;
+    int64_t done = 0;
+    if (vec) {  // 128-bit streaming body
+        const int64_t n4 = nwords >> 2;
+        const uint4 *a4 = (const uint4*)a, *b4 = (const uint4*)b, *c4 = (const uint4*)c;
+        uint4* o4 = (uint4*)out;
+        for (int64_t i = t0; i < n4; i += stride) {
+            uint4 v = xor4(__ldcs(a4 + i), __ldcs(b4 + i));
+            if (c) v = xor4(v, __ldcs(c4 + i));
+            __stcs(o4 + i, v);
+        }
+        done = n4 << 2;
+    }
+    for (int64_t i = done + t0; i < nwords; i += stride) out[i] = a[i] ^ b[i] ^ (c ? c[i] : 0u);
 }
 
 // ---------------------------------------------------------------------------

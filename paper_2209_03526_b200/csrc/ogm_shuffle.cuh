@@ -2,6 +2,8 @@
 // secret-shared shuffle (src/shuffle.py:80-144) for sm_100a.
 #pragma once
 
+#include <cub/cub.cuh>
+
 #include "ogm_aes.cuh"
 #include "ogm_common.cuh"
 #include "ogm_host.cuh"
@@ -210,9 +212,176 @@ __global__ void perm_compose_kernel(const int32_t* __restrict__ outer, const int
         out[i] = __ldg(inner + __ldg(outer + i));
 }
 
+
+// ---------------------------------------------------------------------------
+// Planned two-pass gather for a permutation known ahead of the data.
+//
+// A party's online shuffle step is out[i] = M[k(i)] ^ (terms at i), with k a
+// permutation the party fixed offline (src/shuffle.py:106-143).  A direct
+// gather reads one random 16-byte row per output row; HBM serves that at
+// ~1/4 of streaming bandwidth.  Since k is data-independent, the offline
+// phase plans two streaming passes instead:
+//
+//   pass 1 (bucket scatter):  inter[pos1[j]] = M1[j] ^ M2[j]   (j sequential)
+//       pos1 puts every source row into the bucket of its destination tile,
+//       in increasing j within the bucket, so each bucket fills front to back
+//       and its open lines merge in L2 before they are written back;
+//   pass 2 (tile gather):     out[i] = tile[q2[i]] ^ R[i] ^ M3[i]
+//       one CTA stages a bucket (<= 96 KB) in shared memory and emits its
+//       tile in order: coalesced reads and writes.
+// ---------------------------------------------------------------------------
+__global__ void invert_perm_kernel(const int32_t* __restrict__ k, int64_t n, int32_t* __restrict__ inv) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) inv[k[i]] = (int32_t)i;
+}
+
+__global__ void tile_keys_kernel(const int32_t* __restrict__ inv, int64_t n, int64_t T, int32_t* __restrict__ key,
+                                 int32_t* __restrict__ val) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += stride) {
+        key[j] = (int32_t)(inv[j] / T);
+        val[j] = (int32_t)j;
+    }
+}
+
+__global__ void scatter_pos_kernel(const int32_t* __restrict__ sorted_j, int64_t n, int32_t* __restrict__ pos1) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < n; p += stride) pos1[sorted_j[p]] = (int32_t)p;
+}
+
+__global__ void local_q_kernel(const int32_t* __restrict__ k, const int32_t* __restrict__ pos1, int64_t n, int64_t T,
+                               int32_t* __restrict__ q2) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
+        q2[i] = (int32_t)(pos1[k[i]] - (i / T) * T);
+}
+
+__global__ void bucket_scatter_kernel(const int32_t* __restrict__ pos1, const uint32_t* __restrict__ m1,
+                                      const uint32_t* __restrict__ m2, int64_t rows, int64_t W,
+                                      uint32_t* __restrict__ inter) {
+    const int64_t total = rows * W;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += stride) {
+        const int64_t j = t / W, w = t - j * W;
+        uint32_t v = __ldcs(m1 + t);
+        if (m2) v ^= __ldcs(m2 + t);
+        inter[(int64_t)__ldcs(pos1 + j) * W + w] = v;
+    }
+}
+
+__global__ void __launch_bounds__(512) tile_gather_kernel(const int32_t* __restrict__ q2,
+                                                          const uint32_t* __restrict__ inter,
+                                                          const uint32_t* __restrict__ r,
+                                                          const uint32_t* __restrict__ m3, int64_t rows, int64_t W,
+                                                          int64_t T, uint32_t* __restrict__ out) {
+    extern __shared__ __align__(16) uint32_t tile[];
+    const int64_t ntiles = (rows + T - 1) / T;
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        const int64_t r0 = t * T;
+        const int64_t nr = min(T, rows - r0);
+        const int64_t nw = nr * W;
+        const uint32_t* src = inter + r0 * W;
+        __syncthreads();
+        for (int64_t e = threadIdx.x; e < nw; e += blockDim.x) tile[e] = __ldcs(src + e);
+        __syncthreads();
+        for (int64_t e = threadIdx.x; e < nw; e += blockDim.x) {
+            const int64_t li = e / W, w = e - li * W;
+            const int64_t g = (r0 + li) * W + w;
+            uint32_t v = tile[(int64_t)__ldcs(q2 + r0 + li) * W + w];
+            if (r) v ^= __ldcs(r + g);
+            if (m3) v ^= __ldcs(m3 + g);
+            out[g] = v;
+        }
+    }
+}
+
+
+// 128-bit rows (the C5 shape): one thread per row, uint4 traffic only.
+__global__ void bucket_scatter4_kernel(const int32_t* __restrict__ pos1, const uint4* __restrict__ m1,
+                                       const uint4* __restrict__ m2, int64_t rows, uint4* __restrict__ inter) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < rows; j += stride) {
+        uint4 v = __ldcs(m1 + j);
+        if (m2) v = xor4(v, __ldcs(m2 + j));
+        inter[__ldcs(pos1 + j)] = v;
+    }
+}
+
+__global__ void __launch_bounds__(512) tile_gather4_kernel(const int32_t* __restrict__ q2,
+                                                           const uint4* __restrict__ inter,
+                                                           const uint4* __restrict__ r, const uint4* __restrict__ m3,
+                                                           int64_t rows, int T, uint4* __restrict__ out) {
+    extern __shared__ __align__(16) uint4 tile4[];
+    const int64_t ntiles = (rows + T - 1) / T;
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        const int64_t r0 = t * T;
+        const int nr = (int)min((int64_t)T, rows - r0);
+        __syncthreads();
+        for (int e = threadIdx.x; e < nr; e += blockDim.x) tile4[e] = __ldcs(inter + r0 + e);
+        __syncthreads();
+        for (int e = threadIdx.x; e < nr; e += blockDim.x) {
+            uint4 v = tile4[__ldcs(q2 + r0 + e)];
+            if (r) v = xor4(v, __ldcs(r + r0 + e));
+            if (m3) v = xor4(v, __ldcs(m3 + r0 + e));
+            out[r0 + e] = v;
+        }
+    }
+}
+
+constexpr int64_t kTileBytes = 96 * 1024;
+
+
+// All reservation rounds in ONE CTA (small permutations: no host round
+// trips).  Same reserve / commit / reset phases as the multi-kernel loop,
+// separated by __syncthreads (which orders global memory inside the block).
+constexpr int64_t kPermBlockMax = 1 << 16;
+
+__global__ void __launch_bounds__(1024) perm_rounds_block_kernel(const int32_t* __restrict__ H, int32_t* R,
+                                                                 int32_t* perm, int32_t* liveA, int32_t* liveB,
+                                                                 int32_t n_live) {
+    __shared__ int32_t cnt_next;
+    int32_t* cur = liveA;
+    int32_t* nxt = liveB;
+    int32_t c = n_live;
+    while (c > 0) {
+        for (int32_t t = threadIdx.x; t < c; t += blockDim.x) {
+            const int32_t i = cur[t];
+            atomicMax(&R[i], i);
+            atomicMax(&R[H[i]], i);
+        }
+        if (threadIdx.x == 0) cnt_next = 0;
+        __syncthreads();
+        for (int32_t t = threadIdx.x; t < c; t += blockDim.x) {
+            const int32_t i = cur[t];
+            const int32_t h = H[i];
+            if (R[i] == i && R[h] == i) {
+                const int32_t a = perm[i];
+                perm[i] = perm[h];
+                perm[h] = a;
+            } else {
+                nxt[atomicAdd(&cnt_next, 1)] = i;
+            }
+        }
+        __syncthreads();
+        for (int32_t t = threadIdx.x; t < c; t += blockDim.x) {
+            const int32_t i = cur[t];
+            R[i] = -1;
+            R[H[i]] = -1;
+        }
+        __syncthreads();
+        c = cnt_next;
+        int32_t* tmp = cur;
+        cur = nxt;
+        nxt = tmp;
+        __syncthreads();
+    }
+}
+
 int shuffle_init() {
     OGM_CUDA_TRY(allow_big_smem(perm_draws_kernel, kAesTableBytes));
     OGM_CUDA_TRY(allow_big_smem(shuffle_gather_kernel<true>, kAesTableBytes));
+    OGM_CUDA_TRY(allow_big_smem(tile_gather_kernel, (int)kTileBytes));
+    OGM_CUDA_TRY(allow_big_smem(tile_gather4_kernel, (int)kTileBytes));
     return OGM_OK;
 }
 
@@ -234,6 +403,11 @@ static int seeded_permutation_impl(const uint8_t* key, const uint8_t* label, uin
                                                                         live[0], perm, R);
     OGM_LAUNCH_CHECK();
     if (n < 2) return OGM_OK;
+    if (n <= kPermBlockMax) {
+        perm_rounds_block_kernel<<<1, 1024, 0, st>>>(H, R, perm, live[0], live[1], init_cnt);
+        OGM_LAUNCH_CHECK();
+        return OGM_OK;
+    }
     const int grid = sm_count() * 8, threads = 256;
     int cur = 0;
     int32_t remaining = init_cnt;
@@ -338,6 +512,76 @@ int ogm_shuffle_gather(int64_t rows, int64_t words, int64_t width_bits, const in
         const int64_t cap = (int64_t)sm_count() * 8;
         if (g > cap) g = cap;
         shuffle_gather_kernel<false><<<(int)(g < 1 ? 1 : g), kAesThreads, 0, st>>>(a);
+    }
+    OGM_LAUNCH_CHECK();
+    return OGM_OK;
+}
+
+int64_t ogm_gather_tile_rows(int64_t words) {
+    if (words <= 0) return 0;
+    return ogm::kTileBytes / (4 * words);
+}
+
+int64_t ogm_gather_plan_workspace_bytes(int64_t n) {
+    size_t temp = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, temp, (int32_t*)nullptr, (int32_t*)nullptr, (int32_t*)nullptr,
+                                    (int32_t*)nullptr, (int)(n > 0 ? n : 1));
+    return (int64_t)temp + 5 * 4 * n + 1024;
+}
+
+int ogm_gather_plan(int64_t n, const int32_t* idx, int64_t tile_rows, int32_t* pos1, int32_t* q2, void* workspace,
+                    int64_t workspace_bytes, void* stream) {
+    using namespace ogm;
+    OGM_CHECK_ARG(n >= 0 && n < ((int64_t)1 << 31), OGM_ERR_ARG, "plan size out of range");
+    OGM_CHECK_ARG(tile_rows >= 1, OGM_ERR_ARG, "tile_rows must be positive");
+    if (n == 0) return OGM_OK;
+    cudaStream_t st = as_stream(stream);
+    uint8_t* ws = (uint8_t*)workspace;
+    int32_t* inv = (int32_t*)ws;
+    int32_t* key = inv + n;
+    int32_t* val = key + n;
+    int32_t* skey = val + n;
+    int32_t* sval = skey + n;
+    void* temp = (void*)(((uintptr_t)(sval + n) + 255) & ~(uintptr_t)255);
+    size_t temp_bytes = (size_t)(workspace_bytes - ((uint8_t*)temp - ws));
+    const int g = grid_for(n);
+    invert_perm_kernel<<<g, 256, 0, st>>>(idx, n, inv);
+    tile_keys_kernel<<<g, 256, 0, st>>>(inv, n, tile_rows, key, val);
+    int end_bit = 1;
+    while (((n - 1) / tile_rows) >> end_bit) end_bit++;
+    OGM_CUDA_TRY(cub::DeviceRadixSort::SortPairs(temp, temp_bytes, key, skey, val, sval, (int)n, 0, end_bit, st));
+    scatter_pos_kernel<<<g, 256, 0, st>>>(sval, n, pos1);
+    local_q_kernel<<<g, 256, 0, st>>>(idx, pos1, n, tile_rows, q2);
+    OGM_LAUNCH_CHECK();
+    return OGM_OK;
+}
+
+int ogm_gather_planned(int64_t rows, int64_t words, int64_t tile_rows, const int32_t* pos1, const int32_t* q2,
+                       const uint32_t* m1, const uint32_t* m2, const uint32_t* m3, const uint32_t* r_mat,
+                       uint32_t* inter, uint32_t* out, void* stream) {
+    using namespace ogm;
+    OGM_CHECK_ARG(rows >= 0 && words >= 1 && tile_rows >= 1, OGM_ERR_ARG, "bad planned-gather shape");
+    OGM_CHECK_ARG(tile_rows * words * 4 <= kTileBytes, OGM_ERR_ARG, "tile of %lld rows x %lld words exceeds %lld B",
+                  (long long)tile_rows, (long long)words, (long long)kTileBytes);
+    OGM_CHECK_ARG(m1 && inter && out, OGM_ERR_ARG, "m1, inter and out are required");
+    if (rows == 0) return OGM_OK;
+    OGM_ENSURE_INIT();
+    cudaStream_t st = as_stream(stream);
+    const int64_t ntiles = (rows + tile_rows - 1) / tile_rows;
+    int64_t g = ntiles;
+    const int64_t cap = (int64_t)sm_count() * 2;
+    if (g > cap) g = cap;
+    const bool aligned = ((((uintptr_t)m1) | ((uintptr_t)m2) | ((uintptr_t)m3) | ((uintptr_t)r_mat) |
+                           ((uintptr_t)inter) | ((uintptr_t)out)) & 15) == 0;
+    if (words == 4 && aligned) {
+        bucket_scatter4_kernel<<<grid_for(rows), 256, 0, st>>>(pos1, (const uint4*)m1, (const uint4*)m2, rows,
+                                                               (uint4*)inter);
+        tile_gather4_kernel<<<(int)g, 512, (size_t)(tile_rows * 16), st>>>(
+            q2, (const uint4*)inter, (const uint4*)r_mat, (const uint4*)m3, rows, (int)tile_rows, (uint4*)out);
+    } else {
+        bucket_scatter_kernel<<<grid_for(rows * words), 256, 0, st>>>(pos1, m1, m2, rows, words, inter);
+        tile_gather_kernel<<<(int)g, 512, (size_t)(tile_rows * words * 4), st>>>(q2, inter, r_mat, m3, rows,
+                                                                               words, tile_rows, out);
     }
     OGM_LAUNCH_CHECK();
     return OGM_OK;

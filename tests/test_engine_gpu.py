@@ -281,3 +281,27 @@ def test_sharded_sec_eval_slices_equal_unsharded(world):
             want = oracle.pack_bits(oracle.masked_parity(comps_h[q], comps_h[(q + 1) % 3], *inds_h[ps][q]))
             want = want ^ oracle.zero_share(*zk[q], counters[ps], rows)
             assert np.array_equal(host(got), want), (world, ps, q)
+
+
+@pytest.mark.parametrize("rows,width", [(1, 128), (1000, 128), (70_001, 129), (300_000, 45), (50_000, 700)])
+def test_planned_gather_equals_direct(rows, width):
+    """Two-pass planned gather == direct gather, bit for bit, incl. ragged
+    last tiles, 5-word rows and wide rows."""
+    from paper_2209_03526_b200.prf import seeded_permutation_device
+    from paper_2209_03526_b200.shuffle import GatherPlan, gather
+    from paper_2209_03526_b200.bits import words_for
+    w = words_for(width)
+    g = torch.Generator(device="cuda").manual_seed(rows)
+    mk = lambda: torch.randint(-2**31, 2**31 - 1, (rows, w), dtype=torch.int32, device="cuda", generator=g)  # noqa: E731
+    m1, m2, m3, r = mk(), mk(), mk(), mk()
+    idx = seeded_permutation_device(b"\x05" * 16, b"SHPI", 3, rows)
+    want = gather(rows, width, torch.empty_like(m1), inner=idx, m1=m1, m2=m2, m3=m3, r=r)
+    got = GatherPlan(idx, w).run(torch.empty_like(m1), m1=m1, m2=m2, m3=m3, r=r)
+    assert torch.equal(got, want)
+
+
+def test_shuffle_planned_path_matches_reference(golden, monkeypatch):
+    """The golden shuffle cases again with the planned two-pass gathers forced on."""
+    from paper_2209_03526_b200 import shuffle as shmod
+    monkeypatch.setattr(shmod, "PLAN_MIN_ROWS", 1)
+    test_shuffle_matches_reference(golden)
