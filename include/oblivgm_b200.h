@@ -193,6 +193,9 @@ int ogm_pack_fields(int64_t rows, const uint32_t* flag_bits, int nfields, const 
 int ogm_extract_field(const uint32_t* src, int64_t spitch, const int32_t* idx, int64_t n,
                       int64_t bit_offset, int64_t width, uint32_t* out, int64_t opitch, void* stream);
 
+/* src/engine.py:88-89: clear bits >= width in the last word of every row. */
+int ogm_mask_row_tails(uint32_t* mat, int64_t rows, int64_t pitch, int64_t width, void* stream);
+
 /* src/engine.py:241-245: bit r of out_bits = mat[r][0] & 1 (flag column). */
 int ogm_column_bits(const uint32_t* mat, int64_t pitch, int64_t rows, uint32_t* out_bits, void* stream);
 

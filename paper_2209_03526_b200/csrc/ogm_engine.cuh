@@ -409,6 +409,14 @@ __global__ void extract_field_kernel(const uint32_t* __restrict__ src, int64_t s
     }
 }
 
+// clean row tails after a matrix re-share (src/engine.py:88-89)
+__global__ void mask_row_tails_kernel(uint32_t* __restrict__ mat, int64_t rows, int64_t pitch, int64_t w,
+                                      uint32_t mask) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < rows; r += stride)
+        mat[r * pitch + w - 1] &= mask;
+}
+
 // bit r of out = mat[r][0] & 1 (the flag column, src/engine.py:241-245).
 __global__ void column_bit_kernel(const uint32_t* __restrict__ mat, int64_t pitch, int64_t rows,
                                   uint32_t* __restrict__ out) {
@@ -699,6 +707,16 @@ int ogm_extract_field(const uint32_t* src, int64_t spitch, const int32_t* idx, i
     if (n == 0 || opitch == 0) return OGM_OK;
     extract_field_kernel<<<grid_for(n * opitch), 256, 0, as_stream(stream)>>>(src, spitch, idx, n, bit_offset,
                                                                                width, out, opitch);
+    OGM_LAUNCH_CHECK();
+    return OGM_OK;
+}
+
+int ogm_mask_row_tails(uint32_t* mat, int64_t rows, int64_t pitch, int64_t width, void* stream) {
+    using namespace ogm;
+    OGM_CHECK_ARG(rows >= 0 && width >= 0 && pitch >= (width + 31) / 32, OGM_ERR_ARG, "bad matrix shape");
+    if (rows == 0 || (width & 31) == 0) return OGM_OK;
+    mask_row_tails_kernel<<<grid_for(rows), 256, 0, as_stream(stream)>>>(mat, rows, pitch, (width + 31) / 32,
+                                                                         (1u << (width & 31)) - 1u);
     OGM_LAUNCH_CHECK();
     return OGM_OK;
 }

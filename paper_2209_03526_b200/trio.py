@@ -1,0 +1,421 @@
+"""Trio fast path: the three co-resident servers stepped together in ONE host thread.
+
+The drop-in API (engine.py + net.run_trio) runs each party on its own thread
+exactly like the reference.  When the three logical servers share a GPU
+(BASELINE: "the three logical servers' states are simulated on the same
+devices"), every protocol step can instead be issued once for all three
+parties:
+
+* each share component lives once in HBM and is read once per step
+  (party q's view is (x_q, x_{q+1}), src/graphs.py:382-399);
+* one launch serves the three parties (``nparty=3`` kernels, zero shares
+  for all three from 3 AES streams instead of 6);
+* a re-share is a relabelling: party q's new pair is (blinded_{q-1},
+  blinded_q), so component j of the result is blinded_{j-1} -- the message
+  "sent" to the next party is the very tensor it receives;
+* one host synchronisation per public value (opened counts), nothing else.
+
+Randomness is consumed in the same order as the per-party path (zero-share
+counter per re-share, table id per shuffle, open label per open; SURVEY
+Appendix A.6), so outputs are bit-identical to ``run_trio(sec_match)`` --
+tested against the reference's recorded runs.  Each party's computation is
+unchanged; only the scheduling is fused.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import torch
+
+from . import _lib, fss
+from .bits import BitVector, words_for
+from .engine import MatchedRecord, MatchResultSet, _assemble
+from .net import make_session_configs
+from .rss import DBits, SharedBitVector
+from .shuffle import LABEL_BLIND, LABEL_RAND, _perm, blind_table, compose, gather
+
+A = _lib.ptr_array
+
+
+def _nxt(q: int) -> int:
+    return (q + 1) % 3
+
+
+@dataclass
+class TrioGroup:
+    """Candidate group with its three share components per field."""
+
+    parent_slot: int | None
+    parent_record: int | None
+    count: int
+    id_width: int
+    ids: list                     # [x1, x2, x3] (count, words)
+    attrs: dict                   # name -> [x1, x2, x3]
+    attr_widths: dict
+
+
+@dataclass
+class TrioRecords:
+    """A batch of matched records (rows of the component matrices)."""
+
+    parent_slot: int | None
+    parent_record: int | None
+    count: int
+    id_width: int
+    ids: list
+    attrs: dict
+    attr_widths: dict
+
+
+@dataclass
+class TrioResult:
+    structure: dict
+    records: list                 # per slot: list of (TrioRecords, row)
+    subgraphs: list
+    opened_flags: list = field(default_factory=list)
+
+    def party_results(self) -> list:
+        """Per-party MatchResultSet views (same layout as engine.sec_match)."""
+        out = []
+        for q in range(3):
+            recs = []
+            for slot in self.records:
+                lst = []
+                for batch, i in slot:
+                    def sv(c, width):
+                        return SharedBitVector(q + 1, DBits(c[q][i], width), DBits(c[_nxt(q)][i], width))
+                    lst.append(MatchedRecord(batch.parent_slot, batch.parent_record, sv(batch.ids, batch.id_width),
+                                             {a: sv(batch.attrs[a], batch.attr_widths[a]) for a in batch.attrs}))
+                recs.append(lst)
+            out.append(MatchResultSet(q + 1, self.structure, recs, self.subgraphs, list(self.opened_flags)))
+        return out
+
+
+class Trio:
+    """Session state of the three co-resident parties (src/net.py:221-289)."""
+
+    def __init__(self, master: bytes | None = None, configs=None, device=None):
+        configs = sorted(configs or make_session_configs(master), key=lambda c: c.party_index)
+        self.k = [c.zero_key_own for c in configs]          # k1, k2, k3
+        self.s12 = configs[0].seed_with_next
+        self.s23 = configs[1].seed_with_next
+        self.s31 = configs[2].seed_with_next
+        self.counter = 0          # zero-share counter (lockstep across parties)
+        self.table_id = 0
+        self.label = 0
+        self.opened: list = []
+        self.dev = torch.device(device or "cuda")
+
+    # -- RSS ----------------------------------------------------------------
+    def _empty(self, n: int) -> torch.Tensor:
+        return torch.empty((max(n, 1),), dtype=torch.int32, device=self.dev)[:n]
+
+    def reshare(self, adds: list, nbits: int) -> list:
+        """src/rss.py:164-176 for all parties: comp j := blinded_{j-1}."""
+        outs = [torch.empty_like(a) for a in adds]
+        if nbits:
+            _lib.call("ogm_zero_share_trio", self.k[0], self.k[1], self.k[2], self.counter, nbits, A(adds), A(outs),
+                      _lib.stream_ptr())
+        self.counter += 1
+        return [outs[2], outs[0], outs[1]]
+
+    def reshare_matrix(self, adds: list, width: int) -> list:
+        """src/engine.py:83-92 for all parties (rows*w*32-bit zero share, row tails masked)."""
+        rows, w = adds[0].shape
+        flat = [a.reshape(-1) for a in adds]
+        outs = [torch.empty_like(f) for f in flat]
+        if rows * w:
+            _lib.call("ogm_zero_share_trio", self.k[0], self.k[1], self.k[2], self.counter, rows * w * 32, A(flat),
+                      A(outs), _lib.stream_ptr())
+            if width % 32:
+                for o in outs:
+                    _lib.call("ogm_mask_row_tails", _lib.ptr(o), rows, w, width, _lib.stream_ptr())
+        self.counter += 1
+        outs = [o.reshape(rows, w) for o in outs]
+        return [outs[2], outs[0], outs[1]]
+
+    def xor(self, a: list, b: list) -> list:
+        out = []
+        for x, y in zip(a, b):
+            o = torch.empty_like(x)
+            _lib.call("ogm_xor_words", x.numel(), _lib.ptr(x), _lib.ptr(y), None, _lib.ptr(o), _lib.stream_ptr())
+            out.append(o)
+        return out
+
+    def and_gate(self, a: list, b: list, nbits: int) -> list:
+        """src/rss.py:115-126,179-181 for all parties in one launch."""
+        outs = [torch.empty_like(x) for x in a]
+        _lib.call("ogm_and_terms", a[0].numel(), 3, A(a), A([a[_nxt(q)] for q in range(3)]), A(b),
+                  A([b[_nxt(q)] for q in range(3)]), A(outs), _lib.stream_ptr())
+        return self.reshare(outs, nbits)
+
+    def open(self, comps: list, n: int) -> torch.Tensor:
+        """src/rss.py:184-206: plain = x1 ^ x2 ^ x3; every party notes it."""
+        self.label += 1
+        plain = torch.empty_like(comps[0])
+        _lib.call("ogm_xor_words", plain.numel(), _lib.ptr(comps[0]), _lib.ptr(comps[1]), _lib.ptr(comps[2]),
+                  _lib.ptr(plain), _lib.stream_ptr())
+        host = BitVector(plain, n)
+        self.opened.append((self.label, host))
+        return plain, host
+
+    # -- shuffle --------------------------------------------------------------
+    def shuffle(self, comps: list, width: int) -> list:
+        """src/shuffle.py:80-144 for the three parties: each permutation and
+        blinding table generated once; composed gathers as in ShuffleOffline."""
+        rows = comps[0].shape[0]
+        tid = self.table_id
+        self.table_id += 1
+        s12, s23, s31 = self.s12, self.s23, self.s31
+        pi12, pi23, pi31 = _perm(s12, tid, rows), _perm(s23, tid, rows), _perm(s31, tid, rows)
+        k1, k3 = compose(pi31, pi12), compose(pi23, pi31)
+
+        def tab():
+            return torch.empty((rows, words_for(width)), dtype=torch.int32, device=self.dev)
+
+        bt = (LABEL_BLIND, tid)
+        u = gather(rows, width, tab(), outer=pi31, inner=pi12, t1=(s12, *bt), t2=(s31, *bt))
+        v = gather(rows, width, tab(), inner=pi12, t1=(s12, *bt))
+        w = gather(rows, width, tab(), inner=pi23, t1=(s23, *bt), r=(s12, LABEL_RAND, tid))
+        z = gather(rows, width, tab(), outer=pi23, inner=pi31, t1=(s31, *bt), t2=(s23, *bt), r=(s31, LABEL_RAND, tid))
+        r1 = blind_table(s31, LABEL_RAND, tid, rows, width, self.dev)
+        r2 = blind_table(s12, LABEL_RAND, tid, rows, width, self.dev)
+        ab = torch.empty_like(comps[0])
+        _lib.call("ogm_xor_words", ab.numel(), _lib.ptr(comps[0]), _lib.ptr(comps[1]), None, _lib.ptr(ab),
+                  _lib.stream_ptr())
+        x1 = gather(rows, width, tab(), inner=k1, m1=ab, r=u)               # P1
+        y1 = gather(rows, width, tab(), inner=pi12, m1=comps[2], r=v)      # P2
+        c1 = gather(rows, width, tab(), inner=pi23, m1=x1, r=w)            # P2
+        r3 = gather(rows, width, tab(), inner=k3, m1=y1, m3=c1, r=z)       # P3
+        return [r1, r2, r3]
+
+    # -- engine steps -----------------------------------------------------------
+    def _fde(self, keys: list, domain: int) -> torch.Tensor:
+        return fss.full_domain(fss.KeyBatch.from_keys(keys, self.dev), domain)
+
+    def sec_eval(self, group: TrioGroup, key_pairs: list, attr: str, domain: int, cache: dict) -> list:
+        """src/engine.py:139-165 for all parties; both passes from one read."""
+        parts = [list(zip(fss.key_parts_for_engine(f), fss.key_parts_for_engine(s))) for f, s in key_pairs]
+        npass = len(parts[0])
+        comps = group.attrs[attr]
+        inds = []
+        for ps in range(npass):
+            ck = (id(key_pairs[0][0]), ps)
+            if ck not in cache:
+                keys = [k for q in range(3) for k in parts[q][ps]]
+                by_kind: dict = {}
+                for i, k in enumerate(keys):
+                    by_kind.setdefault(fss.is_comparison(k), []).append(i)
+                rows = [None] * 6
+                for idxs in by_kind.values():
+                    fd = self._fde([keys[i] for i in idxs], domain)
+                    for j, i in enumerate(idxs):
+                        rows[i] = fd[j]
+                cache[ck] = rows
+            inds.append(cache[ck])
+        rows = group.count
+        words = comps[0].shape[1]
+        outs = [self._empty(words_for(rows)) for _ in range(3 * npass)]
+        flat = [t for ps in range(npass) for t in inds[ps]]
+        _lib.call("ogm_masked_parity", rows, words, comps[0].stride(0), 3, A(comps), 3, _lib.int_array([0, 1, 2]),
+                  _lib.int_array([1, 2, 0]), npass, A(flat), A(outs), _lib.stream_ptr())
+        result = None
+        for ps in range(npass):
+            sh = self.reshare(outs[3 * ps:3 * ps + 3], rows)
+            result = sh if result is None else self.xor(result, sh)
+        return result
+
+    def combine(self, bits: list, combiner: str, any_mode: str, n: int) -> list:
+        """src/engine.py:168-189."""
+        if not bits:
+            raise ValueError("no predicate bits to combine")
+        acc = bits[0]
+        if combiner == "ALL":
+            for nxt in bits[1:]:
+                acc = self.and_gate(acc, nxt, n)
+            return acc
+        if combiner != "ANY":
+            raise ValueError(f"unknown combiner {combiner!r}")
+        if any_mode == "xor":
+            for nxt in bits[1:]:
+                acc = self.xor(acc, nxt)
+            return acc
+        if any_mode != "or":
+            raise ValueError(f"unknown ANY mode {any_mode!r}")
+        for nxt in bits[1:]:
+            conj = self.and_gate(acc, nxt, n)
+            acc = self.xor(self.xor(acc, nxt), conj)
+        return acc
+
+    def _fold(self, flags: list, mats: list, width: int) -> list:
+        rows = mats[0].shape[0]
+        flat = [m.reshape(rows, -1) if m.dim() != 2 else m for m in mats]
+        words = flat[0].shape[1]
+        outs = [self._empty(words) for _ in range(3)]
+        _lib.call("ogm_select_fold", rows, words, flat[0].stride(0) if rows else words, 3, A(flat),
+                  A([flat[_nxt(q)] for q in range(3)]), A(flags), A([flags[_nxt(q)] for q in range(3)]), A(outs),
+                  _lib.stream_ptr())
+        return outs
+
+    def fetch_unique(self, group: TrioGroup, flags: list) -> TrioRecords:
+        """src/engine.py:197-217."""
+        ids = self.reshare(self._fold(flags, group.ids, group.id_width), group.id_width)
+        attrs = {}
+        for name in sorted(group.attrs):
+            attrs[name] = self.reshare(self._fold(flags, group.attrs[name], group.attr_widths[name]),
+                                       group.attr_widths[name])
+        return TrioRecords(group.parent_slot, group.parent_record, 1, group.id_width, [c[None] for c in ids],
+                           {a: [c[None] for c in v] for a, v in attrs.items()}, dict(group.attr_widths))
+
+    def _pack(self, flag_bits, fields, rows, width) -> torch.Tensor:
+        out = torch.empty((rows, words_for(width)), dtype=torch.int32, device=self.dev)
+        mats = [f for f, _ in fields]
+        _lib.call("ogm_pack_fields", rows, _lib.ptr(flag_bits), len(fields), A(mats),
+                  _lib.i64_array([m.stride(0) if rows else words_for(wd) for m, wd in fields]),
+                  _lib.i64_array([wd for _, wd in fields]), _lib.ptr(out), out.shape[1], _lib.stream_ptr())
+        return out
+
+    def _column(self, mat) -> torch.Tensor:
+        rows = mat.shape[0]
+        out = self._empty(words_for(rows))
+        _lib.call("ogm_column_bits", _lib.ptr(mat), mat.shape[1], rows, _lib.ptr(out), _lib.stream_ptr())
+        return out
+
+    def _open_keep(self, shuffled: list, rows: int, phase: str, audit: list):
+        plain, host = self.open([self._column(m) for m in shuffled], rows)
+        audit.append((phase, host.to_bits().copy()))
+        idx = torch.empty((max(rows, 1),), dtype=torch.int32, device=self.dev)
+        cnt = torch.zeros((1,), dtype=torch.int64, device=self.dev)
+        nb = int(_lib.load().ogm_compact_workspace_bytes(rows))
+        ws = torch.empty((nb,), dtype=torch.uint8, device=self.dev)
+        _lib.call("ogm_compact_bits", rows, _lib.ptr(plain), _lib.ptr(idx), _lib.ptr(cnt), _lib.ptr(ws), nb,
+                  _lib.stream_ptr())
+        k = int(host.popcount())  # the opened mask is public and already on the host
+        return idx[:k], k
+
+    def _extract(self, src, idx, n, off, width):
+        out = torch.empty((n, words_for(width)), dtype=torch.int32, device=self.dev)
+        if n:
+            _lib.call("ogm_extract_field", _lib.ptr(src), src.shape[1], _lib.ptr(idx), n, off, width, _lib.ptr(out),
+                      out.shape[1], _lib.stream_ptr())
+        return out
+
+    def fetch_multi(self, group: TrioGroup, flags: list, audit: list) -> TrioRecords:
+        """src/engine.py:220-270."""
+        names = sorted(group.attrs)
+        widths = [group.attr_widths[a] for a in names]
+        row_width = 1 + group.id_width + sum(widths)
+        rows = [self._pack(flags[j], [(group.ids[j], group.id_width)] +
+                           [(group.attrs[a][j], w) for a, w in zip(names, widths)], group.count, row_width)
+                for j in range(3)]
+        sh = self.shuffle(rows, row_width)
+        keep, k = self._open_keep(sh, group.count, "fetch", audit)
+        ids = [self._extract(m, keep, k, 1, group.id_width) for m in sh]
+        attrs, off = {}, 1 + group.id_width
+        for a, w in zip(names, widths):
+            attrs[a] = [self._extract(m, keep, k, off, w) for m in sh]
+            off += w
+        return TrioRecords(group.parent_slot, group.parent_record, k, group.id_width, ids, attrs,
+                           dict(zip(names, widths)))
+
+    def _parity_rows(self, mat, w) -> torch.Tensor:
+        rows = mat.shape[0]
+        out = self._empty(words_for(rows))
+        ones = torch.full((w,), -1, dtype=torch.int32, device=self.dev)
+        zeros = torch.zeros((w,), dtype=torch.int32, device=self.dev)
+        _lib.call("ogm_masked_parity", rows, w, mat.stride(0), 2, A([mat, mat]), 1, _lib.int_array([0]),
+                  _lib.int_array([1]), 1, A([ones, zeros]), A([out]), _lib.stream_ptr())
+        return out
+
+    def access(self, rec: TrioRecords, i: int, parent_type: str, child_type: str, needed: list, gshares: list,
+               provenance: tuple, audit: list) -> TrioGroup:
+        """src/engine.py:278-344."""
+        schema = gshares[0].schema
+        parent_slot, parent_rec = provenance
+        x_ne = schema.types[child_type].population
+        w_ne = words_for(x_ne)
+        widths = {a: schema.types[child_type].attrs[a].domain_size for a in needed}
+        lists = [gs.types[parent_type].posting[child_type][0] for gs in gshares]
+        l_max = lists[0].shape[1]
+
+        def empty():
+            z = lambda w: torch.zeros((0, w), dtype=torch.int32, device=self.dev)  # noqa: E731
+            return TrioGroup(parent_slot, parent_rec, 0, x_ne, [z(w_ne)] * 3,
+                             {a: [z(words_for(widths[a]))] * 3 for a in needed}, widths)
+
+        if l_max == 0:
+            return empty()
+        sel = [c[i] for c in rec.ids]
+        adds = [a.reshape(l_max, w_ne) for a in self._fold(sel, lists, x_ne)]
+        fetched = self.reshare_matrix(adds, x_ne)
+        rows = [self._pack(self._parity_rows(f, w_ne), [(f, x_ne)], l_max, 1 + x_ne) for f in fetched]
+        sh = self.shuffle(rows, 1 + x_ne)
+        keep, k = self._open_keep(sh, l_max, "access", audit)
+        if k == 0:
+            return empty()
+        ids = [self._extract(m, keep, k, 1, x_ne) for m in sh]
+        attrs = {}
+        for a in needed:
+            va = [gs.types[child_type].attrs[a][0] for gs in gshares]
+            n = widths[a]
+            adds = []
+            for q in range(3):
+                x, w = va[q].shape
+                out = torch.empty((k, w), dtype=torch.int32, device=self.dev)
+                ws = torch.empty((2 * max(x, 1),), dtype=torch.int32, device=self.dev)
+                _lib.call("ogm_select_many", k, x, w, va[q].stride(0), _lib.ptr(ids[q]), _lib.ptr(ids[_nxt(q)]),
+                          ids[q].stride(0), _lib.ptr(va[q]), _lib.ptr(va[_nxt(q)]), _lib.ptr(out), w, _lib.ptr(ws),
+                          _lib.stream_ptr())
+                adds.append(out)
+            attrs[a] = self.reshare_matrix(adds, n)
+        return TrioGroup(parent_slot, parent_rec, k, x_ne, ids, attrs, widths)
+
+    # -- full query ----------------------------------------------------------
+    def match(self, tokens: list, gshares: list, any_mode: str = "or") -> TrioResult:
+        """src/engine.py:352-417 for the three parties at once.  gshares are the
+        three per-party device shares from graphs.device_trio (component j is
+        party j's share_a)."""
+        schema = gshares[0].schema
+        for t in tokens:
+            if t.schema_digest != schema.digest():
+                raise ValueError("token and graph share were built for different schemas")
+        slots = tokens[0].structure["slots"]
+        audit: list = []
+        groups: list = [[] for _ in slots]
+        records: list = [[] for _ in slots]
+        cache: dict = {}
+        for s, slot in enumerate(slots):
+            vtype = slot["type"]
+            ts = schema.types[vtype]
+            needed = sorted({p["attr"] for p in slot["preds"]})
+            if s == 0:
+                tps = [gs.types[vtype] for gs in gshares]
+                groups[0] = [TrioGroup(None, None, ts.population, ts.population, [t.id_a for t in tps],
+                                       {a: [t.attrs[a][0] for t in tps] for a in needed},
+                                       {a: ts.attrs[a].domain_size for a in needed})]
+            unique_route = (len(slot["preds"]) == 1 and slot["preds"][0]["kind"] == fss.KIND_EQ
+                            and ts.attrs[slot["preds"][0]["attr"]].unique)
+            for group in groups[s]:
+                if group.count == 0:
+                    continue
+                bits = [self.sec_eval(group, [tok.slot_keys[s][pi] for tok in tokens], pred["attr"],
+                                      ts.attrs[pred["attr"]].domain_size, cache)
+                        for pi, pred in enumerate(slot["preds"])]
+                flags = self.combine(bits, slot["combiner"], any_mode, group.count)
+                batch = self.fetch_unique(group, flags) if unique_route else self.fetch_multi(group, flags, audit)
+                records[s].extend((batch, i) for i in range(batch.count))
+            for child in slot["children"]:
+                ctype = slots[child]["type"]
+                cattrs = sorted({p["attr"] for p in slots[child]["preds"]})
+                groups[child] = [self.access(b, i, vtype, ctype, cattrs, gshares, (s, ri), audit)
+                                 for ri, (b, i) in enumerate(records[s])]
+        views = [[_RecView(b.parent_slot, b.parent_record) for b, _ in recs] for recs in records]
+        subgraphs = _assemble(slots, views)
+        return TrioResult(tokens[0].structure, records, subgraphs, audit)
+
+
+@dataclass
+class _RecView:
+    parent_slot: int | None
+    parent_record: int | None

@@ -305,3 +305,34 @@ def test_shuffle_planned_path_matches_reference(golden, monkeypatch):
     from paper_2209_03526_b200 import shuffle as shmod
     monkeypatch.setattr(shmod, "PLAN_MIN_ROWS", 1)
     test_shuffle_matches_reference(golden)
+
+
+@pytest.mark.parametrize("name", ["campus", "unique-chain", "conj", "rand0", "rand1", "rand2"])
+def test_trio_fast_path_matches_reference(golden, name):
+    """The single-thread trio path (one launch per step for all three parties)
+    reproduces the reference's record shares, opened flags and subgraphs."""
+    from paper_2209_03526_b200.trio import Trio
+    g = golden("match")
+    rec = json.loads(str(g[f"{name}_json"]))
+    graph = parse_graph_text(rec["graph"])
+    rng = np.random.default_rng(rec["seed"])
+    schema, shares = encrypt_graph(graph, rec["k"], rng)
+    query = load_query(rec["query"], schema)
+    tokens = gen_token(query, schema, rng)
+    dshares = device_trio(shares)
+    res = Trio(bytes.fromhex(rec["master"])).match(list(tokens), list(dshares), any_mode=rec["mode"])
+    results = res.party_results()
+    matches, _ = open_results(results[:2], schema)
+    assert sorted(list(m) for m in set(matches)) == rec["matches"]
+    assert [list(sg) for sg in res.subgraphs] == rec["subgraphs"]
+    for p, r in enumerate(results):
+        for s, recs in enumerate(r.records):
+            for ri, mr in enumerate(recs):
+                base = f"{name}_p{p}_s{s}_r{ri}"
+                assert np.array_equal(host(mr.vertex_id.share_a.words), g[f"{base}_id_a"]), base
+                assert np.array_equal(host(mr.vertex_id.share_b.words), g[f"{base}_id_b"]), base
+                for a in sorted(mr.attrs):
+                    assert np.array_equal(host(mr.attrs[a].share_a.words), g[f"{base}_{a}_a"]), base
+                    assert np.array_equal(host(mr.attrs[a].share_b.words), g[f"{base}_{a}_b"]), base
+        for j, (_phase, bits) in enumerate(r.opened_flags):
+            assert np.array_equal(bits, g[f"{name}_p{p}_open{j}"])
