@@ -151,7 +151,7 @@ def cpu_eval_rate(kind: str, target_seconds: float, threads: int):
     t = time.perf_counter()
     oracle.eval_points(k0, pts, nthreads=threads)
     rate = 4096 / max(time.perf_counter() - t, 1e-6)
-    n = int(min(max(rate * target_seconds, 4096), 1 << 22)) // 32 * 32
+    n = int(min(max(rate * target_seconds, 4096), DEFAULT_KEYS)) // 32 * 32
     k0, pts = cpu_keys(kind, n, 2)
     t = time.perf_counter()
     oracle.eval_points(k0, pts, nthreads=threads)

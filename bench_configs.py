@@ -297,6 +297,91 @@ def run_c5(args):
 
 
 # ---------------------------------------------------------------------------
+# C3 root-slot pipeline (trio fast path): secEval x2 -> combine -> Case II fetch
+# ---------------------------------------------------------------------------
+
+
+def run_c3_pipeline(args):
+    """Root slot of the medium graph: 200K centre vertices, one-hot ids (200K
+    bits) and two needed attributes (uniform a0, n=182,083; Zipf a2, n=8,969).
+    Predicates: a0 in [lo, hi] (interval, 2 passes) AND a2 = rare value (DPF);
+    combine (1 AND); Case II fetch: shuffle of 200K rows x 391,053 bits (48.9 KB
+    per row, 9.8 GB per component -- SURVEY 8(d) C3 'feasible' row), open the
+    flags, keep the matches.  Blinds on the fly (memory-lean)."""
+    from paper_2209_03526_b200.trio import Trio, TrioGroup
+
+    X = args.rows
+    dev = torch.device("cuda")
+    rng = np.random.default_rng(args.seed)
+    n0, n2 = 182083, 8969
+    v0 = torch.from_numpy(rng.integers(0, n0, size=X).astype(np.int32)).to(dev)
+    ranks = np.arange(1, n2 + 1)
+    pz = 1.0 / ranks ** 1.1
+    v2h = rng.choice(n2, size=X, p=pz / pz.sum()).astype(np.int32)
+    v2 = torch.from_numpy(v2h).to(dev)
+    ids = workloads.shared_one_hot(torch.arange(X, dtype=torch.int32, device=dev), X, args.seed, 60)
+    a0 = workloads.shared_one_hot(v0, n0, args.seed, 70)
+    a2 = workloads.shared_one_hot(v2, n2, args.seed, 80)
+    torch.cuda.synchronize()
+    lo = int(rng.integers(0, n0 // 2))
+    hi = lo + n0 // 10
+    v0h = v0.cpu().numpy()
+    inside = (v0h >= lo) & (v0h <= hi)
+    cnt_all = np.bincount(v2h, minlength=n2)
+    cnt_in = np.bincount(v2h[inside], minlength=n2)
+    cand = np.nonzero((cnt_in >= 1) & (cnt_all <= 6))[0]  # a rare Zipf value with matches in range
+    rare = int(cand[0])
+    want = int(((v2h == rare) & inside).sum())
+    krng = np.random.default_rng(args.seed + 5)
+    iv = [fss.ic_gen(lo, hi, n0, krng) for _ in range(3)]
+    eq = list(fss.bundle_gen("eq", (rare,), n2, krng).pairs)
+
+    def split(pairs):
+        (k11, k21), (k12, k22), (k13, k23) = pairs
+        return [(k11, k12), (k22, k13), (k23, k21)]
+
+    kiv, keq = split(iv), split(eq)
+    group = TrioGroup(None, None, X, X, list(ids), {"a0": list(a0), "a2": list(a2)}, {"a0": n0, "a2": n2})
+    phases = {}
+    lat = []
+    for it in range(args.warmup + args.steps):
+        trio = Trio(b"\x35" * 16)
+        audit: list = []
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        b_iv = trio.sec_eval(group, kiv, "a0", n0, {})
+        b_eq = trio.sec_eval(group, keq, "a2", n2, {})
+        torch.cuda.synchronize()
+        t1 = time.perf_counter()
+        flags = trio.combine([b_iv, b_eq], "ALL", "or", X)
+        torch.cuda.synchronize()
+        t2 = time.perf_counter()
+        # offline phase of the fetch's shuffle (data-independent), timed apart
+        trio.prepare_shuffle(X, 1 + X + n0 + n2)
+        torch.cuda.synchronize()
+        t_off = time.perf_counter()
+        recs = trio.fetch_multi(group, flags, audit)
+        torch.cuda.synchronize()
+        t3 = time.perf_counter()
+        if it >= args.warmup:
+            lat.append((t3 - t_off) + (t2 - t0))
+            for k, v in (("secEval_ms", t1 - t0), ("combine_ms", t2 - t1), ("fetch_online_ms", t3 - t_off),
+                         ("fetch_offline_prep_ms", t_off - t2)):
+                phases.setdefault(k, []).append(1e3 * v)
+        recs_count = recs.count
+        del recs, flags, b_iv, b_eq
+        torch.cuda.empty_cache()
+    row_width = 1 + X + n0 + n2
+    emit({"config": f"C3 root-slot pipeline: {X} candidates, a0 interval + a2 eq, ALL, Case II fetch of "
+                    f"{row_width}-bit rows", "metric": "root_slot_latency_ms", "value": 1e3 * statistics.median(lat),
+          "unit": "ms", "higher_is_better": False, "phases_ms": {k: statistics.median(v) for k, v in phases.items()},
+          "matches_expected": want, "opened_ones": int(audit[0][1].sum()) if audit else None,
+          "fetch_table_GB_per_component": X * words_for(row_width) * 4 / 1e9,
+          "kept_records": int(recs_count), "path": "trio fast path; latency = online (shuffle material prepared "
+          "offline, reported separately)"})
+
+
+# ---------------------------------------------------------------------------
 # C4: large graph, root-slot secEval on the Zipf attribute, rows sharded
 # across ranks (torchrun, one process per GPU; NCCL all-gather of match bits)
 # ---------------------------------------------------------------------------
@@ -366,7 +451,7 @@ def run_c4(args):
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("which", choices=["c1", "c3", "c4", "c5", "all"])
+    ap.add_argument("which", choices=["c1", "c3", "c3p", "c4", "c5", "all"])
     ap.add_argument("--c4-rows", type=int, default=2_000_000)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
@@ -385,6 +470,8 @@ def main():
         run_c5(args)
     if args.which == "c4":
         run_c4(args)
+    if args.which == "c3p":
+        run_c3_pipeline(args)
 
 
 if __name__ == "__main__":

@@ -364,12 +364,27 @@ __device__ __forceinline__ uint32_t field_bits32(const uint32_t* row, int64_t wi
     return sh ? __funnelshift_r(lo, hi, sh) : lo;
 }
 
+__device__ __forceinline__ uint32_t pack_word(const PackArgs& a, int64_t r, int64_t k, int64_t ow);
+
+// wide rows: one CTA per row (grid-stride over rows), threads over words
+__global__ void pack_fields_rows_kernel(const PackArgs a) {
+    const int64_t ow = (a.owidth + 31) >> 5;
+    for (int64_t r = blockIdx.x; r < a.rows; r += gridDim.x)
+        for (int64_t k = threadIdx.x; k < a.opitch; k += blockDim.x) a.out[r * a.opitch + k] = pack_word(a, r, k, ow);
+}
+
 __global__ void pack_fields_kernel(const PackArgs a) {
     const int64_t total = a.rows * a.opitch;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     const int64_t ow = (a.owidth + 31) >> 5;
     for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += stride) {
         const int64_t r = t / a.opitch, k = t % a.opitch;
+        a.out[r * a.opitch + k] = pack_word(a, r, k, ow);
+    }
+}
+
+__device__ __forceinline__ uint32_t pack_word(const PackArgs& a, int64_t r, int64_t k, int64_t ow) {
+    {
         uint32_t v = 0;
         if (k < ow) {
             const int64_t lo = k * 32;
@@ -385,7 +400,7 @@ __global__ void pack_fields_kernel(const PackArgs a) {
                 v |= bits & m;
             }
         }
-        a.out[r * a.opitch + k] = v;
+        return v;
     }
 }
 
@@ -415,6 +430,24 @@ __global__ void mask_row_tails_kernel(uint32_t* __restrict__ mat, int64_t rows, 
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < rows; r += stride)
         mat[r * pitch + w - 1] &= mask;
+}
+
+__global__ void extract_field_rows_kernel(const uint32_t* __restrict__ src, int64_t spitch,
+                                          const int32_t* __restrict__ idx, int64_t n, int64_t off, int64_t width,
+                                          uint32_t* __restrict__ out, int64_t opitch) {
+    const int64_t ow = (width + 31) >> 5;
+    const int64_t sw = (off + width + 31) >> 5;
+    for (int64_t k = blockIdx.x; k < n; k += gridDim.x) {
+        const int64_t r = idx ? idx[k] : k;
+        for (int64_t j = threadIdx.x; j < opitch; j += blockDim.x) {
+            uint32_t v = 0;
+            if (j < ow) {
+                v = field_bits32(src + r * spitch, sw * 32, off + j * 32);
+                if (j == ow - 1 && (width & 31)) v &= (1u << (width & 31)) - 1u;
+            }
+            out[k * opitch + j] = v;
+        }
+    }
 }
 
 // bit r of out = mat[r][0] & 1 (the flag column, src/engine.py:241-245).
@@ -694,7 +727,12 @@ int ogm_pack_fields(int64_t rows, const uint32_t* flag_bits, int nfields, const 
     a.opitch = opitch;
     a.owidth = off;
     a.rows = rows;
-    pack_fields_kernel<<<grid_for(rows * opitch), 256, 0, as_stream(stream)>>>(a);
+    if (opitch >= 256) {
+        int64_t g = rows < (int64_t)sm_count() * 8 ? rows : (int64_t)sm_count() * 8;
+        pack_fields_rows_kernel<<<(int)g, 256, 0, as_stream(stream)>>>(a);
+    } else {
+        pack_fields_kernel<<<grid_for(rows * opitch), 256, 0, as_stream(stream)>>>(a);
+    }
     OGM_LAUNCH_CHECK();
     return OGM_OK;
 }
@@ -705,8 +743,14 @@ int ogm_extract_field(const uint32_t* src, int64_t spitch, const int32_t* idx, i
     OGM_CHECK_ARG(n >= 0 && width >= 0 && bit_offset >= 0, OGM_ERR_ARG, "bad extract arguments");
     OGM_CHECK_ARG(opitch >= (width + 31) / 32, OGM_ERR_ARG, "output pitch too small");
     if (n == 0 || opitch == 0) return OGM_OK;
-    extract_field_kernel<<<grid_for(n * opitch), 256, 0, as_stream(stream)>>>(src, spitch, idx, n, bit_offset,
-                                                                               width, out, opitch);
+    if (opitch >= 256) {
+        int64_t g = n < (int64_t)sm_count() * 8 ? n : (int64_t)sm_count() * 8;
+        extract_field_rows_kernel<<<(int)g, 256, 0, as_stream(stream)>>>(src, spitch, idx, n, bit_offset, width, out,
+                                                                          opitch);
+    } else {
+        extract_field_kernel<<<grid_for(n * opitch), 256, 0, as_stream(stream)>>>(src, spitch, idx, n, bit_offset,
+                                                                                   width, out, opitch);
+    }
     OGM_LAUNCH_CHECK();
     return OGM_OK;
 }

@@ -147,6 +147,51 @@ __device__ __forceinline__ void prf_row_chunk(const AesTab& T, const GatherTerm&
 }
 
 template <bool ONLINE>
+__device__ __forceinline__ void gather_chunk(const AesTab& T, const GatherArgs& a, int64_t i, int64_t c,
+                                             uint32_t tail) {
+    const int nw = (int)min((int64_t)4, a.W - 4 * c);
+    const int64_t k2 = a.P2 ? (int64_t)__ldg(a.P2 + i) : i;
+    const int64_t k1 = a.P1 ? (int64_t)__ldg(a.P1 + k2) : k2;
+    uint32_t acc[4] = {0, 0, 0, 0};
+    const GatherTerm* terms[3] = {&a.t1, &a.t2, &a.r};
+    const int64_t trow[3] = {k1, k2, i};
+#pragma unroll
+    for (int q = 0; q < 3; q++) {
+        const GatherTerm& g = *terms[q];
+        if (g.on == 0) continue;
+        uint32_t v[4] = {0, 0, 0, 0};
+        if (ONLINE && g.on == 1) {
+            prf_row_chunk(T, g, trow[q], a.W, c, nw, v);
+            if (4 * c + nw == a.W) v[nw - 1] &= tail;
+        } else {
+            const uint32_t* src = g.mat + trow[q] * a.W + 4 * c;
+            for (int j = 0; j < nw; j++) v[j] = src[j];
+        }
+#pragma unroll
+        for (int j = 0; j < 4; j++) acc[j] ^= v[j];
+    }
+    const uint32_t* m1 = a.M1 ? a.M1 + k1 * a.W + 4 * c : nullptr;
+    const uint32_t* m2 = a.M2 ? a.M2 + k1 * a.W + 4 * c : nullptr;
+    const uint32_t* m3 = a.M3 ? a.M3 + i * a.W + 4 * c : nullptr;
+    uint32_t* o = a.out + i * a.W + 4 * c;
+    if (nw == 4 && ((a.W & 3) == 0)) {
+        uint4 x = make_uint4(acc[0], acc[1], acc[2], acc[3]);
+        if (m1) x = xor4(x, *reinterpret_cast<const uint4*>(m1));
+        if (m2) x = xor4(x, *reinterpret_cast<const uint4*>(m2));
+        if (m3) x = xor4(x, *reinterpret_cast<const uint4*>(m3));
+        *reinterpret_cast<uint4*>(o) = x;
+    } else {
+        for (int j = 0; j < nw; j++) {
+            uint32_t x = acc[j];
+            if (m1) x ^= m1[j];
+            if (m2) x ^= m2[j];
+            if (m3) x ^= m3[j];
+            o[j] = x;
+        }
+    }
+}
+
+template <bool ONLINE>
 __global__ void __launch_bounds__(kAesThreads) shuffle_gather_kernel(const GatherArgs a) {
     extern __shared__ __align__(128) uint8_t smem_raw[];
     if (ONLINE) {
@@ -155,50 +200,17 @@ __global__ void __launch_bounds__(kAesThreads) shuffle_gather_kernel(const Gathe
     }
     const AesTab T(smem_raw);
     const int64_t nch = (a.W + 3) >> 2;
-    const int64_t total = a.rows * nch;
-    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     const uint32_t tail = (a.width & 31) ? ((1u << (a.width & 31)) - 1u) : 0xffffffffu;
-    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += stride) {
-        const int64_t i = t / nch, c = t % nch;
-        const int nw = (int)min((int64_t)4, a.W - 4 * c);
-        const int64_t k2 = a.P2 ? (int64_t)__ldg(a.P2 + i) : i;
-        const int64_t k1 = a.P1 ? (int64_t)__ldg(a.P1 + k2) : k2;
-        uint32_t acc[4] = {0, 0, 0, 0};
-        const GatherTerm* terms[3] = {&a.t1, &a.t2, &a.r};
-        const int64_t trow[3] = {k1, k2, i};
-#pragma unroll
-        for (int q = 0; q < 3; q++) {
-            const GatherTerm& g = *terms[q];
-            if (g.on == 0) continue;
-            uint32_t v[4] = {0, 0, 0, 0};
-            if (ONLINE && g.on == 1) {
-                prf_row_chunk(T, g, trow[q], a.W, c, nw, v);
-                if (4 * c + nw == a.W) v[nw - 1] &= tail;
-            } else {
-                const uint32_t* src = g.mat + trow[q] * a.W + 4 * c;
-                for (int j = 0; j < nw; j++) v[j] = src[j];
-            }
-#pragma unroll
-            for (int j = 0; j < 4; j++) acc[j] ^= v[j];
-        }
-        const uint32_t* m1 = a.M1 ? a.M1 + k1 * a.W + 4 * c : nullptr;
-        const uint32_t* m2 = a.M2 ? a.M2 + k1 * a.W + 4 * c : nullptr;
-        const uint32_t* m3 = a.M3 ? a.M3 + i * a.W + 4 * c : nullptr;
-        uint32_t* o = a.out + i * a.W + 4 * c;
-        if (nw == 4 && ((a.W & 3) == 0)) {
-            uint4 x = make_uint4(acc[0], acc[1], acc[2], acc[3]);
-            if (m1) x = xor4(x, *reinterpret_cast<const uint4*>(m1));
-            if (m2) x = xor4(x, *reinterpret_cast<const uint4*>(m2));
-            if (m3) x = xor4(x, *reinterpret_cast<const uint4*>(m3));
-            *reinterpret_cast<uint4*>(o) = x;
-        } else {
-            for (int j = 0; j < nw; j++) {
-                uint32_t x = acc[j];
-                if (m1) x ^= m1[j];
-                if (m2) x ^= m2[j];
-                if (m3) x ^= m3[j];
-                o[j] = x;
-            }
+    if (nch >= 64) {
+        // wide rows: a CTA walks rows, its threads walk the row's 4-word chunks
+        for (int64_t i = blockIdx.x; i < a.rows; i += gridDim.x)
+            for (int64_t c = threadIdx.x; c < nch; c += blockDim.x) gather_chunk<ONLINE>(T, a, i, c, tail);
+    } else {
+        const int64_t total = a.rows * nch;
+        const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+        for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += stride) {
+            const int64_t i = t / nch;
+            gather_chunk<ONLINE>(T, a, i, t - i * nch, tail);
         }
     }
 }
@@ -211,7 +223,6 @@ __global__ void perm_compose_kernel(const int32_t* __restrict__ outer, const int
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
         out[i] = __ldg(inner + __ldg(outer + i));
 }
-
 
 // ---------------------------------------------------------------------------
 // Planned two-pass gather for a permutation known ahead of the data.

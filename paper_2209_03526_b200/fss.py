@@ -231,7 +231,9 @@ def full_domain(batch: KeyBatch, n: int, out: torch.Tensor | None = None) -> tor
         raise DomainError(f"requested {n} points from a 2^{batch.bits} domain")
     w = words_for(n)
     if out is None:
-        out = torch.empty((batch.count, w), dtype=torch.int32, device=batch.root.device)
+        # 16-byte row pitch so every key's indicator row feeds 128-bit loads
+        pitch = (w + 3) // 4 * 4
+        out = torch.empty((batch.count, pitch), dtype=torch.int32, device=batch.root.device)[:, :w]
     _lib.call("ogm_fss_full_domain", batch.kind, batch.bits, batch.count, _lib.ptr(batch.root),
               _lib.ptr(batch.seed_cw), _lib.ptr(batch.ctrl), _lib.ptr(batch.flags), n, _lib.ptr(out),
               out.stride(0), _lib.stream_ptr())

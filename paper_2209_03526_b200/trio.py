@@ -161,20 +161,67 @@ class Trio:
         return plain, host
 
     # -- shuffle --------------------------------------------------------------
-    def shuffle(self, comps: list, width: int) -> list:
-        """src/shuffle.py:80-144 for the three parties: each permutation and
-        blinding table generated once; composed gathers as in ShuffleOffline."""
-        rows = comps[0].shape[0]
+    def prepare_shuffle(self, rows: int, width: int) -> None:
+        """Offline phase for the NEXT shuffle (table id self.table_id): the
+        data-independent permutations, their compositions and the permuted,
+        combined blinding tables (see shuffle.ShuffleOffline)."""
         tid = self.table_id
-        self.table_id += 1
         s12, s23, s31 = self.s12, self.s23, self.s31
         pi12, pi23, pi31 = _perm(s12, tid, rows), _perm(s23, tid, rows), _perm(s31, tid, rows)
-        k1, k3 = compose(pi31, pi12), compose(pi23, pi31)
 
         def tab():
             return torch.empty((rows, words_for(width)), dtype=torch.int32, device=self.dev)
 
         bt = (LABEL_BLIND, tid)
+        m = {"pi12": pi12, "pi23": pi23, "k1": compose(pi31, pi12), "k3": compose(pi23, pi31),
+             "u": gather(rows, width, tab(), outer=pi31, inner=pi12, t1=(s12, *bt), t2=(s31, *bt)),
+             "v": gather(rows, width, tab(), inner=pi12, t1=(s12, *bt)),
+             "w": gather(rows, width, tab(), inner=pi23, t1=(s23, *bt), r=(s12, LABEL_RAND, tid)),
+             "z": gather(rows, width, tab(), outer=pi23, inner=pi31, t1=(s31, *bt), t2=(s23, *bt),
+                         r=(s31, LABEL_RAND, tid)),
+             "r1": blind_table(s31, LABEL_RAND, tid, rows, width, self.dev),
+             "r2": blind_table(s12, LABEL_RAND, tid, rows, width, self.dev)}
+        if not hasattr(self, "_prepared"):
+            self._prepared = {}
+        self._prepared[(tid, rows, width)] = m
+
+    def shuffle(self, comps: list, width: int, online_blinds: bool | None = None) -> list:
+        """src/shuffle.py:80-144 for the three parties: each permutation and
+        blinding table generated once; composed gathers as in ShuffleOffline.
+        ``online_blinds`` generates the blinding tables inside the gathers
+        (AES-CTR on the fly) instead of materialising them -- the memory-lean
+        mode for wide rows (default: on for tables above 4 GiB)."""
+        rows = comps[0].shape[0]
+        tid = self.table_id
+        self.table_id += 1
+        prep = getattr(self, "_prepared", {}).pop((tid, rows, width), None)
+        if prep is not None:
+            return self._shuffle_online(comps, width, prep)
+        s12, s23, s31 = self.s12, self.s23, self.s31
+        pi12, pi23, pi31 = _perm(s12, tid, rows), _perm(s23, tid, rows), _perm(s31, tid, rows)
+
+        def tab():
+            return torch.empty((rows, words_for(width)), dtype=torch.int32, device=self.dev)
+
+        bt = (LABEL_BLIND, tid)
+        if online_blinds is None:
+            online_blinds = rows * words_for(width) * 4 > (4 << 30)
+        if online_blinds:
+            ab = torch.empty_like(comps[0])
+            _lib.call("ogm_xor_words", ab.numel(), _lib.ptr(comps[0]), _lib.ptr(comps[1]), None, _lib.ptr(ab),
+                      _lib.stream_ptr())
+            x1 = gather(rows, width, tab(), outer=pi31, inner=pi12, m1=ab, t1=(s12, *bt), t2=(s31, *bt))
+            del ab
+            y1 = gather(rows, width, tab(), inner=pi12, m1=comps[2], t1=(s12, *bt))
+            c1 = gather(rows, width, tab(), inner=pi23, m1=x1, t1=(s23, *bt), r=(s12, LABEL_RAND, tid))
+            del x1
+            r3 = gather(rows, width, tab(), outer=pi23, inner=pi31, m1=y1, t1=(s31, *bt), t2=(s23, *bt), m3=c1,
+                        r=(s31, LABEL_RAND, tid))
+            del y1, c1
+            r1 = blind_table(s31, LABEL_RAND, tid, rows, width, self.dev)
+            r2 = blind_table(s12, LABEL_RAND, tid, rows, width, self.dev)
+            return [r1, r2, r3]
+        k1, k3 = compose(pi31, pi12), compose(pi23, pi31)
         u = gather(rows, width, tab(), outer=pi31, inner=pi12, t1=(s12, *bt), t2=(s31, *bt))
         v = gather(rows, width, tab(), inner=pi12, t1=(s12, *bt))
         w = gather(rows, width, tab(), inner=pi23, t1=(s23, *bt), r=(s12, LABEL_RAND, tid))
@@ -189,6 +236,23 @@ class Trio:
         c1 = gather(rows, width, tab(), inner=pi23, m1=x1, r=w)            # P2
         r3 = gather(rows, width, tab(), inner=k3, m1=y1, m3=c1, r=z)       # P3
         return [r1, r2, r3]
+
+    def _shuffle_online(self, comps: list, width: int, m: dict) -> list:
+        rows = comps[0].shape[0]
+
+        def tab():
+            return torch.empty((rows, words_for(width)), dtype=torch.int32, device=self.dev)
+
+        ab = torch.empty_like(comps[0])
+        _lib.call("ogm_xor_words", ab.numel(), _lib.ptr(comps[0]), _lib.ptr(comps[1]), None, _lib.ptr(ab),
+                  _lib.stream_ptr())
+        x1 = gather(rows, width, tab(), inner=m["k1"], m1=ab, r=m["u"])           # P1
+        del ab
+        y1 = gather(rows, width, tab(), inner=m["pi12"], m1=comps[2], r=m["v"])   # P2
+        c1 = gather(rows, width, tab(), inner=m["pi23"], m1=x1, r=m["w"])         # P2
+        del x1
+        r3 = gather(rows, width, tab(), inner=m["k3"], m1=y1, m3=c1, r=m["z"])    # P3
+        return [m["r1"], m["r2"], r3]
 
     # -- engine steps -----------------------------------------------------------
     def _fde(self, keys: list, domain: int) -> torch.Tensor:
@@ -301,7 +365,7 @@ class Trio:
                       out.shape[1], _lib.stream_ptr())
         return out
 
-    def fetch_multi(self, group: TrioGroup, flags: list, audit: list) -> TrioRecords:
+    def fetch_multi(self, group: TrioGroup, flags: list, audit: list, online_blinds=None) -> TrioRecords:
         """src/engine.py:220-270."""
         names = sorted(group.attrs)
         widths = [group.attr_widths[a] for a in names]
@@ -309,7 +373,8 @@ class Trio:
         rows = [self._pack(flags[j], [(group.ids[j], group.id_width)] +
                            [(group.attrs[a][j], w) for a, w in zip(names, widths)], group.count, row_width)
                 for j in range(3)]
-        sh = self.shuffle(rows, row_width)
+        sh = self.shuffle(rows, row_width, online_blinds)
+        del rows
         keep, k = self._open_keep(sh, group.count, "fetch", audit)
         ids = [self._extract(m, keep, k, 1, group.id_width) for m in sh]
         attrs, off = {}, 1 + group.id_width
