@@ -449,9 +449,64 @@ def run_c4(args):
         dist.destroy_process_group()
 
 
+def run_c5_sharded(args):
+    """C5 under torchrun: rows sharded across ranks, each online step = local
+    pack + NCCL all_to_all + local unpack (sharding.ShardedTrioShuffle)."""
+    import os
+
+    import torch.distributed as dist
+
+    from paper_2209_03526_b200.sharding import ShardedTrioShuffle, ShardPlan
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local),
+                            **({} if "MASTER_ADDR" in os.environ else
+                               {"init_method": "tcp://127.0.0.1:29555", "rank": 0, "world_size": 1}))
+    cfg = make_session_configs(b"\x77" * 16)
+    seeds = (cfg[0].seed_with_next, cfg[1].seed_with_next, cfg[2].seed_with_next)
+    width = 128
+    for lg in range(args.min_log, args.max_log + 1, args.log_step):
+        rows = 1 << lg
+        plan = ShardPlan(rows, world, align=1)
+        lo, hi = plan.bounds(rank)
+        comps = [workloads.device_random_words(rows * 4, args.seed, 20 + c).reshape(rows, 4)[lo:hi].clone()
+                 for c in range(3)]
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        sh = ShardedTrioShuffle(seeds, 0, rows, width, plan, rank)
+        torch.cuda.synchronize()
+        t_off = time.perf_counter() - t0
+        for _ in range(args.warmup):
+            out = sh.online(comps)
+        torch.cuda.synchronize()
+        dist.barrier()
+        ev = events(2)
+        ev[0].record()
+        for _ in range(args.steps):
+            out = sh.online(comps)
+        ev[1].record()
+        torch.cuda.synchronize()
+        ms = torch.tensor([ev[0].elapsed_time(ev[1]) / args.steps], device="cuda")
+        dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+        ms = float(ms.item())
+        nbytes = rows * (14 * 16 + 4 * 4)
+        if rank == 0:
+            emit({"config": f"C5 shuffle 2^{lg} rows x 128-bit, rows sharded x{world}", "metric": "shuffle_online_GBps",
+                  "value": nbytes / (ms * 1e-3) / 1e9, "unit": "GB/s", "ms": ms, "n_gpus": world,
+                  "hbm_frac_per_gpu": nbytes / world / (ms * 1e-3) / 1e9 / HBM_PEAK,
+                  "offline_s": t_off, "cross_gpu_bytes_per_rank": int(4 * rows * 16 * (world - 1) / world / world),
+                  "path": "ShardedTrioShuffle: pack + all_to_all + unpack per step"})
+        del comps, sh, out
+        torch.cuda.empty_cache()
+    dist.destroy_process_group()
+
+
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("which", choices=["c1", "c3", "c3p", "c4", "c5", "all"])
+    ap.add_argument("which", choices=["c1", "c3", "c3p", "c4", "c5", "c5d", "all"])
     ap.add_argument("--c4-rows", type=int, default=2_000_000)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
@@ -472,6 +527,8 @@ def main():
         run_c4(args)
     if args.which == "c3p":
         run_c3_pipeline(args)
+    if args.which == "c5d":
+        run_c5_sharded(args)
 
 
 if __name__ == "__main__":

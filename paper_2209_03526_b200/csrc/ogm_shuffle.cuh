@@ -129,6 +129,7 @@ struct GatherArgs {
     GatherTerm t1, t2, r;
     uint32_t* out;
     int64_t rows, W, width;
+    int64_t row0;  // global index of local row 0 (PRF term at i uses i + row0)
 };
 
 __device__ __forceinline__ void prf_row_chunk(const AesTab& T, const GatherTerm& g, int64_t row, int64_t W,
@@ -154,7 +155,7 @@ __device__ __forceinline__ void gather_chunk(const AesTab& T, const GatherArgs& 
     const int64_t k1 = a.P1 ? (int64_t)__ldg(a.P1 + k2) : k2;
     uint32_t acc[4] = {0, 0, 0, 0};
     const GatherTerm* terms[3] = {&a.t1, &a.t2, &a.r};
-    const int64_t trow[3] = {k1, k2, i};
+    const int64_t trow[3] = {k1, k2, i + a.row0};
 #pragma unroll
     for (int q = 0; q < 3; q++) {
         const GatherTerm& g = *terms[q];
@@ -164,7 +165,7 @@ __device__ __forceinline__ void gather_chunk(const AesTab& T, const GatherArgs& 
             prf_row_chunk(T, g, trow[q], a.W, c, nw, v);
             if (4 * c + nw == a.W) v[nw - 1] &= tail;
         } else {
-            const uint32_t* src = g.mat + trow[q] * a.W + 4 * c;
+            const uint32_t* src = g.mat + (q == 2 ? i : trow[q]) * a.W + 4 * c;
             for (int j = 0; j < nw; j++) v[j] = src[j];
         }
 #pragma unroll
@@ -491,7 +492,7 @@ int ogm_shuffle_gather(int64_t rows, int64_t words, int64_t width_bits, const in
                        const uint8_t* t1_key, const uint8_t* t1_label, uint64_t t1_index, const uint32_t* t1_mat,
                        const uint8_t* t2_key, const uint8_t* t2_label, uint64_t t2_index, const uint32_t* t2_mat,
                        const uint8_t* r_key, const uint8_t* r_label, uint64_t r_index, const uint32_t* r_mat,
-                       uint32_t* out, void* stream) {
+                       int64_t prf_row0, uint32_t* out, void* stream) {
     using namespace ogm;
     OGM_CHECK_ARG(rows >= 0 && words >= 0 && width_bits >= 0 && (width_bits + 31) / 32 == words, OGM_ERR_ARG,
                   "table shares must have %lld words per row for width %lld", (long long)((width_bits + 31) / 32),
@@ -513,6 +514,7 @@ int ogm_shuffle_gather(int64_t rows, int64_t words, int64_t width_bits, const in
     a.rows = rows;
     a.W = words;
     a.width = width_bits;
+    a.row0 = prf_row0;
     const bool online = a.t1.on == 1 || a.t2.on == 1 || a.r.on == 1;
     const int64_t work = rows * ((words + 3) / 4);
     cudaStream_t st = as_stream(stream);

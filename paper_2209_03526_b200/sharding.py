@@ -115,4 +115,118 @@ def sharded_sec_eval_trio(comps, words: int, plan: ShardPlan, rank: int, inds, z
     return result
 
 
-__all__ = ["ShardPlan", "pad_slice", "assemble", "all_gather_bits", "sharded_sec_eval_trio", "fss"]
+# ---------------------------------------------------------------------------
+# Row-sharded 3-party shuffle ("global permutation -> all-to-all")
+# ---------------------------------------------------------------------------
+#
+# Every online step of the shuffle is out[i] = M[k(i)] ^ B[i] (^ m3[i]) with
+# k a permutation fixed offline (shuffle.ShuffleOffline).  Rows of M and out
+# are sharded by ShardPlan.  All three parties live on every GPU, so every
+# rank knows k and plans the exchange locally:
+#   pack    send = M_local[send_idx]          (rows other ranks need from me,
+#                                              grouped by destination rank)
+#   a2a     recv = all_to_all(send)           (the step's only collective)
+#   unpack  out  = recv[recv_pos] ^ B ^ m3    (B = this shard's combined blinds)
+# pack/unpack are ogm_shuffle_gather launches; blinds for the shard come from
+# the PRF with the shard's global row offset, so no blinding data moves.
+
+
+@dataclass
+class ExchangePlan:
+    send_idx: torch.Tensor     # local source rows, grouped by destination rank
+    send_splits: list
+    recv_splits: list
+    recv_pos: torch.Tensor     # position of out row i's source in the recv buffer
+
+
+def exchange_plan(k_full: torch.Tensor, plan: ShardPlan, rank: int) -> ExchangePlan:
+    """Offline index planning for out[i] = M[k_full[i]] on this rank's rows."""
+    dev = k_full.device
+    per = plan.per_rank
+    lo, hi = plan.bounds(rank)
+
+    def owner(x):
+        return torch.clamp(x // per, max=plan.world - 1)
+
+    src = k_full[lo:hi].long()
+    own = owner(src)
+    order = torch.argsort(own, stable=True)             # recv buffer order: by sender, then by i
+    recv_pos = torch.empty_like(order)
+    recv_pos[order] = torch.arange(order.numel(), device=dev)
+    recv_splits = torch.bincount(own, minlength=plan.world).tolist() if order.numel() else [0] * plan.world
+    sends, send_splits = [], []
+    for s in range(plan.world):
+        l2, h2 = plan.bounds(s)
+        srcs = k_full[l2:h2].long()
+        mine = srcs[owner(srcs) == rank] - lo
+        sends.append(mine)
+        send_splits.append(int(mine.numel()))
+    send_idx = torch.cat(sends) if sends else torch.zeros(0, dtype=torch.long, device=dev)
+    return ExchangePlan(send_idx.to(torch.int32), send_splits, recv_splits, recv_pos.to(torch.int32))
+
+
+def _take(rows: int, width: int, src: torch.Tensor, idx: torch.Tensor, r=None, m3=None) -> torch.Tensor:
+    """out[i] = src[idx[i]] ^ r[i] ^ m3[i] on the device (ogm_shuffle_gather)."""
+    from .shuffle import gather
+    out = torch.empty((rows, words_for(width)), dtype=torch.int32, device=src.device)
+    if rows:
+        gather(rows, width, out, inner=idx, m1=src, r=r, m3=m3)
+    return out
+
+
+def exchange_gather(m_local: torch.Tensor, xp: ExchangePlan, width: int, r=None, m3=None, group=None):
+    import torch.distributed as dist
+    send = _take(xp.send_idx.numel(), width, m_local, xp.send_idx)
+    recv = torch.empty((sum(xp.recv_splits), send.shape[1]), dtype=send.dtype, device=send.device)
+    dist.all_to_all_single(recv, send, xp.recv_splits, xp.send_splits, group=group)
+    return _take(xp.recv_pos.numel(), width, recv, xp.recv_pos, r=r, m3=m3)
+
+
+class ShardedTrioShuffle:
+    """Offline material + online steps of one shuffle (table id ``tid``) for
+    this rank's rows; the concatenation over ranks equals the single-GPU
+    trio shuffle (trio.Trio.shuffle) bit for bit."""
+
+    def __init__(self, seeds: tuple, tid: int, rows: int, width: int, plan: ShardPlan, rank: int, device=None):
+        from .prf import seeded_permutation_device
+        from .shuffle import LABEL_BLIND, LABEL_PERM, LABEL_RAND, compose, gather
+        s12, s23, s31 = seeds
+        self.width, self.plan, self.rank = width, plan, rank
+        dev = device or torch.device("cuda")
+        pi12, pi23, pi31 = (seeded_permutation_device(s, LABEL_PERM, tid, rows, device=dev) for s in (s12, s23, s31))
+        k1, k3 = compose(pi31, pi12), compose(pi23, pi31)
+        lo, hi = plan.bounds(rank)
+        n = hi - lo
+        self.lo, self.n = lo, n
+        bt = (LABEL_BLIND, tid)
+
+        def tab():
+            return torch.empty((n, words_for(width)), dtype=torch.int32, device=dev)
+
+        # this shard's combined blinds (destination-indexed), PRF at global rows
+        self.u = gather(n, width, tab(), outer=pi31[lo:hi], inner=pi12, t1=(s12, *bt), t2=(s31, *bt))
+        self.v = gather(n, width, tab(), inner=pi12[lo:hi], t1=(s12, *bt))
+        self.w = gather(n, width, tab(), inner=pi23[lo:hi], t1=(s23, *bt), r=(s12, LABEL_RAND, tid), row0=lo)
+        self.z = gather(n, width, tab(), outer=pi23[lo:hi], inner=pi31, t1=(s31, *bt), t2=(s23, *bt),
+                        r=(s31, LABEL_RAND, tid), row0=lo)
+        self.r1 = gather(n, width, tab(), r=(s31, LABEL_RAND, tid), row0=lo)
+        self.r2 = gather(n, width, tab(), r=(s12, LABEL_RAND, tid), row0=lo)
+        self.xp = {"x1": exchange_plan(k1, plan, rank), "y1": exchange_plan(pi12, plan, rank),
+                   "c1": exchange_plan(pi23, plan, rank), "r3": exchange_plan(k3, plan, rank)}
+
+    def online(self, comps: list, group=None) -> list:
+        """comps: this rank's rows of the three components -> new components."""
+        w = self.width
+        ab = torch.empty_like(comps[0])
+        if ab.numel():
+            _lib.call("ogm_xor_words", ab.numel(), _lib.ptr(comps[0]), _lib.ptr(comps[1]), None, _lib.ptr(ab),
+                      _lib.stream_ptr())
+        x1 = exchange_gather(ab, self.xp["x1"], w, r=self.u, group=group)          # P1
+        y1 = exchange_gather(comps[2], self.xp["y1"], w, r=self.v, group=group)    # P2
+        c1 = exchange_gather(x1, self.xp["c1"], w, r=self.w, group=group)          # P2
+        r3 = exchange_gather(y1, self.xp["r3"], w, r=self.z, m3=c1, group=group)   # P3
+        return [self.r1, self.r2, r3]
+
+
+__all__ = ["ShardPlan", "pad_slice", "assemble", "all_gather_bits", "sharded_sec_eval_trio", "ExchangePlan",
+           "exchange_plan", "exchange_gather", "ShardedTrioShuffle", "fss"]

@@ -336,3 +336,48 @@ def test_trio_fast_path_matches_reference(golden, name):
                     assert np.array_equal(host(mr.attrs[a].share_b.words), g[f"{base}_{a}_b"]), base
         for j, (_phase, bits) in enumerate(r.opened_flags):
             assert np.array_equal(bits, g[f"{name}_p{p}_open{j}"])
+
+
+@pytest.mark.parametrize("world,rows,width", [(1, 1000, 128), (2, 1000, 129), (3, 7001, 70), (8, 50_000, 128)])
+def test_sharded_shuffle_equals_trio_shuffle(world, rows, width):
+    """Row-sharded shuffle (exchange plans + shard blinds at global row offsets)
+    emulated for `world` ranks on one GPU equals the single-GPU trio shuffle."""
+    import paper_2209_03526_b200.sharding as sh
+    from paper_2209_03526_b200.bits import words_for
+    from paper_2209_03526_b200.trio import Trio
+    w = words_for(width)
+    g = torch.Generator(device="cuda").manual_seed(rows + world)
+    comps = [torch.randint(-2**31, 2**31 - 1, (rows, w), dtype=torch.int32, device="cuda", generator=g)
+             for _ in range(3)]
+    if width % 32:
+        for c in comps:
+            c[:, -1] &= (1 << (width % 32)) - 1
+    trio = Trio(b"\x66" * 16)
+    want = trio.shuffle(comps, width, online_blinds=False)
+    seeds = (trio.s12, trio.s23, trio.s31)
+    plan = sh.ShardPlan(rows, world, align=1)
+    ranks = [sh.ShardedTrioShuffle(seeds, 0, rows, width, plan, r) for r in range(world)]
+    loc = [[c[plan.bounds(r)[0]:plan.bounds(r)[1]] for c in comps] for r in range(world)]
+
+    def exchange(step, srcs, rs, m3s=None):
+        sends = [sh._take(ranks[r].xp[step].send_idx.numel(), width, srcs[r], ranks[r].xp[step].send_idx)
+                 for r in range(world)]
+        outs = []
+        for r in range(world):  # all_to_all: rank r receives sender o's chunk for r
+            parts = []
+            for o in range(world):
+                off = sum(ranks[o].xp[step].send_splits[:r])
+                parts.append(sends[o][off: off + ranks[o].xp[step].send_splits[r]])
+            recv = torch.cat(parts)
+            outs.append(sh._take(ranks[r].xp[step].recv_pos.numel(), width, recv, ranks[r].xp[step].recv_pos,
+                                 r=rs[r], m3=None if m3s is None else m3s[r]))
+        return outs
+
+    ab = [loc[r][0] ^ loc[r][1] for r in range(world)]
+    x1 = exchange("x1", ab, [ranks[r].u for r in range(world)])
+    y1 = exchange("y1", [loc[r][2] for r in range(world)], [ranks[r].v for r in range(world)])
+    c1 = exchange("c1", x1, [ranks[r].w for r in range(world)])
+    r3 = exchange("r3", y1, [ranks[r].z for r in range(world)], m3s=c1)
+    assert torch.equal(torch.cat([ranks[r].r1 for r in range(world)]), want[0])
+    assert torch.equal(torch.cat([ranks[r].r2 for r in range(world)]), want[1])
+    assert torch.equal(torch.cat(r3), want[2])

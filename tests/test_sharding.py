@@ -97,3 +97,51 @@ def test_plan_alignment_and_coverage():
             if rows < 5000:
                 assert covered == list(range(rows))
             assert plan.bounds(world - 1)[1] == rows
+
+
+# ---------------------------------------------------------------------------
+# row-sharded shuffle: exchange plans + all_to_all (gloo, CPU)
+# ---------------------------------------------------------------------------
+
+SH_ROWS, SH_W = 1000, 5
+
+
+def _numpy_take(rows, width, src, idx, r=None, m3=None):
+    out = src[idx.long()].clone() if rows else torch.zeros((0, src.shape[1]), dtype=src.dtype)
+    if r is not None:
+        out ^= r
+    if m3 is not None:
+        out ^= m3
+    return out
+
+
+def _xworker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import paper_2209_03526_b200.sharding as sh
+    sh._take = _numpy_take   # test-only CPU data movement; plans + collective are the product's
+    g = torch.Generator().manual_seed(11)
+    M = torch.randint(-2**31, 2**31 - 1, (SH_ROWS, SH_W), dtype=torch.int32, generator=g)
+    k = torch.randperm(SH_ROWS, generator=g).to(torch.int32)
+    plan = sh.ShardPlan(SH_ROWS, world, align=1)
+    lo, hi = plan.bounds(rank)
+    xp = sh.exchange_plan(k, plan, rank)
+    out = sh.exchange_gather(M[lo:hi], xp, 32 * SH_W)
+    q.put((rank, out.numpy().copy(), M[k.long()][lo:hi].numpy().copy()))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_exchange_gather_all_to_all(world):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = 29700 + world * 11 + os.getpid() % 1000
+    procs = [ctx.Process(target=_xworker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    got = [q.get(timeout=120) for _ in range(world)]
+    for p in procs:
+        p.join(60)
+        assert p.exitcode == 0
+    for rank, out, want in got:
+        assert np.array_equal(out, want), rank
