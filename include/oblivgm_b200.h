@@ -215,14 +215,18 @@ int ogm_compact_bits(int64_t n, const uint32_t* bits, int32_t* out_idx, int64_t*
  * src/shuffle.py:69-73 layout; all-NULL = absent.  Rows are `words` words
  * wide (= ceil(width_bits/32)), densely packed.  `prf_row0` is the global
  * row of local row 0 (row-sharded tables): the on-the-fly R term at i uses
- * stream row i + prf_row0; T1/T2 are indexed by the (global) permutations. */
+ * stream row i + prf_row0; T1/T2 are indexed by the (global) permutations.
+ * `pitch` (0 = words) is the in-memory row stride of every matrix argument;
+ * with a 16-byte pitch (zero padding past `words`) all accesses are 128-bit.
+ * The PRF tables follow the reference's dense stream layout regardless. */
 int ogm_shuffle_gather(int64_t rows, int64_t words, int64_t width_bits, const int32_t* perm_outer,
                        const int32_t* perm_inner, const uint32_t* m1, const uint32_t* m2,
                        const uint32_t* m3, const uint8_t* t1_key, const uint8_t* t1_label,
                        uint64_t t1_index, const uint32_t* t1_mat, const uint8_t* t2_key,
                        const uint8_t* t2_label, uint64_t t2_index, const uint32_t* t2_mat,
                        const uint8_t* r_key, const uint8_t* r_label, uint64_t r_index,
-                       const uint32_t* r_mat, int64_t prf_row0, uint32_t* out, void* stream);
+                       const uint32_t* r_mat, int64_t prf_row0, int64_t pitch, uint32_t* out,
+                       void* stream);
 
 /* Offline composition of two known permutations: out[i] = inner[outer[i]]
  * (gather semantics, so M[out] = M[inner][outer] as in src/shuffle.py:76-77). */

@@ -60,7 +60,7 @@ SIGNATURES = {
     "ogm_compact_workspace_bytes": ([_i64], _i64),
     "ogm_compact_bits": ([_i64, _vp, _vp, _vp, _vp, _i64, _vp], _int),
     "ogm_shuffle_gather": ([_i64, _i64, _i64, _vp, _vp, _vp, _vp, _vp, _cp, _cp, _u64, _vp, _cp, _cp, _u64,
-                            _vp, _cp, _cp, _u64, _vp, _i64, _vp, _vp], _int),
+                            _vp, _cp, _cp, _u64, _vp, _i64, _i64, _vp, _vp], _int),
     "ogm_perm_compose": ([_i64, _vp, _vp, _vp, _vp], _int),
     "ogm_gather_tile_rows": ([_i64], _i64),
     "ogm_gather_plan_workspace_bytes": ([_i64], _i64),

@@ -366,9 +366,21 @@ __device__ __forceinline__ uint32_t field_bits32(const uint32_t* row, int64_t wi
 
 __device__ __forceinline__ uint32_t pack_word(const PackArgs& a, int64_t r, int64_t k, int64_t ow);
 
-// wide rows: one CTA per row (grid-stride over rows), threads over words
+// wide rows: one CTA per row (grid-stride over rows), threads over words;
+// with a 16-B output pitch each thread emits a 128-bit group
 __global__ void pack_fields_rows_kernel(const PackArgs a) {
     const int64_t ow = (a.owidth + 31) >> 5;
+    if ((a.opitch & 3) == 0 && (((uintptr_t)a.out) & 15) == 0) {
+        const int64_t ng = a.opitch >> 2;
+        for (int64_t r = blockIdx.x; r < a.rows; r += gridDim.x)
+            for (int64_t gi = threadIdx.x; gi < ng; gi += blockDim.x) {
+                const int64_t k = gi << 2;
+                uint4 v = make_uint4(pack_word(a, r, k, ow), pack_word(a, r, k + 1, ow), pack_word(a, r, k + 2, ow),
+                                     pack_word(a, r, k + 3, ow));
+                reinterpret_cast<uint4*>(a.out + r * a.opitch)[gi] = v;
+            }
+        return;
+    }
     for (int64_t r = blockIdx.x; r < a.rows; r += gridDim.x)
         for (int64_t k = threadIdx.x; k < a.opitch; k += blockDim.x) a.out[r * a.opitch + k] = pack_word(a, r, k, ow);
 }

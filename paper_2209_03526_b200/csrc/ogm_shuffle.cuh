@@ -129,7 +129,8 @@ struct GatherArgs {
     GatherTerm t1, t2, r;
     uint32_t* out;
     int64_t rows, W, width;
-    int64_t row0;  // global index of local row 0 (PRF term at i uses i + row0)
+    int64_t row0;   // global index of local row 0 (PRF term at i uses i + row0)
+    int64_t pitch;  // words per row in memory (>= W; zero padding past W)
 };
 
 __device__ __forceinline__ void prf_row_chunk(const AesTab& T, const GatherTerm& g, int64_t row, int64_t W,
@@ -149,8 +150,10 @@ __device__ __forceinline__ void prf_row_chunk(const AesTab& T, const GatherTerm&
 
 template <bool ONLINE>
 __device__ __forceinline__ void gather_chunk(const AesTab& T, const GatherArgs& a, int64_t i, int64_t c,
-                                             uint32_t tail) {
-    const int nw = (int)min((int64_t)4, a.W - 4 * c);
+                                             uint32_t tail, bool vec) {
+    // words [4c, 4c+nw) of row i; with a 16-B pitch the padding words ride
+    // along as zeros and every access is 128-bit
+    const int nw = (int)min((int64_t)4, a.W - 4 * c);  // words inside the logical row (may be <= 0)
     const int64_t k2 = a.P2 ? (int64_t)__ldg(a.P2 + i) : i;
     const int64_t k1 = a.P1 ? (int64_t)__ldg(a.P1 + k2) : k2;
     uint32_t acc[4] = {0, 0, 0, 0};
@@ -159,23 +162,31 @@ __device__ __forceinline__ void gather_chunk(const AesTab& T, const GatherArgs& 
 #pragma unroll
     for (int q = 0; q < 3; q++) {
         const GatherTerm& g = *terms[q];
-        if (g.on == 0) continue;
+        if (g.on == 0 || nw <= 0) continue;
         uint32_t v[4] = {0, 0, 0, 0};
         if (ONLINE && g.on == 1) {
             prf_row_chunk(T, g, trow[q], a.W, c, nw, v);
             if (4 * c + nw == a.W) v[nw - 1] &= tail;
+#pragma unroll
+            for (int j = 0; j < 4; j++)
+                if (j >= nw) v[j] = 0;
         } else {
-            const uint32_t* src = g.mat + (q == 2 ? i : trow[q]) * a.W + 4 * c;
-            for (int j = 0; j < nw; j++) v[j] = src[j];
+            const uint32_t* src = g.mat + (q == 2 ? i : trow[q]) * a.pitch + 4 * c;
+            if (vec) {
+                const uint4 x = *reinterpret_cast<const uint4*>(src);
+                v[0] = x.x; v[1] = x.y; v[2] = x.z; v[3] = x.w;
+            } else {
+                for (int j = 0; j < nw; j++) v[j] = src[j];
+            }
         }
 #pragma unroll
         for (int j = 0; j < 4; j++) acc[j] ^= v[j];
     }
-    const uint32_t* m1 = a.M1 ? a.M1 + k1 * a.W + 4 * c : nullptr;
-    const uint32_t* m2 = a.M2 ? a.M2 + k1 * a.W + 4 * c : nullptr;
-    const uint32_t* m3 = a.M3 ? a.M3 + i * a.W + 4 * c : nullptr;
-    uint32_t* o = a.out + i * a.W + 4 * c;
-    if (nw == 4 && ((a.W & 3) == 0)) {
+    const uint32_t* m1 = a.M1 ? a.M1 + k1 * a.pitch + 4 * c : nullptr;
+    const uint32_t* m2 = a.M2 ? a.M2 + k1 * a.pitch + 4 * c : nullptr;
+    const uint32_t* m3 = a.M3 ? a.M3 + i * a.pitch + 4 * c : nullptr;
+    uint32_t* o = a.out + i * a.pitch + 4 * c;
+    if (vec) {
         uint4 x = make_uint4(acc[0], acc[1], acc[2], acc[3]);
         if (m1) x = xor4(x, *reinterpret_cast<const uint4*>(m1));
         if (m2) x = xor4(x, *reinterpret_cast<const uint4*>(m2));
@@ -200,18 +211,22 @@ __global__ void __launch_bounds__(kAesThreads) shuffle_gather_kernel(const Gathe
         __syncthreads();
     }
     const AesTab T(smem_raw);
-    const int64_t nch = (a.W + 3) >> 2;
+    // 128-bit path when rows are 16-B pitched and every base is aligned
+    const bool vec = (a.pitch & 3) == 0 &&
+                     ((((uintptr_t)a.M1) | ((uintptr_t)a.M2) | ((uintptr_t)a.M3) | ((uintptr_t)a.out) |
+                       ((uintptr_t)a.t1.mat) | ((uintptr_t)a.t2.mat) | ((uintptr_t)a.r.mat)) & 15) == 0;
+    const int64_t nch = vec ? (a.pitch >> 2) : ((a.W + 3) >> 2);
     const uint32_t tail = (a.width & 31) ? ((1u << (a.width & 31)) - 1u) : 0xffffffffu;
     if (nch >= 64) {
         // wide rows: a CTA walks rows, its threads walk the row's 4-word chunks
         for (int64_t i = blockIdx.x; i < a.rows; i += gridDim.x)
-            for (int64_t c = threadIdx.x; c < nch; c += blockDim.x) gather_chunk<ONLINE>(T, a, i, c, tail);
+            for (int64_t c = threadIdx.x; c < nch; c += blockDim.x) gather_chunk<ONLINE>(T, a, i, c, tail, vec);
     } else {
         const int64_t total = a.rows * nch;
         const int64_t stride = (int64_t)gridDim.x * blockDim.x;
         for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += stride) {
             const int64_t i = t / nch;
-            gather_chunk<ONLINE>(T, a, i, t - i * nch, tail);
+            gather_chunk<ONLINE>(T, a, i, t - i * nch, tail, vec);
         }
     }
 }
@@ -492,7 +507,7 @@ int ogm_shuffle_gather(int64_t rows, int64_t words, int64_t width_bits, const in
                        const uint8_t* t1_key, const uint8_t* t1_label, uint64_t t1_index, const uint32_t* t1_mat,
                        const uint8_t* t2_key, const uint8_t* t2_label, uint64_t t2_index, const uint32_t* t2_mat,
                        const uint8_t* r_key, const uint8_t* r_label, uint64_t r_index, const uint32_t* r_mat,
-                       int64_t prf_row0, uint32_t* out, void* stream) {
+                       int64_t prf_row0, int64_t pitch, uint32_t* out, void* stream) {
     using namespace ogm;
     OGM_CHECK_ARG(rows >= 0 && words >= 0 && width_bits >= 0 && (width_bits + 31) / 32 == words, OGM_ERR_ARG,
                   "table shares must have %lld words per row for width %lld", (long long)((width_bits + 31) / 32),
@@ -515,8 +530,10 @@ int ogm_shuffle_gather(int64_t rows, int64_t words, int64_t width_bits, const in
     a.W = words;
     a.width = width_bits;
     a.row0 = prf_row0;
+    a.pitch = pitch > 0 ? pitch : words;
+    OGM_CHECK_ARG(a.pitch >= words, OGM_ERR_ARG, "pitch %lld below %lld words", (long long)a.pitch, (long long)words);
     const bool online = a.t1.on == 1 || a.t2.on == 1 || a.r.on == 1;
-    const int64_t work = rows * ((words + 3) / 4);
+    const int64_t work = rows * ((a.pitch + 3) / 4);
     cudaStream_t st = as_stream(stream);
     if (online) {
         shuffle_gather_kernel<true><<<aes_grid(work), kAesThreads, kAesTableBytes, st>>>(a);

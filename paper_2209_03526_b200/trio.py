@@ -42,6 +42,21 @@ def _nxt(q: int) -> int:
     return (q + 1) % 3
 
 
+def _pitch(width: int) -> int:
+    """16-byte row pitch of the trio path's match tables (zero padding)."""
+    return (words_for(width) + 3) // 4 * 4
+
+
+def _as_pitched(m: torch.Tensor, width: int) -> torch.Tensor:
+    """A (rows, pitch) buffer holding m's logical (rows, words) content."""
+    p = _pitch(width)
+    if m.dim() == 2 and m.shape[1] == p and m.is_contiguous():
+        return m
+    out = torch.zeros((m.shape[0], p), dtype=m.dtype, device=m.device)
+    out[:, :words_for(width)] = m[:, :words_for(width)]
+    return out
+
+
 @dataclass
 class TrioGroup:
     """Candidate group with its three share components per field."""
@@ -170,7 +185,7 @@ class Trio:
         pi12, pi23, pi31 = _perm(s12, tid, rows), _perm(s23, tid, rows), _perm(s31, tid, rows)
 
         def tab():
-            return torch.empty((rows, words_for(width)), dtype=torch.int32, device=self.dev)
+            return torch.empty((rows, _pitch(width)), dtype=torch.int32, device=self.dev)
 
         bt = (LABEL_BLIND, tid)
         m = {"pi12": pi12, "pi23": pi23, "k1": compose(pi31, pi12), "k3": compose(pi23, pi31),
@@ -179,8 +194,8 @@ class Trio:
              "w": gather(rows, width, tab(), inner=pi23, t1=(s23, *bt), r=(s12, LABEL_RAND, tid)),
              "z": gather(rows, width, tab(), outer=pi23, inner=pi31, t1=(s31, *bt), t2=(s23, *bt),
                          r=(s31, LABEL_RAND, tid)),
-             "r1": blind_table(s31, LABEL_RAND, tid, rows, width, self.dev),
-             "r2": blind_table(s12, LABEL_RAND, tid, rows, width, self.dev)}
+             "r1": gather(rows, width, tab(), r=(s31, LABEL_RAND, tid)),
+             "r2": gather(rows, width, tab(), r=(s12, LABEL_RAND, tid))}
         if not hasattr(self, "_prepared"):
             self._prepared = {}
         self._prepared[(tid, rows, width)] = m
@@ -192,6 +207,7 @@ class Trio:
         (AES-CTR on the fly) instead of materialising them -- the memory-lean
         mode for wide rows (default: on for tables above 4 GiB)."""
         rows = comps[0].shape[0]
+        comps = [_as_pitched(c, width) for c in comps]
         tid = self.table_id
         self.table_id += 1
         prep = getattr(self, "_prepared", {}).pop((tid, rows, width), None)
@@ -201,7 +217,7 @@ class Trio:
         pi12, pi23, pi31 = _perm(s12, tid, rows), _perm(s23, tid, rows), _perm(s31, tid, rows)
 
         def tab():
-            return torch.empty((rows, words_for(width)), dtype=torch.int32, device=self.dev)
+            return torch.empty((rows, _pitch(width)), dtype=torch.int32, device=self.dev)
 
         bt = (LABEL_BLIND, tid)
         if online_blinds is None:
@@ -218,16 +234,16 @@ class Trio:
             r3 = gather(rows, width, tab(), outer=pi23, inner=pi31, m1=y1, t1=(s31, *bt), t2=(s23, *bt), m3=c1,
                         r=(s31, LABEL_RAND, tid))
             del y1, c1
-            r1 = blind_table(s31, LABEL_RAND, tid, rows, width, self.dev)
-            r2 = blind_table(s12, LABEL_RAND, tid, rows, width, self.dev)
+            r1 = gather(rows, width, tab(), r=(s31, LABEL_RAND, tid))
+            r2 = gather(rows, width, tab(), r=(s12, LABEL_RAND, tid))
             return [r1, r2, r3]
         k1, k3 = compose(pi31, pi12), compose(pi23, pi31)
         u = gather(rows, width, tab(), outer=pi31, inner=pi12, t1=(s12, *bt), t2=(s31, *bt))
         v = gather(rows, width, tab(), inner=pi12, t1=(s12, *bt))
         w = gather(rows, width, tab(), inner=pi23, t1=(s23, *bt), r=(s12, LABEL_RAND, tid))
         z = gather(rows, width, tab(), outer=pi23, inner=pi31, t1=(s31, *bt), t2=(s23, *bt), r=(s31, LABEL_RAND, tid))
-        r1 = blind_table(s31, LABEL_RAND, tid, rows, width, self.dev)
-        r2 = blind_table(s12, LABEL_RAND, tid, rows, width, self.dev)
+        r1 = gather(rows, width, tab(), r=(s31, LABEL_RAND, tid))
+        r2 = gather(rows, width, tab(), r=(s12, LABEL_RAND, tid))
         ab = torch.empty_like(comps[0])
         _lib.call("ogm_xor_words", ab.numel(), _lib.ptr(comps[0]), _lib.ptr(comps[1]), None, _lib.ptr(ab),
                   _lib.stream_ptr())
@@ -241,7 +257,7 @@ class Trio:
         rows = comps[0].shape[0]
 
         def tab():
-            return torch.empty((rows, words_for(width)), dtype=torch.int32, device=self.dev)
+            return torch.empty((rows, _pitch(width)), dtype=torch.int32, device=self.dev)
 
         ab = torch.empty_like(comps[0])
         _lib.call("ogm_xor_words", ab.numel(), _lib.ptr(comps[0]), _lib.ptr(comps[1]), None, _lib.ptr(ab),
@@ -333,7 +349,7 @@ class Trio:
                            {a: [c[None] for c in v] for a, v in attrs.items()}, dict(group.attr_widths))
 
     def _pack(self, flag_bits, fields, rows, width) -> torch.Tensor:
-        out = torch.empty((rows, words_for(width)), dtype=torch.int32, device=self.dev)
+        out = torch.empty((rows, _pitch(width)), dtype=torch.int32, device=self.dev)
         mats = [f for f, _ in fields]
         _lib.call("ogm_pack_fields", rows, _lib.ptr(flag_bits), len(fields), A(mats),
                   _lib.i64_array([m.stride(0) if rows else words_for(wd) for m, wd in fields]),
