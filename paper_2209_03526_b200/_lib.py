@@ -70,11 +70,14 @@ SIGNATURES = {
 }
 
 _lib = None
+_device_ok = False
 
 
 def load(require_device: bool = True):
     """Load the library (and, by default, insist on a CUDA device)."""
-    global _lib
+    global _lib, _device_ok
+    if _lib is not None and (_device_ok or not require_device):
+        return _lib
     if _lib is None:
         if not LIB_PATH.exists():
             raise RuntimeError(
@@ -86,8 +89,10 @@ def load(require_device: bool = True):
             fn.argtypes = args
             fn.restype = res
         _lib = lib
-    if require_device and not torch.cuda.is_available():
-        raise RuntimeError("paper_2209_03526_b200 needs a CUDA device (no CPU fallback)")
+    if require_device:
+        if not torch.cuda.is_available():
+            raise RuntimeError("paper_2209_03526_b200 needs a CUDA device (no CPU fallback)")
+        _device_ok = True
     return _lib
 
 
@@ -104,9 +109,16 @@ def check(rc: int) -> None:
     raise RuntimeError(f"libogm_b200 error {rc}: {msg}")
 
 
+_fns: dict = {}
+
+
 def call(name: str, *args) -> None:
-    lib = load()
-    check(getattr(lib, name)(*args))
+    fn = _fns.get(name)
+    if fn is None:
+        fn = _fns[name] = getattr(load(), name)
+    rc = fn(*args)
+    if rc:
+        check(rc)
 
 
 def ptr(t: torch.Tensor | None):
@@ -136,5 +148,8 @@ def i64_array(vals) -> ctypes.Array:
 
 
 def stream_ptr(stream: torch.cuda.Stream | None = None):
-    s = stream if stream is not None else torch.cuda.current_stream()
-    return ctypes.c_void_p(s.cuda_stream)
+    """cudaStream_t of `stream` or of the calling thread's current stream
+    (raw accessor: torch.cuda.current_stream() costs ~10 us per call)."""
+    if stream is not None:
+        return stream.cuda_stream
+    return torch._C._cuda_getCurrentRawStream(torch._C._cuda_getDevice())

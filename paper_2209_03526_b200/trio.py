@@ -366,7 +366,7 @@ class Trio:
         plain, host = self.open([self._column(m) for m in shuffled], rows)
         audit.append((phase, host.to_bits().copy()))
         idx = torch.empty((max(rows, 1),), dtype=torch.int32, device=self.dev)
-        cnt = torch.zeros((1,), dtype=torch.int64, device=self.dev)
+        cnt = torch.empty((1,), dtype=torch.int64, device=self.dev)
         nb = int(_lib.load().ogm_compact_workspace_bytes(rows))
         ws = torch.empty((nb,), dtype=torch.uint8, device=self.dev)
         _lib.call("ogm_compact_bits", rows, _lib.ptr(plain), _lib.ptr(idx), _lib.ptr(cnt), _lib.ptr(ws), nb,
@@ -400,11 +400,18 @@ class Trio:
         return TrioRecords(group.parent_slot, group.parent_record, k, group.id_width, ids, attrs,
                            dict(zip(names, widths)))
 
+    def _consts(self, w: int):
+        """Cached all-ones / all-zeros indicator rows of w words."""
+        cache = self.__dict__.setdefault("_const_cache", {})
+        if w not in cache:
+            cache[w] = (torch.full((w,), -1, dtype=torch.int32, device=self.dev),
+                        torch.zeros((w,), dtype=torch.int32, device=self.dev))
+        return cache[w]
+
     def _parity_rows(self, mat, w) -> torch.Tensor:
         rows = mat.shape[0]
         out = self._empty(words_for(rows))
-        ones = torch.full((w,), -1, dtype=torch.int32, device=self.dev)
-        zeros = torch.zeros((w,), dtype=torch.int32, device=self.dev)
+        ones, zeros = self._consts(w)
         _lib.call("ogm_masked_parity", rows, w, mat.stride(0), 2, A([mat, mat]), 1, _lib.int_array([0]),
                   _lib.int_array([1]), 1, A([ones, zeros]), A([out]), _lib.stream_ptr())
         return out

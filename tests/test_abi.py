@@ -64,5 +64,6 @@ def test_zero_sized_calls_are_noops(lib):
 def test_product_refuses_without_device(monkeypatch):
     import torch
     monkeypatch.setattr(torch.cuda, "is_available", lambda: False)
+    monkeypatch.setattr(_lib, "_device_ok", False)
     with pytest.raises(RuntimeError, match="no CPU fallback"):
         _lib.load()
