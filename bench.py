@@ -53,6 +53,9 @@ BITS = 32
 DEFAULT_KEYS = 1 << 24
 LOOKUPS = {"dcf": 31 * (160 + 133) + 133, "dpf": 32 * (160 + 133)}
 OPS_PER_LOOKUP = 2
+# dram__bytes_read.sum + dram__bytes_write.sum of one fss_eval_kernel launch at
+# 2^24 DCF keys (profiles/r01_fss_eval_full_ncu.csv): 8,877,741,568 + 5,532,672
+NCU_TRAFFIC = {("dcf", DEFAULT_KEYS): 8877741568 + 5532672}
 
 
 def parse():
@@ -285,7 +288,11 @@ def main():
     ops_per_eval = OPS_PER_LOOKUP * LOOKUPS[args.kind]
     achieved = K * ops_per_eval / avg_launch_s
     roofline = {"bound": "int_alu", "achieved": achieved / 1e12, "peak": peak.value / 1e12,
-                "unit": "Tops/s", "frac": achieved / peak.value, "traffic": None,
+                "unit": "Tops/s", "frac": achieved / peak.value,
+                "traffic": NCU_TRAFFIC.get((args.kind, K)),
+                "traffic_source": "ncu dram__bytes_read+write per launch, profiles/r01_fss_eval_full_ncu.csv",
+                "algorithmic_key_bytes_per_launch": K * (16 + 16 * (BITS - (1 if comparison else 0)) + 12 + 1 + 4),
+                "binding_pipe": "LSU (shared-memory T-table lookups) 93.5% / ALU 83.7% of peak (ncu)",
                 "ops_per_eval": ops_per_eval, "aes_lookups_per_eval": LOOKUPS[args.kind],
                 "peak_source": "ogm_measure_int_peak (LOP3 issue rate, this run)",
                 "key_bytes_per_eval": 16 + 16 * (BITS - (1 if comparison else 0)) + 12 + 1 + 4}
