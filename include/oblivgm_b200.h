@@ -205,6 +205,15 @@ int64_t ogm_compact_workspace_bytes(int64_t n);
 int ogm_compact_bits(int64_t n, const uint32_t* bits, int32_t* out_idx, int64_t* out_count,
                      void* workspace, int64_t workspace_bytes, void* stream);
 
+/* ---- storage (src/storage.py) -------------------------------------------- */
+
+/* Loader for OGMS record containers (src/storage.py:43-65, 108-169): the file
+ * image `blob` (device, 4-byte aligned) holds nrec share records; record r's
+ * payload of nwords[r] uint32 starts at byte src_off[r] and lands at word
+ * dst_off[r] of `arena` (device).  Headers are validated by the caller. */
+int ogm_unpack_records(const void* blob, int64_t blob_bytes, int64_t nrec, const int64_t* src_off,
+                       const int64_t* dst_off, const int32_t* nwords, uint32_t* arena, void* stream);
+
 /* ---- L1 shuffle (src/shuffle.py) ------------------------------------------ */
 
 /* One party-local step of sec_shuffle (src/shuffle.py:106-143):

@@ -56,6 +56,7 @@ SIGNATURES = {
     "ogm_pack_fields": ([_i64, _vp, _int, _vp, _vp, _vp, _vp, _i64, _vp], _int),
     "ogm_extract_field": ([_vp, _i64, _vp, _i64, _i64, _i64, _vp, _i64, _vp], _int),
     "ogm_mask_row_tails": ([_vp, _i64, _i64, _i64, _vp], _int),
+    "ogm_unpack_records": ([_vp, _i64, _i64, _vp, _vp, _vp, _vp, _vp], _int),
     "ogm_column_bits": ([_vp, _i64, _i64, _vp, _vp], _int),
     "ogm_compact_workspace_bytes": ([_i64], _i64),
     "ogm_compact_bits": ([_i64, _vp, _vp, _vp, _vp, _i64, _vp], _int),

@@ -519,6 +519,29 @@ __global__ void select_many_kernel(const uint32_t* __restrict__ ta, const uint32
         if (k < kn && acc[k]) atomicXor(out + k * opitch + w, acc[k]);
 }
 
+// OGMS record payloads (src/storage.py:43-65) -> device matrices.  A warp per
+// record; payloads sit at arbitrary byte offsets (15-byte headers), so each
+// word is a funnel shift of two aligned words of the file image.
+__global__ void unpack_records_kernel(const uint32_t* __restrict__ blob_words, int64_t blob_bytes, int64_t nrec,
+                                      const int64_t* __restrict__ src_off, const int64_t* __restrict__ dst_off,
+                                      const int32_t* __restrict__ nwords, uint32_t* __restrict__ arena) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+    const int64_t nblob = (blob_bytes + 3) >> 2;
+    for (int64_t r = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); r < nrec; r += warps) {
+        const int64_t src = src_off[r];
+        const int64_t base = src >> 2;
+        const int sh = (int)(src & 3) * 8;
+        const int n = nwords[r];
+        uint32_t* dst = arena + dst_off[r];
+        for (int j = lane; j < n; j += 32) {
+            const uint32_t lo = blob_words[base + j];
+            const uint32_t hi = (base + j + 1 < nblob) ? blob_words[base + j + 1] : 0u;
+            dst[j] = sh ? __funnelshift_r(lo, hi, sh) : lo;
+        }
+    }
+}
+
 // rows whose bit is set, in order (public compaction after an open).
 struct FlagIter {
     const uint32_t* bits;
@@ -773,6 +796,21 @@ int ogm_mask_row_tails(uint32_t* mat, int64_t rows, int64_t pitch, int64_t width
     if (rows == 0 || (width & 31) == 0) return OGM_OK;
     mask_row_tails_kernel<<<grid_for(rows), 256, 0, as_stream(stream)>>>(mat, rows, pitch, (width + 31) / 32,
                                                                          (1u << (width & 31)) - 1u);
+    OGM_LAUNCH_CHECK();
+    return OGM_OK;
+}
+
+int ogm_unpack_records(const void* blob, int64_t blob_bytes, int64_t nrec, const int64_t* src_off,
+                       const int64_t* dst_off, const int32_t* nwords, uint32_t* arena, void* stream) {
+    using namespace ogm;
+    OGM_CHECK_ARG(nrec >= 0 && blob_bytes >= 0, OGM_ERR_ARG, "negative sizes");
+    OGM_CHECK_ARG((((uintptr_t)blob) & 3) == 0, OGM_ERR_ARG, "blob must be 4-byte aligned");
+    if (nrec == 0) return OGM_OK;
+    int64_t g = (nrec + 7) / 8;
+    const int64_t cap = (int64_t)sm_count() * 16;
+    if (g > cap) g = cap;
+    unpack_records_kernel<<<(int)g, 256, 0, as_stream(stream)>>>((const uint32_t*)blob, blob_bytes, nrec, src_off,
+                                                                 dst_off, nwords, arena);
     OGM_LAUNCH_CHECK();
     return OGM_OK;
 }

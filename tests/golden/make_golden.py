@@ -412,6 +412,36 @@ def match_fixture(ref):
     np.savez_compressed(OUT / "match.npz", **out)
 
 
+def storage_fixture(ref):
+    """Reference-written files: campus schema, 3 graph shares (.ogmg), and the
+    3 result files (.ogmr) of the two-person query (src/storage.py)."""
+    import tempfile
+
+    from oblivgm.engine import EngineConfig, sec_match
+    from oblivgm.graphs import encrypt_graph, parse_graph_text
+    from oblivgm.net import local_runtimes, make_session_configs, run_trio
+    from oblivgm.query import gen_token, load_query
+    from oblivgm.storage import save_graph_share, save_results, save_schema
+
+    graph = parse_graph_text(CAMPUS.read_text())
+    rng = np.random.default_rng(1)
+    schema, shares = encrypt_graph(graph, 2, rng)
+    tokens = gen_token(load_query(TWO_PERSON.read_text(), schema), schema, rng)
+    runtimes = local_runtimes(make_session_configs(b"\x11" * 16))
+    results = run_trio(lambda rt: sec_match(rt, tokens[rt.index - 1], shares[rt.index - 1], EngineConfig()),
+                       runtimes)
+    out = {}
+    with tempfile.TemporaryDirectory() as d:
+        save_schema(f"{d}/schema.json", schema)
+        out["schema_json"] = np.frombuffer(open(f"{d}/schema.json", "rb").read(), np.uint8)
+        for p in range(3):
+            save_graph_share(f"{d}/g{p}.ogmg", shares[p])
+            out[f"ogmg{p}"] = np.frombuffer(open(f"{d}/g{p}.ogmg", "rb").read(), np.uint8)
+            save_results(f"{d}/r{p}.ogmr", results[p], schema)
+            out[f"ogmr{p}"] = np.frombuffer(open(f"{d}/r{p}.ogmr", "rb").read(), np.uint8)
+    np.savez_compressed(OUT / "storage.npz", **out)
+
+
 def main():
     sys.path.insert(0, str(REF))
     import oblivgm as ref
@@ -423,6 +453,7 @@ def main():
     engine_fixture(ref)
     shuffle_fixture(ref)
     match_fixture(ref)
+    storage_fixture(ref)
     for p in sorted(OUT.glob("*.npz")):
         print(p.name, p.stat().st_size)
 
