@@ -301,14 +301,9 @@ def run_c5(args):
 # ---------------------------------------------------------------------------
 
 
-def run_c3_pipeline(args):
-    """Root slot of the medium graph: 200K centre vertices, one-hot ids (200K
-    bits) and two needed attributes (uniform a0, n=182,083; Zipf a2, n=8,969).
-    Predicates: a0 in [lo, hi] (interval, 2 passes) AND a2 = rare value (DPF);
-    combine (1 AND); Case II fetch: shuffle of 200K rows x 391,053 bits (48.9 KB
-    per row, 9.8 GB per component -- SURVEY 8(d) C3 'feasible' row), open the
-    flags, keep the matches.  Blinds on the fly (memory-lean)."""
-    from paper_2209_03526_b200.trio import Trio, TrioGroup
+def c3p_setup(args):
+    """Root-slot shares and tokens of the C3 pipeline (seeded, on the device)."""
+    from paper_2209_03526_b200.trio import TrioGroup
 
     X = args.rows
     dev = torch.device("cuda")
@@ -342,6 +337,20 @@ def run_c3_pipeline(args):
 
     kiv, keq = split(iv), split(eq)
     group = TrioGroup(None, None, X, X, list(ids), {"a0": list(a0), "a2": list(a2)}, {"a0": n0, "a2": n2})
+    return group, kiv, keq, n0, n2, want
+
+
+def run_c3_pipeline(args):
+    """Root slot of the medium graph: 200K centre vertices, one-hot ids (200K
+    bits) and two needed attributes (uniform a0, n=182,083; Zipf a2, n=8,969).
+    Predicates: a0 in [lo, hi] (interval, 2 passes) AND a2 = rare value (DPF);
+    combine (1 AND); Case II fetch: shuffle of 200K rows x 391,053 bits (48.9 KB
+    per row, 9.8 GB per component -- SURVEY 8(d) C3 'feasible' row), open the
+    flags, keep the matches.  Blinds on the fly (memory-lean)."""
+    from paper_2209_03526_b200.trio import Trio
+
+    X = args.rows
+    group, kiv, keq, n0, n2, want = c3p_setup(args)
     phases = {}
     lat = []
     for it in range(args.warmup + args.steps):
@@ -369,8 +378,8 @@ def run_c3_pipeline(args):
                          ("fetch_offline_prep_ms", t_off - t2)):
                 phases.setdefault(k, []).append(1e3 * v)
         recs_count = recs.count
-        del recs, flags, b_iv, b_eq
-        torch.cuda.empty_cache()
+        del recs, flags, b_iv, b_eq  # buffers return to the caching allocator (warm, as in a serving loop)
+    torch.cuda.empty_cache()
     row_width = 1 + X + n0 + n2
     emit({"config": f"C3 root-slot pipeline: {X} candidates, a0 interval + a2 eq, ALL, Case II fetch of "
                     f"{row_width}-bit rows", "metric": "root_slot_latency_ms", "value": 1e3 * statistics.median(lat),

@@ -79,6 +79,12 @@ int ogm_prg_expand(const void* seeds, int64_t n, void* left, void* right, uint8_
 int ogm_prf_words(const uint8_t* key, const uint8_t* label, uint64_t index, uint64_t first_word,
                   int64_t nwords, uint32_t* out, void* stream);
 
+/* src/shuffle.py:69-73 _table: a (rows x width-bit) blinding table, row r =
+ * PRF words [r*W, r*W+W) of (key, label, index), W = ceil(width/32), tail
+ * masked; stored with row pitch `pitch` >= W words, padding zeroed. */
+int ogm_prf_rows(const uint8_t* key, const uint8_t* label, uint64_t index, int64_t rows,
+                 int64_t width_bits, int64_t pitch, uint32_t* out, void* stream);
+
 /* src/rss.py:143-148 ZeroShareContext.next_share at counter `counter`:
  * out = F(key_own, "ZSHR", counter) ^ F(key_prev, "ZSHR", counter), masked to
  * nbits.  If `xor_into` is non-NULL the share is XORed into it and the
@@ -186,6 +192,20 @@ int ogm_select_many(int64_t K, int64_t X, int64_t words, int64_t pitch, const ui
  * tail).  flag_bits (rows bits) may be NULL. */
 int ogm_pack_fields(int64_t rows, const uint32_t* flag_bits, int nfields, const uint32_t* const* fields,
                     const int64_t* fpitch, const int64_t* fwidth, uint32_t* out, int64_t opitch,
+                    void* stream);
+
+/* src/engine.py:227-233 (Case II row layout) fused with the first gather of
+ * the shuffle that consumes those rows (src/shuffle.py:106-118):
+ *   out[i] = XOR over s < nsets of pack(flag_s, fields_s)[src] ^ r_mat[i],
+ *   src = idx ? idx[i] : i
+ * flag_bits is NULL (rows without a flag bit) or nsets bit vectors; fields
+ * and fpitch are nsets x nfields, set-major; fwidth has nfields entries;
+ * r_mat (pitch opitch) may be NULL.  nsets = 2 emits a^b of two share
+ * components, so a party's first shuffle step never materialises its packed
+ * rows.  nsets = 1, idx = r_mat = NULL is ogm_pack_fields. */
+int ogm_pack_gather(int64_t rows, const int32_t* idx, int nsets, const uint32_t* const* flag_bits,
+                    int nfields, const uint32_t* const* fields, const int64_t* fpitch,
+                    const int64_t* fwidth, const uint32_t* r_mat, uint32_t* out, int64_t opitch,
                     void* stream);
 
 /* src/engine.py:249-269 / :331-334 field slicing: out[k] = bits

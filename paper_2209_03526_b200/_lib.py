@@ -38,6 +38,7 @@ SIGNATURES = {
     "ogm_abi_version": ([], _int),
     "ogm_init": ([], _int),
     "ogm_prg_expand": ([_vp, _i64, _vp, _vp, _vp, _vp, _vp, _vp], _int),
+    "ogm_prf_rows": ([_cp, _cp, _u64, _i64, _i64, _i64, _vp, _vp], _int),
     "ogm_prf_words": ([_cp, _cp, _u64, _u64, _i64, _vp, _vp], _int),
     "ogm_zero_share": ([_cp, _cp, _u64, _i64, _vp, _vp, _vp], _int),
     "ogm_zero_share_slice": ([_cp, _cp, _u64, _i64, _u64, _i64, _vp, _vp, _vp], _int),
@@ -54,6 +55,7 @@ SIGNATURES = {
     "ogm_select_fold": ([_i64, _i64, _i64, _int, _vp, _vp, _vp, _vp, _vp, _vp], _int),
     "ogm_select_many": ([_i64, _i64, _i64, _i64, _vp, _vp, _i64, _vp, _vp, _vp, _i64, _vp, _vp], _int),
     "ogm_pack_fields": ([_i64, _vp, _int, _vp, _vp, _vp, _vp, _i64, _vp], _int),
+    "ogm_pack_gather": ([_i64, _vp, _int, _vp, _int, _vp, _vp, _vp, _vp, _vp, _i64, _vp], _int),
     "ogm_extract_field": ([_vp, _i64, _vp, _i64, _i64, _i64, _vp, _i64, _vp], _int),
     "ogm_mask_row_tails": ([_vp, _i64, _i64, _i64, _vp], _int),
     "ogm_unpack_records": ([_vp, _i64, _i64, _vp, _vp, _vp, _vp, _vp], _int),

@@ -336,19 +336,31 @@ __global__ void select_fold_kernel(const FoldArgs a) {
 }
 
 // ---------------------------------------------------------------------------
-// Bit-granular row packing (src/engine.py:227-233, 317-318): row r of the
-// output is flag(r) || field_0[r] || field_1[r] ... with each field's
-// logical width, packed LE with a clean tail.  Thread per (row, out word).
+// Bit-granular row packing (src/engine.py:227-233, 317-318), fused with the
+// first gather of the shuffle that consumes the rows (src/shuffle.py:106-118):
+//
+//   out[i] = XOR_s ( flag_s[src] || field_s0[src] || field_s1[src] ... ) ^ R[i]
+//   src = idx ? idx[i] : i
+//
+// Each field keeps its logical width; rows are packed LE with a clean tail
+// and zero padding up to the output pitch.  With s over two share
+// components the kernel emits a^b directly, and with idx = the party's
+// composed permutation it is the party's first shuffle step -- the packed
+// rows never round-trip through HBM.
 // ---------------------------------------------------------------------------
 constexpr int kMaxFields = 8;
+constexpr int kMaxSets = 3;
 
 struct PackArgs {
-    const uint32_t* flag;  // bit vector (rows bits) for bit 0, or null
-    const uint32_t* f[kMaxFields];
-    int64_t fpitch[kMaxFields];
+    const int32_t* idx;
+    const uint32_t* flag[kMaxSets];  // bit vectors (bit 0 of each row), all null if the rows carry no flag
+    const uint32_t* f[kMaxSets][kMaxFields];
+    int64_t fpitch[kMaxSets][kMaxFields];
     int64_t fwidth[kMaxFields];
     int64_t foff[kMaxFields];
-    int nfields;
+    int nsets, nfields;
+    int vec_fields;  // every field row is 16-B aligned with a 16-B pitch
+    const uint32_t* r;  // XORed rows (pitch opitch) or null
     uint32_t* out;
     int64_t opitch, owidth, rows;
 };
@@ -364,55 +376,176 @@ __device__ __forceinline__ uint32_t field_bits32(const uint32_t* row, int64_t wi
     return sh ? __funnelshift_r(lo, hi, sh) : lo;
 }
 
-__device__ __forceinline__ uint32_t pack_word(const PackArgs& a, int64_t r, int64_t k, int64_t ow);
-
-// wide rows: one CTA per row (grid-stride over rows), threads over words;
-// with a 16-B output pitch each thread emits a 128-bit group
-__global__ void pack_fields_rows_kernel(const PackArgs a) {
-    const int64_t ow = (a.owidth + 31) >> 5;
-    if ((a.opitch & 3) == 0 && (((uintptr_t)a.out) & 15) == 0) {
-        const int64_t ng = a.opitch >> 2;
-        for (int64_t r = blockIdx.x; r < a.rows; r += gridDim.x)
-            for (int64_t gi = threadIdx.x; gi < ng; gi += blockDim.x) {
-                const int64_t k = gi << 2;
-                uint4 v = make_uint4(pack_word(a, r, k, ow), pack_word(a, r, k + 1, ow), pack_word(a, r, k + 2, ow),
-                                     pack_word(a, r, k + 3, ow));
-                reinterpret_cast<uint4*>(a.out + r * a.opitch)[gi] = v;
-            }
-        return;
+// output word k of source row src (any position: flag, field boundaries, tail)
+__device__ __forceinline__ uint32_t pack_word(const PackArgs& a, int64_t src, int64_t k, int64_t ow) {
+    if (k >= ow) return 0;
+    uint32_t v = 0;
+    const int64_t lo = k * 32;
+    for (int s = 0; s < a.nsets; s++) {
+        if (lo == 0 && a.flag[s]) v ^= (__ldg(a.flag[s] + (src >> 5)) >> (src & 31)) & 1u;
+        for (int f = 0; f < a.nfields; f++) {
+            const int64_t o = a.foff[f], wdt = a.fwidth[f];
+            if (o >= lo + 32 || o + wdt <= lo) continue;
+            const uint32_t bits = field_bits32(a.f[s][f] + src * a.fpitch[s][f], wdt, lo - o);
+            // keep only positions inside [o, o+wdt) of this word
+            const int64_t b0 = o > lo ? o - lo : 0;
+            const int64_t b1 = (o + wdt < lo + 32) ? o + wdt - lo : 32;
+            const uint32_t m = (b1 - b0 >= 32) ? 0xffffffffu : (((1u << (b1 - b0)) - 1u) << b0);
+            v ^= bits & m;
+        }
     }
-    for (int64_t r = blockIdx.x; r < a.rows; r += gridDim.x)
-        for (int64_t k = threadIdx.x; k < a.opitch; k += blockDim.x) a.out[r * a.opitch + k] = pack_word(a, r, k, ow);
+    return v;
 }
 
-__global__ void pack_fields_kernel(const PackArgs a) {
+template <int D>
+__device__ __forceinline__ void take4(const uint32_t w[8], int sh, uint32_t o[4]) {
+#pragma unroll
+    for (int j = 0; j < 4; j++) o[j] ^= __funnelshift_r(w[D + j], w[D + j + 1], sh);
+}
+
+// output words [4c, 4c+4) of source row src
+__device__ __forceinline__ void pack_chunk(const PackArgs& a, int64_t src, int64_t c, int64_t ow, uint32_t o[4]) {
+    const int64_t b = c * 128;
+    int f = -1;
+    for (int g = 0; g < a.nfields; g++)
+        if (a.foff[g] <= b && b + 128 <= a.foff[g] + a.fwidth[g]) f = g;
+    o[0] = o[1] = o[2] = o[3] = 0;
+    if (f < 0) {  // flag word, field boundary or tail: word by word
+#pragma unroll
+        for (int j = 0; j < 4; j++) o[j] = pack_word(a, src, 4 * c + j, ow);
+        return;
+    }
+    // interior of one field: 4 output words = a funnel shift of 5 field words
+    const int64_t s0 = b - a.foff[f];
+    const int64_t q = s0 >> 5;
+    const int sh = (int)(s0 & 31);
+    const int d = (int)(q & 3);  // uniform across a warp inside one field
+    const int64_t nw = (a.fwidth[f] + 31) >> 5;
+    for (int s = 0; s < a.nsets; s++) {
+        const uint32_t* row = a.f[s][f] + src * a.fpitch[s][f];
+        uint32_t w[8];
+        if (a.vec_fields) {
+            const uint4 x = __ldg(reinterpret_cast<const uint4*>(row + (q - d)));
+            w[0] = x.x; w[1] = x.y; w[2] = x.z; w[3] = x.w;
+            if (d || sh) {
+                const uint4 y = __ldg(reinterpret_cast<const uint4*>(row + (q - d) + 4));
+                w[4] = y.x; w[5] = y.y; w[6] = y.z; w[7] = y.w;
+            } else {
+                w[4] = w[5] = w[6] = w[7] = 0;
+            }
+            switch (d) {
+                case 0: take4<0>(w, sh, o); break;
+                case 1: take4<1>(w, sh, o); break;
+                case 2: take4<2>(w, sh, o); break;
+                default: take4<3>(w, sh, o); break;
+            }
+        } else {
+#pragma unroll
+            for (int j = 0; j < 4; j++) w[j] = __ldg(row + q + j);
+            w[4] = (sh && q + 4 < nw) ? __ldg(row + q + 4) : 0;
+            take4<0>(w, sh, o);
+        }
+    }
+}
+
+// the field whose interior holds output bits [128c, 128c+128), or -1
+__device__ __forceinline__ int interior_field(const PackArgs& a, int64_t c) {
+    const int64_t b = c * 128;
+    int f = -1;
+    for (int g = 0; g < a.nfields; g++)
+        if (a.foff[g] <= b && b + 128 <= a.foff[g] + a.fwidth[g]) f = g;
+    return f;
+}
+
+// wide rows, NS share sets with 16-B aligned field rows: a CTA walks rows;
+// each thread issues every load of two 128-bit output groups (field words
+// of all sets + the XORed row) before it computes either, so twice the
+// bytes are in flight per warp.  NS = 0: unaligned fields, generic loads.
+template <int NS>
+__global__ void __launch_bounds__(256) pack_gather_rows_kernel(const PackArgs a) {
+    const int64_t ow = (a.owidth + 31) >> 5;
+    const int64_t ng = a.opitch >> 2;
+    const int bd = blockDim.x;
+    for (int64_t i = blockIdx.x; i < a.rows; i += gridDim.x) {
+        const int64_t src = a.idx ? (int64_t)__ldg(a.idx + i) : i;
+        uint4* orow = reinterpret_cast<uint4*>(a.out + i * a.opitch);
+        const uint4* rrow = a.r ? reinterpret_cast<const uint4*>(a.r + i * a.opitch) : nullptr;
+        if constexpr (NS == 0) {
+            for (int64_t c = threadIdx.x; c < ng; c += bd) {
+                uint32_t o[4];
+                pack_chunk(a, src, c, ow, o);
+                uint4 v = make_uint4(o[0], o[1], o[2], o[3]);
+                if (rrow) v = xor4(v, __ldcs(rrow + c));
+                orow[c] = v;
+            }
+        } else {
+            for (int64_t c0 = threadIdx.x; c0 < ng; c0 += 2 * bd) {
+                int64_t cc[2] = {c0, c0 + bd};
+                int fu[2], shu[2], du[2];
+                uint4 rv[2], A[2][NS], B[2][NS];
+#pragma unroll
+                for (int u = 0; u < 2; u++) {
+                    const bool valid = cc[u] < ng;
+                    rv[u] = (rrow && valid) ? __ldcs(rrow + cc[u]) : make_uint4(0, 0, 0, 0);
+                    const int f = valid ? interior_field(a, cc[u]) : -1;
+                    fu[u] = valid ? f : -2;
+                    int64_t base = 0;
+                    shu[u] = du[u] = 0;
+                    if (f >= 0) {
+                        const int64_t s0 = cc[u] * 128 - a.foff[f];
+                        const int64_t q = s0 >> 5;
+                        shu[u] = (int)(s0 & 31);
+                        du[u] = (int)(q & 3);
+                        base = q - du[u];
+                    }
+#pragma unroll
+                    for (int s = 0; s < NS; s++) {
+                        A[u][s] = B[u][s] = make_uint4(0, 0, 0, 0);
+                        if (f >= 0) {
+                            const uint4* row = reinterpret_cast<const uint4*>(a.f[s][f] + src * a.fpitch[s][f] + base);
+                            A[u][s] = __ldcs(row);
+                            if (du[u] || shu[u]) B[u][s] = __ldcs(row + 1);
+                        }
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < 2; u++) {
+                    if (fu[u] == -2) continue;
+                    uint32_t o[4] = {0, 0, 0, 0};
+                    if (fu[u] < 0) {
+#pragma unroll
+                        for (int j = 0; j < 4; j++) o[j] = pack_word(a, src, 4 * cc[u] + j, ow);
+                    } else {
+#pragma unroll
+                        for (int s = 0; s < NS; s++) {
+                            const uint32_t w[8] = {A[u][s].x, A[u][s].y, A[u][s].z, A[u][s].w,
+                                                   B[u][s].x, B[u][s].y, B[u][s].z, B[u][s].w};
+                            switch (du[u]) {
+                                case 0: take4<0>(w, shu[u], o); break;
+                                case 1: take4<1>(w, shu[u], o); break;
+                                case 2: take4<2>(w, shu[u], o); break;
+                                default: take4<3>(w, shu[u], o); break;
+                            }
+                        }
+                    }
+                    orow[cc[u]] = xor4(make_uint4(o[0], o[1], o[2], o[3]), rv[u]);
+                }
+            }
+        }
+    }
+}
+
+// narrow or unaligned rows: thread per (row, output word)
+__global__ void pack_gather_kernel(const PackArgs a) {
     const int64_t total = a.rows * a.opitch;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     const int64_t ow = (a.owidth + 31) >> 5;
     for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += stride) {
-        const int64_t r = t / a.opitch, k = t % a.opitch;
-        a.out[r * a.opitch + k] = pack_word(a, r, k, ow);
-    }
-}
-
-__device__ __forceinline__ uint32_t pack_word(const PackArgs& a, int64_t r, int64_t k, int64_t ow) {
-    {
-        uint32_t v = 0;
-        if (k < ow) {
-            const int64_t lo = k * 32;
-            if (a.flag && lo == 0) v |= (a.flag[r >> 5] >> (r & 31)) & 1u;
-            for (int f = 0; f < a.nfields; f++) {
-                const int64_t o = a.foff[f], wdt = a.fwidth[f];
-                if (o >= lo + 32 || o + wdt <= lo) continue;
-                uint32_t bits = field_bits32(a.f[f] + r * a.fpitch[f], wdt, lo - o);
-                // keep only positions inside [o, o+wdt) of this word
-                const int64_t b0 = o > lo ? o - lo : 0;
-                const int64_t b1 = (o + wdt < lo + 32) ? o + wdt - lo : 32;
-                uint32_t m = (b1 - b0 >= 32) ? 0xffffffffu : (((1u << (b1 - b0)) - 1u) << b0);
-                v |= bits & m;
-            }
-        }
-        return v;
+        const int64_t i = t / a.opitch, k = t - i * a.opitch;
+        const int64_t src = a.idx ? (int64_t)__ldg(a.idx + i) : i;
+        uint32_t v = pack_word(a, src, k, ow);
+        if (a.r) v ^= a.r[t];
+        a.out[t] = v;
     }
 }
 
@@ -739,37 +872,73 @@ int ogm_select_fold(int64_t rows, int64_t words, int64_t pitch, int nparty, cons
     return OGM_OK;
 }
 
-int ogm_pack_fields(int64_t rows, const uint32_t* flag_bits, int nfields, const uint32_t* const* fields,
-                    const int64_t* fpitch, const int64_t* fwidth, uint32_t* out, int64_t opitch,
-                    void* stream) {
+static int pack_launch(int64_t rows, const int32_t* idx, int nsets, const uint32_t* const* flag_bits, int nfields,
+                       const uint32_t* const* fields, const int64_t* fpitch, const int64_t* fwidth,
+                       const uint32_t* r_mat, uint32_t* out, int64_t opitch, void* stream) {
     using namespace ogm;
     OGM_CHECK_ARG(nfields >= 0 && nfields <= kMaxFields, OGM_ERR_ARG, "at most %d fields", kMaxFields);
+    OGM_CHECK_ARG(nsets >= 1 && nsets <= kMaxSets, OGM_ERR_ARG, "1..%d share sets", kMaxSets);
+    OGM_CHECK_ARG(rows >= 0 && opitch >= 0, OGM_ERR_ARG, "negative sizes");
     PackArgs a{};
     int64_t off = flag_bits ? 1 : 0;
+    bool vec = true;
     for (int f = 0; f < nfields; f++) {
-        a.f[f] = fields[f];
-        a.fpitch[f] = fpitch[f];
+        OGM_CHECK_ARG(fwidth[f] >= 0, OGM_ERR_ARG, "negative field width");
         a.fwidth[f] = fwidth[f];
         a.foff[f] = off;
         off += fwidth[f];
+        for (int s = 0; s < nsets; s++) {
+            const uint32_t* p = fields[s * nfields + f];
+            const int64_t fp = fpitch[s * nfields + f];
+            OGM_CHECK_ARG(fp >= (fwidth[f] + 31) / 32, OGM_ERR_ARG, "field %d pitch below its width", f);
+            a.f[s][f] = p;
+            a.fpitch[s][f] = fp;
+            vec = vec && (((uintptr_t)p) & 15) == 0 && (fp & 3) == 0;
+        }
     }
     OGM_CHECK_ARG(opitch >= (off + 31) / 32, OGM_ERR_ARG, "output pitch too small for %lld bits",
                   (long long)off);
-    if (rows == 0) return OGM_OK;
-    a.flag = flag_bits;
+    if (rows == 0 || opitch == 0) return OGM_OK;
+    OGM_ENSURE_INIT();
+    for (int s = 0; s < nsets; s++) {
+        a.flag[s] = flag_bits ? flag_bits[s] : nullptr;
+        OGM_CHECK_ARG(!flag_bits || a.flag[s], OGM_ERR_ARG, "flag vector %d missing", s);
+    }
+    a.idx = idx;
+    a.nsets = nsets;
     a.nfields = nfields;
+    a.vec_fields = vec ? 1 : 0;
+    a.r = r_mat;
     a.out = out;
     a.opitch = opitch;
     a.owidth = off;
     a.rows = rows;
-    if (opitch >= 256) {
+    const bool wide = opitch >= 64 && (opitch & 3) == 0 && (((uintptr_t)out | (uintptr_t)r_mat) & 15) == 0;
+    if (wide) {
         int64_t g = rows < (int64_t)sm_count() * 8 ? rows : (int64_t)sm_count() * 8;
-        pack_fields_rows_kernel<<<(int)g, 256, 0, as_stream(stream)>>>(a);
+        const int ns = vec ? nsets : 0;
+        auto kern = ns == 1 ? pack_gather_rows_kernel<1> : ns == 2 ? pack_gather_rows_kernel<2>
+                  : ns == 3 ? pack_gather_rows_kernel<3> : pack_gather_rows_kernel<0>;
+        kern<<<(int)g, 256, 0, as_stream(stream)>>>(a);
     } else {
-        pack_fields_kernel<<<grid_for(rows * opitch), 256, 0, as_stream(stream)>>>(a);
+        pack_gather_kernel<<<grid_for(rows * opitch), 256, 0, as_stream(stream)>>>(a);
     }
     OGM_LAUNCH_CHECK();
     return OGM_OK;
+}
+
+int ogm_pack_fields(int64_t rows, const uint32_t* flag_bits, int nfields, const uint32_t* const* fields,
+                    const int64_t* fpitch, const int64_t* fwidth, uint32_t* out, int64_t opitch,
+                    void* stream) {
+    const uint32_t* flags[1] = {flag_bits};
+    return pack_launch(rows, nullptr, 1, flag_bits ? flags : nullptr, nfields, fields, fpitch, fwidth, nullptr, out,
+                       opitch, stream);
+}
+
+int ogm_pack_gather(int64_t rows, const int32_t* idx, int nsets, const uint32_t* const* flag_bits, int nfields,
+                    const uint32_t* const* fields, const int64_t* fpitch, const int64_t* fwidth,
+                    const uint32_t* r_mat, uint32_t* out, int64_t opitch, void* stream) {
+    return pack_launch(rows, idx, nsets, flag_bits, nfields, fields, fpitch, fwidth, r_mat, out, opitch, stream);
 }
 
 int ogm_extract_field(const uint32_t* src, int64_t spitch, const int32_t* idx, int64_t n, int64_t bit_offset,

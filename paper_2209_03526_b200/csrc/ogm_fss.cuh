@@ -266,6 +266,44 @@ __global__ void __launch_bounds__(kFssThreads) prf_words_kernel(
     }
 }
 
+// ---------------------------------------------------------------------------
+// src/shuffle.py:69-73 blinding table as pitched rows: row r = PRF stream
+// words [r*W, r*W + W) of (key, label, index), tail masked to the logical
+// width, stored at `pitch` >= W words with zero padding.  One thread per
+// 16-byte CTR block whatever W's alignment, so the AES rate is the bound
+// (generating such rows inside a 4-word-chunked gather costs up to two AES
+// blocks per chunk when W is not a multiple of 4).
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(kFssThreads) prf_rows_kernel(AesKeySched k, uint32_t label_be, uint64_t index,
+                                                               int64_t rows, int64_t W, uint32_t tail,
+                                                               int64_t pitch, uint32_t* __restrict__ out) {
+    OGM_AES_PROLOGUE();
+    const int64_t nblk = (rows * W + 3) >> 2;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t blk = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; blk < nblk; blk += stride) {
+        const uint4 ks = aes128_enc(T, ctr_block(label_be, index, (uint64_t)blk), ParamKey{k.rk});
+        const uint32_t kw[4] = {ks.x, ks.y, ks.z, ks.w};
+        int64_t r = (blk * 4) / W;
+        int64_t col = blk * 4 - r * W;
+#pragma unroll
+        for (int j = 0; j < 4; j++) {
+            if (r < rows) {
+                uint32_t* row = out + r * pitch;
+                if (col == W - 1) {
+                    row[col] = kw[j] & tail;
+                    for (int64_t p = W; p < pitch; p++) row[p] = 0;
+                } else {
+                    row[col] = kw[j];
+                }
+            }
+            if (++col == W) {
+                col = 0;
+                r++;
+            }
+        }
+    }
+}
+
 int fss_init() {
     OGM_CUDA_TRY(allow_big_smem(prg_expand_kernel, kAesTableBytes));
     OGM_CUDA_TRY(allow_big_smem(fss_gen_kernel<false>, kAesTableBytes));
@@ -276,6 +314,7 @@ int fss_init() {
     OGM_CUDA_TRY(allow_big_smem(fss_fde_kernel<true>, kAesTableBytes));
     OGM_CUDA_TRY(allow_big_smem(prf_words_kernel<false>, kAesTableBytes));
     OGM_CUDA_TRY(allow_big_smem(prf_words_kernel<true>, kAesTableBytes));
+    OGM_CUDA_TRY(allow_big_smem(prf_rows_kernel, kAesTableBytes));
     return OGM_OK;
 }
 

@@ -55,6 +55,22 @@ int ogm_prf_words(const uint8_t* key, const uint8_t* label, uint64_t index, uint
     return OGM_OK;
 }
 
+int ogm_prf_rows(const uint8_t* key, const uint8_t* label, uint64_t index, int64_t rows, int64_t width_bits,
+                 int64_t pitch, uint32_t* out, void* stream) {
+    OGM_CHECK_ARG(key && label && out, OGM_ERR_ARG, "PRF key, label and output are required");
+    OGM_CHECK_ARG(rows >= 0 && width_bits >= 0, OGM_ERR_ARG, "negative table shape");
+    const int64_t W = (width_bits + 31) / 32;
+    OGM_CHECK_ARG(pitch >= W, OGM_ERR_ARG, "pitch %lld below %lld words", (long long)pitch, (long long)W);
+    if (rows == 0 || W == 0) return OGM_OK;
+    OGM_ENSURE_INIT();
+    AesKeySched k = make_sched(key);
+    const uint32_t tail = (width_bits & 31) ? ((1u << (width_bits & 31)) - 1u) : 0xffffffffu;
+    prf_rows_kernel<<<aes_grid((rows * W + 3) / 4), kFssThreads, kAesTableBytes, as_stream(stream)>>>(
+        k, label_be(label), index, rows, W, tail, pitch, out);
+    OGM_LAUNCH_CHECK();
+    return OGM_OK;
+}
+
 int ogm_zero_share(const uint8_t* key_own, const uint8_t* key_prev, uint64_t counter, int64_t nbits,
                    const uint32_t* xor_into, uint32_t* out, void* stream) {
     OGM_CHECK_ARG(key_own && key_prev, OGM_ERR_ARG, "zero-share keys are required");

@@ -231,6 +231,77 @@ __global__ void __launch_bounds__(kAesThreads) shuffle_gather_kernel(const Gathe
     }
 }
 
+// The same step when every term is a precomputed matrix (the online phase
+// after ShuffleOffline, and the wide-row material build): no AES tables, so
+// a lean kernel with high occupancy for the random 16-byte row reads of
+// narrow tables, and a row-per-CTA streaming loop for wide rows.
+__device__ __forceinline__ uint4 ld_term(const uint32_t* m, int64_t row, int64_t pitch, int64_t c) {
+    return m ? __ldcs(reinterpret_cast<const uint4*>(m + row * pitch) + c) : make_uint4(0, 0, 0, 0);
+}
+
+__global__ void __launch_bounds__(256) gather_matrix_rows_kernel(const GatherArgs a, int64_t nch) {
+    const uint32_t* T1 = a.t1.on ? a.t1.mat : nullptr;
+    const uint32_t* T2 = a.t2.on ? a.t2.mat : nullptr;
+    const uint32_t* R = a.r.on ? a.r.mat : nullptr;
+    {
+        // wide rows: row indices and bases once per row, then 128-bit streams;
+        // every load of two groups is issued before either store
+        const int bd = blockDim.x;
+        for (int64_t i = blockIdx.x; i < a.rows; i += gridDim.x) {
+            const int64_t k2 = a.P2 ? (int64_t)__ldg(a.P2 + i) : i;
+            const int64_t k1 = a.P1 ? (int64_t)__ldg(a.P1 + k2) : k2;
+            uint4* o = reinterpret_cast<uint4*>(a.out + i * a.pitch);
+            for (int64_t c0 = threadIdx.x; c0 < nch; c0 += 2 * bd) {
+                const int64_t c1 = c0 + bd;
+                const bool v1 = c1 < nch;
+                uint4 x0 = xor4(xor4(ld_term(a.M1, k1, a.pitch, c0), ld_term(a.M2, k1, a.pitch, c0)),
+                                xor4(ld_term(a.M3, i, a.pitch, c0), ld_term(T1, k1, a.pitch, c0)));
+                x0 = xor4(x0, xor4(ld_term(T2, k2, a.pitch, c0), ld_term(R, i, a.pitch, c0)));
+                uint4 x1 = make_uint4(0, 0, 0, 0);
+                if (v1) {
+                    x1 = xor4(xor4(ld_term(a.M1, k1, a.pitch, c1), ld_term(a.M2, k1, a.pitch, c1)),
+                              xor4(ld_term(a.M3, i, a.pitch, c1), ld_term(T1, k1, a.pitch, c1)));
+                    x1 = xor4(x1, xor4(ld_term(T2, k2, a.pitch, c1), ld_term(R, i, a.pitch, c1)));
+                }
+                o[c0] = x0;
+                if (v1) o[c1] = x1;
+            }
+        }
+    }
+}
+
+__global__ void __launch_bounds__(256) gather_matrix_kernel(const GatherArgs a, int64_t nch, int vec) {
+    const uint32_t* T1 = a.t1.on ? a.t1.mat : nullptr;
+    const uint32_t* T2 = a.t2.on ? a.t2.mat : nullptr;
+    const uint32_t* R = a.r.on ? a.r.mat : nullptr;
+    const int64_t total = a.rows * nch;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += stride) {
+        const int64_t i = t / nch, c = t - i * nch;
+        const int64_t k2 = a.P2 ? (int64_t)__ldg(a.P2 + i) : i;
+        const int64_t k1 = a.P1 ? (int64_t)__ldg(a.P1 + k2) : k2;
+        if (vec) {
+            uint4 x = xor4(xor4(ld_term(a.M1, k1, a.pitch, c), ld_term(a.M2, k1, a.pitch, c)),
+                           xor4(ld_term(a.M3, i, a.pitch, c), ld_term(T1, k1, a.pitch, c)));
+            x = xor4(x, xor4(ld_term(T2, k2, a.pitch, c), ld_term(R, i, a.pitch, c)));
+            reinterpret_cast<uint4*>(a.out + i * a.pitch)[c] = x;
+        } else {
+            const int nw = (int)min((int64_t)4, a.W - 4 * c);
+            for (int j = 0; j < nw; j++) {
+                const int64_t w = 4 * c + j;
+                uint32_t x = 0;
+                if (a.M1) x ^= a.M1[k1 * a.pitch + w];
+                if (a.M2) x ^= a.M2[k1 * a.pitch + w];
+                if (a.M3) x ^= a.M3[i * a.pitch + w];
+                if (T1) x ^= T1[k1 * a.pitch + w];
+                if (T2) x ^= T2[k2 * a.pitch + w];
+                if (R) x ^= R[i * a.pitch + w];
+                a.out[i * a.pitch + w] = x;
+            }
+        }
+    }
+}
+
 // out[i] = inner[outer[i]]: the composition a party precomputes offline for
 // the two permutations it knows (pi12 o pi31 at P1, pi31 o pi23 at P3).
 __global__ void perm_compose_kernel(const int32_t* __restrict__ outer, const int32_t* __restrict__ inner,
@@ -538,10 +609,17 @@ int ogm_shuffle_gather(int64_t rows, int64_t words, int64_t width_bits, const in
     if (online) {
         shuffle_gather_kernel<true><<<aes_grid(work), kAesThreads, kAesTableBytes, st>>>(a);
     } else {
-        int64_t g = (work + kAesThreads - 1) / kAesThreads;
+        const bool vec = (a.pitch & 3) == 0 &&
+                         ((((uintptr_t)a.M1) | ((uintptr_t)a.M2) | ((uintptr_t)a.M3) | ((uintptr_t)a.out) |
+                           ((uintptr_t)a.t1.mat) | ((uintptr_t)a.t2.mat) | ((uintptr_t)a.r.mat)) & 15) == 0;
+        const int64_t nch = vec ? (a.pitch >> 2) : ((a.W + 3) >> 2);
         const int64_t cap = (int64_t)sm_count() * 8;
+        int64_t g = (vec && nch >= 64) ? rows : (rows * nch + 255) / 256;
         if (g > cap) g = cap;
-        shuffle_gather_kernel<false><<<(int)(g < 1 ? 1 : g), kAesThreads, 0, st>>>(a);
+        if (vec && nch >= 64)
+            gather_matrix_rows_kernel<<<(int)(g < 1 ? 1 : g), 256, 0, st>>>(a, nch);
+        else
+            gather_matrix_kernel<<<(int)(g < 1 ? 1 : g), 256, 0, st>>>(a, nch, vec ? 1 : 0);
     }
     OGM_LAUNCH_CHECK();
     return OGM_OK;

@@ -58,6 +58,19 @@ def _as_pitched(m: torch.Tensor, width: int) -> torch.Tensor:
 
 
 @dataclass
+class PackedRows:
+    """The three share components of a match table (src/engine.py:227-233:
+    flag bit, then each field at its logical width), described by their
+    fields instead of materialised.  The shuffle packs them inside its first
+    gathers (ogm_pack_gather), so the packed rows never round-trip HBM."""
+
+    rows: int
+    width: int
+    flags: list | None            # [f1, f2, f3] bit vectors, or None (no flag bit)
+    fields: list                  # [([x1, x2, x3], width), ...]
+
+
+@dataclass
 class TrioGroup:
     """Candidate group with its three share components per field."""
 
@@ -183,22 +196,46 @@ class Trio:
         tid = self.table_id
         s12, s23, s31 = self.s12, self.s23, self.s31
         pi12, pi23, pi31 = _perm(s12, tid, rows), _perm(s23, tid, rows), _perm(s31, tid, rows)
-
-        def tab():
-            return torch.empty((rows, _pitch(width)), dtype=torch.int32, device=self.dev)
-
-        bt = (LABEL_BLIND, tid)
-        m = {"pi12": pi12, "pi23": pi23, "k1": compose(pi31, pi12), "k3": compose(pi23, pi31),
-             "u": gather(rows, width, tab(), outer=pi31, inner=pi12, t1=(s12, *bt), t2=(s31, *bt)),
-             "v": gather(rows, width, tab(), inner=pi12, t1=(s12, *bt)),
-             "w": gather(rows, width, tab(), inner=pi23, t1=(s23, *bt), r=(s12, LABEL_RAND, tid)),
-             "z": gather(rows, width, tab(), outer=pi23, inner=pi31, t1=(s31, *bt), t2=(s23, *bt),
-                         r=(s31, LABEL_RAND, tid)),
-             "r1": gather(rows, width, tab(), r=(s31, LABEL_RAND, tid)),
-             "r2": gather(rows, width, tab(), r=(s12, LABEL_RAND, tid))}
+        m = self._material(tid, rows, width, pi12, pi23, pi31)
         if not hasattr(self, "_prepared"):
             self._prepared = {}
         self._prepared[(tid, rows, width)] = m
+
+    def _material(self, tid: int, rows: int, width: int, pi12, pi23, pi31) -> dict:
+        """The data-independent blinds of one shuffle, permuted and combined
+        along each party's gather path (shuffle.ShuffleOffline):
+        U = T12[k1] ^ T31[pi31], V = T12[pi12], W = T23[pi23] ^ R2,
+        Z = T31[k3] ^ T23[pi23] ^ R1, plus R1, R2.  Narrow rows generate the
+        T rows inside the gathers (a 16-B row is one AES block); wide rows
+        generate each table once at the AES rate (ogm_prf_rows) and combine
+        whole rows with streaming gathers."""
+        s12, s23, s31 = self.s12, self.s23, self.s31
+        P = _pitch(width)
+
+        def tab():
+            return torch.empty((rows, P), dtype=torch.int32, device=self.dev)
+
+        m = {"pi12": pi12, "pi23": pi23, "k1": compose(pi31, pi12), "k3": compose(pi23, pi31)}
+        if words_for(width) >= 64:
+            def table(seed, label):
+                return blind_table(seed, label, tid, rows, width, self.dev, pitch=P)
+
+            t12, t31, t23 = table(s12, LABEL_BLIND), table(s31, LABEL_BLIND), table(s23, LABEL_BLIND)
+            m["r1"], m["r2"] = table(s31, LABEL_RAND), table(s12, LABEL_RAND)
+            m["u"] = gather(rows, width, tab(), outer=pi31, inner=pi12, t1=t12, t2=t31)
+            m["v"] = gather(rows, width, tab(), inner=pi12, t1=t12)
+            m["w"] = gather(rows, width, tab(), inner=pi23, t1=t23, r=m["r2"])
+            m["z"] = gather(rows, width, tab(), outer=pi23, inner=pi31, t1=t31, t2=t23, r=m["r1"])
+            return m
+        bt = (LABEL_BLIND, tid)
+        m["u"] = gather(rows, width, tab(), outer=pi31, inner=pi12, t1=(s12, *bt), t2=(s31, *bt))
+        m["v"] = gather(rows, width, tab(), inner=pi12, t1=(s12, *bt))
+        m["w"] = gather(rows, width, tab(), inner=pi23, t1=(s23, *bt), r=(s12, LABEL_RAND, tid))
+        m["z"] = gather(rows, width, tab(), outer=pi23, inner=pi31, t1=(s31, *bt), t2=(s23, *bt),
+                        r=(s31, LABEL_RAND, tid))
+        m["r1"] = gather(rows, width, tab(), r=(s31, LABEL_RAND, tid))
+        m["r2"] = gather(rows, width, tab(), r=(s12, LABEL_RAND, tid))
+        return m
 
     def shuffle(self, comps: list, width: int, online_blinds: bool | None = None) -> list:
         """src/shuffle.py:80-144 for the three parties: each permutation and
@@ -206,8 +243,11 @@ class Trio:
         ``online_blinds`` generates the blinding tables inside the gathers
         (AES-CTR on the fly) instead of materialising them -- the memory-lean
         mode for wide rows (default: on for tables above 4 GiB)."""
-        rows = comps[0].shape[0]
-        comps = [_as_pitched(c, width) for c in comps]
+        if isinstance(comps, PackedRows):
+            rows = comps.rows
+        else:
+            rows = comps[0].shape[0]
+            comps = [_as_pitched(c, width) for c in comps]
         tid = self.table_id
         self.table_id += 1
         prep = getattr(self, "_prepared", {}).pop((tid, rows, width), None)
@@ -223,48 +263,58 @@ class Trio:
         if online_blinds is None:
             online_blinds = rows * words_for(width) * 4 > (4 << 30)
         if online_blinds:
-            ab = torch.empty_like(comps[0])
-            _lib.call("ogm_xor_words", ab.numel(), _lib.ptr(comps[0]), _lib.ptr(comps[1]), None, _lib.ptr(ab),
-                      _lib.stream_ptr())
+            ab = self._xor01(comps)
             x1 = gather(rows, width, tab(), outer=pi31, inner=pi12, m1=ab, t1=(s12, *bt), t2=(s31, *bt))
             del ab
-            y1 = gather(rows, width, tab(), inner=pi12, m1=comps[2], t1=(s12, *bt))
+            c3 = self.pack_gather(comps, (2,)) if isinstance(comps, PackedRows) else comps[2]
+            y1 = gather(rows, width, tab(), inner=pi12, m1=c3, t1=(s12, *bt))
+            del c3
             c1 = gather(rows, width, tab(), inner=pi23, m1=x1, t1=(s23, *bt), r=(s12, LABEL_RAND, tid))
             del x1
             r3 = gather(rows, width, tab(), outer=pi23, inner=pi31, m1=y1, t1=(s31, *bt), t2=(s23, *bt), m3=c1,
                         r=(s31, LABEL_RAND, tid))
             del y1, c1
-            r1 = gather(rows, width, tab(), r=(s31, LABEL_RAND, tid))
-            r2 = gather(rows, width, tab(), r=(s12, LABEL_RAND, tid))
+            r1 = blind_table(s31, LABEL_RAND, tid, rows, width, self.dev, pitch=_pitch(width))
+            r2 = blind_table(s12, LABEL_RAND, tid, rows, width, self.dev, pitch=_pitch(width))
             return [r1, r2, r3]
-        k1, k3 = compose(pi31, pi12), compose(pi23, pi31)
-        u = gather(rows, width, tab(), outer=pi31, inner=pi12, t1=(s12, *bt), t2=(s31, *bt))
-        v = gather(rows, width, tab(), inner=pi12, t1=(s12, *bt))
-        w = gather(rows, width, tab(), inner=pi23, t1=(s23, *bt), r=(s12, LABEL_RAND, tid))
-        z = gather(rows, width, tab(), outer=pi23, inner=pi31, t1=(s31, *bt), t2=(s23, *bt), r=(s31, LABEL_RAND, tid))
-        r1 = gather(rows, width, tab(), r=(s31, LABEL_RAND, tid))
-        r2 = gather(rows, width, tab(), r=(s12, LABEL_RAND, tid))
+        return self._shuffle_online(comps, width, self._material(tid, rows, width, pi12, pi23, pi31))
+
+    def _xor01(self, comps) -> torch.Tensor:
+        if isinstance(comps, PackedRows):
+            return self.pack_gather(comps, (0, 1))
         ab = torch.empty_like(comps[0])
         _lib.call("ogm_xor_words", ab.numel(), _lib.ptr(comps[0]), _lib.ptr(comps[1]), None, _lib.ptr(ab),
                   _lib.stream_ptr())
-        x1 = gather(rows, width, tab(), inner=k1, m1=ab, r=u)               # P1
-        y1 = gather(rows, width, tab(), inner=pi12, m1=comps[2], r=v)      # P2
-        c1 = gather(rows, width, tab(), inner=pi23, m1=x1, r=w)            # P2
-        r3 = gather(rows, width, tab(), inner=k3, m1=y1, m3=c1, r=z)       # P3
-        return [r1, r2, r3]
+        return ab
 
-    def _shuffle_online(self, comps: list, width: int, m: dict) -> list:
-        rows = comps[0].shape[0]
+    def pack_gather(self, pr: PackedRows, sets: tuple, idx=None, r=None) -> torch.Tensor:
+        """XOR over components `sets` of the packed rows, at source rows idx
+        (None = identity), XOR r: one ogm_pack_gather launch."""
+        out = torch.empty((pr.rows, _pitch(pr.width)), dtype=torch.int32, device=self.dev)
+        mats = [pr.fields[f][0][s] for s in sets for f in range(len(pr.fields))]
+        pitches = [m.stride(0) if pr.rows else words_for(pr.fields[f][1])
+                   for m, f in zip(mats, [f for _ in sets for f in range(len(pr.fields))])]
+        flags = A([pr.flags[s] for s in sets]) if pr.flags is not None else None
+        _lib.call("ogm_pack_gather", pr.rows, _lib.ptr(idx), len(sets), flags, len(pr.fields), A(mats),
+                  _lib.i64_array(pitches), _lib.i64_array([wd for _, wd in pr.fields]), _lib.ptr(r), _lib.ptr(out),
+                  out.shape[1], _lib.stream_ptr())
+        return out
+
+    def _shuffle_online(self, comps, width: int, m: dict) -> list:
+        rows = comps.rows if isinstance(comps, PackedRows) else comps[0].shape[0]
 
         def tab():
             return torch.empty((rows, _pitch(width)), dtype=torch.int32, device=self.dev)
 
-        ab = torch.empty_like(comps[0])
-        _lib.call("ogm_xor_words", ab.numel(), _lib.ptr(comps[0]), _lib.ptr(comps[1]), None, _lib.ptr(ab),
-                  _lib.stream_ptr())
-        x1 = gather(rows, width, tab(), inner=m["k1"], m1=ab, r=m["u"])           # P1
-        del ab
-        y1 = gather(rows, width, tab(), inner=m["pi12"], m1=comps[2], r=m["v"])   # P2
+        if isinstance(comps, PackedRows):
+            # P1 packs a^b at its composed permutation, P2 packs c at pi12
+            x1 = self.pack_gather(comps, (0, 1), idx=m["k1"], r=m["u"])             # P1
+            y1 = self.pack_gather(comps, (2,), idx=m["pi12"], r=m["v"])              # P2
+        else:
+            ab = self._xor01(comps)
+            x1 = gather(rows, width, tab(), inner=m["k1"], m1=ab, r=m["u"])           # P1
+            del ab
+            y1 = gather(rows, width, tab(), inner=m["pi12"], m1=comps[2], r=m["v"])   # P2
         c1 = gather(rows, width, tab(), inner=m["pi23"], m1=x1, r=m["w"])         # P2
         del x1
         r3 = gather(rows, width, tab(), inner=m["k3"], m1=y1, m3=c1, r=m["z"])    # P3
@@ -348,14 +398,6 @@ class Trio:
         return TrioRecords(group.parent_slot, group.parent_record, 1, group.id_width, [c[None] for c in ids],
                            {a: [c[None] for c in v] for a, v in attrs.items()}, dict(group.attr_widths))
 
-    def _pack(self, flag_bits, fields, rows, width) -> torch.Tensor:
-        out = torch.empty((rows, _pitch(width)), dtype=torch.int32, device=self.dev)
-        mats = [f for f, _ in fields]
-        _lib.call("ogm_pack_fields", rows, _lib.ptr(flag_bits), len(fields), A(mats),
-                  _lib.i64_array([m.stride(0) if rows else words_for(wd) for m, wd in fields]),
-                  _lib.i64_array([wd for _, wd in fields]), _lib.ptr(out), out.shape[1], _lib.stream_ptr())
-        return out
-
     def _column(self, mat) -> torch.Tensor:
         rows = mat.shape[0]
         out = self._empty(words_for(rows))
@@ -386,9 +428,8 @@ class Trio:
         names = sorted(group.attrs)
         widths = [group.attr_widths[a] for a in names]
         row_width = 1 + group.id_width + sum(widths)
-        rows = [self._pack(flags[j], [(group.ids[j], group.id_width)] +
-                           [(group.attrs[a][j], w) for a, w in zip(names, widths)], group.count, row_width)
-                for j in range(3)]
+        rows = PackedRows(group.count, row_width, list(flags),
+                          [(group.ids, group.id_width)] + [(group.attrs[a], w) for a, w in zip(names, widths)])
         sh = self.shuffle(rows, row_width, online_blinds)
         del rows
         keep, k = self._open_keep(sh, group.count, "fetch", audit)
@@ -437,7 +478,7 @@ class Trio:
         sel = [c[i] for c in rec.ids]
         adds = [a.reshape(l_max, w_ne) for a in self._fold(sel, lists, x_ne)]
         fetched = self.reshare_matrix(adds, x_ne)
-        rows = [self._pack(self._parity_rows(f, w_ne), [(f, x_ne)], l_max, 1 + x_ne) for f in fetched]
+        rows = PackedRows(l_max, 1 + x_ne, [self._parity_rows(f, w_ne) for f in fetched], [(fetched, x_ne)])
         sh = self.shuffle(rows, 1 + x_ne)
         keep, k = self._open_keep(sh, l_max, "access", audit)
         if k == 0:

@@ -14,7 +14,7 @@ import pytest
 import torch
 
 from paper_2209_03526_b200 import fss, rss
-from paper_2209_03526_b200.bits import BitVector
+from paper_2209_03526_b200.bits import BitVector, words_for
 from paper_2209_03526_b200.engine import (CandidateGroup, EngineConfig, _OpenLabels, combine_predicates,
                                           open_results, sec_eval, sec_fetch_multi, sec_fetch_unique, sec_match)
 from paper_2209_03526_b200.graphs import device_trio, encrypt_graph, parse_graph_text
@@ -381,3 +381,68 @@ def test_sharded_shuffle_equals_trio_shuffle(world, rows, width):
     assert torch.equal(torch.cat([ranks[r].r1 for r in range(world)]), want[0][:, :w])
     assert torch.equal(torch.cat([ranks[r].r2 for r in range(world)]), want[1][:, :w])
     assert torch.equal(torch.cat(r3), want[2][:, :w])
+
+
+def _np_pack(rows, flag_bits, fields, width, sets):
+    """Plain bit-level packing (src/engine.py:227-233) of components `sets`."""
+    acc = np.zeros((rows, width), np.uint8)
+    for s in sets:
+        cols = []
+        if flag_bits is not None:
+            fb = np.unpackbits(flag_bits[s].cpu().numpy().view(np.uint8), bitorder="little")[:rows]
+            cols.append(fb[:, None])
+        for mats, wd in fields:
+            m = mats[s].cpu().numpy()
+            cols.append(np.unpackbits(np.ascontiguousarray(m).view(np.uint8), axis=1, bitorder="little")[:, :wd])
+        acc ^= np.concatenate(cols, axis=1)
+    pad = (-width) % 32
+    packed = np.packbits(np.pad(acc, ((0, 0), (0, pad))), axis=1, bitorder="little").view(np.int32)
+    return torch.from_numpy(packed.copy())
+
+
+@pytest.mark.parametrize("widths,aligned,flag", [([45, 129], True, True), ([45, 129], False, True),
+                                                  ([3001, 70000, 129, 5], True, True),
+                                                  ([3001, 70000, 129, 5], False, False),
+                                                  ([200000, 8969], True, True), ([31, 1, 64], True, False)])
+def test_pack_gather_vs_bit_reference(widths, aligned, flag):
+    from paper_2209_03526_b200.trio import PackedRows, Trio, _pitch
+
+    rows = 23
+    g = torch.Generator(device="cuda").manual_seed(sum(widths))
+
+    def mat(wd):
+        w = words_for(wd)
+        pitch = (w + 3) // 4 * 4 if aligned else w
+        m = torch.randint(-2**31, 2**31 - 1, (rows, pitch), dtype=torch.int32, device="cuda", generator=g)
+        return m[:, :w]
+
+    fields = [([mat(wd) for _ in range(3)], wd) for wd in widths]
+    flags = [torch.randint(-2**31, 2**31 - 1, (words_for(rows),), dtype=torch.int32, device="cuda", generator=g)
+             for _ in range(3)] if flag else None
+    width = (1 if flag else 0) + sum(widths)
+    pr = PackedRows(rows, width, flags, fields)
+    t = Trio(b"\x02" * 16)
+    idx = torch.randperm(rows, device="cuda", generator=g).to(torch.int32)
+    r = torch.randint(-2**31, 2**31 - 1, (rows, _pitch(width)), dtype=torch.int32, device="cuda", generator=g)
+    w = words_for(width)
+    for sets in ((0,), (0, 1), (2,), (0, 1, 2)):
+        want = _np_pack(rows, flags, fields, width, sets)
+        got = t.pack_gather(pr, sets).cpu()
+        assert torch.equal(got[:, :w], want), (sets, widths)
+        assert bool((got[:, w:] == 0).all())
+        got = t.pack_gather(pr, sets, idx=idx, r=r).cpu()
+        assert torch.equal(got[:, :w], want[idx.cpu().long()] ^ r.cpu()[:, :w]), (sets, widths)
+
+
+@pytest.mark.parametrize("rows,width,pad", [(1, 1, 0), (37, 31, 3), (37, 32, 0), (19, 33, 2), (23, 129, 3),
+                                           (5, 391053, 3), (300, 2000, 4)])
+def test_prf_rows_vs_oracle(rows, width, pad):
+    import oracle
+    from paper_2209_03526_b200.shuffle import blind_table
+
+    seed = bytes(range(16, 32))
+    w = words_for(width)
+    got = blind_table(seed, b"SHTB", 7, rows, width, pitch=w + pad).cpu().numpy().view(np.uint32)
+    want = oracle.blind_table(seed, b"SHTB", 7, rows, width)
+    assert np.array_equal(got[:, :w], want)
+    assert not got[:, w:].any()
