@@ -395,6 +395,38 @@ __global__ void __launch_bounds__(512) tile_gather_kernel(const int32_t* __restr
 
 
 // 128-bit rows (the C5 shape): one thread per row, uint4 traffic only.
+// Pass 2 with L2-sized windows (tile rows x row bytes > the shared-memory
+// tile): a window's rows are read at random, but the grid sweeps output rows
+// in order, so the live window (~32 MB) stays L2-resident and HBM sees each
+// of its lines once; the streamed terms are evict-first.
+__global__ void window_gather4_kernel(const int32_t* __restrict__ q2, const uint4* __restrict__ inter,
+                                      const uint4* __restrict__ r, const uint4* __restrict__ m3, int64_t rows,
+                                      int64_t T, uint4* __restrict__ out) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < rows; i += stride) {
+        const int64_t src = (i / T) * T + __ldcs(q2 + i);
+        uint4 v = __ldcg(inter + src);
+        if (r) v = xor4(v, __ldcs(r + i));
+        if (m3) v = xor4(v, __ldcs(m3 + i));
+        __stcs(out + i, v);
+    }
+}
+
+__global__ void window_gather_kernel(const int32_t* __restrict__ q2, const uint32_t* __restrict__ inter,
+                                     const uint32_t* __restrict__ r, const uint32_t* __restrict__ m3, int64_t rows,
+                                     int64_t W, int64_t T, uint32_t* __restrict__ out) {
+    const int64_t total = rows * W;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += stride) {
+        const int64_t i = t / W, w = t - i * W;
+        const int64_t src = (i / T) * T + __ldcs(q2 + i);
+        uint32_t v = __ldcg(inter + src * W + w);
+        if (r) v ^= __ldcs(r + t);
+        if (m3) v ^= __ldcs(m3 + t);
+        __stcs(out + t, v);
+    }
+}
+
 __global__ void bucket_scatter4_kernel(const int32_t* __restrict__ pos1, const uint4* __restrict__ m1,
                                        const uint4* __restrict__ m2, int64_t rows, uint4* __restrict__ inter) {
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
@@ -669,8 +701,6 @@ int ogm_gather_planned(int64_t rows, int64_t words, int64_t tile_rows, const int
                        uint32_t* inter, uint32_t* out, void* stream) {
     using namespace ogm;
     OGM_CHECK_ARG(rows >= 0 && words >= 1 && tile_rows >= 1, OGM_ERR_ARG, "bad planned-gather shape");
-    OGM_CHECK_ARG(tile_rows * words * 4 <= kTileBytes, OGM_ERR_ARG, "tile of %lld rows x %lld words exceeds %lld B",
-                  (long long)tile_rows, (long long)words, (long long)kTileBytes);
     OGM_CHECK_ARG(m1 && inter && out, OGM_ERR_ARG, "m1, inter and out are required");
     if (rows == 0) return OGM_OK;
     OGM_ENSURE_INIT();
@@ -681,7 +711,19 @@ int ogm_gather_planned(int64_t rows, int64_t words, int64_t tile_rows, const int
     if (g > cap) g = cap;
     const bool aligned = ((((uintptr_t)m1) | ((uintptr_t)m2) | ((uintptr_t)m3) | ((uintptr_t)r_mat) |
                            ((uintptr_t)inter) | ((uintptr_t)out)) & 15) == 0;
-    if (words == 4 && aligned) {
+    const bool window = tile_rows * words * 4 > kTileBytes;  // L2-window pass 2 instead of smem tiles
+    if (window) {
+        if (words == 4 && aligned) {
+            bucket_scatter4_kernel<<<grid_for(rows), 256, 0, st>>>(pos1, (const uint4*)m1, (const uint4*)m2, rows,
+                                                                   (uint4*)inter);
+            window_gather4_kernel<<<grid_for(rows), 256, 0, st>>>(q2, (const uint4*)inter, (const uint4*)r_mat,
+                                                                  (const uint4*)m3, rows, tile_rows, (uint4*)out);
+        } else {
+            bucket_scatter_kernel<<<grid_for(rows * words), 256, 0, st>>>(pos1, m1, m2, rows, words, inter);
+            window_gather_kernel<<<grid_for(rows * words), 256, 0, st>>>(q2, inter, r_mat, m3, rows, words,
+                                                                         tile_rows, out);
+        }
+    } else if (words == 4 && aligned) {
         bucket_scatter4_kernel<<<grid_for(rows), 256, 0, st>>>(pos1, (const uint4*)m1, (const uint4*)m2, rows,
                                                                (uint4*)inter);
         tile_gather4_kernel<<<(int)g, 512, (size_t)(tile_rows * 16), st>>>(

@@ -446,3 +446,18 @@ def test_prf_rows_vs_oracle(rows, width, pad):
     want = oracle.blind_table(seed, b"SHTB", 7, rows, width)
     assert np.array_equal(got[:, :w], want)
     assert not got[:, w:].any()
+
+
+@pytest.mark.parametrize("rows,words,window", [(70000, 4, 256 << 10), (50001, 5, 200 << 10), (3000, 4, 1 << 20)])
+def test_window_planned_gather_equals_direct(rows, words, window):
+    from paper_2209_03526_b200.shuffle import GatherPlan, gather
+
+    g = torch.Generator(device="cuda").manual_seed(rows)
+    M = torch.randint(-2**31, 2**31 - 1, (rows, words), dtype=torch.int32, device="cuda", generator=g)
+    R = torch.randint(-2**31, 2**31 - 1, (rows, words), dtype=torch.int32, device="cuda", generator=g)
+    idx = torch.randperm(rows, device="cuda", generator=g).to(torch.int32)
+    want = gather(rows, 32 * words, torch.empty_like(M), inner=idx, m1=M, r=R)
+    plan = GatherPlan(idx, words, window_bytes=window)
+    assert plan.tile * words * 4 > 96 * 1024  # the L2-window pass 2, not shared-memory tiles
+    got = plan.run(torch.empty_like(M), m1=M, r=R)
+    assert torch.equal(got, want)
