@@ -17,6 +17,10 @@ seeded inputs (keys generated on the device by ogm_fss_gen from seeded roots).
   2 int ops per AES table lookup of the minimal T-table walk (DCF: 31 levels x
   (160 + 133) + 133 = 9216 lookups/eval), against the measured LOP3 issue
   rate of this GPU (ogm_measure_int_peak).
+* ``query_latency`` -- the metric's second half (BASELINE: "... and end-to-end
+  query latency"): the C1 tiny oblivious match, tokens in -> reconstructed
+  matches, via the trio fast path and via the per-party drop-in API, both
+  checked against the plaintext matcher (rank 0).
 * ``cpu_baseline`` -- the CPU oracle port (oracle/, C, all host threads) on a
   bounded sample of the same workload, rank 0 only.
 
@@ -69,6 +73,8 @@ def parse():
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu", action="store_true")
     p.add_argument("--cpu-seconds", type=float, default=10.0)
+    p.add_argument("--no-query", action="store_true", help="skip the C1 end-to-end query latency")
+    p.add_argument("--query-steps", type=int, default=10)
     return p.parse_args()
 
 
@@ -209,6 +215,57 @@ def run_reference(args):
 # ---------------------------------------------------------------------------
 
 
+def query_latency(steps: int) -> dict:
+    """The metric's second half: end-to-end latency of the C1 tiny oblivious
+    match (BASELINE configs[0]) on this GPU -- tokens in, result shares
+    reconstructed on the host -- through the trio fast path and through the
+    per-party drop-in API (run_trio + sec_match + open_results), each checked
+    against the plaintext matcher."""
+    import torch
+
+    import oracle.matcher as om
+    from paper_2209_03526_b200 import workloads
+    from paper_2209_03526_b200.engine import EngineConfig, open_results, sec_match
+    from paper_2209_03526_b200.graphs import device_trio, encrypt_graph
+    from paper_2209_03526_b200.net import local_runtimes, make_session_configs, run_trio
+    from paper_2209_03526_b200.query import gen_token, load_query
+    from paper_2209_03526_b200.trio import Trio
+
+    graph = workloads.tiny_graph(1)
+    rng = np.random.default_rng(1)
+    schema, shares = encrypt_graph(graph, 2, rng)
+    dshares = device_trio(shares)
+    query = load_query(workloads.tiny_query(graph, 1), schema)
+    tokens = gen_token(query, schema, rng)
+    want = om.oracle_match(graph, query, schema)
+    master = b"\x5a" * 16
+
+    def trio():
+        res = Trio(master).match(list(tokens), list(dshares))
+        return set(open_results(res.party_results()[:2], schema)[0])
+
+    def per_party():
+        rts = local_runtimes(make_session_configs(master))
+        res = run_trio(lambda rt: sec_match(rt, tokens[rt.index - 1], dshares[rt.index - 1], EngineConfig()), rts)
+        return set(open_results(res[:2], schema)[0])
+
+    out = {"workload": "C1 tiny: 1000 vertices, 3 types, 3-vertex path (eq + range + always-true), k=2",
+           "unit": "ms", "steps": steps}
+    for name, fn in (("trio_ms", trio), ("per_party_ms", per_party)):
+        for _ in range(3):
+            got = fn()
+        lat = []
+        for _ in range(steps):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            got = fn()
+            lat.append(1e3 * (time.perf_counter() - t0))
+        out[name] = statistics.median(lat)
+        out[name.replace("_ms", "_oracle_equal")] = got == want
+    out["matches"] = len(want)
+    return out
+
+
 def main():
     args = parse()
     if args.impl == "reference":
@@ -323,6 +380,10 @@ def main():
                "ms_per_step": 1e3 * float(tt.item()) / args.steps}
         del host, hout
 
+    query = None
+    if rank == 0 and not args.no_query:
+        query = query_latency(args.query_steps)
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         import oracle
@@ -342,7 +403,7 @@ def main():
                        "keys_per_gpu": K, "domain_bits": BITS, "points_per_key": 1,
                        "parallelism": f"key-sharded x{world}",
                        "l2": "inputs (9.1 GB of keys) larger than L2; no flush"},
-            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "query_latency": query,
             "gpu_launches": args.steps, "clocks": clk,
             "launch_ms": {"mean": statistics.mean(per_launch), "min": min(per_launch),
                           "max": max(per_launch)},

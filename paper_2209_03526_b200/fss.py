@@ -159,12 +159,17 @@ class KeyBatch:
         ctrl = ctrl.astype(np.uint32)
         flags = np.array([(k.root_t & 1) | ((k.final_cw & 1) << 1) | ((k.add_const & 1) << 2)
                           for k in keys], np.uint8)
-        dev = torch.device(device)
-        return cls(_lib.KIND_DCF if comp else _lib.KIND_DPF, bits,
-                   torch.from_numpy(root.copy()).to(dev),
-                   torch.from_numpy(np.ascontiguousarray(scw)).to(dev),
-                   torch.from_numpy(ctrl.view(np.int32)).to(dev),
-                   torch.from_numpy(flags).to(dev))
+        # one host buffer, one H2D copy: root | seed_cw | ctrl | flags (every
+        # offset a multiple of 16 bytes except the trailing flags)
+        a, b = 16 * n, 16 * n * (1 + bits)
+        buf = np.empty(b + 12 * n + n, np.uint8)
+        buf[:a] = root.reshape(-1)
+        buf[a:b] = np.ascontiguousarray(scw).reshape(-1)
+        buf[b:b + 12 * n] = ctrl.view(np.uint8).reshape(-1)
+        buf[b + 12 * n:] = flags
+        d = torch.from_numpy(buf).to(torch.device(device))
+        return cls(_lib.KIND_DCF if comp else _lib.KIND_DPF, bits, d[:a].view(n, 16), d[a:b].view(bits, n, 16),
+                   d[b:b + 12 * n].view(torch.int32).view(3, n), d[b + 12 * n:])
 
     def to_keys(self) -> list:
         """Unpack into DpfKey/DcfKey objects (host)."""
