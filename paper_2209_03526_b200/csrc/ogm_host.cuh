@@ -120,6 +120,15 @@ static cudaError_t allow_big_smem(KernelT k, int bytes) {
     return cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
 }
 
+// Gather kernels with no shared memory: ask for the maximum L1 carveout, or
+// they inherit whatever split the previous kernel left on the SM (a
+// shared-memory-heavy kernel leaves a small L1, which starves a random-row
+// gather of in-flight misses: measured 2.26 -> 5.5 ms, profiles/r01_c5_plan.md).
+template <class KernelT>
+static cudaError_t prefer_l1(KernelT k) {
+    return cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, 0);
+}
+
 int fss_init();
 int engine_init();
 int shuffle_init();

@@ -238,6 +238,11 @@ __global__ void __launch_bounds__(kAesThreads) shuffle_gather_kernel(const Gathe
 __device__ __forceinline__ uint4 ld_term(const uint32_t* m, int64_t row, int64_t pitch, int64_t c) {
     return m ? __ldcs(reinterpret_cast<const uint4*>(m + row * pitch) + c) : make_uint4(0, 0, 0, 0);
 }
+// gathered (random-row) terms keep normal L2 caching: a planned gather's
+// window must stay resident while its lines are reused
+__device__ __forceinline__ uint4 ld_rand(const uint32_t* m, int64_t row, int64_t pitch, int64_t c) {
+    return m ? __ldcg(reinterpret_cast<const uint4*>(m + row * pitch) + c) : make_uint4(0, 0, 0, 0);
+}
 
 __global__ void __launch_bounds__(256) gather_matrix_rows_kernel(const GatherArgs a, int64_t nch) {
     const uint32_t* T1 = a.t1.on ? a.t1.mat : nullptr;
@@ -278,13 +283,13 @@ __global__ void __launch_bounds__(256) gather_matrix_kernel(const GatherArgs a, 
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += stride) {
         const int64_t i = t / nch, c = t - i * nch;
-        const int64_t k2 = a.P2 ? (int64_t)__ldg(a.P2 + i) : i;
-        const int64_t k1 = a.P1 ? (int64_t)__ldg(a.P1 + k2) : k2;
+        const int64_t k2 = a.P2 ? (int64_t)__ldcs(a.P2 + i) : i;
+        const int64_t k1 = a.P1 ? (int64_t)(a.P2 ? __ldg(a.P1 + k2) : __ldcs(a.P1 + k2)) : k2;
         if (vec) {
-            uint4 x = xor4(xor4(ld_term(a.M1, k1, a.pitch, c), ld_term(a.M2, k1, a.pitch, c)),
-                           xor4(ld_term(a.M3, i, a.pitch, c), ld_term(T1, k1, a.pitch, c)));
-            x = xor4(x, xor4(ld_term(T2, k2, a.pitch, c), ld_term(R, i, a.pitch, c)));
-            reinterpret_cast<uint4*>(a.out + i * a.pitch)[c] = x;
+            uint4 x = xor4(xor4(ld_rand(a.M1, k1, a.pitch, c), ld_rand(a.M2, k1, a.pitch, c)),
+                           xor4(ld_term(a.M3, i, a.pitch, c), ld_rand(T1, k1, a.pitch, c)));
+            x = xor4(x, xor4(ld_rand(T2, k2, a.pitch, c), ld_term(R, i, a.pitch, c)));
+            __stcs(reinterpret_cast<uint4*>(a.out + i * a.pitch) + c, x);  // evict-first: keep L2 for the window
         } else {
             const int nw = (int)min((int64_t)4, a.W - 4 * c);
             for (int j = 0; j < nw; j++) {
@@ -314,151 +319,168 @@ __global__ void perm_compose_kernel(const int32_t* __restrict__ outer, const int
 // ---------------------------------------------------------------------------
 // Planned two-pass gather for a permutation known ahead of the data.
 //
-// A party's online shuffle step is out[i] = M[k(i)] ^ (terms at i), with k a
-// permutation the party fixed offline (src/shuffle.py:106-143).  A direct
-// gather reads one random 16-byte row per output row; HBM serves that at
-// ~1/4 of streaming bandwidth.  Since k is data-independent, the offline
-// phase plans two streaming passes instead:
+// A party's online shuffle step is out[i] = M[idx[i]] ^ (terms at i), with
+// idx a permutation the party fixed offline (src/shuffle.py:106-143).  On
+// B200 a random 16-byte row read from a table much larger than L2 costs a
+// full DRAM access with its own row activation: ~33 G rows/s however narrow
+// the row (profiles/r01_c5_gather_variants.md).  Random reads confined to a
+// CONTIGUOUS window of <= 16 MB run at ~150-160 G rows/s (the window's DRAM
+// pages stay open / L2-resident), while the same reads over scattered 4 KB
+// runs do not (profiles/r01_c5_plan.md).  Since idx is data-independent, the
+// offline phase factors the gather into two passes that only ever touch
+// HBM sequentially or inside one contiguous window:
 //
-//   pass 1 (bucket scatter):  inter[pos1[j]] = M1[j] ^ M2[j]   (j sequential)
-//       pos1 puts every source row into the bucket of its destination tile,
-//       in increasing j within the bucket, so each bucket fills front to back
-//       and its open lines merge in L2 before they are written back;
-//   pass 2 (tile gather):     out[i] = tile[q2[i]] ^ R[i] ^ M3[i]
-//       one CTA stages a bucket (<= 96 KB) in shared memory and emits its
-//       tile in order: coalesced reads and writes.
+//   I-layout: output window d = [d*Wr, (d+1)*Wr) owns I-region d, holding the
+//             rows its outputs need, ordered by source row; P(j) = position
+//             of source row j in I.
+//   pass 1 (partition): a CTA loads a tile of T consecutive source rows
+//             (coalesced), places row j at shared slot lslot[j] (tile rows
+//             grouped by destination region, source order within a group),
+//             then writes slot k to I[gdst[k]]: one contiguous run per region.
+//   pass 2 (window gather): out[i] = I[q2[i]] ^ R[i] ^ M3[i], q2[i] =
+//             P(idx[i]) lies in region d(i): random reads inside one
+//             contiguous window, sequential writes.
 // ---------------------------------------------------------------------------
-__global__ void invert_perm_kernel(const int32_t* __restrict__ k, int64_t n, int32_t* __restrict__ inv) {
+constexpr int64_t kWindowBytes = 8 << 20;      // pass-2 window (contiguous I-region)
+constexpr int64_t kPartSmemBytes = 64 << 10;   // pass-1 tile (3 CTAs per SM)
+constexpr int64_t kMaxDynSmem = 200 << 10;
+
+__device__ __forceinline__ uint4 xorU(uint4 a, uint4 b) { return xor4(a, b); }
+__device__ __forceinline__ uint32_t xorU(uint32_t a, uint32_t b) { return a ^ b; }
+
+__global__ void plan_inv_kernel(const int32_t* __restrict__ idx, int64_t n, int32_t* __restrict__ inv) {
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) inv[k[i]] = (int32_t)i;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) inv[__ldg(idx + i)] = (int32_t)i;
 }
 
-__global__ void tile_keys_kernel(const int32_t* __restrict__ inv, int64_t n, int64_t T, int32_t* __restrict__ key,
-                                 int32_t* __restrict__ val) {
+// key[j] = (tile of j) * nwin + (destination window of j); tile_rows = 0 drops the tile part
+__global__ void plan_keys_kernel(const int32_t* __restrict__ inv, int64_t n, int64_t Wr, int64_t T, int64_t nwin,
+                                 int32_t* __restrict__ key, int32_t* __restrict__ val) {
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += stride) {
-        key[j] = (int32_t)(inv[j] / T);
+        const int64_t d = __ldg(inv + j) / Wr;
+        key[j] = (int32_t)(T ? (j / T) * nwin + d : d);
         val[j] = (int32_t)j;
     }
 }
 
-__global__ void scatter_pos_kernel(const int32_t* __restrict__ sorted_j, int64_t n, int32_t* __restrict__ pos1) {
+__global__ void plan_pos_kernel(const int32_t* __restrict__ sj, int64_t n, int32_t* __restrict__ P) {
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < n; p += stride) pos1[sorted_j[p]] = (int32_t)p;
+    for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < n; p += stride) P[__ldg(sj + p)] = (int32_t)p;
 }
 
-__global__ void local_q_kernel(const int32_t* __restrict__ k, const int32_t* __restrict__ pos1, int64_t n, int64_t T,
+__global__ void plan_q2_kernel(const int32_t* __restrict__ idx, const int32_t* __restrict__ P, int64_t n,
                                int32_t* __restrict__ q2) {
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
-        q2[i] = (int32_t)(pos1[k[i]] - (i / T) * T);
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) q2[i] = __ldg(P + __ldg(idx + i));
 }
 
-__global__ void bucket_scatter_kernel(const int32_t* __restrict__ pos1, const uint32_t* __restrict__ m1,
-                                      const uint32_t* __restrict__ m2, int64_t rows, int64_t W,
-                                      uint32_t* __restrict__ inter) {
-    const int64_t total = rows * W;
+__global__ void plan_slots_kernel(const int32_t* __restrict__ sj2, const int32_t* __restrict__ P, int64_t n,
+                                  int64_t T, int32_t* __restrict__ gdst, uint16_t* __restrict__ lslot) {
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += stride) {
-        const int64_t j = t / W, w = t - j * W;
-        uint32_t v = __ldcs(m1 + t);
-        if (m2) v ^= __ldcs(m2 + t);
-        inter[(int64_t)__ldcs(pos1 + j) * W + w] = v;
+    for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += stride) {
+        const int32_t j = __ldg(sj2 + k);
+        gdst[k] = __ldg(P + j);
+        lslot[j] = (uint16_t)(k % T);
     }
 }
 
-__global__ void __launch_bounds__(512) tile_gather_kernel(const int32_t* __restrict__ q2,
-                                                          const uint32_t* __restrict__ inter,
-                                                          const uint32_t* __restrict__ r,
-                                                          const uint32_t* __restrict__ m3, int64_t rows, int64_t W,
-                                                          int64_t T, uint32_t* __restrict__ out) {
-    extern __shared__ __align__(16) uint32_t tile[];
-    const int64_t ntiles = (rows + T - 1) / T;
-    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
-        const int64_t r0 = t * T;
-        const int64_t nr = min(T, rows - r0);
-        const int64_t nw = nr * W;
-        const uint32_t* src = inter + r0 * W;
-        __syncthreads();
-        for (int64_t e = threadIdx.x; e < nw; e += blockDim.x) tile[e] = __ldcs(src + e);
-        __syncthreads();
-        for (int64_t e = threadIdx.x; e < nw; e += blockDim.x) {
-            const int64_t li = e / W, w = e - li * W;
-            const int64_t g = (r0 + li) * W + w;
-            uint32_t v = tile[(int64_t)__ldcs(q2 + r0 + li) * W + w];
-            if (r) v ^= __ldcs(r + g);
-            if (m3) v ^= __ldcs(m3 + g);
-            out[g] = v;
-        }
-    }
-}
-
-
-// 128-bit rows (the C5 shape): one thread per row, uint4 traffic only.
-// Pass 2 with L2-sized windows (tile rows x row bytes > the shared-memory
-// tile): a window's rows are read at random, but the grid sweeps output rows
-// in order, so the live window (~32 MB) stays L2-resident and HBM sees each
-// of its lines once; the streamed terms are evict-first.
-__global__ void window_gather4_kernel(const int32_t* __restrict__ q2, const uint4* __restrict__ inter,
-                                      const uint4* __restrict__ r, const uint4* __restrict__ m3, int64_t rows,
-                                      int64_t T, uint4* __restrict__ out) {
-    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < rows; i += stride) {
-        const int64_t src = (i / T) * T + __ldcs(q2 + i);
-        uint4 v = __ldcg(inter + src);
-        if (r) v = xor4(v, __ldcs(r + i));
-        if (m3) v = xor4(v, __ldcs(m3 + i));
-        __stcs(out + i, v);
-    }
-}
-
-__global__ void window_gather_kernel(const int32_t* __restrict__ q2, const uint32_t* __restrict__ inter,
-                                     const uint32_t* __restrict__ r, const uint32_t* __restrict__ m3, int64_t rows,
-                                     int64_t W, int64_t T, uint32_t* __restrict__ out) {
-    const int64_t total = rows * W;
-    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += stride) {
-        const int64_t i = t / W, w = t - i * W;
-        const int64_t src = (i / T) * T + __ldcs(q2 + i);
-        uint32_t v = __ldcg(inter + src * W + w);
-        if (r) v ^= __ldcs(r + t);
-        if (m3) v ^= __ldcs(m3 + t);
-        __stcs(out + t, v);
-    }
-}
-
-__global__ void bucket_scatter4_kernel(const int32_t* __restrict__ pos1, const uint4* __restrict__ m1,
-                                       const uint4* __restrict__ m2, int64_t rows, uint4* __restrict__ inter) {
-    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < rows; j += stride) {
-        uint4 v = __ldcs(m1 + j);
-        if (m2) v = xor4(v, __ldcs(m2 + j));
-        inter[__ldcs(pos1 + j)] = v;
-    }
-}
-
-__global__ void __launch_bounds__(512) tile_gather4_kernel(const int32_t* __restrict__ q2,
-                                                           const uint4* __restrict__ inter,
-                                                           const uint4* __restrict__ r, const uint4* __restrict__ m3,
-                                                           int64_t rows, int T, uint4* __restrict__ out) {
-    extern __shared__ __align__(16) uint4 tile4[];
+// pass 1 in units U (uint4 for 16-B-multiple pitches, else words); wu = pitch in U
+template <typename U>
+__global__ void __launch_bounds__(512) plan_partition_kernel(const U* __restrict__ m1, const U* __restrict__ m2,
+                                                             const uint16_t* __restrict__ lslot,
+                                                             const int32_t* __restrict__ gdst, int64_t rows, int T,
+                                                             int wu, U* __restrict__ inter) {
+    extern __shared__ __align__(16) unsigned char part_smem[];
+    U* tile = reinterpret_cast<U*>(part_smem);
     const int64_t ntiles = (rows + T - 1) / T;
     for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
         const int64_t r0 = t * T;
         const int nr = (int)min((int64_t)T, rows - r0);
-        __syncthreads();
-        for (int e = threadIdx.x; e < nr; e += blockDim.x) tile4[e] = __ldcs(inter + r0 + e);
-        __syncthreads();
-        for (int e = threadIdx.x; e < nr; e += blockDim.x) {
-            uint4 v = tile4[__ldcs(q2 + r0 + e)];
-            if (r) v = xor4(v, __ldcs(r + r0 + e));
-            if (m3) v = xor4(v, __ldcs(m3 + r0 + e));
-            out[r0 + e] = v;
+        const int ne = nr * wu;
+        const U* a = m1 + r0 * wu;
+        const U* b = m2 ? m2 + r0 * wu : nullptr;
+        for (int e = threadIdx.x; e < ne; e += blockDim.x) {
+            const int r = wu == 1 ? e : e / wu;
+            U v = __ldcs(a + e);
+            if (b) v = xorU(v, __ldcs(b + e));
+            tile[(int)__ldcs(lslot + r0 + r) * wu + (e - r * wu)] = v;
         }
+        __syncthreads();
+        for (int e = threadIdx.x; e < ne; e += blockDim.x) {
+            const int k = wu == 1 ? e : e / wu;
+            __stcs(inter + (int64_t)__ldcs(gdst + r0 + k) * wu + (e - k * wu), tile[e]);
+        }
+        __syncthreads();
     }
 }
 
-constexpr int64_t kTileBytes = 96 * 1024;
+// pass 1 for 16-byte rows: every thread keeps RPT loads (and RPT index
+// loads) in flight per phase instead of one, so a CTA's load and store
+// phases each cost one memory latency.  Stores are evict-first: L2 appears
+// to keep evict-normal DIRTY lines ahead of clean ones, so normal stores here
+// leave pass 2 an L2 in which its window does not stay resident (pass 2
+// measured 2.26 -> 5.5 ms, DRAM reads 9.7 -> 28.6 GB; profiles/r01_c5_plan.md)
+template <int RPT>
+__global__ void __launch_bounds__(512) plan_partition4_kernel(const uint4* __restrict__ m1, const uint4* __restrict__ m2,
+                                                              const uint16_t* __restrict__ lslot,
+                                                              const int32_t* __restrict__ gdst, int64_t rows,
+                                                              uint4* __restrict__ inter) {
+    extern __shared__ __align__(16) unsigned char part_smem[];
+    uint4* tile = reinterpret_cast<uint4*>(part_smem);
+    constexpr int T = RPT * 512;
+    const int64_t nfull = rows / T;
+    for (int64_t t = blockIdx.x; t < nfull; t += gridDim.x) {
+        const int64_t r0 = t * T + threadIdx.x;
+        uint4 v[RPT];
+        int sl[RPT];
+#pragma unroll
+        for (int k = 0; k < RPT; k++) {
+            v[k] = __ldcs(m1 + r0 + k * 512);
+            sl[k] = __ldcs(lslot + r0 + k * 512);
+        }
+        if (m2) {
+#pragma unroll
+            for (int k = 0; k < RPT; k++) v[k] = xor4(v[k], __ldcs(m2 + r0 + k * 512));
+        }
+#pragma unroll
+        for (int k = 0; k < RPT; k++) tile[sl[k]] = v[k];
+        __syncthreads();
+        int gd[RPT];
+#pragma unroll
+        for (int k = 0; k < RPT; k++) gd[k] = __ldcs(gdst + r0 + k * 512);
+#pragma unroll
+        for (int k = 0; k < RPT; k++) __stcs(inter + gd[k], tile[threadIdx.x + k * 512]);
+        __syncthreads();
+    }
+    // ragged last tile (rows % T): one CTA, one row per thread-step
+    if (blockIdx.x == gridDim.x - 1 && rows % T) {
+        const int64_t b0 = nfull * T;
+        const int nr = (int)(rows - b0);
+        for (int e = threadIdx.x; e < nr; e += 512) {
+            uint4 x = __ldcs(m1 + b0 + e);
+            if (m2) x = xor4(x, __ldcs(m2 + b0 + e));
+            tile[__ldcs(lslot + b0 + e)] = x;
+        }
+        __syncthreads();
+        for (int e = threadIdx.x; e < nr; e += 512) __stcs(inter + __ldcs(gdst + b0 + e), tile[e]);
+    }
+}
+
+// pass 2 for 16-byte rows (the C5 shape): a lean kernel, since with
+// window-local sources the instruction count per row matters
+__global__ void __launch_bounds__(256) win_gather4_kernel(const int32_t* __restrict__ q, const uint4* __restrict__ m1,
+                                                          const uint4* __restrict__ m3, const uint4* __restrict__ r,
+                                                          int64_t rows, uint4* __restrict__ out) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < rows; i += stride) {
+        const uint4* src = m1 + __ldcs(q + i);
+        uint4 v = __ldcg(src);
+        if (m3) v = xor4(v, __ldcs(m3 + i));
+        if (r) v = xor4(v, __ldcs(r + i));
+        __stcs(out + i, v);
+    }
+}
 
 
 // All reservation rounds in ONE CTA (small permutations: no host round
@@ -510,8 +532,9 @@ __global__ void __launch_bounds__(1024) perm_rounds_block_kernel(const int32_t* 
 int shuffle_init() {
     OGM_CUDA_TRY(allow_big_smem(perm_draws_kernel, kAesTableBytes));
     OGM_CUDA_TRY(allow_big_smem(shuffle_gather_kernel<true>, kAesTableBytes));
-    OGM_CUDA_TRY(allow_big_smem(tile_gather_kernel, (int)kTileBytes));
-    OGM_CUDA_TRY(allow_big_smem(tile_gather4_kernel, (int)kTileBytes));
+    OGM_CUDA_TRY(prefer_l1(win_gather4_kernel));
+    OGM_CUDA_TRY(prefer_l1(gather_matrix_kernel));
+    OGM_CUDA_TRY(prefer_l1(gather_matrix_rows_kernel));
     return OGM_OK;
 }
 
@@ -605,6 +628,21 @@ static int set_term(ogm::GatherTerm& g, const uint8_t* key, const uint8_t* label
     return OGM_OK;
 }
 
+static void launch_matrix_gather(const ogm::GatherArgs& a, cudaStream_t st) {
+    using namespace ogm;
+    const bool vec = (a.pitch & 3) == 0 &&
+                     ((((uintptr_t)a.M1) | ((uintptr_t)a.M2) | ((uintptr_t)a.M3) | ((uintptr_t)a.out) |
+                       ((uintptr_t)a.t1.mat) | ((uintptr_t)a.t2.mat) | ((uintptr_t)a.r.mat)) & 15) == 0;
+    const int64_t nch = vec ? (a.pitch >> 2) : ((a.W + 3) >> 2);
+    const int64_t cap = (int64_t)sm_count() * 8;
+    int64_t g = (vec && nch >= 64) ? a.rows : (a.rows * nch + 255) / 256;
+    if (g > cap) g = cap;
+    if (vec && nch >= 64)
+        gather_matrix_rows_kernel<<<(int)(g < 1 ? 1 : g), 256, 0, st>>>(a, nch);
+    else
+        gather_matrix_kernel<<<(int)(g < 1 ? 1 : g), 256, 0, st>>>(a, nch, vec ? 1 : 0);
+}
+
 int ogm_shuffle_gather(int64_t rows, int64_t words, int64_t width_bits, const int32_t* perm_outer,
                        const int32_t* perm_inner, const uint32_t* m1, const uint32_t* m2, const uint32_t* m3,
                        const uint8_t* t1_key, const uint8_t* t1_label, uint64_t t1_index, const uint32_t* t1_mat,
@@ -641,97 +679,132 @@ int ogm_shuffle_gather(int64_t rows, int64_t words, int64_t width_bits, const in
     if (online) {
         shuffle_gather_kernel<true><<<aes_grid(work), kAesThreads, kAesTableBytes, st>>>(a);
     } else {
-        const bool vec = (a.pitch & 3) == 0 &&
-                         ((((uintptr_t)a.M1) | ((uintptr_t)a.M2) | ((uintptr_t)a.M3) | ((uintptr_t)a.out) |
-                           ((uintptr_t)a.t1.mat) | ((uintptr_t)a.t2.mat) | ((uintptr_t)a.r.mat)) & 15) == 0;
-        const int64_t nch = vec ? (a.pitch >> 2) : ((a.W + 3) >> 2);
-        const int64_t cap = (int64_t)sm_count() * 8;
-        int64_t g = (vec && nch >= 64) ? rows : (rows * nch + 255) / 256;
-        if (g > cap) g = cap;
-        if (vec && nch >= 64)
-            gather_matrix_rows_kernel<<<(int)(g < 1 ? 1 : g), 256, 0, st>>>(a, nch);
-        else
-            gather_matrix_kernel<<<(int)(g < 1 ? 1 : g), 256, 0, st>>>(a, nch, vec ? 1 : 0);
+        launch_matrix_gather(a, st);
     }
     OGM_LAUNCH_CHECK();
     return OGM_OK;
 }
 
-int64_t ogm_gather_tile_rows(int64_t words) {
-    if (words <= 0) return 0;
-    return ogm::kTileBytes / (4 * words);
+int64_t ogm_gather_window_rows(int64_t pitch_words) {
+    if (pitch_words <= 0) return 0;
+    const int64_t r = ogm::kWindowBytes / (4 * pitch_words);
+    return r > 0 ? r : 1;
+}
+
+int64_t ogm_gather_tile_rows(int64_t pitch_words) {
+    if (pitch_words <= 0) return 0;
+    int64_t r = ogm::kPartSmemBytes / (4 * pitch_words);
+    if (r > 65536) r = 65536;
+    return r > 0 ? r : 1;
 }
 
 int64_t ogm_gather_plan_workspace_bytes(int64_t n) {
     size_t temp = 0;
     cub::DeviceRadixSort::SortPairs(nullptr, temp, (int32_t*)nullptr, (int32_t*)nullptr, (int32_t*)nullptr,
                                     (int32_t*)nullptr, (int)(n > 0 ? n : 1));
-    return (int64_t)temp + 5 * 4 * n + 1024;
+    return (int64_t)temp + 6 * 4 * n + 1024;
 }
 
-int ogm_gather_plan(int64_t n, const int32_t* idx, int64_t tile_rows, int32_t* pos1, int32_t* q2, void* workspace,
-                    int64_t workspace_bytes, void* stream) {
+int ogm_gather_plan(int64_t n, const int32_t* idx, int64_t window_rows, int64_t tile_rows, int32_t* q2,
+                    int32_t* gdst, uint16_t* lslot, void* workspace, int64_t workspace_bytes, void* stream) {
     using namespace ogm;
     OGM_CHECK_ARG(n >= 0 && n < ((int64_t)1 << 31), OGM_ERR_ARG, "plan size out of range");
-    OGM_CHECK_ARG(tile_rows >= 1, OGM_ERR_ARG, "tile_rows must be positive");
+    OGM_CHECK_ARG(window_rows >= 1 && tile_rows >= 1 && tile_rows <= 65536, OGM_ERR_ARG,
+                  "window_rows must be positive and tile_rows in [1, 65536]");
+    OGM_CHECK_ARG(workspace_bytes >= ogm_gather_plan_workspace_bytes(n), OGM_ERR_ARG, "plan workspace too small");
     if (n == 0) return OGM_OK;
+    const int64_t nwin = (n + window_rows - 1) / window_rows;
+    const int64_t ntiles = (n + tile_rows - 1) / tile_rows;
+    OGM_CHECK_ARG(ntiles * nwin < ((int64_t)1 << 31), OGM_ERR_ARG, "%lld tiles x %lld windows overflow the sort key",
+                  (long long)ntiles, (long long)nwin);
     cudaStream_t st = as_stream(stream);
-    uint8_t* ws = (uint8_t*)workspace;
-    int32_t* inv = (int32_t*)ws;
+    int32_t* inv = (int32_t*)workspace;
     int32_t* key = inv + n;
     int32_t* val = key + n;
     int32_t* skey = val + n;
     int32_t* sval = skey + n;
-    void* temp = (void*)(((uintptr_t)(sval + n) + 255) & ~(uintptr_t)255);
-    size_t temp_bytes = (size_t)(workspace_bytes - ((uint8_t*)temp - ws));
+    int32_t* P = sval + n;
+    void* temp = (void*)(((uintptr_t)(P + n) + 255) & ~(uintptr_t)255);
+    size_t temp_bytes = (size_t)(workspace_bytes - ((uint8_t*)temp - (uint8_t*)workspace));
+    auto bits_for = [](int64_t m) { int b = 1; while ((m - 1) >> b) b++; return b; };
     const int g = grid_for(n);
-    invert_perm_kernel<<<g, 256, 0, st>>>(idx, n, inv);
-    tile_keys_kernel<<<g, 256, 0, st>>>(inv, n, tile_rows, key, val);
-    int end_bit = 1;
-    while (((n - 1) / tile_rows) >> end_bit) end_bit++;
-    OGM_CUDA_TRY(cub::DeviceRadixSort::SortPairs(temp, temp_bytes, key, skey, val, sval, (int)n, 0, end_bit, st));
-    scatter_pos_kernel<<<g, 256, 0, st>>>(sval, n, pos1);
-    local_q_kernel<<<g, 256, 0, st>>>(idx, pos1, n, tile_rows, q2);
+    plan_inv_kernel<<<g, 256, 0, st>>>(idx, n, inv);
+    // I-layout: sources grouped by destination window, source order inside (LSD radix sort is stable)
+    plan_keys_kernel<<<g, 256, 0, st>>>(inv, n, window_rows, 0, nwin, key, val);
+    OGM_CUDA_TRY(cub::DeviceRadixSort::SortPairs(temp, temp_bytes, key, skey, val, sval, (int)n, 0, bits_for(nwin), st));
+    plan_pos_kernel<<<g, 256, 0, st>>>(sval, n, P);
+    plan_q2_kernel<<<g, 256, 0, st>>>(idx, P, n, q2);
+    // pass-1 slots: each tile's rows grouped by destination window, source order inside
+    plan_keys_kernel<<<g, 256, 0, st>>>(inv, n, window_rows, tile_rows, nwin, key, val);
+    OGM_CUDA_TRY(cub::DeviceRadixSort::SortPairs(temp, temp_bytes, key, skey, val, sval, (int)n, 0,
+                                                 bits_for(ntiles * nwin), st));
+    plan_slots_kernel<<<g, 256, 0, st>>>(sval, P, n, tile_rows, gdst, lslot);
     OGM_LAUNCH_CHECK();
     return OGM_OK;
 }
 
-int ogm_gather_planned(int64_t rows, int64_t words, int64_t tile_rows, const int32_t* pos1, const int32_t* q2,
-                       const uint32_t* m1, const uint32_t* m2, const uint32_t* m3, const uint32_t* r_mat,
-                       uint32_t* inter, uint32_t* out, void* stream) {
+int ogm_gather_planned(int64_t rows, int64_t words, int64_t pitch, int64_t tile_rows, const int32_t* q2,
+                       const int32_t* gdst, const uint16_t* lslot, const uint32_t* m1, const uint32_t* m2,
+                       const uint32_t* m3, const uint32_t* r_mat, uint32_t* inter, uint32_t* out, int passes,
+                       void* stream) {
     using namespace ogm;
-    OGM_CHECK_ARG(rows >= 0 && words >= 1 && tile_rows >= 1, OGM_ERR_ARG, "bad planned-gather shape");
-    OGM_CHECK_ARG(m1 && inter && out, OGM_ERR_ARG, "m1, inter and out are required");
+    if (pitch <= 0) pitch = words;
+    OGM_CHECK_ARG(passes >= 1 && passes <= 3, OGM_ERR_ARG, "passes must be 1, 2 or 3 (bit 0 pass 1, bit 1 pass 2)");
+    OGM_CHECK_ARG(rows >= 0 && words >= 1 && pitch >= words, OGM_ERR_ARG, "bad planned-gather shape");
+    OGM_CHECK_ARG(tile_rows >= 1 && tile_rows <= 65536 && tile_rows * pitch * 4 <= (int64_t)kMaxDynSmem,
+                  OGM_ERR_ARG, "tile of %lld rows x %lld words exceeds shared memory", (long long)tile_rows,
+                  (long long)pitch);
+    OGM_CHECK_ARG(q2 && gdst && lslot && m1 && inter && out, OGM_ERR_ARG,
+                  "q2, gdst, lslot, m1, inter and out are required");
     if (rows == 0) return OGM_OK;
     OGM_ENSURE_INIT();
     cudaStream_t st = as_stream(stream);
+    const bool vec = (pitch & 3) == 0 && ((((uintptr_t)m1) | ((uintptr_t)m2) | ((uintptr_t)m3) | ((uintptr_t)r_mat) |
+                                           ((uintptr_t)inter) | ((uintptr_t)out)) & 15) == 0;
+    const size_t smem = (size_t)(tile_rows * pitch * 4);
     const int64_t ntiles = (rows + tile_rows - 1) / tile_rows;
-    int64_t g = ntiles;
-    const int64_t cap = (int64_t)sm_count() * 2;
-    if (g > cap) g = cap;
-    const bool aligned = ((((uintptr_t)m1) | ((uintptr_t)m2) | ((uintptr_t)m3) | ((uintptr_t)r_mat) |
-                           ((uintptr_t)inter) | ((uintptr_t)out)) & 15) == 0;
-    const bool window = tile_rows * words * 4 > kTileBytes;  // L2-window pass 2 instead of smem tiles
-    if (window) {
-        if (words == 4 && aligned) {
-            bucket_scatter4_kernel<<<grid_for(rows), 256, 0, st>>>(pos1, (const uint4*)m1, (const uint4*)m2, rows,
-                                                                   (uint4*)inter);
-            window_gather4_kernel<<<grid_for(rows), 256, 0, st>>>(q2, (const uint4*)inter, (const uint4*)r_mat,
-                                                                  (const uint4*)m3, rows, tile_rows, (uint4*)out);
-        } else {
-            bucket_scatter_kernel<<<grid_for(rows * words), 256, 0, st>>>(pos1, m1, m2, rows, words, inter);
-            window_gather_kernel<<<grid_for(rows * words), 256, 0, st>>>(q2, inter, r_mat, m3, rows, words,
-                                                                         tile_rows, out);
-        }
-    } else if (words == 4 && aligned) {
-        bucket_scatter4_kernel<<<grid_for(rows), 256, 0, st>>>(pos1, (const uint4*)m1, (const uint4*)m2, rows,
-                                                               (uint4*)inter);
-        tile_gather4_kernel<<<(int)g, 512, (size_t)(tile_rows * 16), st>>>(
-            q2, (const uint4*)inter, (const uint4*)r_mat, (const uint4*)m3, rows, (int)tile_rows, (uint4*)out);
+    int per_sm = 1;
+    int64_t g;
+    if (!(passes & 1)) {
+    } else if (vec && pitch == 4 && tile_rows == 4096) {
+        auto k = plan_partition4_kernel<8>;
+        OGM_CUDA_TRY(allow_big_smem(k, (int)smem));
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, 512, smem);
+        g = std::min<int64_t>(std::max<int64_t>(ntiles, 1), (int64_t)sm_count() * std::max(per_sm, 1));
+        k<<<(int)g, 512, smem, st>>>((const uint4*)m1, (const uint4*)m2, lslot, gdst, rows, (uint4*)inter);
+    } else if (vec) {
+        OGM_CUDA_TRY(allow_big_smem(plan_partition_kernel<uint4>, (int)smem));
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, plan_partition_kernel<uint4>, 512, smem);
+        g = std::min<int64_t>(ntiles, (int64_t)sm_count() * std::max(per_sm, 1));
+        plan_partition_kernel<uint4><<<(int)g, 512, smem, st>>>((const uint4*)m1, (const uint4*)m2, lslot, gdst, rows,
+                                                                (int)tile_rows, (int)(pitch / 4), (uint4*)inter);
     } else {
-        bucket_scatter_kernel<<<grid_for(rows * words), 256, 0, st>>>(pos1, m1, m2, rows, words, inter);
-        tile_gather_kernel<<<(int)g, 512, (size_t)(tile_rows * words * 4), st>>>(q2, inter, r_mat, m3, rows,
-                                                                               words, tile_rows, out);
+        OGM_CUDA_TRY(allow_big_smem(plan_partition_kernel<uint32_t>, (int)smem));
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, plan_partition_kernel<uint32_t>, 512, smem);
+        g = std::min<int64_t>(ntiles, (int64_t)sm_count() * std::max(per_sm, 1));
+        plan_partition_kernel<uint32_t><<<(int)g, 512, smem, st>>>(m1, m2, lslot, gdst, rows, (int)tile_rows,
+                                                                   (int)pitch, inter);
+    }
+    if (!(passes & 2)) {
+    } else if (pitch == 4 && vec) {
+        int64_t g2 = std::min<int64_t>((rows + 255) / 256, (int64_t)sm_count() * 8);
+        win_gather4_kernel<<<(int)g2, 256, 0, st>>>(q2, (const uint4*)inter, (const uint4*)m3, (const uint4*)r_mat,
+                                                    rows, (uint4*)out);
+    } else {
+        GatherArgs a{};
+        a.rows = rows;
+        a.W = words;
+        a.width = 32 * words;
+        a.pitch = pitch;
+        a.P1 = q2;
+        a.M1 = inter;
+        a.M3 = m3;
+        if (r_mat) {
+            a.r.on = 2;
+            a.r.mat = r_mat;
+        }
+        a.out = out;
+        launch_matrix_gather(a, st);
     }
     OGM_LAUNCH_CHECK();
     return OGM_OK;

@@ -284,9 +284,10 @@ def test_sharded_sec_eval_slices_equal_unsharded(world):
 
 
 @pytest.mark.parametrize("rows,width", [(1, 128), (1000, 128), (70_001, 129), (300_000, 45), (50_000, 700)])
-def test_planned_gather_equals_direct(rows, width):
-    """Two-pass planned gather == direct gather, bit for bit, incl. ragged
-    last tiles, 5-word rows and wide rows."""
+@pytest.mark.parametrize("window_bytes,tile_rows", [(None, None), (64 << 10, 100)])
+def test_planned_gather_equals_direct(rows, width, window_bytes, tile_rows):
+    """Two-pass L2-window planned gather == direct gather, bit for bit, incl.
+    ragged last windows, 5-word rows, wide rows and many small windows."""
     from paper_2209_03526_b200.prf import seeded_permutation_device
     from paper_2209_03526_b200.shuffle import GatherPlan, gather
     from paper_2209_03526_b200.bits import words_for
@@ -296,14 +297,15 @@ def test_planned_gather_equals_direct(rows, width):
     m1, m2, m3, r = mk(), mk(), mk(), mk()
     idx = seeded_permutation_device(b"\x05" * 16, b"SHPI", 3, rows)
     want = gather(rows, width, torch.empty_like(m1), inner=idx, m1=m1, m2=m2, m3=m3, r=r)
-    got = GatherPlan(idx, w).run(torch.empty_like(m1), m1=m1, m2=m2, m3=m3, r=r)
+    plan = GatherPlan(idx, w, window_bytes=window_bytes, tile_rows=tile_rows)
+    got = plan.run(torch.empty_like(m1), m1=m1, m2=m2, m3=m3, r=r)
     assert torch.equal(got, want)
 
 
 def test_shuffle_planned_path_matches_reference(golden, monkeypatch):
     """The golden shuffle cases again with the planned two-pass gathers forced on."""
     from paper_2209_03526_b200 import shuffle as shmod
-    monkeypatch.setattr(shmod, "PLAN_MIN_ROWS", 1)
+    monkeypatch.setattr(shmod, "PLAN_MIN_BYTES", 0)
     test_shuffle_matches_reference(golden)
 
 
@@ -458,6 +460,23 @@ def test_window_planned_gather_equals_direct(rows, words, window):
     idx = torch.randperm(rows, device="cuda", generator=g).to(torch.int32)
     want = gather(rows, 32 * words, torch.empty_like(M), inner=idx, m1=M, r=R)
     plan = GatherPlan(idx, words, window_bytes=window)
-    assert plan.tile * words * 4 > 96 * 1024  # the L2-window pass 2, not shared-memory tiles
+    assert plan.window == max(1, window // (4 * words))
     got = plan.run(torch.empty_like(M), m1=M, r=R)
     assert torch.equal(got, want)
+
+
+@pytest.mark.parametrize("rows,words,pitch", [(40001, 5, 8), (30000, 4, 8), (20000, 3, 4)])
+def test_planned_gather_pitched_rows(rows, words, pitch):
+    """Planned gather over 16-B-pitched tables (padding words ride along)."""
+    from paper_2209_03526_b200.shuffle import GatherPlan, gather
+
+    g = torch.Generator(device="cuda").manual_seed(rows + pitch)
+    full = lambda: torch.randint(-2**31, 2**31 - 1, (rows, pitch), dtype=torch.int32, device="cuda", generator=g)  # noqa: E731
+    M, R = full(), full()
+    M[:, words:] = 0
+    R[:, words:] = 0
+    idx = torch.randperm(rows, device="cuda", generator=g).to(torch.int32)
+    want = gather(rows, 32 * words, torch.empty_like(M), inner=idx, m1=M, r=R)
+    plan = GatherPlan(idx, pitch, window_bytes=32 << 10, tile_rows=333)
+    got = plan.run(torch.empty_like(M), m1=M, r=R)
+    assert torch.equal(got[:, :words], want[:, :words])
