@@ -240,13 +240,17 @@ def run_c5(args):
         torch.cuda.synchronize()
         t_off = time.perf_counter() - t0
 
-        def online(pre: bool):
+        def online(pre: bool, marks=None):
             # the four party-local steps of src/shuffle.py:106-143 in protocol order
             if pre:
                 off[0].step_x1(comps[0], comps[1], x1)
+                marks and marks[1].record()
                 off[1].step_y1(comps[2], y1)
+                marks and marks[2].record()
                 off[1].step_c1(x1, c1)
+                marks and marks[3].record()
                 off[2].step_r3(y1, c1, r3)
+                marks and marks[4].record()
                 return
             gather(rows, width, x1, outer=pi31, inner=pi12, m1=comps[0], m2=comps[1],
                    t1=(s12, b"SHTB", 0), t2=(s31, b"SHTB", 0))
@@ -274,6 +278,14 @@ def run_c5(args):
                 ev[s + 1].record()
             torch.cuda.synchronize()
             ms = statistics.median(ev[i].elapsed_time(ev[i + 1]) for i in range(args.steps))
+            step_ms = None
+            if pre:
+                marks = events(5)
+                marks[0].record()
+                online(True, marks)
+                torch.cuda.synchronize()
+                step_ms = {k: round(marks[i].elapsed_time(marks[i + 1]), 4)
+                           for i, k in enumerate(("x1 (P1)", "y1 (P2)", "c1 (P2)", "R3 (P3)"))}
             if pre:
                 # algorithmic (protocol) bytes: x1: 2 gathers + U1 + write; y1: gather + V + write;
                 # c1: gather + W + write; R3: gather + c1 + Z + write = 14 row moves (16 B) + 4 index
@@ -289,7 +301,7 @@ def run_c5(args):
                   else "AES-CTR on the fly, nested permutation lookups",
                   "value": nbytes / (ms * 1e-3) / 1e9, "unit": "GB/s", "ms": ms,
                   "hbm_frac": nbytes / (ms * 1e-3) / 1e9 / HBM_PEAK, "algorithmic_bytes_per_row": nbytes // rows,
-                  "rows_per_s": rows / (ms * 1e-3), "offline_perm_s": t_perm, "offline_blinds_s": t_blind,
+                  "rows_per_s": rows / (ms * 1e-3), "step_ms": step_ms, "offline_perm_s": t_perm, "offline_blinds_s": t_blind,
                   "offline_party_material_s": t_off, "bit_exact_recombination": ok})
         del off, pc
         del comps, perms, blinds, x1, y1, c1, r3, r3_pre

@@ -261,26 +261,32 @@ int ogm_shuffle_gather(int64_t rows, int64_t words, int64_t width_bits, const in
  * (gather semantics, so M[out] = M[inner][outer] as in src/shuffle.py:76-77). */
 int ogm_perm_compose(int64_t n, const int32_t* outer, const int32_t* inner, int32_t* out, void* stream);
 
+/* inv[perm[i]] = i (offline: moves a blind from output order to source order). */
+int ogm_perm_invert(int64_t n, const int32_t* perm, int32_t* inv, void* stream);
+
 /* Planned two-pass gather (offline plan for a data-independent permutation):
- * out[i] = (m1 ^ m2)[idx[i]] ^ r_mat[i] ^ m3[i], with bit-identical results
+ * out[i] = (m1 ^ m2 ^ m4)[idx[i]] ^ r_mat[i] ^ m3[i], with bit-identical results
  * to ogm_shuffle_gather, computed as
  *   pass 1: a shared-memory partition of tiles of tile_rows source rows into
- *           `inter` (rows x pitch scratch), one contiguous run per output
- *           window of window_rows rows;
+ *           `inter` (rows x pitch scratch): inter[gdst[k]] = tile[srow[k]],
+ *           one contiguous run per output window of window_rows rows;
  *   pass 2: a gather whose random reads stay inside one contiguous window.
- * ogm_gather_plan derives q2, gdst (n int32 each) and lslot (n uint16) from
+ * ogm_gather_plan derives q2, gdst (n int32 each) and srow (n uint16) from
  * idx; ogm_gather_window_rows / ogm_gather_tile_rows give the defaults for a
- * pitch.  `passes` selects pass 1 (bit 0) and/or pass 2 (bit 1); 3 runs both.
+ * pitch.  m2/m4 are source-order terms XORed in pass 1 (m4: an offline blind
+ * already moved to source order), m3/r_mat output-order terms XORed in pass
+ * 2 -- pass 2 keeps its window L2-resident only with at most one of them
+ * streamed beside it.  `passes` selects pass 1 (bit 0) and/or pass 2 (bit 1).
  * Replaces a direct random-row gather step of src/shuffle.py:106-143. */
 int64_t ogm_gather_window_rows(int64_t pitch_words);
 int64_t ogm_gather_tile_rows(int64_t pitch_words);
 int64_t ogm_gather_plan_workspace_bytes(int64_t n);
 int ogm_gather_plan(int64_t n, const int32_t* idx, int64_t window_rows, int64_t tile_rows, int32_t* q2,
-                    int32_t* gdst, uint16_t* lslot, void* workspace, int64_t workspace_bytes, void* stream);
+                    int32_t* gdst, uint16_t* srow, void* workspace, int64_t workspace_bytes, void* stream);
 int ogm_gather_planned(int64_t rows, int64_t words, int64_t pitch, int64_t tile_rows, const int32_t* q2,
-                       const int32_t* gdst, const uint16_t* lslot, const uint32_t* m1, const uint32_t* m2,
-                       const uint32_t* m3, const uint32_t* r_mat, uint32_t* inter, uint32_t* out, int passes,
-                       void* stream);
+                       const int32_t* gdst, const uint16_t* srow, const uint32_t* m1, const uint32_t* m2,
+                       const uint32_t* m4, const uint32_t* m3, const uint32_t* r_mat, uint32_t* inter, uint32_t* out,
+                       int passes, void* stream);
 
 /* ---- measurement -------------------------------------------------------- */
 

@@ -65,11 +65,12 @@ SIGNATURES = {
     "ogm_shuffle_gather": ([_i64, _i64, _i64, _vp, _vp, _vp, _vp, _vp, _cp, _cp, _u64, _vp, _cp, _cp, _u64,
                             _vp, _cp, _cp, _u64, _vp, _i64, _i64, _vp, _vp], _int),
     "ogm_perm_compose": ([_i64, _vp, _vp, _vp, _vp], _int),
+    "ogm_perm_invert": ([_i64, _vp, _vp, _vp], _int),
     "ogm_gather_window_rows": ([_i64], _i64),
     "ogm_gather_tile_rows": ([_i64], _i64),
     "ogm_gather_plan_workspace_bytes": ([_i64], _i64),
     "ogm_gather_plan": ([_i64, _vp, _i64, _i64, _vp, _vp, _vp, _vp, _i64, _vp], _int),
-    "ogm_gather_planned": ([_i64, _i64, _i64, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _int, _vp], _int),
+    "ogm_gather_planned": ([_i64, _i64, _i64, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _int, _vp], _int),
     "ogm_measure_int_peak": ([ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double)], _int),
 }
 

@@ -333,10 +333,11 @@ __global__ void perm_compose_kernel(const int32_t* __restrict__ outer, const int
 //   I-layout: output window d = [d*Wr, (d+1)*Wr) owns I-region d, holding the
 //             rows its outputs need, ordered by source row; P(j) = position
 //             of source row j in I.
-//   pass 1 (partition): a CTA loads a tile of T consecutive source rows
-//             (coalesced), places row j at shared slot lslot[j] (tile rows
-//             grouped by destination region, source order within a group),
-//             then writes slot k to I[gdst[k]]: one contiguous run per region.
+//   pass 1 (partition): a CTA stages a tile of T consecutive source rows in
+//             shared memory (TMA bulk copies, double-buffered), then writes
+//             I[gdst[k]] = tile[srow[k]] for slots k in order: slots are the
+//             tile's rows grouped by destination region (source order inside
+//             a group), so the writes form one contiguous run per region.
 //   pass 2 (window gather): out[i] = I[q2[i]] ^ R[i] ^ M3[i], q2[i] =
 //             P(idx[i]) lies in region d(i): random reads inside one
 //             contiguous window, sequential writes.
@@ -376,19 +377,23 @@ __global__ void plan_q2_kernel(const int32_t* __restrict__ idx, const int32_t* _
 }
 
 __global__ void plan_slots_kernel(const int32_t* __restrict__ sj2, const int32_t* __restrict__ P, int64_t n,
-                                  int64_t T, int32_t* __restrict__ gdst, uint16_t* __restrict__ lslot) {
+                                  int64_t T, int32_t* __restrict__ gdst, uint16_t* __restrict__ srow) {
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += stride) {
-        const int32_t j = __ldg(sj2 + k);
+        const int32_t j = __ldg(sj2 + k);  // same tile as k: the sort key leads with the tile
         gdst[k] = __ldg(P + j);
-        lslot[j] = (uint16_t)(k % T);
+        srow[k] = (uint16_t)(j % T);
     }
 }
 
-// pass 1 in units U (uint4 for 16-B-multiple pitches, else words); wu = pitch in U
+// Generic pass 1 in units U (uint4 for 16-B-multiple pitches, else words);
+// wu = pitch in U.  Stores are evict-first: L2 appears to keep evict-normal
+// DIRTY lines ahead of clean ones, so normal stores here leave pass 2 an L2
+// in which its window does not stay resident (pass 2 measured 2.26 -> 5.5
+// ms, DRAM reads 9.7 -> 28.6 GB; profiles/r01_c5_plan.md).
 template <typename U>
 __global__ void __launch_bounds__(512) plan_partition_kernel(const U* __restrict__ m1, const U* __restrict__ m2,
-                                                             const uint16_t* __restrict__ lslot,
+                                                             const U* __restrict__ m4, const uint16_t* __restrict__ srow,
                                                              const int32_t* __restrict__ gdst, int64_t rows, int T,
                                                              int wu, U* __restrict__ inter) {
     extern __shared__ __align__(16) unsigned char part_smem[];
@@ -400,70 +405,123 @@ __global__ void __launch_bounds__(512) plan_partition_kernel(const U* __restrict
         const int ne = nr * wu;
         const U* a = m1 + r0 * wu;
         const U* b = m2 ? m2 + r0 * wu : nullptr;
+        const U* d = m4 ? m4 + r0 * wu : nullptr;
         for (int e = threadIdx.x; e < ne; e += blockDim.x) {
-            const int r = wu == 1 ? e : e / wu;
             U v = __ldcs(a + e);
             if (b) v = xorU(v, __ldcs(b + e));
-            tile[(int)__ldcs(lslot + r0 + r) * wu + (e - r * wu)] = v;
+            if (d) v = xorU(v, __ldcs(d + e));
+            tile[e] = v;
         }
         __syncthreads();
         for (int e = threadIdx.x; e < ne; e += blockDim.x) {
             const int k = wu == 1 ? e : e / wu;
-            __stcs(inter + (int64_t)__ldcs(gdst + r0 + k) * wu + (e - k * wu), tile[e]);
+            const int c = e - k * wu;
+            __stcs(inter + (int64_t)__ldcs(gdst + r0 + k) * wu + c, tile[(int)__ldcs(srow + r0 + k) * wu + c]);
         }
         __syncthreads();
     }
 }
 
-// pass 1 for 16-byte rows: every thread keeps RPT loads (and RPT index
-// loads) in flight per phase instead of one, so a CTA's load and store
-// phases each cost one memory latency.  Stores are evict-first: L2 appears
-// to keep evict-normal DIRTY lines ahead of clean ones, so normal stores here
-// leave pass 2 an L2 in which its window does not stay resident (pass 2
-// measured 2.26 -> 5.5 ms, DRAM reads 9.7 -> 28.6 GB; profiles/r01_c5_plan.md)
-template <int RPT>
-__global__ void __launch_bounds__(512) plan_partition4_kernel(const uint4* __restrict__ m1, const uint4* __restrict__ m2,
-                                                              const uint16_t* __restrict__ lslot,
-                                                              const int32_t* __restrict__ gdst, int64_t rows,
-                                                              uint4* __restrict__ inter) {
-    extern __shared__ __align__(16) unsigned char part_smem[];
-    uint4* tile = reinterpret_cast<uint4*>(part_smem);
-    constexpr int T = RPT * 512;
+// ---- TMA-staged pass 1 for 16-byte rows (the C5 shape) --------------------
+// One persistent CTA per SM; stage s holds a tile's rows, srow and gdst,
+// filled by cp.async.bulk on mbarrier s.  While the CTA writes tile t out,
+// tile t + grid is already in flight, so no thread ever waits on a load
+// except at the very start.  m2 (x1's a ^ b) is read per slot straight from
+// global, and so is m4 (a source-order blind): their reads stay inside the
+// tile's 64 KB of each (one DRAM page set).
+constexpr int kTmaTile = 4096;
+constexpr int kTmaThreads = 1024;
+constexpr int kTmaStageBytes = kTmaTile * (16 + 2 + 4);
+constexpr int kTmaSmemBytes = 2 * kTmaStageBytes + 64;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+
+__global__ void __launch_bounds__(kTmaThreads, 1) plan_partition_tma_kernel(
+    const uint4* __restrict__ m1, const uint4* __restrict__ m2, const uint4* __restrict__ m4,
+    const uint16_t* __restrict__ srow, const int32_t* __restrict__ gdst, int64_t rows, uint4* __restrict__ inter) {
+    extern __shared__ __align__(128) unsigned char tma_smem[];
+    constexpr int T = kTmaTile;
+    uint64_t* bar = reinterpret_cast<uint64_t*>(tma_smem + 2 * kTmaStageBytes);
+    auto rows_of = [&](int s) { return reinterpret_cast<uint4*>(tma_smem + s * kTmaStageBytes); };
+    auto srow_of = [&](int s) { return reinterpret_cast<uint16_t*>(tma_smem + s * kTmaStageBytes + T * 16); };
+    auto gdst_of = [&](int s) { return reinterpret_cast<int32_t*>(tma_smem + s * kTmaStageBytes + T * 18); };
     const int64_t nfull = rows / T;
-    for (int64_t t = blockIdx.x; t < nfull; t += gridDim.x) {
-        const int64_t r0 = t * T + threadIdx.x;
-        uint4 v[RPT];
-        int sl[RPT];
-#pragma unroll
-        for (int k = 0; k < RPT; k++) {
-            v[k] = __ldcs(m1 + r0 + k * 512);
-            sl[k] = __ldcs(lslot + r0 + k * 512);
-        }
-        if (m2) {
-#pragma unroll
-            for (int k = 0; k < RPT; k++) v[k] = xor4(v[k], __ldcs(m2 + r0 + k * 512));
-        }
-#pragma unroll
-        for (int k = 0; k < RPT; k++) tile[sl[k]] = v[k];
-        __syncthreads();
-        int gd[RPT];
-#pragma unroll
-        for (int k = 0; k < RPT; k++) gd[k] = __ldcs(gdst + r0 + k * 512);
-#pragma unroll
-        for (int k = 0; k < RPT; k++) __stcs(inter + gd[k], tile[threadIdx.x + k * 512]);
-        __syncthreads();
+    const int64_t G = gridDim.x;
+    if (threadIdx.x == 0) {
+        mbar_init(&bar[0], 1);
+        mbar_init(&bar[1], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-    // ragged last tile (rows % T): one CTA, one row per thread-step
-    if (blockIdx.x == gridDim.x - 1 && rows % T) {
+    __syncthreads();
+    auto issue = [&](int64_t t, int s) {
+        mbar_expect_tx(&bar[s], kTmaStageBytes);
+        bulk_g2s(rows_of(s), m1 + t * T, T * 16, &bar[s]);
+        bulk_g2s(srow_of(s), srow + t * T, T * 2, &bar[s]);
+        bulk_g2s(gdst_of(s), gdst + t * T, T * 4, &bar[s]);
+    };
+    if (threadIdx.x == 0) {
+        if (blockIdx.x < nfull) issue(blockIdx.x, 0);
+        if (blockIdx.x + G < nfull) issue(blockIdx.x + G, 1);
+    }
+    uint32_t parity = 0;  // bit s: phase of stage s
+    int s = 0;
+    for (int64_t t = blockIdx.x; t < nfull; t += G) {
+        mbar_wait(&bar[s], (parity >> s) & 1);
+        parity ^= 1u << s;
+        const uint4* rs = rows_of(s);
+        const uint16_t* sr = srow_of(s);
+        const int32_t* gd = gdst_of(s);
+        const uint4* b = m2 ? m2 + t * T : nullptr;
+        const uint4* d = m4 ? m4 + t * T : nullptr;
+#pragma unroll
+        for (int q = 0; q < T / kTmaThreads; q++) {
+            const int k = threadIdx.x + q * kTmaThreads;
+            const int j = sr[k];
+            uint4 v = rs[j];
+            if (b) v = xor4(v, __ldcg(b + j));
+            if (d) v = xor4(v, __ldcg(d + j));
+            __stcs(inter + gd[k], v);
+        }
+        __syncthreads();  // stage s fully read before it is refilled
+        if (threadIdx.x == 0 && t + 2 * G < nfull) issue(t + 2 * G, s);
+        s ^= 1;
+    }
+    // ragged last tile (rows % T): the last CTA, straight from global
+    if (blockIdx.x == G - 1 && rows % T) {
         const int64_t b0 = nfull * T;
         const int nr = (int)(rows - b0);
-        for (int e = threadIdx.x; e < nr; e += 512) {
-            uint4 x = __ldcs(m1 + b0 + e);
-            if (m2) x = xor4(x, __ldcs(m2 + b0 + e));
-            tile[__ldcs(lslot + b0 + e)] = x;
+        for (int k = threadIdx.x; k < nr; k += kTmaThreads) {
+            const int j = __ldcs(srow + b0 + k);
+            uint4 v = __ldcs(m1 + b0 + j);
+            if (m2) v = xor4(v, __ldcs(m2 + b0 + j));
+            if (m4) v = xor4(v, __ldcs(m4 + b0 + j));
+            __stcs(inter + __ldcs(gdst + b0 + k), v);
         }
-        __syncthreads();
-        for (int e = threadIdx.x; e < nr; e += 512) __stcs(inter + __ldcs(gdst + b0 + e), tile[e]);
     }
 }
 
@@ -602,6 +660,14 @@ int ogm_seeded_permutation(const uint8_t* key, const uint8_t* label, uint64_t in
     return ogm::seeded_permutation_impl(key, label, index, n, perm, workspace, ogm::as_stream(stream));
 }
 
+int ogm_perm_invert(int64_t n, const int32_t* perm, int32_t* inv, void* stream) {
+    OGM_CHECK_ARG(n >= 0 && n < ((int64_t)1 << 31), OGM_ERR_ARG, "permutation size out of range");
+    if (n == 0) return OGM_OK;
+    ogm::plan_inv_kernel<<<ogm::grid_for(n), 256, 0, ogm::as_stream(stream)>>>(perm, n, inv);
+    OGM_LAUNCH_CHECK();
+    return OGM_OK;
+}
+
 int ogm_perm_compose(int64_t n, const int32_t* outer, const int32_t* inner, int32_t* out, void* stream) {
     OGM_CHECK_ARG(n >= 0, OGM_ERR_ARG, "negative length");
     if (n == 0) return OGM_OK;
@@ -706,7 +772,7 @@ int64_t ogm_gather_plan_workspace_bytes(int64_t n) {
 }
 
 int ogm_gather_plan(int64_t n, const int32_t* idx, int64_t window_rows, int64_t tile_rows, int32_t* q2,
-                    int32_t* gdst, uint16_t* lslot, void* workspace, int64_t workspace_bytes, void* stream) {
+                    int32_t* gdst, uint16_t* srow, void* workspace, int64_t workspace_bytes, void* stream) {
     using namespace ogm;
     OGM_CHECK_ARG(n >= 0 && n < ((int64_t)1 << 31), OGM_ERR_ARG, "plan size out of range");
     OGM_CHECK_ARG(window_rows >= 1 && tile_rows >= 1 && tile_rows <= 65536, OGM_ERR_ARG,
@@ -738,15 +804,15 @@ int ogm_gather_plan(int64_t n, const int32_t* idx, int64_t window_rows, int64_t 
     plan_keys_kernel<<<g, 256, 0, st>>>(inv, n, window_rows, tile_rows, nwin, key, val);
     OGM_CUDA_TRY(cub::DeviceRadixSort::SortPairs(temp, temp_bytes, key, skey, val, sval, (int)n, 0,
                                                  bits_for(ntiles * nwin), st));
-    plan_slots_kernel<<<g, 256, 0, st>>>(sval, P, n, tile_rows, gdst, lslot);
+    plan_slots_kernel<<<g, 256, 0, st>>>(sval, P, n, tile_rows, gdst, srow);
     OGM_LAUNCH_CHECK();
     return OGM_OK;
 }
 
 int ogm_gather_planned(int64_t rows, int64_t words, int64_t pitch, int64_t tile_rows, const int32_t* q2,
-                       const int32_t* gdst, const uint16_t* lslot, const uint32_t* m1, const uint32_t* m2,
-                       const uint32_t* m3, const uint32_t* r_mat, uint32_t* inter, uint32_t* out, int passes,
-                       void* stream) {
+                       const int32_t* gdst, const uint16_t* srow, const uint32_t* m1, const uint32_t* m2,
+                       const uint32_t* m4, const uint32_t* m3, const uint32_t* r_mat, uint32_t* inter, uint32_t* out,
+                       int passes, void* stream) {
     using namespace ogm;
     if (pitch <= 0) pitch = words;
     OGM_CHECK_ARG(passes >= 1 && passes <= 3, OGM_ERR_ARG, "passes must be 1, 2 or 3 (bit 0 pass 1, bit 1 pass 2)");
@@ -754,35 +820,35 @@ int ogm_gather_planned(int64_t rows, int64_t words, int64_t pitch, int64_t tile_
     OGM_CHECK_ARG(tile_rows >= 1 && tile_rows <= 65536 && tile_rows * pitch * 4 <= (int64_t)kMaxDynSmem,
                   OGM_ERR_ARG, "tile of %lld rows x %lld words exceeds shared memory", (long long)tile_rows,
                   (long long)pitch);
-    OGM_CHECK_ARG(q2 && gdst && lslot && m1 && inter && out, OGM_ERR_ARG,
-                  "q2, gdst, lslot, m1, inter and out are required");
+    OGM_CHECK_ARG(q2 && gdst && srow && m1 && inter && out, OGM_ERR_ARG,
+                  "q2, gdst, srow, m1, inter and out are required");
     if (rows == 0) return OGM_OK;
     OGM_ENSURE_INIT();
     cudaStream_t st = as_stream(stream);
     const bool vec = (pitch & 3) == 0 && ((((uintptr_t)m1) | ((uintptr_t)m2) | ((uintptr_t)m3) | ((uintptr_t)r_mat) |
-                                           ((uintptr_t)inter) | ((uintptr_t)out)) & 15) == 0;
+                                           ((uintptr_t)m4) | ((uintptr_t)inter) | ((uintptr_t)out)) & 15) == 0;
     const size_t smem = (size_t)(tile_rows * pitch * 4);
     const int64_t ntiles = (rows + tile_rows - 1) / tile_rows;
     int per_sm = 1;
     int64_t g;
     if (!(passes & 1)) {
-    } else if (vec && pitch == 4 && tile_rows == 4096) {
-        auto k = plan_partition4_kernel<8>;
-        OGM_CUDA_TRY(allow_big_smem(k, (int)smem));
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, 512, smem);
-        g = std::min<int64_t>(std::max<int64_t>(ntiles, 1), (int64_t)sm_count() * std::max(per_sm, 1));
-        k<<<(int)g, 512, smem, st>>>((const uint4*)m1, (const uint4*)m2, lslot, gdst, rows, (uint4*)inter);
+    } else if (vec && pitch == 4 && tile_rows == kTmaTile) {
+        OGM_CUDA_TRY(allow_big_smem(plan_partition_tma_kernel, kTmaSmemBytes));
+        g = std::min<int64_t>(std::max<int64_t>(ntiles, 1), (int64_t)sm_count());
+        plan_partition_tma_kernel<<<(int)g, kTmaThreads, kTmaSmemBytes, st>>>(
+            (const uint4*)m1, (const uint4*)m2, (const uint4*)m4, srow, gdst, rows, (uint4*)inter);
     } else if (vec) {
         OGM_CUDA_TRY(allow_big_smem(plan_partition_kernel<uint4>, (int)smem));
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, plan_partition_kernel<uint4>, 512, smem);
         g = std::min<int64_t>(ntiles, (int64_t)sm_count() * std::max(per_sm, 1));
-        plan_partition_kernel<uint4><<<(int)g, 512, smem, st>>>((const uint4*)m1, (const uint4*)m2, lslot, gdst, rows,
+        plan_partition_kernel<uint4><<<(int)g, 512, smem, st>>>((const uint4*)m1, (const uint4*)m2, (const uint4*)m4,
+                                                                srow, gdst, rows,
                                                                 (int)tile_rows, (int)(pitch / 4), (uint4*)inter);
     } else {
         OGM_CUDA_TRY(allow_big_smem(plan_partition_kernel<uint32_t>, (int)smem));
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, plan_partition_kernel<uint32_t>, 512, smem);
         g = std::min<int64_t>(ntiles, (int64_t)sm_count() * std::max(per_sm, 1));
-        plan_partition_kernel<uint32_t><<<(int)g, 512, smem, st>>>(m1, m2, lslot, gdst, rows, (int)tile_rows,
+        plan_partition_kernel<uint32_t><<<(int)g, 512, smem, st>>>(m1, m2, m4, srow, gdst, rows, (int)tile_rows,
                                                                    (int)pitch, inter);
     }
     if (!(passes & 2)) {

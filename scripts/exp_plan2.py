@@ -33,7 +33,7 @@ out = torch.empty_like(M)
 inter = torch.empty_like(M)
 print(f"direct            {t(lambda: gather(rows, 128, out, inner=idx, m1=M, r=R)):.3f} ms")
 want = out.clone()
-for wb in (8 << 20,):
+for wb in [int(x) << 20 for x in (sys.argv[2].split(",") if len(sys.argv) > 2 else ["8"])]:
     for tr in (4096,):
         plan = GatherPlan(idx, 4, window_bytes=wb, tile_rows=tr)
         tt = t(lambda: plan.run(out, m1=M, r=R, inter=inter))
@@ -41,7 +41,8 @@ for wb in (8 << 20,):
         t1 = t(lambda: plan.run(out, m1=M, r=R, inter=inter, passes=1))
         t2 = t(lambda: plan.run(out, m1=M, r=R, inter=inter, passes=2))
         print(f"planned window {wb >> 20:2d} MB tile {tr:5d}: {tt:.3f} ms (pass 1 alone {t1:.3f}, pass 2 alone {t2:.3f})")
-
+if len(sys.argv) > 3:
+    sys.exit(0)
 # alternating sequence with an event after every pass: which pass slows down?
 plan = GatherPlan(idx, 4, window_bytes=8 << 20, tile_rows=4096)
 ev = [torch.cuda.Event(enable_timing=True) for _ in range(13)]
