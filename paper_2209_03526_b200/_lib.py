@@ -74,13 +74,18 @@ SIGNATURES = {
     "ogm_measure_int_peak": ([ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double)], _int),
 }
 
+# Entry points that may block on the device (host syncs); every other entry
+# point only enqueues work on the caller's stream and returns in microseconds.
+BLOCKING = {"ogm_init", "ogm_seeded_permutation", "ogm_fss_eval_points_host", "ogm_measure_int_peak"}
+
 _lib = None
+_fast = None
 _device_ok = False
 
 
 def load(require_device: bool = True):
     """Load the library (and, by default, insist on a CUDA device)."""
-    global _lib, _device_ok
+    global _lib, _fast, _device_ok
     if _lib is not None and (_device_ok or not require_device):
         return _lib
     if _lib is None:
@@ -89,11 +94,17 @@ def load(require_device: bool = True):
                 f"{LIB_PATH} is missing: build it with `python -m paper_2209_03526_b200.build` "
                 "(there is no CPU fallback)")
         lib = ctypes.CDLL(str(LIB_PATH))
+        # the same library through PyDLL: calls keep the GIL.  For the
+        # non-blocking launchers that beats releasing it -- with three party
+        # threads, every released GIL has to be won back (measured on the
+        # per-party C1 path)
+        fast = ctypes.PyDLL(str(LIB_PATH))
         for name, (args, res) in SIGNATURES.items():
-            fn = getattr(lib, name)
-            fn.argtypes = args
-            fn.restype = res
-        _lib = lib
+            for h in (lib, fast):
+                fn = getattr(h, name)
+                fn.argtypes = args
+                fn.restype = res
+        _lib, _fast = lib, fast
     if require_device:
         if not torch.cuda.is_available():
             raise RuntimeError("paper_2209_03526_b200 needs a CUDA device (no CPU fallback)")
@@ -120,7 +131,8 @@ _fns: dict = {}
 def call(name: str, *args) -> None:
     fn = _fns.get(name)
     if fn is None:
-        fn = _fns[name] = getattr(load(), name)
+        load()
+        fn = _fns[name] = getattr(_lib if name in BLOCKING else _fast, name)
     rc = fn(*args)
     if rc:
         check(rc)

@@ -142,7 +142,7 @@ __global__ void __launch_bounds__(256) masked_parity_v2_kernel(const ParityArgs 
     constexpr int NCOMP = NPARTY == 1 ? 2 : 3;
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
-    const int RG = 8 / CW;
+    const int RG = (int)(blockDim.x >> 5) / CW;  // row groups per CTA (CW need not be a power of 2)
     const int rg = warp / CW, wc = warp % CW;
     const int64_t col0 = ((int64_t)blockIdx.x * CW + wc) * 128 + lane * 4;  // first word of this lane
     uint4 ia[NJ], ib[NJ];
@@ -738,22 +738,24 @@ int ogm_masked_parity(int64_t rows, int64_t words, int64_t pitch, int ncomp, con
     cudaStream_t st = as_stream(stream);
     if (aligned && words >= 64) {
         // register-resident indicators; CW warps (x128 columns) per row group
-        int CW = 1;
-        while (CW < 8 && CW * 128 < words) CW <<= 1;
+        // as many 128-word warp columns as the row needs (<= 8): at w = 313 (the
+        // Zipf attributes of C3/C4) 3 warps keep 82% of lanes live where a
+        // power-of-two 4 kept 61%
+        const int CW = (int)std::min<int64_t>(8, (words + 127) / 128);
         const int64_t col_chunks = (words + CW * 128 - 1) / (CW * 128);
         const int64_t ntiles = (rows + 31) / 32;
         const int64_t want_blocks = (int64_t)sm_count() * 6;
         int64_t row_blocks = want_blocks / col_chunks;
         if (row_blocks < 1) row_blocks = 1;
         if (row_blocks > 65535) row_blocks = 65535;
-        const int RG = 8 / CW;
+        const int RG = std::max(1, 8 / CW);
         int64_t tpb = (ntiles + row_blocks - 1) / row_blocks;
         tpb = (tpb + RG - 1) / RG * RG;
         row_blocks = (ntiles + tpb - 1) / tpb;
         for (int j = 0; j < npass * nparty; j++)
             OGM_CUDA_TRY(cudaMemsetAsync(out[j], 0, 4 * ntiles, st));
         dim3 grid((unsigned)col_chunks, (unsigned)row_blocks);
-#define OGM_PARITY2(NP, NS) masked_parity_v2_kernel<NP, NS><<<grid, 256, 0, st>>>(p, CW, tpb)
+#define OGM_PARITY2(NP, NS) masked_parity_v2_kernel<NP, NS><<<grid, 32 * RG * CW, 0, st>>>(p, CW, tpb)
         if (nparty == 1 && npass == 1) OGM_PARITY2(1, 1);
         else if (nparty == 1) OGM_PARITY2(1, 2);
         else if (npass == 1) OGM_PARITY2(3, 1);
