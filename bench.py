@@ -21,6 +21,9 @@ seeded inputs (keys generated on the device by ogm_fss_gen from seeded roots).
   query latency"): the C1 tiny oblivious match, tokens in -> reconstructed
   matches, via the trio fast path and via the per-party drop-in API, both
   checked against the plaintext matcher (rank 0).
+* ``c4_sec_eval`` -- the 16M-vertex config (BASELINE configs[3]): root-slot
+  secEval over 2M candidates, rows sharded over all N ranks with an NCCL
+  all-gather of the match bits (strong scaling, max over ranks).
 * ``cpu_baseline`` -- the CPU oracle port (oracle/, C, all host threads) on a
   bounded sample of the same workload, rank 0 only.
 
@@ -75,6 +78,7 @@ def parse():
     p.add_argument("--cpu-seconds", type=float, default=10.0)
     p.add_argument("--no-query", action="store_true", help="skip the C1 end-to-end query latency")
     p.add_argument("--query-steps", type=int, default=10)
+    p.add_argument("--no-c4", action="store_true", help="skip the C4 sharded secEval leg")
     return p.parse_args()
 
 
@@ -384,6 +388,14 @@ def main():
     if rank == 0 and not args.no_query:
         query = query_latency(args.query_steps)
 
+    # the 16M-vertex config (BASELINE configs[3]): row-sharded secEval over all ranks
+    c4 = None
+    if not args.no_c4:
+        import bench_configs
+        del b0, pts, out
+        torch.cuda.empty_cache()
+        c4 = bench_configs.c4_sec_eval(2_000_000, 1, 10, 3, rank, world)
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         import oracle
@@ -403,7 +415,7 @@ def main():
                        "keys_per_gpu": K, "domain_bits": BITS, "points_per_key": 1,
                        "parallelism": f"key-sharded x{world}",
                        "l2": "inputs (9.1 GB of keys) larger than L2; no flush"},
-            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "query_latency": query,
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "query_latency": query, "c4_sec_eval": c4,
             "gpu_launches": args.steps, "clocks": clk,
             "launch_ms": {"mean": statistics.mean(per_launch), "min": min(per_launch),
                           "max": max(per_launch)},

@@ -36,7 +36,16 @@ from paper_2209_03526_b200.shuffle import ShuffleOffline, blind_table, gather  #
 from paper_2209_03526_b200.prf import seeded_permutation_device  # noqa: E402
 from paper_2209_03526_b200 import workloads  # noqa: E402
 
-HBM_PEAK = 6553.0  # GB/s, MEASURED_PEAKS.json (copy benchmark on this pool)
+def _hbm_peak() -> float:
+    """GB/s: MEASURED_PEAKS.json (driver-written copy benchmark) when present,
+    else its last recorded value for this pool."""
+    try:
+        return float(json.load(open(Path(__file__).resolve().parent / "MEASURED_PEAKS.json"))["hbm_gbs"])
+    except (OSError, KeyError, ValueError):
+        return 6535.4
+
+
+HBM_PEAK = _hbm_peak()
 
 
 def emit(d):
@@ -408,31 +417,28 @@ def run_c3_pipeline(args):
 # ---------------------------------------------------------------------------
 
 
-def run_c4(args):
-    import os
-
+def c4_sec_eval(rows: int, seed: int, steps: int, warmup: int, rank: int, world: int) -> dict:
+    """C4 (BASELINE configs[3]) root-slot secEval, row-sharded over `world`
+    ranks (an initialised NCCL group when world > 1): 2M candidates of one
+    vertex type (16M vertices / 8 types), Zipf(1.1) attribute over 10^4
+    values, an interval predicate (2 DCF passes) for all three parties, match
+    bits all-gathered.  Strong scaling; device time max over ranks."""
     import torch.distributed as dist
 
     from paper_2209_03526_b200.sharding import ShardPlan, sharded_sec_eval_trio
 
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    rows, n = args.c4_rows, 10_000  # 2M vertices of the root type; Zipf(1.1) over 10^4 values
+    n = 10_000
     plan = ShardPlan(rows, world)
     lo, hi = plan.bounds(rank)
-    rng = np.random.default_rng(args.seed)
+    rng = np.random.default_rng(seed)
     ranks = np.arange(1, n + 1)
     p = 1.0 / ranks ** 1.1
     vals_all = rng.choice(n, size=rows, p=p / p.sum()).astype(np.int32)
     vals = torch.from_numpy(vals_all[lo:hi]).cuda()
-    c1, c2, c3 = workloads.shared_one_hot(vals, n, args.seed + rank, 40)
+    c1, c2, c3 = workloads.shared_one_hot(vals, n, seed + rank, 40)
     comps = [c1, c2, c3]
     w = words_for(n)
-    krng = np.random.default_rng(args.seed + 1)  # identical keys on every rank
+    krng = np.random.default_rng(seed + 1)  # identical keys on every rank
     pairs = [fss.ic_gen(100, 4000, n, krng) for _ in range(3)]
     (k11, k21), (k12, k22), (k13, k23) = pairs
     keys = [(k11, k12), (k22, k13), (k23, k21)]
@@ -442,30 +448,46 @@ def run_c4(args):
     cfg = make_session_configs(b"\x44" * 16)
     zk = [(c.zero_key_own, c.zero_key_prev) for c in cfg]
     step = lambda: sharded_sec_eval_trio(comps, w, plan, rank, inds, zk, [0, 1])  # noqa: E731
-    for _ in range(args.warmup):
+    for _ in range(warmup):
         step()
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     ev = events(2)
     ev[0].record()
-    for _ in range(args.steps):
+    for _ in range(steps):
         res = step()
     ev[1].record()
     torch.cuda.synchronize()
-    ms = ev[0].elapsed_time(ev[1]) / args.steps
+    ms = ev[0].elapsed_time(ev[1]) / steps
     t = torch.tensor([ms], device="cuda")
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms = float(t.item())
+    nbytes_local = 3 * (hi - lo) * w * 4
+    return {"config": f"C4 root secEval, {rows} candidates (Zipf attr n={n}, w={w}), interval, "
+                      f"rows sharded x{world}", "metric": "secEval_candidates_per_s",
+            "value": rows / (ms * 1e-3), "unit": "candidates/s", "ms_per_step": ms, "n_gpus": world,
+            "scaling": "strong", "rank0_hbm_GBps": nbytes_local / (ms * 1e-3) / 1e9,
+            "rank0_hbm_frac": nbytes_local / (ms * 1e-3) / 1e9 / HBM_PEAK,
+            "collective": "NCCL all_gather of packed blinded match bits" if world > 1 else "none",
+            "result_words": int(res[0][0].numel())}
+
+
+def run_c4(args):
+    import os
+
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    line = c4_sec_eval(args.c4_rows, args.seed, args.steps, args.warmup, rank, world)
     if rank == 0:
-        nbytes_local = 3 * (hi - lo) * w * 4
-        emit({"config": f"C4 root secEval, {rows} candidates (Zipf attr n={n}, w={w}), interval, "
-                        f"rows sharded x{world}", "metric": "secEval_candidates_per_s",
-              "value": rows / (ms * 1e-3), "unit": "candidates/s", "ms_per_step": ms, "n_gpus": world,
-              "scaling": "strong", "rank0_hbm_GBps": nbytes_local / (ms * 1e-3) / 1e9,
-              "collective": "NCCL all_gather of packed blinded match bits" if world > 1 else "none",
-              "result_words": int(res[0][0].numel())})
+        emit(line)
     if world > 1:
         dist.destroy_process_group()
 

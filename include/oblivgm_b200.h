@@ -149,6 +149,13 @@ int ogm_zero_share_trio(const uint8_t* k1, const uint8_t* k2, const uint8_t* k3,
                         int64_t nbits, const uint32_t* const* xor_into, uint32_t* const* out,
                         void* stream);
 
+/* The same for words [w0, w0 + nwords) of the nbits-bit vector (w0 % 4 == 0),
+ * written to out[q][0 .. nwords): one rank's slice of a row-sharded secEval
+ * (SURVEY 8(e)); the tail mask applies only to the vector's last word. */
+int ogm_zero_share_trio_slice(const uint8_t* k1, const uint8_t* k2, const uint8_t* k3, uint64_t counter,
+                              int64_t nbits, int64_t w0, int64_t nwords, const uint32_t* const* xor_into,
+                              uint32_t* const* out, void* stream);
+
 /* src/rss.py:115-126 and_terms for nparty (1..3) parties: out[q] =
  * a_a[q]&b_a[q] ^ a_a[q]&b_b[q] ^ a_b[q]&b_a[q] over nwords words. */
 int ogm_and_terms(int64_t nwords, int nparty, const uint32_t* const* a_a, const uint32_t* const* a_b,

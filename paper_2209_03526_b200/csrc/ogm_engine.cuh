@@ -222,15 +222,18 @@ struct Zs3Args {
 
 __global__ void __launch_bounds__(kAesThreads) zero_share3_kernel(const Zs3Args a, uint32_t label_be,
                                                                    uint64_t counter, int64_t nwords,
-                                                                   int64_t nbits) {
+                                                                   int64_t nbits, int64_t w0, int64_t nloc) {
+    // words [w0, w0 + nloc) of the nwords-word stream (w0 % 4 == 0: whole
+    // CTR blocks), written to out[q][0 .. nloc)
     extern __shared__ __align__(128) uint8_t smem_raw[];
     aes_fill_tables(smem_raw);
     __syncthreads();
     const AesTab T(smem_raw);
-    const int64_t nblk = (nwords + 3) >> 2;
+    const int64_t nblk = (nloc + 3) >> 2;
+    const int64_t b0 = w0 >> 2;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     for (int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b < nblk; b += stride) {
-        const uint4 ctr = ctr_block(label_be, counter, (uint64_t)b);
+        const uint4 ctr = ctr_block(label_be, counter, (uint64_t)(b0 + b));
         uint4 f[3];
 #pragma unroll
         for (int q = 0; q < 3; q++) f[q] = aes128_enc(T, ctr, ParamKey{a.k[q].rk});
@@ -241,10 +244,10 @@ __global__ void __launch_bounds__(kAesThreads) zero_share3_kernel(const Zs3Args 
 #pragma unroll
             for (int j = 0; j < 4; j++) {
                 const int64_t o = b * 4 + j;
-                if (o >= nwords) break;
+                if (o >= nloc) break;
                 uint32_t v = zw[j];
                 if (a.xin[q]) v ^= a.xin[q][o];
-                if (o == nwords - 1 && (nbits & 31)) v &= (1u << (nbits & 31)) - 1u;
+                if (w0 + o == nwords - 1 && (nbits & 31)) v &= (1u << (nbits & 31)) - 1u;
                 a.out[q][o] = v;
             }
         }
@@ -790,12 +793,17 @@ int ogm_masked_parity(int64_t rows, int64_t words, int64_t pitch, int ncomp, con
     return OGM_OK;
 }
 
-int ogm_zero_share_trio(const uint8_t* k1, const uint8_t* k2, const uint8_t* k3, uint64_t counter,
-                        int64_t nbits, const uint32_t* const* xor_into, uint32_t* const* out, void* stream) {
+static int zero_share_trio_impl(const uint8_t* k1, const uint8_t* k2, const uint8_t* k3, uint64_t counter,
+                                int64_t nbits, int64_t w0, int64_t nloc, const uint32_t* const* xor_into,
+                                uint32_t* const* out, void* stream) {
     using namespace ogm;
     OGM_CHECK_ARG(k1 && k2 && k3 && out, OGM_ERR_ARG, "zero-share keys and outputs are required");
     OGM_CHECK_ARG(nbits >= 0, OGM_ERR_ARG, "negative bit count");
-    if (nbits == 0) return OGM_OK;
+    const int64_t nwords = (nbits + 31) / 32;
+    OGM_CHECK_ARG(w0 >= 0 && (w0 & 3) == 0 && nloc >= 0 && w0 + nloc <= nwords, OGM_ERR_ARG,
+                  "slice [%lld, +%lld) must start on a CTR block inside %lld words", (long long)w0,
+                  (long long)nloc, (long long)nwords);
+    if (nloc == 0) return OGM_OK;
     OGM_ENSURE_INIT();
     static const uint8_t kZshr[4] = {'Z', 'S', 'H', 'R'};
     Zs3Args a{};
@@ -806,11 +814,21 @@ int ogm_zero_share_trio(const uint8_t* k1, const uint8_t* k2, const uint8_t* k3,
         a.xin[q] = xor_into ? xor_into[q] : nullptr;
         a.out[q] = out[q];
     }
-    const int64_t nwords = (nbits + 31) / 32;
-    zero_share3_kernel<<<aes_grid((nwords + 3) / 4), kAesThreads, kAesTableBytes, as_stream(stream)>>>(
-        a, label_be(kZshr), counter, nwords, nbits);
+    zero_share3_kernel<<<aes_grid((nloc + 3) / 4), kAesThreads, kAesTableBytes, as_stream(stream)>>>(
+        a, label_be(kZshr), counter, nwords, nbits, w0, nloc);
     OGM_LAUNCH_CHECK();
     return OGM_OK;
+}
+
+int ogm_zero_share_trio(const uint8_t* k1, const uint8_t* k2, const uint8_t* k3, uint64_t counter,
+                        int64_t nbits, const uint32_t* const* xor_into, uint32_t* const* out, void* stream) {
+    return zero_share_trio_impl(k1, k2, k3, counter, nbits, 0, (nbits + 31) / 32, xor_into, out, stream);
+}
+
+int ogm_zero_share_trio_slice(const uint8_t* k1, const uint8_t* k2, const uint8_t* k3, uint64_t counter,
+                              int64_t nbits, int64_t w0, int64_t nwords, const uint32_t* const* xor_into,
+                              uint32_t* const* out, void* stream) {
+    return zero_share_trio_impl(k1, k2, k3, counter, nbits, w0, nwords, xor_into, out, stream);
 }
 
 int ogm_and_terms(int64_t nwords, int nparty, const uint32_t* const* a_a, const uint32_t* const* a_b,
