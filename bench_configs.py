@@ -61,6 +61,32 @@ def events(n):
 # ---------------------------------------------------------------------------
 
 
+def cpu_port_sec_eval(comps, words: int, ind_of, gpu_bits_of, sample: int) -> dict:
+    """The CPU path beside a secEval line: the oracle port's masked parity
+    (oracle/, C, one core; src/engine.py:76-80) for all 3 parties x 2 passes
+    on the first `sample` candidate rows, timed and extrapolated linearly to
+    the full row count.  Its bits are checked against the GPU result."""
+    import oracle
+
+    rows = comps[0].shape[0]
+    sample = min(sample, rows)
+    host = [c[:sample, :words].cpu().numpy().view(np.uint32) for c in comps]
+    dt, same = 0.0, True
+    for ps in range(2):
+        for p in range(3):
+            ia = ind_of(p, ps)[0].cpu().numpy().view(np.uint32)[:words]
+            ib = ind_of(p, ps)[1].cpu().numpy().view(np.uint32)[:words]
+            t = time.perf_counter()
+            bits = oracle.masked_parity(host[p], host[(p + 1) % 3], ia, ib)
+            dt += time.perf_counter() - t
+            got = oracle.unpack_bits(gpu_bits_of(p, ps), rows)[:sample]
+            same = same and bool(np.array_equal(bits, got))
+    return {"value": 1e3 * dt * rows / sample, "unit": "ms", "cores": 1, "kind": "port",
+            "sample": f"{sample} of {rows} candidates, 3 parties x 2 passes, oracle.masked_parity "
+                      f"(C, src/engine.py:76-80) in {dt:.2f}s, extrapolated linearly",
+            "gpu_bits_equal_on_sample": same}
+
+
 def run_c1(args):
     import oracle.matcher as om
 
@@ -174,6 +200,9 @@ def run_c3(args):
         ref = [o.clone() for o in outs]
         trio()
         ok = all(torch.equal(ref[2 * p + pi], outs[pi * 3 + p]) for p in range(3) for pi in range(2))
+        cpu = cpu_port_sec_eval(comps, w, lambda p, ps: inds[p][ps],
+                                lambda p, ps: ref[2 * p + ps].cpu().numpy().view(np.uint32),
+                                2000 if w > 1000 else 20000)
         for mode, fn, nbytes in (("per-party (3 launches)", lambda: [per_party(p) for p in range(3)], 3 * 2 * X * w * 4),
                                  ("trio-fused", trio, 3 * X * w * 4)):
             for _ in range(args.warmup):
@@ -189,7 +218,7 @@ def run_c3(args):
                             "(2 passes fused)", "metric": "secEval_local_GBps", "mode": mode,
                   "value": nbytes / (ms * 1e-3) / 1e9, "unit": "GB/s", "ms": ms,
                   "hbm_frac": nbytes / (ms * 1e-3) / 1e9 / HBM_PEAK, "algorithmic_bytes": nbytes,
-                  "trio_equals_per_party": ok})
+                  "trio_equals_per_party": ok, "cpu_baseline": cpu})
         # the full protocol step (3 threads, fused passes + 2 reshares per party)
         group = [CandidateGroup(None, None, X, X, comps[p][:, :1], comps[(p + 1) % 3][:, :1],
                                 {"a": (comps[p], comps[(p + 1) % 3])}, {"a": n}) for p in range(3)]
@@ -215,6 +244,8 @@ def run_c3(args):
 
 
 def run_c5(args):
+    import oracle
+
     dev = torch.device("cuda")
     cfg = make_session_configs(b"\x77" * 16)
     s12, s23, s31 = cfg[0].seed_with_next, cfg[1].seed_with_next, cfg[2].seed_with_next
@@ -276,6 +307,17 @@ def run_c5(args):
         r3_pre = r3.clone()
         online(False)
         ok = ok and bool(torch.equal(r3, r3_pre))
+        # the CPU path beside it: the oracle port of src/shuffle.py:80-144 (numpy, one core) on
+        # min(rows, 2^16) rows; at those sizes its R3 must equal ours bit for bit
+        srows = min(rows, 1 << 16)
+        host = [c[:srows].cpu().numpy().view(np.uint32) for c in comps]
+        t0 = time.perf_counter()
+        (_, _, o_r3), _ = oracle.shuffle_trio(s12, s23, s31, 0, host, width)
+        cpu_s = time.perf_counter() - t0
+        cpu = {"value": 1e3 * cpu_s * rows / srows, "unit": "ms", "cores": 1, "kind": "port",
+               "sample": f"{srows} rows: oracle.shuffle_trio (numpy, src/shuffle.py:80-144) in {cpu_s:.2f}s"
+                         + (", extrapolated linearly" if srows < rows else ""),
+               "r3_equal": bool(np.array_equal(o_r3, r3.cpu().numpy().view(np.uint32))) if srows == rows else None}
         del perm, plain
         for pre in (True, False):
             for _ in range(args.warmup):
@@ -310,7 +352,7 @@ def run_c5(args):
                   else "AES-CTR on the fly, nested permutation lookups",
                   "value": nbytes / (ms * 1e-3) / 1e9, "unit": "GB/s", "ms": ms,
                   "hbm_frac": nbytes / (ms * 1e-3) / 1e9 / HBM_PEAK, "algorithmic_bytes_per_row": nbytes // rows,
-                  "rows_per_s": rows / (ms * 1e-3), "step_ms": step_ms, "offline_perm_s": t_perm, "offline_blinds_s": t_blind,
+                  "rows_per_s": rows / (ms * 1e-3), "step_ms": step_ms, "cpu_baseline": cpu, "offline_perm_s": t_perm, "offline_blinds_s": t_blind,
                   "offline_party_material_s": t_off, "bit_exact_recombination": ok})
         del off, pc
         del comps, perms, blinds, x1, y1, c1, r3, r3_pre
@@ -465,13 +507,22 @@ def c4_sec_eval(rows: int, seed: int, steps: int, warmup: int, rank: int, world:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms = float(t.item())
     nbytes_local = 3 * (hi - lo) * w * 4
+    cpu = None
+    if rank == 0 and world == 1:
+        import oracle
+
+        def gpu_bits(p, ps):  # undo the re-share blinding: additive bits = message ^ zero share
+            z = oracle.zero_share(zk[p][0], zk[p][1], ps, rows)
+            return res[ps][p].cpu().numpy().view(np.uint32) ^ z
+
+        cpu = cpu_port_sec_eval(comps, w, lambda p, ps: inds[ps][p], gpu_bits, 20000)
     return {"config": f"C4 root secEval, {rows} candidates (Zipf attr n={n}, w={w}), interval, "
                       f"rows sharded x{world}", "metric": "secEval_candidates_per_s",
             "value": rows / (ms * 1e-3), "unit": "candidates/s", "ms_per_step": ms, "n_gpus": world,
             "scaling": "strong", "rank0_hbm_GBps": nbytes_local / (ms * 1e-3) / 1e9,
             "rank0_hbm_frac": nbytes_local / (ms * 1e-3) / 1e9 / HBM_PEAK,
             "collective": "NCCL all_gather of packed blinded match bits" if world > 1 else "none",
-            "result_words": int(res[0][0].numel())}
+            "result_words": int(res[0][0].numel()), "cpu_baseline": cpu}
 
 
 def run_c4(args):
