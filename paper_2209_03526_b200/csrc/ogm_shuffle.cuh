@@ -346,6 +346,38 @@ constexpr int64_t kWindowBytes = 8 << 20;      // pass-2 window (contiguous I-re
 constexpr int64_t kPartSmemBytes = 64 << 10;   // pass-1 tile (3 CTAs per SM)
 constexpr int64_t kMaxDynSmem = 200 << 10;
 
+// L2 scrub between the passes of a large planned gather.  Pass 1 leaves L2
+// holding its (partly written, evict-first) run lines; with those resident,
+// pass 2's window does not stay in L2 and every random read goes to DRAM
+// (2^28 rows: 2.3 -> 5.6 ms, DRAM reads 9.7 -> 28.6 GB).  Writing one L2's
+// worth of full lines in between (a memset, ~40 us) restores the fast window
+// pass (profiles/r01_c5_plan.md, scripts/exp_plan11.py).  Only worth it when
+// the table is far larger than L2.
+constexpr int64_t kScrubMinBytes = (int64_t)2 << 30;
+
+static void* scrub_buffer(int64_t* bytes) {
+    static std::mutex mu;
+    static void* buf[64] = {};
+    static int64_t len[64] = {};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 0 || dev >= 64) return nullptr;
+    std::lock_guard<std::mutex> g(mu);
+    if (!buf[dev]) {
+        int l2 = 0;
+        cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, dev);
+        int64_t want = l2 > 0 ? (int64_t)l2 : ((int64_t)126 << 20);
+        if (cudaMalloc(&buf[dev], (size_t)want) != cudaSuccess) {
+            cudaGetLastError();
+            buf[dev] = nullptr;
+            return nullptr;
+        }
+        len[dev] = want;
+    }
+    *bytes = len[dev];
+    return buf[dev];
+}
+
 __device__ __forceinline__ uint4 xorU(uint4 a, uint4 b) { return xor4(a, b); }
 __device__ __forceinline__ uint32_t xorU(uint32_t a, uint32_t b) { return a ^ b; }
 
@@ -850,6 +882,10 @@ int ogm_gather_planned(int64_t rows, int64_t words, int64_t pitch, int64_t tile_
         g = std::min<int64_t>(ntiles, (int64_t)sm_count() * std::max(per_sm, 1));
         plan_partition_kernel<uint32_t><<<(int)g, 512, smem, st>>>(m1, m2, m4, srow, gdst, rows, (int)tile_rows,
                                                                    (int)pitch, inter);
+    }
+    if (passes == 3 && rows * pitch * 4 >= kScrubMinBytes) {
+        int64_t sb = 0;
+        if (void* sc = scrub_buffer(&sb)) OGM_CUDA_TRY(cudaMemsetAsync(sc, 0, (size_t)sb, st));
     }
     if (!(passes & 2)) {
     } else if (pitch == 4 && vec) {

@@ -16,7 +16,9 @@ x1, y1, c1, r3, inter = (torch.empty_like(a) for _ in range(5))
 plans = [GatherPlan(torch.randperm(rows, device="cuda").to(torch.int32), 4) for _ in range(4)]
 steps = [(plans[0], dict(m1=a, m2=b, r=U), x1), (plans[1], dict(m1=c, r=V), y1),
          (plans[2], dict(m1=x1, r=W), c1), (plans[3], dict(m1=y1, m3=c1, m4=Z), r3)]
-fresh = len(sys.argv) > 2
+fresh = "fresh" in sys.argv
+ballast = [torch.empty((int(x) << 30,), dtype=torch.uint8, device="cuda").fill_(1)
+           for x in [a[len("ballast="):] for a in sys.argv if a.startswith("ballast=")][:1] for _ in range(1)]
 for rep in range(3):
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(9)]
     ev[0].record()

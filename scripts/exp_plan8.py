@@ -24,6 +24,8 @@ def t(fn, n=5):
 
 
 rows = 1 << int(sys.argv[1])
+ballast = [torch.empty((int(a[8:]) << 30,), dtype=torch.uint8, device="cuda").fill_(1)
+           for a in sys.argv if a.startswith("ballast=")]
 mk = lambda: torch.randint(-2**31, 2**31 - 1, (rows, 4), dtype=torch.int32, device="cuda")  # noqa: E731
 M, R, M3, out, inter = mk(), mk(), mk(), mk(), mk()
 idx = torch.randperm(rows, device="cuda").to(torch.int32)
@@ -34,5 +36,6 @@ for wmb in (1, 2, 4, 8):
     b = t(lambda: plan.run(out, m1=M, r=R, m3=M3, inter=inter, passes=2))
     c = t(lambda: plan.run(out, m1=M, inter=inter, passes=2))
     p1 = t(lambda: plan.run(out, m1=M, inter=inter, passes=1))
-    print(f"window {wmb} MB: pass2 r {a:.3f}  r+m3 {b:.3f}  none {c:.3f}   pass1 {p1:.3f} ms")
+    alt = t(lambda: plan.run(out, m1=M, r=R, inter=inter))
+    print(f"window {wmb} MB: pass2 r {a:.3f}  r+m3 {b:.3f}  none {c:.3f}   pass1 {p1:.3f} ms  both {alt:.3f}")
     del plan
