@@ -234,3 +234,46 @@ def test_domain_errors():
         fss.full_domain_eval(k0, 17)
     with pytest.raises(DomainError):
         fss.dpf_gen(16, 16, rng)
+
+
+@pytest.mark.parametrize("nbits,w0,nw", [(1000, 0, 32), (1000, 8, 24), (4097, 124, 5), (200_003, 4096, 2155),
+                                         (64, 0, 2)])
+def test_zero_share_trio_slice_vs_goldens_and_oracle(golden, nbits, w0, nw):
+    """ogm_zero_share_trio(_slice): the three parties' zero shares in one
+    launch equal the per-party oracle restatement (pinned to the goldens by
+    test_oracle_golden) on the slice, tail mask only on the last word."""
+    g = golden("zero_share")
+    keys = [g["keys"][i].tobytes() for i in range(3)]
+    ctr = 5
+    want = [oracle.zero_share(keys[q], keys[(q + 2) % 3], ctr, nbits)[w0:w0 + nw] for q in range(3)]
+    outs = [torch.empty((nw,), dtype=torch.int32, device="cuda") for _ in range(3)]
+    base = [dev_u32(np.arange(nw, dtype=np.uint32) * np.uint32(40503 + q)) for q in range(3)]
+    A = _lib.ptr_array
+    _lib.call("ogm_zero_share_trio_slice", keys[0], keys[1], keys[2], ctr, nbits, w0, nw, A(base), A(outs),
+              _lib.stream_ptr())
+    for q in range(3):
+        exp = want[q] ^ host_u32(base[q])
+        if w0 + nw == (nbits + 31) // 32 and nbits % 32:
+            exp[-1] &= np.uint32((1 << (nbits % 32)) - 1)
+        assert np.array_equal(host_u32(outs[q]), exp), q
+    if w0 == 0 and nw == (nbits + 31) // 32:
+        full = [torch.empty((nw,), dtype=torch.int32, device="cuda") for _ in range(3)]
+        _lib.call("ogm_zero_share_trio", keys[0], keys[1], keys[2], ctr, nbits, None, A(full), _lib.stream_ptr())
+        for q in range(3):
+            assert np.array_equal(host_u32(full[q]), want[q])
+    with pytest.raises(ValueError, match="CTR block"):
+        _lib.call("ogm_zero_share_trio_slice", keys[0], keys[1], keys[2], ctr, nbits, 2, 1, None, A(outs),
+                  _lib.stream_ptr())
+
+
+@pytest.mark.parametrize("n", [1, 7, 4096, 1 << 20])
+def test_perm_invert(n):
+    from paper_2209_03526_b200.prf import seeded_permutation_device
+
+    p = seeded_permutation_device(b"\x09" * 16, b"SHPI", 4, n)
+    inv = torch.empty_like(p)
+    _lib.call("ogm_perm_invert", n, _lib.ptr(p), _lib.ptr(inv), _lib.stream_ptr())
+    pn = p.cpu().numpy()
+    want = np.empty_like(pn)
+    want[pn] = np.arange(n, dtype=pn.dtype)
+    assert np.array_equal(inv.cpu().numpy(), want)
