@@ -53,6 +53,8 @@ __device__ __forceinline__ void aes_fill_tables(uint8_t* smem) {
 }
 
 struct AesTab {
+    static constexpr int kBytes = kAesTableBytes;
+    __device__ __forceinline__ static void fill(uint8_t* smem) { aes_fill_tables(smem); }
     const uint8_t* base;  // shared-memory table base
     uint32_t off0;        // lane*4
     uint32_t off1;        // lane*4 + 128
@@ -85,6 +87,44 @@ struct AesTab {
     __device__ __forceinline__ uint32_t sub_b0(uint32_t x) const { return lut<2, 0>(x); }
 };
 
+
+// Small-work variant: the four T-tables once (4 KiB, no per-lane
+// replication).  Lookups may bank-conflict (random bytes over 32 banks, ~3-4
+// wavefronts), but the fill is 1024 words instead of 32768 -- for launches
+// with a few thousand AES blocks (tokens, C1-sized shuffles, small domains)
+// the replicated fill IS the kernel: 4 CTAs x 512 threads spent 22-35 us
+// filling 128 KiB each (ncu, profiles/r01_c1_small_aes.md).
+constexpr int kAesSmallBytes = 4 * 1024;
+
+struct AesTabSmall {
+    static constexpr int kBytes = kAesSmallBytes;
+    __device__ __forceinline__ static void fill(uint8_t* smem) {
+        uint32_t* w = reinterpret_cast<uint32_t*>(smem);
+        for (int idx = threadIdx.x; idx < 1024; idx += blockDim.x) {
+            const int t = idx >> 8, e = idx & 255;
+            uint32_t v = c_T0[e];
+            if (t) v = rotl32(v, 8 * t);
+            w[idx] = v;
+        }
+    }
+    const uint32_t* base;
+    __device__ __forceinline__ explicit AesTabSmall(const uint8_t* smem)
+        : base(reinterpret_cast<const uint32_t*>(smem)) {}
+    template <int TBL, int POS>
+    __device__ __forceinline__ uint32_t lut(uint32_t x) const {
+        return base[TBL * 256 + ((x >> (8 * POS)) & 255u)];
+    }
+    __device__ __forceinline__ uint32_t t0(uint32_t x) const { return lut<0, 0>(x); }
+    __device__ __forceinline__ uint32_t t1(uint32_t x) const { return lut<1, 1>(x); }
+    __device__ __forceinline__ uint32_t t2(uint32_t x) const { return lut<2, 2>(x); }
+    __device__ __forceinline__ uint32_t t3(uint32_t x) const { return lut<3, 3>(x); }
+    __device__ __forceinline__ uint32_t sub_col(uint32_t x0, uint32_t x1, uint32_t x2, uint32_t x3) const {
+        uint32_t a = lut<2, 0>(x0), b = lut<3, 1>(x1), c = lut<0, 2>(x2), d = lut<1, 3>(x3);
+        return __byte_perm(__byte_perm(a, b, 0x3250), __byte_perm(c, d, 0x7210), 0x7610);
+    }
+    __device__ __forceinline__ uint32_t sub_b0(uint32_t x) const { return lut<2, 0>(x); }
+};
+
 __device__ __forceinline__ uint32_t xor5(uint32_t a, uint32_t b, uint32_t c, uint32_t d, uint32_t e) {
     return a ^ b ^ c ^ d ^ e;
 }
@@ -111,8 +151,8 @@ struct AesKeySched {
 };
 
 // Full AES-128 encryption of one block (4 LE column words).
-template <class KS>
-__device__ __forceinline__ uint4 aes128_enc(const AesTab& T, uint4 in, const KS& ks) {
+template <class TAB, class KS>
+__device__ __forceinline__ uint4 aes128_enc(const TAB& T, uint4 in, const KS& ks) {
     uint32_t s0 = in.x ^ ks(0), s1 = in.y ^ ks(1), s2 = in.z ^ ks(2), s3 = in.w ^ ks(3);
 #pragma unroll
     for (int r = 1; r < 10; r++) {
@@ -136,7 +176,8 @@ __device__ __forceinline__ uint4 aes128_enc(const AesTab& T, uint4 in, const KS&
 // full, column 0 of round 9, one S-box lookup in round 10 (133 lookups
 // instead of 160).  Returns the three PRG control/value bits
 // (src/prf.py:53-56): bit0 t_left, bit1 t_right, bit2 value.
-__device__ __forceinline__ uint32_t prg_ctrl_bits(const AesTab& T, uint4 s) {
+template <class TAB>
+__device__ __forceinline__ uint32_t prg_ctrl_bits(const TAB& T, uint4 s) {
     PrgKey<2> ks;
     uint32_t s0 = s.x ^ ks(0), s1 = s.y ^ ks(1), s2 = s.z ^ ks(2), s3 = s.w ^ ks(3);
 #pragma unroll
@@ -151,9 +192,54 @@ __device__ __forceinline__ uint32_t prg_ctrl_bits(const AesTab& T, uint4 s) {
     return (T.sub_b0(c0) ^ ks(40) ^ s.x) & 7u;
 }
 
-// Matyas-Meyer-Oseas child seed: AES_K(s) ^ s (src/prf.py:51-52).
+// Small-work builds: one out-of-line, rolled AES per kernel instead of an
+// unrolled copy per call site.  A C1-sized shuffle launch spent 155 of 212
+// PC samples in "no instruction" (i-cache misses over ~50 KB of unrolled
+// rounds on 16 cold SMs) -- code size, not arithmetic, was its runtime.
 template <class KS>
-__device__ __forceinline__ uint4 prg_child(const AesTab& T, uint4 s, const KS& ks) {
+__device__ __noinline__ uint4 aes128_enc_rolled(const AesTabSmall T, uint4 in, const KS ks) {
+    uint32_t s0 = in.x ^ ks(0), s1 = in.y ^ ks(1), s2 = in.z ^ ks(2), s3 = in.w ^ ks(3);
+#pragma unroll 1
+    for (int r = 1; r < 10; r++) {
+        uint32_t n0 = xor5(T.t0(s0), T.t1(s1), T.t2(s2), T.t3(s3), ks(4 * r + 0));
+        uint32_t n1 = xor5(T.t0(s1), T.t1(s2), T.t2(s3), T.t3(s0), ks(4 * r + 1));
+        uint32_t n2 = xor5(T.t0(s2), T.t1(s3), T.t2(s0), T.t3(s1), ks(4 * r + 2));
+        uint32_t n3 = xor5(T.t0(s3), T.t1(s0), T.t2(s1), T.t3(s2), ks(4 * r + 3));
+        s0 = n0; s1 = n1; s2 = n2; s3 = n3;
+    }
+    uint4 o;
+    o.x = T.sub_col(s0, s1, s2, s3) ^ ks(40);
+    o.y = T.sub_col(s1, s2, s3, s0) ^ ks(41);
+    o.z = T.sub_col(s2, s3, s0, s1) ^ ks(42);
+    o.w = T.sub_col(s3, s0, s1, s2) ^ ks(43);
+    return o;
+}
+
+template <class KS>
+__device__ __forceinline__ uint4 aes128_enc(const AesTabSmall& T, uint4 in, const KS& ks) {
+    return aes128_enc_rolled(T, in, ks);
+}
+
+__device__ __noinline__ uint32_t prg_ctrl_bits_rolled(const AesTabSmall T, uint4 s) {
+    PrgKey<2> ks;
+    uint32_t s0 = s.x ^ ks(0), s1 = s.y ^ ks(1), s2 = s.z ^ ks(2), s3 = s.w ^ ks(3);
+#pragma unroll 1
+    for (int r = 1; r < 9; r++) {
+        uint32_t n0 = xor5(T.t0(s0), T.t1(s1), T.t2(s2), T.t3(s3), ks(4 * r + 0));
+        uint32_t n1 = xor5(T.t0(s1), T.t1(s2), T.t2(s3), T.t3(s0), ks(4 * r + 1));
+        uint32_t n2 = xor5(T.t0(s2), T.t1(s3), T.t2(s0), T.t3(s1), ks(4 * r + 2));
+        uint32_t n3 = xor5(T.t0(s3), T.t1(s0), T.t2(s1), T.t3(s2), ks(4 * r + 3));
+        s0 = n0; s1 = n1; s2 = n2; s3 = n3;
+    }
+    uint32_t c0 = xor5(T.t0(s0), T.t1(s1), T.t2(s2), T.t3(s3), ks(36));
+    return (T.sub_b0(c0) ^ ks(40) ^ s.x) & 7u;
+}
+
+__device__ __forceinline__ uint32_t prg_ctrl_bits(const AesTabSmall& T, uint4 s) { return prg_ctrl_bits_rolled(T, s); }
+
+// Matyas-Meyer-Oseas child seed: AES_K(s) ^ s (src/prf.py:51-52).
+template <class TAB, class KS>
+__device__ __forceinline__ uint4 prg_child(const TAB& T, uint4 s, const KS& ks) {
     uint4 c = aes128_enc(T, s, ks);
     return make_uint4(c.x ^ s.x, c.y ^ s.y, c.z ^ s.z, c.w ^ s.w);
 }

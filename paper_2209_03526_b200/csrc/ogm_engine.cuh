@@ -220,15 +220,16 @@ struct Zs3Args {
     uint32_t* out[3];
 };
 
+template <class TAB = AesTab>
 __global__ void __launch_bounds__(kAesThreads) zero_share3_kernel(const Zs3Args a, uint32_t label_be,
                                                                    uint64_t counter, int64_t nwords,
                                                                    int64_t nbits, int64_t w0, int64_t nloc) {
     // words [w0, w0 + nloc) of the nwords-word stream (w0 % 4 == 0: whole
     // CTR blocks), written to out[q][0 .. nloc)
     extern __shared__ __align__(128) uint8_t smem_raw[];
-    aes_fill_tables(smem_raw);
+    TAB::fill(smem_raw);
     __syncthreads();
-    const AesTab T(smem_raw);
+    const TAB T(smem_raw);
     const int64_t nblk = (nloc + 3) >> 2;
     const int64_t b0 = w0 >> 2;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
@@ -685,7 +686,7 @@ struct FlagIter {
 };
 
 int engine_init() {
-    OGM_CUDA_TRY(allow_big_smem(zero_share3_kernel, kAesTableBytes));
+    OGM_CUDA_TRY(allow_big_smem(zero_share3_kernel<AesTab>, kAesTableBytes));
     return OGM_OK;
 }
 
@@ -814,8 +815,8 @@ static int zero_share_trio_impl(const uint8_t* k1, const uint8_t* k2, const uint
         a.xin[q] = xor_into ? xor_into[q] : nullptr;
         a.out[q] = out[q];
     }
-    zero_share3_kernel<<<aes_grid((nloc + 3) / 4), kAesThreads, kAesTableBytes, as_stream(stream)>>>(
-        a, label_be(kZshr), counter, nwords, nbits, w0, nloc);
+    aes_launch(zero_share3_kernel<AesTab>, zero_share3_kernel<AesTabSmall>, (nloc + 3) / 4, kAesThreads,
+               as_stream(stream), a, label_be(kZshr), counter, nwords, nbits, w0, nloc);
     OGM_LAUNCH_CHECK();
     return OGM_OK;
 }

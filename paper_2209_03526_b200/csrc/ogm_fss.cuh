@@ -13,11 +13,12 @@ namespace ogm {
 
 constexpr int kFssThreads = kAesThreads;
 
-#define OGM_AES_PROLOGUE()                              \
+#define OGM_AES_PROLOGUE_T(TABT)                        \
     extern __shared__ __align__(128) uint8_t smem_raw[]; \
-    aes_fill_tables(smem_raw);                          \
+    TABT::fill(smem_raw);                               \
     __syncthreads();                                    \
-    const AesTab T(smem_raw)
+    const TABT T(smem_raw)
+#define OGM_AES_PROLOGUE() OGM_AES_PROLOGUE_T(AesTab)
 
 // ---------------------------------------------------------------------------
 // src/prf.py:41-57 prg_expand: one thread per seed, 2 full AES + ctrl AES.
@@ -42,12 +43,12 @@ __global__ void __launch_bounds__(kFssThreads) prg_expand_kernel(
 // src/fss.py:116-157 _tree_gen, one thread per key pair (6 AES per level:
 // both children + control for both parties' seeds).
 // ---------------------------------------------------------------------------
-template <bool DCF>
+template <bool DCF, class TAB = AesTab>
 __global__ void __launch_bounds__(kFssThreads) fss_gen_kernel(
     int bits, int64_t K, const uint32_t* __restrict__ alphas, const uint4* __restrict__ roots0,
     const uint4* __restrict__ roots1, uint4* __restrict__ scw_out, uint32_t* __restrict__ ctrl_out,
     uint8_t* __restrict__ final_out) {
-    OGM_AES_PROLOGUE();
+    OGM_AES_PROLOGUE_T(TAB);
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < K; k += stride) {
         uint4 s0 = roots0[k], s1 = roots1[k];
@@ -146,12 +147,12 @@ struct FdeNode {
     uint32_t t, acc, idx, rd;
 };
 
-template <bool DCF>
+template <bool DCF, class TAB = AesTab>
 __global__ void __launch_bounds__(kFssThreads) fss_fde_kernel(
     int bits, int nkeys, const uint4* __restrict__ root, const uint4* __restrict__ scw,
     const uint32_t* __restrict__ ctrl, const uint8_t* __restrict__ flags, int64_t n, int kk,
     uint32_t* __restrict__ out, int64_t pitch) {
-    OGM_AES_PROLOGUE();
+    OGM_AES_PROLOGUE_T(TAB);
     const int lane = threadIdx.x & 31;
     const int L = 1 << kk;
     const int G = 32 / L;
@@ -236,11 +237,11 @@ __global__ void __launch_bounds__(kFssThreads) fss_fde_kernel(
 // src/prf.py:70-92 prf_stream as words: one thread per 16-byte CTR block.
 // src/rss.py:143-148 zero shares: two keys, XOR, tail mask, optional fold.
 // ---------------------------------------------------------------------------
-template <bool ZERO>
+template <bool ZERO, class TAB = AesTab>
 __global__ void __launch_bounds__(kFssThreads) prf_words_kernel(
     AesKeySched k1, AesKeySched k2, uint32_t label_be, uint64_t index, uint64_t first_word,
     int64_t nwords, int64_t nbits, const uint32_t* __restrict__ xor_into, uint32_t* __restrict__ out) {
-    OGM_AES_PROLOGUE();
+    OGM_AES_PROLOGUE_T(TAB);
     const uint64_t b0 = first_word >> 2;
     const uint64_t b1 = (first_word + (uint64_t)nwords + 3) >> 2;
     const int64_t nblk = (int64_t)(b1 - b0);
@@ -274,10 +275,11 @@ __global__ void __launch_bounds__(kFssThreads) prf_words_kernel(
 // (generating such rows inside a 4-word-chunked gather costs up to two AES
 // blocks per chunk when W is not a multiple of 4).
 // ---------------------------------------------------------------------------
+template <class TAB = AesTab>
 __global__ void __launch_bounds__(kFssThreads) prf_rows_kernel(AesKeySched k, uint32_t label_be, uint64_t index,
                                                                int64_t rows, int64_t W, uint32_t tail,
                                                                int64_t pitch, uint32_t* __restrict__ out) {
-    OGM_AES_PROLOGUE();
+    OGM_AES_PROLOGUE_T(TAB);
     const int64_t nblk = (rows * W + 3) >> 2;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     for (int64_t blk = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; blk < nblk; blk += stride) {
@@ -306,15 +308,15 @@ __global__ void __launch_bounds__(kFssThreads) prf_rows_kernel(AesKeySched k, ui
 
 int fss_init() {
     OGM_CUDA_TRY(allow_big_smem(prg_expand_kernel, kAesTableBytes));
-    OGM_CUDA_TRY(allow_big_smem(fss_gen_kernel<false>, kAesTableBytes));
-    OGM_CUDA_TRY(allow_big_smem(fss_gen_kernel<true>, kAesTableBytes));
+    OGM_CUDA_TRY(allow_big_smem(fss_gen_kernel<false, AesTab>, kAesTableBytes));
+    OGM_CUDA_TRY(allow_big_smem(fss_gen_kernel<true, AesTab>, kAesTableBytes));
     OGM_CUDA_TRY(allow_big_smem(fss_eval_kernel<false>, kAesTableBytes));
     OGM_CUDA_TRY(allow_big_smem(fss_eval_kernel<true>, kAesTableBytes));
-    OGM_CUDA_TRY(allow_big_smem(fss_fde_kernel<false>, kAesTableBytes));
-    OGM_CUDA_TRY(allow_big_smem(fss_fde_kernel<true>, kAesTableBytes));
-    OGM_CUDA_TRY(allow_big_smem(prf_words_kernel<false>, kAesTableBytes));
-    OGM_CUDA_TRY(allow_big_smem(prf_words_kernel<true>, kAesTableBytes));
-    OGM_CUDA_TRY(allow_big_smem(prf_rows_kernel, kAesTableBytes));
+    OGM_CUDA_TRY(allow_big_smem(fss_fde_kernel<false, AesTab>, kAesTableBytes));
+    OGM_CUDA_TRY(allow_big_smem(fss_fde_kernel<true, AesTab>, kAesTableBytes));
+    OGM_CUDA_TRY(allow_big_smem(prf_words_kernel<false, AesTab>, kAesTableBytes));
+    OGM_CUDA_TRY(allow_big_smem(prf_words_kernel<true, AesTab>, kAesTableBytes));
+    OGM_CUDA_TRY(allow_big_smem(prf_rows_kernel<AesTab>, kAesTableBytes));
     return OGM_OK;
 }
 

@@ -177,4 +177,22 @@ static int aes_grid(int64_t work_threads) {
     return (int)g;
 }
 
+// AES-table kernels come in two builds: replicated 128 KiB tables (one CTA
+// per SM, conflict-free lookups: the throughput path) and 4 KiB tables
+// (AesTabSmall: cheap fill, some bank conflicts) for launches whose whole
+// work is a few hundred CTAs' worth of 128-thread blocks, where the 32768-word
+// replicated fill dominates.  Same arguments, same results.
+constexpr int kAesSmallThreads = 128;
+constexpr int64_t kAesSmallMaxWork = 32768;
+
+template <class KB, class KS, class... Args>
+static void aes_launch(KB big, KS small, int64_t work, int big_threads, cudaStream_t st, Args... args) {
+    if (work <= kAesSmallMaxWork) {
+        const int64_t g = (work + kAesSmallThreads - 1) / kAesSmallThreads;
+        small<<<(int)(g > 0 ? g : 1), kAesSmallThreads, kAesSmallBytes, st>>>(args...);
+    } else {
+        big<<<aes_grid(work), big_threads, kAesTableBytes, st>>>(args...);
+    }
+}
+
 }  // namespace ogm

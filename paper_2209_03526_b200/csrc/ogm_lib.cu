@@ -49,8 +49,9 @@ int ogm_prf_words(const uint8_t* key, const uint8_t* label, uint64_t index, uint
     OGM_ENSURE_INIT();
     AesKeySched k = make_sched(key);
     int64_t nblk = (int64_t)(((first_word + nwords + 3) >> 2) - (first_word >> 2));
-    prf_words_kernel<false><<<aes_grid(nblk), kFssThreads, kAesTableBytes, as_stream(stream)>>>(
-        k, k, label_be(label), index, first_word, nwords, nwords * 32, nullptr, out);
+    aes_launch(prf_words_kernel<false, AesTab>, prf_words_kernel<false, AesTabSmall>, nblk, kFssThreads,
+               as_stream(stream), k, k, label_be(label), index, first_word, nwords, nwords * 32,
+               (const uint32_t*)nullptr, out);
     OGM_LAUNCH_CHECK();
     return OGM_OK;
 }
@@ -65,8 +66,8 @@ int ogm_prf_rows(const uint8_t* key, const uint8_t* label, uint64_t index, int64
     OGM_ENSURE_INIT();
     AesKeySched k = make_sched(key);
     const uint32_t tail = (width_bits & 31) ? ((1u << (width_bits & 31)) - 1u) : 0xffffffffu;
-    prf_rows_kernel<<<aes_grid((rows * W + 3) / 4), kFssThreads, kAesTableBytes, as_stream(stream)>>>(
-        k, label_be(label), index, rows, W, tail, pitch, out);
+    aes_launch(prf_rows_kernel<AesTab>, prf_rows_kernel<AesTabSmall>, (rows * W + 3) / 4, kFssThreads,
+               as_stream(stream), k, label_be(label), index, rows, W, tail, pitch, out);
     OGM_LAUNCH_CHECK();
     return OGM_OK;
 }
@@ -80,9 +81,9 @@ int ogm_zero_share(const uint8_t* key_own, const uint8_t* key_prev, uint64_t cou
     static const uint8_t kZshr[4] = {'Z', 'S', 'H', 'R'};  // src/rss.py:141
     AesKeySched k1 = make_sched(key_own), k2 = make_sched(key_prev);
     int64_t nwords = (nbits + 31) / 32;
-    prf_words_kernel<true><<<aes_grid((nwords + 3) / 4), kFssThreads, kAesTableBytes,
-                             as_stream(stream)>>>(k1, k2, label_be(kZshr), counter, 0, nwords, nbits,
-                                                  xor_into, out);
+    aes_launch(prf_words_kernel<true, AesTab>, prf_words_kernel<true, AesTabSmall>, (nwords + 3) / 4,
+               kFssThreads, as_stream(stream), k1, k2, label_be(kZshr), counter, (uint64_t)0, nwords, nbits,
+               xor_into, out);
     OGM_LAUNCH_CHECK();
     return OGM_OK;
 }
@@ -100,8 +101,9 @@ int ogm_zero_share_slice(const uint8_t* key_own, const uint8_t* key_prev, uint64
     static const uint8_t kZshr[4] = {'Z', 'S', 'H', 'R'};
     AesKeySched k1 = make_sched(key_own), k2 = make_sched(key_prev);
     int64_t nblk = (int64_t)(((first_word + nwords + 3) >> 2) - (first_word >> 2));
-    prf_words_kernel<true><<<aes_grid(nblk), kFssThreads, kAesTableBytes, as_stream(stream)>>>(
-        k1, k2, label_be(kZshr), counter, first_word, nwords, total_nbits, xor_into, out);
+    aes_launch(prf_words_kernel<true, AesTab>, prf_words_kernel<true, AesTabSmall>, nblk, kFssThreads,
+               as_stream(stream), k1, k2, label_be(kZshr), counter, first_word, nwords, total_nbits, xor_into,
+               out);
     OGM_LAUNCH_CHECK();
     return OGM_OK;
 }
@@ -114,11 +116,12 @@ int ogm_fss_gen(int kind, int bits, int64_t K, const uint32_t* alphas, const voi
     if (K == 0) return OGM_OK;
     OGM_ENSURE_INIT();
     if (kind == OGM_KIND_DCF)
-        fss_gen_kernel<true><<<aes_grid(K), kFssThreads, kAesTableBytes, as_stream(stream)>>>(
-            bits, K, alphas, (const uint4*)roots0, (const uint4*)roots1, (uint4*)seed_cw, ctrl, final_cw);
+        aes_launch(fss_gen_kernel<true, AesTab>, fss_gen_kernel<true, AesTabSmall>, K, kFssThreads, as_stream(stream),
+                   bits, K, alphas, (const uint4*)roots0, (const uint4*)roots1, (uint4*)seed_cw, ctrl, final_cw);
     else
-        fss_gen_kernel<false><<<aes_grid(K), kFssThreads, kAesTableBytes, as_stream(stream)>>>(
-            bits, K, alphas, (const uint4*)roots0, (const uint4*)roots1, (uint4*)seed_cw, ctrl, final_cw);
+        aes_launch(fss_gen_kernel<false, AesTab>, fss_gen_kernel<false, AesTabSmall>, K, kFssThreads,
+                   as_stream(stream), bits, K, alphas, (const uint4*)roots0, (const uint4*)roots1, (uint4*)seed_cw,
+                   ctrl, final_cw);
     OGM_LAUNCH_CHECK();
     return OGM_OK;
 }
@@ -231,11 +234,13 @@ int ogm_fss_full_domain(int kind, int bits, int nkeys, const void* root, const v
     while (kk > 0 && (int64_t)nkeys * words * (32 >> kk) < (int64_t)sm_count() * kFssThreads) kk--;
     const int64_t slots = (int64_t)nkeys * words * (32 >> kk);
     if (kind == OGM_KIND_DCF)
-        fss_fde_kernel<true><<<aes_grid(slots), kFssThreads, kAesTableBytes, as_stream(stream)>>>(
-            bits, nkeys, (const uint4*)root, (const uint4*)seed_cw, ctrl, flags, n, kk, out_words, pitch);
+        aes_launch(fss_fde_kernel<true, AesTab>, fss_fde_kernel<true, AesTabSmall>, slots, kFssThreads,
+                   as_stream(stream), bits, nkeys, (const uint4*)root, (const uint4*)seed_cw, ctrl, flags, n, kk,
+                   out_words, pitch);
     else
-        fss_fde_kernel<false><<<aes_grid(slots), kFssThreads, kAesTableBytes, as_stream(stream)>>>(
-            bits, nkeys, (const uint4*)root, (const uint4*)seed_cw, ctrl, flags, n, kk, out_words, pitch);
+        aes_launch(fss_fde_kernel<false, AesTab>, fss_fde_kernel<false, AesTabSmall>, slots, kFssThreads,
+                   as_stream(stream), bits, nkeys, (const uint4*)root, (const uint4*)seed_cw, ctrl, flags, n, kk,
+                   out_words, pitch);
     OGM_LAUNCH_CHECK();
     return OGM_OK;
 }

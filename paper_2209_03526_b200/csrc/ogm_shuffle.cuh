@@ -26,13 +26,14 @@ namespace ogm {
 // has all its predecessors done, so the result equals the sequential loop.
 // ---------------------------------------------------------------------------
 
+template <class TAB = AesTab>
 __global__ void __launch_bounds__(kAesThreads) perm_draws_kernel(
     AesKeySched key, uint32_t label_be, uint64_t index, int64_t n, int32_t* __restrict__ H,
     int32_t* __restrict__ live, int32_t* __restrict__ perm, int32_t* __restrict__ R) {
     extern __shared__ __align__(128) uint8_t smem_raw[];
-    aes_fill_tables(smem_raw);
+    TAB::fill(smem_raw);
     __syncthreads();
-    const AesTab T(smem_raw);
+    const TAB T(smem_raw);
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     for (int64_t x = tid; x < n; x += stride) {
@@ -133,7 +134,8 @@ struct GatherArgs {
     int64_t pitch;  // words per row in memory (>= W; zero padding past W)
 };
 
-__device__ __forceinline__ void prf_row_chunk(const AesTab& T, const GatherTerm& g, int64_t row, int64_t W,
+template <class TAB>
+__device__ __forceinline__ void prf_row_chunk(const TAB& T, const GatherTerm& g, int64_t row, int64_t W,
                                               int64_t c, int nw, uint32_t v[4]) {
     const uint64_t g0 = (uint64_t)row * (uint64_t)W + 4 * (uint64_t)c;
     const uint64_t b0 = g0 >> 2;
@@ -148,8 +150,8 @@ __device__ __forceinline__ void prf_row_chunk(const AesTab& T, const GatherTerm&
     for (int j = 0; j < 4; j++) v[j] = w8[(off + j) & 7];
 }
 
-template <bool ONLINE>
-__device__ __forceinline__ void gather_chunk(const AesTab& T, const GatherArgs& a, int64_t i, int64_t c,
+template <bool ONLINE, class TAB>
+__device__ __forceinline__ void gather_chunk(const TAB& T, const GatherArgs& a, int64_t i, int64_t c,
                                              uint32_t tail, bool vec) {
     // words [4c, 4c+nw) of row i; with a 16-B pitch the padding words ride
     // along as zeros and every access is 128-bit
@@ -203,14 +205,14 @@ __device__ __forceinline__ void gather_chunk(const AesTab& T, const GatherArgs& 
     }
 }
 
-template <bool ONLINE>
+template <bool ONLINE, class TAB = AesTab>
 __global__ void __launch_bounds__(kAesThreads) shuffle_gather_kernel(const GatherArgs a) {
     extern __shared__ __align__(128) uint8_t smem_raw[];
     if (ONLINE) {
-        aes_fill_tables(smem_raw);
+        TAB::fill(smem_raw);
         __syncthreads();
     }
-    const AesTab T(smem_raw);
+    const TAB T(smem_raw);
     // 128-bit path when rows are 16-B pitched and every base is aligned
     const bool vec = (a.pitch & 3) == 0 &&
                      ((((uintptr_t)a.M1) | ((uintptr_t)a.M2) | ((uintptr_t)a.M3) | ((uintptr_t)a.out) |
@@ -220,13 +222,13 @@ __global__ void __launch_bounds__(kAesThreads) shuffle_gather_kernel(const Gathe
     if (nch >= 64) {
         // wide rows: a CTA walks rows, its threads walk the row's 4-word chunks
         for (int64_t i = blockIdx.x; i < a.rows; i += gridDim.x)
-            for (int64_t c = threadIdx.x; c < nch; c += blockDim.x) gather_chunk<ONLINE>(T, a, i, c, tail, vec);
+            for (int64_t c = threadIdx.x; c < nch; c += blockDim.x) gather_chunk<ONLINE, TAB>(T, a, i, c, tail, vec);
     } else {
         const int64_t total = a.rows * nch;
         const int64_t stride = (int64_t)gridDim.x * blockDim.x;
         for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += stride) {
             const int64_t i = t / nch;
-            gather_chunk<ONLINE>(T, a, i, t - i * nch, tail, vec);
+            gather_chunk<ONLINE, TAB>(T, a, i, t - i * nch, tail, vec);
         }
     }
 }
@@ -620,8 +622,8 @@ __global__ void __launch_bounds__(1024) perm_rounds_block_kernel(const int32_t* 
 }
 
 int shuffle_init() {
-    OGM_CUDA_TRY(allow_big_smem(perm_draws_kernel, kAesTableBytes));
-    OGM_CUDA_TRY(allow_big_smem(shuffle_gather_kernel<true>, kAesTableBytes));
+    OGM_CUDA_TRY(allow_big_smem(perm_draws_kernel<AesTab>, kAesTableBytes));
+    OGM_CUDA_TRY(allow_big_smem(shuffle_gather_kernel<true, AesTab>, kAesTableBytes));
     OGM_CUDA_TRY(prefer_l1(win_gather4_kernel));
     OGM_CUDA_TRY(prefer_l1(gather_matrix_kernel));
     OGM_CUDA_TRY(prefer_l1(gather_matrix_rows_kernel));
@@ -642,7 +644,7 @@ static int seeded_permutation_impl(const uint8_t* key, const uint8_t* label, uin
     const int32_t init_cnt = (int32_t)(n - 1);
     OGM_CUDA_TRY(cudaMemcpyAsync(&cnts[0], &init_cnt, 4, cudaMemcpyHostToDevice, st));
     OGM_CUDA_TRY(cudaMemsetAsync(&cnts[1], 0, 4, st));
-    perm_draws_kernel<<<aes_grid(n), kAesThreads, kAesTableBytes, st>>>(ks, label_be(label), index, n, H,
+    aes_launch(perm_draws_kernel<AesTab>, perm_draws_kernel<AesTabSmall>, n, kAesThreads, st, ks, label_be(label), index, n, H,
                                                                         live[0], perm, R);
     OGM_LAUNCH_CHECK();
     if (n < 2) return OGM_OK;
@@ -775,7 +777,8 @@ int ogm_shuffle_gather(int64_t rows, int64_t words, int64_t width_bits, const in
     const int64_t work = rows * ((a.pitch + 3) / 4);
     cudaStream_t st = as_stream(stream);
     if (online) {
-        shuffle_gather_kernel<true><<<aes_grid(work), kAesThreads, kAesTableBytes, st>>>(a);
+        aes_launch(shuffle_gather_kernel<true, AesTab>, shuffle_gather_kernel<true, AesTabSmall>, work, kAesThreads, st,
+                   a);
     } else {
         launch_matrix_gather(a, st);
     }
