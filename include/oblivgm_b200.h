@@ -295,6 +295,21 @@ int ogm_gather_planned(int64_t rows, int64_t words, int64_t pitch, int64_t tile_
                        const uint32_t* m4, const uint32_t* m3, const uint32_t* r_mat, uint32_t* inter, uint32_t* out,
                        int passes, void* stream);
 
+/* Trio fast path (three co-resident parties): one whole 3-party shuffle of
+ * src/shuffle.py:80-144 -- permutations, blinding material and the four
+ * online steps -- in one call, bit-identical to the per-party protocol.
+ * The rows are packed from `nfields` fields per component (fields[c*nfields
+ * + f], c = 0..2; fpitch[c*nfields + f]; fwidth[f]; flags[c] a per-row flag bit vector
+ * packed first, or NULL) exactly as ogm_pack_gather does, `width_bits` =
+ * packed row width, `pitch` (a multiple of 4) the output row pitch.
+ * out[0..2] (rows x pitch) receive the new components R1, R2, R3.  Seeds are
+ * HOST pointers (s12 = seed shared by P1/P2, ...); tid = the table id. */
+int64_t ogm_trio_shuffle_workspace_bytes(int64_t rows, int64_t pitch);
+int ogm_trio_shuffle(const uint8_t* s12, const uint8_t* s23, const uint8_t* s31, uint64_t tid, int64_t rows,
+                     int64_t width_bits, int64_t pitch, int nfields, const uint32_t* const* fields,
+                     const int64_t* fpitch, const int64_t* fwidth, const uint32_t* const* flags,
+                     uint32_t* const* out, void* workspace, int64_t workspace_bytes, void* stream);
+
 /* ---- measurement -------------------------------------------------------- */
 
 /* Roofline denominator for the integer-ALU-bound kernels: issue rate of

@@ -72,6 +72,8 @@ SIGNATURES = {
     "ogm_gather_plan_workspace_bytes": ([_i64], _i64),
     "ogm_gather_plan": ([_i64, _vp, _i64, _i64, _vp, _vp, _vp, _vp, _i64, _vp], _int),
     "ogm_gather_planned": ([_i64, _i64, _i64, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _int, _vp], _int),
+    "ogm_trio_shuffle_workspace_bytes": ([_i64, _i64], _i64),
+    "ogm_trio_shuffle": ([_cp, _cp, _cp, _u64, _i64, _i64, _i64, _int, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _vp], _int),
     "ogm_measure_int_peak": ([ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double)], _int),
 }
 

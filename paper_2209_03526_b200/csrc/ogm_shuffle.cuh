@@ -915,4 +915,107 @@ int ogm_gather_planned(int64_t rows, int64_t words, int64_t pitch, int64_t tile_
     return OGM_OK;
 }
 
+// ---------------------------------------------------------------------------
+// Trio fast path: one whole 3-party shuffle (src/shuffle.py:80-144) for the
+// three co-resident parties in ONE call -- offline material and online steps
+// -- replacing ~25 host dispatches per shuffle (trio.Trio.shuffle).  Same
+// launches, same order, same results as the Python composition:
+//   pi12, pi23, pi31 = SHPI permutations of table id `tid`
+//   k1 = pi12 o pi31, k3 = pi31 o pi23                    (perm_compose)
+//   U = T12[k1] ^ T31[pi31], V = T12[pi12], W = T23[pi23] ^ R2,
+//   Z = T31[k3] ^ T23[pi23] ^ R1     (AES on the fly for narrow rows, from
+//                                     ogm_prf_rows tables for >= 64 words)
+//   x1 = pack(c1 ^ c2)[k1] ^ U, y1 = pack(c3)[pi12] ^ V       (P1, P2)
+//   c1 = x1[pi23] ^ W                                          (P2)
+//   R3 = y1[k3] ^ c1 ^ Z                                       (P3)
+// out = (R1, R2, R3), the new components.
+// ---------------------------------------------------------------------------
+static int64_t al256(int64_t b) { return (b + 255) & ~(int64_t)255; }
+
+int64_t ogm_trio_shuffle_workspace_bytes(int64_t rows, int64_t pitch) {
+    if (rows <= 0) return 256;
+    return 5 * al256(rows * 4) + al256(ogm_perm_workspace_bytes(rows)) + 7 * al256(rows * pitch * 4);
+}
+
+int ogm_trio_shuffle(const uint8_t* s12, const uint8_t* s23, const uint8_t* s31, uint64_t tid, int64_t rows,
+                     int64_t width_bits, int64_t pitch, int nfields, const uint32_t* const* fields,
+                     const int64_t* fpitch, const int64_t* fwidth, const uint32_t* const* flags,
+                     uint32_t* const* out, void* workspace, int64_t workspace_bytes, void* stream) {
+    using namespace ogm;
+    OGM_CHECK_ARG(s12 && s23 && s31 && out && fields, OGM_ERR_ARG, "seeds, fields and outputs are required");
+    OGM_CHECK_ARG(rows >= 0 && nfields >= 1 && width_bits >= 1 && pitch >= (width_bits + 31) / 32 && pitch % 4 == 0,
+                  OGM_ERR_ARG, "bad trio shuffle shape");
+    OGM_CHECK_ARG(workspace_bytes >= ogm_trio_shuffle_workspace_bytes(rows, pitch), OGM_ERR_ARG,
+                  "trio shuffle workspace too small");
+    if (rows == 0) return OGM_OK;
+    static const uint8_t kPi[4] = {'S', 'H', 'P', 'I'}, kTb[4] = {'S', 'H', 'T', 'B'}, kRd[4] = {'S', 'H', 'R', 'D'};
+    uint8_t* w = (uint8_t*)workspace;
+    auto take = [&](int64_t bytes) { uint8_t* p = w; w += al256(bytes); return p; };
+    int32_t* pi12 = (int32_t*)take(rows * 4);
+    int32_t* pi23 = (int32_t*)take(rows * 4);
+    int32_t* pi31 = (int32_t*)take(rows * 4);
+    int32_t* k1 = (int32_t*)take(rows * 4);
+    int32_t* k3 = (int32_t*)take(rows * 4);
+    void* pws = take(ogm_perm_workspace_bytes(rows));
+    const int64_t tb = rows * pitch * 4;
+    uint32_t *u = (uint32_t*)take(tb), *v = (uint32_t*)take(tb), *wm = (uint32_t*)take(tb), *z = (uint32_t*)take(tb);
+    uint32_t *x1 = (uint32_t*)take(tb), *y1 = (uint32_t*)take(tb), *c1 = (uint32_t*)take(tb);
+    const int64_t W = (width_bits + 31) / 32;
+    int rc;
+#define OGM_TRY(x) \
+    if ((rc = (x)) != OGM_OK) return rc
+    OGM_TRY(ogm_seeded_permutation(s12, kPi, tid, rows, pi12, pws, stream));
+    OGM_TRY(ogm_seeded_permutation(s23, kPi, tid, rows, pi23, pws, stream));
+    OGM_TRY(ogm_seeded_permutation(s31, kPi, tid, rows, pi31, pws, stream));
+    OGM_TRY(ogm_perm_compose(rows, pi31, pi12, k1, stream));
+    OGM_TRY(ogm_perm_compose(rows, pi23, pi31, k3, stream));
+    uint32_t *r1 = out[0], *r2 = out[1], *r3 = out[2];
+    OGM_TRY(ogm_prf_rows(s31, kRd, tid, rows, width_bits, pitch, r1, stream));
+    OGM_TRY(ogm_prf_rows(s12, kRd, tid, rows, width_bits, pitch, r2, stream));
+    const int64_t P = pitch;
+    if (W >= 64) {
+        // wide rows: each blinding table once at the AES rate, then streaming combines
+        uint32_t *t12 = x1, *t31 = y1, *t23 = c1;  // scratch until the online steps
+        OGM_TRY(ogm_prf_rows(s12, kTb, tid, rows, width_bits, pitch, t12, stream));
+        OGM_TRY(ogm_prf_rows(s31, kTb, tid, rows, width_bits, pitch, t31, stream));
+        OGM_TRY(ogm_prf_rows(s23, kTb, tid, rows, width_bits, pitch, t23, stream));
+        OGM_TRY(ogm_shuffle_gather(rows, W, width_bits, pi31, pi12, nullptr, nullptr, nullptr, nullptr, nullptr, 0,
+                                   t12, nullptr, nullptr, 0, t31, nullptr, nullptr, 0, nullptr, 0, P, u, stream));
+        OGM_TRY(ogm_shuffle_gather(rows, W, width_bits, nullptr, pi12, nullptr, nullptr, nullptr, nullptr, nullptr, 0,
+                                   t12, nullptr, nullptr, 0, nullptr, nullptr, nullptr, 0, nullptr, 0, P, v, stream));
+        OGM_TRY(ogm_shuffle_gather(rows, W, width_bits, nullptr, pi23, nullptr, nullptr, nullptr, nullptr, nullptr, 0,
+                                   t23, nullptr, nullptr, 0, nullptr, nullptr, nullptr, 0, r2, 0, P, wm, stream));
+        OGM_TRY(ogm_shuffle_gather(rows, W, width_bits, pi23, pi31, nullptr, nullptr, nullptr, nullptr, nullptr, 0,
+                                   t31, nullptr, nullptr, 0, t23, nullptr, nullptr, 0, r1, 0, P, z, stream));
+    } else {
+        OGM_TRY(ogm_shuffle_gather(rows, W, width_bits, pi31, pi12, nullptr, nullptr, nullptr, s12, kTb, tid, nullptr,
+                                   s31, kTb, tid, nullptr, nullptr, nullptr, 0, nullptr, 0, P, u, stream));
+        OGM_TRY(ogm_shuffle_gather(rows, W, width_bits, nullptr, pi12, nullptr, nullptr, nullptr, s12, kTb, tid,
+                                   nullptr, nullptr, nullptr, 0, nullptr, nullptr, nullptr, 0, nullptr, 0, P, v,
+                                   stream));
+        OGM_TRY(ogm_shuffle_gather(rows, W, width_bits, nullptr, pi23, nullptr, nullptr, nullptr, s23, kTb, tid,
+                                   nullptr, nullptr, nullptr, 0, nullptr, s12, kRd, tid, nullptr, 0, P, wm, stream));
+        OGM_TRY(ogm_shuffle_gather(rows, W, width_bits, pi23, pi31, nullptr, nullptr, nullptr, s31, kTb, tid, nullptr,
+                                   s23, kTb, tid, nullptr, s31, kRd, tid, nullptr, 0, P, z, stream));
+    }
+    // online: P1 packs c1 ^ c2 at k1, P2 packs c3 at pi12 (ogm_pack_gather, set-major field lists)
+    const uint32_t* set01[2 * 64];
+    OGM_CHECK_ARG(nfields <= 64, OGM_ERR_ARG, "at most 64 fields");
+    for (int f = 0; f < nfields; f++) {
+        set01[f] = fields[f];
+        set01[nfields + f] = fields[nfields + f];
+    }
+    const uint32_t* fl01[2] = {flags ? flags[0] : nullptr, flags ? flags[1] : nullptr};
+    const uint32_t* fl2[1] = {flags ? flags[2] : nullptr};
+    OGM_TRY(ogm_pack_gather(rows, k1, 2, flags ? fl01 : nullptr, nfields, set01, fpitch, fwidth, u, x1, P, stream));
+    OGM_TRY(ogm_pack_gather(rows, pi12, 1, flags ? fl2 : nullptr, nfields, fields + 2 * nfields, fpitch + 2 * nfields,
+                            fwidth, v, y1, P, stream));
+    OGM_TRY(ogm_shuffle_gather(rows, W, width_bits, nullptr, pi23, x1, nullptr, nullptr, nullptr, nullptr, 0, nullptr,
+                               nullptr, nullptr, 0, nullptr, nullptr, nullptr, 0, wm, 0, P, c1, stream));
+    OGM_TRY(ogm_shuffle_gather(rows, W, width_bits, nullptr, k3, y1, nullptr, c1, nullptr, nullptr, 0, nullptr, nullptr,
+                               nullptr, 0, nullptr, nullptr, nullptr, 0, z, 0, P, r3, stream));
+#undef OGM_TRY
+    return OGM_OK;
+}
+
 }  // extern "C"

@@ -253,6 +253,11 @@ class Trio:
         prep = getattr(self, "_prepared", {}).pop((tid, rows, width), None)
         if prep is not None:
             return self._shuffle_online(comps, width, prep)
+        if online_blinds is None:
+            online_blinds = rows * words_for(width) * 4 > (4 << 30)
+        if not online_blinds:
+            return self._shuffle_native(comps, rows, width, tid)
+        # memory-lean mode: blinding rows generated inside the gathers
         s12, s23, s31 = self.s12, self.s23, self.s31
         pi12, pi23, pi31 = _perm(s12, tid, rows), _perm(s23, tid, rows), _perm(s31, tid, rows)
 
@@ -260,24 +265,46 @@ class Trio:
             return torch.empty((rows, _pitch(width)), dtype=torch.int32, device=self.dev)
 
         bt = (LABEL_BLIND, tid)
-        if online_blinds is None:
-            online_blinds = rows * words_for(width) * 4 > (4 << 30)
-        if online_blinds:
-            ab = self._xor01(comps)
-            x1 = gather(rows, width, tab(), outer=pi31, inner=pi12, m1=ab, t1=(s12, *bt), t2=(s31, *bt))
-            del ab
-            c3 = self.pack_gather(comps, (2,)) if isinstance(comps, PackedRows) else comps[2]
-            y1 = gather(rows, width, tab(), inner=pi12, m1=c3, t1=(s12, *bt))
-            del c3
-            c1 = gather(rows, width, tab(), inner=pi23, m1=x1, t1=(s23, *bt), r=(s12, LABEL_RAND, tid))
-            del x1
-            r3 = gather(rows, width, tab(), outer=pi23, inner=pi31, m1=y1, t1=(s31, *bt), t2=(s23, *bt), m3=c1,
-                        r=(s31, LABEL_RAND, tid))
-            del y1, c1
-            r1 = blind_table(s31, LABEL_RAND, tid, rows, width, self.dev, pitch=_pitch(width))
-            r2 = blind_table(s12, LABEL_RAND, tid, rows, width, self.dev, pitch=_pitch(width))
-            return [r1, r2, r3]
-        return self._shuffle_online(comps, width, self._material(tid, rows, width, pi12, pi23, pi31))
+        ab = self._xor01(comps)
+        x1 = gather(rows, width, tab(), outer=pi31, inner=pi12, m1=ab, t1=(s12, *bt), t2=(s31, *bt))
+        del ab
+        c3 = self.pack_gather(comps, (2,)) if isinstance(comps, PackedRows) else comps[2]
+        y1 = gather(rows, width, tab(), inner=pi12, m1=c3, t1=(s12, *bt))
+        del c3
+        c1 = gather(rows, width, tab(), inner=pi23, m1=x1, t1=(s23, *bt), r=(s12, LABEL_RAND, tid))
+        del x1
+        r3 = gather(rows, width, tab(), outer=pi23, inner=pi31, m1=y1, t1=(s31, *bt), t2=(s23, *bt), m3=c1,
+                    r=(s31, LABEL_RAND, tid))
+        del y1, c1
+        r1 = blind_table(s31, LABEL_RAND, tid, rows, width, self.dev, pitch=_pitch(width))
+        r2 = blind_table(s12, LABEL_RAND, tid, rows, width, self.dev, pitch=_pitch(width))
+        return [r1, r2, r3]
+
+    def _shuffle_native(self, comps, rows: int, width: int, tid: int) -> list:
+        """The whole shuffle (material + four online steps) in one
+        ogm_trio_shuffle call: the same launches as _material +
+        _shuffle_online, without ~25 host dispatches."""
+        P = _pitch(width)
+        if isinstance(comps, PackedRows):
+            fields = list(comps.fields)
+            flags = comps.flags
+        else:
+            fields = [(comps, width)]
+            flags = None
+        nf = len(fields)
+        mats = [fields[f][0][c] for c in range(3) for f in range(nf)]
+        pitches = [m.stride(0) if m.dim() == 2 else words_for(fields[f][1])
+                   for m, f in zip(mats, [f for _ in range(3) for f in range(nf)])]
+        out = [torch.empty((rows, P), dtype=torch.int32, device=self.dev) for _ in range(3)]
+        lib = _lib.load()
+        nb = int(lib.ogm_trio_shuffle_workspace_bytes(rows, P))
+        ws = self.__dict__.get("_shuffle_ws")
+        if ws is None or ws.numel() < nb:
+            ws = self._shuffle_ws = torch.empty((nb,), dtype=torch.uint8, device=self.dev)
+        _lib.call("ogm_trio_shuffle", self.s12, self.s23, self.s31, tid, rows, width, P, nf, A(mats),
+                  _lib.i64_array(pitches), _lib.i64_array([w for _, w in fields]), A(flags) if flags else None,
+                  A(out), _lib.ptr(ws), nb, _lib.stream_ptr())
+        return out
 
     def _xor01(self, comps) -> torch.Tensor:
         if isinstance(comps, PackedRows):
