@@ -239,6 +239,64 @@ def run_c3(args):
 
 
 # ---------------------------------------------------------------------------
+# Edge-list fetch (sec_access posting fold, src/engine.py:309-311) at scale
+# ---------------------------------------------------------------------------
+
+
+def run_access(args):
+    """The oblivious edge-list fetch's bandwidth kernel: the matched parent's
+    one-hot id folded over the posting tensor (X parents x L_max slots x
+    w(X_ne) words per component), all three parties in one launch.  The
+    dense reference layout is infeasible at C3 (L_max = 4096 -> ~4 TB per
+    component), so the C3 shape is scaled to X = X_ne =
+    20,000 and L_max = 64 (3.2 GB per component).  Check: XOR of the three
+    parties' additive folds equals the selected parent's plaintext posting
+    row (RSS reconstruction, size-independent)."""
+    dev = torch.device("cuda")
+    X, L, xne = args.access_rows, 64, args.access_rows
+    w = words_for(xne)
+    words = L * w
+    pitch = (words + 3) // 4 * 4
+    comps = [workloads.device_random_words(X * pitch, args.seed, 60 + c).reshape(X, pitch) for c in range(3)]
+    for c in comps:
+        c[:, words:] = 0
+    target = int(np.random.default_rng(args.seed).integers(0, X))
+    onehot = torch.zeros((words_for(X),), dtype=torch.int32, device=dev)
+    onehot[target // 32] = int(np.int32(np.uint32(1 << (target % 32))))
+    s1 = workloads.device_random_words(words_for(X), args.seed, 70)
+    s2 = workloads.device_random_words(words_for(X), args.seed, 71)
+    if X % 32:
+        s1[-1] &= (1 << (X % 32)) - 1
+        s2[-1] &= (1 << (X % 32)) - 1
+    sel = [s1, s2, onehot ^ s1 ^ s2]
+    outs = [torch.empty((words,), dtype=torch.int32, device=dev) for _ in range(3)]
+    A = _lib.ptr_array
+
+    def fold():
+        _lib.call("ogm_select_fold", X, words, pitch, 3, A(comps), A([comps[(q + 1) % 3] for q in range(3)]),
+                  A(sel), A([sel[(q + 1) % 3] for q in range(3)]), A(outs), _lib.stream_ptr())
+
+    fold()
+    got = outs[0] ^ outs[1] ^ outs[2]
+    want = (comps[0][target] ^ comps[1][target] ^ comps[2][target])[:words]
+    ok = bool(torch.equal(got, want))
+    for _ in range(args.warmup):
+        fold()
+    ev = events(args.steps + 1)
+    ev[0].record()
+    for s_ in range(args.steps):
+        fold()
+        ev[s_ + 1].record()
+    torch.cuda.synchronize()
+    ms = statistics.median(ev[i].elapsed_time(ev[i + 1]) for i in range(args.steps))
+    nbytes = 3 * X * words * 4
+    emit({"config": f"edge-list fetch fold: {X} parents x L_max {L} x w(X_ne={xne})={w} words, 3 parties",
+          "metric": "access_fold_GBps", "value": nbytes / (ms * 1e-3) / 1e9, "unit": "GB/s", "ms": ms,
+          "hbm_frac": nbytes / (ms * 1e-3) / 1e9 / HBM_PEAK, "algorithmic_bytes": nbytes,
+          "reconstructs_selected_row": ok})
+
+
+# ---------------------------------------------------------------------------
 # C5: shuffle / fetch sweep
 # ---------------------------------------------------------------------------
 
@@ -600,7 +658,8 @@ def run_c5_sharded(args):
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("which", choices=["c1", "c3", "c3p", "c4", "c5", "c5d", "all"])
+    ap.add_argument("which", choices=["c1", "c3", "c3p", "c4", "c5", "c5d", "access", "all"])
+    ap.add_argument("--access-rows", type=int, default=20_000)
     ap.add_argument("--c4-rows", type=int, default=2_000_000)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
@@ -623,6 +682,8 @@ def main():
         run_c3_pipeline(args)
     if args.which == "c5d":
         run_c5_sharded(args)
+    if args.which in ("access", "all"):
+        run_access(args)
 
 
 if __name__ == "__main__":

@@ -339,6 +339,62 @@ __global__ void select_fold_kernel(const FoldArgs a) {
     }
 }
 
+// The trio case of the fold (B_q = A_{q+1}: the three co-resident parties,
+// each component stored once) as a bandwidth kernel -- the sec_access posting
+// fold (src/engine.py:309-311) and the Case I fold stream whole tensors.
+// Each thread owns one 16-byte column chunk and a strided set of row blocks;
+// every component is loaded once per row (the generic kernel loads it twice,
+// as party q's A and party q-1's B), RB rows of 128-bit loads are in flight
+// per thread, the row's three selection bits are warp-broadcast loads, and
+// partial folds combine with atomicXor.
+template <int RB>
+__global__ void __launch_bounds__(256) select_fold_trio4_kernel(const FoldArgs a, int64_t nch, int64_t rgroups) {
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t c = t % nch;
+    const int64_t g = t / nch;
+    if (g >= rgroups) return;
+    const int64_t p4 = a.pitch >> 2;
+    const uint4* X0 = reinterpret_cast<const uint4*>(a.A[0]) + c;
+    const uint4* X1 = reinterpret_cast<const uint4*>(a.A[1]) + c;
+    const uint4* X2 = reinterpret_cast<const uint4*>(a.A[2]) + c;
+    uint4 acc[3] = {make_uint4(0, 0, 0, 0), make_uint4(0, 0, 0, 0), make_uint4(0, 0, 0, 0)};
+    for (int64_t r0 = g * RB; r0 < a.rows; r0 += rgroups * RB) {
+        uint4 v[RB][3];
+        uint32_t f[RB][3];
+#pragma unroll
+        for (int k = 0; k < RB; k++) {
+            const int64_t r = r0 + k;
+            const bool ok = r < a.rows;
+            const int64_t o = ok ? r * p4 : 0;
+            v[k][0] = ok ? __ldcs(X0 + o) : make_uint4(0, 0, 0, 0);
+            v[k][1] = ok ? __ldcs(X1 + o) : make_uint4(0, 0, 0, 0);
+            v[k][2] = ok ? __ldcs(X2 + o) : make_uint4(0, 0, 0, 0);
+#pragma unroll
+            for (int q = 0; q < 3; q++) f[k][q] = ok ? (__ldg(a.fa[q] + (r >> 5)) >> (r & 31)) & 1u : 0u;
+        }
+#pragma unroll
+        for (int k = 0; k < RB; k++) {
+#pragma unroll
+            for (int q = 0; q < 3; q++) {
+                const uint32_t ma = 0u - f[k][q], mb = 0u - f[k][(q + 1) % 3];
+                const uint4 x = v[k][q], y = v[k][(q + 1) % 3];
+                acc[q].x ^= ((x.x ^ y.x) & ma) ^ (x.x & mb);
+                acc[q].y ^= ((x.y ^ y.y) & ma) ^ (x.y & mb);
+                acc[q].z ^= ((x.z ^ y.z) & ma) ^ (x.z & mb);
+                acc[q].w ^= ((x.w ^ y.w) & ma) ^ (x.w & mb);
+            }
+        }
+    }
+#pragma unroll
+    for (int q = 0; q < 3; q++) {
+        const int64_t w = c * 4;
+        const uint32_t vals[4] = {acc[q].x, acc[q].y, acc[q].z, acc[q].w};
+#pragma unroll
+        for (int j = 0; j < 4; j++)
+            if (w + j < a.words && vals[j]) atomicXor(a.out[q] + w + j, vals[j]);
+    }
+}
+
 // ---------------------------------------------------------------------------
 // Bit-granular row packing (src/engine.py:227-233, 317-318), fused with the
 // first gather of the shuffle that consumes the rows (src/shuffle.py:106-118):
@@ -883,6 +939,24 @@ int ogm_select_fold(int64_t rows, int64_t words, int64_t pitch, int nparty, cons
     a.rows = rows;
     a.words = words;
     a.pitch = pitch;
+    bool trio = nparty == 3 && (pitch & 3) == 0;
+    for (int q = 0; q < nparty && trio; q++)
+        trio = B[q] == A[(q + 1) % 3] && fb[q] == fa[(q + 1) % 3] && (((uintptr_t)A[q]) & 15) == 0;
+    if (trio) {
+        const int64_t nch = (words + 3) / 4;
+        // ~32K threads' worth of (chunk, row-group) work per SM: many short row
+        // strides beat few long ones (access fold at 20K x 40K words: 2048/SM
+        // 5.3 TB/s, 16384/SM 6.59, 32768/SM 6.64, 65536/SM 6.53)
+        constexpr int RB = 4;
+        int64_t rgroups = ((int64_t)sm_count() * 32768 + nch - 1) / nch;
+        const int64_t rblocks = (rows + RB - 1) / RB;
+        if (rgroups > rblocks) rgroups = rblocks;
+        if (rgroups < 1) rgroups = 1;
+        const int64_t threads = nch * rgroups;
+        select_fold_trio4_kernel<RB><<<(int)((threads + 255) / 256), 256, 0, st>>>(a, nch, rgroups);
+        OGM_LAUNCH_CHECK();
+        return OGM_OK;
+    }
     int64_t threads_total = words * rows;
     int64_t cap = (int64_t)sm_count() * 2048;
     if (threads_total > cap) threads_total = cap;
