@@ -339,45 +339,52 @@ __global__ void select_fold_kernel(const FoldArgs a) {
     }
 }
 
-// The trio case of the fold (B_q = A_{q+1}: the three co-resident parties,
-// each component stored once) as a bandwidth kernel -- the sec_access posting
-// fold (src/engine.py:309-311) and the Case I fold stream whole tensors.
-// Each thread owns one 16-byte column chunk and a strided set of row blocks;
-// every component is loaded once per row (the generic kernel loads it twice,
-// as party q's A and party q-1's B), RB rows of 128-bit loads are in flight
-// per thread, the row's three selection bits are warp-broadcast loads, and
-// partial folds combine with atomicXor.
-template <int RB>
-__global__ void __launch_bounds__(256) select_fold_trio4_kernel(const FoldArgs a, int64_t nch, int64_t rgroups) {
+// The fold as a bandwidth kernel for aligned 16-byte-pitched tensors -- the
+// sec_access posting fold (src/engine.py:309-311) and the Case I fold stream
+// whole tensors.  NP = 3 is the trio case (B_q = A_{q+1}, fb_q = fa_{q+1}: the
+// three co-resident parties, each component stored once and loaded once per
+// row; the generic kernel loads it twice), NP = 1 one party's (A, B).  Each
+// thread owns one 16-byte column chunk and a strided set of RB-row blocks
+// (RB rows of 128-bit loads in flight), the row's selection bits are
+// warp-broadcast loads, and partial folds combine with atomicXor.
+template <int NP, int RB>
+__global__ void __launch_bounds__(256) select_fold_vec4_kernel(const FoldArgs a, int64_t nch, int64_t rgroups) {
+    constexpr int NC = NP == 1 ? 2 : 3;
     const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t c = t % nch;
     const int64_t g = t / nch;
     if (g >= rgroups) return;
     const int64_t p4 = a.pitch >> 2;
-    const uint4* X0 = reinterpret_cast<const uint4*>(a.A[0]) + c;
-    const uint4* X1 = reinterpret_cast<const uint4*>(a.A[1]) + c;
-    const uint4* X2 = reinterpret_cast<const uint4*>(a.A[2]) + c;
-    uint4 acc[3] = {make_uint4(0, 0, 0, 0), make_uint4(0, 0, 0, 0), make_uint4(0, 0, 0, 0)};
+    const uint4* X[NC];
+    const uint32_t* F[NC];
+#pragma unroll
+    for (int k = 0; k < NC; k++) {
+        X[k] = reinterpret_cast<const uint4*>(NP == 1 && k == 1 ? a.B[0] : a.A[k]) + c;
+        F[k] = NP == 1 && k == 1 ? a.fb[0] : a.fa[k];
+    }
+    uint4 acc[NP];
+#pragma unroll
+    for (int q = 0; q < NP; q++) acc[q] = make_uint4(0, 0, 0, 0);
     for (int64_t r0 = g * RB; r0 < a.rows; r0 += rgroups * RB) {
-        uint4 v[RB][3];
-        uint32_t f[RB][3];
+        uint4 v[RB][NC];
+        uint32_t f[RB][NC];
 #pragma unroll
         for (int k = 0; k < RB; k++) {
             const int64_t r = r0 + k;
             const bool ok = r < a.rows;
             const int64_t o = ok ? r * p4 : 0;
-            v[k][0] = ok ? __ldcs(X0 + o) : make_uint4(0, 0, 0, 0);
-            v[k][1] = ok ? __ldcs(X1 + o) : make_uint4(0, 0, 0, 0);
-            v[k][2] = ok ? __ldcs(X2 + o) : make_uint4(0, 0, 0, 0);
 #pragma unroll
-            for (int q = 0; q < 3; q++) f[k][q] = ok ? (__ldg(a.fa[q] + (r >> 5)) >> (r & 31)) & 1u : 0u;
+            for (int m = 0; m < NC; m++) {
+                v[k][m] = ok ? __ldcs(X[m] + o) : make_uint4(0, 0, 0, 0);
+                f[k][m] = ok ? (__ldg(F[m] + (r >> 5)) >> (r & 31)) & 1u : 0u;
+            }
         }
 #pragma unroll
         for (int k = 0; k < RB; k++) {
 #pragma unroll
-            for (int q = 0; q < 3; q++) {
-                const uint32_t ma = 0u - f[k][q], mb = 0u - f[k][(q + 1) % 3];
-                const uint4 x = v[k][q], y = v[k][(q + 1) % 3];
+            for (int q = 0; q < NP; q++) {
+                const uint32_t ma = 0u - f[k][q], mb = 0u - f[k][(q + 1) % NC];
+                const uint4 x = v[k][q], y = v[k][(q + 1) % NC];
                 acc[q].x ^= ((x.x ^ y.x) & ma) ^ (x.x & mb);
                 acc[q].y ^= ((x.y ^ y.y) & ma) ^ (x.y & mb);
                 acc[q].z ^= ((x.z ^ y.z) & ma) ^ (x.z & mb);
@@ -386,7 +393,7 @@ __global__ void __launch_bounds__(256) select_fold_trio4_kernel(const FoldArgs a
         }
     }
 #pragma unroll
-    for (int q = 0; q < 3; q++) {
+    for (int q = 0; q < NP; q++) {
         const int64_t w = c * 4;
         const uint32_t vals[4] = {acc[q].x, acc[q].y, acc[q].z, acc[q].w};
 #pragma unroll
@@ -939,21 +946,26 @@ int ogm_select_fold(int64_t rows, int64_t words, int64_t pitch, int nparty, cons
     a.rows = rows;
     a.words = words;
     a.pitch = pitch;
-    bool trio = nparty == 3 && (pitch & 3) == 0;
-    for (int q = 0; q < nparty && trio; q++)
-        trio = B[q] == A[(q + 1) % 3] && fb[q] == fa[(q + 1) % 3] && (((uintptr_t)A[q]) & 15) == 0;
-    if (trio) {
-        const int64_t nch = (words + 3) / 4;
+    bool vec = (pitch & 3) == 0 && (nparty == 1 || nparty == 3);
+    for (int q = 0; q < nparty && vec; q++) {
+        vec = (((uintptr_t)A[q]) & 15) == 0 && (((uintptr_t)B[q]) & 15) == 0;
+        if (nparty == 3) vec = vec && B[q] == A[(q + 1) % 3] && fb[q] == fa[(q + 1) % 3];
+    }
+    if (vec) {
         // ~32K threads' worth of (chunk, row-group) work per SM: many short row
         // strides beat few long ones (access fold at 20K x 40K words: 2048/SM
         // 5.3 TB/s, 16384/SM 6.59, 32768/SM 6.64, 65536/SM 6.53)
         constexpr int RB = 4;
+        const int64_t nch = (words + 3) / 4;
         int64_t rgroups = ((int64_t)sm_count() * 32768 + nch - 1) / nch;
         const int64_t rblocks = (rows + RB - 1) / RB;
         if (rgroups > rblocks) rgroups = rblocks;
         if (rgroups < 1) rgroups = 1;
-        const int64_t threads = nch * rgroups;
-        select_fold_trio4_kernel<RB><<<(int)((threads + 255) / 256), 256, 0, st>>>(a, nch, rgroups);
+        const int blocks = (int)((nch * rgroups + 255) / 256);
+        if (nparty == 3)
+            select_fold_vec4_kernel<3, RB><<<blocks, 256, 0, st>>>(a, nch, rgroups);
+        else
+            select_fold_vec4_kernel<1, RB><<<blocks, 256, 0, st>>>(a, nch, rgroups);
         OGM_LAUNCH_CHECK();
         return OGM_OK;
     }

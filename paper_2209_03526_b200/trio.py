@@ -29,7 +29,7 @@ from dataclasses import dataclass, field
 import torch
 
 from . import _lib, fss
-from .bits import BitVector, words_for
+from .bits import BitVector, rows2d, words_for
 from .engine import MatchedRecord, MatchResultSet, _assemble
 from .net import make_session_configs
 from .rss import DBits, SharedBitVector
@@ -407,7 +407,7 @@ class Trio:
 
     def _fold(self, flags: list, mats: list, width: int) -> list:
         rows = mats[0].shape[0]
-        flat = [m.reshape(rows, -1) if m.dim() != 2 else m for m in mats]
+        flat = [rows2d(m) for m in mats]  # padded row pitches stay zero-copy
         words = flat[0].shape[1]
         outs = [self._empty(words) for _ in range(3)]
         _lib.call("ogm_select_fold", rows, words, flat[0].stride(0) if rows else words, 3, A(flat),
