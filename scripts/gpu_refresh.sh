@@ -14,4 +14,10 @@ timeout 1500 python bench_configs.py c5 --min-log 16 --max-log 28 > $O/c5.jsonl 
 for f in c1 c3 c3p c4 c5; do echo "$f: $(wc -l < $O/$f.jsonl) lines; $(tail -1 $O/$f.err)"; done
 # launch list of the headline command (cold, serialised: shares only)
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file $O/bench_launches.csv \
-  python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu --no-query > $O/bench_ncu.log 2>&1; echo "ncu rc=$?"
+  python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu --no-query --no-c4 > $O/bench_ncu.log 2>&1; echo "ncu rc=$?"
+timeout 600 python bench_configs.py access > $O/access.jsonl 2> $O/access.err
+timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -k regex:select_fold --csv \
+  python bench_configs.py access --steps 2 --warmup 1 > $O/access_ncu.csv 2>&1
+timeout 600 ncu --profile-from-start off --metrics gpu__time_duration.sum --clock-control none --csv \
+  python scripts/exp_trio_gpu.py > $O/trio_c1_launches.csv 2>&1
+echo refresh-done
