@@ -239,6 +239,114 @@ def run_c3(args):
 
 
 # ---------------------------------------------------------------------------
+# Per-function throughput beside the CPU port
+# ---------------------------------------------------------------------------
+
+
+def run_funcs(args):
+    """One line per primitive of the path at a GPU-filling size, device-timed,
+    with the oracle port timed on the host (one core) on a bounded sample;
+    results of the two are compared on the sample where that is cheap."""
+    import oracle
+
+    dev = torch.device("cuda")
+    gen = torch.Generator(device="cuda").manual_seed(args.seed)
+
+    def timed(fn, reps=5):
+        for _ in range(2):
+            fn()
+        ev = events(reps + 1)
+        ev[0].record()
+        for i in range(reps):
+            fn()
+            ev[i + 1].record()
+        torch.cuda.synchronize()
+        return statistics.median(ev[i].elapsed_time(ev[i + 1]) for i in range(reps)) * 1e-3
+
+    def cpu(fn):
+        t = time.perf_counter()
+        r = fn()
+        return time.perf_counter() - t, r
+
+    def line(row, ref, name, unit, gpu_rate, n_gpu, cpu_rate, n_cpu, equal, survey):
+        emit({"row": row, "reference": ref, "function": name, "unit": unit, "value": gpu_rate,
+              "gpu_sample": n_gpu, "cpu_baseline": {"value": cpu_rate, "unit": unit, "cores": 1, "kind": "port",
+                                                      "sample": n_cpu},
+              "gpu_equals_port_on_sample": equal, "survey_time_today_1core": survey})
+
+    # a1 prg_expand (src/prf.py:41-57): 3 AES per seed
+    n = 1 << 24
+    seeds = torch.randint(0, 256, (n, 16), dtype=torch.uint8, device=dev, generator=gen)
+    from paper_2209_03526_b200 import prf
+    t = timed(lambda: prf.prg_expand(seeds))
+    sm = seeds[: 1 << 16].cpu().numpy().view(np.uint64).reshape(-1, 2)
+    tc, ref = cpu(lambda: oracle.prg_expand(sm))
+    got = prf.prg_expand(seeds[: 1 << 16])
+    eq = bool(np.array_equal(got[0].cpu().numpy().view(np.uint64).reshape(-1, 2), ref[0]))
+    line("a1", "src/prf.py:41-57", "prg_expand", "seeds/s", n / t, n, (1 << 16) / tc, 1 << 16, eq,
+         "8-15 M nodes/s batched")
+    del seeds
+    # a2 prf_stream (src/prf.py:70-92): AES-CTR
+    nw = 1 << 28
+    out = torch.empty((nw,), dtype=torch.int32, device=dev)
+    key = bytes(range(16))
+    t = timed(lambda: prf.prf_words_device(key, b"SHTB", 7, nw, out=out))
+    tc, ref = cpu(lambda: oracle.prf_stream(key, b"SHTB", 7, 1 << 24))
+    eq = out[: 1 << 22].cpu().numpy().tobytes() == ref
+    line("a2", "src/prf.py:70-92", "prf_stream (AES-128-CTR)", "GB/s", 4 * nw / t / 1e9, 4 * nw,
+         (1 << 24) / tc / 1e9, 1 << 24, eq, "0.33 GB/s")
+    del out
+    # a3 seeded_permutation (src/prf.py:95-105): Fisher-Yates
+    n = 1 << 24
+    t = timed(lambda: prf.seeded_permutation_device(key, b"SHPI", 3, n), reps=3)
+    tc, ref = cpu(lambda: oracle.seeded_permutation(key, b"SHPI", 3, 1 << 20))
+    eq = bool(np.array_equal(prf.seeded_permutation_device(key, b"SHPI", 3, 1 << 20).cpu().numpy(), ref))
+    line("a3", "src/prf.py:95-105", "seeded_permutation", "swaps/s", (n - 1) / t, n, ((1 << 20) - 1) / tc, 1 << 20,
+         eq, "0.85 M swaps/s")
+    # a6 keygen (src/fss.py:116-157): DCF, 32-bit domain
+    k = 1 << 22
+    alphas = torch.randint(-(1 << 31), 1 << 31, (k,), dtype=torch.int32, device=dev, generator=gen)
+    r0 = torch.randint(0, 256, (k, 16), dtype=torch.uint8, device=dev, generator=gen)
+    r1 = torch.randint(0, 256, (k, 16), dtype=torch.uint8, device=dev, generator=gen)
+    t = timed(lambda: fss.gen_batch(True, 32, alphas, r0, r1), reps=3)
+    ks = 4096
+    a_h = alphas[:ks].cpu().numpy().view(np.uint32).astype(np.uint64)
+    tc, (o0, _) = cpu(lambda: oracle.tree_gen_batch(a_h, 32, r0[:ks].cpu().numpy(), r1[:ks].cpu().numpy(), True,
+                                                     nthreads=1))
+    b0, _ = fss.gen_batch(True, 32, alphas[:ks], r0[:ks], r1[:ks])
+    eq = bool(np.array_equal(b0.seed_cw.cpu().numpy().transpose(1, 0, 2), o0.seed_cw))
+    line("a6", "src/fss.py:116-157", "dcf keygen (_tree_gen, 32-bit)", "key pairs/s", k / t, k, ks / tc, ks, eq,
+         "1.39 ms/pair")
+    del alphas, r0, r1
+    # a8 full-domain eval (src/fss.py:302-337): 16 keys x 2^20 leaves
+    nk, dom = 16, 1 << 20
+    al = torch.randint(0, dom, (nk,), dtype=torch.int32, device=dev, generator=gen)
+    rr = torch.randint(0, 256, (nk, 16), dtype=torch.uint8, device=dev, generator=gen)
+    kb, _ = fss.gen_batch(True, 20, al, rr, rr)
+    fd = fss.full_domain(kb, dom)
+    t = timed(lambda: fss.full_domain(kb, dom, out=fd))
+    ok0, _ = oracle.tree_gen_batch(al[:1].cpu().numpy().view(np.uint32).astype(np.uint64), 20, rr[:1].cpu().numpy(),
+                                   rr[:1].cpu().numpy(), True)
+    tc, ref = cpu(lambda: oracle.full_domain(ok0, 0, dom))
+    eq = bool(np.array_equal(fd[0].cpu().numpy().view(np.uint32), ref))
+    line("a8", "src/fss.py:302-337", "full-domain eval (DCF, 2^20 leaves)", "leaves/s", nk * dom / t, nk * dom,
+         dom / tc, dom, eq, "~9.5 M leaves/s")
+    # a10 zero shares, three parties per launch (src/rss.py:143-148)
+    nbits = 1 << 32
+    outs = [torch.empty((nbits // 32,), dtype=torch.int32, device=dev) for _ in range(3)]
+    cfgs = make_session_configs(b"\x12" * 16)
+    zk = [c.zero_key_own for c in cfgs]
+    A = _lib.ptr_array
+    t = timed(lambda: _lib.call("ogm_zero_share_trio", zk[0], zk[1], zk[2], 9, nbits, None, A(outs),
+                                _lib.stream_ptr()))
+    tc, ref = cpu(lambda: oracle.zero_share(zk[0], zk[2], 9, 1 << 24))
+    eq = bool(np.array_equal(outs[0][: (1 << 24) // 32].cpu().numpy().view(np.uint32), ref))
+    line("a10", "src/rss.py:143-148", "zero shares, 3 parties per launch", "GB/s of shares",
+         3 * nbits / 8 / t / 1e9, 3 * nbits, (1 << 24) / 8 / tc / 1e9, 1 << 24, eq, "AES-CTR 0.33 GB/s")
+    del outs
+
+
+# ---------------------------------------------------------------------------
 # Edge-list fetch (sec_access posting fold, src/engine.py:309-311) at scale
 # ---------------------------------------------------------------------------
 
@@ -658,7 +766,7 @@ def run_c5_sharded(args):
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("which", choices=["c1", "c3", "c3p", "c4", "c5", "c5d", "access", "all"])
+    ap.add_argument("which", choices=["c1", "c3", "c3p", "c4", "c5", "c5d", "access", "funcs", "all"])
     ap.add_argument("--access-rows", type=int, default=20_000)
     ap.add_argument("--c4-rows", type=int, default=2_000_000)
     ap.add_argument("--steps", type=int, default=5)
@@ -684,6 +792,8 @@ def main():
         run_c5_sharded(args)
     if args.which in ("access", "all"):
         run_access(args)
+    if args.which in ("funcs", "all"):
+        run_funcs(args)
 
 
 if __name__ == "__main__":
