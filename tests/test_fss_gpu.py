@@ -277,3 +277,34 @@ def test_perm_invert(n):
     want = np.empty_like(pn)
     want[pn] = np.arange(n, dtype=pn.dtype)
     assert np.array_equal(inv.cpu().numpy(), want)
+
+
+def test_c2_full_size_eval_matches_oracle():
+    """BASELINE config 2 at full size: all 2^24 DCF keys (32-bit domain), one
+    point each, evaluated on the GPU and by the oracle's C restatement of
+    src/fss.py:257-281 (all host threads) on the very same key material --
+    bit-exact for every key, plus the pair property for both parties."""
+    K, bits = 1 << 24, 32
+    g = torch.Generator(device="cuda").manual_seed(2424)
+    alphas = torch.randint(-(1 << 31), 1 << 31, (K,), dtype=torch.int32, device="cuda", generator=g)
+    pts = torch.randint(-(1 << 31), 1 << 31, (K,), dtype=torch.int32, device="cuda", generator=g)
+    r0 = torch.randint(0, 256, (K, 16), dtype=torch.uint8, device="cuda", generator=g)
+    r1 = torch.randint(0, 256, (K, 16), dtype=torch.uint8, device="cuda", generator=g)
+    b0, b1 = fss.gen_batch(True, bits, alphas, r0, r1)
+    e0 = unpack(host_u32(fss.eval_points(b0, pts)), K)
+    e1 = unpack(host_u32(fss.eval_points(b1, pts)), K)
+    a = alphas.cpu().numpy().view(np.uint32)
+    x = pts.cpu().numpy().view(np.uint32)
+    assert np.array_equal(e0 ^ e1, (x < a).astype(np.uint8))
+    # the device key material of party 0 as an oracle TreeKey (key-major)
+    ctrl = b0.ctrl.cpu().numpy().view(np.uint32)                     # (3, K) bit-planes over levels
+    lv = np.arange(bits, dtype=np.uint32)
+    cc = np.zeros((K, bits), np.uint8)
+    for j in range(3):
+        cc |= (((ctrl[j][:, None] >> lv[None, :]) & 1) << j).astype(np.uint8)
+    flags = b0.flags.cpu().numpy()
+    key = oracle.TreeKey(bits, True, b0.root.cpu().numpy(), flags & 1,
+                         b0.seed_cw.cpu().numpy().transpose(1, 0, 2), cc, (flags >> 1) & 1, (flags >> 2) & 1)
+    del ctrl, cc
+    want = oracle.eval_points(key, x.astype(np.uint64))
+    assert np.array_equal(e0, want)
