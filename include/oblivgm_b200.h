@@ -310,6 +310,18 @@ int ogm_trio_shuffle(const uint8_t* s12, const uint8_t* s23, const uint8_t* s31,
                      const int64_t* fpitch, const int64_t* fwidth, const uint32_t* const* flags,
                      uint32_t* const* out, void* workspace, int64_t workspace_bytes, void* stream);
 
+/* Trio fast path: open the flag column (bit 0 of every row) of a shuffled
+ * table held as three components comps[0..2] (rows x pitch): plain = the
+ * XOR of the column (copied to plain_host, words_for(rows) words: the vector
+ * every party notes), keep the flagged rows in order, and write each kept
+ * row's field f (bits [bit_off[f], +width[f])) of component c to
+ * out[c*nfields + f] (capacity rows, pitch opitch[f]).  Synchronous;
+ * *kept = number of kept rows (src/engine.py:243-269, 321-334). */
+int64_t ogm_trio_open_keep_workspace_bytes(int64_t rows);
+int ogm_trio_open_keep(const uint32_t* const* comps, int64_t rows, int64_t pitch, uint32_t* plain_host, int nfields,
+                       const int64_t* bit_off, const int64_t* width, uint32_t* const* out, const int64_t* opitch,
+                       int64_t* kept, void* workspace, int64_t workspace_bytes, void* stream);
+
 /* ---- measurement -------------------------------------------------------- */
 
 /* Roofline denominator for the integer-ALU-bound kernels: issue rate of

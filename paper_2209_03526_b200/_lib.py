@@ -74,12 +74,15 @@ SIGNATURES = {
     "ogm_gather_planned": ([_i64, _i64, _i64, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _int, _vp], _int),
     "ogm_trio_shuffle_workspace_bytes": ([_i64, _i64], _i64),
     "ogm_trio_shuffle": ([_cp, _cp, _cp, _u64, _i64, _i64, _i64, _int, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _vp], _int),
+    "ogm_trio_open_keep_workspace_bytes": ([_i64], _i64),
+    "ogm_trio_open_keep": ([_vp, _i64, _i64, _vp, _int, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _vp], _int),
     "ogm_measure_int_peak": ([ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double)], _int),
 }
 
 # Entry points that may block on the device (host syncs); every other entry
 # point only enqueues work on the caller's stream and returns in microseconds.
-BLOCKING = {"ogm_init", "ogm_seeded_permutation", "ogm_fss_eval_points_host", "ogm_measure_int_peak"}
+BLOCKING = {"ogm_init", "ogm_seeded_permutation", "ogm_fss_eval_points_host", "ogm_measure_int_peak",
+            "ogm_trio_open_keep", "ogm_trio_shuffle"}
 
 _lib = None
 _fast = None

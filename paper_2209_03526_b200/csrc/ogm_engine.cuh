@@ -676,6 +676,25 @@ __global__ void column_bit_kernel(const uint32_t* __restrict__ mat, int64_t pitc
     }
 }
 
+// The opened flag column of a trio table: bit i of word w = XOR over the
+// three components of bit 0 of row 32w+i (src/rss.py:184-206 on the column).
+__global__ void column_open3_kernel(const uint32_t* __restrict__ m0, const uint32_t* __restrict__ m1,
+                                    const uint32_t* __restrict__ m2, int64_t pitch, int64_t rows,
+                                    uint32_t* __restrict__ out) {
+    const int64_t nw = (rows + 31) >> 5;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; w < nw; w += stride) {
+        uint32_t v = 0;
+        const int64_t r0 = w << 5;
+        const int n = (int)min((int64_t)32, rows - r0);
+        for (int i = 0; i < n; i++) {
+            const int64_t o = (r0 + i) * pitch;
+            v |= ((m0[o] ^ m1[o] ^ m2[o]) & 1u) << i;
+        }
+        out[w] = v;
+    }
+}
+
 // ---------------------------------------------------------------------------
 // src/engine.py:105-120 _select_many_additive: GF(2) product of K one-hot
 // selector rows (K, X) with (X, W) share rows.  Selectors are transposed to
@@ -1149,6 +1168,53 @@ int ogm_select_many(int64_t K, int64_t X, int64_t words, int64_t pitch, const ui
                                                                               out + k0 * opitch, opitch);
     }
     OGM_LAUNCH_CHECK();
+    return OGM_OK;
+}
+
+// Trio fast path: open the flag column of a shuffled three-component table,
+// keep the flagged rows in order and slice their fields out (src/engine.py:
+// 243-269, 321-334) -- one synchronous call instead of ~12 dispatches.
+int64_t ogm_trio_open_keep_workspace_bytes(int64_t rows) {
+    const int64_t w = (rows + 31) / 32;
+    return ((w * 4 + 255) & ~(int64_t)255) + ((rows * 4 + 255) & ~(int64_t)255) + 256 +
+           ogm_compact_workspace_bytes(rows > 0 ? rows : 1);
+}
+
+int ogm_trio_open_keep(const uint32_t* const* comps, int64_t rows, int64_t pitch, uint32_t* plain_host, int nfields,
+                       const int64_t* bit_off, const int64_t* width, uint32_t* const* out, const int64_t* opitch,
+                       int64_t* kept, void* workspace, int64_t workspace_bytes, void* stream) {
+    using namespace ogm;
+    OGM_CHECK_ARG(comps && plain_host && kept && rows >= 0 && pitch >= 1 && nfields >= 0, OGM_ERR_ARG,
+                  "bad open-keep arguments");
+    OGM_CHECK_ARG(workspace_bytes >= ogm_trio_open_keep_workspace_bytes(rows), OGM_ERR_ARG,
+                  "open-keep workspace too small");
+    *kept = 0;
+    if (rows == 0) return OGM_OK;
+    OGM_ENSURE_INIT();
+    cudaStream_t st = as_stream(stream);
+    const int64_t nw = (rows + 31) / 32;
+    uint8_t* w = (uint8_t*)workspace;
+    uint32_t* plain = (uint32_t*)w;
+    w += (nw * 4 + 255) & ~(int64_t)255;
+    int32_t* idx = (int32_t*)w;
+    w += (rows * 4 + 255) & ~(int64_t)255;
+    int64_t* cnt = (int64_t*)w;
+    w += 256;
+    column_open3_kernel<<<grid_for(nw), 256, 0, st>>>(comps[0], comps[1], comps[2], pitch, rows, plain);
+    OGM_LAUNCH_CHECK();
+    int rc = ogm_compact_bits(rows, plain, idx, cnt, w, ogm_compact_workspace_bytes(rows), stream);
+    if (rc) return rc;
+    OGM_CUDA_TRY(cudaMemcpyAsync(plain_host, plain, nw * 4, cudaMemcpyDeviceToHost, st));
+    OGM_CUDA_TRY(cudaStreamSynchronize(st));
+    int64_t k = 0;
+    for (int64_t i = 0; i < nw; i++) k += __builtin_popcount(plain_host[i]);
+    *kept = k;
+    for (int c = 0; c < 3; c++)
+        for (int f = 0; f < nfields; f++) {
+            rc = ogm_extract_field(comps[c], pitch, idx, k, bit_off[f], width[f], out[c * nfields + f], opitch[f],
+                                   stream);
+            if (rc) return rc;
+        }
     return OGM_OK;
 }
 

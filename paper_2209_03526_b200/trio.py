@@ -24,8 +24,10 @@ unchanged; only the scheduling is fused.
 
 from __future__ import annotations
 
+import ctypes
 from dataclasses import dataclass, field
 
+import numpy as np
 import torch
 
 from . import _lib, fss
@@ -425,30 +427,33 @@ class Trio:
         return TrioRecords(group.parent_slot, group.parent_record, 1, group.id_width, [c[None] for c in ids],
                            {a: [c[None] for c in v] for a, v in attrs.items()}, dict(group.attr_widths))
 
-    def _column(self, mat) -> torch.Tensor:
-        rows = mat.shape[0]
-        out = self._empty(words_for(rows))
-        _lib.call("ogm_column_bits", _lib.ptr(mat), mat.shape[1], rows, _lib.ptr(out), _lib.stream_ptr())
-        return out
-
-    def _open_keep(self, shuffled: list, rows: int, phase: str, audit: list):
-        plain, host = self.open([self._column(m) for m in shuffled], rows)
-        audit.append((phase, host.to_bits().copy()))
-        idx = torch.empty((max(rows, 1),), dtype=torch.int32, device=self.dev)
-        cnt = torch.empty((1,), dtype=torch.int64, device=self.dev)
-        nb = int(_lib.load().ogm_compact_workspace_bytes(rows))
-        ws = torch.empty((nb,), dtype=torch.uint8, device=self.dev)
-        _lib.call("ogm_compact_bits", rows, _lib.ptr(plain), _lib.ptr(idx), _lib.ptr(cnt), _lib.ptr(ws), nb,
+    def _open_keep(self, shuffled: list, rows: int, phase: str, audit: list, fields: list) -> tuple:
+        """src/engine.py:243-269 / :321-334 for all parties in one synchronous
+        call (ogm_trio_open_keep): open the flag column (the next open label),
+        keep the flagged rows in order and slice each (bit offset, width)
+        field out of the three components.  Returns (k, [[c1, c2, c3] per field])."""
+        self.label += 1
+        nw = words_for(rows)
+        host = np.empty((max(nw, 1),), np.uint32)
+        outs = [[torch.empty((max(rows, 1), words_for(w)), dtype=torch.int32, device=self.dev) for _ in range(3)]
+                for _, w in fields]
+        lib = _lib.load()
+        nb = int(lib.ogm_trio_open_keep_workspace_bytes(rows))
+        ws = self.__dict__.get("_open_ws")
+        if ws is None or ws.numel() < nb:
+            ws = self._open_ws = torch.empty((nb,), dtype=torch.uint8, device=self.dev)
+        kept = ctypes.c_int64(0)
+        nf = len(fields)
+        _lib.call("ogm_trio_open_keep", A(shuffled), rows, shuffled[0].stride(0), host.ctypes.data, nf,
+                  _lib.i64_array([o for o, _ in fields]), _lib.i64_array([w for _, w in fields]),
+                  A([outs[f][c] for c in range(3) for f in range(nf)]),
+                  _lib.i64_array([words_for(w) for _, w in fields]), ctypes.byref(kept), _lib.ptr(ws), nb,
                   _lib.stream_ptr())
-        k = int(host.popcount())  # the opened mask is public and already on the host
-        return idx[:k], k
-
-    def _extract(self, src, idx, n, off, width):
-        out = torch.empty((n, words_for(width)), dtype=torch.int32, device=self.dev)
-        if n:
-            _lib.call("ogm_extract_field", _lib.ptr(src), src.shape[1], _lib.ptr(idx), n, off, width, _lib.ptr(out),
-                      out.shape[1], _lib.stream_ptr())
-        return out
+        opened = BitVector(host[:nw], rows)
+        self.opened.append((self.label, opened))
+        audit.append((phase, opened.to_bits().copy()))
+        k = int(kept.value)
+        return k, [[o[:k] for o in per] for per in outs]
 
     def fetch_multi(self, group: TrioGroup, flags: list, audit: list, online_blinds=None) -> TrioRecords:
         """src/engine.py:220-270."""
@@ -459,12 +464,13 @@ class Trio:
                           [(group.ids, group.id_width)] + [(group.attrs[a], w) for a, w in zip(names, widths)])
         sh = self.shuffle(rows, row_width, online_blinds)
         del rows
-        keep, k = self._open_keep(sh, group.count, "fetch", audit)
-        ids = [self._extract(m, keep, k, 1, group.id_width) for m in sh]
-        attrs, off = {}, 1 + group.id_width
-        for a, w in zip(names, widths):
-            attrs[a] = [self._extract(m, keep, k, off, w) for m in sh]
+        fields, off = [(1, group.id_width)], 1 + group.id_width
+        for w in widths:
+            fields.append((off, w))
             off += w
+        k, got = self._open_keep(sh, group.count, "fetch", audit, fields)
+        ids = got[0]
+        attrs = dict(zip(names, got[1:]))
         return TrioRecords(group.parent_slot, group.parent_record, k, group.id_width, ids, attrs,
                            dict(zip(names, widths)))
 
@@ -507,10 +513,10 @@ class Trio:
         fetched = self.reshare_matrix(adds, x_ne)
         rows = PackedRows(l_max, 1 + x_ne, [self._parity_rows(f, w_ne) for f in fetched], [(fetched, x_ne)])
         sh = self.shuffle(rows, 1 + x_ne)
-        keep, k = self._open_keep(sh, l_max, "access", audit)
+        k, got = self._open_keep(sh, l_max, "access", audit, [(1, x_ne)])
         if k == 0:
             return empty()
-        ids = [self._extract(m, keep, k, 1, x_ne) for m in sh]
+        ids = got[0]
         attrs = {}
         for a in needed:
             va = [gs.types[child_type].attrs[a][0] for gs in gshares]
