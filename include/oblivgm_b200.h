@@ -149,6 +149,13 @@ int ogm_zero_share_trio(const uint8_t* k1, const uint8_t* k2, const uint8_t* k3,
                         int64_t nbits, const uint32_t* const* xor_into, uint32_t* const* out,
                         void* stream);
 
+/* The matrix re-share of src/engine.py:83-92 for the three parties: the
+ * zero share of rows*words*32 bits XORed into xor_into[q], every row's tail
+ * (bits >= width of each `words`-word row) masked after the XOR. */
+int ogm_zero_share_trio_rows(const uint8_t* k1, const uint8_t* k2, const uint8_t* k3, uint64_t counter, int64_t rows,
+                             int64_t words, int64_t width, const uint32_t* const* xor_into, uint32_t* const* out,
+                             void* stream);
+
 /* The same for words [w0, w0 + nwords) of the nbits-bit vector (w0 % 4 == 0),
  * written to out[q][0 .. nwords): one rank's slice of a row-sharded secEval
  * (SURVEY 8(e)); the tail mask applies only to the vector's last word. */

@@ -223,7 +223,8 @@ struct Zs3Args {
 template <class TAB = AesTab>
 __global__ void __launch_bounds__(kAesThreads) zero_share3_kernel(const Zs3Args a, uint32_t label_be,
                                                                    uint64_t counter, int64_t nwords,
-                                                                   int64_t nbits, int64_t w0, int64_t nloc) {
+                                                                   int64_t nbits, int64_t w0, int64_t nloc,
+                                                                   int64_t row_words, uint32_t row_tail) {
     // words [w0, w0 + nloc) of the nwords-word stream (w0 % 4 == 0: whole
     // CTR blocks), written to out[q][0 .. nloc)
     extern __shared__ __align__(128) uint8_t smem_raw[];
@@ -249,6 +250,8 @@ __global__ void __launch_bounds__(kAesThreads) zero_share3_kernel(const Zs3Args 
                 uint32_t v = zw[j];
                 if (a.xin[q]) v ^= a.xin[q][o];
                 if (w0 + o == nwords - 1 && (nbits & 31)) v &= (1u << (nbits & 31)) - 1u;
+                // matrix re-share (src/engine.py:86-89): every row's tail masked after the XOR
+                if (row_words && (w0 + o) % row_words == row_words - 1) v &= row_tail;
                 a.out[q][o] = v;
             }
         }
@@ -878,7 +881,8 @@ int ogm_masked_parity(int64_t rows, int64_t words, int64_t pitch, int ncomp, con
 
 static int zero_share_trio_impl(const uint8_t* k1, const uint8_t* k2, const uint8_t* k3, uint64_t counter,
                                 int64_t nbits, int64_t w0, int64_t nloc, const uint32_t* const* xor_into,
-                                uint32_t* const* out, void* stream) {
+                                uint32_t* const* out, void* stream, int64_t row_words = 0,
+                                uint32_t row_tail = 0xffffffffu) {
     using namespace ogm;
     OGM_CHECK_ARG(k1 && k2 && k3 && out, OGM_ERR_ARG, "zero-share keys and outputs are required");
     OGM_CHECK_ARG(nbits >= 0, OGM_ERR_ARG, "negative bit count");
@@ -898,7 +902,7 @@ static int zero_share_trio_impl(const uint8_t* k1, const uint8_t* k2, const uint
         a.out[q] = out[q];
     }
     aes_launch(zero_share3_kernel<AesTab>, zero_share3_kernel<AesTabSmall>, (nloc + 3) / 4, kAesThreads,
-               as_stream(stream), a, label_be(kZshr), counter, nwords, nbits, w0, nloc);
+               as_stream(stream), a, label_be(kZshr), counter, nwords, nbits, w0, nloc, row_words, row_tail);
     OGM_LAUNCH_CHECK();
     return OGM_OK;
 }
@@ -906,6 +910,16 @@ static int zero_share_trio_impl(const uint8_t* k1, const uint8_t* k2, const uint
 int ogm_zero_share_trio(const uint8_t* k1, const uint8_t* k2, const uint8_t* k3, uint64_t counter,
                         int64_t nbits, const uint32_t* const* xor_into, uint32_t* const* out, void* stream) {
     return zero_share_trio_impl(k1, k2, k3, counter, nbits, 0, (nbits + 31) / 32, xor_into, out, stream);
+}
+
+int ogm_zero_share_trio_rows(const uint8_t* k1, const uint8_t* k2, const uint8_t* k3, uint64_t counter, int64_t rows,
+                             int64_t words, int64_t width, const uint32_t* const* xor_into, uint32_t* const* out,
+                             void* stream) {
+    OGM_CHECK_ARG(rows >= 0 && words >= 0 && width >= 0 && (width + 31) / 32 <= words, OGM_ERR_ARG,
+                  "bad re-share matrix shape");
+    const uint32_t tail = (width & 31) ? ((1u << (width & 31)) - 1u) : 0xffffffffu;
+    return zero_share_trio_impl(k1, k2, k3, counter, rows * words * 32, 0, rows * words, xor_into, out, stream,
+                                words, tail);
 }
 
 int ogm_zero_share_trio_slice(const uint8_t* k1, const uint8_t* k2, const uint8_t* k3, uint64_t counter,

@@ -156,11 +156,8 @@ class Trio:
         flat = [a.reshape(-1) for a in adds]
         outs = [torch.empty_like(f) for f in flat]
         if rows * w:
-            _lib.call("ogm_zero_share_trio", self.k[0], self.k[1], self.k[2], self.counter, rows * w * 32, A(flat),
-                      A(outs), _lib.stream_ptr())
-            if width % 32:
-                for o in outs:
-                    _lib.call("ogm_mask_row_tails", _lib.ptr(o), rows, w, width, _lib.stream_ptr())
+            _lib.call("ogm_zero_share_trio_rows", self.k[0], self.k[1], self.k[2], self.counter, rows, w, width,
+                      A(flat), A(outs), _lib.stream_ptr())
         self.counter += 1
         outs = [o.reshape(rows, w) for o in outs]
         return [outs[2], outs[0], outs[1]]
