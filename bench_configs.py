@@ -32,7 +32,7 @@ from paper_2209_03526_b200.engine import CandidateGroup, EngineConfig, open_resu
 from paper_2209_03526_b200.graphs import device_trio, encrypt_graph  # noqa: E402
 from paper_2209_03526_b200.net import local_runtimes, make_session_configs, run_trio  # noqa: E402
 from paper_2209_03526_b200.query import gen_token, load_query  # noqa: E402
-from paper_2209_03526_b200.shuffle import ShuffleOffline, blind_table, gather  # noqa: E402
+from paper_2209_03526_b200.shuffle import ShuffleOffline, blind_table, gather, shuffle_online_fused  # noqa: E402
 from paper_2209_03526_b200.prf import seeded_permutation_device  # noqa: E402
 from paper_2209_03526_b200 import workloads  # noqa: E402
 
@@ -446,8 +446,13 @@ def run_c5(args):
         torch.cuda.synchronize()
         t_off = time.perf_counter() - t0
 
+        fused = off[0].plan_x1 is None and rows * 16 <= (32 << 20)  # measured: fused wins up to 2^21 rows
+
         def online(pre: bool, marks=None):
             # the four party-local steps of src/shuffle.py:106-143 in protocol order
+            if pre and fused and marks is None:
+                shuffle_online_fused(off, comps[0], comps[1], comps[2], x1, y1, c1, r3)
+                return
             if pre:
                 off[0].step_x1(comps[0], comps[1], x1)
                 marks and marks[1].record()
@@ -485,16 +490,20 @@ def run_c5(args):
                          + (", extrapolated linearly" if srows < rows else ""),
                "r3_equal": bool(np.array_equal(o_r3, r3.cpu().numpy().view(np.uint32))) if srows == rows else None}
         del perm, plain
+        # tables below ~4x L2: flush L2 (write 512 MB) between timed iterations, outside the events
+        flush = torch.empty((512 << 20,), dtype=torch.uint8, device=dev) if rows * 16 * 4 < (512 << 20) else None
         for pre in (True, False):
             for _ in range(args.warmup):
                 online(pre)
-            ev = events(args.steps + 1)
-            ev[0].record()
+            ev = events(2 * args.steps)
             for s in range(args.steps):
+                if flush is not None:
+                    flush.zero_()
+                ev[2 * s].record()
                 online(pre)
-                ev[s + 1].record()
+                ev[2 * s + 1].record()
             torch.cuda.synchronize()
-            ms = statistics.median(ev[i].elapsed_time(ev[i + 1]) for i in range(args.steps))
+            ms = statistics.median(ev[2 * i].elapsed_time(ev[2 * i + 1]) for i in range(args.steps))
             step_ms = None
             if pre:
                 marks = events(5)
@@ -512,8 +521,10 @@ def run_c5(args):
                 # 10 row moves + 6 index reads (2 of them dependent/random); blinds by AES
                 nbytes = rows * (10 * 16 + 6 * 4)
             emit({"config": f"C5 shuffle 2^{lg} rows x 128-bit", "metric": "shuffle_online_GBps",
+                  "l2": "flushed between timed iterations" if flush is not None else "tables larger than L2",
                   "blinds": ("offline (ShuffleOffline: composed perms + permuted combined blinds"
-                             + (", planned two-pass gathers)" if off[1].plan_y1 is not None else ", direct gathers)"))
+                             + (", planned two-pass gathers)" if off[1].plan_y1 is not None
+                                else ", one cooperative launch)" if fused else ", direct gathers)"))
                   if pre
                   else "AES-CTR on the fly, nested permutation lookups",
                   "value": nbytes / (ms * 1e-3) / 1e9, "unit": "GB/s", "ms": ms,

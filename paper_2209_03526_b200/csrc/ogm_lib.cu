@@ -2,6 +2,7 @@
 //
 // Single translation unit (the kernels live in the included .cuh files) so
 // the __constant__ AES tables need no relocatable device code.
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 #include <stdarg.h>
 #include <stdint.h>

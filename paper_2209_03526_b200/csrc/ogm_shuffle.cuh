@@ -680,6 +680,42 @@ static int seeded_permutation_impl(const uint8_t* key, const uint8_t* label, uin
 
 }  // namespace ogm
 
+// ---------------------------------------------------------------------------
+// The online phase of a whole 3-party shuffle (offline material prepared:
+// composed permutations, permuted combined blinds) in ONE cooperative launch
+// for tables that sit in L2 (<= 64 MB): the four party steps of
+// src/shuffle.py:106-143 as three grid-synchronised phases
+//   x1 = (a ^ b)[k1] ^ U,  y1 = c[pi12] ^ V     (P1, P2: independent)
+//   c1 = x1[pi23] ^ W                           (P2, after x1 arrives)
+//   R3 = y1[k3] ^ c1 ^ Z                        (P3, after y1, c1 arrive)
+// Every message is still written to memory; only the launch boundaries go.
+// 16-byte rows (pitch 4 words).
+// ---------------------------------------------------------------------------
+struct Shuffle4Args {
+    const int32_t *k1, *pi12, *pi23, *k3;
+    const uint4 *a, *b, *c, *U, *V, *W, *Z;
+    uint4 *x1, *y1, *c1, *r3;
+    int64_t rows;
+};
+
+__global__ void __launch_bounds__(256) shuffle_online_coop_kernel(const Shuffle4Args p) {
+    namespace cg = cooperative_groups;
+    cg::grid_group grid = cg::this_grid();
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    const int64_t t0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    for (int64_t i = t0; i < p.rows; i += stride) {
+        const int64_t k = __ldg(p.k1 + i), j = __ldg(p.pi12 + i);
+        p.x1[i] = ogm::xor4(ogm::xor4(__ldcg(p.a + k), __ldcg(p.b + k)), __ldcs(p.U + i));
+        p.y1[i] = ogm::xor4(__ldcg(p.c + j), __ldcs(p.V + i));
+    }
+    grid.sync();
+    for (int64_t i = t0; i < p.rows; i += stride)
+        p.c1[i] = ogm::xor4(__ldcg(p.x1 + __ldg(p.pi23 + i)), __ldcs(p.W + i));
+    grid.sync();
+    for (int64_t i = t0; i < p.rows; i += stride)
+        p.r3[i] = ogm::xor4(ogm::xor4(__ldcg(p.y1 + __ldg(p.k3 + i)), __ldcg(p.c1 + i)), __ldcs(p.Z + i));
+}
+
 extern "C" {
 
 int64_t ogm_perm_workspace_bytes(int64_t n) { return ogm::perm_ws_bytes(n < 0 ? 0 : n); }
@@ -1015,6 +1051,32 @@ int ogm_trio_shuffle(const uint8_t* s12, const uint8_t* s23, const uint8_t* s31,
     OGM_TRY(ogm_shuffle_gather(rows, W, width_bits, nullptr, k3, y1, nullptr, c1, nullptr, nullptr, 0, nullptr, nullptr,
                                nullptr, 0, nullptr, nullptr, nullptr, 0, z, 0, P, r3, stream));
 #undef OGM_TRY
+    return OGM_OK;
+}
+
+int ogm_shuffle_online_fused(int64_t rows, const int32_t* k1, const int32_t* pi12, const int32_t* pi23,
+                             const int32_t* k3, const uint32_t* a, const uint32_t* b, const uint32_t* c,
+                             const uint32_t* U, const uint32_t* V, const uint32_t* W, const uint32_t* Z, uint32_t* x1,
+                             uint32_t* y1, uint32_t* c1, uint32_t* r3, void* stream) {
+    using namespace ogm;
+    OGM_CHECK_ARG(rows >= 0 && rows < ((int64_t)1 << 31), OGM_ERR_ARG, "rows out of range");
+    const void* ptrs[] = {a, b, c, U, V, W, Z, x1, y1, c1, r3};
+    for (const void* q : ptrs)
+        OGM_CHECK_ARG(q && (((uintptr_t)q) & 15) == 0, OGM_ERR_ARG, "16-byte aligned tables are required");
+    OGM_CHECK_ARG(k1 && pi12 && pi23 && k3, OGM_ERR_ARG, "permutations are required");
+    if (rows == 0) return OGM_OK;
+    OGM_ENSURE_INIT();
+    Shuffle4Args p{k1, pi12, pi23, k3, (const uint4*)a, (const uint4*)b, (const uint4*)c, (const uint4*)U,
+                   (const uint4*)V, (const uint4*)W, (const uint4*)Z, (uint4*)x1, (uint4*)y1, (uint4*)c1,
+                   (uint4*)r3, rows};
+    int per_sm = 0;
+    OGM_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, shuffle_online_coop_kernel, 256, 0));
+    int64_t g = (int64_t)sm_count() * std::max(per_sm, 1);
+    const int64_t need = (rows + 255) / 256;
+    if (g > need) g = need;
+    void* args[] = {&p};
+    OGM_CUDA_TRY(cudaLaunchCooperativeKernel((const void*)shuffle_online_coop_kernel, dim3((unsigned)g), dim3(256),
+                                             args, 0, as_stream(stream)));
     return OGM_OK;
 }
 

@@ -480,3 +480,28 @@ def test_planned_gather_pitched_rows(rows, words, pitch):
     plan = GatherPlan(idx, pitch, window_bytes=32 << 10, tile_rows=333)
     got = plan.run(torch.empty_like(M), m1=M, r=R)
     assert torch.equal(got[:, :words], want[:, :words])
+
+
+@pytest.mark.parametrize("rows", [1, 999, 1 << 16, 300_001])
+def test_shuffle_online_fused_equals_party_steps(rows):
+    """The one-launch online shuffle (ogm_shuffle_online_fused) writes the same
+    messages x1, y1, c1 and the same new component R3 as the four
+    ShuffleOffline party steps."""
+    from paper_2209_03526_b200 import workloads
+    from paper_2209_03526_b200.net import make_session_configs
+    from paper_2209_03526_b200.shuffle import ShuffleOffline, shuffle_online_fused
+
+    cfg = make_session_configs(b"\x3c" * 16)
+    comps = [workloads.device_random_words(rows * 4, 5, 80 + c).reshape(rows, 4) for c in range(3)]
+    off = [ShuffleOffline(p + 1, cfg[p].seed_with_next, cfg[p].seed_with_prev, 2, rows, 128, plan=False)
+           for p in range(3)]
+    e = lambda: torch.empty_like(comps[0])  # noqa: E731
+    want = [e() for _ in range(4)]
+    off[0].step_x1(comps[0], comps[1], want[0])
+    off[1].step_y1(comps[2], want[1])
+    off[1].step_c1(want[0], want[2])
+    off[2].step_r3(want[1], want[2], want[3])
+    got = [e() for _ in range(4)]
+    shuffle_online_fused(off, comps[0], comps[1], comps[2], *got)
+    for g_, w_ in zip(got, want):
+        assert torch.equal(g_, w_)
