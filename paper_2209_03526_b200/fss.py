@@ -111,6 +111,28 @@ def is_comparison(key) -> bool:
 # ---------------------------------------------------------------------------
 
 
+def pack_keys(keys: list, bits: int) -> np.ndarray:
+    """Host image of a KeyBatch, one buffer for one H2D copy:
+    root (n,16) | seed_cw (bits,n,16) | ctrl (3,n) u32 bit-planes over levels
+    | flags (n,) u8 (bit0 root_t, bit1 final_cw, bit2 add_const).  Every
+    offset is a multiple of 16 bytes except the trailing flags."""
+    n = len(keys)
+    a, b = 16 * n, 16 * n * (1 + bits)
+    buf = np.empty(b + 12 * n + n, np.uint8)
+    buf[:a] = np.frombuffer(b"".join([k.root_seed for k in keys]), np.uint8)
+    scw = np.frombuffer(b"".join([np.ascontiguousarray(k.seed_cw, np.uint64).tobytes() for k in keys]),
+                        np.uint8).reshape(n, bits, 16)
+    buf[a:b].reshape(bits, n, 16)[...] = scw.transpose(1, 0, 2)
+    cc = np.frombuffer(b"".join([np.asarray(k.ctrl_cw, np.uint8).tobytes() for k in keys]),
+                       np.uint8).reshape(n, bits)
+    planes = (cc[None, :, :] >> np.arange(3, dtype=np.uint8)[:, None, None]) & 1   # (3, n, bits)
+    packed = np.zeros((3, n, 4), np.uint8)
+    packed[:, :, :(bits + 7) // 8] = np.packbits(planes, axis=2, bitorder="little")
+    buf[b:b + 12 * n] = packed.reshape(-1)
+    buf[b + 12 * n:] = [(k.root_t & 1) | ((k.final_cw & 1) << 1) | ((k.add_const & 1) << 2) for k in keys]
+    return buf
+
+
 class KeyBatch:
     """K tree keys of one kind and depth in the device SoA layout.
 
@@ -150,23 +172,8 @@ class KeyBatch:
         if not 1 <= bits <= MAX_DEVICE_BITS:
             raise DomainError(f"domain_bits {bits} outside 1..{MAX_DEVICE_BITS}")
         n = len(keys)
-        root = np.frombuffer(b"".join(k.root_seed for k in keys), np.uint8).reshape(n, 16)
-        scw = np.stack([np.ascontiguousarray(k.seed_cw, np.uint64).view(np.uint8).reshape(bits, 16)
-                        for k in keys], axis=1)
-        cc = np.stack([np.asarray(k.ctrl_cw, np.uint8) for k in keys]).astype(np.uint32)  # (n, bits)
-        sh = (np.uint32(1) << np.arange(bits, dtype=np.uint32))[None, :]
-        ctrl = np.stack([((cc >> j) & 1) * sh for j in range(3)]).sum(axis=2, dtype=np.uint64)
-        ctrl = ctrl.astype(np.uint32)
-        flags = np.array([(k.root_t & 1) | ((k.final_cw & 1) << 1) | ((k.add_const & 1) << 2)
-                          for k in keys], np.uint8)
-        # one host buffer, one H2D copy: root | seed_cw | ctrl | flags (every
-        # offset a multiple of 16 bytes except the trailing flags)
+        buf = pack_keys(keys, bits)
         a, b = 16 * n, 16 * n * (1 + bits)
-        buf = np.empty(b + 12 * n + n, np.uint8)
-        buf[:a] = root.reshape(-1)
-        buf[a:b] = np.ascontiguousarray(scw).reshape(-1)
-        buf[b:b + 12 * n] = ctrl.view(np.uint8).reshape(-1)
-        buf[b + 12 * n:] = flags
         d = torch.from_numpy(buf).to(torch.device(device))
         return cls(_lib.KIND_DCF if comp else _lib.KIND_DPF, bits, d[:a].view(n, 16), d[a:b].view(bits, n, 16),
                    d[b:b + 12 * n].view(torch.int32).view(3, n), d[b + 12 * n:])
