@@ -479,13 +479,15 @@ class Trio:
                         torch.zeros((w,), dtype=torch.int32, device=self.dev))
         return cache[w]
 
-    def _parity_rows(self, mat, w) -> torch.Tensor:
-        rows = mat.shape[0]
-        out = self._empty(words_for(rows))
+    def _parity_rows(self, mats: list, w) -> list:
+        """Row parities of the three components in one trio launch: party q's
+        parity(A_q & 1...1 ^ B_q & 0) is the parity of component q's row."""
+        rows = mats[0].shape[0]
+        outs = [self._empty(words_for(rows)) for _ in range(3)]
         ones, zeros = self._consts(w)
-        _lib.call("ogm_masked_parity", rows, w, mat.stride(0), 2, A([mat, mat]), 1, _lib.int_array([0]),
-                  _lib.int_array([1]), 1, A([ones, zeros]), A([out]), _lib.stream_ptr())
-        return out
+        _lib.call("ogm_masked_parity", rows, w, mats[0].stride(0), 3, A(mats), 3, _lib.int_array([0, 1, 2]),
+                  _lib.int_array([1, 2, 0]), 1, A([ones, zeros] * 3), A(outs), _lib.stream_ptr())
+        return outs
 
     def access(self, rec: TrioRecords, i: int, parent_type: str, child_type: str, needed: list, gshares: list,
                provenance: tuple, audit: list) -> TrioGroup:
@@ -508,7 +510,7 @@ class Trio:
         sel = [c[i] for c in rec.ids]
         adds = [a.reshape(l_max, w_ne) for a in self._fold(sel, lists, x_ne)]
         fetched = self.reshare_matrix(adds, x_ne)
-        rows = PackedRows(l_max, 1 + x_ne, [self._parity_rows(f, w_ne) for f in fetched], [(fetched, x_ne)])
+        rows = PackedRows(l_max, 1 + x_ne, self._parity_rows(fetched, w_ne), [(fetched, x_ne)])
         sh = self.shuffle(rows, 1 + x_ne)
         k, got = self._open_keep(sh, l_max, "access", audit, [(1, x_ne)])
         if k == 0:
