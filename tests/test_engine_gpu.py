@@ -505,3 +505,35 @@ def test_shuffle_online_fused_equals_party_steps(rows):
     shuffle_online_fused(off, comps[0], comps[1], comps[2], *got)
     for g_, w_ in zip(got, want):
         assert torch.equal(g_, w_)
+
+
+def test_c5_planned_shuffle_matches_oracle_at_scale():
+    """C5 at 2^23 rows x 128 bits (128 MB tables: the planned two-pass gathers
+    with source-order blinds and the L2-window pass): the four party steps'
+    new components equal the oracle's numpy restatement of
+    src/shuffle.py:80-144 bit for bit."""
+    import oracle
+    from paper_2209_03526_b200 import workloads
+    from paper_2209_03526_b200.net import make_session_configs
+    from paper_2209_03526_b200.shuffle import ShuffleOffline
+
+    rows = 1 << 23
+    cfg = make_session_configs(b"\x5c" * 16)
+    s12, s23, s31 = cfg[0].seed_with_next, cfg[1].seed_with_next, cfg[2].seed_with_next
+    comps = [workloads.device_random_words(rows * 4, 9, 90 + c).reshape(rows, 4) for c in range(3)]
+    off = [ShuffleOffline(p + 1, cfg[p].seed_with_next, cfg[p].seed_with_prev, 4, rows, 128) for p in range(3)]
+    assert off[0].plan_x1 is not None and off[2].plan_r3 is not None
+    e = lambda: torch.empty_like(comps[0])  # noqa: E731
+    x1, y1, c1, r3 = e(), e(), e(), e()
+    off[0].step_x1(comps[0], comps[1], x1)
+    off[1].step_y1(comps[2], y1)
+    off[1].step_c1(x1, c1)
+    off[2].step_r3(y1, c1, r3)
+    host = [c.cpu().numpy().view(np.uint32) for c in comps]
+    (o1, o2, o3), (m_x1, m_y1, m_c1, _) = oracle.shuffle_trio(s12, s23, s31, 4, host, 128)
+    assert np.array_equal(x1.cpu().numpy().view(np.uint32), m_x1)
+    assert np.array_equal(y1.cpu().numpy().view(np.uint32), m_y1)
+    assert np.array_equal(c1.cpu().numpy().view(np.uint32), m_c1)
+    assert np.array_equal(r3.cpu().numpy().view(np.uint32), o3)
+    assert np.array_equal(off[0].out_a.cpu().numpy().view(np.uint32), o1)
+    assert np.array_equal(off[0].out_b.cpu().numpy().view(np.uint32), o2)
