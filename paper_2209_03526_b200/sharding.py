@@ -18,6 +18,7 @@ from __future__ import annotations
 
 from dataclasses import dataclass
 
+import numpy as np
 import torch
 
 from . import _lib, fss
@@ -110,6 +111,92 @@ def sharded_sec_eval_trio(comps, words: int, plan: ShardPlan, rank: int, inds, z
                       counters[ps], plan.rows, w0, w1 - w0, A(adds), A(adds), _lib.stream_ptr())
         result.append([all_gather_bits(add, plan, group) if plan.world > 1 else add for add in adds])
     return result
+
+
+# ---------------------------------------------------------------------------
+# Sharded folds (Case I fetch, sec_access posting fold) and the
+# sharded open + compaction
+# ---------------------------------------------------------------------------
+#
+# A fold XOR-reduces over candidate rows, so a row shard folds its own rows
+# and one exchange combines the partials.  NCCL has no XOR reduction: the
+# exchange is an all-gather of the per-rank partials followed by a local XOR
+# fold -- w(width) words per rank per party, tiny next to the fold's read.
+
+
+def xor_allreduce(t: torch.Tensor, group=None) -> torch.Tensor:
+    """XOR of `t` over all ranks (same shape everywhere): all-gather + fold."""
+    import torch.distributed as dist
+    world = dist.get_world_size(group)
+    flat = t.reshape(-1).contiguous()
+    out = torch.empty((world * flat.numel(),), dtype=flat.dtype, device=flat.device)
+    dist.all_gather_into_tensor(out, flat, group=group)
+    out = out.view(world, flat.numel())
+    acc = out[0].clone()
+    for r in range(1, world):
+        acc ^= out[r]
+    return acc.reshape(t.shape)
+
+
+def _fold_local(rows: int, words: int, mats: list, flags: list) -> list:
+    """The three parties' partial folds of this rank's rows (one trio launch)."""
+    outs = [torch.empty((max(words, 1),), dtype=torch.int32, device=mats[0].device)[:words] for _ in range(3)]
+    A = _lib.ptr_array
+    _lib.call("ogm_select_fold", rows, words, mats[0].stride(0) if rows else words, 3, A(mats),
+              A([mats[(q + 1) % 3] for q in range(3)]), A(flags), A([flags[(q + 1) % 3] for q in range(3)]),
+              A(outs), _lib.stream_ptr())
+    return outs
+
+
+def sharded_fold_trio(mats_local: list, flags_full: list, plan: ShardPlan, rank: int, group=None) -> list:
+    """src/engine.py:95-102 (_select_one_additive) over row-sharded matrices
+    for the three co-resident parties: mats_local[c] holds this rank's rows
+    [lo, hi) of component c (rows x pitch), flags_full[c] the full selection
+    bit vector of component c (replicated: C/8 bytes).  Returns every
+    party's additive fold, identical on all ranks to the unsharded fold."""
+    lo, hi = plan.bounds(rank)
+    if lo % 32:
+        raise ValueError("fold shards must start on a 32-row word boundary")
+    words = mats_local[0].shape[1] if mats_local[0].dim() == 2 else 0
+    w0 = lo // 32
+    flags = [f[w0:] for f in flags_full]  # bit 0 of word 0 = this shard's first row
+    parts = _fold_local(hi - lo, words, mats_local, flags)
+    if plan.world == 1:
+        return parts
+    return [xor_allreduce(p_, group) for p_ in parts]
+
+
+def _compact(bits: torch.Tensor, n: int, k: int) -> torch.Tensor:
+    """Indices of the set bits among the first n (device compaction, order kept)."""
+    idx = torch.empty((max(n, 1),), dtype=torch.int32, device=bits.device)
+    cnt = torch.empty((1,), dtype=torch.int64, device=bits.device)
+    nb = int(_lib.load().ogm_compact_workspace_bytes(n))
+    ws = torch.empty((nb,), dtype=torch.uint8, device=bits.device)
+    _lib.call("ogm_compact_bits", n, _lib.ptr(bits), _lib.ptr(idx), _lib.ptr(cnt), _lib.ptr(ws), nb,
+              _lib.stream_ptr())
+    return idx[:k]
+
+
+def sharded_keep(plain_local: torch.Tensor, plan: ShardPlan, rank: int, group=None):
+    """Open + compaction over a row-sharded table (src/engine.py:243-252).
+
+    plain_local = this rank's opened flag bits (packed, rows [lo, hi)).  The
+    one exchange is the all-gather of the opened bits -- every party notes
+    the whole opened vector anyway (src/rss.py:184-206) -- so each rank
+    derives all shards' kept counts from it and the exclusive scan needs no
+    further collective.  Kept rows keep the global shuffled order: shards
+    are contiguous row ranges, so rank r's kept rows follow ranks < r.
+    Returns (full opened vector on the host, this rank's kept local rows on
+    the device, global position of its first kept row, global kept count)."""
+    lo, hi = plan.bounds(rank)
+    if any(plan.bounds(r)[0] % 32 for r in range(plan.world)):
+        raise ValueError("keep shards must start on 32-row word boundaries")
+    full = all_gather_bits(plain_local, plan, group) if plan.world > 1 else plain_local
+    host = full.cpu().numpy().view(np.uint32)
+    bits = np.unpackbits(host.view(np.uint8), bitorder="little")[: plan.rows]
+    counts = [int(bits[a:b].sum()) for a, b in (plan.bounds(r) for r in range(plan.world))]
+    local = _compact(plain_local, hi - lo, counts[rank])
+    return host, local, sum(counts[:rank]), sum(counts)
 
 
 # ---------------------------------------------------------------------------

@@ -537,3 +537,34 @@ def test_c5_planned_shuffle_matches_oracle_at_scale():
     assert np.array_equal(r3.cpu().numpy().view(np.uint32), o3)
     assert np.array_equal(off[0].out_a.cpu().numpy().view(np.uint32), o1)
     assert np.array_equal(off[0].out_b.cpu().numpy().view(np.uint32), o2)
+
+
+@pytest.mark.parametrize("world", [1, 2, 3, 8])
+def test_sharded_fold_and_keep_slices_on_device(world):
+    """The device side of the sharded fold and keep: each rank's
+    fold of its row slice (flag bits sliced at its first row) XORed over the
+    ranks equals the unsharded fold; each rank's device compaction of its
+    opened slice, offset by the exclusive scan, gives the global kept rows."""
+    from paper_2209_03526_b200 import sharding as sh
+
+    rows, words = 5000, 13
+    g = torch.Generator(device="cuda").manual_seed(world)
+    mats = [torch.randint(-2**31, 2**31 - 1, (rows, 16), dtype=torch.int32, device="cuda", generator=g)[:, :words]
+            for _ in range(3)]
+    flags = [torch.randint(-2**31, 2**31 - 1, ((rows + 31) // 32,), dtype=torch.int32, device="cuda", generator=g)
+             for _ in range(3)]
+    want = sh._fold_local(rows, words, mats, flags)
+    plan = sh.ShardPlan(rows, world)
+    acc = [torch.zeros_like(w) for w in want]
+    kept = []
+    bits = np.unpackbits(flags[0].cpu().numpy().view(np.uint8), bitorder="little")[:rows]
+    for r in range(world):
+        lo, hi = plan.bounds(r)
+        part = sh._fold_local(hi - lo, words, [m[lo:hi] for m in mats], [f[lo // 32:] for f in flags])
+        acc = [a ^ p_ for a, p_ in zip(acc, part)]
+        k = int(bits[lo:hi].sum())
+        local = sh._compact(flags[0][lo // 32:], hi - lo, k)
+        kept += (local.cpu().numpy() + lo).tolist()
+    for a, w_ in zip(acc, want):
+        assert torch.equal(a, w_)
+    assert kept == np.nonzero(bits)[0].tolist()

@@ -145,3 +145,82 @@ def test_exchange_gather_all_to_all(world):
         assert p.exitcode == 0
     for rank, out, want in got:
         assert np.array_equal(out, want), rank
+
+
+# ---------------------------------------------------------------------------
+# sharded folds (XOR all-reduce) and sharded open + compaction (gloo, CPU)
+# ---------------------------------------------------------------------------
+
+F_ROWS, F_WORDS = 700, 6
+
+
+def _fold_inputs():
+    rng = np.random.default_rng(77)
+    mats = [rng.integers(0, 1 << 32, (F_ROWS, F_WORDS), dtype=np.uint32) for _ in range(3)]
+    flags = [rng.integers(0, 1 << 32, -(-F_ROWS // 32), dtype=np.uint32) for _ in range(3)]
+    return mats, flags
+
+
+def _numpy_fold(rows, words, mats, flags):
+    """src/engine.py:95-102 for the three parties (test-only CPU stand-in for the kernel)."""
+    out = []
+    for q in range(3):
+        a, b = mats[q].numpy().view(np.uint32)[:rows], mats[(q + 1) % 3].numpy().view(np.uint32)[:rows]
+        fa = np.unpackbits(flags[q].numpy().view(np.uint8), bitorder="little")[:rows].astype(bool)
+        fb = np.unpackbits(flags[(q + 1) % 3].numpy().view(np.uint8), bitorder="little")[:rows].astype(bool)
+        acc = np.bitwise_xor.reduce(a[fa] ^ b[fa], axis=0) if fa.any() else np.zeros(words, np.uint32)
+        acc = acc ^ (np.bitwise_xor.reduce(a[fb], axis=0) if fb.any() else np.zeros(words, np.uint32))
+        out.append(torch.from_numpy(np.asarray(acc, np.uint32).view(np.int32).copy()))
+    return out
+
+
+def _numpy_compact(bits, n, k):
+    b = np.unpackbits(bits.numpy().view(np.uint8), bitorder="little")[:n]
+    return torch.from_numpy(np.nonzero(b)[0].astype(np.int32))[:k]
+
+
+def _fworker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import paper_2209_03526_b200.sharding as sh
+    sh._fold_local = _numpy_fold     # test-only CPU arithmetic; slicing + collectives are the product's
+    sh._compact = _numpy_compact
+    mats, flags = _fold_inputs()
+    plan = sh.ShardPlan(F_ROWS, world, align=32)
+    lo, hi = plan.bounds(rank)
+    t = lambda a: torch.from_numpy(np.ascontiguousarray(a).view(np.int32).copy())  # noqa: E731
+    folds = sh.sharded_fold_trio([t(m[lo:hi]) for m in mats], [t(f) for f in flags], plan, rank)
+    plain = np.unpackbits(flags[0].view(np.uint8), bitorder="little")[:F_ROWS]
+    local_bits = np.packbits(np.concatenate([plain[lo:hi], np.zeros((-(hi - lo)) % 32, np.uint8)]),
+                             bitorder="little").view(np.uint32)
+    host, local, first, total = sh.sharded_keep(t(local_bits), plan, rank)
+    q.put((rank, [f.numpy().view(np.uint32).copy() for f in folds], host.copy(), (local.numpy() + lo).tolist(),
+           first, total))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_sharded_fold_and_keep(world):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = 29900 + world * 13 + os.getpid() % 1000
+    procs = [ctx.Process(target=_fworker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    got = sorted((q.get(timeout=120) for _ in range(world)), key=lambda x: x[0])
+    for p in procs:
+        p.join(60)
+        assert p.exitcode == 0
+    mats, flags = _fold_inputs()
+    want = _numpy_fold(F_ROWS, F_WORDS, [torch.from_numpy(m.view(np.int32)) for m in mats],
+                       [torch.from_numpy(f.view(np.int32)) for f in flags])
+    plain = np.unpackbits(flags[0].view(np.uint8), bitorder="little")[:F_ROWS]
+    kept = np.nonzero(plain)[0].tolist()
+    order = []
+    for rank, folds, host, local, first, total in got:
+        for party in range(3):
+            assert np.array_equal(folds[party], want[party].numpy().view(np.uint32)), (world, rank, party)
+        assert np.array_equal(np.unpackbits(host.view(np.uint8), bitorder="little")[:F_ROWS], plain)
+        assert total == len(kept) and first == len(order)
+        order += local
+    assert order == kept
