@@ -11,6 +11,7 @@ timeout 900 python bench_configs.py c3 > $O/c3.jsonl 2> $O/c3.err
 timeout 900 python bench_configs.py c3p > $O/c3p.jsonl 2> $O/c3p.err
 timeout 900 python bench_configs.py c4 > $O/c4.jsonl 2> $O/c4.err
 timeout 1500 python bench_configs.py c5 --min-log 16 --max-log 28 > $O/c5.jsonl 2> $O/c5.err
+timeout 600 python bench_configs.py funcs > $O/funcs.jsonl 2> $O/funcs.err
 for f in c1 c3 c3p c4 c5; do echo "$f: $(wc -l < $O/$f.jsonl) lines; $(tail -1 $O/$f.err)"; done
 # launch list of the headline command (cold, serialised: shares only)
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file $O/bench_launches.csv \
