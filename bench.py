@@ -17,6 +17,9 @@ seeded inputs (keys generated on the device by ogm_fss_gen from seeded roots).
   2 int ops per AES table lookup of the minimal T-table walk (DCF: 31 levels x
   (160 + 133) + 133 = 9216 lookups/eval), against the measured LOP3 issue
   rate of this GPU (ogm_measure_int_peak).
+* ``paired`` -- the paired DPF run of the same shapes (BASELINE configs[1]),
+  device-timed the same way (``--kind dpf`` makes DPF the headline and DCF
+  the pair).
 * ``query_latency`` -- the metric's second half (BASELINE: "... and end-to-end
   query latency"): the C1 tiny oblivious match, tokens in -> reconstructed
   matches, via the trio fast path and via the per-party drop-in API, both
@@ -79,6 +82,7 @@ def parse():
     p.add_argument("--no-query", action="store_true", help="skip the C1 end-to-end query latency")
     p.add_argument("--query-steps", type=int, default=10)
     p.add_argument("--no-c4", action="store_true", help="skip the C4 sharded secEval leg")
+    p.add_argument("--no-paired", action="store_true", help="skip the paired DPF (or DCF) run")
     return p.parse_args()
 
 
@@ -384,6 +388,36 @@ def main():
                "ms_per_step": 1e3 * float(tt.item()) / args.steps}
         del host, hout
 
+    # the paired run of the metric's other half: DPF (equality) keys of the same
+    # shapes, device-timed the same way (BASELINE configs[1]: "A paired DPF run")
+    paired = None
+    if not args.no_paired:
+        other = not comparison
+        del b0
+        torch.cuda.empty_cache()
+        pb0, _ = fss.gen_batch(other, BITS, alphas, r0, torch.randint(0, 256, (K, 16), dtype=torch.uint8,
+                                                                       device="cuda", generator=gen))
+        for _ in range(args.warmup):
+            fss.eval_points(pb0, pts, out)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        pev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+        pev[0].record(stream)
+        for _ in range(args.steps):
+            fss.eval_points(pb0, pts, out)
+        pev[1].record(stream)
+        torch.cuda.synchronize()
+        pt = torch.tensor([pev[0].elapsed_time(pev[1])], dtype=torch.float64, device="cuda")
+        if world > 1:
+            dist.all_reduce(pt, op=dist.ReduceOp.MAX)
+        kind_o = "dcf" if other else "dpf"
+        paired = {"kind": kind_o, "value": world * K * args.steps / (float(pt.item()) * 1e-3), "unit": UNIT,
+                  "ms_per_step": float(pt.item()) / args.steps,
+                  "roofline_frac": (K * OPS_PER_LOOKUP * LOOKUPS[kind_o] / (float(pt.item()) * 1e-3 / args.steps))
+                  / peak.value}
+        b0 = pb0
+
     query = None
     if rank == 0 and not args.no_query:
         query = query_latency(args.query_steps)
@@ -415,7 +449,8 @@ def main():
                        "keys_per_gpu": K, "domain_bits": BITS, "points_per_key": 1,
                        "parallelism": f"key-sharded x{world}",
                        "l2": "inputs (9.1 GB of keys) larger than L2; no flush"},
-            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "query_latency": query, "c4_sec_eval": c4,
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "paired": paired, "query_latency": query,
+            "c4_sec_eval": c4,
             "gpu_launches": args.steps, "clocks": clk,
             "launch_ms": {"mean": statistics.mean(per_launch), "min": min(per_launch),
                           "max": max(per_launch)},
