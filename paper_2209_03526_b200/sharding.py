@@ -79,6 +79,44 @@ def all_gather_bits(local: torch.Tensor, plan: ShardPlan, group=None) -> torch.T
     return assemble(out, plan)
 
 
+def sec_eval_local_packed(comps, words: int, plan: ShardPlan, rank: int, inds, zero_keys, counters) -> torch.Tensor:
+    """This rank's share of a row-sharded secEval for all three parties: the
+    blinded packed bits of its rows for every (pass, party), as one
+    zero-padded (3*npass, words_per_rank) buffer ready for ONE all-gather
+    (at 8 GPUs the per-call collective latency, not the kernel, bounds the
+    strong scaling).  Row j = pass j // 3, party j % 3."""
+    lo, hi = plan.bounds(rank)
+    nloc = hi - lo
+    npass = len(inds)
+    nvec = 3 * npass
+    packed = torch.zeros((nvec, max(plan.words_per_rank, 1)), dtype=torch.int32, device=comps[0].device)
+    outs = [packed[j] for j in range(nvec)]
+    A = _lib.ptr_array
+    if nloc:
+        flat = [t for ps in range(npass) for q in range(3) for t in inds[ps][q]]
+        _lib.call("ogm_masked_parity", nloc, words, comps[0].stride(0), 3, A(comps), 3,
+                  _lib.int_array([0, 1, 2]), _lib.int_array([1, 2, 0]), npass, A(flat), A(outs),
+                  _lib.stream_ptr())
+    w0, w1 = plan.word_bounds(rank)
+    for ps in range(npass):
+        adds = [outs[ps * 3 + q][: w1 - w0] for q in range(3)]
+        if w1 > w0:
+            # all three parties' zero-share slices in one launch (3 AES per block, not 6)
+            _lib.call("ogm_zero_share_trio_slice", zero_keys[0][0], zero_keys[1][0], zero_keys[2][0],
+                      counters[ps], plan.rows, w0, w1 - w0, A(adds), A(adds), _lib.stream_ptr())
+    return packed
+
+
+def assemble_many(gathered: torch.Tensor, plan: ShardPlan) -> list:
+    """(world, nvec, words_per_rank) all-gathered buffers -> nvec full vectors."""
+    nvec = gathered.shape[1]
+    res = []
+    for j in range(nvec):
+        parts = [gathered[r, j, : plan.word_bounds(r)[1] - plan.word_bounds(r)[0]] for r in range(plan.world)]
+        res.append(torch.cat(parts)[: plan.total_words])
+    return res
+
+
 def sharded_sec_eval_trio(comps, words: int, plan: ShardPlan, rank: int, inds, zero_keys, counters,
                           group=None) -> list:
     """One secEval for all three parties on this rank's row shard.
@@ -90,27 +128,16 @@ def sharded_sec_eval_trio(comps, words: int, plan: ShardPlan, rank: int, inds, z
     Returns per pass the three parties' full blinded vectors (all ranks),
     i.e. the re-share messages; component j of the result is blinded_{j-1}.
     """
-    lo, hi = plan.bounds(rank)
-    nloc = hi - lo
-    npass = len(inds)
-    dev = comps[0].device
-    outs = [torch.empty((max(words_for(nloc), 1),), dtype=torch.int32, device=dev) for _ in range(3 * npass)]
-    A = _lib.ptr_array
-    if nloc:
-        flat = [t for ps in range(npass) for q in range(3) for t in inds[ps][q]]
-        _lib.call("ogm_masked_parity", nloc, words, comps[0].stride(0), 3, A(comps), 3,
-                  _lib.int_array([0, 1, 2]), _lib.int_array([1, 2, 0]), npass, A(flat), A(outs),
-                  _lib.stream_ptr())
-    w0, w1 = plan.word_bounds(rank)
-    result = []
-    for ps in range(npass):
-        adds = [outs[ps * 3 + q][: w1 - w0] for q in range(3)]
-        if w1 > w0:
-            # all three parties' zero-share slices in one launch (3 AES per block, not 6)
-            _lib.call("ogm_zero_share_trio_slice", zero_keys[0][0], zero_keys[1][0], zero_keys[2][0],
-                      counters[ps], plan.rows, w0, w1 - w0, A(adds), A(adds), _lib.stream_ptr())
-        result.append([all_gather_bits(add, plan, group) if plan.world > 1 else add for add in adds])
-    return result
+    import torch.distributed as dist
+    packed = sec_eval_local_packed(comps, words, plan, rank, inds, zero_keys, counters)
+    nvec, wpr = packed.shape
+    if plan.world == 1:
+        full = [packed[j][: plan.total_words] for j in range(nvec)]
+    else:
+        out = torch.empty((plan.world * nvec * wpr,), dtype=packed.dtype, device=packed.device)
+        dist.all_gather_into_tensor(out, packed.reshape(-1), group=group)
+        full = assemble_many(out.view(plan.world, nvec, wpr), plan)
+    return [[full[ps * 3 + q] for q in range(3)] for ps in range(nvec // 3)]
 
 
 # ---------------------------------------------------------------------------

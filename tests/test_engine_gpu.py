@@ -236,7 +236,8 @@ def test_sharded_sec_eval_slices_equal_unsharded(world):
     import oracle
     from paper_2209_03526_b200 import _lib
     from paper_2209_03526_b200.graphs import padded_device_matrix
-    from paper_2209_03526_b200.sharding import ShardPlan, assemble, pad_slice, sharded_sec_eval_trio
+    from paper_2209_03526_b200.sharding import (ShardPlan, assemble_many, sec_eval_local_packed,
+                                                sharded_sec_eval_trio)
     rows, words, counters = 5000, 70, [7, 8]
     rng = np.random.default_rng(world)
     comps_h = [rng.integers(0, 1 << 32, (rows, words), dtype=np.uint32) for _ in range(3)]
@@ -247,40 +248,21 @@ def test_sharded_sec_eval_slices_equal_unsharded(world):
     comps = [padded_device_matrix(c) for c in comps_h]
     inds = [[(dev(a), dev(b)) for a, b in ps] for ps in inds_h]
     plan = ShardPlan(rows, world)
-    chunks = [[[] for _ in range(3)] for _ in range(2)]
-    for r in range(world):
-        lo, hi = plan.bounds(r)
-        local = [c[lo:hi] for c in comps]
-        res = sharded_sec_eval_trio(local, words, ShardPlan(rows, 1) if world == 1 else plan, r, inds, zk,
-                                    counters) if world == 1 else None
-        if world > 1:
-            # same steps as sharded_sec_eval_trio minus the collective
-            nloc = hi - lo
-            outs = [torch.empty((max((nloc + 31) // 32, 1),), dtype=torch.int32, device="cuda") for _ in range(6)]
-            A = _lib.ptr_array
-            if nloc:
-                flat = [t for ps in range(2) for q in range(3) for t in inds[ps][q]]
-                _lib.call("ogm_masked_parity", nloc, words, local[0].stride(0), 3, A(local), 3,
-                          _lib.int_array([0, 1, 2]), _lib.int_array([1, 2, 0]), 2, A(flat), A(outs),
-                          _lib.stream_ptr())
-            w0, w1 = plan.word_bounds(r)
-            for ps in range(2):
-                for q in range(3):
-                    add = outs[ps * 3 + q][: w1 - w0]
-                    if w1 > w0:
-                        _lib.call("ogm_zero_share_slice", zk[q][0], zk[q][1], counters[ps], rows, w0, w1 - w0,
-                                  _lib.ptr(add), _lib.ptr(add), _lib.stream_ptr())
-                    chunks[ps][q].append(pad_slice(add, plan))
-        else:
-            for ps in range(2):
-                for q in range(3):
-                    chunks[ps][q] = [res[ps][q]]
+    if world == 1:
+        res = sharded_sec_eval_trio(comps, words, plan, 0, inds, zk, counters)
+        full = [res[j // 3][j % 3] for j in range(6)]
+    else:
+        # every rank's packed buffer, then the product's assembly of the all-gather
+        packs = []
+        for r in range(world):
+            lo, hi = plan.bounds(r)
+            packs.append(sec_eval_local_packed([c[lo:hi] for c in comps], words, plan, r, inds, zk, counters))
+        full = assemble_many(torch.stack(packs), plan)
     for ps in range(2):
         for q in range(3):
-            got = chunks[ps][q][0] if world == 1 else assemble(torch.cat(chunks[ps][q]), plan)
             want = oracle.pack_bits(oracle.masked_parity(comps_h[q], comps_h[(q + 1) % 3], *inds_h[ps][q]))
             want = want ^ oracle.zero_share(*zk[q], counters[ps], rows)
-            assert np.array_equal(host(got), want), (world, ps, q)
+            assert np.array_equal(host(full[ps * 3 + q]), want), (world, ps, q)
 
 
 @pytest.mark.parametrize("rows,width", [(1, 128), (1000, 128), (70_001, 129), (300_000, 45), (50_000, 700)])

@@ -224,3 +224,47 @@ def test_sharded_fold_and_keep(world):
         assert total == len(kept) and first == len(order)
         order += local
     assert order == kept
+
+
+def _pworker(rank, world, port, q):
+    """sharded_sec_eval_trio's exchange: one all-gather of the packed
+    (pass, party) buffer + assembly; the per-rank arithmetic is the oracle."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import paper_2209_03526_b200.sharding as sh
+    comps, inds = _inputs()
+    plan = ShardPlan(ROWS, world)
+    lo, hi = plan.bounds(rank)
+    w0, w1 = plan.word_bounds(rank)
+
+    def local_packed(*_a, **_k):
+        packed = torch.zeros((3, plan.words_per_rank), dtype=torch.int32)
+        for party in range(3):
+            bits = oracle.masked_parity(comps[party][lo:hi], comps[(party + 1) % 3][lo:hi], *inds[party])
+            local = oracle.pack_bits(bits) if hi > lo else np.zeros(0, np.uint32)
+            local = local ^ _zero_share_slice(party, w0, w1 - w0)
+            packed[party, : local.size] = torch.from_numpy(local.view(np.int32).copy())
+        return packed
+
+    sh.sec_eval_local_packed = local_packed   # test-only CPU arithmetic; exchange + assembly are the product's
+    res = sh.sharded_sec_eval_trio(None, WORDS, plan, rank, [None], None, [COUNTER])
+    q.put((rank, [t.numpy().view(np.uint32).copy() for t in res[0]]))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_sharded_sec_eval_single_all_gather(world):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = 30100 + world * 17 + os.getpid() % 1000
+    procs = [ctx.Process(target=_pworker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    got = dict(q.get(timeout=120) for _ in range(world))
+    for p in procs:
+        p.join(60)
+        assert p.exitcode == 0
+    want = _blinded_reference()
+    for r in range(world):
+        for party in range(3):
+            assert np.array_equal(got[r][party], want[party]), (world, r, party)
