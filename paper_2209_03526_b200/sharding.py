@@ -85,6 +85,8 @@ def sec_eval_local_packed(comps, words: int, plan: ShardPlan, rank: int, inds, z
     zero-padded (3*npass, words_per_rank) buffer ready for ONE all-gather
     (at 8 GPUs the per-call collective latency, not the kernel, bounds the
     strong scaling).  Row j = pass j // 3, party j % 3."""
+    if plan.per_rank % 32:
+        raise ValueError("secEval shards need row counts that are multiples of 32 (default ShardPlan alignment)")
     lo, hi = plan.bounds(rank)
     nloc = hi - lo
     npass = len(inds)
@@ -108,13 +110,13 @@ def sec_eval_local_packed(comps, words: int, plan: ShardPlan, rank: int, inds, z
 
 
 def assemble_many(gathered: torch.Tensor, plan: ShardPlan) -> list:
-    """(world, nvec, words_per_rank) all-gathered buffers -> nvec full vectors."""
-    nvec = gathered.shape[1]
-    res = []
-    for j in range(nvec):
-        parts = [gathered[r, j, : plan.word_bounds(r)[1] - plan.word_bounds(r)[0]] for r in range(plan.world)]
-        res.append(torch.cat(parts)[: plan.total_words])
-    return res
+    """(world, nvec, words_per_rank) all-gathered buffers -> nvec full vectors.
+    Every rank but the trailing ones holds exactly words_per_rank words (the
+    plan gives each per_rank rows, a multiple of 32), so all padding sits at
+    the end: one transposing copy, then a slice."""
+    world, nvec, wpr = gathered.shape
+    flat = gathered.permute(1, 0, 2).reshape(nvec, world * wpr)
+    return [flat[j, : plan.total_words] for j in range(nvec)]
 
 
 def sharded_sec_eval_trio(comps, words: int, plan: ShardPlan, rank: int, inds, zero_keys, counters,
