@@ -149,6 +149,14 @@ int ogm_zero_share_trio(const uint8_t* k1, const uint8_t* k2, const uint8_t* k3,
                         int64_t nbits, const uint32_t* const* xor_into, uint32_t* const* out,
                         void* stream);
 
+/* Two consecutive re-shares' slices (counters counter1, counter2 -- the two
+ * passes of an interval predicate) in one launch: out1 as
+ * ogm_zero_share_trio_slice at counter1, out2 at counter2. */
+int ogm_zero_share_trio_slice2(const uint8_t* k1, const uint8_t* k2, const uint8_t* k3, uint64_t counter1,
+                               uint64_t counter2, int64_t nbits, int64_t w0, int64_t nwords,
+                               const uint32_t* const* xor_into1, uint32_t* const* out1,
+                               const uint32_t* const* xor_into2, uint32_t* const* out2, void* stream);
+
 /* The matrix re-share of src/engine.py:83-92 for the three parties: the
  * zero share of rows*words*32 bits XORed into xor_into[q], every row's tail
  * (bits >= width of each `words`-word row) masked after the XOR. */

@@ -50,6 +50,7 @@ SIGNATURES = {
     "ogm_fss_full_domain": ([_int, _int, _int, _vp, _vp, _vp, _vp, _i64, _vp, _i64, _vp], _int),
     "ogm_zero_share_trio": ([_cp, _cp, _cp, _u64, _i64, _vp, _vp, _vp], _int),
     "ogm_zero_share_trio_rows": ([_cp, _cp, _cp, _u64, _i64, _i64, _i64, _vp, _vp, _vp], _int),
+    "ogm_zero_share_trio_slice2": ([_cp, _cp, _cp, _u64, _u64, _i64, _i64, _i64, _vp, _vp, _vp, _vp, _vp], _int),
     "ogm_zero_share_trio_slice": ([_cp, _cp, _cp, _u64, _i64, _i64, _i64, _vp, _vp, _vp], _int),
     "ogm_and_terms": ([_i64, _int, _vp, _vp, _vp, _vp, _vp, _vp], _int),
     "ogm_xor_words": ([_i64, _vp, _vp, _vp, _vp, _vp], _int),

@@ -216,17 +216,19 @@ __global__ void __launch_bounds__(256) masked_parity_v2_kernel(const ParityArgs 
 // ---------------------------------------------------------------------------
 struct Zs3Args {
     AesKeySched k[3];
-    const uint32_t* xin[3];
-    uint32_t* out[3];
+    const uint32_t* xin[2][3];  // per pass (two zero-share counters per launch at most)
+    uint32_t* out[2][3];
+    uint64_t counter[2];
+    int npass;
 };
 
 template <class TAB = AesTab>
 __global__ void __launch_bounds__(kAesThreads) zero_share3_kernel(const Zs3Args a, uint32_t label_be,
-                                                                   uint64_t counter, int64_t nwords,
-                                                                   int64_t nbits, int64_t w0, int64_t nloc,
-                                                                   int64_t row_words, uint32_t row_tail) {
+                                                                   int64_t nwords, int64_t nbits, int64_t w0,
+                                                                   int64_t nloc, int64_t row_words,
+                                                                   uint32_t row_tail) {
     // words [w0, w0 + nloc) of the nwords-word stream (w0 % 4 == 0: whole
-    // CTR blocks), written to out[q][0 .. nloc)
+    // CTR blocks) for each of npass counters, written to out[pass][q][0 .. nloc)
     extern __shared__ __align__(128) uint8_t smem_raw[];
     TAB::fill(smem_raw);
     __syncthreads();
@@ -234,8 +236,10 @@ __global__ void __launch_bounds__(kAesThreads) zero_share3_kernel(const Zs3Args 
     const int64_t nblk = (nloc + 3) >> 2;
     const int64_t b0 = w0 >> 2;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b < nblk; b += stride) {
-        const uint4 ctr = ctr_block(label_be, counter, (uint64_t)(b0 + b));
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < nblk * a.npass; t += stride) {
+        const int ps = t >= nblk ? 1 : 0;
+        const int64_t b = t - ps * nblk;
+        const uint4 ctr = ctr_block(label_be, a.counter[ps], (uint64_t)(b0 + b));
         uint4 f[3];
 #pragma unroll
         for (int q = 0; q < 3; q++) f[q] = aes128_enc(T, ctr, ParamKey{a.k[q].rk});
@@ -243,16 +247,18 @@ __global__ void __launch_bounds__(kAesThreads) zero_share3_kernel(const Zs3Args 
         for (int q = 0; q < 3; q++) {
             const uint4 z = xor4(f[q], f[(q + 2) % 3]);
             const uint32_t zw[4] = {z.x, z.y, z.z, z.w};
+            const uint32_t* xin = a.xin[ps][q];
+            uint32_t* out = a.out[ps][q];
 #pragma unroll
             for (int j = 0; j < 4; j++) {
                 const int64_t o = b * 4 + j;
                 if (o >= nloc) break;
                 uint32_t v = zw[j];
-                if (a.xin[q]) v ^= a.xin[q][o];
+                if (xin) v ^= xin[o];
                 if (w0 + o == nwords - 1 && (nbits & 31)) v &= (1u << (nbits & 31)) - 1u;
                 // matrix re-share (src/engine.py:86-89): every row's tail masked after the XOR
                 if (row_words && (w0 + o) % row_words == row_words - 1) v &= row_tail;
-                a.out[q][o] = v;
+                out[o] = v;
             }
         }
     }
@@ -882,9 +888,11 @@ int ogm_masked_parity(int64_t rows, int64_t words, int64_t pitch, int ncomp, con
 static int zero_share_trio_impl(const uint8_t* k1, const uint8_t* k2, const uint8_t* k3, uint64_t counter,
                                 int64_t nbits, int64_t w0, int64_t nloc, const uint32_t* const* xor_into,
                                 uint32_t* const* out, void* stream, int64_t row_words = 0,
-                                uint32_t row_tail = 0xffffffffu) {
+                                uint32_t row_tail = 0xffffffffu, int npass = 1, uint64_t counter2 = 0,
+                                const uint32_t* const* xor_into2 = nullptr, uint32_t* const* out2 = nullptr) {
     using namespace ogm;
-    OGM_CHECK_ARG(k1 && k2 && k3 && out, OGM_ERR_ARG, "zero-share keys and outputs are required");
+    OGM_CHECK_ARG(k1 && k2 && k3 && out && (npass == 1 || out2), OGM_ERR_ARG,
+                  "zero-share keys and outputs are required");
     OGM_CHECK_ARG(nbits >= 0, OGM_ERR_ARG, "negative bit count");
     const int64_t nwords = (nbits + 31) / 32;
     OGM_CHECK_ARG(w0 >= 0 && (w0 & 3) == 0 && nloc >= 0 && w0 + nloc <= nwords, OGM_ERR_ARG,
@@ -897,12 +905,19 @@ static int zero_share_trio_impl(const uint8_t* k1, const uint8_t* k2, const uint
     a.k[0] = make_sched(k1);
     a.k[1] = make_sched(k2);
     a.k[2] = make_sched(k3);
+    a.npass = npass;
+    a.counter[0] = counter;
+    a.counter[1] = counter2;
     for (int q = 0; q < 3; q++) {
-        a.xin[q] = xor_into ? xor_into[q] : nullptr;
-        a.out[q] = out[q];
+        a.xin[0][q] = xor_into ? xor_into[q] : nullptr;
+        a.out[0][q] = out[q];
+        if (npass == 2) {
+            a.xin[1][q] = xor_into2 ? xor_into2[q] : nullptr;
+            a.out[1][q] = out2[q];
+        }
     }
-    aes_launch(zero_share3_kernel<AesTab>, zero_share3_kernel<AesTabSmall>, (nloc + 3) / 4, kAesThreads,
-               as_stream(stream), a, label_be(kZshr), counter, nwords, nbits, w0, nloc, row_words, row_tail);
+    aes_launch(zero_share3_kernel<AesTab>, zero_share3_kernel<AesTabSmall>, npass * ((nloc + 3) / 4), kAesThreads,
+               as_stream(stream), a, label_be(kZshr), nwords, nbits, w0, nloc, row_words, row_tail);
     OGM_LAUNCH_CHECK();
     return OGM_OK;
 }
@@ -920,6 +935,14 @@ int ogm_zero_share_trio_rows(const uint8_t* k1, const uint8_t* k2, const uint8_t
     const uint32_t tail = (width & 31) ? ((1u << (width & 31)) - 1u) : 0xffffffffu;
     return zero_share_trio_impl(k1, k2, k3, counter, rows * words * 32, 0, rows * words, xor_into, out, stream,
                                 words, tail);
+}
+
+int ogm_zero_share_trio_slice2(const uint8_t* k1, const uint8_t* k2, const uint8_t* k3, uint64_t counter1,
+                               uint64_t counter2, int64_t nbits, int64_t w0, int64_t nwords,
+                               const uint32_t* const* xor_into1, uint32_t* const* out1,
+                               const uint32_t* const* xor_into2, uint32_t* const* out2, void* stream) {
+    return zero_share_trio_impl(k1, k2, k3, counter1, nbits, w0, nwords, xor_into1, out1, stream, 0, 0xffffffffu, 2,
+                                counter2, xor_into2, out2);
 }
 
 int ogm_zero_share_trio_slice(const uint8_t* k1, const uint8_t* k2, const uint8_t* k3, uint64_t counter,

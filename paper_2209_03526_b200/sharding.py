@@ -100,12 +100,15 @@ def sec_eval_local_packed(comps, words: int, plan: ShardPlan, rank: int, inds, z
                   _lib.int_array([0, 1, 2]), _lib.int_array([1, 2, 0]), npass, A(flat), A(outs),
                   _lib.stream_ptr())
     w0, w1 = plan.word_bounds(rank)
-    for ps in range(npass):
-        adds = [outs[ps * 3 + q][: w1 - w0] for q in range(3)]
-        if w1 > w0:
-            # all three parties' zero-share slices in one launch (3 AES per block, not 6)
-            _lib.call("ogm_zero_share_trio_slice", zero_keys[0][0], zero_keys[1][0], zero_keys[2][0],
-                      counters[ps], plan.rows, w0, w1 - w0, A(adds), A(adds), _lib.stream_ptr())
+    adds = [[outs[ps * 3 + q][: w1 - w0] for q in range(3)] for ps in range(npass)]
+    k = (zero_keys[0][0], zero_keys[1][0], zero_keys[2][0])
+    if w1 > w0 and npass == 2:
+        # both passes, all three parties: one launch (3 AES per block and pass, not 6)
+        _lib.call("ogm_zero_share_trio_slice2", *k, counters[0], counters[1], plan.rows, w0, w1 - w0,
+                  A(adds[0]), A(adds[0]), A(adds[1]), A(adds[1]), _lib.stream_ptr())
+    elif w1 > w0:
+        _lib.call("ogm_zero_share_trio_slice", *k, counters[0], plan.rows, w0, w1 - w0, A(adds[0]), A(adds[0]),
+                  _lib.stream_ptr())
     return packed
 
 

@@ -308,3 +308,22 @@ def test_c2_full_size_eval_matches_oracle():
     del ctrl, cc
     want = oracle.eval_points(key, x.astype(np.uint64))
     assert np.array_equal(e0, want)
+
+
+def test_zero_share_trio_slice2_equals_two_slices(golden):
+    """Both passes' zero-share slices in one launch == two single-counter launches."""
+    g = golden("zero_share")
+    keys = [g["keys"][i].tobytes() for i in range(3)]
+    nbits, w0, nw = 250_003, 4096, 3717
+    A = _lib.ptr_array
+    mk = lambda: [torch.empty((nw,), dtype=torch.int32, device="cuda") for _ in range(3)]  # noqa: E731
+    base = [[dev_u32(np.arange(nw, dtype=np.uint32) * np.uint32(7 + 3 * p + q)) for q in range(3)] for p in range(2)]
+    one = [mk(), mk()]
+    for p, ctr in enumerate((11, 12)):
+        _lib.call("ogm_zero_share_trio_slice", *keys, ctr, nbits, w0, nw, A(base[p]), A(one[p]), _lib.stream_ptr())
+    two = [mk(), mk()]
+    _lib.call("ogm_zero_share_trio_slice2", *keys, 11, 12, nbits, w0, nw, A(base[0]), A(two[0]), A(base[1]),
+              A(two[1]), _lib.stream_ptr())
+    for p in range(2):
+        for q in range(3):
+            assert torch.equal(one[p][q], two[p][q])
