@@ -365,8 +365,13 @@ def main():
     # end-to-end through the C ABI from pinned host buffers
     e2e = None
     if not args.no_e2e:
-        host = [t_.cpu().pin_memory() for t_ in (b0.root, b0.seed_cw, b0.ctrl, b0.flags, pts)]
-        hout = torch.zeros(((K + 31) // 32,), dtype=torch.int32).pin_memory()
+        def pinned_copy(t_):  # straight into page-locked memory (no pageable staging copy per rank)
+            h = torch.empty(t_.shape, dtype=t_.dtype, pin_memory=True)
+            h.copy_(t_)
+            return h
+
+        host = [pinned_copy(t_) for t_ in (b0.root, b0.seed_cw, b0.ctrl, b0.flags, pts)]
+        hout = torch.zeros(((K + 31) // 32,), dtype=torch.int32, pin_memory=True)
         kind = _lib.KIND_DCF if comparison else _lib.KIND_DPF
         fn = lib.ogm_fss_eval_points_host
         argv = [kind, BITS, K, *(_lib.ptr(h) for h in host), _lib.ptr(hout)]
