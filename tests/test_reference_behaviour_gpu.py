@@ -334,3 +334,41 @@ def test_open_label_guard():
     sx = rss.share(bv([0, 1, 1, 0]), rng)
     with pytest.raises(ProtocolError, match="label"):
         run_local_trio(lambda rt: rss.open_shared(rt, sx[rt.index - 1], label=rt.index))
+
+
+@pytest.mark.parametrize("text,qtext,mode", [
+    (CAMPUS, "Q u U place = Beijing\nQ p P age > 100\nQE u p\n", "or"),
+    (CAMPUS, "Q u U place = Harbin\nQ p P age >= 35\nQ p P age <= 40\nQE u p\n", "or"),
+    ("V P p1 a=1\nV P p2 a=2\nV C c1 z=10\nV C c2 z=20\nE p2 c1\nE p2 c2\n",
+     "Q root P a = 1\nQ leaf C z >= 10\nQE root leaf\n", "or"),
+    ("V P p1 a=1\nV P p2 a=2\nV C c1 z=10\nV C c2 z=20\nV C c3 z=30\nE p1 c1\nE p1 c2\nE p1 c3\nE p2 c2\n",
+     "Q root P a = 1\nQ leaf C z >= 10\nQE root leaf\n", "or"),
+    ("V P p1 a=1 b=1\nV P p2 a=1 b=5\nV P p3 a=3 b=1\nV P p4 a=3 b=5\nE p1 p2\nE p3 p4\n",
+     "Q root P a = 1\nQ root P b = 1\nQC root ANY\n", "or"),
+    ("V P p1 a=1 b=1\nV P p2 a=1 b=5\nV P p3 a=3 b=1\nV P p4 a=3 b=5\nE p1 p2\nE p3 p4\n",
+     "Q root P a = 1\nQ root P b = 1\nQC root ANY\n", "xor"),
+    ("V P p1 a=1\nV P p2 a=1\nV P p3 a=2\nV P p4 a=2\nE p1 p2\nE p3 p4\n", "Q root P a = 1\n", "or"),
+    (CAMPUS, "Q root P age = 35\n", "or"),
+])
+def test_trio_path_equals_per_party_on_edge_cases(text, qtext, mode):
+    """The same edge cases (empty root, all-dummy posting lists, ANY modes,
+    unique route) through the trio fast path: identical matches, identical
+    record shares, and identical opened vectors with identical labels."""
+    from paper_2209_03526_b200.trio import Trio
+
+    got, rts, res, schema, tokens = run_query(text, qtext, mode=mode)
+    graph = parse_graph_text(text)
+    rng = np.random.default_rng(1)
+    schema2, shares = encrypt_graph(graph, 2, rng)
+    tokens2 = gen_token(load_query(qtext, schema2), schema2, rng)
+    tr = Trio(b"\x11" * 16)
+    tres = tr.match(list(tokens2), list(device_trio(shares)), any_mode=mode)
+    views = tres.party_results()
+    assert set(open_results(views[:2], schema2)[0]) == got
+    assert [(lbl, v.to_bits().tolist()) for lbl, v in tr.opened] == \
+        [(lbl, v.to_bits().tolist()) for lbl, v in rts[0].opened]
+    for q in range(3):
+        for s_, (a_recs, b_recs) in enumerate(zip(res[q].records, views[q].records)):
+            assert len(a_recs) == len(b_recs), s_
+            for ra, rb in zip(a_recs, b_recs):
+                assert np.array_equal(np.asarray(ra.vertex_id.share_a.to_bits()), np.asarray(rb.vertex_id.share_a.to_bits()))
