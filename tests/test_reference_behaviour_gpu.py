@@ -372,3 +372,80 @@ def test_trio_path_equals_per_party_on_edge_cases(text, qtext, mode):
             assert len(a_recs) == len(b_recs), s_
             for ra, rb in zip(a_recs, b_recs):
                 assert np.array_equal(np.asarray(ra.vertex_id.share_a.to_bits()), np.asarray(rb.vertex_id.share_a.to_bits()))
+
+
+def _random_graph_text(rng):
+    n = int(rng.integers(60, 161))
+    types = "ABC"[: int(rng.integers(2, 4))]
+    doms = {(t, a): int(rng.integers(8, 65)) for t in types for a in ("a0", "a1")}
+    lines, vt = [], []
+    for i in range(n):
+        t = types[int(rng.integers(0, len(types)))]
+        vt.append(t)
+        lines.append(f"V {t} v{i} a0={int(rng.integers(0, doms[(t, 'a0')]))} a1={int(rng.integers(0, doms[(t, 'a1')]))}")
+    seen = set()
+    for _ in range(2 * n):
+        a, b = int(rng.integers(0, n)), int(rng.integers(0, n))
+        if a == b or (a, b) in seen or (b, a) in seen:
+            continue
+        seen.add((a, b))
+        lines.append(f"E v{a} v{b}")
+    return "\n".join(lines) + "\n"
+
+
+def _random_query_text(rng, schema):
+    types = sorted(schema.types)
+    m = int(rng.integers(2, 5))
+    qv = [types[int(rng.integers(0, len(types)))]]
+    edges = []
+    for i in range(1, m):
+        p = int(rng.integers(0, i))
+        opts = sorted(schema.types[qv[p]].posting_types)
+        if not opts:
+            break
+        qv.append(opts[int(rng.integers(0, len(opts)))])
+        edges.append((p, i))
+    lines = []
+    for i, t in enumerate(qv):
+        for _ in range(int(rng.integers(1, 3))):
+            a = ("a0", "a1")[int(rng.integers(0, 2))]
+            vals = sorted(schema.types[t].attrs[a].values, key=float)
+            op = ("=", "<", "<=", ">", ">=", "in")[int(rng.integers(0, 6))]
+            if op == "in":
+                lo, hi = sorted(int(rng.integers(0, len(vals))) for _ in range(2))
+                lines.append(f"Q q{i} {t} {a} in {vals[lo]} {vals[hi]}")
+            else:
+                lines.append(f"Q q{i} {t} {a} {op} {vals[int(rng.integers(0, len(vals)))]}")
+    lines += [f"QE q{p} q{c}" for p, c in edges]
+    return "\n".join(lines) + "\n"
+
+
+def test_random_corpus_equals_oracle_both_paths():
+    """Acceptance criterion 1 of the reference (tests/test_acceptance.py:26-55)
+    restated on our own seeded random graphs/queries: 30 graph/query pairs,
+    the per-party drop-in path and the trio fast path both return exactly the
+    plaintext matcher's subgraphs, and the same opened vectors."""
+    import oracle.matcher as om
+    from paper_2209_03526_b200.trio import Trio
+
+    nonempty = 0
+    for trial in range(30):
+        rng = np.random.default_rng(5000 + trial)
+        text = _random_graph_text(rng)
+        graph = parse_graph_text(text)
+        schema, shares = encrypt_graph(graph, 2, np.random.default_rng(trial))
+        qtext = _random_query_text(rng, schema)
+        query = load_query(qtext, schema)
+        tokens = gen_token(query, schema, np.random.default_rng(100 + trial))
+        want = om.oracle_match(graph, query, schema)
+        d = device_trio(shares)
+        master = bytes([trial]) * 16
+        rts = local_runtimes(make_session_configs(master))
+        res = run_trio(lambda rt: sec_match(rt, tokens[rt.index - 1], d[rt.index - 1], EngineConfig()), rts)
+        assert set(open_results(res[:2], schema)[0]) == want, (trial, qtext)
+        tr = Trio(master)
+        tres = tr.match(list(tokens), list(d))
+        assert set(open_results(tres.party_results()[:2], schema)[0]) == want, (trial, qtext)
+        assert [v.to_bits().tolist() for _, v in tr.opened] == [v.to_bits().tolist() for _, v in rts[0].opened]
+        nonempty += bool(want)
+    assert nonempty >= 5
