@@ -9,6 +9,7 @@ this runs on the GPU box).
 """
 
 import numpy as np
+import torch
 import pytest
 from hypothesis import given, settings
 from hypothesis import strategies as st
@@ -449,3 +450,53 @@ def test_random_corpus_equals_oracle_both_paths():
         assert [v.to_bits().tolist() for _, v in tr.opened] == [v.to_bits().tolist() for _, v in rts[0].opened]
         nonempty += bool(want)
     assert nonempty >= 5
+
+
+def test_fss_exhaustive_600_checks():
+    """Acceptance criterion 3 (tests/test_acceptance.py:83-113): 100 random
+    parameter sets x {DPF, <, <=, >, >=, interval}, domains 2..4096, each key
+    pair's full-domain XOR equal to the brute-force indicator."""
+    rng = np.random.default_rng(7)
+    checked = 0
+    for _ in range(100):
+        n = int(rng.integers(2, 4097))
+        alpha = int(rng.integers(0, n))
+        assert indicator(fss.dpf_gen(alpha, n, rng), n).tolist() == brute("eq", (alpha,), n).tolist()
+        checked += 1
+        for kind in ("lt", "le", "gt", "ge"):
+            a = int(rng.integers(0, n))
+            assert indicator(fss.cmp_gen(kind, a, n, rng), n).tolist() == brute(kind, (a,), n).tolist()
+            checked += 1
+        lo = int(rng.integers(0, n))
+        hi = int(rng.integers(lo, n))
+        assert indicator(fss.ic_gen(lo, hi, n, rng), n).tolist() == brute("iv", (lo, hi), n).tolist()
+        checked += 1
+    assert checked == 600
+
+
+def test_shuffle_exhaustive_sizes_both_paths():
+    """Acceptance criterion 5 (tests/test_acceptance.py:153-195): table sizes
+    1..64, the reconstructed order equals the seeded composed permutation and
+    the multiset is preserved -- through the per-party sec_shuffle and the
+    trio shuffle (one ogm_trio_shuffle call), which must agree share for share."""
+    from paper_2209_03526_b200.trio import Trio
+
+    rng = np.random.default_rng(12)
+    master = b"\x55" * 16
+    configs = make_session_configs(master)
+    s12, s23, s31 = (configs[0].seed_with_next, configs[1].seed_with_next, configs[2].seed_with_next)
+    for size in range(1, 65):
+        rows = [BitVector.random(40, rng) for _ in range(size)]
+        shares = [rss.share(r, rng) for r in rows]
+        outs = run_trio(lambda rt: sec_shuffle(rt, MatchTable.from_rows([shares[i][rt.index - 1] for i in range(size)])),
+                        local_runtimes(make_session_configs(master)))
+        got = [rss.reconstruct([outs[0].row(i), outs[1].row(i), outs[2].row(i)]) for i in range(size)]
+        perm = composed_permutation(s12, s23, s31, 0, size)
+        assert got == [rows[int(i)] for i in perm], size
+        # the trio path: components x_j = party j's share_a
+        comps = [torch.stack([torch.as_tensor(shares[i][c].share_a.words).cuda() for i in range(size)]) for c in range(3)]
+        tr = Trio(master)
+        new = tr.shuffle(comps, 40)
+        for c in range(3):
+            want_c = outs[c].share_a.cpu().numpy().view(np.uint32)
+            assert np.array_equal(new[c][:, : want_c.shape[1]].cpu().numpy().view(np.uint32), want_c), (size, c)
