@@ -348,6 +348,103 @@ int ogm_shuffle_online_fused(int64_t rows, const int32_t* k1, const int32_t* pi1
                              const uint32_t* U, const uint32_t* V, const uint32_t* W, const uint32_t* Z, uint32_t* x1,
                              uint32_t* y1, uint32_t* c1, uint32_t* r3, void* stream);
 
+/* ---- native trio executor (src/engine.py:352-417 for three co-resident
+ * parties) ------------------------------------------------------------------
+ * The whole sec_match of the trio fast path in one call: the same launches,
+ * in the same order, consuming zero-share counters, table ids and open
+ * labels exactly as trio.Trio.match does (bit-identical record shares and
+ * opened vectors).  All device buffers the executor creates are carved from
+ * `arena`; batches point into it.  Component c of every matrix is party c's
+ * share_a (src/graphs.py:382-399). */
+#define OGM_TRIO_MAX_ATTRS 8
+
+typedef struct {
+    const uint32_t* c[3]; /* three components, rows x pitch words */
+    int64_t pitch;        /* words per row in memory */
+    int64_t width;        /* logical bits per row */
+    int32_t unique;       /* attribute with unique values (Case I route) */
+} ogm_trio_mat;
+
+typedef struct {
+    int32_t child_type;
+    int64_t l_max;        /* posting slots per parent */
+    ogm_trio_mat lists;   /* X x (l_max * w(child population)) flattened rows */
+} ogm_trio_posting;
+
+typedef struct {
+    int64_t population;
+    ogm_trio_mat ids;
+    int32_t nattrs;
+    const ogm_trio_mat* attrs;        /* by attribute id (sorted attribute names) */
+    int32_t npostings;
+    const ogm_trio_posting* postings;
+} ogm_trio_type;
+
+typedef struct {
+    int32_t attr;                     /* attribute id of the slot's type */
+    int32_t npass;                    /* 1, or 2 for an interval */
+    const uint32_t* ind[2][3][2];     /* [pass][party][first/second key] full-domain indicators */
+} ogm_trio_pred;
+
+typedef struct {
+    int32_t type;
+    int32_t combiner_all;             /* 1 ALL, 0 ANY */
+    int32_t unique_route;             /* Case I fetch (src/engine.py:382-386) */
+    int32_t npreds;
+    const ogm_trio_pred* preds;
+    int32_t nneeded;                  /* attribute ids of the slot's predicates, sorted by name */
+    const int32_t* needed;
+    int32_t nchildren;
+    const int32_t* children;
+} ogm_trio_slot;
+
+typedef struct {
+    const uint8_t* zero_key[3];       /* k1, k2, k3 (own zero-share keys) */
+    const uint8_t* s12;
+    const uint8_t* s23;
+    const uint8_t* s31;
+    uint64_t counter;                 /* in: next zero-share counter; out: after the query */
+    uint64_t table_id;                /* in/out: next shuffle table id */
+    uint32_t label;                   /* in/out: last open label */
+    int32_t any_xor;                  /* ANY combiner as XOR chain (else logical or) */
+    int32_t ntypes;
+    const ogm_trio_type* types;
+    int32_t nslots;
+    const ogm_trio_slot* slots;       /* BFS order: slot 0 is the root */
+} ogm_trio_plan;
+
+typedef struct {
+    int32_t slot, parent_slot, parent_record; /* -1: root */
+    int64_t count;                    /* records in this batch */
+    int64_t id_width;
+    uint32_t* ids[3];
+    int64_t ids_pitch;
+    int32_t nattrs;
+    int32_t attr_id[OGM_TRIO_MAX_ATTRS];
+    int64_t attr_width[OGM_TRIO_MAX_ATTRS];
+    uint32_t* attrs[OGM_TRIO_MAX_ATTRS][3];
+    int64_t attr_pitch[OGM_TRIO_MAX_ATTRS];
+} ogm_trio_batch;
+
+typedef struct {
+    int32_t phase;                    /* 0 fetch, 1 access */
+    uint32_t label;
+    int64_t nbits;
+    int64_t bits_off;                 /* word offset into open_bits */
+} ogm_trio_open;
+
+typedef struct {
+    int32_t max_batches, nbatches;
+    ogm_trio_batch* batches;
+    int32_t max_opens, nopens;
+    ogm_trio_open* opens;
+    uint32_t* open_bits;              /* host words */
+    int64_t open_bits_cap, open_bits_used;
+    int64_t arena_used;               /* bytes; on OGM_ERR_NOMEM, the size that would have been needed so far */
+} ogm_trio_out;
+
+int ogm_trio_match(ogm_trio_plan* plan, ogm_trio_out* out, void* arena, int64_t arena_bytes, void* stream);
+
 /* ---- measurement -------------------------------------------------------- */
 
 /* Roofline denominator for the integer-ALU-bound kernels: issue rate of

@@ -79,13 +79,14 @@ SIGNATURES = {
     "ogm_trio_open_keep_workspace_bytes": ([_i64], _i64),
     "ogm_trio_open_keep": ([_vp, _i64, _i64, _vp, _int, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _vp], _int),
     "ogm_shuffle_online_fused": ([_i64] + [_vp] * 15 + [_vp], _int),
+    "ogm_trio_match": ([_vp, _vp, _vp, _i64, _vp], _int),
     "ogm_measure_int_peak": ([ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double)], _int),
 }
 
 # Entry points that may block on the device (host syncs); every other entry
 # point only enqueues work on the caller's stream and returns in microseconds.
 BLOCKING = {"ogm_init", "ogm_seeded_permutation", "ogm_fss_eval_points_host", "ogm_measure_int_peak",
-            "ogm_trio_open_keep", "ogm_trio_shuffle"}
+            "ogm_trio_open_keep", "ogm_trio_shuffle", "ogm_trio_match"}
 
 _lib = None
 _fast = None

@@ -17,6 +17,7 @@
 #include "ogm_fss.cuh"
 #include "ogm_engine.cuh"
 #include "ogm_shuffle.cuh"
+#include "ogm_trio.cuh"
 #include "ogm_measure.cuh"
 
 

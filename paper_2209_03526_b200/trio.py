@@ -533,10 +533,15 @@ class Trio:
         return TrioGroup(parent_slot, parent_rec, k, x_ne, ids, attrs, widths)
 
     # -- full query ----------------------------------------------------------
-    def match(self, tokens: list, gshares: list, any_mode: str = "or") -> TrioResult:
+    def match(self, tokens: list, gshares: list, any_mode: str = "or", native: bool = True) -> TrioResult:
         """src/engine.py:352-417 for the three parties at once.  gshares are the
         three per-party device shares from graphs.device_trio (component j is
-        party j's share_a)."""
+        party j's share_a).  ``native`` runs the schedule in the C++ executor
+        (ogm_trio_match: one C-ABI call); ``native=False`` issues the same
+        steps from Python (kept as the readable restatement, tested equal)."""
+        if native:
+            from .trio_native import match_native
+            return match_native(self, tokens, gshares, any_mode)
         schema = gshares[0].schema
         for t in tokens:
             if t.schema_digest != schema.digest():

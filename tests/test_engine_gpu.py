@@ -291,10 +291,12 @@ def test_shuffle_planned_path_matches_reference(golden, monkeypatch):
     test_shuffle_matches_reference(golden)
 
 
+@pytest.mark.parametrize("native", [True, False])
 @pytest.mark.parametrize("name", ["campus", "unique-chain", "conj", "rand0", "rand1", "rand2"])
-def test_trio_fast_path_matches_reference(golden, name):
+def test_trio_fast_path_matches_reference(golden, name, native):
     """The single-thread trio path (one launch per step for all three parties)
-    reproduces the reference's record shares, opened flags and subgraphs."""
+    reproduces the reference's record shares, opened flags and subgraphs --
+    both the native executor (ogm_trio_match) and the Python schedule."""
     from paper_2209_03526_b200.trio import Trio
     g = golden("match")
     rec = json.loads(str(g[f"{name}_json"]))
@@ -304,7 +306,7 @@ def test_trio_fast_path_matches_reference(golden, name):
     query = load_query(rec["query"], schema)
     tokens = gen_token(query, schema, rng)
     dshares = device_trio(shares)
-    res = Trio(bytes.fromhex(rec["master"])).match(list(tokens), list(dshares), any_mode=rec["mode"])
+    res = Trio(bytes.fromhex(rec["master"])).match(list(tokens), list(dshares), any_mode=rec["mode"], native=native)
     results = res.party_results()
     matches, _ = open_results(results[:2], schema)
     assert sorted(list(m) for m in set(matches)) == rec["matches"]
