@@ -85,19 +85,16 @@ def _mat(comps, width: int, unique: bool = False) -> Mat:
     return m
 
 
-def match_native(trio, tokens: list, gshares: list, any_mode: str = "or"):
-    from .trio import TrioRecords, TrioResult, _RecView
-    from .engine import _assemble
-
+def _type_tables(gshares: list):
+    """The schema-wide part of the plan (type tables: ids, attributes,
+    flattened posting lists of the three components), built once per set of
+    device shares and cached on the first share object."""
+    key = tuple(id(g) for g in gshares)
+    cached = getattr(gshares[0], "_native_plan", None)
+    if cached is not None and cached[0] == key:
+        return cached[1]
     schema = gshares[0].schema
-    for t in tokens:
-        if t.schema_digest != schema.digest():
-            raise ValueError("token and graph share were built for different schemas")
-    if any_mode not in ("or", "xor"):
-        raise ValueError(f"unknown ANY mode {any_mode!r}")
-    slots = tokens[0].structure["slots"]
-    keep = []  # every tensor / ctypes buffer the call reads stays alive here
-
+    keep = []
     tnames = sorted(schema.types)
     tindex = {t: i for i, t in enumerate(tnames)}
     anames = {t: sorted(schema.types[t].attrs) for t in tnames}
@@ -128,6 +125,25 @@ def match_native(trio, tokens: list, gshares: list, any_mode: str = "or"):
         types[i].postings = parr
         keep += [attrs, parr]
 
+    out = (tnames, tindex, anames, types)
+    gshares[0]._native_plan = (key, out, keep, list(gshares))
+    return out
+
+
+def match_native(trio, tokens: list, gshares: list, any_mode: str = "or"):
+    from .trio import TrioRecords, TrioResult, _RecView
+    from .engine import _assemble
+
+    schema = gshares[0].schema
+    for t in tokens:
+        if t.schema_digest != schema.digest():
+            raise ValueError("token and graph share were built for different schemas")
+    if any_mode not in ("or", "xor"):
+        raise ValueError(f"unknown ANY mode {any_mode!r}")
+    slots = tokens[0].structure["slots"]
+    keep = []  # every tensor / ctypes buffer the call reads stays alive here
+
+    tnames, tindex, anames, types = _type_tables(gshares)
     sarr = (Slot * len(slots))()
     for s, slot in enumerate(slots):
         vtype = slot["type"]
@@ -176,7 +192,7 @@ def match_native(trio, tokens: list, gshares: list, any_mode: str = "or"):
     keep.append(seeds)
     fn = _lib.load().ogm_trio_match  # releases the GIL: the call synchronises on every open
     arena_bytes = max(getattr(trio, "_arena_bytes", 0), 64 << 20)
-    max_batches, max_opens, bits_cap = 4096, 4096, 1 << 20
+    max_batches, max_opens, bits_cap = 256, 256, 1 << 15
     while True:
         plan = Plan()
         for q in range(3):
@@ -191,7 +207,7 @@ def match_native(trio, tokens: list, gshares: list, any_mode: str = "or"):
         arena = torch.empty((arena_bytes,), dtype=torch.uint8, device=trio.dev)
         batches = (Batch * max_batches)()
         opens = (Open * max_opens)()
-        bits = np.zeros(bits_cap, np.uint32)
+        bits = np.empty(bits_cap, np.uint32)
         out = Out(max_batches, 0, batches, max_opens, 0, opens, bits.ctypes.data_as(_u32p), bits_cap, 0, 0)
         rc = fn(ctypes.addressof(plan), ctypes.addressof(out), arena.data_ptr(), arena.numel(), _lib.stream_ptr())
         if rc == _lib.OGM_ERR_NOMEM:
