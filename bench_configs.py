@@ -32,7 +32,8 @@ from paper_2209_03526_b200.engine import CandidateGroup, EngineConfig, open_resu
 from paper_2209_03526_b200.graphs import device_trio, encrypt_graph  # noqa: E402
 from paper_2209_03526_b200.net import local_runtimes, make_session_configs, run_trio  # noqa: E402
 from paper_2209_03526_b200.query import gen_token, load_query  # noqa: E402
-from paper_2209_03526_b200.shuffle import ShuffleOffline, blind_table, gather, shuffle_online_fused  # noqa: E402
+from paper_2209_03526_b200.shuffle import (ShuffleOffline, blind_table, gather, shuffle_online_fused,  # noqa: E402
+                                            shuffle_online_planned)
 from paper_2209_03526_b200.prf import seeded_permutation_device  # noqa: E402
 from paper_2209_03526_b200 import workloads  # noqa: E402
 
@@ -441,17 +442,25 @@ def run_c5(args):
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         pc = {(s, 0, rows): perms[s] for s in perms}
-        off = [ShuffleOffline(p + 1, cfg[p].seed_with_next, cfg[p].seed_with_prev, 0, rows, width, perm_cache=pc)
+        # measured: one cooperative launch wins up to 2^21 rows, the chained planned gathers from 2^22
+        fused = rows * 16 <= (32 << 20)
+        off = [ShuffleOffline(p + 1, cfg[p].seed_with_next, cfg[p].seed_with_prev, 0, rows, width, perm_cache=pc,
+                              plan=not fused)
                for p in range(3)]
+        if not fused:
+            for o in off:
+                o.chain_blinds()
         torch.cuda.synchronize()
         t_off = time.perf_counter() - t0
-
-        fused = off[0].plan_x1 is None and rows * 16 <= (32 << 20)  # measured: fused wins up to 2^21 rows
 
         def online(pre: bool, marks=None):
             # the four party-local steps of src/shuffle.py:106-143 in protocol order
             if pre and fused and marks is None:
                 shuffle_online_fused(off, comps[0], comps[1], comps[2], x1, y1, c1, r3)
+                return
+            if pre and marks is None:
+                # x1, y1, c1 handed over in shared memory; their buffers are the scratch
+                shuffle_online_planned(off, comps[0], comps[1], comps[2], r3, inter=[x1, y1, c1])
                 return
             if pre:
                 off[0].step_x1(comps[0], comps[1], x1)
@@ -512,6 +521,7 @@ def run_c5(args):
                 torch.cuda.synchronize()
                 step_ms = {k: round(marks[i].elapsed_time(marks[i + 1]), 4)
                            for i, k in enumerate(("x1 (P1)", "y1 (P2)", "c1 (P2)", "R3 (P3)"))}
+                step_ms["note"] = "the per-party steps (drop-in path), one untimed-loop run, for the breakdown"
             if pre:
                 # algorithmic (protocol) bytes: x1: 2 gathers + U1 + write; y1: gather + V + write;
                 # c1: gather + W + write; R3: gather + c1 + Z + write = 14 row moves (16 B) + 4 index
@@ -523,8 +533,8 @@ def run_c5(args):
             emit({"config": f"C5 shuffle 2^{lg} rows x 128-bit", "metric": "shuffle_online_GBps",
                   "l2": "flushed between timed iterations" if flush is not None else "tables larger than L2",
                   "blinds": ("offline (ShuffleOffline: composed perms + permuted combined blinds"
-                             + (", planned two-pass gathers)" if off[1].plan_y1 is not None
-                                else ", one cooperative launch)" if fused else ", direct gathers)"))
+                             + (", planned gathers chained through shared memory)" if not fused
+                                else ", one cooperative launch)"))
                   if pre
                   else "AES-CTR on the fly, nested permutation lookups",
                   "value": nbytes / (ms * 1e-3) / 1e9, "unit": "GB/s", "ms": ms,

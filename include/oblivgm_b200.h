@@ -348,6 +348,21 @@ int ogm_shuffle_online_fused(int64_t rows, const int32_t* k1, const int32_t* pi1
                              const uint32_t* U, const uint32_t* V, const uint32_t* W, const uint32_t* Z, uint32_t* x1,
                              uint32_t* y1, uint32_t* c1, uint32_t* r3, void* stream);
 
+/* The online phase of one 3-party shuffle of 16-byte rows over planned
+ * gathers (src/shuffle.py:106-143; the four gathers' plans from
+ * ogm_gather_plan in step order x1 (k1), y1 (pi12), c1 (pi23), R3 (k3), tile
+ * 4096 rows).  Every blind is in its step's SOURCE order (U', V', W', Z').
+ * Each message is handed from sender to receiver tile by tile in shared
+ * memory: the sender's window pass feeds the receiver's partition pass in one
+ * kernel.  x1, y1, c1 (optional, may be NULL) receive copies of the
+ * messages; inter[0..2] are three table-sized scratch buffers.  r3 = the new
+ * component R3. */
+int ogm_shuffle_online_planned(int64_t rows, const int32_t* const* q2, const int32_t* const* gdst,
+                               const uint16_t* const* srow, const uint32_t* a, const uint32_t* b, const uint32_t* c,
+                               const uint32_t* u_src, const uint32_t* v_src, const uint32_t* w_src,
+                               const uint32_t* z_src, uint32_t* const* inter, uint32_t* x1, uint32_t* y1, uint32_t* c1,
+                               uint32_t* r3, void* stream);
+
 /* ---- native trio executor (src/engine.py:352-417 for three co-resident
  * parties) ------------------------------------------------------------------
  * The whole sec_match of the trio fast path in one call: the same launches,

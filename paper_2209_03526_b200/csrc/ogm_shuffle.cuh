@@ -457,12 +457,12 @@ __global__ void __launch_bounds__(512) plan_partition_kernel(const U* __restrict
 }
 
 // ---- TMA-staged pass 1 for 16-byte rows (the C5 shape) --------------------
-// One persistent CTA per SM; stage s holds a tile's rows, srow and gdst,
-// filled by cp.async.bulk on mbarrier s.  While the CTA writes tile t out,
-// tile t + grid is already in flight, so no thread ever waits on a load
-// except at the very start.  m2 (x1's a ^ b) is read per slot straight from
-// global, and so is m4 (a source-order blind): their reads stay inside the
-// tile's 64 KB of each (one DRAM page set).
+// One persistent CTA per SM; stage s holds a tile's rows (m1), srow and gdst,
+// filled by cp.async.bulk on mbarrier s, two tiles ahead.  The optional
+// terms m2 and m4 (x1's second component; a source-order blind) are read in
+// row order, coalesced, into registers one tile ahead, and XORed into the
+// staged rows before the scatter; so while tile t is written out, the loads
+// of the CTA's next tile are in flight.
 constexpr int kTmaTile = 4096;
 constexpr int kTmaThreads = 1024;
 constexpr int kTmaStageBytes = kTmaTile * (16 + 2 + 4);
@@ -500,6 +500,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) plan_partition_tma_kernel(
     const uint16_t* __restrict__ srow, const int32_t* __restrict__ gdst, int64_t rows, uint4* __restrict__ inter) {
     extern __shared__ __align__(128) unsigned char tma_smem[];
     constexpr int T = kTmaTile;
+    constexpr int Q = T / kTmaThreads;
     uint64_t* bar = reinterpret_cast<uint64_t*>(tma_smem + 2 * kTmaStageBytes);
     auto rows_of = [&](int s) { return reinterpret_cast<uint4*>(tma_smem + s * kTmaStageBytes); };
     auto srow_of = [&](int s) { return reinterpret_cast<uint16_t*>(tma_smem + s * kTmaStageBytes + T * 16); };
@@ -522,24 +523,38 @@ __global__ void __launch_bounds__(kTmaThreads, 1) plan_partition_tma_kernel(
         if (blockIdx.x < nfull) issue(blockIdx.x, 0);
         if (blockIdx.x + G < nfull) issue(blockIdx.x + G, 1);
     }
+    uint4 ra[Q], rb[Q];
+    const uint4 z4 = make_uint4(0, 0, 0, 0);
+    auto load = [&](int64_t t) {
+#pragma unroll
+        for (int i = 0; i < Q; i++) {
+            const int64_t e = t * T + threadIdx.x + i * kTmaThreads;
+            ra[i] = m2 ? __ldcs(m2 + e) : z4;
+            rb[i] = m4 ? __ldcs(m4 + e) : z4;
+        }
+    };
+    if ((int64_t)blockIdx.x < nfull) load(blockIdx.x);
     uint32_t parity = 0;  // bit s: phase of stage s
     int s = 0;
     for (int64_t t = blockIdx.x; t < nfull; t += G) {
         mbar_wait(&bar[s], (parity >> s) & 1);
         parity ^= 1u << s;
-        const uint4* rs = rows_of(s);
+        uint4* rs = rows_of(s);
+        if (m2 || m4) {
+#pragma unroll
+            for (int i = 0; i < Q; i++) {
+                const int k = threadIdx.x + i * kTmaThreads;
+                rs[k] = xor4(rs[k], xor4(ra[i], rb[i]));
+            }
+            __syncthreads();
+            if (t + G < nfull) load(t + G);
+        }
         const uint16_t* sr = srow_of(s);
         const int32_t* gd = gdst_of(s);
-        const uint4* b = m2 ? m2 + t * T : nullptr;
-        const uint4* d = m4 ? m4 + t * T : nullptr;
 #pragma unroll
-        for (int q = 0; q < T / kTmaThreads; q++) {
-            const int k = threadIdx.x + q * kTmaThreads;
-            const int j = sr[k];
-            uint4 v = rs[j];
-            if (b) v = xor4(v, __ldcg(b + j));
-            if (d) v = xor4(v, __ldcg(d + j));
-            __stcs(inter + gd[k], v);
+        for (int i = 0; i < Q; i++) {
+            const int k = threadIdx.x + i * kTmaThreads;
+            __stcs(inter + gd[k], rs[sr[k]]);
         }
         __syncthreads();  // stage s fully read before it is refilled
         if (threadIdx.x == 0 && t + 2 * G < nfull) issue(t + 2 * G, s);
@@ -556,6 +571,125 @@ __global__ void __launch_bounds__(kTmaThreads, 1) plan_partition_tma_kernel(
             if (m4) v = xor4(v, __ldcs(m4 + b0 + j));
             __stcs(inter + __ldcs(gdst + b0 + k), v);
         }
+    }
+}
+
+
+// ---- chained passes: one party's window pass feeding the next party's
+// partition pass, tile by tile in shared memory -------------------------------
+// In the 3-party shuffle a message is consumed by exactly one gather of the
+// receiving party (x1 -> c1 at pi23, y1 -> R3 at k3).  With planned gathers
+// the sender's window pass writes the message in order and the receiver's
+// partition pass reads it straight back.  Here one persistent CTA per SM
+// builds a 4096-row tile of the message from the sender's intermediate
+// (random reads inside one 8 MB window), XORs the receiver's source-order
+// blind into it in shared memory, and writes the tile out as the receiver's
+// window runs.  The message never round-trips HBM (optionally it is also
+// stored, for transcripts and tests).
+// The window gathers go straight to shared memory with cp.async, three
+// tiles deep, so a CTA always has two tiles of random reads in flight while
+// it scatters the third (register-staged loads allowed only one: each tile
+// then waited out its slowest DRAM miss, 2.7 vs 5.0 TB/s).  q, blind, srow
+// and gdst are read in slot / row order, coalesced.
+constexpr int kChainStages = 3;
+constexpr int kChainSmem2 = kChainStages * kTmaTile * 16;
+constexpr int64_t kDualMaxBytes = (int64_t)256 << 20;  // measured: one dual window pass wins up to 2^24 rows
+
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+__global__ void __launch_bounds__(kTmaThreads, 1) plan_chain_kernel(
+    const int32_t* __restrict__ q, const uint4* __restrict__ inter_a, const uint4* __restrict__ blind,
+    const uint16_t* __restrict__ srow, const int32_t* __restrict__ gdst, int64_t rows, uint4* __restrict__ inter_b,
+    uint4* __restrict__ msg) {
+    extern __shared__ __align__(128) unsigned char tma_smem[];
+    constexpr int T = kTmaTile;
+    constexpr int Q = T / kTmaThreads;
+    auto buf = [&](int64_t j) { return reinterpret_cast<uint4*>(tma_smem) + (int)(j % kChainStages) * T; };
+    const int64_t nfull = rows / T;
+    const int64_t G = gridDim.x;
+    const int64_t nmine = nfull > blockIdx.x ? (nfull - blockIdx.x + G - 1) / G : 0;
+    auto tile = [&](int64_t j) { return blockIdx.x + j * G; };
+    int32_t qn[Q];
+    auto load_q = [&](int64_t j) {
+        if (j < nmine) {
+#pragma unroll
+            for (int i = 0; i < Q; i++) qn[i] = __ldcs(q + tile(j) * T + threadIdx.x + i * kTmaThreads);
+        }
+    };
+    auto gather = [&](int64_t j) {  // uses qn (tile j), then prefetches q of tile j + 1
+        if (j < nmine) {
+            uint4* b = buf(j);
+#pragma unroll
+            for (int i = 0; i < Q; i++) cp_async16(b + threadIdx.x + i * kTmaThreads, inter_a + qn[i]);
+        }
+        cp_async_commit();  // empty groups keep the wait count uniform
+        load_q(j + 1);
+    };
+    load_q(0);
+    gather(0);
+    gather(1);
+    for (int64_t j = 0; j < nmine; j++) {
+        const int64_t t = tile(j);
+        uint4 bl[Q];
+        uint16_t sr[Q];
+        int32_t gd[Q];
+#pragma unroll
+        for (int i = 0; i < Q; i++) {
+            const int k = threadIdx.x + i * kTmaThreads;
+            bl[i] = __ldcs(blind + t * T + k);
+            sr[i] = __ldcs(srow + t * T + k);
+            gd[i] = __ldcs(gdst + t * T + k);
+        }
+        gather(j + 2);   // buffer (j + 2) % 3 was freed by the barrier closing tile j - 1
+        cp_async_wait<2>();  // this thread's gathers of tile j have landed
+        uint4* rs = buf(j);
+#pragma unroll
+        for (int i = 0; i < Q; i++) {
+            const int k = threadIdx.x + i * kTmaThreads;
+            const uint4 v = rs[k];
+            if (msg) __stcs(msg + t * T + k, v);
+            rs[k] = xor4(v, bl[i]);
+        }
+        __syncthreads();
+#pragma unroll
+        for (int i = 0; i < Q; i++) __stcs(inter_b + gd[i], rs[sr[i]]);
+        __syncthreads();
+    }
+    cp_async_wait<0>();
+    // ragged last tile: the last CTA, through buffer 0 (nothing is in flight any more)
+    if (blockIdx.x == G - 1 && rows % T) {
+        __syncthreads();
+        const int64_t b0 = nfull * T;
+        const int nr = (int)(rows - b0);
+        uint4* rs = buf(0);
+        for (int k = threadIdx.x; k < nr; k += kTmaThreads) {
+            const uint4 m = __ldcg(inter_a + __ldcs(q + b0 + k));
+            if (msg) __stcs(msg + b0 + k, m);
+            rs[k] = xor4(m, __ldcs(blind + b0 + k));
+        }
+        __syncthreads();
+        for (int k = threadIdx.x; k < nr; k += kTmaThreads) __stcs(inter_b + __ldcs(gdst + b0 + k), rs[__ldcs(srow + b0 + k)]);
+    }
+}
+
+// the last window passes of two planned gathers with the same output order,
+// XORed: R3[i] = Ir[qr[i]] ^ c1[i], c1[i] = Ic[qc[i]] (msg: c1 stored too)
+__global__ void __launch_bounds__(256) win_gather_dual4_kernel(const int32_t* __restrict__ qa,
+                                                               const uint4* __restrict__ ia,
+                                                               const int32_t* __restrict__ qb,
+                                                               const uint4* __restrict__ ib, int64_t rows,
+                                                               uint4* __restrict__ out, uint4* __restrict__ msg) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < rows; i += stride) {
+        const uint4 va = __ldcg(ia + __ldcs(qa + i));
+        const uint4 vb = __ldcg(ib + __ldcs(qb + i));
+        if (msg) __stcs(msg + i, va);
+        __stcs(out + i, xor4(va, vb));
     }
 }
 
@@ -625,6 +759,7 @@ int shuffle_init() {
     OGM_CUDA_TRY(allow_big_smem(perm_draws_kernel<AesTab>, kAesTableBytes));
     OGM_CUDA_TRY(allow_big_smem(shuffle_gather_kernel<true, AesTab>, kAesTableBytes));
     OGM_CUDA_TRY(prefer_l1(win_gather4_kernel));
+    OGM_CUDA_TRY(prefer_l1(win_gather_dual4_kernel));
     OGM_CUDA_TRY(prefer_l1(gather_matrix_kernel));
     OGM_CUDA_TRY(prefer_l1(gather_matrix_rows_kernel));
     return OGM_OK;
@@ -1051,6 +1186,70 @@ int ogm_trio_shuffle(const uint8_t* s12, const uint8_t* s23, const uint8_t* s31,
     OGM_TRY(ogm_shuffle_gather(rows, W, width_bits, nullptr, k3, y1, nullptr, c1, nullptr, nullptr, 0, nullptr, nullptr,
                                nullptr, 0, nullptr, nullptr, nullptr, 0, z, 0, P, r3, stream));
 #undef OGM_TRY
+    return OGM_OK;
+}
+
+// The online phase of one 3-party shuffle of 16-byte rows for the three
+// co-resident parties over planned gathers, with each message handed from
+// sender to receiver in shared memory (plan_chain_kernel).  Plans in
+// step order x1 (k1), y1 (pi12), c1 (pi23), R3 (k3); every blind is in the
+// source order of its step (ShuffleOffline with plans):
+//   P1: I1 = part1(a ^ b ^ U')            P2: Iy = part2(c ^ V')
+//   P1 -> P2: x1 = win1(I1); Ic = part3(x1 ^ W')
+//   P2 -> P3: y1 = win2(Iy); Ir = part4(y1 ^ Z')
+//   P2 -> P3, P3: c1 = win3(Ic); R3 = win4(Ir) ^ c1
+// x1, y1, c1 are optional copies of the messages; inter[0..2] are three
+// table-sized scratch buffers.
+int ogm_shuffle_online_planned(int64_t rows, const int32_t* const* q2, const int32_t* const* gdst,
+                               const uint16_t* const* srow, const uint32_t* a, const uint32_t* b, const uint32_t* c,
+                               const uint32_t* u_src, const uint32_t* v_src, const uint32_t* w_src,
+                               const uint32_t* z_src, uint32_t* const* inter, uint32_t* x1, uint32_t* y1, uint32_t* c1,
+                               uint32_t* r3, void* stream) {
+    using namespace ogm;
+    OGM_CHECK_ARG(rows >= 0 && rows < ((int64_t)1 << 31), OGM_ERR_ARG, "rows out of range");
+    OGM_CHECK_ARG(q2 && gdst && srow && inter, OGM_ERR_ARG, "plans and scratch are required");
+    const void* need[] = {a, b, c, u_src, v_src, w_src, z_src, r3, inter[0], inter[1], inter[2]};
+    for (const void* p : need)
+        OGM_CHECK_ARG(p && (((uintptr_t)p) & 15) == 0, OGM_ERR_ARG, "16-byte aligned tables are required");
+    const void* opt[] = {x1, y1, c1};
+    for (const void* p : opt) OGM_CHECK_ARG((((uintptr_t)p) & 15) == 0, OGM_ERR_ARG, "16-byte aligned tables are required");
+    for (int k = 0; k < 4; k++) OGM_CHECK_ARG(q2[k] && gdst[k] && srow[k], OGM_ERR_ARG, "plan %d is incomplete", k);
+    if (rows == 0) return OGM_OK;
+    OGM_ENSURE_INIT();
+    cudaStream_t st = as_stream(stream);
+    OGM_CUDA_TRY(allow_big_smem(plan_partition_tma_kernel, kTmaSmemBytes));
+    OGM_CUDA_TRY(allow_big_smem(plan_chain_kernel, kChainSmem2));
+    const int64_t ntiles = (rows + kTmaTile - 1) / kTmaTile;
+    const int g = (int)std::min<int64_t>(ntiles, (int64_t)sm_count());
+    const bool scrub = rows * 16 >= kScrubMinBytes;
+    auto scrub_l2 = [&]() -> int {
+        int64_t sb = 0;
+        if (scrub)
+            if (void* sc = scrub_buffer(&sb)) OGM_CUDA_TRY(cudaMemsetAsync(sc, 0, (size_t)sb, st));
+        return OGM_OK;
+    };
+    using U4 = const uint4*;
+    uint4 *i0 = (uint4*)inter[0], *i1 = (uint4*)inter[1], *i2 = (uint4*)inter[2];
+    constexpr int TT = kTmaThreads;
+    plan_partition_tma_kernel<<<g, TT, kTmaSmemBytes, st>>>((U4)a, (U4)b, (U4)u_src, srow[0], gdst[0], rows, i0);
+    plan_partition_tma_kernel<<<g, TT, kTmaSmemBytes, st>>>((U4)c, (U4)v_src, nullptr, srow[1], gdst[1], rows, i1);
+    if (scrub_l2() != OGM_OK) return OGM_ERR_CUDA;
+    plan_chain_kernel<<<g, TT, kChainSmem2, st>>>(q2[0], i0, (U4)w_src, srow[2], gdst[2], rows, i2, (uint4*)x1);
+    if (scrub_l2() != OGM_OK) return OGM_ERR_CUDA;
+    plan_chain_kernel<<<g, TT, kChainSmem2, st>>>(q2[1], i1, (U4)z_src, srow[3], gdst[3], rows, i0, (uint4*)y1);
+    if (scrub_l2() != OGM_OK) return OGM_ERR_CUDA;
+    const int64_t g2 = std::min<int64_t>((rows + 255) / 256, (int64_t)sm_count() * 8);
+    if (rows * 16 <= kDualMaxBytes) {
+        win_gather_dual4_kernel<<<(int)g2, 256, 0, st>>>(q2[2], i2, q2[3], i0, rows, (uint4*)r3, (uint4*)c1);
+    } else {
+        // two random windows at once thrash L2 far above its size (2^26 rows: 2.06 ms and 11 GB read
+        // instead of 2.7): c1's window pass, then R3's with c1 streamed
+        uint4* c1m = c1 ? (uint4*)c1 : i1;
+        win_gather4_kernel<<<(int)g2, 256, 0, st>>>(q2[2], i2, nullptr, nullptr, rows, c1m);
+        if (scrub_l2() != OGM_OK) return OGM_ERR_CUDA;
+        win_gather4_kernel<<<(int)g2, 256, 0, st>>>(q2[3], i0, c1m, nullptr, rows, (uint4*)r3);
+    }
+    OGM_LAUNCH_CHECK();
     return OGM_OK;
 }
 

@@ -521,6 +521,40 @@ def test_c5_planned_shuffle_matches_oracle_at_scale():
     assert np.array_equal(r3.cpu().numpy().view(np.uint32), o3)
     assert np.array_equal(off[0].out_a.cpu().numpy().view(np.uint32), o1)
     assert np.array_equal(off[0].out_b.cpu().numpy().view(np.uint32), o2)
+    # the chained online shuffle (messages handed over in shared memory): same messages, same R3
+    from paper_2209_03526_b200.shuffle import shuffle_online_planned
+    msgs = [e(), e(), e()]
+    r3c = shuffle_online_planned(off, comps[0], comps[1], comps[2], e(), msgs=msgs)
+    for got, want in zip(msgs + [r3c], (m_x1, m_y1, m_c1, o3)):
+        assert np.array_equal(got.cpu().numpy().view(np.uint32), want)
+    r3n = shuffle_online_planned(off, comps[0], comps[1], comps[2], e())
+    assert torch.equal(r3n, r3c)
+
+
+@pytest.mark.parametrize("rows", [4096, 3 * 4096 + 77, 148 * 4096 + 4095, 1 << 20, (1 << 24) + 3 * 4096 + 5])
+def test_chained_online_shuffle_equals_party_steps(rows):
+    """ogm_shuffle_online_planned (each message handed from sender to
+    receiver tile by tile in shared memory; ragged last tiles; the dual
+    window pass) gives the four per-party planned steps' messages and R3."""
+    from paper_2209_03526_b200 import workloads
+    from paper_2209_03526_b200.net import make_session_configs
+    from paper_2209_03526_b200.shuffle import ShuffleOffline, shuffle_online_planned
+
+    cfg = make_session_configs(b"\x3a" * 16)
+    comps = [workloads.device_random_words(rows * 4, 5, 50 + c).reshape(rows, 4) for c in range(3)]
+    off = [ShuffleOffline(p + 1, cfg[p].seed_with_next, cfg[p].seed_with_prev, 2, rows, 128, plan=True)
+           for p in range(3)]
+    e = lambda: torch.empty_like(comps[0])  # noqa: E731
+    want = [e() for _ in range(4)]
+    off[0].step_x1(comps[0], comps[1], want[0])
+    off[1].step_y1(comps[2], want[1])
+    off[1].step_c1(want[0], want[2])
+    off[2].step_r3(want[1], want[2], want[3])
+    msgs = [e(), e(), e()]
+    r3 = shuffle_online_planned(off, comps[0], comps[1], comps[2], e(), msgs=msgs)
+    for got, w in zip(msgs + [r3], want):
+        assert torch.equal(got, w)
+    assert torch.equal(shuffle_online_planned(off, comps[0], comps[1], comps[2], e()), want[3])
 
 
 @pytest.mark.parametrize("world", [1, 2, 3, 8])
