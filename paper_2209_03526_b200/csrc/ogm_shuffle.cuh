@@ -1243,7 +1243,8 @@ int ogm_shuffle_online_planned(int64_t rows, const int32_t* const* q2, const int
         win_gather_dual4_kernel<<<(int)g2, 256, 0, st>>>(q2[2], i2, q2[3], i0, rows, (uint4*)r3, (uint4*)c1);
     } else {
         // two random windows at once thrash L2 far above its size (2^26 rows: 2.06 ms and 11 GB read
-        // instead of 2.7): c1's window pass, then R3's with c1 streamed
+        // instead of 2.7; smaller windows do not rescue it, scripts/exp_chain_win.py): c1's window
+        // pass, then R3's with c1 streamed
         uint4* c1m = c1 ? (uint4*)c1 : i1;
         win_gather4_kernel<<<(int)g2, 256, 0, st>>>(q2[2], i2, nullptr, nullptr, rows, c1m);
         if (scrub_l2() != OGM_OK) return OGM_ERR_CUDA;
