@@ -209,6 +209,118 @@ __global__ void __launch_bounds__(256) masked_parity_v2_kernel(const ParityArgs 
 }
 
 // ---------------------------------------------------------------------------
+// Masked parity for rows of at most 1024 words (the Zipf attributes of
+// C3/C4, w = 313): indicators in registers as in v2, but the share rows are
+// staged in shared memory by bulk copies (TMA), S stages deep, so the bytes
+// in flight no longer ride on the registers of two CTAs per SM (v2 at C4:
+// 128 registers, 18.75% occupancy, 5.26 TB/s).  One persistent CTA per SM;
+// a stage is RT consecutive rows of every component -- contiguous at the row
+// pitch, so one bulk copy per component.  Warp (rg, wc) owns the 128-word
+// column chunk wc and rows rg, rg + RGW, ... of each stage; RT divides 32,
+// so a stage's rows fall in one output word.
+// ---------------------------------------------------------------------------
+constexpr int kParTmaSmemMax = 200 * 1024;
+constexpr int kParTmaMaxWords = 1024;
+
+template <int NPARTY, int NPASS>
+__global__ void __launch_bounds__(512, 1) masked_parity_tma_kernel(const ParityArgs p, int CW, int RT, int S) {
+    constexpr int NJ = NPARTY * NPASS;
+    constexpr int NCOMP = NPARTY == 1 ? 2 : 3;
+    extern __shared__ __align__(128) unsigned char par_smem[];
+    const int64_t P = p.pitch;
+    const int64_t comp_bytes = (int64_t)RT * P * 4;  // one component's rows in a stage
+    uint64_t* bar = reinterpret_cast<uint64_t*>(par_smem + S * NCOMP * comp_bytes);
+    auto stage = [&](int s, int c) {
+        return reinterpret_cast<const uint32_t*>(par_smem + (s * NCOMP + c) * comp_bytes);
+    };
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int RGW = (int)(blockDim.x >> 5) / CW;
+    const int rg = warp / CW, wc = warp % CW;
+    const int64_t col0 = (int64_t)wc * 128 + lane * 4;
+    uint4 ia[NJ], ib[NJ];
+#pragma unroll
+    for (int j = 0; j < NJ; j++) {
+        uint32_t a4[4], b4[4];
+#pragma unroll
+        for (int e = 0; e < 4; e++) {
+            const bool in = col0 + e < p.words;
+            a4[e] = in ? __ldg(p.ind[2 * j] + col0 + e) : 0u;
+            b4[e] = in ? __ldg(p.ind[2 * j + 1] + col0 + e) : 0u;
+        }
+        ia[j] = make_uint4(a4[0], a4[1], a4[2], a4[3]);
+        ib[j] = make_uint4(b4[0], b4[1], b4[2], b4[3]);
+    }
+    const bool lane_live = col0 < P;
+    const int64_t ntile = (p.rows + RT - 1) / RT;
+    const int64_t G = gridDim.x;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < S; s++) mbar_init(&bar[s], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    auto issue = [&](int64_t t, int s) {
+        const int64_t r0 = t * RT;
+        const uint32_t bytes = (uint32_t)(min((int64_t)RT, p.rows - r0) * P * 4);
+        mbar_expect_tx(&bar[s], NCOMP * bytes);
+#pragma unroll
+        for (int c = 0; c < NCOMP; c++)
+            bulk_g2s((void*)stage(s, c), p.comp[c] + r0 * P, bytes, &bar[s]);
+    };
+    if (threadIdx.x == 0)
+        for (int s = 0; s < S; s++)
+            if (blockIdx.x + s * G < ntile) issue(blockIdx.x + s * G, s);
+    uint32_t phase = 0;  // bit s: phase of stage s
+    int s = 0;
+    for (int64_t t = blockIdx.x; t < ntile; t += G) {
+        mbar_wait(&bar[s], (phase >> s) & 1);
+        phase ^= 1u << s;
+        const int64_t r0 = t * RT;
+        const int nr = (int)min((int64_t)RT, p.rows - r0);
+        const int sh = (int)(r0 & 31);
+        // lane-local parity bits, one per (row, j), shifted in (no ballot per row);
+        // then ONE butterfly XOR over the lanes of all j's bits packed in a word
+        uint32_t acc[NJ];
+#pragma unroll
+        for (int j = 0; j < NJ; j++) acc[j] = 0;
+        int nrw = 0;
+        for (int r = rg; r < nr; r += RGW, nrw++) {
+            uint4 cv[NCOMP];
+#pragma unroll
+            for (int c = 0; c < NCOMP; c++)
+                cv[c] = lane_live ? *reinterpret_cast<const uint4*>(stage(s, c) + r * P + col0)
+                                  : make_uint4(0, 0, 0, 0);
+#pragma unroll
+            for (int ps = 0; ps < NPASS; ps++) {
+#pragma unroll
+                for (int q = 0; q < NPARTY; q++) {
+                    const int j = ps * NPARTY + q;
+                    const uint4 A = cv[q], B = cv[(q + 1) % NCOMP];
+                    const uint32_t part = ((A.x & ia[j].x) ^ (B.x & ib[j].x)) ^ ((A.y & ia[j].y) ^ (B.y & ib[j].y)) ^
+                                          ((A.z & ia[j].z) ^ (B.z & ib[j].z)) ^ ((A.w & ia[j].w) ^ (B.w & ib[j].w));
+                    acc[j] = (acc[j] << 1) | (__popc(part) & 1u);
+                }
+            }
+        }
+        if (nrw > 0) {  // warp-uniform; NJ * nrw <= 32 (host picks RT accordingly)
+            uint32_t packed = 0;
+#pragma unroll
+            for (int j = 0; j < NJ; j++) packed |= acc[j] << (j * nrw);
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) packed ^= __shfl_xor_sync(0xffffffffu, packed, off);
+            if (lane < NJ) {
+                const uint32_t a = packed >> (lane * nrw);
+                uint32_t v = 0;
+                for (int i = 0; i < nrw; i++) v |= ((a >> (nrw - 1 - i)) & 1u) << (sh + rg + i * RGW);
+                if (v) atomicXor(p.out[lane] + (r0 >> 5), v);
+            }
+        }
+        __syncthreads();  // stage s fully read before it is refilled
+        if (threadIdx.x == 0 && t + S * G < ntile) issue(t + S * G, s);
+        s = s + 1 == S ? 0 : s + 1;
+    }
+}
+
+// ---------------------------------------------------------------------------
 // src/rss.py:143-148 for all three parties at once: alpha_q = F(k_q) ^
 // F(k_{q-1}) (party q holds its own key and its predecessor's,
 // src/net.py:229-232), optionally XORed into per-party buffers.  3 AES per
@@ -831,6 +943,36 @@ int ogm_masked_parity(int64_t rows, int64_t words, int64_t pitch, int ncomp, con
     p.words = words;
     p.pitch = pitch;
     cudaStream_t st = as_stream(stream);
+    if (aligned && words >= 64 && pitch <= kParTmaMaxWords) {
+        // short rows: bulk-copy staged rows (masked_parity_tma_kernel)
+        const int CW = (int)((words + 127) / 128);
+        int RGW = 1;
+        while (RGW * 2 * CW <= 16) RGW <<= 1;
+        // a warp's rows per stage times the (pass, party) count must fit one packed word
+        const int rows_per_warp = 32 / (npass * nparty);
+        int RT = 32;
+        while (RT > 1 && ((int64_t)ncomp * RT * pitch * 4 > kParTmaSmemMax / 3 || RT > RGW * rows_per_warp)) RT >>= 1;
+        if (RGW > RT) RGW = RT;
+        const int64_t stage_bytes = (int64_t)ncomp * RT * pitch * 4;
+        const int S = (int)std::min<int64_t>(6, kParTmaSmemMax / stage_bytes);
+        const int64_t ntile = (rows + RT - 1) / RT;
+        const int G = (int)std::min<int64_t>(ntile, (int64_t)sm_count());
+        const size_t smem = (size_t)(S * stage_bytes + 8 * S);
+        for (int j = 0; j < npass * nparty; j++)
+            OGM_CUDA_TRY(cudaMemsetAsync(out[j], 0, 4 * ((rows + 31) / 32), st));
+#define OGM_PARITY_TMA(NP, NS)                                                                   \
+    do {                                                                                         \
+        OGM_CUDA_TRY(allow_big_smem(masked_parity_tma_kernel<NP, NS>, (int)smem));               \
+        masked_parity_tma_kernel<NP, NS><<<G, 32 * CW * RGW, smem, st>>>(p, CW, RT, S);          \
+    } while (0)
+        if (nparty == 1 && npass == 1) OGM_PARITY_TMA(1, 1);
+        else if (nparty == 1) OGM_PARITY_TMA(1, 2);
+        else if (npass == 1) OGM_PARITY_TMA(3, 1);
+        else OGM_PARITY_TMA(3, 2);
+#undef OGM_PARITY_TMA
+        OGM_LAUNCH_CHECK();
+        return OGM_OK;
+    }
     if (aligned && words >= 64) {
         // register-resident indicators; CW warps (x128 columns) per row group
         // as many 128-word warp columns as the row needs (<= 8): at w = 313 (the
