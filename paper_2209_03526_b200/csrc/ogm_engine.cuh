@@ -130,9 +130,11 @@ __global__ void __launch_bounds__(256) masked_parity_kernel(const ParityArgs p) 
 // a chunk of columns and keeps its slice of all 2*NPARTY*NPASS indicators in
 // registers (one uint4 per vector per lane); warps then stream rows through
 // it.  For each row a lane folds its 4 words into a 32-bit partial per
-// (pass, party); the row's partial parity over the warp's 128 columns is
-// popc(ballot(popc(partial) & 1)) & 1.  32 rows make an output word, which is
-// XORed into the (pre-zeroed) result -- parity is XOR-linear, so column
+// (pass, party).  Trio: each lane shifts popc(partial) & 1 into a per-(pass,
+// party) word, one bit per row, and after 32 rows one butterfly XOR over the
+// lanes gives the warp's 128-column partial parities of the tile (an output
+// word); per party the row's parity is popc(ballot(popc(partial) & 1)) & 1.
+// The word is XORed into the (pre-zeroed) result -- parity is XOR-linear, so column
 // chunks and warps combine with atomicXor.  Shares are read exactly once,
 // with 128-bit loads, and the indicator traffic is paid once per CTA.
 // ---------------------------------------------------------------------------
@@ -192,19 +194,31 @@ __global__ void __launch_bounds__(256) masked_parity_v2_kernel(const ParityArgs 
                         const uint4 A = cv[r][q], B = cv[r][(q + 1) % NCOMP];
                         const uint32_t part = ((A.x & ia[j].x) ^ (B.x & ib[j].x)) ^ ((A.y & ia[j].y) ^ (B.y & ib[j].y)) ^
                                               ((A.z & ia[j].z) ^ (B.z & ib[j].z)) ^ ((A.w & ia[j].w) ^ (B.w & ib[j].w));
-                        const uint32_t bal = __ballot_sync(0xffffffffu, __popc(part) & 1);
-                        word[j] |= (uint32_t)(__popc(bal) & 1) << (i0 + r);
+                        if constexpr (NPARTY == 1) {  // measured faster per party (C3 uniform 3.9 vs 5.5 ms)
+                            const uint32_t bal = __ballot_sync(0xffffffffu, __popc(part) & 1);
+                            word[j] |= (uint32_t)(__popc(bal) & 1) << (i0 + r);
+                        } else {
+                            word[j] = (word[j] << 1) | (__popc(part) & 1u);  // lane-local, row i0 + r
+                        }
                     }
                 }
             }
         }
-        if (lane < NJ) {
-            uint32_t v = 0;
+        // rows were shifted in first-to-last over a whole number of RB batches:
+        // bit-reverse, drop the padding, then XOR over the lanes (one butterfly per j)
+        const int npad = (nrow + RB - 1) / RB * RB;
+        uint32_t v = 0;
 #pragma unroll
-            for (int j = 0; j < NJ; j++)
-                if (j == lane) v = word[j];
-            if (v) atomicXor(p.out[lane] + tile, v);
+        for (int j = 0; j < NJ; j++) {
+            uint32_t w = word[j];
+            if constexpr (NPARTY != 1) {
+                w = __brev(w) >> (32 - npad);
+#pragma unroll
+                for (int off = 16; off > 0; off >>= 1) w ^= __shfl_xor_sync(0xffffffffu, w, off);
+            }
+            if (j == lane) v = w;
         }
+        if (lane < NJ && v) atomicXor(p.out[lane] + tile, v);
     }
 }
 
