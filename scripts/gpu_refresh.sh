@@ -21,4 +21,8 @@ timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__byte
   python bench_configs.py access --steps 2 --warmup 1 > $O/access_ncu.csv 2>&1
 timeout 600 ncu --profile-from-start off --metrics gpu__time_duration.sum --clock-control none --csv \
   python scripts/exp_trio_gpu.py > $O/trio_c1_launches.csv 2>&1
+timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \
+  -k "regex:plan_|win_gather" --csv python bench_configs.py c5 --min-log 24 --max-log 24 --steps 2 --warmup 1 > $O/c5_24_ncu.csv 2>&1
+timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \
+  -k "regex:masked_parity|zero_share" --csv python bench_configs.py c4 --steps 2 --warmup 1 > $O/c4_ncu.csv 2>&1
 echo refresh-done
