@@ -771,6 +771,38 @@ __global__ void extract_field_kernel(const uint32_t* __restrict__ src, int64_t s
     }
 }
 
+// Several narrow extractions from the same kept rows in one launch
+// (blockIdx.y = job): the trio open-keep's 3 components x fields.
+constexpr int kMaxExtract = 24;
+struct ExtractJob {
+    const uint32_t* src;
+    uint32_t* out;
+    int64_t off, width, opitch;
+};
+struct ExtractJobs {
+    ExtractJob j[kMaxExtract];
+    const int32_t* idx;
+    int64_t spitch, n;
+};
+
+__global__ void extract_field_multi_kernel(const ExtractJobs J) {
+    const ExtractJob& e = J.j[blockIdx.y];
+    const int64_t ow = (e.width + 31) >> 5;
+    const int64_t total = J.n * e.opitch;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    const int64_t sw = (e.off + e.width + 31) >> 5;
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += stride) {
+        const int64_t k = t / e.opitch, j = t % e.opitch;
+        uint32_t v = 0;
+        if (j < ow) {
+            const int64_t r = J.idx ? J.idx[k] : k;
+            v = field_bits32(e.src + r * J.spitch, sw * 32, e.off + j * 32);
+            if (j == ow - 1 && (e.width & 31)) v &= (1u << (e.width & 31)) - 1u;
+        }
+        e.out[k * e.opitch + j] = v;
+    }
+}
+
 // clean row tails after a matrix re-share (src/engine.py:88-89)
 __global__ void mask_row_tails_kernel(uint32_t* __restrict__ mat, int64_t rows, int64_t pitch, int64_t w,
                                       uint32_t mask) {
@@ -1402,6 +1434,25 @@ int ogm_trio_open_keep(const uint32_t* const* comps, int64_t rows, int64_t pitch
     int64_t k = 0;
     for (int64_t i = 0; i < nw; i++) k += __builtin_popcount(plain_host[i]);
     *kept = k;
+    bool narrow = 3 * nfields <= kMaxExtract;
+    for (int f = 0; f < nfields; f++) narrow = narrow && opitch[f] < 256;
+    if (narrow && k > 0 && nfields > 0) {
+        ExtractJobs J{};
+        int64_t most = 0;
+        for (int c = 0; c < 3; c++)
+            for (int f = 0; f < nfields; f++) {
+                J.j[c * nfields + f] = ExtractJob{comps[c], out[c * nfields + f], bit_off[f], width[f], opitch[f]};
+                most = std::max(most, k * opitch[f]);
+            }
+        J.idx = idx;
+        J.spitch = pitch;
+        J.n = k;
+        if (most > 0) {
+            extract_field_multi_kernel<<<dim3((unsigned)grid_for(most), (unsigned)(3 * nfields)), 256, 0, st>>>(J);
+            OGM_LAUNCH_CHECK();
+        }
+        return OGM_OK;
+    }
     for (int c = 0; c < 3; c++)
         for (int f = 0; f < nfields; f++) {
             rc = ogm_extract_field(comps[c], pitch, idx, k, bit_off[f], width[f], out[c * nfields + f], opitch[f],

@@ -26,14 +26,11 @@ namespace ogm {
 // has all its predecessors done, so the result equals the sequential loop.
 // ---------------------------------------------------------------------------
 
-template <class TAB = AesTab>
-__global__ void __launch_bounds__(kAesThreads) perm_draws_kernel(
-    AesKeySched key, uint32_t label_be, uint64_t index, int64_t n, int32_t* __restrict__ H,
-    int32_t* __restrict__ live, int32_t* __restrict__ perm, int32_t* __restrict__ R) {
-    extern __shared__ __align__(128) uint8_t smem_raw[];
-    TAB::fill(smem_raw);
-    __syncthreads();
-    const TAB T(smem_raw);
+template <class TAB>
+__device__ __forceinline__ void perm_draws_body(const TAB& T, const AesKeySched& key, uint32_t label_be,
+                                                uint64_t index, int64_t n, int32_t* __restrict__ H,
+                                                int32_t* __restrict__ live, int32_t* __restrict__ perm,
+                                                int32_t* __restrict__ R) {
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     for (int64_t x = tid; x < n; x += stride) {
@@ -54,6 +51,43 @@ __global__ void __launch_bounds__(kAesThreads) perm_draws_kernel(
             live[q] = (int32_t)i;
         }
     }
+}
+
+template <class TAB = AesTab>
+__global__ void __launch_bounds__(kAesThreads) perm_draws_kernel(
+    AesKeySched key, uint32_t label_be, uint64_t index, int64_t n, int32_t* __restrict__ H,
+    int32_t* __restrict__ live, int32_t* __restrict__ perm, int32_t* __restrict__ R, int32_t* __restrict__ cnts) {
+    extern __shared__ __align__(128) uint8_t smem_raw[];
+    TAB::fill(smem_raw);
+    __syncthreads();
+    const TAB T(smem_raw);
+    if (blockIdx.x == 0 && threadIdx.x == 0) {  // live counts of the multi-launch rounds (no pageable H2D copy)
+        cnts[0] = (int32_t)(n - 1);
+        cnts[1] = 0;
+    }
+    perm_draws_body(T, key, label_be, index, n, H, live, perm, R);
+}
+
+// The three permutations of one shuffle (same label, index and size,
+// different pairwise keys) in one launch each for draws and rounds
+// (small tables: the trio executor's shuffles).
+struct PermJob {
+    AesKeySched key;
+    int32_t *H, *R, *live0, *live1, *perm;
+};
+struct PermJobs3 {
+    PermJob j[3];
+};
+
+template <class TAB>
+__global__ void __launch_bounds__(kAesThreads) perm_draws3_kernel(const PermJobs3 jobs, uint32_t label_be,
+                                                                  uint64_t index, int64_t n) {
+    extern __shared__ __align__(128) uint8_t smem_raw[];
+    TAB::fill(smem_raw);
+    __syncthreads();
+    const TAB T(smem_raw);
+    const PermJob& j = jobs.j[blockIdx.y];
+    perm_draws_body(T, j.key, label_be, index, n, j.H, j.live0, j.perm, j.R);
 }
 
 __global__ void perm_reserve_kernel(const int32_t* __restrict__ live, const int32_t* __restrict__ cnt,
@@ -205,14 +239,8 @@ __device__ __forceinline__ void gather_chunk(const TAB& T, const GatherArgs& a, 
     }
 }
 
-template <bool ONLINE, class TAB = AesTab>
-__global__ void __launch_bounds__(kAesThreads) shuffle_gather_kernel(const GatherArgs a) {
-    extern __shared__ __align__(128) uint8_t smem_raw[];
-    if (ONLINE) {
-        TAB::fill(smem_raw);
-        __syncthreads();
-    }
-    const TAB T(smem_raw);
+template <bool ONLINE, class TAB>
+__device__ __forceinline__ void gather_body(const TAB& T, const GatherArgs& a) {
     // 128-bit path when rows are 16-B pitched and every base is aligned
     const bool vec = (a.pitch & 3) == 0 &&
                      ((((uintptr_t)a.M1) | ((uintptr_t)a.M2) | ((uintptr_t)a.M3) | ((uintptr_t)a.out) |
@@ -231,6 +259,35 @@ __global__ void __launch_bounds__(kAesThreads) shuffle_gather_kernel(const Gathe
             gather_chunk<ONLINE, TAB>(T, a, i, t - i * nch, tail, vec);
         }
     }
+}
+
+template <bool ONLINE, class TAB = AesTab>
+__global__ void __launch_bounds__(kAesThreads) shuffle_gather_kernel(const GatherArgs a) {
+    extern __shared__ __align__(128) uint8_t smem_raw[];
+    if (ONLINE) {
+        TAB::fill(smem_raw);
+        __syncthreads();
+    }
+    const TAB T(smem_raw);
+    gather_body<ONLINE, TAB>(T, a);
+}
+
+// Up to kMultiGather independent gathers of the same shape in ONE launch
+// (blockIdx.y picks one): the trio shuffle's blinding tables of a small
+// table, which are otherwise six tiny launches that each mostly fill AES
+// tables.
+constexpr int kMultiGather = 6;
+struct GatherArgsN {
+    GatherArgs g[kMultiGather];
+};
+
+template <class TAB>
+__global__ void __launch_bounds__(kAesThreads) shuffle_gather_multi_kernel(const GatherArgsN m) {
+    extern __shared__ __align__(128) uint8_t smem_raw[];
+    TAB::fill(smem_raw);
+    __syncthreads();
+    const TAB T(smem_raw);
+    gather_body<true, TAB>(T, m.g[blockIdx.y]);
 }
 
 // The same step when every term is a precomputed matrix (the online phase
@@ -313,6 +370,18 @@ __global__ void __launch_bounds__(256) gather_matrix_kernel(const GatherArgs a, 
 // the two permutations it knows (pi12 o pi31 at P1, pi31 o pi23 at P3).
 __global__ void perm_compose_kernel(const int32_t* __restrict__ outer, const int32_t* __restrict__ inner,
                                     int64_t n, int32_t* __restrict__ out) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
+        out[i] = __ldg(inner + __ldg(outer + i));
+}
+
+// k1 = pi12 o pi31 and k3 = pi31 o pi23 of one small shuffle in one launch
+__global__ void perm_compose2_kernel(const int32_t* __restrict__ o0, const int32_t* __restrict__ i0,
+                                     int32_t* __restrict__ r0, const int32_t* __restrict__ o1,
+                                     const int32_t* __restrict__ i1, int32_t* __restrict__ r1, int64_t n) {
+    const int32_t* outer = blockIdx.y ? o1 : o0;
+    const int32_t* inner = blockIdx.y ? i1 : i0;
+    int32_t* out = blockIdx.y ? r1 : r0;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
         out[i] = __ldg(inner + __ldg(outer + i));
@@ -687,7 +756,7 @@ __global__ void __launch_bounds__(256) win_gather4_kernel(const int32_t* __restr
 // separated by __syncthreads (which orders global memory inside the block).
 constexpr int64_t kPermBlockMax = 1 << 16;
 
-__global__ void __launch_bounds__(1024) perm_rounds_block_kernel(const int32_t* __restrict__ H, int32_t* R,
+__device__ __forceinline__ void perm_rounds_block_body(const int32_t* __restrict__ H, int32_t* R,
                                                                  int32_t* perm, int32_t* liveA, int32_t* liveB,
                                                                  int32_t n_live) {
     __shared__ int32_t cnt_next;
@@ -728,6 +797,17 @@ __global__ void __launch_bounds__(1024) perm_rounds_block_kernel(const int32_t* 
     }
 }
 
+__global__ void __launch_bounds__(1024) perm_rounds_block_kernel(const int32_t* __restrict__ H, int32_t* R,
+                                                                 int32_t* perm, int32_t* liveA, int32_t* liveB,
+                                                                 int32_t n_live) {
+    perm_rounds_block_body(H, R, perm, liveA, liveB, n_live);
+}
+
+__global__ void __launch_bounds__(1024) perm_rounds3_block_kernel(const PermJobs3 jobs, int32_t n_live) {
+    const PermJob& j = jobs.j[blockIdx.x];
+    perm_rounds_block_body(j.H, j.R, j.perm, j.live0, j.live1, n_live);
+}
+
 int shuffle_init() {
     OGM_CUDA_TRY(allow_big_smem(perm_draws_kernel<AesTab>, kAesTableBytes));
     OGM_CUDA_TRY(allow_big_smem(shuffle_gather_kernel<true, AesTab>, kAesTableBytes));
@@ -750,10 +830,8 @@ static int seeded_permutation_impl(const uint8_t* key, const uint8_t* label, uin
     int32_t* live[2] = {R + n, R + 2 * n};
     AesKeySched ks = make_sched(key);
     const int32_t init_cnt = (int32_t)(n - 1);
-    OGM_CUDA_TRY(cudaMemcpyAsync(&cnts[0], &init_cnt, 4, cudaMemcpyHostToDevice, st));
-    OGM_CUDA_TRY(cudaMemsetAsync(&cnts[1], 0, 4, st));
-    aes_launch(perm_draws_kernel<AesTab>, perm_draws_kernel<AesTabSmall>, n, kAesThreads, st, ks, label_be(label), index, n, H,
-                                                                        live[0], perm, R);
+    aes_launch(perm_draws_kernel<AesTab>, perm_draws_kernel<AesTabSmall>, n, kAesThreads, st, ks, label_be(label),
+               index, n, H, live[0], perm, R, cnts);
     OGM_LAUNCH_CHECK();
     if (n < 2) return OGM_OK;
     if (n <= kPermBlockMax) {
@@ -1076,9 +1154,28 @@ int ogm_gather_planned(int64_t rows, int64_t words, int64_t pitch, int64_t tile_
 // ---------------------------------------------------------------------------
 static int64_t al256(int64_t b) { return (b + 255) & ~(int64_t)255; }
 
+namespace ogm {
+// the three SHPI permutations of one small shuffle: one draws launch, one
+// rounds launch (a CTA per permutation); ws holds 3 perm workspaces
+static int seeded_permutations3_small(const uint8_t* const keys[3], const uint8_t* label, uint64_t index,
+                                      int64_t n, int32_t* const perms[3], uint8_t* ws, cudaStream_t st) {
+    PermJobs3 J{};
+    for (int q = 0; q < 3; q++) {
+        int32_t* H = (int32_t*)(ws + q * perm_ws_bytes(n) + 256);
+        J.j[q] = PermJob{make_sched(keys[q]), H, H + n, H + 2 * n, H + 3 * n, perms[q]};
+    }
+    const int64_t g = (n + kAesSmallThreads - 1) / kAesSmallThreads;
+    perm_draws3_kernel<AesTabSmall><<<dim3((unsigned)(g > 0 ? g : 1), 3), kAesSmallThreads, kAesSmallBytes, st>>>(
+        J, label_be(label), index, n);
+    if (n >= 2) perm_rounds3_block_kernel<<<3, 1024, 0, st>>>(J, (int32_t)(n - 1));
+    OGM_LAUNCH_CHECK();
+    return OGM_OK;
+}
+}  // namespace ogm
+
 int64_t ogm_trio_shuffle_workspace_bytes(int64_t rows, int64_t pitch) {
     if (rows <= 0) return 256;
-    return 5 * al256(rows * 4) + al256(ogm_perm_workspace_bytes(rows)) + 7 * al256(rows * pitch * 4);
+    return 5 * al256(rows * 4) + 3 * al256(ogm_perm_workspace_bytes(rows)) + 7 * al256(rows * pitch * 4);
 }
 
 int ogm_trio_shuffle(const uint8_t* s12, const uint8_t* s23, const uint8_t* s31, uint64_t tid, int64_t rows,
@@ -1100,7 +1197,7 @@ int ogm_trio_shuffle(const uint8_t* s12, const uint8_t* s23, const uint8_t* s31,
     int32_t* pi31 = (int32_t*)take(rows * 4);
     int32_t* k1 = (int32_t*)take(rows * 4);
     int32_t* k3 = (int32_t*)take(rows * 4);
-    void* pws = take(ogm_perm_workspace_bytes(rows));
+    void* pws = take(3 * al256(ogm_perm_workspace_bytes(rows)));
     const int64_t tb = rows * pitch * 4;
     uint32_t *u = (uint32_t*)take(tb), *v = (uint32_t*)take(tb), *wm = (uint32_t*)take(tb), *z = (uint32_t*)take(tb);
     uint32_t *x1 = (uint32_t*)take(tb), *y1 = (uint32_t*)take(tb), *c1 = (uint32_t*)take(tb);
@@ -1108,16 +1205,62 @@ int ogm_trio_shuffle(const uint8_t* s12, const uint8_t* s23, const uint8_t* s31,
     int rc;
 #define OGM_TRY(x) \
     if ((rc = (x)) != OGM_OK) return rc
-    OGM_TRY(ogm_seeded_permutation(s12, kPi, tid, rows, pi12, pws, stream));
-    OGM_TRY(ogm_seeded_permutation(s23, kPi, tid, rows, pi23, pws, stream));
-    OGM_TRY(ogm_seeded_permutation(s31, kPi, tid, rows, pi31, pws, stream));
-    OGM_TRY(ogm_perm_compose(rows, pi31, pi12, k1, stream));
-    OGM_TRY(ogm_perm_compose(rows, pi23, pi31, k3, stream));
+    OGM_ENSURE_INIT();
+    const bool small = rows <= kPermBlockMax && rows <= kAesSmallMaxWork && (width_bits + 31) / 32 < 64;
+    if (small) {
+        // small tables (the trio executor's shuffles): 3 permutations per launch, all six
+        // blinding/output tables in one launch
+        const uint8_t* keys[3] = {s12, s23, s31};
+        int32_t* perms[3] = {pi12, pi23, pi31};
+        static_assert(sizeof(void*) == 8, "64-bit");
+        OGM_TRY(seeded_permutations3_small(keys, kPi, tid, rows, perms, (uint8_t*)pws, as_stream(stream)));
+    } else {
+        OGM_TRY(ogm_seeded_permutation(s12, kPi, tid, rows, pi12, pws, stream));
+        OGM_TRY(ogm_seeded_permutation(s23, kPi, tid, rows, pi23, pws, stream));
+        OGM_TRY(ogm_seeded_permutation(s31, kPi, tid, rows, pi31, pws, stream));
+    }
+    if (small) {
+        perm_compose2_kernel<<<dim3((unsigned)((rows + 255) / 256), 2), 256, 0, as_stream(stream)>>>(
+            pi31, pi12, k1, pi23, pi31, k3, rows);
+        OGM_LAUNCH_CHECK();
+    } else {
+        OGM_TRY(ogm_perm_compose(rows, pi31, pi12, k1, stream));
+        OGM_TRY(ogm_perm_compose(rows, pi23, pi31, k3, stream));
+    }
     uint32_t *r1 = out[0], *r2 = out[1], *r3 = out[2];
+    const int64_t P = pitch;
+    if (small) {
+        // U = T12[k1] ^ T31[pi31], V = T12[pi12], W = T23[pi23] ^ R2, Z = T31[k3] ^ T23[pi23] ^ R1, R1, R2:
+        // the same six gathers as below, blockIdx.y-indexed in one launch
+        GatherArgsN m{};
+        auto base = [&](GatherArgs& a, uint32_t* o) {
+            a.out = o;
+            a.rows = rows;
+            a.W = W;
+            a.width = width_bits;
+            a.row0 = 0;
+            a.pitch = P;
+        };
+        auto term = [&](GatherTerm& g, const uint8_t* key, const uint8_t* label) { set_term(g, key, label, tid, nullptr); };
+        GatherArgs* g = m.g;
+        base(g[0], u); g[0].P2 = pi31; g[0].P1 = pi12; term(g[0].t1, s12, kTb); term(g[0].t2, s31, kTb);
+        base(g[1], v); g[1].P1 = pi12; term(g[1].t1, s12, kTb);
+        base(g[2], wm); g[2].P1 = pi23; term(g[2].t1, s23, kTb); term(g[2].r, s12, kRd);
+        base(g[3], z); g[3].P2 = pi23; g[3].P1 = pi31; term(g[3].t1, s31, kTb); term(g[3].t2, s23, kTb);
+        term(g[3].r, s31, kRd);
+        base(g[4], r1); term(g[4].r, s31, kRd);
+        base(g[5], r2); term(g[5].r, s12, kRd);
+        const int64_t work = rows * ((P + 3) / 4);
+        const int64_t gx = (work + kAesSmallThreads - 1) / kAesSmallThreads;
+        shuffle_gather_multi_kernel<AesTabSmall><<<dim3((unsigned)(gx > 0 ? gx : 1), kMultiGather), kAesSmallThreads,
+                                                   kAesSmallBytes, as_stream(stream)>>>(m);
+        OGM_LAUNCH_CHECK();
+    } else {
     OGM_TRY(ogm_prf_rows(s31, kRd, tid, rows, width_bits, pitch, r1, stream));
     OGM_TRY(ogm_prf_rows(s12, kRd, tid, rows, width_bits, pitch, r2, stream));
-    const int64_t P = pitch;
-    if (W >= 64) {
+    }
+    if (small) {
+    } else if (W >= 64) {
         // wide rows: each blinding table once at the AES rate, then streaming combines
         uint32_t *t12 = x1, *t31 = y1, *t23 = c1;  // scratch until the online steps
         OGM_TRY(ogm_prf_rows(s12, kTb, tid, rows, width_bits, pitch, t12, stream));
