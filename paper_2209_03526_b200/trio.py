@@ -105,6 +105,61 @@ class TrioResult:
     subgraphs: list
     opened_flags: list = field(default_factory=list)
 
+    def open(self, schema):
+        """engine.open_results(self.party_results()[:2], schema) -- the same
+        (matches, details) -- straight from the record batches: ONE
+        device-to-host copy of every batch matrix of the three components, then
+        vectorised XOR and one-hot decoding per batch (src/engine.py:458-500)."""
+        slots = self.structure["slots"]
+        order, mats = [], []
+        for s, slot in enumerate(slots):
+            names = sorted({p["attr"] for p in slot["preds"]})
+            seen = {}
+            for batch, _ in self.records[s]:
+                if id(batch) in seen:
+                    continue
+                seen[id(batch)] = batch
+                fields = [("id", batch.ids, batch.id_width)] + [(a, batch.attrs[a], batch.attr_widths[a])
+                                                                 for a in names]
+                for name, comps, width in fields:
+                    order.append((s, id(batch), name, comps[0].shape))
+                    mats += [c.reshape(-1) for c in comps]
+        host = torch.cat(mats).cpu().numpy().view(np.uint32) if mats else np.zeros(0, np.uint32)
+        plain, off = {}, 0
+        for s, bid, name, shape in order:
+            n = int(np.prod(shape))
+            c = [host[off + q * n: off + (q + 1) * n].reshape(shape) for q in range(3)]
+            off += 3 * n
+            x = c[0] ^ c[1] ^ c[2]
+            weight = np.bitwise_count(x).sum(axis=1) if x.size else np.zeros(shape[0], np.int64)
+            if (weight > 1).any():
+                raise ValueError(f"expected Hamming weight <= 1, got {int(weight[weight > 1][0])}")
+            word = np.argmax(x != 0, axis=1) if x.size else np.zeros(shape[0], np.int64)
+            val = x[np.arange(shape[0]), word] if x.size else np.zeros(shape[0], np.uint32)
+            hot = word * 32 + np.log2(np.maximum(val, 1)).astype(np.int64)
+            plain[(s, bid, name)] = [None if w == 0 else int(h) for w, h in zip(weight, hot)]
+        decoded = []
+        for s, slot in enumerate(slots):
+            ts = schema.types[slot["type"]]
+            names = sorted({p["attr"] for p in slot["preds"]})
+            out = []
+            for batch, i in self.records[s]:
+                hot = plain[(s, id(batch), "id")][i]
+                attrs = {}
+                for a in names:
+                    idx = plain[(s, id(batch), a)][i]
+                    attrs[a] = None if idx is None else ts.attrs[a].values[idx]
+                out.append((None if hot is None else ts.ext_ids[hot], attrs))
+            decoded.append(out)
+        matches, details = [], []
+        for combo in self.subgraphs:
+            ids = tuple(decoded[s][ri][0] for s, ri in enumerate(combo))
+            if any(v is None for v in ids):
+                continue
+            matches.append(ids)
+            details.append([decoded[s][ri] for s, ri in enumerate(combo)])
+        return matches, details
+
     def party_results(self) -> list:
         """Per-party MatchResultSet views (same layout as engine.sec_match)."""
         out = []

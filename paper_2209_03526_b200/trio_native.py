@@ -145,6 +145,7 @@ def match_native(trio, tokens: list, gshares: list, any_mode: str = "or"):
 
     tnames, tindex, anames, types = _type_tables(gshares)
     sarr = (Slot * len(slots))()
+    fde_jobs: list = []   # (preds, pred, pass, key positions, keys, domain): expanded after the loop
     for s, slot in enumerate(slots):
         vtype = slot["type"]
         ts = schema.types[vtype]
@@ -162,15 +163,8 @@ def match_native(trio, tokens: list, gshares: list, any_mode: str = "or"):
                 by_kind: dict = {}
                 for i, k in enumerate(keys):
                     by_kind.setdefault(fss.is_comparison(k), []).append(i)
-                rows = [None] * 6
                 for idxs in by_kind.values():
-                    fd = fss.full_domain(fss.KeyBatch.from_keys([keys[i] for i in idxs], trio.dev), domain)
-                    keep.append(fd)
-                    for j, i in enumerate(idxs):
-                        rows[i] = fd[j]
-                for q in range(3):
-                    for ab in range(2):
-                        preds[pi].ind[ps * 6 + q * 2 + ab] = rows[2 * q + ab].data_ptr()
+                    fde_jobs.append((preds, pi, ps, idxs, [keys[i] for i in idxs], domain))
         unique_route = (len(slot["preds"]) == 1 and slot["preds"][0]["kind"] == fss.KIND_EQ
                         and ts.attrs[slot["preds"][0]["attr"]].unique)
         nd = (_i32 * max(1, len(needed)))(*[anames[vtype].index(a) for a in needed])
@@ -187,6 +181,31 @@ def match_native(trio, tokens: list, gshares: list, any_mode: str = "or"):
         sarr[s].needed = nd
         sarr[s].nchildren = len(slot["children"])
         sarr[s].children = ch
+
+    # every predicate pass's key batches: ONE host image, ONE host-to-device copy, then the
+    # full-domain expansions (src/fss.py:302-337) straight from device slices
+    images, offs, total = [], [], 0
+    for *_, ks, _ in fde_jobs:
+        img = fss.pack_keys(ks, ks[0].domain_bits)
+        offs.append(total)
+        images.append(img)
+        total += (img.size + 15) // 16 * 16
+    if fde_jobs:
+        host = np.zeros(total, np.uint8)
+        for img, o in zip(images, offs):
+            host[o: o + img.size] = img
+        dev = torch.from_numpy(host).to(trio.dev)
+        keep.append(dev)
+        for (preds, pi, ps, idxs, ks, domain), o in zip(fde_jobs, offs):
+            n, bits = len(ks), ks[0].domain_bits
+            a, b = 16 * n, 16 * n * (1 + bits)
+            d = dev[o: o + b + 13 * n]
+            kb = fss.KeyBatch(_lib.KIND_DCF if fss.is_comparison(ks[0]) else _lib.KIND_DPF, bits, d[:a].view(n, 16),
+                              d[a:b].view(bits, n, 16), d[b:b + 12 * n].view(torch.int32).view(3, n), d[b + 12 * n:])
+            fd = fss.full_domain(kb, domain)
+            keep.append(fd)
+            for j, i in enumerate(idxs):   # key i of the pass: party i // 2, share i % 2 (a, b)
+                preds[pi].ind[ps * 6 + i] = fd[j].data_ptr()
 
     seeds = [ctypes.create_string_buffer(bytes(x), 16) for x in (*trio.k, trio.s12, trio.s23, trio.s31)]
     keep.append(seeds)

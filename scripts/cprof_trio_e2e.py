@@ -24,7 +24,7 @@ tokens = list(gen_token(load_query(q, schema), schema, rng))
 
 def one():
     res = Trio(b"\x5a" * 16).match(tokens, d)
-    return open_results(res.party_results()[:2], schema)
+    return res.open(schema)
 
 
 for _ in range(5):

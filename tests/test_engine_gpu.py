@@ -308,8 +308,9 @@ def test_trio_fast_path_matches_reference(golden, name, native):
     dshares = device_trio(shares)
     res = Trio(bytes.fromhex(rec["master"])).match(list(tokens), list(dshares), any_mode=rec["mode"], native=native)
     results = res.party_results()
-    matches, _ = open_results(results[:2], schema)
+    matches, details = open_results(results[:2], schema)
     assert sorted(list(m) for m in set(matches)) == rec["matches"]
+    assert res.open(schema) == (matches, details)  # the batched reconstruction
     assert [list(sg) for sg in res.subgraphs] == rec["subgraphs"]
     for p, r in enumerate(results):
         for s, recs in enumerate(r.records):

@@ -366,6 +366,7 @@ def test_trio_path_equals_per_party_on_edge_cases(text, qtext, mode):
     tres = tr.match(list(tokens2), list(device_trio(shares)), any_mode=mode)
     views = tres.party_results()
     assert set(open_results(views[:2], schema2)[0]) == got
+    assert tres.open(schema2) == open_results(views[:2], schema2)
     assert [(lbl, v.to_bits().tolist()) for lbl, v in tr.opened] == \
         [(lbl, v.to_bits().tolist()) for lbl, v in rts[0].opened]
     for q in range(3):
@@ -446,7 +447,9 @@ def test_random_corpus_equals_oracle_both_paths():
         assert set(open_results(res[:2], schema)[0]) == want, (trial, qtext)
         tr = Trio(master)
         tres = tr.match(list(tokens), list(d))
-        assert set(open_results(tres.party_results()[:2], schema)[0]) == want, (trial, qtext)
+        opened = open_results(tres.party_results()[:2], schema)
+        assert set(opened[0]) == want, (trial, qtext)
+        assert tres.open(schema) == opened, (trial, qtext)
         assert [v.to_bits().tolist() for _, v in tr.opened] == [v.to_bits().tolist() for _, v in rts[0].opened]
         nonempty += bool(want)
     assert nonempty >= 5
