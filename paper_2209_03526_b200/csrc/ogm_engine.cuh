@@ -349,7 +349,7 @@ struct Zs3Args {
 };
 
 template <class TAB = AesTab>
-__global__ void __launch_bounds__(kAesThreads) zero_share3_kernel(const Zs3Args a, uint32_t label_be,
+__global__ void __launch_bounds__(kAesThreads) zero_share3_kernel(const __grid_constant__ Zs3Args a, uint32_t label_be,
                                                                    int64_t nwords, int64_t nbits, int64_t w0,
                                                                    int64_t nloc, int64_t row_words,
                                                                    uint32_t row_tail) {
@@ -785,7 +785,7 @@ struct ExtractJobs {
     int64_t spitch, n;
 };
 
-__global__ void extract_field_multi_kernel(const ExtractJobs J) {
+__global__ void extract_field_multi_kernel(const __grid_constant__ ExtractJobs J) {
     const ExtractJob& e = J.j[blockIdx.y];
     const int64_t ow = (e.width + 31) >> 5;
     const int64_t total = J.n * e.opitch;

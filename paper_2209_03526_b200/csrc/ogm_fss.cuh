@@ -239,7 +239,7 @@ __global__ void __launch_bounds__(kFssThreads) fss_fde_kernel(
 // ---------------------------------------------------------------------------
 template <bool ZERO, class TAB = AesTab>
 __global__ void __launch_bounds__(kFssThreads) prf_words_kernel(
-    AesKeySched k1, AesKeySched k2, uint32_t label_be, uint64_t index, uint64_t first_word,
+    const __grid_constant__ AesKeySched k1, const __grid_constant__ AesKeySched k2, uint32_t label_be, uint64_t index, uint64_t first_word,
     int64_t nwords, int64_t nbits, const uint32_t* __restrict__ xor_into, uint32_t* __restrict__ out) {
     OGM_AES_PROLOGUE_T(TAB);
     const uint64_t b0 = first_word >> 2;
@@ -276,7 +276,7 @@ __global__ void __launch_bounds__(kFssThreads) prf_words_kernel(
 // blocks per chunk when W is not a multiple of 4).
 // ---------------------------------------------------------------------------
 template <class TAB = AesTab>
-__global__ void __launch_bounds__(kFssThreads) prf_rows_kernel(AesKeySched k, uint32_t label_be, uint64_t index,
+__global__ void __launch_bounds__(kFssThreads) prf_rows_kernel(const __grid_constant__ AesKeySched k, uint32_t label_be, uint64_t index,
                                                                int64_t rows, int64_t W, uint32_t tail,
                                                                int64_t pitch, uint32_t* __restrict__ out) {
     OGM_AES_PROLOGUE_T(TAB);

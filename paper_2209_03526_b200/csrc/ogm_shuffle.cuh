@@ -55,7 +55,7 @@ __device__ __forceinline__ void perm_draws_body(const TAB& T, const AesKeySched&
 
 template <class TAB = AesTab>
 __global__ void __launch_bounds__(kAesThreads) perm_draws_kernel(
-    AesKeySched key, uint32_t label_be, uint64_t index, int64_t n, int32_t* __restrict__ H,
+    const __grid_constant__ AesKeySched key, uint32_t label_be, uint64_t index, int64_t n, int32_t* __restrict__ H,
     int32_t* __restrict__ live, int32_t* __restrict__ perm, int32_t* __restrict__ R, int32_t* __restrict__ cnts) {
     extern __shared__ __align__(128) uint8_t smem_raw[];
     TAB::fill(smem_raw);
@@ -80,7 +80,7 @@ struct PermJobs3 {
 };
 
 template <class TAB>
-__global__ void __launch_bounds__(kAesThreads) perm_draws3_kernel(const PermJobs3 jobs, uint32_t label_be,
+__global__ void __launch_bounds__(kAesThreads) perm_draws3_kernel(const __grid_constant__ PermJobs3 jobs, uint32_t label_be,
                                                                   uint64_t index, int64_t n) {
     extern __shared__ __align__(128) uint8_t smem_raw[];
     TAB::fill(smem_raw);
@@ -262,7 +262,7 @@ __device__ __forceinline__ void gather_body(const TAB& T, const GatherArgs& a) {
 }
 
 template <bool ONLINE, class TAB = AesTab>
-__global__ void __launch_bounds__(kAesThreads) shuffle_gather_kernel(const GatherArgs a) {
+__global__ void __launch_bounds__(kAesThreads) shuffle_gather_kernel(const __grid_constant__ GatherArgs a) {
     extern __shared__ __align__(128) uint8_t smem_raw[];
     if (ONLINE) {
         TAB::fill(smem_raw);
@@ -282,7 +282,7 @@ struct GatherArgsN {
 };
 
 template <class TAB>
-__global__ void __launch_bounds__(kAesThreads) shuffle_gather_multi_kernel(const GatherArgsN m) {
+__global__ void __launch_bounds__(kAesThreads) shuffle_gather_multi_kernel(const __grid_constant__ GatherArgsN m) {
     extern __shared__ __align__(128) uint8_t smem_raw[];
     TAB::fill(smem_raw);
     __syncthreads();
@@ -803,7 +803,7 @@ __global__ void __launch_bounds__(1024) perm_rounds_block_kernel(const int32_t* 
     perm_rounds_block_body(H, R, perm, liveA, liveB, n_live);
 }
 
-__global__ void __launch_bounds__(1024) perm_rounds3_block_kernel(const PermJobs3 jobs, int32_t n_live) {
+__global__ void __launch_bounds__(1024) perm_rounds3_block_kernel(const __grid_constant__ PermJobs3 jobs, int32_t n_live) {
     const PermJob& j = jobs.j[blockIdx.x];
     perm_rounds_block_body(j.H, j.R, j.perm, j.live0, j.live1, n_live);
 }
