@@ -345,6 +345,44 @@ def run_funcs(args):
     line("a10", "src/rss.py:143-148", "zero shares, 3 parties per launch", "GB/s of shares",
          3 * nbits / 8 / t / 1e9, 3 * nbits, (1 << 24) / 8 / tc / 1e9, 1 << 24, eq, "AES-CTR 0.33 GB/s")
     del outs
+    # a11 and_terms (src/rss.py:115-126), three parties per launch: z_q = a_q b_q ^ a_q b_q+1 ^ a_q+1 b_q
+    nw = 1 << 26
+    va = [torch.randint(-2**31, 2**31 - 1, (nw,), dtype=torch.int32, device=dev, generator=gen) for _ in range(3)]
+    vb = [torch.randint(-2**31, 2**31 - 1, (nw,), dtype=torch.int32, device=dev, generator=gen) for _ in range(3)]
+    zo = [torch.empty_like(va[0]) for _ in range(3)]
+    nx = [1, 2, 0]
+    args = (A([va[q] for q in range(3)]), A([va[nx[q]] for q in range(3)]), A([vb[q] for q in range(3)]),
+            A([vb[nx[q]] for q in range(3)]), A(zo))
+    t = timed(lambda: _lib.call("ogm_and_terms", nw, 3, *args, _lib.stream_ptr()))
+    ns = 1 << 22
+    ha = [v[:ns].cpu().numpy().view(np.uint32) for v in va]
+    hb = [v[:ns].cpu().numpy().view(np.uint32) for v in vb]
+    tc, ref = cpu(lambda: (ha[0] & hb[0]) ^ (ha[0] & hb[1]) ^ (ha[1] & hb[0]))
+    eq = bool(np.array_equal(zo[0][:ns].cpu().numpy().view(np.uint32), ref))
+    line("a11", "src/rss.py:115-126", "and_terms, 3 parties per launch (6 input + 3 output vectors)", "GB/s",
+         9 * 4 * nw / t / 1e9, 32 * nw, 5 * 4 * ns / tc / 1e9, 32 * ns, eq, "negligible")
+    del va, vb, zo
+    # a12 Case I fold (src/engine.py:95-102,197-217), 3 parties: out_q = XOR_c fa_q(c)(A_q^B_q)[c] ^ fb_q(c) A_q[c]
+    rows, words = 200_000, 1024
+    comps = [torch.randint(-2**31, 2**31 - 1, (rows, words), dtype=torch.int32, device=dev, generator=gen)
+             for _ in range(3)]
+    fl = [torch.randint(-2**31, 2**31 - 1, ((rows + 31) // 32,), dtype=torch.int32, device=dev, generator=gen)
+          for _ in range(3)]
+    fo = [torch.empty((words,), dtype=torch.int32, device=dev) for _ in range(3)]
+    fargs = (A(comps), A([comps[nx[q]] for q in range(3)]), A(fl), A([fl[nx[q]] for q in range(3)]), A(fo))
+    t = timed(lambda: _lib.call("ogm_select_fold", rows, words, words, 3, *fargs, _lib.stream_ptr()))
+    rs = 2048
+    _lib.call("ogm_select_fold", rs, words, words, 3, *fargs, _lib.stream_ptr())
+    hA = comps[0][:rs].cpu().numpy().view(np.uint32)
+    hB = comps[1][:rs].cpu().numpy().view(np.uint32)
+    bits_a = np.unpackbits(fl[0][:rs // 32].cpu().numpy().view(np.uint8), bitorder="little").astype(bool)
+    bits_b = np.unpackbits(fl[1][:rs // 32].cpu().numpy().view(np.uint8), bitorder="little").astype(bool)
+    tc, ref = cpu(lambda: np.bitwise_xor.reduce(np.where(bits_a[:, None], hA ^ hB, 0)
+                                               ^ np.where(bits_b[:, None], hA, 0), axis=0))
+    eq = bool(np.array_equal(fo[0].cpu().numpy().view(np.uint32), ref))
+    line("a12", "src/engine.py:95-102", "Case I fold (select_fold, 3 parties, 200K x 1024-word rows)", "GB/s",
+         3 * rows * words * 4 / t / 1e9, rows, 2 * rs * words * 4 / tc / 1e9, rs, eq, "small")
+    del comps, fl, fo
 
 
 # ---------------------------------------------------------------------------
