@@ -174,7 +174,13 @@ class KeyBatch:
         n = len(keys)
         buf = pack_keys(keys, bits)
         a, b = 16 * n, 16 * n * (1 + bits)
-        d = torch.from_numpy(buf).to(torch.device(device))
+        dev = torch.device(device)
+        host = torch.from_numpy(buf)
+        if dev.type == "cuda":
+            # pinned + non-blocking: a pageable copy would synchronise the stream on every batch
+            d = host.pin_memory().to(dev, non_blocking=True)
+        else:
+            d = host.to(dev)
         return cls(_lib.KIND_DCF if comp else _lib.KIND_DPF, bits, d[:a].view(n, 16), d[a:b].view(bits, n, 16),
                    d[b:b + 12 * n].view(torch.int32).view(3, n), d[b + 12 * n:])
 

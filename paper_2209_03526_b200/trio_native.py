@@ -194,7 +194,7 @@ def match_native(trio, tokens: list, gshares: list, any_mode: str = "or"):
         host = np.zeros(total, np.uint8)
         for img, o in zip(images, offs):
             host[o: o + img.size] = img
-        dev = torch.from_numpy(host).to(trio.dev)
+        dev = torch.from_numpy(host).pin_memory().to(trio.dev, non_blocking=True)
         keep.append(dev)
         for (preds, pi, ps, idxs, ks, domain), o in zip(fde_jobs, offs):
             n, bits = len(ks), ks[0].domain_bits
