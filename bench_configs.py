@@ -494,7 +494,7 @@ def run_c5(args):
         def online(pre: bool, marks=None):
             # the four party-local steps of src/shuffle.py:106-143 in protocol order
             if pre and fused and marks is None:
-                shuffle_online_fused(off, comps[0], comps[1], comps[2], x1, y1, c1, r3)
+                shuffle_online_fused(off, comps[0], comps[1], comps[2], x1, y1, None, r3)
                 return
             if pre and marks is None:
                 # x1, y1, c1 handed over in shared memory; their buffers are the scratch

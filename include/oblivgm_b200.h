@@ -340,9 +340,10 @@ int ogm_trio_open_keep(const uint32_t* const* comps, int64_t rows, int64_t pitch
 /* The online phase of one 3-party shuffle with prepared material (composed
  * permutations k1 = pi12 o pi31, k3 = pi31 o pi23; permuted combined blinds
  * U, V, W, Z as in shuffle.ShuffleOffline) for 16-byte rows, all four party
- * steps of src/shuffle.py:106-143 in one cooperative launch (three
- * grid-synchronised phases; every message is still written): x1, y1, c1 and
- * the new component r3.  For tables that fit L2 (launch-bound sizes). */
+ * steps of src/shuffle.py:106-143 in one cooperative launch (two
+ * grid-synchronised phases): x1, y1, c1 (optional, may be NULL: it feeds R3
+ * at the same index) and the new component r3.  For tables that fit L2
+ * (launch-bound sizes). */
 int ogm_shuffle_online_fused(int64_t rows, const int32_t* k1, const int32_t* pi12, const int32_t* pi23,
                              const int32_t* k3, const uint32_t* a, const uint32_t* b, const uint32_t* c,
                              const uint32_t* U, const uint32_t* V, const uint32_t* W, const uint32_t* Z, uint32_t* x1,

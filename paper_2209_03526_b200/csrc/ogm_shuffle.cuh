@@ -895,11 +895,13 @@ __global__ void __launch_bounds__(256) shuffle_online_coop_kernel(const Shuffle4
         p.y1[i] = ogm::xor4(__ldcg(p.c + j), __ldcs(p.V + i));
     }
     grid.sync();
-    for (int64_t i = t0; i < p.rows; i += stride)
-        p.c1[i] = ogm::xor4(__ldcg(p.x1 + __ldg(p.pi23 + i)), __ldcs(p.W + i));
-    grid.sync();
-    for (int64_t i = t0; i < p.rows; i += stride)
-        p.r3[i] = ogm::xor4(ogm::xor4(__ldcg(p.y1 + __ldg(p.k3 + i)), __ldcg(p.c1 + i)), __ldcs(p.Z + i));
+    // c1 (P2 -> P3) feeds R3 at the same index: one phase, c1 kept in registers (stored only
+    // when the caller wants the message)
+    for (int64_t i = t0; i < p.rows; i += stride) {
+        const uint4 c = ogm::xor4(__ldcg(p.x1 + __ldg(p.pi23 + i)), __ldcs(p.W + i));
+        if (p.c1) p.c1[i] = c;
+        p.r3[i] = ogm::xor4(ogm::xor4(__ldcg(p.y1 + __ldg(p.k3 + i)), c), __ldcs(p.Z + i));
+    }
 }
 
 extern "C" {
@@ -1376,9 +1378,10 @@ int ogm_shuffle_online_fused(int64_t rows, const int32_t* k1, const int32_t* pi1
                              uint32_t* y1, uint32_t* c1, uint32_t* r3, void* stream) {
     using namespace ogm;
     OGM_CHECK_ARG(rows >= 0 && rows < ((int64_t)1 << 31), OGM_ERR_ARG, "rows out of range");
-    const void* ptrs[] = {a, b, c, U, V, W, Z, x1, y1, c1, r3};
+    const void* ptrs[] = {a, b, c, U, V, W, Z, x1, y1, r3};
     for (const void* q : ptrs)
         OGM_CHECK_ARG(q && (((uintptr_t)q) & 15) == 0, OGM_ERR_ARG, "16-byte aligned tables are required");
+    OGM_CHECK_ARG((((uintptr_t)c1) & 15) == 0, OGM_ERR_ARG, "16-byte aligned tables are required");
     OGM_CHECK_ARG(k1 && pi12 && pi23 && k3, OGM_ERR_ARG, "permutations are required");
     if (rows == 0) return OGM_OK;
     OGM_ENSURE_INIT();

@@ -488,6 +488,9 @@ def test_shuffle_online_fused_equals_party_steps(rows):
     off[2].step_r3(want[1], want[2], want[3])
     got = [e() for _ in range(4)]
     shuffle_online_fused(off, comps[0], comps[1], comps[2], *got)
+    r3_only = torch.empty_like(got[3])
+    shuffle_online_fused(off, comps[0], comps[1], comps[2], got[0], got[1], None, r3_only)
+    assert torch.equal(r3_only, want[3])
     for g_, w_ in zip(got, want):
         assert torch.equal(g_, w_)
 
