@@ -195,11 +195,14 @@ def test_open_label_guard_and_and_gate():
     assert rss.reconstruct(z) == (a & b)
 
 
-@pytest.mark.parametrize("words,rows", [(11, 70), (64, 1000), (100, 333), (5691, 2048)])
+@pytest.mark.parametrize("words,rows", [(11, 70), (64, 1000), (100, 333), (5691, 2048), (313, 2013), (129, 4097),
+                                        (1024, 77), (1025, 100)])
 @pytest.mark.parametrize("npass", [1, 2])
 def test_masked_parity_kernels_vs_oracle(words, rows, npass):
-    """Both kernel paths (unaligned G-lane, aligned register-indicator) for
-    per-party and trio launches against the oracle's src/engine.py:76-80."""
+    """Every kernel path (unaligned G-lane; aligned TMA-staged rows up to 1024
+    words, with ragged stages and any warp-column count; aligned
+    register-indicator beyond) for per-party and trio launches against the
+    oracle's src/engine.py:76-80."""
     import oracle
     from paper_2209_03526_b200 import _lib
     from paper_2209_03526_b200.graphs import padded_device_matrix
