@@ -32,7 +32,9 @@ class DBits:
         if words.numel() != words_for(logical_len):
             raise ValueError(f"expected {words_for(logical_len)} words for {logical_len} bits, "
                              f"got {words.numel()}")
-        self.words = words.reshape(-1)
+        # a torch call here is a GIL hand-off point for the three party threads: skip it when the
+        # words are already a flat vector
+        self.words = words if words.dim() == 1 else words.reshape(-1)
         self.logical_len = logical_len
 
     @classmethod
