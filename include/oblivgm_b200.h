@@ -194,6 +194,12 @@ int ogm_masked_parity(int64_t rows, int64_t words, int64_t pitch, int ncomp, con
                       int nparty, const int32_t* a_idx, const int32_t* b_idx, int npass,
                       const uint32_t* const* ind, uint32_t* const* out, void* stream);
 
+/* The same, XORed into out (which the caller initialised, e.g. with the
+ * pass's zero share) instead of overwriting it: no zeroing launches. */
+int ogm_masked_parity_acc(int64_t rows, int64_t words, int64_t pitch, int ncomp, const uint32_t* const* comps,
+                          int nparty, const int32_t* a_idx, const int32_t* b_idx, int npass,
+                          const uint32_t* const* ind, uint32_t* const* out, void* stream);
+
 /* src/engine.py:95-102 _select_one_additive for nparty parties (Case I
  * fetch, src/engine.py:197-217, and the posting fold of sec_access,
  * src/engine.py:309-311): out[q] (words) = XOR over rows c of

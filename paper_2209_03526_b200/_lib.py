@@ -55,6 +55,7 @@ SIGNATURES = {
     "ogm_and_terms": ([_i64, _int, _vp, _vp, _vp, _vp, _vp, _vp], _int),
     "ogm_xor_words": ([_i64, _vp, _vp, _vp, _vp, _vp], _int),
     "ogm_masked_parity": ([_i64, _i64, _i64, _int, _vp, _int, _vp, _vp, _int, _vp, _vp, _vp], _int),
+    "ogm_masked_parity_acc": ([_i64, _i64, _i64, _int, _vp, _int, _vp, _vp, _int, _vp, _vp, _vp], _int),
     "ogm_select_fold": ([_i64, _i64, _i64, _int, _vp, _vp, _vp, _vp, _vp, _vp], _int),
     "ogm_select_many": ([_i64, _i64, _i64, _i64, _vp, _vp, _i64, _vp, _vp, _vp, _i64, _vp, _vp], _int),
     "ogm_pack_fields": ([_i64, _vp, _int, _vp, _vp, _vp, _vp, _i64, _vp], _int),

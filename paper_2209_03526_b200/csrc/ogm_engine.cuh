@@ -36,6 +36,7 @@ struct ParityArgs {
     uint32_t* out[kMaxPass * kMaxParty];
     int a_idx[kMaxParty], b_idx[kMaxParty];
     int ncomp, nparty, npass, G;
+    int acc;  // XOR the parities into out (caller-initialised) instead of overwriting it
     int64_t rows, words, pitch;
 };
 
@@ -117,7 +118,7 @@ __global__ void __launch_bounds__(256) masked_parity_kernel(const ParityArgs p) 
         }
         if (lane == 0) {
 #pragma unroll
-            for (int j = 0; j < NJ; j++) p.out[j][tile] = outw[j];
+            for (int j = 0; j < NJ; j++) p.out[j][tile] = p.acc ? p.out[j][tile] ^ outw[j] : outw[j];
         }
     }
 }
@@ -952,12 +953,10 @@ static int grid_for(int64_t work, int threads = 256) {
 // ===========================================================================
 // C ABI
 // ===========================================================================
-extern "C" {
-
-int ogm_masked_parity(int64_t rows, int64_t words, int64_t pitch, int ncomp, const uint32_t* const* comps,
-                      int nparty, const int32_t* a_idx, const int32_t* b_idx, int npass,
-                      const uint32_t* const* ind, uint32_t* const* out, void* stream) {
-    using namespace ogm;
+namespace ogm {
+static int masked_parity_impl(int64_t rows, int64_t words, int64_t pitch, int ncomp, const uint32_t* const* comps,
+                              int nparty, const int32_t* a_idx, const int32_t* b_idx, int npass,
+                              const uint32_t* const* ind, uint32_t* const* out, bool acc, void* stream) {
     OGM_CHECK_ARG(rows >= 0 && words >= 0 && pitch >= words, OGM_ERR_ARG, "bad matrix shape");
     OGM_CHECK_ARG((nparty == 1 && ncomp == 2) || (nparty == 3 && ncomp == 3), OGM_ERR_ARG,
                   "need nparty=1 with 2 components (A, B) or nparty=3 with 3 components");
@@ -985,6 +984,7 @@ int ogm_masked_parity(int64_t rows, int64_t words, int64_t pitch, int ncomp, con
     p.ncomp = ncomp;
     p.nparty = nparty;
     p.npass = npass;
+    p.acc = acc ? 1 : 0;
     p.rows = rows;
     p.words = words;
     p.pitch = pitch;
@@ -1004,8 +1004,9 @@ int ogm_masked_parity(int64_t rows, int64_t words, int64_t pitch, int ncomp, con
         const int64_t ntile = (rows + RT - 1) / RT;
         const int G = (int)std::min<int64_t>(ntile, (int64_t)sm_count());
         const size_t smem = (size_t)(S * stage_bytes + 8 * S);
-        for (int j = 0; j < npass * nparty; j++)
-            OGM_CUDA_TRY(cudaMemsetAsync(out[j], 0, 4 * ((rows + 31) / 32), st));
+        if (!acc)
+            for (int j = 0; j < npass * nparty; j++)
+                OGM_CUDA_TRY(cudaMemsetAsync(out[j], 0, 4 * ((rows + 31) / 32), st));
 #define OGM_PARITY_TMA(NP, NS)                                                                   \
     do {                                                                                         \
         OGM_CUDA_TRY(allow_big_smem(masked_parity_tma_kernel<NP, NS>, (int)smem));               \
@@ -1035,8 +1036,9 @@ int ogm_masked_parity(int64_t rows, int64_t words, int64_t pitch, int ncomp, con
         int64_t tpb = (ntiles + row_blocks - 1) / row_blocks;
         tpb = (tpb + RG - 1) / RG * RG;
         row_blocks = (ntiles + tpb - 1) / tpb;
-        for (int j = 0; j < npass * nparty; j++)
-            OGM_CUDA_TRY(cudaMemsetAsync(out[j], 0, 4 * ntiles, st));
+        if (!acc)
+            for (int j = 0; j < npass * nparty; j++)
+                OGM_CUDA_TRY(cudaMemsetAsync(out[j], 0, 4 * ntiles, st));
         dim3 grid((unsigned)col_chunks, (unsigned)row_blocks);
 #define OGM_PARITY2(NP, NS) masked_parity_v2_kernel<NP, NS><<<grid, 32 * RG * CW, 0, st>>>(p, CW, tpb)
         if (nparty == 1 && npass == 1) OGM_PARITY2(1, 1);
@@ -1071,6 +1073,23 @@ int ogm_masked_parity(int64_t rows, int64_t words, int64_t pitch, int ncomp, con
 #undef OGM_PARITY_LAUNCH
     OGM_LAUNCH_CHECK();
     return OGM_OK;
+}
+}  // namespace ogm
+
+extern "C" {
+
+int ogm_masked_parity(int64_t rows, int64_t words, int64_t pitch, int ncomp, const uint32_t* const* comps,
+                      int nparty, const int32_t* a_idx, const int32_t* b_idx, int npass,
+                      const uint32_t* const* ind, uint32_t* const* out, void* stream) {
+    return ogm::masked_parity_impl(rows, words, pitch, ncomp, comps, nparty, a_idx, b_idx, npass, ind, out, false,
+                                   stream);
+}
+
+int ogm_masked_parity_acc(int64_t rows, int64_t words, int64_t pitch, int ncomp, const uint32_t* const* comps,
+                          int nparty, const int32_t* a_idx, const int32_t* b_idx, int npass,
+                          const uint32_t* const* ind, uint32_t* const* out, void* stream) {
+    return ogm::masked_parity_impl(rows, words, pitch, ncomp, comps, nparty, a_idx, b_idx, npass, ind, out, true,
+                                   stream);
 }
 
 static int zero_share_trio_impl(const uint8_t* k1, const uint8_t* k2, const uint8_t* k3, uint64_t counter,

@@ -91,23 +91,29 @@ def sec_eval_local_packed(comps, words: int, plan: ShardPlan, rank: int, inds, z
     nloc = hi - lo
     npass = len(inds)
     nvec = 3 * npass
-    packed = torch.zeros((nvec, max(plan.words_per_rank, 1)), dtype=torch.int32, device=comps[0].device)
+    w0, w1 = plan.word_bounds(rank)
+    wpr = max(plan.words_per_rank, 1)
+    # the zero shares are written first (they initialise the words), then the parities are
+    # XORed in: no zeroing launches; only a short last shard's padding is cleared
+    packed = torch.empty((nvec, wpr), dtype=torch.int32, device=comps[0].device)
+    if w1 - w0 < wpr:
+        packed[:, w1 - w0:].zero_()
     outs = [packed[j] for j in range(nvec)]
     A = _lib.ptr_array
-    if nloc:
-        flat = [t for ps in range(npass) for q in range(3) for t in inds[ps][q]]
-        _lib.call("ogm_masked_parity", nloc, words, comps[0].stride(0), 3, A(comps), 3,
-                  _lib.int_array([0, 1, 2]), _lib.int_array([1, 2, 0]), npass, A(flat), A(outs),
-                  _lib.stream_ptr())
-    w0, w1 = plan.word_bounds(rank)
     adds = [[outs[ps * 3 + q][: w1 - w0] for q in range(3)] for ps in range(npass)]
     k = (zero_keys[0][0], zero_keys[1][0], zero_keys[2][0])
+    none3 = A([None, None, None])
     if w1 > w0 and npass == 2:
         # both passes, all three parties: one launch (3 AES per block and pass, not 6)
         _lib.call("ogm_zero_share_trio_slice2", *k, counters[0], counters[1], plan.rows, w0, w1 - w0,
-                  A(adds[0]), A(adds[0]), A(adds[1]), A(adds[1]), _lib.stream_ptr())
+                  none3, A(adds[0]), none3, A(adds[1]), _lib.stream_ptr())
     elif w1 > w0:
-        _lib.call("ogm_zero_share_trio_slice", *k, counters[0], plan.rows, w0, w1 - w0, A(adds[0]), A(adds[0]),
+        _lib.call("ogm_zero_share_trio_slice", *k, counters[0], plan.rows, w0, w1 - w0, none3, A(adds[0]),
+                  _lib.stream_ptr())
+    if nloc:
+        flat = [t for ps in range(npass) for q in range(3) for t in inds[ps][q]]
+        _lib.call("ogm_masked_parity_acc", nloc, words, comps[0].stride(0), 3, A(comps), 3,
+                  _lib.int_array([0, 1, 2]), _lib.int_array([1, 2, 0]), npass, A(flat), A(outs),
                   _lib.stream_ptr())
     return packed
 
