@@ -391,6 +391,52 @@ __global__ void __launch_bounds__(kAesThreads) zero_share3_kernel(const __grid_c
     }
 }
 
+// The same stream for small launches (the latency-bound zero shares of C1 and
+// of a rank's secEval slice): a CTA of three warps, warp q encrypting 32
+// counter blocks under party q's key only (one AES per thread instead of
+// three, and a warp-uniform key), partners exchanged through shared memory.
+template <class TAB>
+__global__ void __launch_bounds__(96) zero_share3x_kernel(const __grid_constant__ Zs3Args a, uint32_t label_be,
+                                                          int64_t nwords, int64_t nbits, int64_t w0, int64_t nloc,
+                                                          int64_t row_words, uint32_t row_tail) {
+    extern __shared__ __align__(128) uint8_t smem_raw[];
+    TAB::fill(smem_raw);
+    uint4* xch = reinterpret_cast<uint4*>(smem_raw + TAB::kBytes);  // [3][32]
+    __syncthreads();
+    const TAB T(smem_raw);
+    const int q = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t nblk = (nloc + 3) >> 2;
+    const int64_t items = nblk * a.npass;
+    const int64_t b0 = w0 >> 2;
+    for (int64_t g = blockIdx.x; g * 32 < items; g += gridDim.x) {
+        const int64_t t = g * 32 + lane;
+        const bool valid = t < items;
+        const int ps = t >= nblk ? 1 : 0;
+        const int64_t b = t - ps * nblk;
+        uint4 f = make_uint4(0, 0, 0, 0);
+        if (valid) f = aes128_enc(T, ctr_block(label_be, a.counter[ps], (uint64_t)(b0 + b)), ParamKey{a.k[q].rk});
+        xch[q * 32 + lane] = f;
+        __syncthreads();
+        if (valid) {
+            const uint4 z = xor4(f, xch[((q + 2) % 3) * 32 + lane]);
+            const uint32_t zw[4] = {z.x, z.y, z.z, z.w};
+            const uint32_t* xin = a.xin[ps][q];
+            uint32_t* out = a.out[ps][q];
+#pragma unroll
+            for (int j = 0; j < 4; j++) {
+                const int64_t o = b * 4 + j;
+                if (o >= nloc) break;
+                uint32_t v = zw[j];
+                if (xin) v ^= xin[o];
+                if (w0 + o == nwords - 1 && (nbits & 31)) v &= (1u << (nbits & 31)) - 1u;
+                if (row_words && (w0 + o) % row_words == row_words - 1) v &= row_tail;
+                out[o] = v;
+            }
+        }
+        __syncthreads();  // xch is rewritten by the next group
+    }
+}
+
 // ---------------------------------------------------------------------------
 // src/rss.py:115-126 and_terms (per party), src/engine.py:174-189 XOR folds.
 // ---------------------------------------------------------------------------
@@ -1123,8 +1169,15 @@ static int zero_share_trio_impl(const uint8_t* k1, const uint8_t* k2, const uint
             a.out[1][q] = out2[q];
         }
     }
-    aes_launch(zero_share3_kernel<AesTab>, zero_share3_kernel<AesTabSmall>, npass * ((nloc + 3) / 4), kAesThreads,
-               as_stream(stream), a, label_be(kZshr), nwords, nbits, w0, nloc, row_words, row_tail);
+    const int64_t items = npass * ((nloc + 3) / 4);
+    if (items <= kAesSmallMaxWork) {
+        const int64_t g = (items + 31) / 32;
+        zero_share3x_kernel<AesTabSmall><<<(int)g, 96, kAesSmallBytes + 3 * 32 * 16, as_stream(stream)>>>(
+            a, label_be(kZshr), nwords, nbits, w0, nloc, row_words, row_tail);
+    } else {
+        aes_launch(zero_share3_kernel<AesTab>, zero_share3_kernel<AesTabSmall>, items, kAesThreads,
+                   as_stream(stream), a, label_be(kZshr), nwords, nbits, w0, nloc, row_words, row_tail);
+    }
     OGM_LAUNCH_CHECK();
     return OGM_OK;
 }
