@@ -387,7 +387,8 @@ def main():
         tt = torch.tensor([el], dtype=torch.float64, device="cuda")
         if world > 1:
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        h2d = sum(h.numel() * h.element_size() for h in host)
+        # bytes the call copies: a DCF's last-level seed correction is never read, so not sent
+        h2d = sum(h.numel() * h.element_size() for h in host) - (16 * K if comparison else 0)
         e2e = {"value": world * K * args.steps / float(tt.item()), "unit": UNIT,
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": hout.numel() * 4,
                "ms_per_step": 1e3 * float(tt.item()) / args.steps}

@@ -128,7 +128,8 @@ int ogm_fss_eval_points(int kind, int bits, int64_t K, const void* root, const v
 /* Same computation from HOST buffers (the end-to-end call a CPU caller
  * makes): copies keys/points in, evaluates, copies the packed bits out and
  * synchronizes.  Host buffers should be pinned for full PCIe bandwidth.
- * The transfer is chunked and overlapped with evaluation on two streams. */
+ * The transfer is chunked and overlapped with evaluation on two streams.
+ * For DCF keys the last level's seed correction (never read) is not copied. */
 int ogm_fss_eval_points_host(int kind, int bits, int64_t K, const void* root_h,
                              const void* seed_cw_h, const uint32_t* ctrl_h, const uint8_t* flags_h,
                              const uint32_t* points_h, uint32_t* out_bits_h);

@@ -202,8 +202,11 @@ int ogm_fss_eval_points_host(int kind, int bits, int64_t K, const void* root_h, 
         uint32_t* d_pts = (uint32_t*)(((uintptr_t)(d_flags + Kc) + 15) & ~(uintptr_t)15);
         uint32_t* d_out = (uint32_t*)(((uintptr_t)(d_pts + Kc) + 15) & ~(uintptr_t)15);
         OGM_CUDA_TRY(cudaMemcpyAsync(d_root, rh + 16 * k0, 16 * kc, cudaMemcpyHostToDevice, st));
-        OGM_CUDA_TRY(cudaMemcpy2DAsync(d_cw, 16 * kc, ch + 16 * k0, 16 * K, 16 * kc, bits,
-                                       cudaMemcpyHostToDevice, st));
+        // a DCF walk never reads the last level's seed correction (fss_eval_kernel): not copied
+        const int cw_levels = kind == OGM_KIND_DCF ? bits - 1 : bits;
+        if (cw_levels > 0)
+            OGM_CUDA_TRY(cudaMemcpy2DAsync(d_cw, 16 * kc, ch + 16 * k0, 16 * K, 16 * kc, cw_levels,
+                                           cudaMemcpyHostToDevice, st));
         OGM_CUDA_TRY(cudaMemcpy2DAsync(d_ctrl, 4 * kc, ctrl_h + k0, 4 * K, 4 * kc, 3, cudaMemcpyHostToDevice, st));
         OGM_CUDA_TRY(cudaMemcpyAsync(d_flags, flags_h + k0, kc, cudaMemcpyHostToDevice, st));
         OGM_CUDA_TRY(cudaMemcpyAsync(d_pts, points_h + k0, 4 * kc, cudaMemcpyHostToDevice, st));
