@@ -1,5 +1,5 @@
 """Chained online shuffle: window size of the c1 / R3 plans x dual-or-split last pass (2^lg rows).
-usage: OGM_DUAL_MAX_MB=... python scripts/exp_chain_win.py lg win_mb [win_mb ...]"""
+usage: python scripts/exp_chain_win.py lg win_mb [win_mb ...] [--all]  (--all: every plan, not just c1/R3)"""
 import statistics
 import sys
 
@@ -22,9 +22,14 @@ e = lambda: torch.empty_like(comps[0])  # noqa: E731
 want = shuffle_online_planned(off, comps[0], comps[1], comps[2], e())
 inter = [e() for _ in range(3)]
 r3 = e()
-for wmb in map(float, sys.argv[2:]):
-    off[1].plan_c1 = GatherPlan(off[1].pi23, 4, window_bytes=int(wmb * (1 << 20)))
-    off[2].plan_r3 = GatherPlan(off[2].k3, 4, window_bytes=int(wmb * (1 << 20)))
+ALL = "--all" in sys.argv
+for wmb in [float(x) for x in sys.argv[2:] if not x.startswith("--")]:
+    wb = int(wmb * (1 << 20))
+    off[1].plan_c1 = GatherPlan(off[1].pi23, 4, window_bytes=wb)
+    off[2].plan_r3 = GatherPlan(off[2].k3, 4, window_bytes=wb)
+    if ALL:  # the first two plans too (their windows feed the chained kernels)
+        off[0].plan_x1 = GatherPlan(off[0].k1, 4, window_bytes=wb)
+        off[1].plan_y1 = GatherPlan(off[1].pi12, 4, window_bytes=wb)
     fn = lambda: shuffle_online_planned(off, comps[0], comps[1], comps[2], r3, inter=inter)  # noqa: E731
     fn()
     ok = torch.equal(r3, want)
