@@ -196,16 +196,24 @@ def match_native(trio, tokens: list, gshares: list, any_mode: str = "or"):
             host[o: o + img.size] = img
         dev = torch.from_numpy(host).pin_memory().to(trio.dev, non_blocking=True)
         keep.append(dev)
-        for (preds, pi, ps, idxs, ks, domain), o in zip(fde_jobs, offs):
+        # every expansion writes into one allocation (16-byte row pitch), device pointers by offset
+        pitches = [(words_for(job[5]) + 3) // 4 * 4 for job in fde_jobs]
+        outs = torch.empty((sum(len(job[4]) * p for job, p in zip(fde_jobs, pitches)),), dtype=torch.int32,
+                           device=trio.dev)
+        keep.append(outs)
+        base, obase, oo = dev.data_ptr(), outs.data_ptr(), 0
+        stream = _lib.stream_ptr()
+        for (preds, pi, ps, idxs, ks, domain), o, pitch in zip(fde_jobs, offs, pitches):
             n, bits = len(ks), ks[0].domain_bits
+            if not 1 <= bits <= fss.MAX_DEVICE_BITS:
+                raise fss.DomainError(f"domain_bits {bits} outside 1..{fss.MAX_DEVICE_BITS}")
             a, b = 16 * n, 16 * n * (1 + bits)
-            d = dev[o: o + b + 13 * n]
-            kb = fss.KeyBatch(_lib.KIND_DCF if fss.is_comparison(ks[0]) else _lib.KIND_DPF, bits, d[:a].view(n, 16),
-                              d[a:b].view(bits, n, 16), d[b:b + 12 * n].view(torch.int32).view(3, n), d[b + 12 * n:])
-            fd = fss.full_domain(kb, domain)
-            keep.append(fd)
+            kind = _lib.KIND_DCF if fss.is_comparison(ks[0]) else _lib.KIND_DPF
+            _lib.call("ogm_fss_full_domain", kind, bits, n, base + o, base + o + a, base + o + b,
+                      base + o + b + 12 * n, domain, obase + 4 * oo, pitch, stream)
             for j, i in enumerate(idxs):   # key i of the pass: party i // 2, share i % 2 (a, b)
-                preds[pi].ind[ps * 6 + i] = fd[j].data_ptr()
+                preds[pi].ind[ps * 6 + i] = obase + 4 * (oo + j * pitch)
+            oo += n * pitch
 
     seeds = [ctypes.create_string_buffer(bytes(x), 16) for x in (*trio.k, trio.s12, trio.s23, trio.s31)]
     keep.append(seeds)
