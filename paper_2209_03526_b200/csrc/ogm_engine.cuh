@@ -1278,7 +1278,10 @@ int ogm_select_fold(int64_t rows, int64_t words, int64_t pitch, int nparty, cons
         // but every row group ends in one atomicXor per output word: for narrow rows
         // (Case I fold, 1024-word rows) that many groups made the fold atomic-bound
         // (200K rows: 2.7 TB/s), so a group walks at least 16 row blocks
-        if (rgroups > rblocks / 16) rgroups = rblocks / 16;
+        // (never below one resident wave's worth of threads: small folds stay latency-bound)
+        const int64_t fill = ((int64_t)sm_count() * 2048 + nch - 1) / nch;
+        const int64_t cap16 = std::max(rblocks / 16, fill);
+        if (rgroups > cap16) rgroups = cap16;
         if (rgroups > rblocks) rgroups = rblocks;
         if (rgroups < 1) rgroups = 1;
         const int blocks = (int)((nch * rgroups + 255) / 256);
