@@ -231,6 +231,28 @@ def test_masked_parity_kernels_vs_oracle(words, rows, npass):
                 assert torch.equal(o1, outs[j])
 
 
+@pytest.mark.parametrize("words,rows", [(11, 70), (313, 2013), (5691, 300)])
+def test_masked_parity_acc_xors_into_out(words, rows):
+    """ogm_masked_parity_acc (every kernel path) XORs the parities into the
+    caller's buffer: prefill ^ ogm_masked_parity's output."""
+    from paper_2209_03526_b200 import _lib
+    from paper_2209_03526_b200.graphs import padded_device_matrix
+    rng = np.random.default_rng(words + rows)
+    comps = [padded_device_matrix(rng.integers(0, 1 << 32, (rows, words), dtype=np.uint32)) for _ in range(3)]
+    inds = [dev(rng.integers(0, 1 << 32, words, dtype=np.uint32)) for _ in range(12)]
+    nw = (rows + 31) // 32
+    A = _lib.ptr_array
+    args = (rows, words, comps[0].stride(0), 3, A(comps), 3, _lib.int_array([0, 1, 2]), _lib.int_array([1, 2, 0]), 2,
+            A(inds))
+    plain = [torch.empty((nw,), dtype=torch.int32, device="cuda") for _ in range(6)]
+    _lib.call("ogm_masked_parity", *args, A(plain), _lib.stream_ptr())
+    pre = [dev(rng.integers(0, 1 << 32, nw, dtype=np.uint32)) for _ in range(6)]
+    acc = [p.clone() for p in pre]
+    _lib.call("ogm_masked_parity_acc", *args, A(acc), _lib.stream_ptr())
+    for a, p, q in zip(acc, pre, plain):
+        assert torch.equal(a, p ^ q)
+
+
 @pytest.mark.parametrize("world", [1, 2, 3, 8])
 def test_sharded_sec_eval_slices_equal_unsharded(world):
     """Per-rank shards (masked parity on the row slice + zero-share slice by
