@@ -12,6 +12,8 @@ from __future__ import annotations
 
 import hashlib
 
+import threading
+
 import numpy as np
 import torch
 
@@ -95,6 +97,23 @@ def zero_share_device(key_own: bytes, key_prev: bytes, counter: int, nbits: int,
     return out
 
 
+_TLS = threading.local()
+
+
+def _thread_workspace(nbytes: int, dev) -> torch.Tensor:
+    """Scratch for the permutation rounds, kept per host thread (each party
+    thread launches on its own stream, so reuse is stream-ordered) and grown
+    on demand: one allocation instead of one per permutation."""
+    key = (str(dev), _lib.stream_ptr())   # reuse is ordered only on the same stream
+    cache = getattr(_TLS, "ws", None)
+    if cache is None:
+        cache = _TLS.ws = {}
+    buf = cache.get(key)
+    if buf is None or buf.numel() < nbytes:
+        buf = cache[key] = torch.empty((max(nbytes, 1 << 16),), dtype=torch.uint8, device=dev)
+    return buf
+
+
 def seeded_permutation_device(key: bytes, label: bytes, index: int, n: int,
                               out: torch.Tensor | None = None, workspace: torch.Tensor | None = None,
                               device=None) -> torch.Tensor:
@@ -104,7 +123,7 @@ def seeded_permutation_device(key: bytes, label: bytes, index: int, n: int,
         out = torch.empty((n,), dtype=torch.int32, device=dev)
     nbytes = int(_lib.load().ogm_perm_workspace_bytes(n))
     if workspace is None or workspace.numel() < nbytes:
-        workspace = torch.empty((nbytes,), dtype=torch.uint8, device=dev)
+        workspace = _thread_workspace(nbytes, dev)
     _lib.call("ogm_seeded_permutation", key, label, index, n, _lib.ptr(out), _lib.ptr(workspace),
               _lib.stream_ptr())
     return out
