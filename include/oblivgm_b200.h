@@ -359,12 +359,18 @@ int ogm_shuffle_online_fused(int64_t rows, const int32_t* k1, const int32_t* pi1
 /* The online phase of one 3-party shuffle of 16-byte rows over planned
  * gathers (src/shuffle.py:106-143; the four gathers' plans from
  * ogm_gather_plan in step order x1 (k1), y1 (pi12), c1 (pi23), R3 (k3), tile
- * 4096 rows).  Every blind is in its step's SOURCE order (U', V', W', Z').
+ * 4096 rows).  Every blind is in its step's SOURCE order (U', V', W', Z'),
+ * except W above the size ogm_shuffle_online_planned_w_output_order names.
  * Each message is handed from sender to receiver tile by tile in shared
  * memory: the sender's window pass feeds the receiver's partition pass in one
  * kernel.  x1, y1, c1 (optional, may be NULL) receive copies of the
  * messages; inter[0..2] are three table-sized scratch buffers.  r3 = the new
  * component R3. */
+/* 1 when ogm_shuffle_online_planned expects P2's blind (w_src) in c1's OUTPUT
+ * order for this table size (large tables: W then streams in c1's window
+ * pass), 0 when it expects it in c1's source order like the other blinds. */
+int ogm_shuffle_online_planned_w_output_order(int64_t rows);
+
 int ogm_shuffle_online_planned(int64_t rows, const int32_t* const* q2, const int32_t* const* gdst,
                                const uint16_t* const* srow, const uint32_t* a, const uint32_t* b, const uint32_t* c,
                                const uint32_t* u_src, const uint32_t* v_src, const uint32_t* w_src,

@@ -683,19 +683,21 @@ __global__ void __launch_bounds__(kTmaThreads, 1) plan_chain_kernel(
 #pragma unroll
         for (int i = 0; i < Q; i++) {
             const int k = threadIdx.x + i * kTmaThreads;
-            bl[i] = __ldcs(blind + t * T + k);
+            bl[i] = blind ? __ldcs(blind + t * T + k) : make_uint4(0, 0, 0, 0);
             sr[i] = __ldcs(srow + t * T + k);
             gd[i] = __ldcs(gdst + t * T + k);
         }
         gather(j + 2);   // buffer (j + 2) % 3 was freed by the barrier closing tile j - 1
         cp_async_wait<2>();  // this thread's gathers of tile j have landed
         uint4* rs = buf(j);
+        if (blind || msg) {
 #pragma unroll
-        for (int i = 0; i < Q; i++) {
-            const int k = threadIdx.x + i * kTmaThreads;
-            const uint4 v = rs[k];
-            if (msg) __stcs(msg + t * T + k, v);
-            rs[k] = xor4(v, bl[i]);
+            for (int i = 0; i < Q; i++) {
+                const int k = threadIdx.x + i * kTmaThreads;
+                const uint4 v = rs[k];
+                if (msg) __stcs(msg + t * T + k, v);
+                rs[k] = xor4(v, bl[i]);
+            }
         }
         __syncthreads();
 #pragma unroll
@@ -712,7 +714,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) plan_chain_kernel(
         for (int k = threadIdx.x; k < nr; k += kTmaThreads) {
             const uint4 m = __ldcg(inter_a + __ldcs(q + b0 + k));
             if (msg) __stcs(msg + b0 + k, m);
-            rs[k] = xor4(m, __ldcs(blind + b0 + k));
+            rs[k] = blind ? xor4(m, __ldcs(blind + b0 + k)) : m;
         }
         __syncthreads();
         for (int k = threadIdx.x; k < nr; k += kTmaThreads) __stcs(inter_b + __ldcs(gdst + b0 + k), rs[__ldcs(srow + b0 + k)]);
@@ -725,10 +727,12 @@ __global__ void __launch_bounds__(256) win_gather_dual4_kernel(const int32_t* __
                                                                const uint4* __restrict__ ia,
                                                                const int32_t* __restrict__ qb,
                                                                const uint4* __restrict__ ib, int64_t rows,
-                                                               uint4* __restrict__ out, uint4* __restrict__ msg) {
+                                                               uint4* __restrict__ out, uint4* __restrict__ msg,
+                                                               const uint4* __restrict__ ta) {
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < rows; i += stride) {
-        const uint4 va = __ldcg(ia + __ldcs(qa + i));
+        uint4 va = __ldcg(ia + __ldcs(qa + i));
+        if (ta) va = xor4(va, __ldcs(ta + i));
         const uint4 vb = __ldcg(ib + __ldcs(qb + i));
         if (msg) __stcs(msg + i, va);
         __stcs(out + i, xor4(va, vb));
@@ -1318,6 +1322,10 @@ int ogm_trio_shuffle(const uint8_t* s12, const uint8_t* s23, const uint8_t* s31,
 //   P2 -> P3, P3: c1 = win3(Ic); R3 = win4(Ir) ^ c1
 // x1, y1, c1 are optional copies of the messages; inter[0..2] are three
 // table-sized scratch buffers.
+int ogm_shuffle_online_planned_w_output_order(int64_t rows) {
+    return rows * 16 > ogm::kDualMaxBytes ? 1 : 0;
+}
+
 int ogm_shuffle_online_planned(int64_t rows, const int32_t* const* q2, const int32_t* const* gdst,
                                const uint16_t* const* srow, const uint32_t* a, const uint32_t* b, const uint32_t* c,
                                const uint32_t* u_src, const uint32_t* v_src, const uint32_t* w_src,
@@ -1352,19 +1360,25 @@ int ogm_shuffle_online_planned(int64_t rows, const int32_t* const* q2, const int
     plan_partition_tma_kernel<<<g, TT, kTmaSmemBytes, st>>>((U4)a, (U4)b, (U4)u_src, srow[0], gdst[0], rows, i0);
     plan_partition_tma_kernel<<<g, TT, kTmaSmemBytes, st>>>((U4)c, (U4)v_src, nullptr, srow[1], gdst[1], rows, i1);
     if (scrub_l2() != OGM_OK) return OGM_ERR_CUDA;
-    plan_chain_kernel<<<g, TT, kChainSmem2, st>>>(q2[0], i0, (U4)w_src, srow[2], gdst[2], rows, i2, (uint4*)x1);
+    // above the dual-pass size P2's blind W stays in c1's OUTPUT order: the x1 -> c1 chain kernel
+    // then needs no XOR pass (it is MIO-bound) and W streams in c1's own window pass (2-3% at
+    // 2^26-2^28; with the dual pass an extra stream costs more than it saves)
+    const bool w_out = ogm_shuffle_online_planned_w_output_order(rows) != 0;
+    plan_chain_kernel<<<g, TT, kChainSmem2, st>>>(q2[0], i0, w_out ? nullptr : (U4)w_src, srow[2], gdst[2], rows, i2,
+                                                  (uint4*)x1);
     if (scrub_l2() != OGM_OK) return OGM_ERR_CUDA;
     plan_chain_kernel<<<g, TT, kChainSmem2, st>>>(q2[1], i1, (U4)z_src, srow[3], gdst[3], rows, i0, (uint4*)y1);
     if (scrub_l2() != OGM_OK) return OGM_ERR_CUDA;
     const int64_t g2 = std::min<int64_t>((rows + 255) / 256, (int64_t)sm_count() * 8);
     if (rows * 16 <= kDualMaxBytes) {
-        win_gather_dual4_kernel<<<(int)g2, 256, 0, st>>>(q2[2], i2, q2[3], i0, rows, (uint4*)r3, (uint4*)c1);
+        win_gather_dual4_kernel<<<(int)g2, 256, 0, st>>>(q2[2], i2, q2[3], i0, rows, (uint4*)r3, (uint4*)c1,
+                                                         w_out ? (U4)w_src : nullptr);
     } else {
         // two random windows at once thrash L2 far above its size (2^26 rows: 2.06 ms and 11 GB read
         // instead of 2.7; smaller windows do not rescue it, scripts/exp_chain_win.py): c1's window
         // pass, then R3's with c1 streamed
         uint4* c1m = c1 ? (uint4*)c1 : i1;
-        win_gather4_kernel<<<(int)g2, 256, 0, st>>>(q2[2], i2, nullptr, nullptr, rows, c1m);
+        win_gather4_kernel<<<(int)g2, 256, 0, st>>>(q2[2], i2, w_out ? (U4)w_src : nullptr, nullptr, rows, c1m);
         if (scrub_l2() != OGM_OK) return OGM_ERR_CUDA;
         win_gather4_kernel<<<(int)g2, 256, 0, st>>>(q2[3], i0, c1m, nullptr, rows, (uint4*)r3);
     }
