@@ -32,10 +32,9 @@ for lg in map(int, sys.argv[1:]):
     e = lambda: torch.empty_like(comps[0])  # noqa: E731
     off = [ShuffleOffline(p + 1, cfg[p].seed_with_next, cfg[p].seed_with_prev, 0, rows, 128, plan=True)
            for p in range(3)]
-    u_src = source_order(off[0].u, off[0].k1)
-    v_src = source_order(off[1].v, off[1].pi12)
-    w_src = source_order(off[1].w, off[1].pi23)
-    z_src = off[2].z
+    # the blinds as the chained shuffle expects them (W in c1's output order above 256 MB)
+    (u_src,), (v_src, w_src), (z_src,) = off[0].chain_blinds(), off[1].chain_blinds(), off[2].chain_blinds()
+    w_steps = source_order(off[1].w, off[1].pi23)   # the per-party steps with source-order blinds
     plans = [off[0].plan_x1, off[1].plan_y1, off[1].plan_c1, off[2].plan_r3]
     want = [e() for _ in range(4)]
     off[0].step_x1(comps[0], comps[1], want[0])
@@ -73,7 +72,7 @@ for lg in map(int, sys.argv[1:]):
     def steps_src():
         plans[0].run(x1, m1=comps[0], m2=comps[1], m4=u_src)
         plans[1].run(y1, m1=comps[2], m4=v_src)
-        plans[2].run(c1, m1=x1, m4=w_src)
+        plans[2].run(c1, m1=x1, m4=w_steps)
         plans[3].run(r3, m1=y1, m3=c1, m4=z_src)
 
     steps_src()
@@ -97,5 +96,5 @@ for lg in map(int, sys.argv[1:]):
         res[name] = statistics.median(ts)
     print(f"2^{lg} equal={ok}: " + "  ".join(f"{k} {v:.4f} ms ({240 * rows / (v * 1e-3) / 1e9 / 6535:.3f})"
                                             for k, v in res.items()), flush=True)
-    del off, plans, want, inter, got, comps, u_src, v_src, w_src, z_src, x1, y1, c1, r3, sink
+    del off, plans, want, inter, got, comps, u_src, v_src, w_src, z_src, w_steps, x1, y1, c1, r3, sink
     torch.cuda.empty_cache()
