@@ -83,7 +83,68 @@ def parse():
     p.add_argument("--query-steps", type=int, default=10)
     p.add_argument("--no-c4", action="store_true", help="skip the C4 sharded secEval leg")
     p.add_argument("--no-paired", action="store_true", help="skip the paired DPF (or DCF) run")
+    p.add_argument("--no-c5", action="store_true", help="skip the C5 shuffle/fetch leg")
+    p.add_argument("--c5-logs", default="24,28", help="C5 table sizes (log2 rows), comma separated")
+    p.add_argument("--ref-keys", type=int, default=1 << 22, help="keys per reference-arm step")
+    p.add_argument("--dry-run", action="store_true",
+                   help="launcher check without a GPU: ranks join a gloo group and rank 0 prints the line")
     return p.parse_args()
+
+
+def free_port() -> int:
+    import socket
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def launch_ranks(args) -> int | None:
+    """``--gpus N`` outside torchrun: re-run this script under
+    torch.distributed.run with N ranks, one per GPU (the driver's own launch
+    line), and return its exit code.  Inside torchrun: None, after checking
+    that WORLD_SIZE agrees with --gpus."""
+    env_world = os.environ.get("WORLD_SIZE")
+    if env_world is not None:
+        if int(env_world) != args.gpus:
+            raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={env_world}")
+        return None
+    if args.gpus <= 1:
+        return None
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", f"--master-port={free_port()}", str(Path(__file__).resolve()),
+           *sys.argv[1:]]
+    return subprocess.call(cmd, env=env)
+
+
+def run_dry(args):
+    """The launcher without a GPU: every rank joins a gloo group, the group's
+    size is checked with one all-reduce, rank 0 prints the JSON line shape."""
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    seen = world
+    if world > 1:
+        dist.init_process_group("gloo")
+        t = torch.ones(1)
+        dist.all_reduce(t)
+        seen = int(t.item())
+        dist.destroy_process_group()
+    if rank == 0:
+        print(json.dumps({"metric": METRIC, "value": None, "unit": UNIT, "n_gpus": world, "dry_run": True,
+                          "comm_ranks": seen, "config": config_for(args, world)}), flush=True)
+
+
+def config_for(args, world: int) -> dict:
+    """The workload description both arms print (same keys)."""
+    return {"workload": f"C2 batched {args.kind.upper()} micro (BASELINE configs[1])",
+            "keys_per_gpu": args.keys, "domain_bits": BITS, "points_per_key": 1,
+            "parallelism": f"key-sharded x{world}",
+            "l2": "inputs (9.1 GB of keys) larger than L2; no flush"}
 
 
 # ---------------------------------------------------------------------------
@@ -187,13 +248,18 @@ def cpu_model() -> str:
 
 
 def run_reference(args):
+    """The reference's CPU implementation of the path (the oracle/ C port of
+    src/fss.py:257-281 -- the reference itself is pure Python with no
+    compiled path), all host threads, on the GPU arm's config: each step
+    evaluates ``--ref-keys`` (default 2^22) of the workload's keys."""
     rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", str(args.gpus)))
     if rank != 0:
         return
     import oracle
     oracle.build()
     threads = os.cpu_count() or 1
-    sample = 1 << 16
+    sample = min(args.ref_keys, args.keys)
     k0, pts = cpu_keys(args.kind, sample, 3)
     for _ in range(args.warmup):
         oracle.eval_points(k0, pts, nthreads=threads)
@@ -207,13 +273,13 @@ def run_reference(args):
     desc = (f"{sample} of the {args.keys} keys per step ({args.kind.upper()}, 32-bit domain), "
             f"oracle/ C port of src/fss.py:257-281, {threads} threads on {cpu_model()}")
     line = {
-        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32",
-        "data": "synthetic", "config": {"workload": f"C2 batched {args.kind.upper()} micro",
-                                        "keys": args.keys, "domain_bits": BITS, "points_per_key": 1},
+        "data": "synthetic", "config": config_for(args, world),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port", "sample": desc},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "step_s": {"min": min(times), "max": max(times), "median": statistics.median(times)},
     }
     print(json.dumps(line), flush=True)
 
@@ -274,8 +340,51 @@ def query_latency(steps: int) -> dict:
     return out
 
 
+def c5_legs(args, world: int) -> dict:
+    """BASELINE configs[4] at each --c5-logs size: the 128-bit shuffle and
+    the fetch of 1%, 10% and 100% of 129-bit rows (bench_configs.c5_*_leg),
+    each with hbm_frac, a bit-exactness gate and the oracle port beside it.
+    Under torchrun every rank shuffles its own tables (replicas, weak
+    scaling); ms is the max over ranks."""
+    import torch
+    import torch.distributed as dist
+
+    import bench_configs
+
+    def worst(ms: float) -> float:
+        if world == 1:
+            return ms
+        t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    peak = bench_configs.HBM_PEAK
+    out = {"workload": "C5 shuffle/fetch sweep (BASELINE configs[4]): 128-bit rows x 3 share components; "
+                       "fetch rows = flag + 128-bit id (129 bits)", "unit": "ms", "hbm_peak_GBps": peak,
+           "scaling": "weak (replicas)" if world > 1 else None, "shuffle": [], "fetch": []}
+    torch.cuda.empty_cache()
+    for lg in [int(x) for x in args.c5_logs.split(",") if x]:
+        sh = bench_configs.c5_shuffle_leg(lg, args.steps, args.warmup)
+        fe = bench_configs.c5_fetch_leg(lg, args.steps, args.warmup)
+        for e, per_row in [(sh, 240)] + [(f, f["algorithmic_bytes_per_row"]) for f in fe]:
+            e["ms"] = worst(e["ms"])
+            e["GBps"] = per_row * e["rows"] / (e["ms"] * 1e-3) / 1e9
+            e["hbm_frac"] = e["GBps"] / peak
+            e["rows_per_s_all_ranks"] = world * e["rows"] / (e["ms"] * 1e-3)
+        out["shuffle"].append(sh)
+        out["fetch"].extend(fe)
+        torch.cuda.empty_cache()
+    return out
+
+
 def main():
     args = parse()
+    rc = launch_ranks(args)
+    if rc is not None:
+        sys.exit(rc)
+    if args.dry_run:
+        run_dry(args)
+        return
     if args.impl == "reference":
         run_reference(args)
         return
@@ -288,8 +397,14 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
+    comm_ranks = world
     if world > 1:
+        os.environ.setdefault("NCCL_DEBUG", "INFO")   # communicator size visible in the log
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        ones = torch.ones(1, device="cuda")
+        dist.all_reduce(ones)
+        comm_ranks = int(ones.item())
     lib = _lib.load()
     _lib.check(lib.ogm_init())
 
@@ -436,6 +551,11 @@ def main():
         torch.cuda.empty_cache()
         c4 = bench_configs.c4_sec_eval(2_000_000, 1, 10, 3, rank, world)
 
+    # C5 (BASELINE configs[4]): shuffle and 1/10/100% fetch bandwidth, every rank its own tables
+    c5 = None
+    if not args.no_c5:
+        c5 = c5_legs(args, world)
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         import oracle
@@ -451,12 +571,9 @@ def main():
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
-            "config": {"workload": f"C2 batched {args.kind.upper()} micro (BASELINE configs[1])",
-                       "keys_per_gpu": K, "domain_bits": BITS, "points_per_key": 1,
-                       "parallelism": f"key-sharded x{world}",
-                       "l2": "inputs (9.1 GB of keys) larger than L2; no flush"},
+            "config": config_for(args, world), "comm_ranks": comm_ranks,
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "paired": paired, "query_latency": query,
-            "c4_sec_eval": c4,
+            "c4_sec_eval": c4, "c5": c5,
             "gpu_launches": args.steps, "clocks": clk,
             "launch_ms": {"mean": statistics.mean(per_launch), "min": min(per_launch),
                           "max": max(per_launch)},

@@ -585,6 +585,195 @@ def run_c5(args):
 
 
 # ---------------------------------------------------------------------------
+# C5 leg of bench.py: shuffle of 128-bit rows + the 1% / 10% / 100% fetch
+# ---------------------------------------------------------------------------
+
+
+def _timed_steps(fn, steps: int, warmup: int, flush: torch.Tensor | None) -> float:
+    """ms per step: CUDA events around each step on the launching stream,
+    the L2 flush (when given) outside them."""
+    for _ in range(warmup):
+        fn()
+    torch.cuda.synchronize()
+    ev = events(2 * steps)
+    for k in range(steps):
+        if flush is not None:
+            flush.zero_()
+        ev[2 * k].record()
+        fn()
+        ev[2 * k + 1].record()
+    torch.cuda.synchronize()
+    return sum(ev[2 * k].elapsed_time(ev[2 * k + 1]) for k in range(steps)) / steps
+
+
+def _bits_of(words: torch.Tensor, n: int) -> torch.Tensor:
+    """Packed bit vector -> (n,) int32 0/1 (device)."""
+    sh = torch.arange(32, device=words.device, dtype=torch.int32)
+    return ((words[: (n + 31) // 32].unsqueeze(1) >> sh) & 1).reshape(-1)[:n]
+
+
+def _random_bits(n: int, seed: int, stream_id: int) -> torch.Tensor:
+    w = workloads.device_random_words(words_for(n), seed, stream_id)
+    if n % 32:
+        w[-1] &= (1 << (n % 32)) - 1
+    return w
+
+
+def _bernoulli_bits(n: int, p: float, seed: int) -> torch.Tensor:
+    """Packed Bernoulli(p) bits (device, seeded)."""
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    b = (torch.rand(n, device="cuda", generator=g) < p).to(torch.int64)
+    pad = (-n) % 32
+    if pad:
+        b = torch.cat([b, torch.zeros(pad, dtype=torch.int64, device="cuda")])
+    w = (b.reshape(-1, 32) << torch.arange(32, device="cuda", dtype=torch.int64)).sum(1)
+    return torch.where(w >= (1 << 31), w - (1 << 32), w).to(torch.int32)
+
+
+def c5_shuffle_leg(lg: int, steps: int, warmup: int, seed: int = 1) -> dict:
+    """C5 (BASELINE configs[4]): the three-party shuffle of 2^lg rows x 128
+    bits, offline material prepared (ShuffleOffline), online phase timed:
+    one cooperative launch up to 2^21 rows, the chained planned gathers above.
+    Gate: R1 ^ R2 ^ R3 == the plaintext table under the composed permutation,
+    at full size, plus the oracle port's R3 bit for bit on a 2^16-row run."""
+    import oracle
+
+    rows = 1 << lg
+    cfg = make_session_configs(b"\x77" * 16)
+    seeds = (cfg[0].seed_with_next, cfg[1].seed_with_next, cfg[2].seed_with_next)
+    comps = [workloads.device_random_words(rows * 4, seed, 20 + c).reshape(rows, 4) for c in range(3)]
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    pc: dict = {}
+    fused = rows * 16 <= (32 << 20)
+    pairs = [(seeds[0], seeds[2]), (seeds[1], seeds[0]), (seeds[2], seeds[1])]
+    off = [ShuffleOffline(p + 1, *pairs[p], 0, rows, 128, perm_cache=pc, plan=not fused) for p in range(3)]
+    if not fused:
+        for o in off:
+            o.chain_blinds()
+    torch.cuda.synchronize()
+    t_off = time.perf_counter() - t0
+    r3 = torch.empty_like(comps[0])
+    inter = [torch.empty_like(comps[0]) for _ in range(3)]
+
+    def online():
+        if fused:
+            shuffle_online_fused(off, comps[0], comps[1], comps[2], inter[0], inter[1], None, r3)
+        else:
+            shuffle_online_planned(off, comps[0], comps[1], comps[2], r3, inter=inter)
+
+    flush = torch.empty((512 << 20,), dtype=torch.uint8, device="cuda") if rows * 16 * 4 < (512 << 20) else None
+    ms = _timed_steps(online, steps, warmup, flush)
+    pi12, pi23, pi31 = (pc[(s, 0, rows)].long() for s in seeds)
+    perm = pi12[pi31[pi23]]
+    ok = bool(torch.equal(off[0].out_a ^ off[0].out_b ^ r3, (comps[0] ^ comps[1] ^ comps[2])[perm]))
+    del perm, pi12, pi23, pi31, off, pc, inter
+    torch.cuda.empty_cache()
+    # CPU path beside it: oracle.shuffle_trio (numpy, 1 core) on a 2^16-row run, R3 compared
+    srows = min(rows, 1 << 16)
+    sc = [c[:srows].contiguous() for c in comps]
+    soff = [ShuffleOffline(p + 1, *pairs[p], 0, srows, 128, plan=False) for p in range(3)]
+    sr3 = torch.empty_like(sc[0])
+    shuffle_online_fused(soff, sc[0], sc[1], sc[2], torch.empty_like(sc[0]), torch.empty_like(sc[0]), None, sr3)
+    host = [c.cpu().numpy().view(np.uint32) for c in sc]
+    t0 = time.perf_counter()
+    (_, _, o_r3), _ = oracle.shuffle_trio(*seeds, 0, host, 128)
+    cpu_s = time.perf_counter() - t0
+    sample_equal = bool(np.array_equal(o_r3, sr3.cpu().numpy().view(np.uint32)))
+    nbytes = rows * (14 * 16 + 4 * 4)
+    return {"rows": rows, "ms": ms, "GBps": nbytes / (ms * 1e-3) / 1e9,
+            "hbm_frac": nbytes / (ms * 1e-3) / 1e9 / HBM_PEAK, "algorithmic_bytes_per_row": 240,
+            "path": "one cooperative launch" if fused else "chained planned gathers (5 launches)",
+            "offline_s": t_off, "l2": "flushed between steps" if flush is not None else "tables larger than L2",
+            "gate": {"recombination_full_size": ok, "r3_equal_to_oracle_on_2^16_run": sample_equal},
+            "cpu_baseline": {"value": 1e3 * cpu_s * rows / srows, "unit": "ms", "cores": 1, "kind": "port",
+                             "sample": f"{srows} rows: oracle.shuffle_trio (numpy, src/shuffle.py:80-144) in "
+                                       f"{cpu_s:.3f}s, extrapolated linearly to {rows} rows"}}
+
+
+def c5_fetch_leg(lg: int, steps: int, warmup: int, ps=(0.01, 0.1, 1.0), seed: int = 1) -> list:
+    """C5 fetch (BASELINE configs[4], "oblivious fetch of 1%, 10% and 100% of
+    rows"): sec_fetch_multi (src/engine.py:220-270) of rows = flag + 128-bit
+    id (129 bits), shuffled, flag column opened, flagged rows kept; the
+    flag-split trio path (fetch.FlaggedFetch), offline material prepared once
+    per size, online phase timed per p.  Gates at full size: the opened
+    column equals the plaintext flags under the composed permutation, and
+    the kept records recombine to the plaintext rows in shuffled order; on a
+    2^16-row run every record share equals the oracle's sec_fetch_multi."""
+    import oracle
+    from paper_2209_03526_b200.fetch import FlaggedFetch
+
+    rows = 1 << lg
+    cfg = make_session_configs(b"\x78" * 16)
+    seeds = (cfg[0].seed_with_next, cfg[1].seed_with_next, cfg[2].seed_with_next)
+    payload = [workloads.device_random_words(rows * 4, seed, 30 + c).reshape(rows, 4) for c in range(3)]
+    f12 = [_random_bits(rows, seed, 40), _random_bits(rows, seed, 41)]
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    pc: dict = {}
+    ff = FlaggedFetch(seeds, 0, rows, perm_cache=pc)
+    torch.cuda.synchronize()
+    t_off = time.perf_counter() - t0
+    pi12, pi23, pi31 = (pc[(s, 0, rows)].long() for s in seeds)
+    perm = pi12[pi31[pi23]]
+    del pi12, pi23, pi31
+    plain_rows = (payload[0] ^ payload[1] ^ payload[2])[perm]
+    flush = torch.empty((512 << 20,), dtype=torch.uint8, device="cuda") if rows * 16 * 4 < (512 << 20) else None
+    out = []
+    for i, p in enumerate(ps):
+        fp = _bernoulli_bits(rows, p, seed + 100 + i)
+        flags = [f12[0], f12[1], fp ^ f12[0] ^ f12[1]]
+        ms = _timed_steps(lambda: ff.online(flags, payload), steps, warmup, flush)
+        k = ff.kept()
+        opened = _bits_of(ff.plain, rows)
+        ok_open = bool(torch.equal(opened, _bits_of(fp, rows)[perm]))
+        kept_idx = torch.nonzero(opened).reshape(-1)
+        recs = ff.records()
+        ok_recs = k == kept_idx.numel() and bool(torch.equal(recs[0] ^ recs[1] ^ recs[2], plain_rows[kept_idx]))
+        del kept_idx, opened, recs
+        # algorithmic bytes: 14 moves of a 129-bit row + 4 index reads (the shuffle), the open's
+        # three flag columns, and per kept row three 16-B payload reads + writes
+        nbytes = rows * (14 * 129 / 8 + 16 + 3 / 8) + k * 6 * 16
+        out.append({"rows": rows, "p": p, "kept": k, "ms": ms, "GBps": nbytes / (ms * 1e-3) / 1e9,
+                    "hbm_frac": nbytes / (ms * 1e-3) / 1e9 / HBM_PEAK,
+                    "algorithmic_bytes_per_row": nbytes / rows,
+                    "survey_bytes_per_row": 248 + 12 * p * 16,
+                    "path": ("flag-split: 16-B payload shuffle ("
+                             + ("one cooperative launch" if ff.fused else "chained planned gathers")
+                             + ") + flag-column bit gathers (2 launches) + hand-written keep (3 launches)"),
+                    "offline_s": t_off, "l2": "flushed between steps" if flush is not None else "tables larger than L2",
+                    "gate": {"opened_equals_permuted_flags": ok_open, "records_recombine": ok_recs}})
+        if not (ok_open and ok_recs):
+            raise SystemExit(f"C5 fetch gate failed at 2^{lg} rows, p={p}")
+    del ff, pc, perm, plain_rows, payload, f12
+    torch.cuda.empty_cache()
+    # the CPU path beside it: oracle.fetch_multi_trio (numpy, 1 core) on 2^16 rows at p = 0.1, and our
+    # fetch on the same 2^16-row inputs, record share for record share
+    srows = min(rows, 1 << 16)
+    rng = np.random.default_rng(seed)
+    ids = [rng.integers(0, 1 << 32, size=(srows, 4), dtype=np.uint32) for _ in range(3)]
+    fl = [oracle.pack_bits(rng.integers(0, 2, srows, dtype=np.uint8)) for _ in range(2)]
+    fl.append(oracle.pack_bits((rng.random(srows) < 0.1).astype(np.uint8)) ^ fl[0] ^ fl[1])
+    dev = lambda a: torch.from_numpy(np.ascontiguousarray(a).view(np.int32).copy()).cuda()  # noqa: E731
+    sf = FlaggedFetch(seeds, 0, srows)
+    sf.online([dev(f) for f in fl], [dev(m) for m in ids])
+    t0 = time.perf_counter()
+    keep, _, want = oracle.fetch_multi_trio(*seeds, 0, fl, ids, 128)
+    cpu_s = time.perf_counter() - t0
+    got = sf.records()
+    equal = keep.size == got[0].shape[0] and all(
+        np.array_equal(g.cpu().numpy().view(np.uint32), w) for g, w in zip(got, want))
+    for o in out:
+        o["gate"]["records_equal_to_oracle_on_2^16_run"] = equal
+        o["cpu_baseline"] = {"value": 1e3 * cpu_s * rows / srows, "unit": "ms", "cores": 1, "kind": "port",
+                             "sample": f"{srows} rows, p=0.1: oracle.fetch_multi_trio (numpy, src/engine.py:220-270) "
+                                       f"in {cpu_s:.3f}s, extrapolated linearly to {rows} rows"}
+    if not equal:
+        raise SystemExit("C5 fetch differs from the oracle on the 2^16-row run")
+    return out
+
+
+# ---------------------------------------------------------------------------
 # C3 root-slot pipeline (trio fast path): secEval x2 -> combine -> Case II fetch
 # ---------------------------------------------------------------------------
 
@@ -689,7 +878,12 @@ def c4_sec_eval(rows: int, seed: int, steps: int, warmup: int, rank: int, world:
     ranks (an initialised NCCL group when world > 1): 2M candidates of one
     vertex type (16M vertices / 8 types), Zipf(1.1) attribute over 10^4
     values, an interval predicate (2 DCF passes) for all three parties, match
-    bits all-gathered.  Strong scaling; device time max over ranks."""
+    bits all-gathered.  Strong scaling; device time max over ranks.
+
+    Shares are drawn by GLOBAL row (workloads.shared_one_hot row0), so every
+    world size shares the same table; rank 0 then gates the all-gathered
+    result bit for bit against the oracle port on rows taken from EVERY
+    rank's shard (regenerated from the same streams)."""
     import torch.distributed as dist
 
     from paper_2209_03526_b200.sharding import ShardPlan, sharded_sec_eval_trio
@@ -702,8 +896,7 @@ def c4_sec_eval(rows: int, seed: int, steps: int, warmup: int, rank: int, world:
     p = 1.0 / ranks ** 1.1
     vals_all = rng.choice(n, size=rows, p=p / p.sum()).astype(np.int32)
     vals = torch.from_numpy(vals_all[lo:hi]).cuda()
-    c1, c2, c3 = workloads.shared_one_hot(vals, n, seed + rank, 40)
-    comps = [c1, c2, c3]
+    comps = list(workloads.shared_one_hot(vals, n, seed, 40, row0=lo))
     w = words_for(n)
     krng = np.random.default_rng(seed + 1)  # identical keys on every rank
     pairs = [fss.ic_gen(100, 4000, n, krng) for _ in range(3)]
@@ -732,22 +925,47 @@ def c4_sec_eval(rows: int, seed: int, steps: int, warmup: int, rank: int, world:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms = float(t.item())
     nbytes_local = 3 * (hi - lo) * w * 4
-    cpu = None
-    if rank == 0 and world == 1:
+    cpu = gate = None
+    if rank == 0:
         import oracle
 
-        def gpu_bits(p, ps):  # undo the re-share blinding: additive bits = message ^ zero share
-            z = oracle.zero_share(zk[p][0], zk[p][1], ps, rows)
-            return res[ps][p].cpu().numpy().view(np.uint32) ^ z
+        zero = {(p_, ps): oracle.zero_share(zk[p_][0], zk[p_][1], ps, rows) for p_ in range(3) for ps in range(2)}
 
-        cpu = cpu_port_sec_eval(comps, w, lambda p, ps: inds[ps][p], gpu_bits, 20000)
+        def gpu_bits(p_, ps):  # undo the re-share blinding: additive bits = message ^ zero share
+            return res[ps][p_].cpu().numpy().view(np.uint32) ^ zero[(p_, ps)]
+
+        if world == 1:
+            cpu = cpu_port_sec_eval(comps, w, lambda p_, ps: inds[ps][p_], gpu_bits, 20000)
+        # N-rank parity gate: 2048 rows from the start of every shard, shares regenerated by global row
+        per = 2048
+        checked, equal = 0, True
+        full = {(p_, ps): oracle.unpack_bits(gpu_bits(p_, ps), rows) for p_ in range(3) for ps in range(2)}
+        for r in range(world):
+            r_lo, r_hi = plan.bounds(r)
+            m = min(per, r_hi - r_lo)
+            if m <= 0:
+                continue
+            sub = torch.from_numpy(vals_all[r_lo:r_lo + m]).cuda()
+            sc = [c.cpu().numpy().view(np.uint32) for c in workloads.shared_one_hot(sub, n, seed, 40, row0=r_lo)]
+            for ps in range(2):
+                for p_ in range(3):
+                    ia = inds[ps][p_][0].cpu().numpy().view(np.uint32)[:w]
+                    ib = inds[ps][p_][1].cpu().numpy().view(np.uint32)[:w]
+                    want = oracle.masked_parity(sc[p_], sc[(p_ + 1) % 3], ia, ib)
+                    equal = equal and bool(np.array_equal(want, full[(p_, ps)][r_lo:r_lo + m]))
+            checked += m
+        gate = {"rows_checked": checked, "shards_checked": world, "equal_to_oracle": equal,
+                "how": "all-gathered re-shared bits ^ zero share == oracle.masked_parity on the first "
+                       f"{per} rows of every rank's shard (shares drawn by global row)"}
+        if not equal:
+            raise SystemExit("C4 sharded secEval differs from the oracle port")
     return {"config": f"C4 root secEval, {rows} candidates (Zipf attr n={n}, w={w}), interval, "
                       f"rows sharded x{world}", "metric": "secEval_candidates_per_s",
             "value": rows / (ms * 1e-3), "unit": "candidates/s", "ms_per_step": ms, "n_gpus": world,
             "scaling": "strong", "rank0_hbm_GBps": nbytes_local / (ms * 1e-3) / 1e9,
             "rank0_hbm_frac": nbytes_local / (ms * 1e-3) / 1e9 / HBM_PEAK,
             "collective": "NCCL all_gather of packed blinded match bits" if world > 1 else "none",
-            "result_words": int(res[0][0].numel()), "cpu_baseline": cpu}
+            "result_words": int(res[0][0].numel()), "cpu_baseline": cpu, "parity_gate": gate}
 
 
 def run_c4(args):

@@ -254,6 +254,41 @@ int64_t ogm_compact_workspace_bytes(int64_t n);
 int ogm_compact_bits(int64_t n, const uint32_t* bits, int32_t* out_idx, int64_t* out_count,
                      void* workspace, int64_t workspace_bytes, void* stream);
 
+/* Keep the rows whose mask bit is set, in order (src/engine.py:249-269 /
+ * :327-334, the np.nonzero + row loop after an open): optionally their
+ * indices to out_idx, and their 16-byte-pitched rows of nmat (<= 8) matrices
+ * mats[j] (pitch words) to consecutive rows of outs[j] (opitch words).  The
+ * kept count goes to *count (device int64).  Hand-written three-launch
+ * compaction (chunk popcounts, one-CTA scan, warp-per-chunk emit). */
+int64_t ogm_keep_rows_workspace_bytes(int64_t rows);
+int ogm_keep_rows(int64_t rows, const uint32_t* bits, int nmat, const uint32_t* const* mats, int64_t pitch,
+                  uint32_t* const* outs, int64_t opitch, int32_t* out_idx, int64_t* count, void* workspace,
+                  int64_t workspace_bytes, void* stream);
+
+/* ---- flagged-row fetch in the flag-split layout (src/engine.py:220-270) ---
+ * A sec_fetch_multi row [flag | 128-bit payload] is 129 bits (5 words).  The
+ * fetch keeps it split: payload as a 16-byte row, flag as a bit column
+ * (bit permutations and XORs commute with the shuffle, so results are the
+ * reference's bits).  ogm_split_flag_rows turns a 5-word-row table (blinds
+ * drawn in the reference layout) into the two parts: payload[i] = bits
+ * 1..128 of row i, bit i of flags = bit 0 of row i. */
+int ogm_split_flag_rows(int64_t rows, const uint32_t* in, int64_t pitch, uint32_t* payload, uint32_t* flags,
+                        void* stream);
+
+/* The flag column through one 3-party shuffle (src/shuffle.py:106-143 on bit
+ * 0 of every row), for the three co-resident parties, with the same composed
+ * permutations and split blinds as the payload:
+ *   x1f = (f1 ^ f2)[k1] ^ Uf,  y1f = f3[pi12] ^ Vf,  c1f = x1f[pi23] ^ Wf,
+ *   r3f = y1f[k3] ^ c1f ^ Zf,  plain = R1f ^ R2f ^ r3f (the opened column,
+ *   optional; src/rss.py:184-206).
+ * All columns are packed bit vectors; x1f, y1f are scratch (or the message
+ * copies), c1f and plain optional. */
+int ogm_flag_shuffle_trio(int64_t rows, const int32_t* k1, const int32_t* pi12, const int32_t* pi23,
+                          const int32_t* k3, const uint32_t* f1, const uint32_t* f2, const uint32_t* f3,
+                          const uint32_t* uf, const uint32_t* vf, const uint32_t* wf, const uint32_t* zf,
+                          const uint32_t* r1f, const uint32_t* r2f, uint32_t* x1f, uint32_t* y1f, uint32_t* c1f,
+                          uint32_t* r3f, uint32_t* plain, void* stream);
+
 /* ---- storage (src/storage.py) -------------------------------------------- */
 
 /* Loader for OGMS record containers (src/storage.py:43-65, 108-169): the file
@@ -359,23 +394,34 @@ int ogm_shuffle_online_fused(int64_t rows, const int32_t* k1, const int32_t* pi1
 /* The online phase of one 3-party shuffle of 16-byte rows over planned
  * gathers (src/shuffle.py:106-143; the four gathers' plans from
  * ogm_gather_plan in step order x1 (k1), y1 (pi12), c1 (pi23), R3 (k3), tile
- * 4096 rows).  Every blind is in its step's SOURCE order (U', V', W', Z'),
- * except W above the size ogm_shuffle_online_planned_w_output_order names.
+ * 4096 rows).  Every blind is in its step's SOURCE order (U', V', W', Z').
  * Each message is handed from sender to receiver tile by tile in shared
  * memory: the sender's window pass feeds the receiver's partition pass in one
  * kernel.  x1, y1, c1 (optional, may be NULL) receive copies of the
  * messages; inter[0..2] are three table-sized scratch buffers.  r3 = the new
  * component R3. */
-/* 1 when ogm_shuffle_online_planned expects P2's blind (w_src) in c1's OUTPUT
- * order for this table size (large tables: W then streams in c1's window
- * pass), 0 when it expects it in c1's source order like the other blinds. */
-int ogm_shuffle_online_planned_w_output_order(int64_t rows);
-
 int ogm_shuffle_online_planned(int64_t rows, const int32_t* const* q2, const int32_t* const* gdst,
                                const uint16_t* const* srow, const uint32_t* a, const uint32_t* b, const uint32_t* c,
                                const uint32_t* u_src, const uint32_t* v_src, const uint32_t* w_src,
                                const uint32_t* z_src, uint32_t* const* inter, uint32_t* x1, uint32_t* y1, uint32_t* c1,
                                uint32_t* r3, void* stream);
+
+/* The preferred order of P2's blind W for ogm_shuffle_online_planned_ex at
+ * this table size: 1 = c1's OUTPUT order (large tables: W then streams in
+ * c1's window pass and the x1 -> c1 chain kernel skips its XOR pass),
+ * 0 = c1's source order like the other blinds. */
+int ogm_shuffle_online_planned_w_output_order(int64_t rows);
+
+/* ogm_shuffle_online_planned with the order of w_src explicit:
+ * w_output_order = 1 takes W in c1's output order, 0 in its source order
+ * (any table size; the order ogm_shuffle_online_planned_w_output_order
+ * returns is the faster one).  ABI version 2. */
+int ogm_shuffle_online_planned_ex(int64_t rows, const int32_t* const* q2, const int32_t* const* gdst,
+                                  const uint16_t* const* srow, const uint32_t* a, const uint32_t* b,
+                                  const uint32_t* c, const uint32_t* u_src, const uint32_t* v_src,
+                                  const uint32_t* w_src, int w_output_order, const uint32_t* z_src,
+                                  uint32_t* const* inter, uint32_t* x1, uint32_t* y1, uint32_t* c1, uint32_t* r3,
+                                  void* stream);
 
 /* ---- native trio executor (src/engine.py:352-417 for three co-resident
  * parties) ------------------------------------------------------------------

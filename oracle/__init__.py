@@ -293,3 +293,27 @@ def shuffle_trio(s12: bytes, s23: bytes, s31: bytes, tid: int, comps, width: int
     c2 = ((msg_y1 ^ t31)[pi31] ^ t23)[pi23] ^ r1
     r3 = msg_c1 ^ c2
     return (r1, r2, r3), (msg_x1, msg_y1, msg_c1, r3)
+
+
+def fetch_multi_trio(s12: bytes, s23: bytes, s31: bytes, tid: int, flag_comps, id_comps, id_width: int):
+    """src/engine.py:220-270 (sec_fetch_multi with ``attrs={}``) for all three
+    parties at once: rows = flag bit ‖ id bits (src/engine.py:227-237, bit 0 =
+    flag), one shuffle of table id ``tid`` (src/shuffle.py:80-144), open the
+    flag column (src/rss.py:184-206: plain = R1 ^ R2 ^ R3), keep the flagged
+    rows in order and slice the id back out (src/engine.py:249-269).
+
+    ``flag_comps`` = three packed bit vectors, ``id_comps`` = three (rows,
+    words_for(id_width)) matrices.  Returns (kept row indices, opened flag
+    bits (rows,), [id share component c of every kept row for c = 0, 1, 2])."""
+    rows = int(np.asarray(id_comps[0]).shape[0])
+    width = 1 + id_width
+    comps = []
+    for f, ids in zip(flag_comps, id_comps):
+        fbits = unpack_bits(np.asarray(f, np.uint32), rows)
+        ibits = unpack_bits(np.asarray(ids, np.uint32).reshape(rows, -1), id_width)
+        comps.append(pack_bits(np.concatenate([fbits[:, None], ibits], axis=1)))
+    (r1, r2, r3), _ = shuffle_trio(s12, s23, s31, tid, comps, width)
+    plain = ((r1 ^ r2 ^ r3)[:, 0] & 1).astype(np.uint8)
+    keep = np.nonzero(plain)[0]
+    recs = [pack_bits(unpack_bits(m[keep], width)[:, 1:]) for m in (r1, r2, r3)]
+    return keep, plain, recs

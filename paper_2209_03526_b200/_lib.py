@@ -66,6 +66,10 @@ SIGNATURES = {
     "ogm_column_bits": ([_vp, _i64, _i64, _vp, _vp], _int),
     "ogm_compact_workspace_bytes": ([_i64], _i64),
     "ogm_compact_bits": ([_i64, _vp, _vp, _vp, _vp, _i64, _vp], _int),
+    "ogm_keep_rows_workspace_bytes": ([_i64], _i64),
+    "ogm_keep_rows": ([_i64, _vp, _int, _vp, _i64, _vp, _i64, _vp, _vp, _vp, _i64, _vp], _int),
+    "ogm_split_flag_rows": ([_i64, _vp, _i64, _vp, _vp, _vp], _int),
+    "ogm_flag_shuffle_trio": ([_i64] + [_vp] * 19, _int),
     "ogm_shuffle_gather": ([_i64, _i64, _i64, _vp, _vp, _vp, _vp, _vp, _cp, _cp, _u64, _vp, _cp, _cp, _u64,
                             _vp, _cp, _cp, _u64, _vp, _i64, _i64, _vp, _vp], _int),
     "ogm_perm_compose": ([_i64, _vp, _vp, _vp, _vp], _int),
@@ -81,6 +85,7 @@ SIGNATURES = {
     "ogm_trio_open_keep": ([_vp, _i64, _i64, _vp, _int, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _vp], _int),
     "ogm_shuffle_online_fused": ([_i64] + [_vp] * 15 + [_vp], _int),
     "ogm_shuffle_online_planned": ([_i64] + [_vp] * 16, _int),
+    "ogm_shuffle_online_planned_ex": ([_i64] + [_vp] * 9 + [_int] + [_vp] * 7, _int),
     "ogm_shuffle_online_planned_w_output_order": ([_i64], _int),
     "ogm_trio_match": ([_vp, _vp, _vp, _i64, _vp], _int),
     "ogm_measure_int_peak": ([ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double)], _int),

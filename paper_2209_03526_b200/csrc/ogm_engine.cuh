@@ -10,7 +10,6 @@
 // per party thread) reads only its own two.
 #pragma once
 
-#include <cub/cub.cuh>
 
 #include "ogm_aes.cuh"
 #include "ogm_common.cuh"
@@ -975,12 +974,6 @@ __global__ void unpack_records_kernel(const uint32_t* __restrict__ blob_words, i
     }
 }
 
-// rows whose bit is set, in order (public compaction after an open).
-struct FlagIter {
-    const uint32_t* bits;
-    __host__ __device__ bool operator()(int64_t i) const { return (bits[i >> 5] >> (i & 31)) & 1u; }
-};
-
 int engine_init() {
     OGM_CUDA_TRY(allow_big_smem(zero_share3_kernel<AesTab>, kAesTableBytes));
     return OGM_OK;
@@ -1423,29 +1416,13 @@ int ogm_column_bits(const uint32_t* mat, int64_t pitch, int64_t rows, uint32_t* 
     return OGM_OK;
 }
 
-int64_t ogm_compact_workspace_bytes(int64_t n) {
-    size_t bytes = 0;
-    cub::CountingInputIterator<int64_t> it(0);
-    cub::TransformInputIterator<bool, ogm::FlagIter, cub::CountingInputIterator<int64_t>> flags(
-        it, ogm::FlagIter{nullptr});
-    cub::DeviceSelect::Flagged(nullptr, bytes, it, flags, (int32_t*)nullptr, (int64_t*)nullptr, n);
-    return (int64_t)bytes + 256;
-}
+int64_t ogm_compact_workspace_bytes(int64_t n) { return ogm_keep_rows_workspace_bytes(n); }
 
+// indices of the set bits, in order: the hand-written keep (ogm_fetch.cuh) with no row copies
 int ogm_compact_bits(int64_t n, const uint32_t* bits, int32_t* out_idx, int64_t* out_count, void* workspace,
                      int64_t workspace_bytes, void* stream) {
-    using namespace ogm;
     OGM_CHECK_ARG(n >= 0, OGM_ERR_ARG, "negative length");
-    if (n == 0) {
-        OGM_CUDA_TRY(cudaMemsetAsync(out_count, 0, 8, as_stream(stream)));
-        return OGM_OK;
-    }
-    cub::CountingInputIterator<int64_t> it(0);
-    cub::TransformInputIterator<bool, FlagIter, cub::CountingInputIterator<int64_t>> flags(it, FlagIter{bits});
-    size_t bytes = (size_t)workspace_bytes;
-    OGM_CUDA_TRY(cub::DeviceSelect::Flagged(workspace, bytes, it, flags, out_idx, out_count, n,
-                                            as_stream(stream)));
-    return OGM_OK;
+    return ogm_keep_rows(n, bits, 0, nullptr, 0, nullptr, 0, out_idx, out_count, workspace, workspace_bytes, stream);
 }
 
 int ogm_select_many(int64_t K, int64_t X, int64_t words, int64_t pitch, const uint32_t* sel_a,

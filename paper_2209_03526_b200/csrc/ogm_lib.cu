@@ -17,6 +17,7 @@
 #include "ogm_fss.cuh"
 #include "ogm_engine.cuh"
 #include "ogm_shuffle.cuh"
+#include "ogm_fetch.cuh"
 #include "ogm_trio.cuh"
 #include "ogm_measure.cuh"
 
@@ -29,7 +30,7 @@ using namespace ogm;
 extern "C" {
 
 const char* ogm_last_error(void) { return get_error(); }
-int ogm_abi_version(void) { return 1; }
+int ogm_abi_version(void) { return 2; }
 int ogm_init(void) { return device_init(); }
 
 int ogm_prg_expand(const void* seeds, int64_t n, void* left, void* right, uint8_t* t_left,

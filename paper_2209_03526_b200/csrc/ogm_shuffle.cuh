@@ -1331,6 +1331,16 @@ int ogm_shuffle_online_planned(int64_t rows, const int32_t* const* q2, const int
                                const uint32_t* u_src, const uint32_t* v_src, const uint32_t* w_src,
                                const uint32_t* z_src, uint32_t* const* inter, uint32_t* x1, uint32_t* y1, uint32_t* c1,
                                uint32_t* r3, void* stream) {
+    return ogm_shuffle_online_planned_ex(rows, q2, gdst, srow, a, b, c, u_src, v_src, w_src, 0, z_src, inter, x1, y1,
+                                         c1, r3, stream);
+}
+
+int ogm_shuffle_online_planned_ex(int64_t rows, const int32_t* const* q2, const int32_t* const* gdst,
+                                  const uint16_t* const* srow, const uint32_t* a, const uint32_t* b,
+                                  const uint32_t* c, const uint32_t* u_src, const uint32_t* v_src,
+                                  const uint32_t* w_src, int w_output_order, const uint32_t* z_src,
+                                  uint32_t* const* inter, uint32_t* x1, uint32_t* y1, uint32_t* c1, uint32_t* r3,
+                                  void* stream) {
     using namespace ogm;
     OGM_CHECK_ARG(rows >= 0 && rows < ((int64_t)1 << 31), OGM_ERR_ARG, "rows out of range");
     OGM_CHECK_ARG(q2 && gdst && srow && inter, OGM_ERR_ARG, "plans and scratch are required");
@@ -1363,7 +1373,7 @@ int ogm_shuffle_online_planned(int64_t rows, const int32_t* const* q2, const int
     // above the dual-pass size P2's blind W stays in c1's OUTPUT order: the x1 -> c1 chain kernel
     // then needs no XOR pass (it is MIO-bound) and W streams in c1's own window pass (2-3% at
     // 2^26-2^28; with the dual pass an extra stream costs more than it saves)
-    const bool w_out = ogm_shuffle_online_planned_w_output_order(rows) != 0;
+    const bool w_out = w_output_order != 0;
     plan_chain_kernel<<<g, TT, kChainSmem2, st>>>(q2[0], i0, w_out ? nullptr : (U4)w_src, srow[2], gdst[2], rows, i2,
                                                   (uint4*)x1);
     if (scrub_l2() != OGM_OK) return OGM_ERR_CUDA;

@@ -1,0 +1,117 @@
+"""Fetch of flagged 128-bit rows for the three co-resident parties
+(src/engine.py:220-270, ``sec_fetch_multi`` with a 128-bit id and no
+attributes -- the C5 fetch shape), in the flag-split layout.
+
+The reference builds rows ``flag | id`` (129 bits, 5 words, src/engine.py:
+227-237), shuffles them (src/shuffle.py:80-144), opens the flag column
+(src/rss.py:184-206) and slices the kept rows' ids back out.  Here the rows
+stay split -- the payload as aligned 16-byte rows, the flag as a bit column
+-- because every shuffle step is a row permutation plus XORs of equally laid
+out rows (csrc/ogm_fetch.cuh).  The blinds are drawn in the reference's
+5-word layout and split offline (``ShuffleOffline(flag_split=True)``), so
+the kept records are bit-identical to the reference's.
+
+Online phase (what the C5 fetch bench times):
+  1. payload: the 16-byte three-party shuffle -- one cooperative launch up
+     to 2^21 rows, the chained planned gathers above (shuffle.py);
+  2. flag column: two bit-gather launches (ogm_flag_shuffle_trio), which
+     also write the opened column;
+  3. keep: hand-written compaction copying the kept payload rows of the
+     three new components (ogm_keep_rows).
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import torch
+
+from . import _lib
+from .bits import words_for
+from .shuffle import FLAG_ROW_BITS, ShuffleOffline, shuffle_online_fused, shuffle_online_planned
+
+FUSED_MAX_BYTES = 32 << 20   # one cooperative launch up to 2^21 16-byte rows (measured crossover)
+
+
+class FlaggedFetch:
+    """Offline material and online phase of one fetch of ``rows`` flagged
+    128-bit rows for table id ``tid``.  ``seeds`` = (s12, s23, s31), the
+    pairwise seeds (party 1 holds s12 and s31, and so on)."""
+
+    def __init__(self, seeds: tuple, tid: int, rows: int, device=None, perm_cache=None, plan: bool | None = None):
+        s12, s23, s31 = seeds
+        self.rows, self.tid = rows, tid
+        self.dev = torch.device(device or "cuda")
+        self.fused = rows * 16 <= FUSED_MAX_BYTES if plan is None else not plan
+        pairs = [(s12, s31), (s23, s12), (s31, s23)]
+        pc = {} if perm_cache is None else perm_cache
+        self.off = [ShuffleOffline(p + 1, *pairs[p], tid, rows, FLAG_ROW_BITS, device=self.dev, perm_cache=pc,
+                                   plan=not self.fused, flag_split=True) for p in range(3)]
+        p1, p2, p3 = self.off
+        if not self.fused:
+            for o in self.off:
+                o.chain_blinds()
+            # the chained shuffle reads only the source-order blinds; the output-order copies go
+            p1.u = p2.v = None
+            if not p2.w_output_order:
+                p2.w = None
+        # R1 / R2 are held once (P1's pair); P2's and P3's copies are the same tables
+        p2.out_a = p3.out_b = None
+        self.r1, self.r2 = p1.out_a, p1.out_b
+        self.r1f, self.r2f = p1.flag["out_a"], p1.flag["out_b"]
+        nw = words_for(rows)
+
+        def vec():
+            return torch.empty((max(nw, 1),), dtype=torch.int32, device=self.dev)
+
+        self.r3 = torch.empty((rows, 4), dtype=torch.int32, device=self.dev)
+        self.x1f, self.y1f, self.r3f, self.plain = vec(), vec(), vec(), vec()
+        self.inter = ([torch.empty_like(self.r3) for _ in range(3)] if not self.fused
+                      else [torch.empty_like(self.r3) for _ in range(2)])
+        self.outs = [torch.empty((max(rows, 1), 4), dtype=torch.int32, device=self.dev) for _ in range(3)]
+        nb = int(_lib.load().ogm_keep_rows_workspace_bytes(rows))
+        self.ws = torch.empty((nb,), dtype=torch.uint8, device=self.dev)
+        self.count = torch.zeros((1,), dtype=torch.int64, device=self.dev)
+
+    def online(self, flags: list, payload: list) -> None:
+        """The three parties' online fetch over component flags [f1, f2, f3]
+        (packed bit vectors) and payloads [p1, p2, p3] ((rows, 4) int32):
+        leaves the new components' flag column opened in ``plain``, the
+        kept count in ``count`` (device) and the kept records' payload
+        share components in ``outs`` (rows [0, count)).  No host sync."""
+        rows = self.rows
+        if rows == 0:
+            self.count.zero_()
+            return
+        p1, p2, p3 = self.off
+        a, b, c = payload
+        for t in payload:
+            if t.shape != (rows, 4) or not t.is_contiguous():
+                raise ValueError("payload components must be contiguous (rows, 4) tables")
+        if self.fused:
+            shuffle_online_fused(self.off, a, b, c, self.inter[0], self.inter[1], None, self.r3)
+        else:
+            shuffle_online_planned(self.off, a, b, c, self.r3, inter=self.inter)
+        P = _lib.ptr
+        _lib.call("ogm_flag_shuffle_trio", rows, P(p1.k1), P(p2.pi12), P(p2.pi23), P(p3.k3), P(flags[0]),
+                  P(flags[1]), P(flags[2]), P(p1.flag["u"]), P(p2.flag["v"]), P(p2.flag["w"]), P(p3.flag["z"]),
+                  P(self.r1f), P(self.r2f), P(self.x1f), P(self.y1f), None, P(self.r3f), P(self.plain),
+                  _lib.stream_ptr())
+        mats = (ctypes.c_void_p * 3)(P(self.r1), P(self.r2), P(self.r3))
+        outs = (ctypes.c_void_p * 3)(*[P(o) for o in self.outs])
+        _lib.call("ogm_keep_rows", rows, P(self.plain), 3, ctypes.addressof(mats), 4, ctypes.addressof(outs), 4,
+                  None, P(self.count), P(self.ws), self.ws.numel(), _lib.stream_ptr())
+
+    def components(self) -> list:
+        """The shuffled table's new components (R1, R2, R3): payload tables
+        and flag columns, [(payload, flag bits)] * 3."""
+        return [(self.r1, self.r1f), (self.r2, self.r2f), (self.r3, self.r3f)]
+
+    def kept(self) -> int:
+        """Host copy of the kept count (one synchronisation)."""
+        return int(self.count.item())
+
+    def records(self) -> list:
+        """[c1, c2, c3]: the kept rows' payload share components, (k, 4) each."""
+        k = self.kept()
+        return [o[:k] for o in self.outs]

@@ -103,8 +103,15 @@ _TLS = threading.local()
 def _thread_workspace(nbytes: int, dev) -> torch.Tensor:
     """Scratch for the permutation rounds, kept per host thread (each party
     thread launches on its own stream, so reuse is stream-ordered) and grown
-    on demand: one allocation instead of one per permutation."""
-    key = (str(dev), _lib.stream_ptr())   # reuse is ordered only on the same stream
+    on demand: one allocation instead of one per permutation.  Only
+    scratch up to WORKSPACE_CACHE_MAX is kept (large permutations, e.g. 4 GB
+    at 2^28 rows, allocate per call and free with the caching allocator);
+    the key is the stream of ``dev`` itself, not the current device's."""
+    dev = torch.device(dev)
+    if nbytes > WORKSPACE_CACHE_MAX:
+        return torch.empty((nbytes,), dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream(dev).cuda_stream if dev.type == "cuda" else 0
+    key = (str(dev), stream)   # reuse is ordered only on the same stream
     cache = getattr(_TLS, "ws", None)
     if cache is None:
         cache = _TLS.ws = {}
@@ -112,6 +119,14 @@ def _thread_workspace(nbytes: int, dev) -> torch.Tensor:
     if buf is None or buf.numel() < nbytes:
         buf = cache[key] = torch.empty((max(nbytes, 1 << 16),), dtype=torch.uint8, device=dev)
     return buf
+
+
+WORKSPACE_CACHE_MAX = 256 << 20
+
+
+def release_workspaces() -> None:
+    """Drop this thread's cached permutation scratch."""
+    _TLS.ws = {}
 
 
 def seeded_permutation_device(key: bytes, label: bytes, index: int, n: int,

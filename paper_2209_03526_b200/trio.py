@@ -507,8 +507,44 @@ class Trio:
         k = int(kept.value)
         return k, [[o[:k] for o in per] for per in outs]
 
+    def prepare_fetch(self, rows: int) -> None:
+        """Offline phase of the NEXT fetch of ``rows`` flagged 128-bit rows
+        (table id self.table_id): the FlaggedFetch material, parked until
+        fetch_multi consumes it."""
+        from .fetch import FlaggedFetch
+        tid = self.table_id
+        if not hasattr(self, "_prepared_fetch"):
+            self._prepared_fetch = {}
+        self._prepared_fetch[(tid, rows)] = FlaggedFetch((self.s12, self.s23, self.s31), tid, rows, self.dev)
+
+    def _fetch_flagged128(self, group: TrioGroup, flags: list, audit: list) -> TrioRecords:
+        """src/engine.py:220-270 for a group whose rows are a 128-bit id and
+        no attributes (the C5 fetch shape), in the flag-split layout
+        (fetch.FlaggedFetch): same table id, open label and records as the
+        packed-row path, bit for bit."""
+        from .fetch import FlaggedFetch
+        rows = group.count
+        tid = self.table_id
+        self.table_id += 1
+        ff = getattr(self, "_prepared_fetch", {}).pop((tid, rows), None)
+        if ff is None:
+            ff = FlaggedFetch((self.s12, self.s23, self.s31), tid, rows, self.dev)
+        payload = [c if c.dim() == 2 and c.shape[1] == 4 and c.is_contiguous() else
+                   rows2d(c).reshape(rows, -1)[:, :4].contiguous() for c in group.ids]
+        ff.online(list(flags), payload)
+        self.label += 1
+        host = ff.plain[: words_for(rows)].cpu().numpy().view(np.uint32)
+        opened = BitVector(host, rows)
+        self.opened.append((self.label, opened))
+        audit.append(("fetch", opened.to_bits().copy()))
+        k = ff.kept()
+        ids = [o[:k] if 2 * k >= rows else o[:k].clone() for o in ff.outs]
+        return TrioRecords(group.parent_slot, group.parent_record, k, group.id_width, ids, {}, {})
+
     def fetch_multi(self, group: TrioGroup, flags: list, audit: list, online_blinds=None) -> TrioRecords:
         """src/engine.py:220-270."""
+        if group.id_width == 128 and not group.attrs and group.count > 0:
+            return self._fetch_flagged128(group, flags, audit)
         names = sorted(group.attrs)
         widths = [group.attr_widths[a] for a in names]
         row_width = 1 + group.id_width + sum(widths)
@@ -593,10 +629,15 @@ class Trio:
         three per-party device shares from graphs.device_trio (component j is
         party j's share_a).  ``native`` runs the schedule in the C++ executor
         (ogm_trio_match: one C-ABI call); ``native=False`` issues the same
-        steps from Python (kept as the readable restatement, tested equal)."""
+        steps from Python (kept as the readable restatement, tested equal).
+        The native executor takes at most OGM_TRIO_MAX_ATTRS needed
+        attributes per slot; wider slots run the Python schedule (the
+        reference has no such limit)."""
         if native:
-            from .trio_native import match_native
-            return match_native(self, tokens, gshares, any_mode)
+            from .trio_native import MAX_ATTRS, match_native
+            slots = tokens[0].structure["slots"] if tokens else []
+            if all(len({p["attr"] for p in sl["preds"]}) <= MAX_ATTRS for sl in slots):
+                return match_native(self, tokens, gshares, any_mode)
         schema = gshares[0].schema
         for t in tokens:
             if t.schema_digest != schema.digest():

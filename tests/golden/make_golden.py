@@ -347,6 +347,49 @@ def shuffle_fixture(ref):
     np.savez_compressed(OUT / "shuffle.npz", **out)
 
 
+def c5_fetch_fixture(ref):
+    """sec_fetch_multi at the C5 fetch shape (src/engine.py:220-270): rows =
+    flag bit + 128-bit id, no attributes, ~10% of the rows flagged; 4096
+    rows (the largest size the pure-Python reference runs in seconds)."""
+    from oblivgm import rss
+    from oblivgm.bits import BitVector
+    from oblivgm.engine import CandidateGroup, _OpenLabels, sec_fetch_multi
+    from oblivgm.net import local_runtimes, make_session_configs, run_trio
+
+    out = {}
+    for ci, (rows, p) in enumerate(((4096, 0.1), (777, 0.01), (64, 1.0))):
+        rng = np.random.default_rng(900 + ci)
+        ids = [rng.integers(0, 1 << 32, size=(rows, 4), dtype=np.uint32) for _ in range(3)]
+        plain = (rng.random(rows) < p).astype(np.uint8)
+        fsh = rss.share(BitVector.from_bits(plain), rng)
+        groups = [CandidateGroup(None, None, rows, 128, ids[q], ids[(q + 1) % 3], {}, {}) for q in range(3)]
+        master = bytes([0xC5, ci]) * 8
+        runtimes = local_runtimes(make_session_configs(master))
+
+        def worker(rt):
+            audit = []
+            return sec_fetch_multi(rt, groups[rt.index - 1], fsh[rt.index - 1], _OpenLabels(), audit), audit
+
+        res = run_trio(worker, runtimes)
+        tag = f"cf{ci}"
+        out[f"{tag}_rows"] = np.array(rows)
+        out[f"{tag}_master"] = np.frombuffer(master, np.uint8)
+        for c in range(3):
+            out[f"{tag}_id{c}"] = ids[c]
+            out[f"{tag}_flag{c}"] = fsh[c].share_a.words
+        for q in range(3):
+            recs, audit = res[q]
+            out[f"{tag}_n{q}"] = np.array(len(recs))
+            out[f"{tag}_ida{q}"] = (np.stack([r.vertex_id.share_a.words for r in recs]) if recs
+                                    else np.zeros((0, 4), np.uint32))
+            out[f"{tag}_idb{q}"] = (np.stack([r.vertex_id.share_b.words for r in recs]) if recs
+                                    else np.zeros((0, 4), np.uint32))
+            out[f"{tag}_audit{q}"] = audit[0][1]
+            out[f"{tag}_digest{q}"] = np.frombuffer(bytes.fromhex(runtimes[q].transcript_digest()), np.uint8)
+    out["cases"] = np.array([f"cf{i}" for i in range(3)])
+    np.savez_compressed(OUT / "c5fetch.npz", **out)
+
+
 CAMPUS = Path("/root/reference/pkg/demos/data/campus.graph")
 TWO_PERSON = Path("/root/reference/pkg/demos/data/two-person.query")
 
@@ -444,6 +487,11 @@ def storage_fixture(ref):
 
 def main():
     sys.path.insert(0, str(REF))
+    if len(sys.argv) > 1:   # e.g. `make_golden.py c5_fetch_fixture`: regenerate the named fixtures only
+        import oblivgm as ref
+        for name in sys.argv[1:]:
+            globals()[name](ref)
+        return
     import oblivgm as ref
     from oblivgm import fss, prf, rss
 
@@ -454,6 +502,7 @@ def main():
     shuffle_fixture(ref)
     match_fixture(ref)
     storage_fixture(ref)
+    c5_fetch_fixture(ref)
     for p in sorted(OUT.glob("*.npz")):
         print(p.name, p.stat().st_size)
 

@@ -1,0 +1,146 @@
+"""The C5 fetch: sec_fetch_multi of flag + 128-bit id rows (src/engine.py:
+220-270), shuffle -> open the flag column -> keep the flagged rows.
+
+* CPU: the oracle restatement (oracle.fetch_multi_trio) against the live
+  reference's recorded runs (tests/golden/c5fetch.npz, make_golden.py).
+* GPU: the flag-split fetch (fetch.FlaggedFetch, the C5 bench path) against
+  the oracle at up to 2^20 rows on both shuffle executions, the Trio API on
+  the golden, and the per-party drop-in path against the split path.
+"""
+
+import hashlib
+
+import numpy as np
+import pytest
+
+import oracle
+
+
+def _seeds(master: bytes):
+    """src/net.py:221-233 pair seeds (s12, s23, s31)."""
+    d = lambda s: hashlib.sha256(master + b"/" + s.encode()).digest()[:16]  # noqa: E731
+    return d("pair-seed-12"), d("pair-seed-23"), d("pair-seed-31")
+
+
+def _case(g, tag):
+    rows = int(g[f"{tag}_rows"])
+    master = g[f"{tag}_master"].tobytes()
+    ids = [g[f"{tag}_id{c}"] for c in range(3)]
+    flags = [g[f"{tag}_flag{c}"] for c in range(3)]
+    return rows, master, ids, flags
+
+
+def test_oracle_fetch_matches_reference(golden):
+    g = golden("c5fetch")
+    for tag in g["cases"]:
+        rows, master, ids, flags = _case(g, tag)
+        keep, plain, recs = oracle.fetch_multi_trio(*_seeds(master), 0, flags, ids, 128)
+        for q in range(3):
+            assert np.array_equal(plain, g[f"{tag}_audit{q}"]), tag
+            assert int(g[f"{tag}_n{q}"]) == keep.size
+            assert np.array_equal(recs[q], g[f"{tag}_ida{q}"].reshape(-1, 4)), (tag, q)
+            assert np.array_equal(recs[(q + 1) % 3], g[f"{tag}_idb{q}"].reshape(-1, 4)), (tag, q)
+
+
+# ---------------------------------------------------------------------------
+# GPU
+# ---------------------------------------------------------------------------
+
+
+def _dev(a):
+    import torch
+    return torch.from_numpy(np.ascontiguousarray(a, np.uint32).view(np.int32).copy()).cuda()
+
+
+def _inputs(rows: int, p: float, seed: int):
+    rng = np.random.default_rng(seed)
+    ids = [rng.integers(0, 1 << 32, size=(rows, 4), dtype=np.uint32) for _ in range(3)]
+    plain = (rng.random(rows) < p).astype(np.uint8)
+    f1 = oracle.pack_bits(rng.integers(0, 2, rows, dtype=np.uint8))
+    f2 = oracle.pack_bits(rng.integers(0, 2, rows, dtype=np.uint8))
+    f3 = oracle.pack_bits(plain) ^ f1 ^ f2
+    return ids, [f1, f2, f3], plain
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("rows,p,plan", [(1, 1.0, False), (33, 0.5, False), (1000, 0.1, False),
+                                         (1 << 20, 0.1, False), (1 << 20, 0.01, True),
+                                         ((1 << 20) + 77, 1.0, True), (40000, 0.0, True)])
+def test_flagged_fetch_matches_oracle(rows, p, plan):
+    """Records, opened flags and the three new components of the split
+    fetch equal the oracle's sec_fetch_multi bit for bit."""
+    import torch
+
+    from paper_2209_03526_b200.fetch import FlaggedFetch
+
+    seeds = _seeds(bytes([0x5f, rows & 0xFF]) * 8)
+    ids, flags, plain = _inputs(rows, p, rows)
+    ff = FlaggedFetch(seeds, 3, rows, plan=plan)
+    ff.online([_dev(f) for f in flags], [_dev(m) for m in ids])
+    keep, want_plain, want = oracle.fetch_multi_trio(*seeds, 3, flags, ids, 128)
+    got_plain = oracle.unpack_bits(ff.plain.cpu().numpy().view(np.uint32), rows)
+    assert np.array_equal(got_plain, want_plain)
+    recs = ff.records()
+    assert recs[0].shape[0] == keep.size == int(want_plain.sum())
+    for c in range(3):
+        assert np.array_equal(recs[c].cpu().numpy().view(np.uint32), want[c]), c
+    # the shuffled table itself: R_c payload = bits 1..128, flag = bit 0 of the oracle's rows
+    comps5 = [oracle.pack_bits(np.concatenate([oracle.unpack_bits(f, rows)[:, None],
+                                               oracle.unpack_bits(m, 128)], axis=1)) for f, m in zip(flags, ids)]
+    (r1, r2, r3), _ = oracle.shuffle_trio(*seeds, 3, comps5, 129)
+    for (pay, fl), r in zip(ff.components(), (r1, r2, r3)):
+        bits = oracle.unpack_bits(r, 129)
+        assert np.array_equal(pay.cpu().numpy().view(np.uint32), oracle.pack_bits(bits[:, 1:]))
+        assert np.array_equal(oracle.unpack_bits(fl.cpu().numpy().view(np.uint32), rows), bits[:, 0])
+    torch.cuda.synchronize()
+
+
+@pytest.mark.gpu
+def test_trio_fetch_multi_matches_reference_golden(golden):
+    """Trio.fetch_multi (the split path for 128-bit ids) reproduces the live
+    reference's records and opened flags at the C5 fetch shape."""
+    from paper_2209_03526_b200.trio import Trio, TrioGroup
+
+    g = golden("c5fetch")
+    for tag in g["cases"]:
+        rows, master, ids, flags = _case(g, tag)
+        trio = Trio(master)
+        group = TrioGroup(None, None, rows, 128, [_dev(m) for m in ids], {}, {})
+        audit = []
+        rec = trio.fetch_multi(group, [_dev(f) for f in flags], audit)
+        assert np.array_equal(audit[0][1], g[f"{tag}_audit0"])
+        assert rec.count == int(g[f"{tag}_n0"])
+        for q in range(3):
+            assert np.array_equal(rec.ids[q].cpu().numpy().view(np.uint32), g[f"{tag}_ida{q}"].reshape(-1, 4))
+
+
+@pytest.mark.gpu
+def test_per_party_fetch_equals_split_fetch(golden):
+    """The per-party drop-in sec_fetch_multi (three threads, packed 5-word
+    rows) gives the same records and transcript digests as the reference;
+    the split trio path gives the same records."""
+    from paper_2209_03526_b200.engine import CandidateGroup, _OpenLabels, sec_fetch_multi
+    from paper_2209_03526_b200.net import local_runtimes, make_session_configs, run_trio
+    from paper_2209_03526_b200.rss import DBits, SharedBitVector
+
+    g = golden("c5fetch")
+    for tag in g["cases"]:
+        rows, master, ids, flags = _case(g, tag)
+        rts = local_runtimes(make_session_configs(master), transcript=True)
+
+        def worker(rt):
+            q = rt.index - 1
+            grp = CandidateGroup(None, None, rows, 128, _dev(ids[q]), _dev(ids[(q + 1) % 3]), {}, {})
+            fl = SharedBitVector(rt.index, DBits(_dev(flags[q]), rows), DBits(_dev(flags[(q + 1) % 3]), rows))
+            audit = []
+            return sec_fetch_multi(rt, grp, fl, _OpenLabels(), audit), audit
+
+        res = run_trio(worker, rts)
+        for q in range(3):
+            recs, audit = res[q]
+            assert len(recs) == int(g[f"{tag}_n{q}"])
+            assert np.array_equal(np.asarray(audit[0][1]), g[f"{tag}_audit{q}"])
+            if recs:
+                got = np.stack([r.vertex_id.share_a.words.cpu().numpy().view(np.uint32) for r in recs])
+                assert np.array_equal(got, g[f"{tag}_ida{q}"].reshape(-1, 4))
+            assert rts[q].transcript_digest() == g[f"{tag}_digest{q}"].tobytes().hex()
