@@ -48,13 +48,22 @@ __global__ void __launch_bounds__(256) split_flag_rows_kernel(const uint32_t* __
 }
 
 // Flag column of the 3-party shuffle, phase 1 (P1's x1 and P2's y1 bits):
-//   x1f[i] = (f1 ^ f2)[k1[i]] ^ Uf[i],   y1f[i] = f3[pi12[i]] ^ Vf[i]
-// One warp per 32 output rows = one output word; the bit columns are small
-// (rows / 8 bytes) and stay in L2, so the cost is the index stream.
+//   x1f[i] = f12[k1[i]] ^ Uf[i],   y1f[i] = f3[pi12[i]] ^ Vf[i]
+// (f12 = f1 ^ f2, P1's two components XORed in one streaming pass first).
+// One warp per 32 output rows = one output word.  The bit columns are small
+// (rows / 8 bytes) and stay in L2; what bounds these kernels is the L1
+// rate for uncoalesced loads (~1 sector per clock per SM: every random bit
+// read is its own sector), so each row costs exactly one random read per
+// gather step (profiles/r02_c5_fetch_ncu.md).
+__global__ void __launch_bounds__(256) flag_xor2_kernel(const uint32_t* __restrict__ a, const uint32_t* __restrict__ b,
+                                                        int64_t nw, uint32_t* __restrict__ out) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; w < nw; w += stride) out[w] = a[w] ^ b[w];
+}
+
 __global__ void __launch_bounds__(256) flag_shuffle1_kernel(int64_t rows, const int32_t* __restrict__ k1,
                                                             const int32_t* __restrict__ pi12,
-                                                            const uint32_t* __restrict__ f1,
-                                                            const uint32_t* __restrict__ f2,
+                                                            const uint32_t* __restrict__ f12,
                                                             const uint32_t* __restrict__ f3,
                                                             const uint32_t* __restrict__ uf,
                                                             const uint32_t* __restrict__ vf, uint32_t* __restrict__ x1f,
@@ -64,8 +73,7 @@ __global__ void __launch_bounds__(256) flag_shuffle1_kernel(int64_t rows, const 
         const int64_t i = base + lane_id();
         uint32_t bx = 0, by = 0;
         if (i < rows) {
-            const int32_t j = __ldcs(k1 + i);
-            bx = bit_at(f1, j) ^ bit_at(f2, j);
+            bx = bit_at(f12, __ldcs(k1 + i));
             by = bit_at(f3, __ldcs(pi12 + i));
         }
         const uint32_t wx = __ballot_sync(0xffffffffu, bx), wy = __ballot_sync(0xffffffffu, by);
@@ -264,7 +272,11 @@ int ogm_flag_shuffle_trio(int64_t rows, const int32_t* k1, const int32_t* pi12, 
     OGM_CHECK_ARG(!plain || (r1f && r2f), OGM_ERR_ARG, "the opened column needs R1f and R2f");
     cudaStream_t st = as_stream(stream);
     const int g = grid_for(rows);
-    flag_shuffle1_kernel<<<g, 256, 0, st>>>(rows, k1, pi12, f1, f2, f3, uf, vf, x1f, y1f);
+    const int64_t nw = (rows + 31) / 32;
+    // P1's f1 ^ f2 is staged in r3f's words: phase 1 reads it, only phase 2 writes r3f
+    uint32_t* f12 = r3f;
+    flag_xor2_kernel<<<grid_for(nw), 256, 0, st>>>(f1, f2, nw, f12);
+    flag_shuffle1_kernel<<<g, 256, 0, st>>>(rows, k1, pi12, f12, f3, uf, vf, x1f, y1f);
     flag_shuffle2_kernel<<<g, 256, 0, st>>>(rows, pi23, k3, x1f, y1f, wf, zf, r1f, r2f, c1f, r3f, plain);
     OGM_LAUNCH_CHECK();
     return OGM_OK;

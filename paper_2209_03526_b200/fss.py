@@ -14,6 +14,8 @@ warp reads key k with coalesced 128-bit loads.
 
 from __future__ import annotations
 
+import functools
+import itertools
 import struct
 from dataclasses import dataclass
 
@@ -92,13 +94,13 @@ class FssKeyBundle:
             raise ValueError(f"unknown predicate kind {self.predicate_kind!r}")
         if len(self.pairs) != 3:
             raise ValueError("a bundle holds exactly three key pairs")
-        bits = {k.domain_bits for pair in self.pairs for k in pair}
-        if len(bits) != 1:
+        if len(set(k.domain_bits for k in itertools.chain.from_iterable(self.pairs))) > 1:
             raise ValueError("all six keys must share domain_bits")
 
     @property
     def domain_bits(self) -> int:
-        return self.pairs[0][0].domain_bits
+        first, _ = self.pairs[0]
+        return first.domain_bits
 
 
 def is_comparison(key) -> bool:
@@ -309,15 +311,13 @@ def cmp_gen(kind: str, alpha: int, domain_size: int, rng: np.random.Generator):
     if not 0 <= alpha < domain_size:
         raise DomainError(f"alpha {alpha} outside domain of size {domain_size}")
     bits = domain_bits_for(domain_size)
-    full = 1 << bits
-    if kind == KIND_LT:
-        threshold, const = alpha, 0
-    elif kind == KIND_GE:
-        threshold, const = alpha, 1
-    elif kind == KIND_LE:
-        threshold, const = (0, 1) if alpha + 1 == full else (alpha + 1, 0)
-    else:
-        threshold, const = (0, 0) if alpha + 1 == full else (alpha + 1, 1)
+    # every kind is the strict tree "x < t" plus a public constant on key 1;
+    # at the top of the domain "x < 2^bits" is always true, so t wraps to 0
+    # and the constant flips (src/fss.py:199-210)
+    wraps = alpha + 1 == 1 << bits
+    threshold, const = {KIND_LT: (alpha, 0), KIND_GE: (alpha, 1),
+                        KIND_LE: (0, 1) if wraps else (alpha + 1, 0),
+                        KIND_GT: (0, 0) if wraps else (alpha + 1, 1)}[kind]
     k1, k2 = _tree_gen(threshold, bits, rng, comparison=True)
     return _with_const(k1, const), k2
 
@@ -347,16 +347,16 @@ def ic_gen(low: int, high: int, domain_size: int, rng: np.random.Generator,
 
 
 def bundle_gen(kind: str, operands: tuple, domain_size: int, rng: np.random.Generator) -> FssKeyBundle:
-    """src/fss.py:237-249."""
-    def pair():
-        if kind == KIND_EQ:
-            return dpf_gen(operands[0], domain_size, rng)
-        if kind in COMPARISON_KINDS:
-            return cmp_gen(kind, operands[0], domain_size, rng)
-        if kind == KIND_INTERVAL:
-            return ic_gen(operands[0], operands[1], domain_size, rng)
+    """src/fss.py:237-249: three independent pairs, generated one after the other."""
+    if kind == KIND_EQ:
+        make = functools.partial(dpf_gen, operands[0], domain_size, rng)
+    elif kind in COMPARISON_KINDS:
+        make = functools.partial(cmp_gen, kind, operands[0], domain_size, rng)
+    elif kind == KIND_INTERVAL:
+        make = functools.partial(ic_gen, operands[0], operands[1], domain_size, rng)
+    else:
         raise ValueError(f"unknown predicate kind {kind!r}")
-    return FssKeyBundle(kind, (pair(), pair(), pair()))
+    return FssKeyBundle(kind, tuple(make() for _ in range(3)))
 
 
 # ---------------------------------------------------------------------------
@@ -415,80 +415,73 @@ def full_domain_eval(key, n: int) -> BitVector:
 # serialization (src/fss.py:351-469), byte-identical wire form
 # ---------------------------------------------------------------------------
 
-_CMP_HEADER = struct.Struct("<BBBB")
+# Tree key: <tag, domain_bits, add_const, root_t> + 16-byte root seed, then
+# per level the 16-byte seed correction and the control byte, then final_cw.
+# Interval key: <tag, domain_bits, closed flags, 0> + two length-prefixed
+# tree keys (lower, upper).
+_HEAD = struct.Struct("<BBBB")
+_U32 = struct.Struct("<I")
+_LEVEL = np.dtype([("cw", "<u8", (2,)), ("ctrl", "u1")])   # 17 bytes, packed
 
 
 def _serialize_tree_key(key) -> bytes:
+    levels = np.empty(key.domain_bits, dtype=_LEVEL)
+    levels["cw"] = np.asarray(key.seed_cw, np.uint64).reshape(key.domain_bits, 2)
+    levels["ctrl"] = np.asarray(key.ctrl_cw, np.uint8)
     tag = _TAG_DCF if is_comparison(key) else _TAG_DPF
-    out = bytearray(_CMP_HEADER.pack(tag, key.domain_bits, key.add_const, key.root_t))
-    out += key.root_seed
-    for lvl in range(key.domain_bits):
-        out += np.ascontiguousarray(key.seed_cw[lvl], np.uint64).tobytes()
-        out.append(int(key.ctrl_cw[lvl]))
-    out.append(key.final_cw)
-    return bytes(out)
+    return b"".join((_HEAD.pack(tag, key.domain_bits, key.add_const, key.root_t), bytes(key.root_seed),
+                     levels.tobytes(), bytes([key.final_cw])))
 
 
 def serialize_key(key) -> bytes:
-    if type(key).__name__ == "IntervalKey":
-        flags = (1 if key.closed_low else 0) | (2 if key.closed_high else 0)
-        lo = _serialize_tree_key(key.lower)
-        up = _serialize_tree_key(key.upper)
-        head = struct.pack("<BBBB", _TAG_INTERVAL, key.domain_bits, flags, 0)
-        return head + struct.pack("<I", len(lo)) + lo + struct.pack("<I", len(up)) + up
-    return _serialize_tree_key(key)
+    if type(key).__name__ != "IntervalKey":
+        return _serialize_tree_key(key)
+    flags = int(bool(key.closed_low)) | (int(bool(key.closed_high)) << 1)
+    parts = [_HEAD.pack(_TAG_INTERVAL, key.domain_bits, flags, 0)]
+    for sub in (key.lower, key.upper):
+        blob = _serialize_tree_key(sub)
+        parts += [_U32.pack(len(blob)), blob]
+    return b"".join(parts)
 
 
 def _parse_tree_key(buf: bytes, offset: int = 0):
-    tag, bits, add_const, root_t = _CMP_HEADER.unpack_from(buf, offset)
+    """(key, end offset) of the tree key at ``offset``."""
+    tag, bits, add_const, root_t = _HEAD.unpack_from(buf, offset)
     if tag not in (_TAG_DPF, _TAG_DCF):
         raise ValueError(f"bad key tag {tag}")
-    pos = offset + _CMP_HEADER.size
-    root_seed = bytes(buf[pos:pos + SEED_BYTES])
-    if len(root_seed) != SEED_BYTES:
+    seed_at = offset + _HEAD.size
+    levels_at = seed_at + SEED_BYTES
+    final_at = levels_at + bits * _LEVEL.itemsize
+    if final_at + 1 > len(buf):
         raise ValueError("truncated key")
-    pos += SEED_BYTES
-    seed_cw = np.zeros((bits, 2), np.uint64)
-    ctrl_cw = np.zeros(bits, np.uint8)
-    for lvl in range(bits):
-        chunk = buf[pos:pos + SEED_BYTES + 1]
-        if len(chunk) != SEED_BYTES + 1:
-            raise ValueError("truncated key")
-        seed_cw[lvl] = np.frombuffer(chunk[:SEED_BYTES], np.uint64)
-        ctrl_cw[lvl] = chunk[SEED_BYTES]
-        pos += SEED_BYTES + 1
-    if pos + 1 > len(buf):
-        raise ValueError("truncated key")
-    final_cw = buf[pos]
-    pos += 1
+    levels = np.frombuffer(buf, dtype=_LEVEL, count=bits, offset=levels_at)
     cls = DcfKey if tag == _TAG_DCF else DpfKey
-    return cls(domain_bits=bits, root_seed=root_seed, root_t=root_t, seed_cw=seed_cw,
-               ctrl_cw=ctrl_cw, final_cw=final_cw, add_const=add_const), pos
+    key = cls(domain_bits=bits, root_seed=bytes(buf[seed_at:levels_at]), root_t=root_t,
+              seed_cw=levels["cw"].copy(), ctrl_cw=levels["ctrl"].copy(), final_cw=buf[final_at],
+              add_const=add_const)
+    return key, final_at + 1
 
 
 def parse_key(buf: bytes):
     if not buf:
         raise ValueError("empty key buffer")
-    if buf[0] == _TAG_INTERVAL:
-        _, bits, flags, _ = struct.unpack_from("<BBBB", buf, 0)
-        pos = 4
-        (lo_len,) = struct.unpack_from("<I", buf, pos)
-        pos += 4
-        lower, end = _parse_tree_key(buf, pos)
-        if end - pos != lo_len:
+    if buf[0] != _TAG_INTERVAL:
+        key, end = _parse_tree_key(buf, 0)
+        if end != len(buf):
+            raise ValueError("trailing bytes after key")
+        return key
+    _, bits, flags, _ = _HEAD.unpack_from(buf, 0)
+    subs, pos = [], _HEAD.size
+    for last in (False, True):
+        (declared,) = _U32.unpack_from(buf, pos)
+        sub, end = _parse_tree_key(buf, pos + _U32.size)
+        if end - (pos + _U32.size) != declared or (last and end != len(buf)):
             raise ValueError("interval sub-key length mismatch")
+        subs.append(sub)
         pos = end
-        (up_len,) = struct.unpack_from("<I", buf, pos)
-        pos += 4
-        upper, end = _parse_tree_key(buf, pos)
-        if end - pos != up_len or end != len(buf):
-            raise ValueError("interval sub-key length mismatch")
-        if not is_comparison(lower) or not is_comparison(upper):
-            raise ValueError("interval sub-keys must be comparison keys")
-        if lower.domain_bits != bits or upper.domain_bits != bits:
-            raise ValueError("interval sub-key domain mismatch")
-        return IntervalKey(lower, upper, bool(flags & 1), bool(flags & 2))
-    key, end = _parse_tree_key(buf, 0)
-    if end != len(buf):
-        raise ValueError("trailing bytes after key")
-    return key
+    lower, upper = subs
+    if not (is_comparison(lower) and is_comparison(upper)):
+        raise ValueError("interval sub-keys must be comparison keys")
+    if {lower.domain_bits, upper.domain_bits} != {bits}:
+        raise ValueError("interval sub-key domain mismatch")
+    return IntervalKey(lower, upper, bool(flags & 1), bool(flags & 2))

@@ -145,36 +145,40 @@ class PeerLink:
 
 @dataclass
 class PhaseStats:
+    """Frames, wire bytes and logical bits sent (src/net.py:168-178)."""
+
     bytes_sent: int = 0
     frames_sent: int = 0
     logical_bits: int = 0
 
     def add(self, nbytes: int, bits: int) -> None:
-        self.bytes_sent += nbytes
-        self.frames_sent += 1
-        self.logical_bits += bits
+        self.bytes_sent, self.frames_sent, self.logical_bits = (
+            self.bytes_sent + nbytes, self.frames_sent + 1, self.logical_bits + bits)
 
 
 class Meter:
-    """Per-party traffic accounting by phase (src/net.py:180-199)."""
+    """Per-party traffic accounting by protocol phase (src/net.py:180-199):
+    sends count toward the total and toward the innermost open phase
+    ("(none)" outside every phase)."""
 
     def __init__(self):
-        self.phases: dict[str, PhaseStats] = {}
         self.total = PhaseStats()
-        self._stack: list[str] = []
+        self.phases: dict[str, PhaseStats] = {}
+        self._open: list[str] = []
 
     @contextmanager
     def phase(self, name: str):
-        self._stack.append(name)
+        depth = len(self._open)
+        self._open.append(name)
         try:
             yield
         finally:
-            self._stack.pop()
+            del self._open[depth:]
 
     def record_send(self, nbytes: int, logical_bits: int) -> None:
-        self.total.add(nbytes, logical_bits)
-        name = self._stack[-1] if self._stack else "(none)"
-        self.phases.setdefault(name, PhaseStats()).add(nbytes, logical_bits)
+        current = self._open[-1] if self._open else "(none)"
+        for stats in (self.total, self.phases.setdefault(current, PhaseStats())):
+            stats.add(nbytes, logical_bits)
 
 
 @dataclass
@@ -218,18 +222,13 @@ class PartyRuntime:
                  recv_timeout: float = 120.0, device: int | None = None):
         from .rss import ZeroShareContext
 
-        self.index = config.party_index
-        self.session = config.session
-        self.config = config
-        self.links = links
-        self.zs = ZeroShareContext(config.zero_key_own, config.zero_key_prev)
-        self.seed_with_next = config.seed_with_next
-        self.seed_with_prev = config.seed_with_prev
+        self.config, self.links, self.recv_timeout = config, links, recv_timeout
+        self.index, self.session = config.party_index, config.session
+        self.seed_with_next, self.seed_with_prev = config.seed_with_next, config.seed_with_prev
+        self.zs = ZeroShareContext(config.zero_key_own, config.zero_key_prev)   # src/rss.py:129-154
         self.meter = Meter()
-        self.opened: list[tuple[int, object]] = []
-        self.recv_timeout = recv_timeout
-        self._next = next_party(self.index)
-        self._prev = prev_party(self.index)
+        self.opened: list[tuple[int, object]] = []   # (label, plaintext) of every open, in order
+        self._next, self._prev = next_party(self.index), prev_party(self.index)
         self._table_counter = 0
         self._transcript = transcript
         self.device = torch.device("cuda", torch.cuda.current_device() if device is None else device)
@@ -324,12 +323,10 @@ def run_trio(worker, runtimes: list[PartyRuntime], close_channels=None):
         t.start()
     for t in threads:
         t.join()
-    real = [e for e in errors if e is not None and not _is_channel_closed(e)]
-    if real:
-        raise real[0]
-    closed = [e for e in errors if e is not None]
-    if closed:
-        raise closed[0]
+    # the root cause first: a party that failed on its own, not on a channel another party closed
+    failures = sorted((e for e in errors if e is not None), key=_is_channel_closed)
+    if failures:
+        raise failures[0]
     return results
 
 

@@ -186,19 +186,28 @@ def _record_table(schema: GraphSchema):
     return hdr, width, mat, dst, layout, pos
 
 
+def _container_party(buf: bytes, magic: bytes, schema: GraphSchema, kind: str) -> int:
+    """Check a container header (src/storage.py:108-127, 255-268): length,
+    magic, version and schema digest; returns the party index.  ``kind`` is
+    "graph" or "result" (the error texts differ as in the reference)."""
+    noun = {"graph": ("graph share", "graph share file", "graph share"),
+            "result": ("result share", "result file", "result file")}[kind]
+    if len(buf) < _CONTAINER_HEADER.size:
+        raise StorageError(f"truncated {noun[1]}")
+    got_magic, version, party, digest = _CONTAINER_HEADER.unpack_from(buf, 0)
+    for ok, msg in ((got_magic == magic, f"not a {noun[0]} file"),
+                    (version == VERSION, f"unsupported {noun[2]} version {version}"),
+                    (digest == schema.digest(), f"{noun[2]} does not match the schema sidecar")):
+        if not ok:
+            raise StorageError(msg)
+    return party
+
+
 def load_graph_share(path, schema: GraphSchema, device="cuda") -> GraphShare:
     """src/storage.py:110-169; returns a GraphShare whose matrices live in HBM
     (``device=None``: host numpy, parsed the same way)."""
     buf = Path(path).read_bytes()
-    if len(buf) < _CONTAINER_HEADER.size:
-        raise StorageError("truncated graph share file")
-    magic, version, party, digest = _CONTAINER_HEADER.unpack_from(buf, 0)
-    if magic != GRAPH_MAGIC:
-        raise StorageError("not a graph share file")
-    if version != VERSION:
-        raise StorageError(f"unsupported graph share version {version}")
-    if digest != schema.digest():
-        raise StorageError("graph share does not match the schema sidecar")
+    party = _container_party(buf, GRAPH_MAGIC, schema, "graph")
     hdr, width, mats, dsts, layout, end = _record_table(schema)
     if end != len(buf):
         raise StorageError("trailing bytes in graph share file" if end < len(buf) else "truncated graph share file")
@@ -277,23 +286,13 @@ def save_results(path, results: MatchResultSet, schema: GraphSchema) -> None:
 
 def load_results(path, schema: GraphSchema, device="cuda") -> MatchResultSet:
     buf = Path(path).read_bytes()
-    if len(buf) < _CONTAINER_HEADER.size:
-        raise StorageError("truncated result file")
-    magic, version, party, digest = _CONTAINER_HEADER.unpack_from(buf, 0)
-    if magic != RESULT_MAGIC:
-        raise StorageError("not a result share file")
-    if version != VERSION:
-        raise StorageError(f"unsupported result file version {version}")
-    if digest != schema.digest():
-        raise StorageError("result file does not match the schema sidecar")
-    pos = _CONTAINER_HEADER.size
-    (json_len,) = struct.unpack_from("<I", buf, pos)
-    pos += 4
+    party = _container_party(buf, RESULT_MAGIC, schema, "result")
+    (json_len,) = struct.unpack_from("<I", buf, _CONTAINER_HEADER.size)
+    pos = _CONTAINER_HEADER.size + 4 + json_len
     try:
-        manifest = json.loads(buf[pos:pos + json_len].decode())
+        manifest = json.loads(buf[pos - json_len:pos].decode())
     except (UnicodeDecodeError, json.JSONDecodeError) as exc:
         raise StorageError(f"corrupt result manifest: {exc}") from None
-    pos += json_len
 
     def next_shared(w: int):
         nonlocal pos
@@ -305,16 +304,14 @@ def load_results(path, schema: GraphSchema, device="cuda") -> MatchResultSet:
             raise StorageError("record width does not match the schema")
         return SharedBitVector(party, DBits.from_host(va, device), DBits.from_host(vb, device))
 
-    records = []
-    for s, slot in enumerate(manifest["structure"]["slots"]):
-        ts = schema.types[slot["type"]]
-        needed = sorted({p["attr"] for p in slot["preds"]})
-        out = []
-        for meta in manifest["records"][s]:
-            vid = next_shared(ts.population)
-            attrs = {a: next_shared(ts.attrs[a].domain_size) for a in needed}
-            out.append(MatchedRecord(meta["parent_slot"], meta["parent_record"], vid, attrs))
-        records.append(out)
+    def record(ts, needed: list, meta: dict) -> MatchedRecord:
+        vid = next_shared(ts.population)   # the id first, then the attributes in name order
+        return MatchedRecord(meta["parent_slot"], meta["parent_record"], vid,
+                             {a: next_shared(ts.attrs[a].domain_size) for a in needed})
+
+    slots = manifest["structure"]["slots"]
+    records = [[record(schema.types[slot["type"]], sorted({p["attr"] for p in slot["preds"]}), meta)
+                for meta in metas] for slot, metas in zip(slots, manifest["records"])]
     if pos != len(buf):
         raise StorageError("trailing bytes in result file")
     return MatchResultSet(party, manifest["structure"], records, [tuple(sg) for sg in manifest["subgraphs"]])
