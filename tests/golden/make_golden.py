@@ -413,6 +413,12 @@ def match_fixture(ref):
              ("conj", "Q u U place = Harbin\nQ p P age >= 35\nQ p P age <= 40\nQE u p\n")]
     for name, q in extra:
         runs.append((name, CAMPUS.read_text(), q, 2, 1, b"\x11" * 16, "or"))
+    # BASELINE configs[0] (C1) exactly as bench.py builds it: 1000 vertices, 3 types, k = 2
+    sys.path.insert(0, str(OUT.parent.parent))
+    from paper_2209_03526_b200.graphs import parse_graph_text as our_parse
+    from paper_2209_03526_b200.workloads import tiny_graph_text, tiny_query
+    c1_text = tiny_graph_text(1)
+    runs.append(("c1", c1_text, tiny_query(our_parse(c1_text), 1), 2, 1, b"\x5a" * 16, "or"))
     for trial in range(3):
         rng = np.random.default_rng(7000 + trial)
         g = random_graph(rng, n_vertices=int(rng.integers(90, 150)), n_types=3, avg_degree=5.0)

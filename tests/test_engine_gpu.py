@@ -144,7 +144,7 @@ def test_shuffle_matches_reference(golden):
             assert rts[p].meter.total.bytes_sent == int(g[f"{tag}_bytes{p}"])
 
 
-@pytest.mark.parametrize("name", ["campus", "unique-chain", "conj", "rand0", "rand1", "rand2"])
+@pytest.mark.parametrize("name", ["campus", "unique-chain", "conj", "rand0", "rand1", "rand2", "c1"])
 def test_sec_match_end_to_end_matches_reference(golden, name):
     g = golden("match")
     rec = json.loads(str(g[f"{name}_json"]))
@@ -175,6 +175,24 @@ def test_sec_match_end_to_end_matches_reference(golden, name):
             assert np.array_equal(bits, g[f"{name}_p{p}_open{j}"])
     assert [rt.transcript_digest() for rt in rts] == rec["digests"]
     assert [rt.meter.total.bytes_sent for rt in rts] == rec["bytes"]
+
+
+@pytest.mark.parametrize("native", [True, False])
+def test_c1_config_matches_reference(golden, native):
+    """BASELINE configs[0] (C1: 1000 vertices, 3 types, 3-vertex path, k = 2)
+    share by share: the golden is the live reference's sec_match on exactly
+    the graph, query, seeds and session master bench.py's query_latency leg
+    uses; the per-party drop-in path and the trio path (native executor or
+    Python schedule) reproduce every record share, opened vector, subgraph,
+    transcript digest and byte count."""
+    from paper_2209_03526_b200 import workloads
+    rec = json.loads(str(golden("match")["c1_json"]))
+    assert rec["graph"] == workloads.tiny_graph_text(1)
+    assert rec["query"] == workloads.tiny_query(workloads.tiny_graph(1), 1)
+    assert (rec["k"], rec["seed"], rec["master"]) == (2, 1, (b"\x5a" * 16).hex())
+    if native:
+        test_sec_match_end_to_end_matches_reference(golden, "c1")
+    test_trio_fast_path_matches_reference(golden, "c1", native)
 
 
 def test_open_label_guard_and_and_gate():
@@ -317,7 +335,7 @@ def test_shuffle_planned_path_matches_reference(golden, monkeypatch):
 
 
 @pytest.mark.parametrize("native", [True, False])
-@pytest.mark.parametrize("name", ["campus", "unique-chain", "conj", "rand0", "rand1", "rand2"])
+@pytest.mark.parametrize("name", ["campus", "unique-chain", "conj", "rand0", "rand1", "rand2", "c1"])
 def test_trio_fast_path_matches_reference(golden, name, native):
     """The single-thread trio path (one launch per step for all three parties)
     reproduces the reference's record shares, opened flags and subgraphs --
