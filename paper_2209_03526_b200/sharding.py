@@ -27,6 +27,97 @@ from .bits import words_for
 ALIGN_ROWS = 128  # one AES-CTR block of packed bits
 
 
+class Comm:
+    """The two collectives the sharded stages need, over ``world`` ranks.
+    ``group`` arguments below accept a Comm or a torch.distributed process
+    group (None = the default group)."""
+
+    rank: int = 0
+    world: int = 1
+
+    def all_gather(self, t: torch.Tensor) -> torch.Tensor:
+        """Every rank's ``t`` (same shape on all), concatenated flat in rank order."""
+        raise NotImplementedError
+
+    def all_to_all(self, recv: torch.Tensor, send: torch.Tensor, recv_splits: list, send_splits: list) -> None:
+        """Rows send[sum(send_splits[:r]) : ...] go to rank r; recv holds
+        every rank's rows for this one, in rank order."""
+        raise NotImplementedError
+
+
+class DistComm(Comm):
+    """torch.distributed: NCCL on device tensors (over NVLink); gloo stages
+    device tensors through the host."""
+
+    def __init__(self, group=None):
+        import torch.distributed as dist
+        self.dist, self.group = dist, group
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+        self.host = dist.get_backend(group) == "gloo"
+
+    def all_gather(self, t: torch.Tensor) -> torch.Tensor:
+        flat = t.reshape(-1).contiguous()
+        src = flat.cpu() if self.host else flat
+        out = torch.empty((self.world * flat.numel(),), dtype=flat.dtype, device=src.device)
+        self.dist.all_gather_into_tensor(out, src, group=self.group)
+        return out.to(flat.device)
+
+    def all_to_all(self, recv, send, recv_splits, send_splits) -> None:
+        if not self.host:
+            self.dist.all_to_all_single(recv, send, recv_splits, send_splits, group=self.group)
+            return
+        r = torch.empty(recv.shape, dtype=recv.dtype)
+        self.dist.all_to_all_single(r, send.cpu(), recv_splits, send_splits, group=self.group)
+        recv.copy_(r)
+
+
+class ThreadComm:
+    """``world`` emulated ranks in one process, one thread each, sharing a
+    device (tests): collectives meet at a barrier.  ``comm.rank_view(r)`` is
+    rank r's Comm."""
+
+    def __init__(self, world: int):
+        import threading
+        self.world = world
+        self._barrier = threading.Barrier(world)
+        self._slots: list = [None] * world
+
+    def rank_view(self, rank: int) -> "Comm":
+        return _ThreadRank(self, rank)
+
+
+class _ThreadRank(Comm):
+    def __init__(self, hub: ThreadComm, rank: int):
+        self.hub, self.rank, self.world = hub, rank, hub.world
+
+    def _exchange(self, item):
+        if item is not None and isinstance(item[0], torch.Tensor) and item[0].is_cuda:
+            torch.cuda.current_stream(item[0].device).synchronize()   # the deposit is complete
+        self.hub._slots[self.rank] = item
+        self.hub._barrier.wait()
+        got = list(self.hub._slots)
+        self.hub._barrier.wait()   # every rank has read the slots before they are reused
+        return got
+
+    def all_gather(self, t: torch.Tensor) -> torch.Tensor:
+        got = self._exchange((t.reshape(-1).contiguous(),))
+        return torch.cat([g[0].to(t.device) for g in got])
+
+    def all_to_all(self, recv, send, recv_splits, send_splits) -> None:
+        got = self._exchange((send, list(send_splits)))
+        parts = []
+        for src_send, src_splits in got:
+            off = sum(src_splits[: self.rank])
+            parts.append(src_send[off: off + src_splits[self.rank]].to(recv.device))
+        if parts and recv.numel():
+            recv.copy_(torch.cat(parts))
+
+
+def as_comm(group) -> Comm:
+    return group if isinstance(group, Comm) else DistComm(group)
+
+
 @dataclass(frozen=True)
 class ShardPlan:
     rows: int
@@ -72,11 +163,7 @@ def assemble(gathered: torch.Tensor, plan: ShardPlan) -> torch.Tensor:
 
 
 def all_gather_bits(local: torch.Tensor, plan: ShardPlan, group=None) -> torch.Tensor:
-    import torch.distributed as dist
-    chunk = pad_slice(local, plan)
-    out = torch.empty((plan.world * plan.words_per_rank,), dtype=chunk.dtype, device=chunk.device)
-    dist.all_gather_into_tensor(out, chunk, group=group)
-    return assemble(out, plan)
+    return assemble(as_comm(group).all_gather(pad_slice(local, plan)), plan)
 
 
 def sec_eval_local_packed(comps, words: int, plan: ShardPlan, rank: int, inds, zero_keys, counters) -> torch.Tensor:
@@ -139,14 +226,12 @@ def sharded_sec_eval_trio(comps, words: int, plan: ShardPlan, rank: int, inds, z
     Returns per pass the three parties' full blinded vectors (all ranks),
     i.e. the re-share messages; component j of the result is blinded_{j-1}.
     """
-    import torch.distributed as dist
     packed = sec_eval_local_packed(comps, words, plan, rank, inds, zero_keys, counters)
     nvec, wpr = packed.shape
     if plan.world == 1:
         full = [packed[j][: plan.total_words] for j in range(nvec)]
     else:
-        out = torch.empty((plan.world * nvec * wpr,), dtype=packed.dtype, device=packed.device)
-        dist.all_gather_into_tensor(out, packed.reshape(-1), group=group)
+        out = as_comm(group).all_gather(packed)
         full = assemble_many(out.view(plan.world, nvec, wpr), plan)
     return [[full[ps * 3 + q] for q in range(3)] for ps in range(nvec // 3)]
 
@@ -164,12 +249,10 @@ def sharded_sec_eval_trio(comps, words: int, plan: ShardPlan, rank: int, inds, z
 
 def xor_allreduce(t: torch.Tensor, group=None) -> torch.Tensor:
     """XOR of `t` over all ranks (same shape everywhere): all-gather + fold."""
-    import torch.distributed as dist
-    world = dist.get_world_size(group)
+    comm = as_comm(group)
     flat = t.reshape(-1).contiguous()
-    out = torch.empty((world * flat.numel(),), dtype=flat.dtype, device=flat.device)
-    dist.all_gather_into_tensor(out, flat, group=group)
-    out = out.view(world, flat.numel())
+    out = comm.all_gather(flat).view(comm.world, flat.numel())
+    world = comm.world
     acc = out[0].clone()
     for r in range(1, world):
         acc ^= out[r]
@@ -297,10 +380,9 @@ def _take(rows: int, width: int, src: torch.Tensor, idx: torch.Tensor, r=None, m
 
 
 def exchange_gather(m_local: torch.Tensor, xp: ExchangePlan, width: int, r=None, m3=None, group=None):
-    import torch.distributed as dist
     send = _take(xp.send_idx.numel(), width, m_local, xp.send_idx)
     recv = torch.empty((sum(xp.recv_splits), send.shape[1]), dtype=send.dtype, device=send.device)
-    dist.all_to_all_single(recv, send, xp.recv_splits, xp.send_splits, group=group)
+    as_comm(group).all_to_all(recv, send, xp.recv_splits, xp.send_splits)
     return _take(xp.recv_pos.numel(), width, recv, xp.recv_pos, r=r, m3=m3)
 
 
@@ -350,5 +432,5 @@ class ShardedTrioShuffle:
         return [self.r1, self.r2, r3]
 
 
-__all__ = ["ShardPlan", "pad_slice", "assemble", "all_gather_bits", "sharded_sec_eval_trio", "ExchangePlan",
+__all__ = ["Comm", "DistComm", "ThreadComm", "as_comm", "ShardPlan", "pad_slice", "assemble", "all_gather_bits", "sharded_sec_eval_trio", "ExchangePlan",
            "exchange_plan", "exchange_gather", "ShardedTrioShuffle", "fss"]

@@ -405,11 +405,12 @@ class Trio:
     def _fde(self, keys: list, domain: int) -> torch.Tensor:
         return fss.full_domain(fss.KeyBatch.from_keys(keys, self.dev), domain)
 
-    def sec_eval(self, group: TrioGroup, key_pairs: list, attr: str, domain: int, cache: dict) -> list:
-        """src/engine.py:139-165 for all parties; both passes from one read."""
+    def _pass_indicators(self, key_pairs: list, domain: int, cache: dict) -> list:
+        """Per pass, the six full-domain indicator rows [P1 a, P1 b, P2 a,
+        P2 b, P3 a, P3 b] of one predicate (src/engine.py:150-158), cached
+        per key."""
         parts = [list(zip(fss.key_parts_for_engine(f), fss.key_parts_for_engine(s))) for f, s in key_pairs]
         npass = len(parts[0])
-        comps = group.attrs[attr]
         inds = []
         for ps in range(npass):
             ck = (id(key_pairs[0][0]), ps)
@@ -425,6 +426,13 @@ class Trio:
                         rows[i] = fd[j]
                 cache[ck] = rows
             inds.append(cache[ck])
+        return inds
+
+    def sec_eval(self, group: TrioGroup, key_pairs: list, attr: str, domain: int, cache: dict) -> list:
+        """src/engine.py:139-165 for all parties; both passes from one read."""
+        inds = self._pass_indicators(key_pairs, domain, cache)
+        npass = len(inds)
+        comps = group.attrs[attr]
         rows = group.count
         words = comps[0].shape[1]
         outs = [self._empty(words_for(rows)) for _ in range(3 * npass)]
@@ -624,6 +632,13 @@ class Trio:
         return TrioGroup(parent_slot, parent_rec, k, x_ne, ids, attrs, widths)
 
     # -- full query ----------------------------------------------------------
+    def _root_group(self, gshares: list, vtype: str, ts, needed: list) -> TrioGroup:
+        """Every vertex of the root type is a candidate (src/engine.py:372-379)."""
+        tps = [gs.types[vtype] for gs in gshares]
+        return TrioGroup(None, None, ts.population, ts.population, [t.id_a for t in tps],
+                         {a: [t.attrs[a][0] for t in tps] for a in needed},
+                         {a: ts.attrs[a].domain_size for a in needed})
+
     def match(self, tokens: list, gshares: list, any_mode: str = "or", native: bool = True) -> TrioResult:
         """src/engine.py:352-417 for the three parties at once.  gshares are the
         three per-party device shares from graphs.device_trio (component j is
@@ -652,10 +667,7 @@ class Trio:
             ts = schema.types[vtype]
             needed = sorted({p["attr"] for p in slot["preds"]})
             if s == 0:
-                tps = [gs.types[vtype] for gs in gshares]
-                groups[0] = [TrioGroup(None, None, ts.population, ts.population, [t.id_a for t in tps],
-                                       {a: [t.attrs[a][0] for t in tps] for a in needed},
-                                       {a: ts.attrs[a].domain_size for a in needed})]
+                groups[0] = [self._root_group(gshares, vtype, ts, needed)]
             unique_route = (len(slot["preds"]) == 1 and slot["preds"][0]["kind"] == fss.KIND_EQ
                             and ts.attrs[slot["preds"][0]["attr"]].unique)
             for group in groups[s]:
