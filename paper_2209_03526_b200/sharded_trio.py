@@ -250,6 +250,8 @@ def run_emulated(world: int, fn, device=None) -> list:
     results: list = [None] * world
     errors: list = [None] * world
     dev = torch.device(device or "cuda")
+    if dev.index is None:
+        dev = torch.device("cuda", torch.cuda.current_device())
 
     def run(r):
         try:

@@ -276,7 +276,7 @@ def sharded_fold_trio(mats_local: list, flags_full: list, plan: ShardPlan, rank:
     bit vector of component c (replicated: C/8 bytes).  Returns every
     party's additive fold, identical on all ranks to the unsharded fold."""
     lo, hi = plan.bounds(rank)
-    if lo % 32:
+    if hi > lo and lo % 32:
         raise ValueError("fold shards must start on a 32-row word boundary")
     words = mats_local[0].shape[1] if mats_local[0].dim() == 2 else 0
     w0 = lo // 32
@@ -310,7 +310,7 @@ def sharded_keep(plain_local: torch.Tensor, plan: ShardPlan, rank: int, group=No
     Returns (full opened vector on the host, this rank's kept local rows on
     the device, global position of its first kept row, global kept count)."""
     lo, hi = plan.bounds(rank)
-    if any(plan.bounds(r)[0] % 32 for r in range(plan.world)):
+    if any(b[0] % 32 and b[1] > b[0] for b in (plan.bounds(r) for r in range(plan.world))):
         raise ValueError("keep shards must start on 32-row word boundaries")
     full = all_gather_bits(plain_local, plan, group) if plan.world > 1 else plain_local
     host = full.cpu().numpy().view(np.uint32)
@@ -389,19 +389,38 @@ def exchange_gather(m_local: torch.Tensor, xp: ExchangePlan, width: int, r=None,
 class ShardedTrioShuffle:
     """Offline material + online steps of one shuffle (table id ``tid``) for
     this rank's rows; the concatenation over ranks equals the single-GPU
-    trio shuffle (trio.Trio.shuffle) bit for bit."""
+    trio shuffle (trio.Trio.shuffle) bit for bit.
+
+    At one rank the exchange is the identity, so the online phase IS the
+    single-GPU one (shuffle.ShuffleOffline: the chained planned gathers for
+    16-byte rows, planned gathers per step otherwise).  With more ranks each
+    step is pack -> all-to-all -> unpack; when a rank's table is past
+    PLAN_MIN_BYTES the pack and unpack gathers run planned (partition pass +
+    window pass) like the single-GPU shuffle."""
 
     def __init__(self, seeds: tuple, tid: int, rows: int, width: int, plan: ShardPlan, rank: int, device=None):
         from .prf import seeded_permutation_device
-        from .shuffle import LABEL_BLIND, LABEL_PERM, LABEL_RAND, compose, gather
+        from .shuffle import (LABEL_BLIND, LABEL_PERM, LABEL_RAND, PLAN_MIN_BYTES, GatherPlan, ShuffleOffline,
+                              compose, gather)
         s12, s23, s31 = seeds
         self.width, self.plan, self.rank = width, plan, rank
         dev = device or torch.device("cuda")
         pi12, pi23, pi31 = (seeded_permutation_device(s, LABEL_PERM, tid, rows, device=dev) for s in (s12, s23, s31))
-        k1, k3 = compose(pi31, pi12), compose(pi23, pi31)
         lo, hi = plan.bounds(rank)
         n = hi - lo
         self.lo, self.n = lo, n
+        self.single = None
+        if plan.world == 1:
+            pc = {(s12, tid, rows): pi12, (s23, tid, rows): pi23, (s31, tid, rows): pi31}
+            pairs = [(s12, s31), (s23, s12), (s31, s23)]
+            self.single = [ShuffleOffline(p + 1, *pairs[p], tid, rows, width, device=dev, perm_cache=pc)
+                           for p in range(3)]
+            self.fast = words_for(width) == 4 and rows > 0
+            if self.fast and self.single[0].plan_x1 is not None:
+                for o in self.single:
+                    o.chain_blinds()
+            return
+        k1, k3 = compose(pi31, pi12), compose(pi23, pi31)
         bt = (LABEL_BLIND, tid)
 
         def tab():
@@ -417,19 +436,62 @@ class ShardedTrioShuffle:
         self.r2 = gather(n, width, tab(), r=(s12, LABEL_RAND, tid), row0=lo)
         self.xp = {"x1": exchange_plan(k1, plan, rank), "y1": exchange_plan(pi12, plan, rank),
                    "c1": exchange_plan(pi23, plan, rank), "r3": exchange_plan(k3, plan, rank)}
+        big = n * words_for(width) * 4 >= PLAN_MIN_BYTES
+        self.plans = {}
+        if big:   # local gathers over tables past L2: planned (partition + window passes)
+            for k_, xp in self.xp.items():
+                self.plans[k_] = (GatherPlan(xp.send_idx, words_for(width)) if xp.send_idx.numel() else None,
+                                  GatherPlan(xp.recv_pos, words_for(width)) if xp.recv_pos.numel() else None)
+
+    def _step(self, name: str, m_local, r=None, m3=None, group=None):
+        xp = self.xp[name]
+        pack, unpack = self.plans.get(name, (None, None))
+        w = self.width
+        if pack is None and unpack is None:
+            return exchange_gather(m_local, xp, w, r=r, m3=m3, group=group)
+        nw = words_for(w)
+        send = torch.empty((xp.send_idx.numel(), nw), dtype=torch.int32, device=m_local.device)
+        if pack is not None:
+            pack.run(send, m1=m_local)
+        recv = torch.empty((sum(xp.recv_splits), nw), dtype=torch.int32, device=m_local.device)
+        as_comm(group).all_to_all(recv, send, xp.recv_splits, xp.send_splits)
+        out = torch.empty((xp.recv_pos.numel(), nw), dtype=torch.int32, device=m_local.device)
+        if unpack is not None:
+            unpack.run(out, m1=recv, r=r, m3=m3)
+        return out
 
     def online(self, comps: list, group=None) -> list:
         """comps: this rank's rows of the three components -> new components."""
-        w = self.width
+        if self.single is not None:
+            return self._online_single(comps)
         ab = torch.empty_like(comps[0])
         if ab.numel():
             _lib.call("ogm_xor_words", ab.numel(), _lib.ptr(comps[0]), _lib.ptr(comps[1]), None, _lib.ptr(ab),
                       _lib.stream_ptr())
-        x1 = exchange_gather(ab, self.xp["x1"], w, r=self.u, group=group)          # P1
-        y1 = exchange_gather(comps[2], self.xp["y1"], w, r=self.v, group=group)    # P2
-        c1 = exchange_gather(x1, self.xp["c1"], w, r=self.w, group=group)          # P2
-        r3 = exchange_gather(y1, self.xp["r3"], w, r=self.z, m3=c1, group=group)   # P3
+        x1 = self._step("x1", ab, r=self.u, group=group)            # P1
+        y1 = self._step("y1", comps[2], r=self.v, group=group)      # P2
+        c1 = self._step("c1", x1, r=self.w, group=group)            # P2
+        r3 = self._step("r3", y1, r=self.z, m3=c1, group=group)     # P3
         return [self.r1, self.r2, r3]
+
+    def _online_single(self, comps: list) -> list:
+        from .shuffle import shuffle_online_fused, shuffle_online_planned
+        p1, p2, p3 = self.single
+        a, b, c = comps
+        r3 = torch.empty_like(a)
+        if self.n == 0:
+            return [p1.out_a, p1.out_b, r3]
+        if self.fast and p1.plan_x1 is not None:
+            shuffle_online_planned(self.single, a, b, c, r3)
+        elif self.fast:
+            shuffle_online_fused(self.single, a, b, c, torch.empty_like(a), torch.empty_like(a), None, r3)
+        else:
+            x1, y1, c1 = torch.empty_like(a), torch.empty_like(a), torch.empty_like(a)
+            p1.step_x1(a, b, x1)
+            p2.step_y1(c, y1)
+            p2.step_c1(x1, c1)
+            p3.step_r3(y1, c1, r3)
+        return [p1.out_a, p1.out_b, r3]
 
 
 __all__ = ["Comm", "DistComm", "ThreadComm", "as_comm", "ShardPlan", "pad_slice", "assemble", "all_gather_bits", "sharded_sec_eval_trio", "ExchangePlan",

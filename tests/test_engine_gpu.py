@@ -368,12 +368,16 @@ def test_trio_fast_path_matches_reference(golden, name, native):
             assert np.array_equal(bits, g[f"{name}_p{p}_open{j}"])
 
 
-@pytest.mark.parametrize("world,rows,width", [(1, 1000, 128), (2, 1000, 129), (3, 7001, 70), (8, 50_000, 128)])
+@pytest.mark.parametrize("world,rows,width", [(1, 1000, 128), (2, 1000, 129), (3, 7001, 70), (8, 50_000, 128),
+                                              (1, 1 << 23, 128), (1, 300_000, 129), (2, (1 << 24) + 96, 128)])
 def test_sharded_shuffle_equals_trio_shuffle(world, rows, width):
-    """Row-sharded shuffle (exchange plans + shard blinds at global row offsets)
-    emulated for `world` ranks on one GPU equals the single-GPU trio shuffle."""
+    """Row-sharded shuffle emulated for `world` ranks on one GPU (ThreadComm:
+    one thread per rank, all-to-all at a barrier) equals the single-GPU trio
+    shuffle.  Covers the one-rank path (the single-GPU chained / per-step
+    planned shuffle) and planned pack/unpack gathers (2 x 2^23 rows)."""
     import paper_2209_03526_b200.sharding as sh
     from paper_2209_03526_b200.bits import words_for
+    from paper_2209_03526_b200.sharded_trio import run_emulated
     from paper_2209_03526_b200.trio import Trio
     w = words_for(width)
     g = torch.Generator(device="cuda").manual_seed(rows + world)
@@ -383,34 +387,18 @@ def test_sharded_shuffle_equals_trio_shuffle(world, rows, width):
         for c in comps:
             c[:, -1] &= (1 << (width % 32)) - 1
     trio = Trio(b"\x66" * 16)
-    want = trio.shuffle(comps, width, online_blinds=False)
+    want = [c[:, :w] for c in trio.shuffle(comps, width, online_blinds=False)]
     seeds = (trio.s12, trio.s23, trio.s31)
     plan = sh.ShardPlan(rows, world, align=1)
-    ranks = [sh.ShardedTrioShuffle(seeds, 0, rows, width, plan, r) for r in range(world)]
-    loc = [[c[plan.bounds(r)[0]:plan.bounds(r)[1]] for c in comps] for r in range(world)]
 
-    def exchange(step, srcs, rs, m3s=None):
-        sends = [sh._take(ranks[r].xp[step].send_idx.numel(), width, srcs[r], ranks[r].xp[step].send_idx)
-                 for r in range(world)]
-        outs = []
-        for r in range(world):  # all_to_all: rank r receives sender o's chunk for r
-            parts = []
-            for o in range(world):
-                off = sum(ranks[o].xp[step].send_splits[:r])
-                parts.append(sends[o][off: off + ranks[o].xp[step].send_splits[r]])
-            recv = torch.cat(parts)
-            outs.append(sh._take(ranks[r].xp[step].recv_pos.numel(), width, recv, ranks[r].xp[step].recv_pos,
-                                 r=rs[r], m3=None if m3s is None else m3s[r]))
-        return outs
+    def rank_fn(comm):
+        lo, hi = plan.bounds(comm.rank)
+        shuf = sh.ShardedTrioShuffle(seeds, 0, rows, width, plan, comm.rank)
+        return shuf.online([c[lo:hi].contiguous() for c in comps], comm)
 
-    ab = [loc[r][0] ^ loc[r][1] for r in range(world)]
-    x1 = exchange("x1", ab, [ranks[r].u for r in range(world)])
-    y1 = exchange("y1", [loc[r][2] for r in range(world)], [ranks[r].v for r in range(world)])
-    c1 = exchange("c1", x1, [ranks[r].w for r in range(world)])
-    r3 = exchange("r3", y1, [ranks[r].z for r in range(world)], m3s=c1)
-    assert torch.equal(torch.cat([ranks[r].r1 for r in range(world)]), want[0][:, :w])
-    assert torch.equal(torch.cat([ranks[r].r2 for r in range(world)]), want[1][:, :w])
-    assert torch.equal(torch.cat(r3), want[2][:, :w])
+    outs = run_emulated(world, rank_fn)
+    for j in range(3):
+        assert torch.equal(torch.cat([o[j] for o in outs]), want[j]), j
 
 
 def _np_pack(rows, flag_bits, fields, width, sets):
