@@ -288,7 +288,53 @@ def local_runtimes(configs: list[PartyConfig], recv_timeout: float = 120.0,
         tr = _new_transcript(cfg) if transcript else None
         links = {j: PeerLink(q[(i, j)], q[(j, i)], cfg.session, tr) for j in (1, 2, 3) if j != i}
         out.append(PartyRuntime(cfg, links, tr, recv_timeout, device))
+    meeting = CoResidentMeeting()
+    for rt in out:
+        rt.meeting = meeting   # engine.sec_match's co-resident fast path (off with transcripts)
     return out
+
+
+class CoResidentMeeting:
+    """Where the three co-resident runtimes of one local session meet.
+
+    Each party thread calls ``meet(rt, item, fn)``; the third arrival runs
+    ``fn({1: item1, 2: item2, 3: item3})`` once (on its own CUDA stream, which
+    it synchronises) and every caller gets the result -- or the exception it
+    raised.  A caller whose peers do not arrive within ``rt.recv_timeout``
+    gets a ProtocolError, like a receive that times out."""
+
+    def __init__(self):
+        self._cv = threading.Condition()
+        self._pending: dict = {}
+        self._done: dict = {}    # round -> [result, callers still to collect]
+        self._round = 0
+
+    def meet(self, rt, item, fn):
+        with self._cv:
+            rnd = self._round
+            if rt.index in self._pending:
+                raise ProtocolError(f"party {rt.index} entered the co-resident meeting twice")
+            self._pending[rt.index] = item
+            if len(self._pending) == 3:
+                calls, self._pending = self._pending, {}
+                try:
+                    res = fn(calls)
+                    torch.cuda.current_stream().synchronize()
+                except BaseException as exc:  # noqa: BLE001
+                    res = exc
+                self._done[rnd] = [res, 3]
+                self._round += 1
+                self._cv.notify_all()
+            elif not self._cv.wait_for(lambda: self._round > rnd, timeout=rt.recv_timeout):
+                self._pending.pop(rt.index, None)
+                raise ProtocolError(f"party {rt.index}: co-resident peers did not reach sec_match (timeout)")
+            entry = self._done[rnd]
+            entry[1] -= 1
+            if entry[1] == 0:
+                del self._done[rnd]
+        if isinstance(entry[0], BaseException):
+            raise entry[0]
+        return entry[0]
 
 
 def _is_channel_closed(exc: BaseException) -> bool:

@@ -195,6 +195,49 @@ def test_c1_config_matches_reference(golden, native):
     test_trio_fast_path_matches_reference(golden, "c1", native)
 
 
+@pytest.mark.parametrize("name", ["campus", "c1", "rand1", "rand2"])
+def test_co_resident_sec_match_matches_reference(golden, name):
+    """The drop-in per-party API without transcripts: the three party
+    threads meet and run the native trio executor once (engine.
+    _meet_and_match).  Record shares, opened vectors and subgraphs equal
+    the reference's run; each runtime's zero-share counter, table counter
+    and opened values advance exactly as the per-party protocol's, so a
+    second sec_match on the same runtimes matches the per-party path too."""
+    g = golden("match")
+    rec = json.loads(str(g[f"{name}_json"]))
+    rng = np.random.default_rng(rec["seed"])
+    schema, shares = encrypt_graph(parse_graph_text(rec["graph"]), rec["k"], rng)
+    tokens = gen_token(load_query(rec["query"], schema), schema, rng)
+    dshares = device_trio(shares)
+    cfg = EngineConfig(any_mode=rec["mode"])
+    fast = local_runtimes(make_session_configs(bytes.fromhex(rec["master"])))
+    slow = local_runtimes(make_session_configs(bytes.fromhex(rec["master"])), transcript=True)
+    for rnd in range(2):
+        got = run_trio(lambda rt: sec_match(rt, tokens[rt.index - 1], dshares[rt.index - 1], cfg), fast)
+        want = run_trio(lambda rt: sec_match(rt, tokens[rt.index - 1], dshares[rt.index - 1], cfg), slow)
+        for a, b in zip(got, want):
+            assert a.subgraphs == b.subgraphs
+            assert [len(r) for r in a.records] == [len(r) for r in b.records]
+            for ra, rb in zip(a.records, b.records):
+                for x, y in zip(ra, rb):
+                    assert torch.equal(x.vertex_id.share_a.words, y.vertex_id.share_a.words)
+                    assert torch.equal(x.vertex_id.share_b.words, y.vertex_id.share_b.words)
+                    for n in x.attrs:
+                        assert torch.equal(x.attrs[n].share_a.words, y.attrs[n].share_a.words)
+            assert [(p, list(map(int, v))) for p, v in a.opened_flags] == \
+                [(p, list(map(int, v))) for p, v in b.opened_flags]
+        for f, s in zip(fast, slow):
+            assert (f.zs.counter, f._table_counter) == (s.zs.counter, s._table_counter)
+            assert [(lab, v.to_bits().tolist()) for lab, v in f.opened] == \
+                [(lab, (v if isinstance(v, BitVector) else BitVector(v.words, v.logical_len)).to_bits().tolist())
+                 for lab, v in s.opened]
+        if rnd == 0:
+            assert sorted(list(m) for m in set(open_results(got[:2], schema)[0])) == rec["matches"]
+            for p, r in enumerate(got):
+                for j, (_phase, bits) in enumerate(r.opened_flags):
+                    assert np.array_equal(bits, g[f"{name}_p{p}_open{j}"])
+
+
 def test_open_label_guard_and_and_gate():
     from paper_2209_03526_b200.errors import ProtocolError
     rng = np.random.default_rng(9)

@@ -282,7 +282,9 @@ def run_query(text, qtext, k=2, seed=1, master=b"\x11" * 16, mode="or"):
     tokens = gen_token(load_query(qtext, schema), schema, rng)
     d = device_trio(shares)
     rts = local_runtimes(make_session_configs(master))
-    res = run_trio(lambda rt: sec_match(rt, tokens[rt.index - 1], d[rt.index - 1], EngineConfig(any_mode=mode)), rts)
+    # co_resident=False: the per-party protocol threads (the trio paths are compared against it)
+    res = run_trio(lambda rt: sec_match(rt, tokens[rt.index - 1], d[rt.index - 1],
+                                        EngineConfig(any_mode=mode, co_resident=False)), rts)
     return set(open_results(res[:2], schema)[0]), rts, res, schema, tokens
 
 
@@ -443,7 +445,8 @@ def test_random_corpus_equals_oracle_both_paths():
         d = device_trio(shares)
         master = bytes([trial]) * 16
         rts = local_runtimes(make_session_configs(master))
-        res = run_trio(lambda rt: sec_match(rt, tokens[rt.index - 1], d[rt.index - 1], EngineConfig()), rts)
+        res = run_trio(lambda rt: sec_match(rt, tokens[rt.index - 1], d[rt.index - 1],
+                                            EngineConfig(co_resident=False)), rts)
         assert set(open_results(res[:2], schema)[0]) == want, (trial, qtext)
         tr = Trio(master)
         tres = tr.match(list(tokens), list(d))
