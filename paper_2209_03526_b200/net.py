@@ -215,6 +215,22 @@ def prev_party(i: int) -> int:
     return (i + 1) % 3 + 1
 
 
+_STREAMS: dict = {}
+_STREAMS_LOCK = threading.Lock()
+
+
+def _party_stream(device: torch.device, party: int) -> torch.cuda.Stream:
+    """One CUDA stream per (device, party index), reused by every session:
+    the caching allocator pools blocks per stream, so a fresh stream per
+    session would start from an empty pool (cudaMalloc on every query)."""
+    key = (device.index, party)
+    with _STREAMS_LOCK:
+        st = _STREAMS.get(key)
+        if st is None:
+            st = _STREAMS[key] = torch.cuda.Stream(device=device)
+    return st
+
+
 class PartyRuntime:
     """One party's handle on a live session (src/net.py:236-289), device messages."""
 
@@ -232,7 +248,7 @@ class PartyRuntime:
         self._table_counter = 0
         self._transcript = transcript
         self.device = torch.device("cuda", torch.cuda.current_device() if device is None else device)
-        self.stream = torch.cuda.Stream(device=self.device)
+        self.stream = _party_stream(self.device, self.index)
 
     def _send(self, peer: int, op: int, payload, logical_bits: int) -> None:
         nbytes = self.links[peer].send(op, as_message(payload))

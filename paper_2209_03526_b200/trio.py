@@ -173,7 +173,9 @@ class TrioResult:
                     lst.append(MatchedRecord(batch.parent_slot, batch.parent_record, sv(batch.ids, batch.id_width),
                                              {a: sv(batch.attrs[a], batch.attr_widths[a]) for a in batch.attrs}))
                 recs.append(lst)
-            out.append(MatchResultSet(q + 1, self.structure, recs, self.subgraphs, list(self.opened_flags)))
+            mrs = MatchResultSet(q + 1, self.structure, recs, self.subgraphs, list(self.opened_flags))
+            mrs._trio = self   # engine.open_results reconstructs from the batches when all parties share it
+            out.append(mrs)
         return out
 
 
