@@ -84,6 +84,8 @@ def parse():
     p.add_argument("--no-c4", action="store_true", help="skip the C4 sharded secEval leg")
     p.add_argument("--no-paired", action="store_true", help="skip the paired DPF (or DCF) run")
     p.add_argument("--no-c5", action="store_true", help="skip the C5 shuffle/fetch leg")
+    p.add_argument("--no-live-ref", action="store_true",
+                   help="skip timing the live reference (baseline/_ref) on this host")
     p.add_argument("--c5-logs", default="24,28", help="C5 table sizes (log2 rows), comma separated")
     p.add_argument("--ref-keys", type=int, default=1 << 22, help="keys per reference-arm step")
     p.add_argument("--dry-run", action="store_true",
@@ -337,6 +339,7 @@ def query_latency(steps: int) -> dict:
         out[name] = statistics.median(lat)
         out[name.replace("_ms", "_oracle_equal")] = got == want
     out["matches"] = len(want)
+    out["match_list"] = sorted(list(m) for m in want)
     return out
 
 
@@ -566,6 +569,13 @@ def main():
                "sample": f"{n} keys x 1 point ({args.kind.upper()}, 32-bit) in {dt:.1f}s, "
                          f"oracle/ C port of src/fss.py:257-281 on {cpu_model()}"}
 
+    live = None
+    if rank == 0 and world == 1 and not args.no_live_ref:
+        import bench_reference
+        live = bench_reference.live_reference([int(x) for x in args.c5_logs.split(",") if x])
+        if query is not None and "c1" in live:
+            live["c1"]["matches_equal_ours"] = live["c1"]["matches"] == sorted(query.get("match_list", []))
+
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -573,7 +583,7 @@ def main():
             "scaling": "weak", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
             "config": config_for(args, world), "comm_ranks": comm_ranks,
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "paired": paired, "query_latency": query,
-            "c4_sec_eval": c4, "c5": c5,
+            "c4_sec_eval": c4, "c5": c5, "live_reference": live,
             "gpu_launches": args.steps, "clocks": clk,
             "launch_ms": {"mean": statistics.mean(per_launch), "min": min(per_launch),
                           "max": max(per_launch)},
