@@ -412,14 +412,19 @@ int ogm_shuffle_online_planned(int64_t rows, const int32_t* const* q2, const int
  * 0 = c1's source order like the other blinds. */
 int ogm_shuffle_online_planned_w_output_order(int64_t rows);
 
-/* ogm_shuffle_online_planned with the order of w_src explicit:
- * w_output_order = 1 takes W in c1's output order, 0 in its source order
- * (any table size; the order ogm_shuffle_online_planned_w_output_order
- * returns is the faster one).  ABI version 2. */
+/* ogm_shuffle_online_planned with the orders of P2's and P3's blinds
+ * explicit.  v_order: 0 = y1's source order, 2 = SLOT order of y1's partition
+ * plan (srow[1]).  w_order: 0 = c1's source order (x1 rows), 1 = c1's OUTPUT order
+ * (W then streams in c1's window pass; faster for the sizes
+ * ogm_shuffle_online_planned_w_output_order names), 2 = SLOT order of c1's
+ * partition plan (tile t, slot k holds row t*4096 + srow[2][t*4096 + k]: the
+ * blind is XORed as rows are scattered, no separate pass).  z_order: 0 =
+ * R3's source order (y1 rows), 2 = slot order of R3's partition plan.
+ * ABI version 2. */
 int ogm_shuffle_online_planned_ex(int64_t rows, const int32_t* const* q2, const int32_t* const* gdst,
                                   const uint16_t* const* srow, const uint32_t* a, const uint32_t* b,
-                                  const uint32_t* c, const uint32_t* u_src, const uint32_t* v_src,
-                                  const uint32_t* w_src, int w_output_order, const uint32_t* z_src,
+                                  const uint32_t* c, const uint32_t* u_src, const uint32_t* v_src, int v_order,
+                                  const uint32_t* w_src, int w_order, const uint32_t* z_src, int z_order,
                                   uint32_t* const* inter, uint32_t* x1, uint32_t* y1, uint32_t* c1, uint32_t* r3,
                                   void* stream);
 

@@ -85,7 +85,7 @@ SIGNATURES = {
     "ogm_trio_open_keep": ([_vp, _i64, _i64, _vp, _int, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _vp], _int),
     "ogm_shuffle_online_fused": ([_i64] + [_vp] * 15 + [_vp], _int),
     "ogm_shuffle_online_planned": ([_i64] + [_vp] * 16, _int),
-    "ogm_shuffle_online_planned_ex": ([_i64] + [_vp] * 9 + [_int] + [_vp] * 7, _int),
+    "ogm_shuffle_online_planned_ex": ([_i64] + [_vp] * 8 + [_int, _vp, _int, _vp, _int] + [_vp] * 6, _int),
     "ogm_shuffle_online_planned_w_output_order": ([_i64], _int),
     "ogm_trio_match": ([_vp, _vp, _vp, _i64, _vp], _int),
     "ogm_measure_int_peak": ([ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double)], _int),

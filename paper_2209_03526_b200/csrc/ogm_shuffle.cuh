@@ -537,6 +537,10 @@ constexpr int kTmaThreads = 1024;
 constexpr int kTmaStageBytes = kTmaTile * (16 + 2 + 4);
 constexpr int kTmaSmemBytes = 2 * kTmaStageBytes + 64;
 
+// SLOT_M2: m2 is a blind in SLOT order (tile t, slot k <- source row
+// t*T + srow[t*T + k]) and m4 is null: it is XORed into each row as the row
+// is scattered, with no shared-memory XOR pass over the staged tile.
+template <bool SLOT_M2>
 __global__ void __launch_bounds__(kTmaThreads, 1) plan_partition_tma_kernel(
     const uint4* __restrict__ m1, const uint4* __restrict__ m2, const uint4* __restrict__ m4,
     const uint16_t* __restrict__ srow, const int32_t* __restrict__ gdst, int64_t rows, uint4* __restrict__ inter) {
@@ -582,21 +586,33 @@ __global__ void __launch_bounds__(kTmaThreads, 1) plan_partition_tma_kernel(
         mbar_wait(&bar[s], (parity >> s) & 1);
         parity ^= 1u << s;
         uint4* rs = rows_of(s);
-        if (m2 || m4) {
+        const uint16_t* sr = srow_of(s);
+        const int32_t* gd = gdst_of(s);
+        if (SLOT_M2) {
+            uint4 cur[Q];
+#pragma unroll
+            for (int i = 0; i < Q; i++) cur[i] = ra[i];
+            if (t + G < nfull) load(t + G);   // the next tile's blind streams in during this scatter
 #pragma unroll
             for (int i = 0; i < Q; i++) {
                 const int k = threadIdx.x + i * kTmaThreads;
-                rs[k] = xor4(rs[k], xor4(ra[i], rb[i]));
+                __stcs(inter + gd[k], xor4(rs[sr[k]], cur[i]));
             }
-            __syncthreads();
-            if (t + G < nfull) load(t + G);
-        }
-        const uint16_t* sr = srow_of(s);
-        const int32_t* gd = gdst_of(s);
+        } else {
+            if (m2 || m4) {
 #pragma unroll
-        for (int i = 0; i < Q; i++) {
-            const int k = threadIdx.x + i * kTmaThreads;
-            __stcs(inter + gd[k], rs[sr[k]]);
+                for (int i = 0; i < Q; i++) {
+                    const int k = threadIdx.x + i * kTmaThreads;
+                    rs[k] = xor4(rs[k], xor4(ra[i], rb[i]));
+                }
+                __syncthreads();
+                if (t + G < nfull) load(t + G);
+            }
+#pragma unroll
+            for (int i = 0; i < Q; i++) {
+                const int k = threadIdx.x + i * kTmaThreads;
+                __stcs(inter + gd[k], rs[sr[k]]);
+            }
         }
         __syncthreads();  // stage s fully read before it is refilled
         if (threadIdx.x == 0 && t + 2 * G < nfull) issue(t + 2 * G, s);
@@ -609,7 +625,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) plan_partition_tma_kernel(
         for (int k = threadIdx.x; k < nr; k += kTmaThreads) {
             const int j = __ldcs(srow + b0 + k);
             uint4 v = __ldcs(m1 + b0 + j);
-            if (m2) v = xor4(v, __ldcs(m2 + b0 + j));
+            if (m2) v = xor4(v, __ldcs(m2 + b0 + (SLOT_M2 ? k : j)));
             if (m4) v = xor4(v, __ldcs(m4 + b0 + j));
             __stcs(inter + __ldcs(gdst + b0 + k), v);
         }
@@ -644,6 +660,12 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
+// SLOT_BLIND: `blind` is in the receiver partition's SLOT order (tile t,
+// slot k -> source row t*T + srow[t*T + k], arranged offline), so it is
+// XORed into each row as it is scattered: no separate shared-memory XOR pass
+// over the staged tile (the pass this kernel was MIO-throttled on).  Else
+// `blind` is in source (tile row) order and XORed in place before the scatter.
+template <bool SLOT_BLIND>
 __global__ void __launch_bounds__(kTmaThreads, 1) plan_chain_kernel(
     const int32_t* __restrict__ q, const uint4* __restrict__ inter_a, const uint4* __restrict__ blind,
     const uint16_t* __restrict__ srow, const int32_t* __restrict__ gdst, int64_t rows, uint4* __restrict__ inter_b,
@@ -675,6 +697,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) plan_chain_kernel(
     load_q(0);
     gather(0);
     gather(1);
+    const uint4 z4 = make_uint4(0, 0, 0, 0);
     for (int64_t j = 0; j < nmine; j++) {
         const int64_t t = tile(j);
         uint4 bl[Q];
@@ -683,25 +706,25 @@ __global__ void __launch_bounds__(kTmaThreads, 1) plan_chain_kernel(
 #pragma unroll
         for (int i = 0; i < Q; i++) {
             const int k = threadIdx.x + i * kTmaThreads;
-            bl[i] = blind ? __ldcs(blind + t * T + k) : make_uint4(0, 0, 0, 0);
+            bl[i] = blind ? __ldcs(blind + t * T + k) : z4;
             sr[i] = __ldcs(srow + t * T + k);
             gd[i] = __ldcs(gdst + t * T + k);
         }
         gather(j + 2);   // buffer (j + 2) % 3 was freed by the barrier closing tile j - 1
         cp_async_wait<2>();  // this thread's gathers of tile j have landed
         uint4* rs = buf(j);
-        if (blind || msg) {
+        if ((!SLOT_BLIND && blind) || msg) {
 #pragma unroll
             for (int i = 0; i < Q; i++) {
                 const int k = threadIdx.x + i * kTmaThreads;
                 const uint4 v = rs[k];
                 if (msg) __stcs(msg + t * T + k, v);
-                rs[k] = xor4(v, bl[i]);
+                if (!SLOT_BLIND) rs[k] = xor4(v, bl[i]);
             }
         }
         __syncthreads();
 #pragma unroll
-        for (int i = 0; i < Q; i++) __stcs(inter_b + gd[i], rs[sr[i]]);
+        for (int i = 0; i < Q; i++) __stcs(inter_b + gd[i], SLOT_BLIND ? xor4(rs[sr[i]], bl[i]) : rs[sr[i]]);
         __syncthreads();
     }
     cp_async_wait<0>();
@@ -714,43 +737,91 @@ __global__ void __launch_bounds__(kTmaThreads, 1) plan_chain_kernel(
         for (int k = threadIdx.x; k < nr; k += kTmaThreads) {
             const uint4 m = __ldcg(inter_a + __ldcs(q + b0 + k));
             if (msg) __stcs(msg + b0 + k, m);
-            rs[k] = blind ? xor4(m, __ldcs(blind + b0 + k)) : m;
+            rs[k] = (!SLOT_BLIND && blind) ? xor4(m, __ldcs(blind + b0 + k)) : m;
         }
         __syncthreads();
-        for (int k = threadIdx.x; k < nr; k += kTmaThreads) __stcs(inter_b + __ldcs(gdst + b0 + k), rs[__ldcs(srow + b0 + k)]);
+        for (int k = threadIdx.x; k < nr; k += kTmaThreads) {
+            const uint4 v = rs[__ldcs(srow + b0 + k)];
+            __stcs(inter_b + __ldcs(gdst + b0 + k), (SLOT_BLIND && blind) ? xor4(v, __ldcs(blind + b0 + k)) : v);
+        }
     }
 }
 
 // the last window passes of two planned gathers with the same output order,
-// XORed: R3[i] = Ir[qr[i]] ^ c1[i], c1[i] = Ic[qc[i]] (msg: c1 stored too)
+// XORed: R3[i] = Ir[qr[i]] ^ c1[i], c1[i] = Ic[qc[i]] (msg: c1 stored too).
+// kRows rows per thread per step, all index and window loads issued before
+// any is used.  Measured: 4 rows per thread LOSE (2^24 0.89 -> 0.93 ms, 2^28
+// 16.3 -> 22.4 ms): the grid then spans 4x more output rows at once, i.e.
+// reads from several windows at a time, and the windows stop staying in L2
+// (the same effect as two windows per pass above 256 MB).  One row per thread.
+constexpr int kWinRows = 1;
+
+template <int kRows>
 __global__ void __launch_bounds__(256) win_gather_dual4_kernel(const int32_t* __restrict__ qa,
                                                                const uint4* __restrict__ ia,
                                                                const int32_t* __restrict__ qb,
                                                                const uint4* __restrict__ ib, int64_t rows,
                                                                uint4* __restrict__ out, uint4* __restrict__ msg,
                                                                const uint4* __restrict__ ta) {
-    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < rows; i += stride) {
-        uint4 va = __ldcg(ia + __ldcs(qa + i));
-        if (ta) va = xor4(va, __ldcs(ta + i));
-        const uint4 vb = __ldcg(ib + __ldcs(qb + i));
-        if (msg) __stcs(msg + i, va);
-        __stcs(out + i, xor4(va, vb));
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x * kRows;
+    for (int64_t i0 = (int64_t)blockIdx.x * blockDim.x * kRows + threadIdx.x; i0 < rows; i0 += stride) {
+        int32_t xa[kRows], xb[kRows];
+#pragma unroll
+        for (int u = 0; u < kRows; u++) {
+            const int64_t i = i0 + (int64_t)u * blockDim.x;
+            xa[u] = i < rows ? __ldcs(qa + i) : 0;
+            xb[u] = i < rows ? __ldcs(qb + i) : 0;
+        }
+        uint4 va[kRows], vb[kRows];
+#pragma unroll
+        for (int u = 0; u < kRows; u++) {
+            const int64_t i = i0 + (int64_t)u * blockDim.x;
+            if (i < rows) {
+                va[u] = __ldcg(ia + xa[u]);
+                vb[u] = __ldcg(ib + xb[u]);
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < kRows; u++) {
+            const int64_t i = i0 + (int64_t)u * blockDim.x;
+            if (i < rows) {
+                uint4 a = va[u];
+                if (ta) a = xor4(a, __ldcs(ta + i));
+                if (msg) __stcs(msg + i, a);
+                __stcs(out + i, xor4(a, vb[u]));
+            }
+        }
     }
 }
 
 // pass 2 for 16-byte rows (the C5 shape): a lean kernel, since with
 // window-local sources the instruction count per row matters
+template <int kRows>
 __global__ void __launch_bounds__(256) win_gather4_kernel(const int32_t* __restrict__ q, const uint4* __restrict__ m1,
                                                           const uint4* __restrict__ m3, const uint4* __restrict__ r,
                                                           int64_t rows, uint4* __restrict__ out) {
-    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < rows; i += stride) {
-        const uint4* src = m1 + __ldcs(q + i);
-        uint4 v = __ldcg(src);
-        if (m3) v = xor4(v, __ldcs(m3 + i));
-        if (r) v = xor4(v, __ldcs(r + i));
-        __stcs(out + i, v);
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x * kRows;
+    for (int64_t i0 = (int64_t)blockIdx.x * blockDim.x * kRows + threadIdx.x; i0 < rows; i0 += stride) {
+        int32_t x[kRows];
+#pragma unroll
+        for (int u = 0; u < kRows; u++) {
+            const int64_t i = i0 + (int64_t)u * blockDim.x;
+            x[u] = i < rows ? __ldcs(q + i) : 0;
+        }
+        uint4 v[kRows];
+#pragma unroll
+        for (int u = 0; u < kRows; u++)
+            if (i0 + (int64_t)u * blockDim.x < rows) v[u] = __ldcg(m1 + x[u]);
+#pragma unroll
+        for (int u = 0; u < kRows; u++) {
+            const int64_t i = i0 + (int64_t)u * blockDim.x;
+            if (i < rows) {
+                uint4 w = v[u];
+                if (m3) w = xor4(w, __ldcs(m3 + i));
+                if (r) w = xor4(w, __ldcs(r + i));
+                __stcs(out + i, w);
+            }
+        }
     }
 }
 
@@ -815,8 +886,8 @@ __global__ void __launch_bounds__(1024) perm_rounds3_block_kernel(const __grid_c
 int shuffle_init() {
     OGM_CUDA_TRY(allow_big_smem(perm_draws_kernel<AesTab>, kAesTableBytes));
     OGM_CUDA_TRY(allow_big_smem(shuffle_gather_kernel<true, AesTab>, kAesTableBytes));
-    OGM_CUDA_TRY(prefer_l1(win_gather4_kernel));
-    OGM_CUDA_TRY(prefer_l1(win_gather_dual4_kernel));
+    OGM_CUDA_TRY(prefer_l1(win_gather4_kernel<kWinRows>));
+    OGM_CUDA_TRY(prefer_l1(win_gather_dual4_kernel<kWinRows>));
     OGM_CUDA_TRY(prefer_l1(gather_matrix_kernel));
     OGM_CUDA_TRY(prefer_l1(gather_matrix_rows_kernel));
     return OGM_OK;
@@ -1096,9 +1167,9 @@ int ogm_gather_planned(int64_t rows, int64_t words, int64_t pitch, int64_t tile_
     int64_t g;
     if (!(passes & 1)) {
     } else if (vec && pitch == 4 && tile_rows == kTmaTile) {
-        OGM_CUDA_TRY(allow_big_smem(plan_partition_tma_kernel, kTmaSmemBytes));
+        OGM_CUDA_TRY(allow_big_smem(plan_partition_tma_kernel<false>, kTmaSmemBytes));
         g = std::min<int64_t>(std::max<int64_t>(ntiles, 1), (int64_t)sm_count());
-        plan_partition_tma_kernel<<<(int)g, kTmaThreads, kTmaSmemBytes, st>>>(
+        plan_partition_tma_kernel<false><<<(int)g, kTmaThreads, kTmaSmemBytes, st>>>(
             (const uint4*)m1, (const uint4*)m2, (const uint4*)m4, srow, gdst, rows, (uint4*)inter);
     } else if (vec) {
         OGM_CUDA_TRY(allow_big_smem(plan_partition_kernel<uint4>, (int)smem));
@@ -1120,8 +1191,8 @@ int ogm_gather_planned(int64_t rows, int64_t words, int64_t pitch, int64_t tile_
     }
     if (!(passes & 2)) {
     } else if (pitch == 4 && vec) {
-        int64_t g2 = std::min<int64_t>((rows + 255) / 256, (int64_t)sm_count() * 8);
-        win_gather4_kernel<<<(int)g2, 256, 0, st>>>(q2, (const uint4*)inter, (const uint4*)m3, (const uint4*)r_mat,
+        int64_t g2 = std::min<int64_t>((rows + 256 * kWinRows - 1) / (256 * kWinRows), (int64_t)sm_count() * 8);
+        win_gather4_kernel<kWinRows><<<(int)g2, 256, 0, st>>>(q2, (const uint4*)inter, (const uint4*)m3, (const uint4*)r_mat,
                                                     rows, (uint4*)out);
     } else {
         GatherArgs a{};
@@ -1331,14 +1402,14 @@ int ogm_shuffle_online_planned(int64_t rows, const int32_t* const* q2, const int
                                const uint32_t* u_src, const uint32_t* v_src, const uint32_t* w_src,
                                const uint32_t* z_src, uint32_t* const* inter, uint32_t* x1, uint32_t* y1, uint32_t* c1,
                                uint32_t* r3, void* stream) {
-    return ogm_shuffle_online_planned_ex(rows, q2, gdst, srow, a, b, c, u_src, v_src, w_src, 0, z_src, inter, x1, y1,
-                                         c1, r3, stream);
+    return ogm_shuffle_online_planned_ex(rows, q2, gdst, srow, a, b, c, u_src, v_src, 0, w_src, 0, z_src, 0, inter,
+                                         x1, y1, c1, r3, stream);
 }
 
 int ogm_shuffle_online_planned_ex(int64_t rows, const int32_t* const* q2, const int32_t* const* gdst,
                                   const uint16_t* const* srow, const uint32_t* a, const uint32_t* b,
-                                  const uint32_t* c, const uint32_t* u_src, const uint32_t* v_src,
-                                  const uint32_t* w_src, int w_output_order, const uint32_t* z_src,
+                                  const uint32_t* c, const uint32_t* u_src, const uint32_t* v_src, int v_order,
+                                  const uint32_t* w_src, int w_order, const uint32_t* z_src, int z_order,
                                   uint32_t* const* inter, uint32_t* x1, uint32_t* y1, uint32_t* c1, uint32_t* r3,
                                   void* stream) {
     using namespace ogm;
@@ -1353,8 +1424,12 @@ int ogm_shuffle_online_planned_ex(int64_t rows, const int32_t* const* q2, const 
     if (rows == 0) return OGM_OK;
     OGM_ENSURE_INIT();
     cudaStream_t st = as_stream(stream);
-    OGM_CUDA_TRY(allow_big_smem(plan_partition_tma_kernel, kTmaSmemBytes));
-    OGM_CUDA_TRY(allow_big_smem(plan_chain_kernel, kChainSmem2));
+    OGM_CHECK_ARG((v_order == 0 || v_order == 2) && w_order >= 0 && w_order <= 2 && (z_order == 0 || z_order == 2),
+                  OGM_ERR_ARG, "blind orders: v 0 (source) / 2 (slot), w 0 / 1 (output) / 2, z 0 / 2");
+    OGM_CUDA_TRY(allow_big_smem(plan_partition_tma_kernel<false>, kTmaSmemBytes));
+    OGM_CUDA_TRY(allow_big_smem(plan_partition_tma_kernel<true>, kTmaSmemBytes));
+    OGM_CUDA_TRY(allow_big_smem(plan_chain_kernel<false>, kChainSmem2));
+    OGM_CUDA_TRY(allow_big_smem(plan_chain_kernel<true>, kChainSmem2));
     const int64_t ntiles = (rows + kTmaTile - 1) / kTmaTile;
     const int g = (int)std::min<int64_t>(ntiles, (int64_t)sm_count());
     const bool scrub = rows * 16 >= kScrubMinBytes;
@@ -1367,30 +1442,44 @@ int ogm_shuffle_online_planned_ex(int64_t rows, const int32_t* const* q2, const 
     using U4 = const uint4*;
     uint4 *i0 = (uint4*)inter[0], *i1 = (uint4*)inter[1], *i2 = (uint4*)inter[2];
     constexpr int TT = kTmaThreads;
-    plan_partition_tma_kernel<<<g, TT, kTmaSmemBytes, st>>>((U4)a, (U4)b, (U4)u_src, srow[0], gdst[0], rows, i0);
-    plan_partition_tma_kernel<<<g, TT, kTmaSmemBytes, st>>>((U4)c, (U4)v_src, nullptr, srow[1], gdst[1], rows, i1);
+    plan_partition_tma_kernel<false><<<g, TT, kTmaSmemBytes, st>>>((U4)a, (U4)b, (U4)u_src, srow[0], gdst[0], rows,
+                                                                   i0);
+    if (v_order == 2)
+        plan_partition_tma_kernel<true><<<g, TT, kTmaSmemBytes, st>>>((U4)c, (U4)v_src, nullptr, srow[1], gdst[1],
+                                                                      rows, i1);
+    else
+        plan_partition_tma_kernel<false><<<g, TT, kTmaSmemBytes, st>>>((U4)c, (U4)v_src, nullptr, srow[1], gdst[1],
+                                                                       rows, i1);
     if (scrub_l2() != OGM_OK) return OGM_ERR_CUDA;
     // above the dual-pass size P2's blind W stays in c1's OUTPUT order: the x1 -> c1 chain kernel
     // then needs no XOR pass (it is MIO-bound) and W streams in c1's own window pass (2-3% at
     // 2^26-2^28; with the dual pass an extra stream costs more than it saves)
-    const bool w_out = w_output_order != 0;
-    plan_chain_kernel<<<g, TT, kChainSmem2, st>>>(q2[0], i0, w_out ? nullptr : (U4)w_src, srow[2], gdst[2], rows, i2,
-                                                  (uint4*)x1);
+    const bool w_out = w_order == 1;
+    auto chain = [&](bool slot, const int32_t* q, const uint4* ia, const uint4* bl, const uint16_t* sr,
+                     const int32_t* gd, uint4* ib, uint4* msg) {
+        if (slot)
+            plan_chain_kernel<true><<<g, TT, kChainSmem2, st>>>(q, ia, bl, sr, gd, rows, ib, msg);
+        else
+            plan_chain_kernel<false><<<g, TT, kChainSmem2, st>>>(q, ia, bl, sr, gd, rows, ib, msg);
+    };
+    chain(w_order == 2, q2[0], i0, w_out ? nullptr : (U4)w_src, srow[2], gdst[2], i2, (uint4*)x1);
     if (scrub_l2() != OGM_OK) return OGM_ERR_CUDA;
-    plan_chain_kernel<<<g, TT, kChainSmem2, st>>>(q2[1], i1, (U4)z_src, srow[3], gdst[3], rows, i0, (uint4*)y1);
+    chain(z_order == 2, q2[1], i1, (U4)z_src, srow[3], gdst[3], i0, (uint4*)y1);
     if (scrub_l2() != OGM_OK) return OGM_ERR_CUDA;
-    const int64_t g2 = std::min<int64_t>((rows + 255) / 256, (int64_t)sm_count() * 8);
+    const int64_t g2 = std::min<int64_t>((rows + 256 * kWinRows - 1) / (256 * kWinRows), (int64_t)sm_count() * 8);
     if (rows * 16 <= kDualMaxBytes) {
-        win_gather_dual4_kernel<<<(int)g2, 256, 0, st>>>(q2[2], i2, q2[3], i0, rows, (uint4*)r3, (uint4*)c1,
+        win_gather_dual4_kernel<kWinRows><<<(int)g2, 256, 0, st>>>(q2[2], i2, q2[3], i0, rows, (uint4*)r3, (uint4*)c1,
                                                          w_out ? (U4)w_src : nullptr);
     } else {
         // two random windows at once thrash L2 far above its size (2^26 rows: 2.06 ms and 11 GB read
         // instead of 2.7; smaller windows do not rescue it, scripts/exp_chain_win.py): c1's window
         // pass, then R3's with c1 streamed
         uint4* c1m = c1 ? (uint4*)c1 : i1;
-        win_gather4_kernel<<<(int)g2, 256, 0, st>>>(q2[2], i2, w_out ? (U4)w_src : nullptr, nullptr, rows, c1m);
+        win_gather4_kernel<kWinRows><<<(int)g2, 256, 0, st>>>(
+            q2[2], i2, w_out ? (U4)w_src : nullptr, nullptr, rows, c1m);
         if (scrub_l2() != OGM_OK) return OGM_ERR_CUDA;
-        win_gather4_kernel<<<(int)g2, 256, 0, st>>>(q2[3], i0, c1m, nullptr, rows, (uint4*)r3);
+        win_gather4_kernel<kWinRows><<<(int)g2, 256, 0, st>>>(
+            q2[3], i0, c1m, nullptr, rows, (uint4*)r3);
     }
     OGM_LAUNCH_CHECK();
     return OGM_OK;

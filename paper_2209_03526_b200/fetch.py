@@ -51,8 +51,8 @@ class FlaggedFetch:
         if not self.fused:
             for o in self.off:
                 o.chain_blinds()
-            # the chained shuffle reads only the source-order blinds; the output-order copies go
-            p1.u = p2.v = None
+            # the chained shuffle reads only its chain blinds (chain_blinds); the other copies go
+            p1.u = p2.v = p3.z = None
             if not p2.w_output_order:
                 p2.w = None
         # R1 / R2 are held once (P1's pair); P2's and P3's copies are the same tables
