@@ -200,15 +200,36 @@ __global__ void __launch_bounds__(1024) keep_scan_kernel(const int32_t* __restri
     }
 }
 
+// Emit: each warp walks its chunk 32 mask words at a time.  Kept rows are
+// queued in a per-warp shared-memory list (position, source row) in order;
+// whenever the list could overflow it is flushed with ALL lanes copying one
+// queued row each, so a sparse mask (1% kept) still has 32 independent row
+// copies in flight per warp instead of one at a time.
+constexpr int kKeepQueue = 64;
+
 __global__ void __launch_bounds__(256) keep_emit_kernel(const uint32_t* __restrict__ bits, int64_t rows,
                                                         int64_t nchunks, int64_t chunk_words,
                                                         const int64_t* __restrict__ offsets,
                                                         const __grid_constant__ KeepMats m,
                                                         int32_t* __restrict__ out_idx) {
+    __shared__ int64_t q_pos[8][kKeepQueue];
+    __shared__ int32_t q_row[8][kKeepQueue];
     const int64_t nw = (rows + 31) / 32;
     const int64_t warps = (int64_t)gridDim.x * (blockDim.x / 32);
     const uint32_t lane = lane_id();
+    const int wi = threadIdx.x / 32;
     const uint32_t below = (1u << lane) - 1u;
+    int queued = 0;
+    auto flush = [&]() {
+        __syncwarp();
+        for (int e = (int)lane; e < queued; e += 32) {
+            const int64_t pos = q_pos[wi][e];
+            const int64_t row = q_row[wi][e];
+            for (int j = 0; j < m.n; j++) __stcs(m.out[j] + pos * m.opitch, __ldcs(m.in[j] + row * m.pitch));
+        }
+        __syncwarp();
+        queued = 0;
+    };
     for (int64_t c = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / 32; c < nchunks; c += warps) {
         int64_t base = __ldg(offsets + c);
         const int64_t end = min(nw, (c + 1) * chunk_words);
@@ -222,21 +243,28 @@ __global__ void __launch_bounds__(256) keep_emit_kernel(const uint32_t* __restri
                 if ((int)lane >= o) incl += v;
             }
             const int excl = incl - cnt;
-#pragma unroll 4
             for (int k = 0; k < 32; k++) {
                 const uint32_t word = __shfl_sync(0xffffffffu, mine, k);
-                const int off = __shfl_sync(0xffffffffu, excl, k);
                 if (!word) continue;
+                const int off = __shfl_sync(0xffffffffu, excl, k);
+                const int n = __popc(word);
+                if (m.n && queued + n > kKeepQueue) flush();
                 if ((word >> lane) & 1u) {
-                    const int64_t pos = base + off + __popc(word & below);
+                    const int r = __popc(word & below);
+                    const int64_t pos = base + off + r;
                     const int64_t row = (wb + k) * 32 + lane;
                     if (out_idx) out_idx[pos] = (int32_t)row;
-                    for (int j = 0; j < m.n; j++) __stcs(m.out[j] + pos * m.opitch, __ldcs(m.in[j] + row * m.pitch));
+                    if (m.n) {
+                        q_pos[wi][queued + r] = pos;
+                        q_row[wi][queued + r] = (int32_t)row;
+                    }
                 }
+                queued += m.n ? n : 0;
             }
             base += __shfl_sync(0xffffffffu, incl, 31);
         }
     }
+    if (m.n) flush();
 }
 
 }  // namespace ogm
