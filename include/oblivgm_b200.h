@@ -119,6 +119,13 @@ int ogm_fss_gen(int kind, int bits, int64_t K, const uint32_t* alphas, const voi
                 const void* roots1, void* seed_cw, uint32_t* ctrl, uint8_t* final_cw,
                 void* stream);
 
+/* ogm_fss_gen writing both parties' per-key flag bytes in the layout the
+ * eval entry points read (bit 0 root_t -- 0 for party 0, 1 for party 1 --,
+ * bit 1 final_cw, bit 2 add_const = 0) instead of final_cw alone. */
+int ogm_fss_gen_pair(int kind, int bits, int64_t K, const uint32_t* alphas, const void* roots0,
+                     const void* roots1, void* seed_cw, uint32_t* ctrl, uint8_t* flags0, uint8_t* flags1,
+                     void* stream);
+
 /* src/fss.py:257-299 _walk_eval / dpf_eval / dcf_eval: one point per key,
  * one thread per (key, point).  out_bits: ceil(K/32) words, bit k = key k. */
 int ogm_fss_eval_points(int kind, int bits, int64_t K, const void* root, const void* seed_cw,

@@ -45,6 +45,7 @@ SIGNATURES = {
     "ogm_perm_workspace_bytes": ([_i64], _i64),
     "ogm_seeded_permutation": ([_cp, _cp, _u64, _i64, _vp, _vp, _vp], _int),
     "ogm_fss_gen": ([_int, _int, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp], _int),
+    "ogm_fss_gen_pair": ([_int, _int, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp], _int),
     "ogm_fss_eval_points": ([_int, _int, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp], _int),
     "ogm_fss_eval_points_host": ([_int, _int, _i64, _vp, _vp, _vp, _vp, _vp, _vp], _int),
     "ogm_fss_full_domain": ([_int, _int, _int, _vp, _vp, _vp, _vp, _i64, _vp, _i64, _vp], _int),

@@ -47,7 +47,7 @@ template <bool DCF, class TAB = AesTab>
 __global__ void __launch_bounds__(kFssThreads) fss_gen_kernel(
     int bits, int64_t K, const uint32_t* __restrict__ alphas, const uint4* __restrict__ roots0,
     const uint4* __restrict__ roots1, uint4* __restrict__ scw_out, uint32_t* __restrict__ ctrl_out,
-    uint8_t* __restrict__ final_out) {
+    uint8_t* __restrict__ final_out, uint8_t* __restrict__ flags1_out) {
     OGM_AES_PROLOGUE_T(TAB);
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < K; k += stride) {
@@ -81,7 +81,13 @@ __global__ void __launch_bounds__(kFssThreads) fss_gen_kernel(
         ctrl_out[k] = tlw;
         ctrl_out[K + k] = trw;
         ctrl_out[2 * K + k] = vw;
-        final_out[k] = DCF ? 0 : (uint8_t)((((s0.x ^ s1.x) & 1u)) ^ 1u);
+        const uint8_t fin = DCF ? 0 : (uint8_t)((((s0.x ^ s1.x) & 1u)) ^ 1u);
+        if (flags1_out) {   // the eval kernels' flag bytes (bit 0 root_t, bit 1 final_cw) of both parties
+            final_out[k] = (uint8_t)(fin << 1);
+            flags1_out[k] = (uint8_t)((fin << 1) | 1u);
+        } else {
+            final_out[k] = fin;
+        }
     }
 }
 

@@ -111,8 +111,9 @@ int ogm_zero_share_slice(const uint8_t* key_own, const uint8_t* key_prev, uint64
     return OGM_OK;
 }
 
-int ogm_fss_gen(int kind, int bits, int64_t K, const uint32_t* alphas, const void* roots0,
-                const void* roots1, void* seed_cw, uint32_t* ctrl, uint8_t* final_cw, void* stream) {
+static int fss_gen_impl(int kind, int bits, int64_t K, const uint32_t* alphas, const void* roots0,
+                        const void* roots1, void* seed_cw, uint32_t* ctrl, uint8_t* out0, uint8_t* out1,
+                        void* stream) {
     OGM_CHECK_ARG(kind == OGM_KIND_DPF || kind == OGM_KIND_DCF, OGM_ERR_ARG, "unknown key kind %d", kind);
     OGM_CHECK_ARG(bits >= 1 && bits <= 32, OGM_ERR_DOMAIN, "domain_bits %d outside 1..32", bits);
     OGM_CHECK_ARG(K >= 0, OGM_ERR_ARG, "negative key count");
@@ -120,13 +121,25 @@ int ogm_fss_gen(int kind, int bits, int64_t K, const uint32_t* alphas, const voi
     OGM_ENSURE_INIT();
     if (kind == OGM_KIND_DCF)
         aes_launch(fss_gen_kernel<true, AesTab>, fss_gen_kernel<true, AesTabSmall>, K, kFssThreads, as_stream(stream),
-                   bits, K, alphas, (const uint4*)roots0, (const uint4*)roots1, (uint4*)seed_cw, ctrl, final_cw);
+                   bits, K, alphas, (const uint4*)roots0, (const uint4*)roots1, (uint4*)seed_cw, ctrl, out0, out1);
     else
         aes_launch(fss_gen_kernel<false, AesTab>, fss_gen_kernel<false, AesTabSmall>, K, kFssThreads,
                    as_stream(stream), bits, K, alphas, (const uint4*)roots0, (const uint4*)roots1, (uint4*)seed_cw,
-                   ctrl, final_cw);
+                   ctrl, out0, out1);
     OGM_LAUNCH_CHECK();
     return OGM_OK;
+}
+
+int ogm_fss_gen(int kind, int bits, int64_t K, const uint32_t* alphas, const void* roots0,
+                const void* roots1, void* seed_cw, uint32_t* ctrl, uint8_t* final_cw, void* stream) {
+    return fss_gen_impl(kind, bits, K, alphas, roots0, roots1, seed_cw, ctrl, final_cw, nullptr, stream);
+}
+
+int ogm_fss_gen_pair(int kind, int bits, int64_t K, const uint32_t* alphas, const void* roots0,
+                     const void* roots1, void* seed_cw, uint32_t* ctrl, uint8_t* flags0, uint8_t* flags1,
+                     void* stream) {
+    OGM_CHECK_ARG(K == 0 || (flags0 && flags1), OGM_ERR_ARG, "both parties' flag outputs are required");
+    return fss_gen_impl(kind, bits, K, alphas, roots0, roots1, seed_cw, ctrl, flags0, flags1, stream);
 }
 
 int ogm_fss_eval_points(int kind, int bits, int64_t K, const void* root, const void* seed_cw,

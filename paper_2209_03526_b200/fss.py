@@ -219,12 +219,11 @@ def gen_batch(comparison: bool, bits: int, alphas: torch.Tensor, roots0: torch.T
     dev = alphas.device
     scw = torch.empty((bits, k, 16), dtype=torch.uint8, device=dev)
     ctrl = torch.empty((3, k), dtype=torch.int32, device=dev)
-    fin = torch.empty((k,), dtype=torch.uint8, device=dev)
+    f0 = torch.empty((k,), dtype=torch.uint8, device=dev)
+    f1 = torch.empty((k,), dtype=torch.uint8, device=dev)
     kind = _lib.KIND_DCF if comparison else _lib.KIND_DPF
-    _lib.call("ogm_fss_gen", kind, bits, k, _lib.ptr(alphas), _lib.ptr(roots0), _lib.ptr(roots1),
-              _lib.ptr(scw), _lib.ptr(ctrl), _lib.ptr(fin), _lib.stream_ptr())
-    f0 = fin << 1
-    f1 = f0 | 1
+    _lib.call("ogm_fss_gen_pair", kind, bits, k, _lib.ptr(alphas), _lib.ptr(roots0), _lib.ptr(roots1),
+              _lib.ptr(scw), _lib.ptr(ctrl), _lib.ptr(f0), _lib.ptr(f1), _lib.stream_ptr())
     return (KeyBatch(kind, bits, roots0, scw, ctrl, f0), KeyBatch(kind, bits, roots1, scw, ctrl, f1))
 
 
