@@ -1,4 +1,4 @@
-"""Chained planned online shuffle (ogm_shuffle_online_planned: each message
+"""Chained planned online shuffle (ogm_shuffle_online_planned_ex: each message
 handed sender -> receiver in shared memory) vs the four planned party steps,
 at 2^lg rows x 128 bits.  Checks x1, y1, c1, R3 against the step-wise path,
 then times: steps (output-order blinds), steps with source-order blinds, the
@@ -49,10 +49,12 @@ for lg in map(int, sys.argv[1:]):
     it = (ctypes.c_void_p * 3)(*[P(t) for t in inter])
 
     def chained(msgs: bool):
-        _lib.call("ogm_shuffle_online_planned", rows, ctypes.addressof(q2), ctypes.addressof(gd), ctypes.addressof(sr),
-                  P(comps[0]), P(comps[1]), P(comps[2]), P(u_src), P(v_src), P(w_src), P(z_src),
-                  ctypes.addressof(it), P(got[0]) if msgs else None, P(got[1]) if msgs else None,
-                  P(got[2]) if msgs else None, P(got[3]), _lib.stream_ptr())
+        # chain_blinds(): U', V' in source order, W and Z in slot order (W in output order above 256 MB)
+        _lib.call("ogm_shuffle_online_planned_ex", rows, ctypes.addressof(q2), ctypes.addressof(gd),
+                  ctypes.addressof(sr), P(comps[0]), P(comps[1]), P(comps[2]), P(u_src), P(v_src), 0, P(w_src),
+                  1 if off[1].w_output_order else 2, P(z_src), 2, ctypes.addressof(it),
+                  P(got[0]) if msgs else None, P(got[1]) if msgs else None, P(got[2]) if msgs else None,
+                  P(got[3]), _lib.stream_ptr())
 
     chained(True)
     torch.cuda.synchronize()
