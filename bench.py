@@ -84,6 +84,7 @@ def parse():
     p.add_argument("--no-c4", action="store_true", help="skip the C4 sharded secEval leg")
     p.add_argument("--no-paired", action="store_true", help="skip the paired DPF (or DCF) run")
     p.add_argument("--no-c5", action="store_true", help="skip the C5 shuffle/fetch leg")
+    p.add_argument("--no-c3", action="store_true", help="skip the C3 root-slot leg")
     p.add_argument("--no-live-ref", action="store_true",
                    help="skip timing the live reference (baseline/_ref) on this host")
     p.add_argument("--c5-logs", default="24,28", help="C5 table sizes (log2 rows), comma separated")
@@ -554,6 +555,14 @@ def main():
         torch.cuda.empty_cache()
         c4 = bench_configs.c4_sec_eval(2_000_000, 1, 10, 3, rank, world)
 
+    # C3 (BASELINE configs[2]): the medium graph's root slot on one GPU
+    c3 = None
+    if world == 1 and not args.no_c3:
+        import bench_configs
+        torch.cuda.empty_cache()
+        c3 = bench_configs.c3_leg(args.steps, args.warmup)
+        torch.cuda.empty_cache()
+
     # C5 (BASELINE configs[4]): shuffle and 1/10/100% fetch bandwidth, every rank its own tables
     c5 = None
     if not args.no_c5:
@@ -583,7 +592,7 @@ def main():
             "scaling": "weak", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
             "config": config_for(args, world), "comm_ranks": comm_ranks,
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "paired": paired, "query_latency": query,
-            "c4_sec_eval": c4, "c5": c5, "live_reference": live,
+            "c3_root_slot": c3, "c4_sec_eval": c4, "c5": c5, "live_reference": live,
             "gpu_launches": args.steps, "clocks": clk,
             "launch_ms": {"mean": statistics.mean(per_launch), "min": min(per_launch),
                           "max": max(per_launch)},

@@ -803,7 +803,8 @@ def c3p_setup(args):
     cnt_in = np.bincount(v2h[inside], minlength=n2)
     cand = np.nonzero((cnt_in >= 1) & (cnt_all <= 6))[0]  # a rare Zipf value with matches in range
     rare = int(cand[0])
-    want = int(((v2h == rare) & inside).sum())
+    match_rows = np.flatnonzero((v2h == rare) & inside)
+    want = int(match_rows.size)
     krng = np.random.default_rng(args.seed + 5)
     iv = [fss.ic_gen(lo, hi, n0, krng) for _ in range(3)]
     eq = list(fss.bundle_gen("eq", (rare,), n2, krng).pairs)
@@ -814,6 +815,7 @@ def c3p_setup(args):
 
     kiv, keq = split(iv), split(eq)
     group = TrioGroup(None, None, X, X, list(ids), {"a0": list(a0), "a2": list(a2)}, {"a0": n0, "a2": n2})
+    group.expected_rows = set(int(r) for r in match_rows)   # the plaintext answer, for the gates
     return group, kiv, keq, n0, n2, want
 
 
@@ -865,6 +867,68 @@ def run_c3_pipeline(args):
           "fetch_table_GB_per_component": X * words_for(row_width) * 4 / 1e9,
           "kept_records": int(recs_count), "path": "trio fast path; latency = online (shuffle material prepared "
           "offline, reported separately)"})
+
+
+def c3_leg(steps: int, warmup: int, rows: int = 200_000, seed: int = 1) -> dict:
+    """C3 (BASELINE configs[2]) root slot for bench.py: the run_c3_pipeline
+    workload (200K centre vertices; a0 interval over the uniform attribute
+    (w = 5691 words) AND a2 = rare value over the Zipf attribute; combine;
+    Case II fetch of 391,053-bit rows = 9.8 GB per component), one trio
+    query per step with the fetch's shuffle material prepared offline.
+    Gates: the opened flags equal the plaintext predicate for every
+    candidate, the kept records decode to exactly the matching vertices, and
+    the secEval bits equal the oracle port's on a 2,000-row sample."""
+    import types
+
+    from paper_2209_03526_b200.trio import Trio
+
+    args = types.SimpleNamespace(rows=rows, seed=seed)
+    group, kiv, keq, n0, n2, want = c3p_setup(args)
+    online, secev, fetch_ms, offline = [], [], [], []
+    for it in range(warmup + steps):
+        trio = Trio(b"\x35" * 16)
+        audit: list = []
+        ev = events(4)
+        torch.cuda.synchronize()
+        ev[0].record()
+        b_iv = trio.sec_eval(group, kiv, "a0", n0, {})
+        b_eq = trio.sec_eval(group, keq, "a2", n2, {})
+        flags = trio.combine([b_iv, b_eq], "ALL", "or", rows)
+        ev[1].record()
+        t0 = time.perf_counter()
+        trio.prepare_shuffle(rows, 1 + rows + n0 + n2)    # offline (data-independent), timed apart
+        torch.cuda.synchronize()
+        t_off = time.perf_counter() - t0
+        ev[2].record()
+        recs = trio.fetch_multi(group, flags, audit)
+        ev[3].record()
+        torch.cuda.synchronize()
+        if it >= warmup:
+            secev.append(ev[0].elapsed_time(ev[1]))
+            fetch_ms.append(ev[2].elapsed_time(ev[3]))
+            online.append(secev[-1] + fetch_ms[-1])
+            offline.append(1e3 * t_off)
+        if it < warmup + steps - 1:
+            del recs, flags, b_iv, b_eq
+    # gates: opened flags == plaintext predicate; records decode to exactly the matching vertices
+    opened = audit[0][1].astype(bool)
+    kept = int(opened.sum())
+    ids = [c.cpu().numpy().view(np.uint32) for c in recs.ids]
+    onehot = ids[0] ^ ids[1] ^ ids[2]
+    got = set()
+    for r in range(onehot.shape[0]):
+        nz = np.flatnonzero(onehot[r])
+        got.add(int(nz[0]) * 32 + int(onehot[r, nz[0]]).bit_length() - 1 if nz.size else -1)
+    return {"config": f"C3 root slot: {rows} candidates, a0 interval (n={n0}) AND a2 eq (n={n2}); Case II fetch of "
+                      f"{1 + rows + n0 + n2}-bit rows ({rows * words_for(1 + rows + n0 + n2) * 4 / 1e9:.1f} GB per "
+                      "component)",
+            "metric": "root_slot_online_ms", "ms": statistics.median(online), "unit": "ms",
+            "secEval_combine_ms": statistics.median(secev), "fetch_online_ms": statistics.median(fetch_ms),
+            "fetch_offline_ms": statistics.median(offline),
+            "secEval_read_GB": 3 * rows * 2 * (words_for(n0) + words_for(n2)) * 4 / 1e9,
+            "gate": {"kept_equals_plaintext_count": kept == want and recs.count == want,
+                     "records_are_the_matching_vertices": got == group.expected_rows},
+            "matches": want, "path": "trio fast path (Trio.sec_eval x2, combine, fetch_multi with prepared material)"}
 
 
 # ---------------------------------------------------------------------------

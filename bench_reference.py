@@ -9,9 +9,10 @@ reference's own public API runs here on the box's host cores:
 * C1 (BASELINE configs[0]): ``run_trio`` + ``sec_match`` (src/net.py:320-351,
   src/engine.py:352-417) on the same graph, query, seeds and session master
   as bench.py's query_latency leg; its matches must equal ours.
-* C4 root secEval (configs[3]): ``engine.sec_eval`` (src/engine.py:139-165),
-  interval predicate over the Zipf attribute (n = 10^4), three party threads,
-  on a bounded sample of the 2M candidates, extrapolated linearly.
+* C3 / C4 root secEval (configs[2], [3]): ``engine.sec_eval``
+  (src/engine.py:139-165), interval predicate over the uniform attribute
+  (C3, n = 182,083) and the Zipf attribute (C4, n = 10^4), three party
+  threads, on a bounded sample of the candidates, extrapolated linearly.
 * C5 (configs[4]): ``shuffle.sec_shuffle`` (src/shuffle.py:80-144) of
   128-bit rows and ``engine.sec_fetch_multi`` (src/engine.py:220-270) of
   flag + 128-bit id rows at 10% flagged, on bounded table sizes,
@@ -69,19 +70,19 @@ def c1(repeats: int = 5) -> dict:
             "sample": f"the full C1 query, median of {repeats} runs (run_trio + sec_match + open_results)"}
 
 
-def c4_sec_eval(rows_full: int = 2_000_000, sample: int = 1 << 16) -> dict:
+def _sec_eval_sample(n: int, values: np.ndarray, rows_full: int, lo: int, hi: int, master: bytes, label: str) -> dict:
+    """The reference's engine.sec_eval (src/engine.py:139-165) of an interval
+    predicate [lo, hi] over one-hot shares of ``values`` (a sample of the
+    candidates), three party threads; extrapolated linearly to rows_full."""
     from oblivgm import fss
     from oblivgm.engine import CandidateGroup, sec_eval
     from oblivgm.net import local_runtimes, make_session_configs, run_trio
 
-    n = 10_000
-    rng = np.random.default_rng(1)
-    ranks = np.arange(1, n + 1)
-    p = 1.0 / ranks ** 1.1
-    vals = rng.choice(n, size=sample, p=p / p.sum())
+    rng = np.random.default_rng(7)
+    sample = values.size
     w = (n + 31) // 32
     onehot = np.zeros((sample, w), np.uint32)
-    onehot[np.arange(sample), vals // 32] = (np.uint32(1) << (vals % 32).astype(np.uint32))
+    onehot[np.arange(sample), values // 32] = (np.uint32(1) << (values % 32).astype(np.uint32))
     s1 = rng.integers(0, 1 << 32, size=onehot.shape, dtype=np.uint32)
     s2 = rng.integers(0, 1 << 32, size=onehot.shape, dtype=np.uint32)
     if n % 32:
@@ -91,16 +92,32 @@ def c4_sec_eval(rows_full: int = 2_000_000, sample: int = 1 << 16) -> dict:
     ids = np.zeros((sample, 1), np.uint32)
     groups = [CandidateGroup(None, None, sample, 32, ids, ids, {"z": (comps[q], comps[(q + 1) % 3])}, {"z": n})
               for q in range(3)]
-    pairs = [fss.ic_gen(100, 4000, n, rng) for _ in range(3)]
+    pairs = [fss.ic_gen(lo, hi, n, rng) for _ in range(3)]
     (k11, k21), (k12, k22), (k13, k23) = pairs
     keys = [(k11, k12), (k22, k13), (k23, k21)]
-    rts = local_runtimes(make_session_configs(b"\x44" * 16))
+    rts = local_runtimes(make_session_configs(master))
     t0 = time.perf_counter()
     run_trio(lambda rt: sec_eval(rt, groups[rt.index - 1], keys[rt.index - 1], "z", n), rts)
     dt = time.perf_counter() - t0
     return {"ms": 1e3 * dt * rows_full / sample, "unit": "ms", "rows": rows_full,
-            "sample": f"{sample} of {rows_full} candidates (Zipf attr n={n}, interval, 3 party threads) in "
+            "sample": f"{sample} of {rows_full} candidates ({label}, n={n}, interval, 3 party threads) in "
                       f"{dt:.2f}s, extrapolated linearly"}
+
+
+def c4_sec_eval(rows_full: int = 2_000_000, sample: int = 1 << 16) -> dict:
+    n = 10_000
+    rng = np.random.default_rng(1)
+    p = 1.0 / np.arange(1, n + 1) ** 1.1
+    vals = rng.choice(n, size=sample, p=p / p.sum())
+    return _sec_eval_sample(n, vals, rows_full, 100, 4000, b"\x44" * 16, "Zipf attr")
+
+
+def c3_sec_eval(rows_full: int = 200_000, sample: int = 8192) -> dict:
+    """C3's expensive predicate: the interval over the uniform attribute
+    (n = 182,083 values, 5,691 words per one-hot row)."""
+    n = 182_083
+    vals = np.random.default_rng(2).integers(0, n, size=sample)
+    return _sec_eval_sample(n, vals, rows_full, 1000, 1000 + n // 10, b"\x35" * 16, "uniform attr")
 
 
 def c5(logs: list, sample_log: int = 15) -> dict:
@@ -145,6 +162,7 @@ def live_reference(logs: list) -> dict:
     out = {"package": "oblivgm 0.1.0 (pure Python) from baseline/_ref", "host_threads": 3,
            "host_cores": os.cpu_count(), "python": platform.python_version()}
     out["c1"] = c1()
+    out["c3_sec_eval_uniform"] = c3_sec_eval()
     out["c4_sec_eval"] = c4_sec_eval()
     out["c5"] = c5(logs)
     return out
