@@ -925,7 +925,14 @@ def c3_leg(steps: int, warmup: int, rows: int = 200_000, seed: int = 1) -> dict:
             "metric": "root_slot_online_ms", "ms": statistics.median(online), "unit": "ms",
             "secEval_combine_ms": statistics.median(secev), "fetch_online_ms": statistics.median(fetch_ms),
             "fetch_offline_ms": statistics.median(offline),
-            "secEval_read_GB": 3 * rows * 2 * (words_for(n0) + words_for(n2)) * 4 / 1e9,
+            # the trio path reads each share component once for all parties and both interval passes
+            "secEval_read_GB": 3 * rows * (words_for(n0) + words_for(n2)) * 4 / 1e9,
+            "secEval_hbm_frac": 3 * rows * (words_for(n0) + words_for(n2)) * 4 / (statistics.median(secev) * 1e-3)
+            / 1e9 / HBM_PEAK,
+            # fetch: 14 moves of the 16-byte-pitched row (the shuffle), blinds generated on the fly
+            "fetch_row_bytes": 4 * ((words_for(1 + rows + n0 + n2) + 3) // 4 * 4),
+            "fetch_hbm_frac": 14 * rows * 4 * ((words_for(1 + rows + n0 + n2) + 3) // 4 * 4)
+            / (statistics.median(fetch_ms) * 1e-3) / 1e9 / HBM_PEAK,
             "gate": {"kept_equals_plaintext_count": kept == want and recs.count == want,
                      "records_are_the_matching_vertices": got == group.expected_rows},
             "matches": want, "path": "trio fast path (Trio.sec_eval x2, combine, fetch_multi with prepared material)"}
