@@ -554,6 +554,8 @@ def main():
         del b0, pts, out
         torch.cuda.empty_cache()
         c4 = bench_configs.c4_sec_eval(2_000_000, 1, 10, 3, rank, world)
+        torch.cuda.empty_cache()
+        c4["root_slot"] = bench_configs.c4_root_slot(2_000_000, 1, 10, 3, rank, world)
 
     # C3 (BASELINE configs[2]): the medium graph's root slot on one GPU
     c3 = None

@@ -36,6 +36,7 @@ from paper_2209_03526_b200.shuffle import (ShuffleOffline, blind_table, gather, 
                                             shuffle_online_planned)
 from paper_2209_03526_b200.prf import seeded_permutation_device  # noqa: E402
 from paper_2209_03526_b200 import workloads  # noqa: E402
+from paper_2209_03526_b200.trio import TrioGroup  # noqa: E402
 
 def _hbm_peak() -> float:
     """GB/s: MEASURED_PEAKS.json (driver-written copy benchmark) when present,
@@ -942,6 +943,102 @@ def c3_leg(steps: int, warmup: int, rows: int = 200_000, seed: int = 1) -> dict:
 # C4: large graph, root-slot secEval on the Zipf attribute, rows sharded
 # across ranks (torchrun, one process per GPU; NCCL all-gather of match bits)
 # ---------------------------------------------------------------------------
+
+
+def c4_root_slot(rows: int, seed: int, steps: int, warmup: int, rank: int, world: int) -> dict:
+    """C4 (BASELINE configs[3]) root slot end to end: two predicates over the
+    two Zipf attributes (a2 in [100, 4000]: DCF interval, 2 passes; a3 = v*:
+    DPF), combined with AND, then the Case II fetch of the matches.
+
+    secEval runs row-sharded (sharded_trio.ShardedTrio: one all-gather per
+    predicate); combine is replicated.  The fetch cannot use the reference's
+    row layout here (a one-hot id over 2M vertices is 250 KB per row, 500 GB
+    per component -- SURVEY Appendix B), so it fetches flag + a 128-bit
+    compact record per vertex (vertex index and the two attribute values)
+    through the pinned C5 fetch path (Trio.fetch_multi, flag-split), with the
+    32 MB record table replicated on every rank.  The record encoding is
+    outside the reference layout (parity of that choice unpinned); the
+    secEval, combine and fetch arithmetic are the pinned paths.  Gates: the
+    opened flags equal the plaintext predicate on every row and the kept
+    records recombine to the matching vertices' records."""
+    import torch.distributed as dist
+
+    from paper_2209_03526_b200.sharded_trio import ShardedGroup, ShardedTrio
+    from paper_2209_03526_b200.sharding import ShardPlan, ThreadComm
+
+    n = 10_000
+    plan = ShardPlan(rows, world)
+    lo, hi = plan.bounds(rank)
+    rng = np.random.default_rng(seed)
+    pz = 1.0 / np.arange(1, n + 1) ** 1.1
+    pz /= pz.sum()
+    a2 = rng.choice(n, size=rows, p=pz).astype(np.int32)
+    a3 = rng.choice(n, size=rows, p=pz).astype(np.int32)
+    v_star = 7                                    # a3 value with ~1% frequency under Zipf(1.1)
+    want = (a2 >= 100) & (a2 <= 4000) & (a3 == v_star)
+    c2 = list(workloads.shared_one_hot(torch.from_numpy(a2[lo:hi]).cuda(), n, seed, 40, row0=lo))
+    c3 = list(workloads.shared_one_hot(torch.from_numpy(a3[lo:hi]).cuda(), n, seed, 50, row0=lo))
+    ids_dummy = [torch.zeros((hi - lo, 1), dtype=torch.int32, device="cuda") for _ in range(3)]
+    group = ShardedGroup(None, None, rows, 32, ids_dummy, {"a2": c2, "a3": c3}, {"a2": n, "a3": n},
+                         plan=plan, rank=rank)
+    krng = np.random.default_rng(seed + 1)          # identical keys on every rank
+
+    def split(pairs):
+        (k11, k21), (k12, k22), (k13, k23) = pairs
+        return [(k11, k12), (k22, k13), (k23, k21)]
+
+    kiv = split([fss.ic_gen(100, 4000, n, krng) for _ in range(3)])
+    keq = split(list(fss.bundle_gen("eq", (v_star,), n, krng).pairs))
+    # compact records: (vertex index, a2, a3, 0) shared three ways, replicated (32 MB per component)
+    plain = torch.from_numpy(np.stack([np.arange(rows, dtype=np.int32), a2, a3, np.zeros(rows, np.int32)], 1)).cuda()
+    r1 = workloads.device_random_words(rows * 4, seed, 60).reshape(rows, 4)
+    r2 = workloads.device_random_words(rows * 4, seed, 61).reshape(rows, 4)
+    rec_comps = [r1, r2, plain ^ r1 ^ r2]
+    fetch_group = None
+    tim = {"secEval_ms": [], "combine_ms": [], "fetch_ms": [], "total_ms": []}
+    for it in range(warmup + steps):
+        trio = ShardedTrio(b"\x4c" * 16, None if world > 1 else ThreadComm(1).rank_view(0))
+        trio.prepare_fetch(rows)                    # offline: the fetch's shuffle material (table id 0)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        ev = events(4)
+        ev[0].record()
+        b_iv = trio.sec_eval(group, kiv, "a2", n, {})
+        b_eq = trio.sec_eval(group, keq, "a3", n, {})
+        ev[1].record()
+        flags = trio.combine([b_iv, b_eq], "ALL", "or", rows)
+        ev[2].record()
+        fetch_group = TrioGroup(None, None, rows, 128, rec_comps, {}, {})
+        audit: list = []
+        recs = trio.fetch_multi(fetch_group, flags, audit)
+        ev[3].record()
+        torch.cuda.synchronize()
+        if it >= warmup:
+            for k, (a, b) in (("secEval_ms", (0, 1)), ("combine_ms", (1, 2)), ("fetch_ms", (2, 3)),
+                              ("total_ms", (0, 3))):
+                tim[k].append(ev[a].elapsed_time(ev[b]))
+    med = {k: statistics.median(v) for k, v in tim.items()}
+    if world > 1:
+        t = torch.tensor([med["total_ms"]], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        med["total_ms"] = float(t.item())
+    opened = audit[0][1].astype(bool)
+    got = (recs.ids[0] ^ recs.ids[1] ^ recs.ids[2]).cpu().numpy()
+    ok_open = int(opened.sum()) == int(want.sum())
+    ok_recs = bool(np.array_equal(np.sort(got[:, 0]), np.flatnonzero(want))) and bool(
+        np.array_equal(got[np.argsort(got[:, 0]), 1:3], np.stack([a2, a3], 1)[want]))
+    nbytes_local = 3 * (hi - lo) * 2 * words_for(n) * 4
+    return {"config": f"C4 root slot: {rows} candidates, a2 in [100, 4000] (Zipf, n={n}) AND a3 = {v_star}; "
+                      f"Case II fetch of compact 128-bit records; rows sharded x{world}",
+            "metric": "root_slot_ms", "ms": med["total_ms"], "unit": "ms", "n_gpus": world,
+            "phases_ms": {k: med[k] for k in ("secEval_ms", "combine_ms", "fetch_ms")},
+            "matches": int(want.sum()), "kept": int(recs.count),
+            "rank0_secEval_hbm_frac": nbytes_local / (med["secEval_ms"] * 1e-3) / 1e9 / HBM_PEAK,
+            "fetch": "flag + 128-bit compact record (vertex index, a2, a3), replicated table; the reference "
+                     "layout's one-hot id row is 500 GB per component at this size (SURVEY Appendix B)",
+            "gate": {"opened_count_equals_plaintext": ok_open and int(recs.count) == int(want.sum()),
+                     "records_are_the_matches": ok_recs}}
 
 
 def c4_sec_eval(rows: int, seed: int, steps: int, warmup: int, rank: int, world: int) -> dict:
