@@ -305,6 +305,24 @@ int ogm_flag_shuffle_trio(int64_t rows, const int32_t* k1, const int32_t* pi12, 
 int ogm_unpack_records(const void* blob, int64_t blob_bytes, int64_t nrec, const int64_t* src_off,
                        const int64_t* dst_off, const int32_t* nwords, uint32_t* arena, void* stream);
 
+/* ---- graph outsourcing on the device (src/graphs.py:327-400) -------------
+ * ogm_pcg64_u32: out[0..n) = the next n values numpy's
+ * Generator(PCG64).integers(0, 2**32, dtype=uint32) would return from the
+ * generator state (state, inc: 128-bit little-endian word pairs; has_uint32 /
+ * uinteger: numpy's buffered high half).  Jump-ahead per thread, so the
+ * stream is drawn in parallel, bit-identical to the host generator.
+ * ogm_deal_rows: the three XOR share components of drawn rows
+ * (src/graphs.py:327-332): row i's first component is words[s1_off[i] ..
+ * + drawn[i]), its second words[s2_off[i] .. + drawn[i]), its third their
+ * XOR; words from drawn[i] up to the row pitch are zero (k-padding slots and
+ * row padding).  ogm_deal_hot_bits then folds the plaintext one-hot bits into
+ * the third component: c3[word[j]] ^= mask[j] (distinct words). */
+int ogm_pcg64_u32(const uint64_t* state, const uint64_t* inc, int has_uint32, uint32_t uinteger, int64_t n,
+                  uint32_t* out, void* stream);
+int ogm_deal_rows(const uint32_t* words, const int64_t* s1_off, const int64_t* s2_off, const int64_t* drawn,
+                  int64_t rows, int64_t pitch, uint32_t* c1, uint32_t* c2, uint32_t* c3, void* stream);
+int ogm_deal_hot_bits(const int64_t* word, const uint32_t* mask, int64_t n, uint32_t* c3, void* stream);
+
 /* ---- L1 shuffle (src/shuffle.py) ------------------------------------------ */
 
 /* One party-local step of sec_shuffle (src/shuffle.py:106-143):

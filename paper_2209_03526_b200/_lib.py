@@ -68,6 +68,9 @@ SIGNATURES = {
     "ogm_compact_workspace_bytes": ([_i64], _i64),
     "ogm_compact_bits": ([_i64, _vp, _vp, _vp, _vp, _i64, _vp], _int),
     "ogm_keep_rows_workspace_bytes": ([_i64], _i64),
+    "ogm_pcg64_u32": ([_vp, _vp, _int, ctypes.c_uint32, _i64, _vp, _vp], _int),
+    "ogm_deal_rows": ([_vp, _vp, _vp, _vp, _i64, _i64, _vp, _vp, _vp, _vp], _int),
+    "ogm_deal_hot_bits": ([_vp, _vp, _i64, _vp, _vp], _int),
     "ogm_keep_rows": ([_i64, _vp, _int, _vp, _i64, _vp, _i64, _vp, _vp, _vp, _i64, _vp], _int),
     "ogm_split_flag_rows": ([_i64, _vp, _i64, _vp, _vp, _vp], _int),
     "ogm_flag_shuffle_trio": ([_i64] + [_vp] * 19, _int),

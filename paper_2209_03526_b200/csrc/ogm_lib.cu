@@ -18,6 +18,7 @@
 #include "ogm_engine.cuh"
 #include "ogm_shuffle.cuh"
 #include "ogm_fetch.cuh"
+#include "ogm_dealer.cuh"
 #include "ogm_trio.cuh"
 #include "ogm_measure.cuh"
 
