@@ -296,6 +296,23 @@ int ogm_flag_shuffle_trio(int64_t rows, const int32_t* k1, const int32_t* pi12, 
                           const uint32_t* r1f, const uint32_t* r2f, uint32_t* x1f, uint32_t* y1f, uint32_t* c1f,
                           uint32_t* r3f, uint32_t* plain, void* stream);
 
+/* The online phase of a flag-split fetch shuffle for >= 2^22 rows in one
+ * call: flag phase 1 (x1f, y1f), then the chained planned payload shuffle
+ * (as ogm_shuffle_online_planned_ex with V in source order and Z in slot
+ * order) whose final window passes also compute c1f, r3f and the opened
+ * column `plain` -- the flag column needs the rows in output order, which
+ * those passes walk anyway.  Same results as ogm_shuffle_online_planned_ex +
+ * ogm_flag_shuffle_trio. */
+int ogm_fetch128_online_planned(int64_t rows, const int32_t* const* q2, const int32_t* const* gdst,
+                                const uint16_t* const* srow, const uint32_t* a, const uint32_t* b, const uint32_t* c,
+                                const uint32_t* u_src, const uint32_t* v_src, const uint32_t* w_blind, int w_order,
+                                const uint32_t* z_slot, uint32_t* const* inter, uint32_t* r3, const int32_t* k1,
+                                const int32_t* pi12, const int32_t* pi23, const int32_t* k3, const uint32_t* f1,
+                                const uint32_t* f2, const uint32_t* f3, const uint32_t* uf, const uint32_t* vf,
+                                const uint32_t* wf, const uint32_t* zf, const uint32_t* r1f, const uint32_t* r2f,
+                                uint32_t* x1f, uint32_t* y1f, uint32_t* c1f, uint32_t* r3f, uint32_t* plain,
+                                void* stream);
+
 /* ---- storage (src/storage.py) -------------------------------------------- */
 
 /* Loader for OGMS record containers (src/storage.py:43-65, 108-169): the file

@@ -310,6 +310,37 @@ int ogm_flag_shuffle_trio(int64_t rows, const int32_t* k1, const int32_t* pi12, 
     return OGM_OK;
 }
 
+// The whole online fetch shuffle of flag-split rows (>= 2^22 rows): flag
+// phase 1 (f1 ^ f2, then x1f / y1f), then the chained planned payload shuffle
+// whose final window passes carry flag phase 2 and the open (FlagTail): one
+// launch sequence, no separate phase-2 flag kernel.  Arguments as
+// ogm_shuffle_online_planned_ex (V in source order, Z in slot order) and
+// ogm_flag_shuffle_trio; c1f is scratch when the passes are split (> 256 MB).
+int ogm_fetch128_online_planned(int64_t rows, const int32_t* const* q2, const int32_t* const* gdst,
+                                const uint16_t* const* srow, const uint32_t* a, const uint32_t* b, const uint32_t* c,
+                                const uint32_t* u_src, const uint32_t* v_src, const uint32_t* w_blind, int w_order,
+                                const uint32_t* z_slot, uint32_t* const* inter, uint32_t* r3, const int32_t* k1,
+                                const int32_t* pi12, const int32_t* pi23, const int32_t* k3, const uint32_t* f1,
+                                const uint32_t* f2, const uint32_t* f3, const uint32_t* uf, const uint32_t* vf,
+                                const uint32_t* wf, const uint32_t* zf, const uint32_t* r1f, const uint32_t* r2f,
+                                uint32_t* x1f, uint32_t* y1f, uint32_t* c1f, uint32_t* r3f, uint32_t* plain,
+                                void* stream) {
+    using namespace ogm;
+    OGM_CHECK_ARG(rows >= 0 && rows < ((int64_t)1 << 31), OGM_ERR_ARG, "rows out of range");
+    if (rows == 0) return OGM_OK;
+    const void* need[] = {k1, pi12, pi23, k3, f1, f2, f3, uf, vf, wf, zf, r1f, r2f, x1f, y1f, c1f, r3f, plain};
+    for (const void* p : need) OGM_CHECK_ARG(p, OGM_ERR_ARG, "permutations, flag columns and scratch are required");
+    cudaStream_t st = as_stream(stream);
+    const int64_t nw = (rows + 31) / 32;
+    uint32_t* f12 = r3f;   // P1's f1 ^ f2, staged in r3f's words: written only by the last pass
+    flag_xor2_kernel<<<grid_for(nw), 256, 0, st>>>(f1, f2, nw, f12);
+    flag_shuffle1_kernel<<<grid_for(rows), 256, 0, st>>>(rows, k1, pi12, f12, f3, uf, vf, x1f, y1f);
+    OGM_LAUNCH_CHECK();
+    const FlagTail ft{pi23, k3, x1f, y1f, wf, zf, r1f, r2f, c1f, r3f, plain};
+    return shuffle_online_planned_impl(rows, q2, gdst, srow, a, b, c, u_src, v_src, 0, w_blind, w_order, z_slot, 2,
+                                       inter, nullptr, nullptr, nullptr, r3, &ft, stream);
+}
+
 int64_t ogm_keep_rows_workspace_bytes(int64_t rows) {
     const int64_t nc = ((rows > 0 ? rows : 1) + 1023) / 1024;  // chunks of the smallest size (32 words)
     return ((nc * 4 + 255) & ~(int64_t)255) + nc * 8 + 256;

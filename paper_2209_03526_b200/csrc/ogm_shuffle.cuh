@@ -747,81 +747,105 @@ __global__ void __launch_bounds__(kTmaThreads, 1) plan_chain_kernel(
     }
 }
 
+// The flag column of a flag-split fetch (csrc/ogm_fetch.cuh) rides along the
+// final window passes: its phase 2 (P2's c1 bits, P3's R3 bits and the opened
+// column) needs the rows in output order, which these passes walk anyway.
+// Each warp owns 32 consecutive output rows, so a bit column word is one
+// ballot.  All pointers null = a plain shuffle.
+struct FlagTail {
+    const int32_t* pi23;      // c1's permutation
+    const int32_t* k3;        // R3's composed permutation
+    const uint32_t* x1f;      // P1's message bits (phase 1)
+    const uint32_t* y1f;      // P2's message bits (phase 1)
+    const uint32_t* wf;       // W's flag column (output order)
+    const uint32_t* zf;       // Z's flag column (output order)
+    const uint32_t* r1f;      // R1, R2 flag columns (for the open)
+    const uint32_t* r2f;
+    uint32_t* c1f;            // P2's c1 bits (needed between the split passes)
+    uint32_t* r3f;            // the new component's flag column
+    uint32_t* plain;          // the opened column R1f ^ R2f ^ R3f
+};
+
+__device__ __forceinline__ uint32_t tail_bit(const uint32_t* __restrict__ v, int64_t j) {
+    return (__ldg(v + (j >> 5)) >> (j & 31)) & 1u;
+}
+
+// FLAG: 0 none; 1 c1 bits (the first of the split passes); 2 R3 bits and the
+// open (the second split pass, c1 bits from pass 1); 3 both (the dual pass)
+template <int FLAG>
+__device__ __forceinline__ void flag_tail_word(const FlagTail& ft, int64_t base, int64_t i, bool valid) {
+    uint32_t bc = 0, br = 0;
+    if (valid) {
+        if (FLAG & 1) bc = tail_bit(ft.x1f, __ldcs(ft.pi23 + i));
+        if (FLAG & 2) br = tail_bit(ft.y1f, __ldcs(ft.k3 + i));
+    }
+    const uint32_t wc = (FLAG & 1) ? __ballot_sync(0xffffffffu, bc) : 0u;
+    const uint32_t wr = (FLAG & 2) ? __ballot_sync(0xffffffffu, br) : 0u;
+    if ((threadIdx.x & 31) == 0) {
+        const int64_t w = base >> 5;
+        uint32_t c;
+        if (FLAG & 1) {
+            c = wc ^ __ldg(ft.wf + w);
+            if (ft.c1f) ft.c1f[w] = c;
+        } else {
+            c = __ldg(ft.c1f + w);
+        }
+        if (FLAG & 2) {
+            const uint32_t r = wr ^ c ^ __ldg(ft.zf + w);
+            ft.r3f[w] = r;
+            if (ft.plain) ft.plain[w] = __ldg(ft.r1f + w) ^ __ldg(ft.r2f + w) ^ r;
+        }
+    }
+}
+
 // the last window passes of two planned gathers with the same output order,
 // XORed: R3[i] = Ir[qr[i]] ^ c1[i], c1[i] = Ic[qc[i]] (msg: c1 stored too).
-// kRows rows per thread per step, all index and window loads issued before
-// any is used.  Measured: 4 rows per thread LOSE (2^24 0.89 -> 0.93 ms, 2^28
-// 16.3 -> 22.4 ms): the grid then spans 4x more output rows at once, i.e.
-// reads from several windows at a time, and the windows stop staying in L2
-// (the same effect as two windows per pass above 256 MB).  One row per thread.
-constexpr int kWinRows = 1;
-
-template <int kRows>
+// One row per thread.  Measured: 4 rows per thread LOSE (2^24 0.89 -> 0.93
+// ms, 2^28 16.3 -> 22.4 ms): the grid then spans 4x more output rows at once,
+// i.e. reads from several windows at a time, and the windows stop staying in
+// L2 (the same effect as two windows per pass above 256 MB).  Warps walk 32
+// consecutive rows together (the flag tail's ballots).
+template <int FLAG>
 __global__ void __launch_bounds__(256) win_gather_dual4_kernel(const int32_t* __restrict__ qa,
                                                                const uint4* __restrict__ ia,
                                                                const int32_t* __restrict__ qb,
                                                                const uint4* __restrict__ ib, int64_t rows,
                                                                uint4* __restrict__ out, uint4* __restrict__ msg,
-                                                               const uint4* __restrict__ ta) {
-    const int64_t stride = (int64_t)gridDim.x * blockDim.x * kRows;
-    for (int64_t i0 = (int64_t)blockIdx.x * blockDim.x * kRows + threadIdx.x; i0 < rows; i0 += stride) {
-        int32_t xa[kRows], xb[kRows];
-#pragma unroll
-        for (int u = 0; u < kRows; u++) {
-            const int64_t i = i0 + (int64_t)u * blockDim.x;
-            xa[u] = i < rows ? __ldcs(qa + i) : 0;
-            xb[u] = i < rows ? __ldcs(qb + i) : 0;
+                                                               const uint4* __restrict__ ta,
+                                                               const __grid_constant__ FlagTail ft) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t base = (int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31); base < rows; base += stride) {
+        const int64_t i = base + (threadIdx.x & 31);
+        const bool valid = i < rows;
+        if (valid) {
+            uint4 va = __ldcg(ia + __ldcs(qa + i));
+            if (ta) va = xor4(va, __ldcs(ta + i));
+            const uint4 vb = __ldcg(ib + __ldcs(qb + i));
+            if (msg) __stcs(msg + i, va);
+            __stcs(out + i, xor4(va, vb));
         }
-        uint4 va[kRows], vb[kRows];
-#pragma unroll
-        for (int u = 0; u < kRows; u++) {
-            const int64_t i = i0 + (int64_t)u * blockDim.x;
-            if (i < rows) {
-                va[u] = __ldcg(ia + xa[u]);
-                vb[u] = __ldcg(ib + xb[u]);
-            }
-        }
-#pragma unroll
-        for (int u = 0; u < kRows; u++) {
-            const int64_t i = i0 + (int64_t)u * blockDim.x;
-            if (i < rows) {
-                uint4 a = va[u];
-                if (ta) a = xor4(a, __ldcs(ta + i));
-                if (msg) __stcs(msg + i, a);
-                __stcs(out + i, xor4(a, vb[u]));
-            }
-        }
+        if (FLAG) flag_tail_word<FLAG>(ft, base, i, valid);
     }
 }
 
 // pass 2 for 16-byte rows (the C5 shape): a lean kernel, since with
 // window-local sources the instruction count per row matters
-template <int kRows>
+template <int FLAG>
 __global__ void __launch_bounds__(256) win_gather4_kernel(const int32_t* __restrict__ q, const uint4* __restrict__ m1,
                                                           const uint4* __restrict__ m3, const uint4* __restrict__ r,
-                                                          int64_t rows, uint4* __restrict__ out) {
-    const int64_t stride = (int64_t)gridDim.x * blockDim.x * kRows;
-    for (int64_t i0 = (int64_t)blockIdx.x * blockDim.x * kRows + threadIdx.x; i0 < rows; i0 += stride) {
-        int32_t x[kRows];
-#pragma unroll
-        for (int u = 0; u < kRows; u++) {
-            const int64_t i = i0 + (int64_t)u * blockDim.x;
-            x[u] = i < rows ? __ldcs(q + i) : 0;
+                                                          int64_t rows, uint4* __restrict__ out,
+                                                          const __grid_constant__ FlagTail ft) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t base = (int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31); base < rows; base += stride) {
+        const int64_t i = base + (threadIdx.x & 31);
+        const bool valid = i < rows;
+        if (valid) {
+            uint4 v = __ldcg(m1 + __ldcs(q + i));
+            if (m3) v = xor4(v, __ldcs(m3 + i));
+            if (r) v = xor4(v, __ldcs(r + i));
+            __stcs(out + i, v);
         }
-        uint4 v[kRows];
-#pragma unroll
-        for (int u = 0; u < kRows; u++)
-            if (i0 + (int64_t)u * blockDim.x < rows) v[u] = __ldcg(m1 + x[u]);
-#pragma unroll
-        for (int u = 0; u < kRows; u++) {
-            const int64_t i = i0 + (int64_t)u * blockDim.x;
-            if (i < rows) {
-                uint4 w = v[u];
-                if (m3) w = xor4(w, __ldcs(m3 + i));
-                if (r) w = xor4(w, __ldcs(r + i));
-                __stcs(out + i, w);
-            }
-        }
+        if (FLAG) flag_tail_word<FLAG>(ft, base, i, valid);
     }
 }
 
@@ -886,8 +910,8 @@ __global__ void __launch_bounds__(1024) perm_rounds3_block_kernel(const __grid_c
 int shuffle_init() {
     OGM_CUDA_TRY(allow_big_smem(perm_draws_kernel<AesTab>, kAesTableBytes));
     OGM_CUDA_TRY(allow_big_smem(shuffle_gather_kernel<true, AesTab>, kAesTableBytes));
-    OGM_CUDA_TRY(prefer_l1(win_gather4_kernel<kWinRows>));
-    OGM_CUDA_TRY(prefer_l1(win_gather_dual4_kernel<kWinRows>));
+    OGM_CUDA_TRY(prefer_l1(win_gather4_kernel<0>));
+    OGM_CUDA_TRY(prefer_l1(win_gather_dual4_kernel<0>));
     OGM_CUDA_TRY(prefer_l1(gather_matrix_kernel));
     OGM_CUDA_TRY(prefer_l1(gather_matrix_rows_kernel));
     return OGM_OK;
@@ -1191,9 +1215,9 @@ int ogm_gather_planned(int64_t rows, int64_t words, int64_t pitch, int64_t tile_
     }
     if (!(passes & 2)) {
     } else if (pitch == 4 && vec) {
-        int64_t g2 = std::min<int64_t>((rows + 256 * kWinRows - 1) / (256 * kWinRows), (int64_t)sm_count() * 8);
-        win_gather4_kernel<kWinRows><<<(int)g2, 256, 0, st>>>(q2, (const uint4*)inter, (const uint4*)m3, (const uint4*)r_mat,
-                                                    rows, (uint4*)out);
+        int64_t g2 = std::min<int64_t>((rows + 255) / 256, (int64_t)sm_count() * 8);
+        win_gather4_kernel<0><<<(int)g2, 256, 0, st>>>(q2, (const uint4*)inter, (const uint4*)m3, (const uint4*)r_mat,
+                                                    rows, (uint4*)out, FlagTail{});
     } else {
         GatherArgs a{};
         a.rows = rows;
@@ -1393,6 +1417,16 @@ int ogm_trio_shuffle(const uint8_t* s12, const uint8_t* s23, const uint8_t* s31,
 //   P2 -> P3, P3: c1 = win3(Ic); R3 = win4(Ir) ^ c1
 // x1, y1, c1 are optional copies of the messages; inter[0..2] are three
 // table-sized scratch buffers.
+}  // extern "C"
+namespace ogm {
+int shuffle_online_planned_impl(int64_t rows, const int32_t* const* q2, const int32_t* const* gdst,
+                                const uint16_t* const* srow, const uint32_t* a, const uint32_t* b, const uint32_t* c,
+                                const uint32_t* u_src, const uint32_t* v_src, int v_order, const uint32_t* w_src,
+                                int w_order, const uint32_t* z_src, int z_order, uint32_t* const* inter, uint32_t* x1,
+                                uint32_t* y1, uint32_t* c1, uint32_t* r3, const FlagTail* ft, void* stream);
+}
+extern "C" {
+
 int ogm_shuffle_online_planned_w_output_order(int64_t rows) {
     return rows * 16 > ogm::kDualMaxBytes ? 1 : 0;
 }
@@ -1412,7 +1446,19 @@ int ogm_shuffle_online_planned_ex(int64_t rows, const int32_t* const* q2, const 
                                   const uint32_t* w_src, int w_order, const uint32_t* z_src, int z_order,
                                   uint32_t* const* inter, uint32_t* x1, uint32_t* y1, uint32_t* c1, uint32_t* r3,
                                   void* stream) {
-    using namespace ogm;
+    return ogm::shuffle_online_planned_impl(rows, q2, gdst, srow, a, b, c, u_src, v_src, v_order, w_src, w_order,
+                                            z_src, z_order, inter, x1, y1, c1, r3, nullptr, stream);
+}
+}  // extern "C"
+
+namespace ogm {
+// the chained online shuffle; ft (optional) adds the flag-split fetch's flag
+// tail to the final window passes (ogm_fetch128_online)
+int shuffle_online_planned_impl(int64_t rows, const int32_t* const* q2, const int32_t* const* gdst,
+                                const uint16_t* const* srow, const uint32_t* a, const uint32_t* b, const uint32_t* c,
+                                const uint32_t* u_src, const uint32_t* v_src, int v_order, const uint32_t* w_src,
+                                int w_order, const uint32_t* z_src, int z_order, uint32_t* const* inter, uint32_t* x1,
+                                uint32_t* y1, uint32_t* c1, uint32_t* r3, const FlagTail* ft, void* stream) {
     OGM_CHECK_ARG(rows >= 0 && rows < ((int64_t)1 << 31), OGM_ERR_ARG, "rows out of range");
     OGM_CHECK_ARG(q2 && gdst && srow && inter, OGM_ERR_ARG, "plans and scratch are required");
     const void* need[] = {a, b, c, u_src, v_src, w_src, z_src, r3, inter[0], inter[1], inter[2]};
@@ -1466,24 +1512,38 @@ int ogm_shuffle_online_planned_ex(int64_t rows, const int32_t* const* q2, const 
     if (scrub_l2() != OGM_OK) return OGM_ERR_CUDA;
     chain(z_order == 2, q2[1], i1, (U4)z_src, srow[3], gdst[3], i0, (uint4*)y1);
     if (scrub_l2() != OGM_OK) return OGM_ERR_CUDA;
-    const int64_t g2 = std::min<int64_t>((rows + 256 * kWinRows - 1) / (256 * kWinRows), (int64_t)sm_count() * 8);
+    const int64_t g2 = std::min<int64_t>((rows + 255) / 256, (int64_t)sm_count() * 8);
+    const FlagTail none{};
     if (rows * 16 <= kDualMaxBytes) {
-        win_gather_dual4_kernel<kWinRows><<<(int)g2, 256, 0, st>>>(q2[2], i2, q2[3], i0, rows, (uint4*)r3, (uint4*)c1,
-                                                         w_out ? (U4)w_src : nullptr);
+        if (ft)
+            win_gather_dual4_kernel<3><<<(int)g2, 256, 0, st>>>(q2[2], i2, q2[3], i0, rows, (uint4*)r3, (uint4*)c1,
+                                                                w_out ? (U4)w_src : nullptr, *ft);
+        else
+            win_gather_dual4_kernel<0><<<(int)g2, 256, 0, st>>>(q2[2], i2, q2[3], i0, rows, (uint4*)r3, (uint4*)c1,
+                                                                w_out ? (U4)w_src : nullptr, none);
     } else {
         // two random windows at once thrash L2 far above its size (2^26 rows: 2.06 ms and 11 GB read
         // instead of 2.7; smaller windows do not rescue it, scripts/exp_chain_win.py): c1's window
         // pass, then R3's with c1 streamed
         uint4* c1m = c1 ? (uint4*)c1 : i1;
-        win_gather4_kernel<kWinRows><<<(int)g2, 256, 0, st>>>(
-            q2[2], i2, w_out ? (U4)w_src : nullptr, nullptr, rows, c1m);
+        if (ft)
+            win_gather4_kernel<1><<<(int)g2, 256, 0, st>>>(q2[2], i2, w_out ? (U4)w_src : nullptr, nullptr, rows, c1m,
+                                                           *ft);
+        else
+            win_gather4_kernel<0><<<(int)g2, 256, 0, st>>>(q2[2], i2, w_out ? (U4)w_src : nullptr, nullptr, rows, c1m,
+                                                           none);
         if (scrub_l2() != OGM_OK) return OGM_ERR_CUDA;
-        win_gather4_kernel<kWinRows><<<(int)g2, 256, 0, st>>>(
-            q2[3], i0, c1m, nullptr, rows, (uint4*)r3);
+        if (ft)
+            win_gather4_kernel<2><<<(int)g2, 256, 0, st>>>(q2[3], i0, c1m, nullptr, rows, (uint4*)r3, *ft);
+        else
+            win_gather4_kernel<0><<<(int)g2, 256, 0, st>>>(q2[3], i0, c1m, nullptr, rows, (uint4*)r3, none);
     }
     OGM_LAUNCH_CHECK();
     return OGM_OK;
 }
+}  // namespace ogm
+
+extern "C" {
 
 int ogm_shuffle_online_fused(int64_t rows, const int32_t* k1, const int32_t* pi12, const int32_t* pi23,
                              const int32_t* k3, const uint32_t* a, const uint32_t* b, const uint32_t* c,

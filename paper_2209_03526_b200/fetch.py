@@ -12,11 +12,16 @@ out rows (csrc/ogm_fetch.cuh).  The blinds are drawn in the reference's
 the kept records are bit-identical to the reference's.
 
 Online phase (what the C5 fetch bench times):
-  1. payload: the 16-byte three-party shuffle -- one cooperative launch up
-     to 2^21 rows, the chained planned gathers above (shuffle.py);
-  2. flag column: two bit-gather launches (ogm_flag_shuffle_trio), which
-     also write the opened column;
-  3. keep: hand-written compaction copying the kept payload rows of the
+  1. up to 2^21 rows: the 16-byte three-party shuffle in one cooperative
+     launch, then the flag column's two bit-gather launches
+     (ogm_flag_shuffle_trio, which also write the opened column);
+     from 2^22 rows: the chained planned payload shuffle, then the same two
+     flag launches; above 256 MB tables ONE launch sequence
+     (ogm_fetch128_online_planned): the flag column's first phase, then the
+     payload shuffle whose split final window passes also compute the flag
+     column's second phase and the opened column (they walk the rows in
+     output order anyway);
+  2. keep: hand-written compaction copying the kept payload rows of the
      three new components (ogm_keep_rows).
 """
 
@@ -31,6 +36,7 @@ from .bits import words_for
 from .shuffle import FLAG_ROW_BITS, ShuffleOffline, shuffle_online_fused, shuffle_online_planned
 
 FUSED_MAX_BYTES = 32 << 20   # one cooperative launch up to 2^21 16-byte rows (measured crossover)
+FLAG_TAIL_MIN_BYTES = 256 << 20   # above: the flag column's phase 2 rides the split window passes
 
 
 class FlaggedFetch:
@@ -38,7 +44,8 @@ class FlaggedFetch:
     128-bit rows for table id ``tid``.  ``seeds`` = (s12, s23, s31), the
     pairwise seeds (party 1 holds s12 and s31, and so on)."""
 
-    def __init__(self, seeds: tuple, tid: int, rows: int, device=None, perm_cache=None, plan: bool | None = None):
+    def __init__(self, seeds: tuple, tid: int, rows: int, device=None, perm_cache=None, plan: bool | None = None,
+                 flag_tail: bool | None = None):
         s12, s23, s31 = seeds
         self.rows, self.tid = rows, tid
         self.dev = torch.device(device or "cuda")
@@ -65,7 +72,11 @@ class FlaggedFetch:
             return torch.empty((max(nw, 1),), dtype=torch.int32, device=self.dev)
 
         self.r3 = torch.empty((rows, 4), dtype=torch.int32, device=self.dev)
-        self.x1f, self.y1f, self.r3f, self.plain = vec(), vec(), vec(), vec()
+        self.x1f, self.y1f, self.c1f, self.r3f, self.plain = vec(), vec(), vec(), vec(), vec()
+        self.plans = None if self.fused else [p1.plan_x1, p2.plan_y1, p2.plan_c1, p3.plan_r3]
+        # the flag tail rides the final window passes only where they are split (> 256 MB):
+        # measured 1% faster at 2^28, 2% slower folded into the dual pass at 2^24
+        self.flag_tail = not self.fused and (rows * 16 > FLAG_TAIL_MIN_BYTES if flag_tail is None else flag_tail)
         self.inter = ([torch.empty_like(self.r3) for _ in range(3)] if not self.fused
                       else [torch.empty_like(self.r3) for _ in range(2)])
         self.outs = [torch.empty((max(rows, 1), 4), dtype=torch.int32, device=self.dev) for _ in range(3)]
@@ -88,15 +99,29 @@ class FlaggedFetch:
         for t in payload:
             if t.shape != (rows, 4) or not t.is_contiguous():
                 raise ValueError("payload components must be contiguous (rows, 4) tables")
-        if self.fused:
-            shuffle_online_fused(self.off, a, b, c, self.inter[0], self.inter[1], None, self.r3)
-        else:
-            shuffle_online_planned(self.off, a, b, c, self.r3, inter=self.inter)
         P = _lib.ptr
-        _lib.call("ogm_flag_shuffle_trio", rows, P(p1.k1), P(p2.pi12), P(p2.pi23), P(p3.k3), P(flags[0]),
-                  P(flags[1]), P(flags[2]), P(p1.flag["u"]), P(p2.flag["v"]), P(p2.flag["w"]), P(p3.flag["z"]),
-                  P(self.r1f), P(self.r2f), P(self.x1f), P(self.y1f), None, P(self.r3f), P(self.plain),
-                  _lib.stream_ptr())
+        if self.fused or not self.flag_tail:
+            if self.fused:
+                shuffle_online_fused(self.off, a, b, c, self.inter[0], self.inter[1], None, self.r3)
+            else:
+                shuffle_online_planned(self.off, a, b, c, self.r3, inter=self.inter)
+            _lib.call("ogm_flag_shuffle_trio", rows, P(p1.k1), P(p2.pi12), P(p2.pi23), P(p3.k3), P(flags[0]),
+                      P(flags[1]), P(flags[2]), P(p1.flag["u"]), P(p2.flag["v"]), P(p2.flag["w"]), P(p3.flag["z"]),
+                      P(self.r1f), P(self.r2f), P(self.x1f), P(self.y1f), None, P(self.r3f), P(self.plain),
+                      _lib.stream_ptr())
+        else:
+            # one launch sequence: flag phase 1, then the chained payload shuffle whose final
+            # window passes also produce the flag column's phase 2 and the opened column
+            (u,), (v, w), (z,) = p1.chain_blinds(), p2.chain_blinds(), p3.chain_blinds()
+            arr = lambda xs: (ctypes.c_void_p * len(xs))(*[P(x) for x in xs])  # noqa: E731
+            q2, gd, sr, it = (arr([pl.q2 for pl in self.plans]), arr([pl.gdst for pl in self.plans]),
+                              arr([pl.srow for pl in self.plans]), arr(self.inter))
+            _lib.call("ogm_fetch128_online_planned", rows, ctypes.addressof(q2), ctypes.addressof(gd),
+                      ctypes.addressof(sr), P(a), P(b), P(c), P(u), P(v), P(w), 1 if p2.w_output_order else 2,
+                      P(z), ctypes.addressof(it), P(self.r3), P(p1.k1), P(p2.pi12), P(p2.pi23), P(p3.k3),
+                      P(flags[0]), P(flags[1]), P(flags[2]), P(p1.flag["u"]), P(p2.flag["v"]), P(p2.flag["w"]),
+                      P(p3.flag["z"]), P(self.r1f), P(self.r2f), P(self.x1f), P(self.y1f), P(self.c1f),
+                      P(self.r3f), P(self.plain), _lib.stream_ptr())
         mats = (ctypes.c_void_p * 3)(P(self.r1), P(self.r2), P(self.r3))
         outs = (ctypes.c_void_p * 3)(*[P(o) for o in self.outs])
         _lib.call("ogm_keep_rows", rows, P(self.plain), 3, ctypes.addressof(mats), 4, ctypes.addressof(outs), 4,

@@ -63,19 +63,25 @@ def _inputs(rows: int, p: float, seed: int):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("rows,p,plan", [(1, 1.0, False), (33, 0.5, False), (1000, 0.1, False),
-                                         (1 << 20, 0.1, False), (1 << 20, 0.01, True),
-                                         ((1 << 20) + 77, 1.0, True), (40000, 0.0, True)])
-def test_flagged_fetch_matches_oracle(rows, p, plan):
+@pytest.mark.parametrize("rows,p,plan,tail", [(1, 1.0, False, None), (33, 0.5, False, None),
+                                              (1000, 0.1, False, None), (1 << 20, 0.1, False, None),
+                                              (1 << 20, 0.01, True, None), ((1 << 20) + 77, 1.0, True, None),
+                                              (40000, 0.0, True, None), ((1 << 20) + 77, 0.3, True, True),
+                                              (1 << 22, 0.1, True, True), ((1 << 24) + 33, 0.05, None, None)])
+def test_flagged_fetch_matches_oracle(rows, p, plan, tail):
     """Records, opened flags and the three new components of the split
-    fetch equal the oracle's sec_fetch_multi bit for bit."""
+    fetch equal the oracle's sec_fetch_multi bit for bit: one cooperative
+    launch, the chained shuffle + flag kernels, and the flag column riding
+    the final window passes (dual pass; split passes above 256 MB)."""
     import torch
 
     from paper_2209_03526_b200.fetch import FlaggedFetch
 
     seeds = _seeds(bytes([0x5f, rows & 0xFF]) * 8)
     ids, flags, plain = _inputs(rows, p, rows)
-    ff = FlaggedFetch(seeds, 3, rows, plan=plan)
+    ff = FlaggedFetch(seeds, 3, rows, plan=plan, flag_tail=tail)
+    if rows > (1 << 24):
+        assert ff.flag_tail   # the split final window passes carry the flag column
     ff.online([_dev(f) for f in flags], [_dev(m) for m in ids])
     keep, want_plain, want = oracle.fetch_multi_trio(*seeds, 3, flags, ids, 128)
     got_plain = oracle.unpack_bits(ff.plain.cpu().numpy().view(np.uint32), rows)
