@@ -301,10 +301,12 @@ int ogm_flag_shuffle_trio(int64_t rows, const int32_t* k1, const int32_t* pi12, 
  * (as ogm_shuffle_online_planned_ex with V in source order and Z in slot
  * order) whose final window passes also compute c1f, r3f and the opened
  * column `plain` -- the flag column needs the rows in output order, which
- * those passes walk anyway.  Same results as ogm_shuffle_online_planned_ex +
+ * those passes walk anyway.  qs as ogm_shuffle_online_planned_slots (may be
+ * NULL).  Same results as ogm_shuffle_online_planned_ex +
  * ogm_flag_shuffle_trio. */
 int ogm_fetch128_online_planned(int64_t rows, const int32_t* const* q2, const int32_t* const* gdst,
-                                const uint16_t* const* srow, const uint32_t* a, const uint32_t* b, const uint32_t* c,
+                                const uint16_t* const* srow, const int32_t* const* qs, const uint32_t* a,
+                                const uint32_t* b, const uint32_t* c,
                                 const uint32_t* u_src, const uint32_t* v_src, const uint32_t* w_blind, int w_order,
                                 const uint32_t* z_slot, uint32_t* const* inter, uint32_t* r3, const int32_t* k1,
                                 const int32_t* pi12, const int32_t* pi23, const int32_t* k3, const uint32_t* f1,
@@ -469,6 +471,20 @@ int ogm_shuffle_online_planned_ex(int64_t rows, const int32_t* const* q2, const 
                                   const uint32_t* w_src, int w_order, const uint32_t* z_src, int z_order,
                                   uint32_t* const* inter, uint32_t* x1, uint32_t* y1, uint32_t* c1, uint32_t* r3,
                                   void* stream);
+
+/* The chained online shuffle with the flat hand-over: qs[0] = x1's window
+ * index composed with c1's partition slot order (qs[0][t*4096 + k] =
+ * q2[0][t*4096 + srow[2][t*4096 + k]]), qs[1] the same for y1 -> R3 (q2[1],
+ * srow[3]).  Each slot then fetches its message row from the sender's window
+ * and scatters it as the receiver's partition in one streaming pass (no
+ * shared-memory staging).  Blinds: U', V' in source order, W in c1's output
+ * (w_order 1) or slot (2) order, Z in slot order.  Same results as
+ * ogm_shuffle_online_planned_ex. */
+int ogm_shuffle_online_planned_slots(int64_t rows, const int32_t* const* q2, const int32_t* const* gdst,
+                                     const uint16_t* const* srow, const int32_t* const* qs, const uint32_t* a,
+                                     const uint32_t* b, const uint32_t* c, const uint32_t* u_src,
+                                     const uint32_t* v_src, const uint32_t* w_blind, int w_order,
+                                     const uint32_t* z_slot, uint32_t* const* inter, uint32_t* r3, void* stream);
 
 /* ---- native trio executor (src/engine.py:352-417 for three co-resident
  * parties) ------------------------------------------------------------------

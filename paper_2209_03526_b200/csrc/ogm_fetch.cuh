@@ -314,10 +314,12 @@ int ogm_flag_shuffle_trio(int64_t rows, const int32_t* k1, const int32_t* pi12, 
 // phase 1 (f1 ^ f2, then x1f / y1f), then the chained planned payload shuffle
 // whose final window passes carry flag phase 2 and the open (FlagTail): one
 // launch sequence, no separate phase-2 flag kernel.  Arguments as
-// ogm_shuffle_online_planned_ex (V in source order, Z in slot order) and
-// ogm_flag_shuffle_trio; c1f is scratch when the passes are split (> 256 MB).
+// ogm_shuffle_online_planned_slots (qs: the composed slot indices, may be
+// null for the staged hand-over) and ogm_flag_shuffle_trio; c1f is scratch
+// when the passes are split (> 256 MB).
 int ogm_fetch128_online_planned(int64_t rows, const int32_t* const* q2, const int32_t* const* gdst,
-                                const uint16_t* const* srow, const uint32_t* a, const uint32_t* b, const uint32_t* c,
+                                const uint16_t* const* srow, const int32_t* const* qs, const uint32_t* a,
+                                const uint32_t* b, const uint32_t* c,
                                 const uint32_t* u_src, const uint32_t* v_src, const uint32_t* w_blind, int w_order,
                                 const uint32_t* z_slot, uint32_t* const* inter, uint32_t* r3, const int32_t* k1,
                                 const int32_t* pi12, const int32_t* pi23, const int32_t* k3, const uint32_t* f1,
@@ -338,7 +340,7 @@ int ogm_fetch128_online_planned(int64_t rows, const int32_t* const* q2, const in
     OGM_LAUNCH_CHECK();
     const FlagTail ft{pi23, k3, x1f, y1f, wf, zf, r1f, r2f, c1f, r3f, plain};
     return shuffle_online_planned_impl(rows, q2, gdst, srow, a, b, c, u_src, v_src, 0, w_blind, w_order, z_slot, 2,
-                                       inter, nullptr, nullptr, nullptr, r3, &ft, stream);
+                                       inter, nullptr, nullptr, nullptr, r3, &ft, qs, stream);
 }
 
 int64_t ogm_keep_rows_workspace_bytes(int64_t rows) {

@@ -449,6 +449,21 @@ static void* scrub_buffer(int64_t* bytes) {
     return buf[dev];
 }
 
+// two chunk counters per device for the flat chain passes (stream-ordered reuse)
+static void* flat_counters() {
+    static std::mutex mu;
+    static void* buf[64] = {};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 0 || dev >= 64) return nullptr;
+    std::lock_guard<std::mutex> g(mu);
+    if (!buf[dev] && cudaMalloc(&buf[dev], 256) != cudaSuccess) {
+        cudaGetLastError();
+        buf[dev] = nullptr;
+    }
+    return buf[dev];
+}
+
 __device__ __forceinline__ uint4 xorU(uint4 a, uint4 b) { return xor4(a, b); }
 __device__ __forceinline__ uint32_t xorU(uint32_t a, uint32_t b) { return a ^ b; }
 
@@ -743,6 +758,44 @@ __global__ void __launch_bounds__(kTmaThreads, 1) plan_chain_kernel(
         for (int k = threadIdx.x; k < nr; k += kTmaThreads) {
             const uint4 v = rs[__ldcs(srow + b0 + k)];
             __stcs(inter_b + __ldcs(gdst + b0 + k), (SLOT_BLIND && blind) ? xor4(v, __ldcs(blind + b0 + k)) : v);
+        }
+    }
+}
+
+// The chained hand-over without shared memory: the sender's window index,
+// composed offline with the receiver partition's slot order
+// (qs[t*T + k] = q[t*T + srow[t*T + k]]), lets each slot fetch its message
+// row straight from the sender's window and scatter it to the receiver's
+// intermediate: ib[gdst[s]] = ia[qs[s]] ^ bl[s] (bl in slot order).  Slots
+// of one tile are consecutive, so the reads stay inside one window (L2) and
+// consecutive slots of a run write consecutive rows.  A flat streaming pass
+// like the window passes: no staging, no barriers, no MIO traffic -- the
+// staged kernel above was bound by exactly those (LSU and MIO throttles).
+// Chunks of kFlatChunk slots are handed out in order through an atomic
+// counter, so the slots in flight stay inside a narrow range of consecutive
+// tiles -- one sender window -- however unevenly the blocks progress (a
+// grid-stride loop lets slow blocks lag into earlier windows; at 2^26 rows
+// that made the window reads miss L2: 77 instead of 40 B/row).
+constexpr int kFlatChunk = 2048;
+
+__global__ void __launch_bounds__(256) chain_flat_kernel(const int32_t* __restrict__ qs,
+                                                         const uint4* __restrict__ ia,
+                                                         const uint4* __restrict__ bl,
+                                                         const int32_t* __restrict__ gdst, int64_t rows,
+                                                         uint4* __restrict__ ib, unsigned long long* next) {
+    __shared__ int64_t chunk;
+    for (;;) {
+        if (threadIdx.x == 0) chunk = (int64_t)atomicAdd(next, 1ull);
+        __syncthreads();
+        const int64_t c0 = chunk * kFlatChunk;
+        __syncthreads();
+        if (c0 >= rows) break;
+        const int64_t c1 = min(rows, c0 + kFlatChunk);
+#pragma unroll 4
+        for (int64_t s = c0 + threadIdx.x; s < c1; s += blockDim.x) {
+            uint4 v = __ldcg(ia + __ldcs(qs + s));
+            if (bl) v = xor4(v, __ldcs(bl + s));
+            __stcs(ib + __ldcs(gdst + s), v);
         }
     }
 }
@@ -1423,7 +1476,8 @@ int shuffle_online_planned_impl(int64_t rows, const int32_t* const* q2, const in
                                 const uint16_t* const* srow, const uint32_t* a, const uint32_t* b, const uint32_t* c,
                                 const uint32_t* u_src, const uint32_t* v_src, int v_order, const uint32_t* w_src,
                                 int w_order, const uint32_t* z_src, int z_order, uint32_t* const* inter, uint32_t* x1,
-                                uint32_t* y1, uint32_t* c1, uint32_t* r3, const FlagTail* ft, void* stream);
+                                uint32_t* y1, uint32_t* c1, uint32_t* r3, const FlagTail* ft,
+                                const int32_t* const* qs, void* stream);
 }
 extern "C" {
 
@@ -1447,7 +1501,7 @@ int ogm_shuffle_online_planned_ex(int64_t rows, const int32_t* const* q2, const 
                                   uint32_t* const* inter, uint32_t* x1, uint32_t* y1, uint32_t* c1, uint32_t* r3,
                                   void* stream) {
     return ogm::shuffle_online_planned_impl(rows, q2, gdst, srow, a, b, c, u_src, v_src, v_order, w_src, w_order,
-                                            z_src, z_order, inter, x1, y1, c1, r3, nullptr, stream);
+                                            z_src, z_order, inter, x1, y1, c1, r3, nullptr, nullptr, stream);
 }
 }  // extern "C"
 
@@ -1458,7 +1512,8 @@ int shuffle_online_planned_impl(int64_t rows, const int32_t* const* q2, const in
                                 const uint16_t* const* srow, const uint32_t* a, const uint32_t* b, const uint32_t* c,
                                 const uint32_t* u_src, const uint32_t* v_src, int v_order, const uint32_t* w_src,
                                 int w_order, const uint32_t* z_src, int z_order, uint32_t* const* inter, uint32_t* x1,
-                                uint32_t* y1, uint32_t* c1, uint32_t* r3, const FlagTail* ft, void* stream) {
+                                uint32_t* y1, uint32_t* c1, uint32_t* r3, const FlagTail* ft,
+                                const int32_t* const* qs, void* stream) {
     OGM_CHECK_ARG(rows >= 0 && rows < ((int64_t)1 << 31), OGM_ERR_ARG, "rows out of range");
     OGM_CHECK_ARG(q2 && gdst && srow && inter, OGM_ERR_ARG, "plans and scratch are required");
     const void* need[] = {a, b, c, u_src, v_src, w_src, z_src, r3, inter[0], inter[1], inter[2]};
@@ -1508,9 +1563,23 @@ int shuffle_online_planned_impl(int64_t rows, const int32_t* const* q2, const in
         else
             plan_chain_kernel<false><<<g, TT, kChainSmem2, st>>>(q, ia, bl, sr, gd, rows, ib, msg);
     };
-    chain(w_order == 2, q2[0], i0, w_out ? nullptr : (U4)w_src, srow[2], gdst[2], i2, (uint4*)x1);
+    const int64_t gf = std::min<int64_t>((rows + kFlatChunk - 1) / kFlatChunk, (int64_t)sm_count() * 8);
+    unsigned long long* ctr = nullptr;
+    if (qs) {
+        ctr = (unsigned long long*)flat_counters();
+        if (!ctr) return OGM_ERR_CUDA;
+        OGM_CUDA_TRY(cudaMemsetAsync(ctr, 0, 2 * sizeof(unsigned long long), st));
+    }
+    // the flat hand-over needs the composed indices, slot-order (or no) blinds and no message copies
+    if (qs && qs[0] && !x1 && (w_order == 2 || w_out))
+        chain_flat_kernel<<<(int)gf, 256, 0, st>>>(qs[0], i0, w_out ? nullptr : (U4)w_src, gdst[2], rows, i2, ctr);
+    else
+        chain(w_order == 2, q2[0], i0, w_out ? nullptr : (U4)w_src, srow[2], gdst[2], i2, (uint4*)x1);
     if (scrub_l2() != OGM_OK) return OGM_ERR_CUDA;
-    chain(z_order == 2, q2[1], i1, (U4)z_src, srow[3], gdst[3], i0, (uint4*)y1);
+    if (qs && qs[1] && !y1 && z_order == 2)
+        chain_flat_kernel<<<(int)gf, 256, 0, st>>>(qs[1], i1, (U4)z_src, gdst[3], rows, i0, ctr + 1);
+    else
+        chain(z_order == 2, q2[1], i1, (U4)z_src, srow[3], gdst[3], i0, (uint4*)y1);
     if (scrub_l2() != OGM_OK) return OGM_ERR_CUDA;
     const int64_t g2 = std::min<int64_t>((rows + 255) / 256, (int64_t)sm_count() * 8);
     const FlagTail none{};
@@ -1544,6 +1613,18 @@ int shuffle_online_planned_impl(int64_t rows, const int32_t* const* q2, const in
 }  // namespace ogm
 
 extern "C" {
+
+int ogm_shuffle_online_planned_slots(int64_t rows, const int32_t* const* q2, const int32_t* const* gdst,
+                                     const uint16_t* const* srow, const int32_t* const* qs, const uint32_t* a,
+                                     const uint32_t* b, const uint32_t* c, const uint32_t* u_src,
+                                     const uint32_t* v_src, const uint32_t* w_blind, int w_order,
+                                     const uint32_t* z_slot, uint32_t* const* inter, uint32_t* r3, void* stream) {
+    using namespace ogm;
+    OGM_CHECK_ARG(qs && qs[0] && qs[1], OGM_ERR_ARG, "the two composed slot indices are required");
+    OGM_CHECK_ARG(w_order == 1 || w_order == 2, OGM_ERR_ARG, "W in c1's output (1) or slot (2) order");
+    return shuffle_online_planned_impl(rows, q2, gdst, srow, a, b, c, u_src, v_src, 0, w_blind, w_order, z_slot, 2,
+                                       inter, nullptr, nullptr, nullptr, r3, nullptr, qs, stream);
+}
 
 int ogm_shuffle_online_fused(int64_t rows, const int32_t* k1, const int32_t* pi12, const int32_t* pi23,
                              const int32_t* k3, const uint32_t* a, const uint32_t* b, const uint32_t* c,
