@@ -780,8 +780,10 @@ __global__ void __launch_bounds__(kTmaThreads, 1) plan_chain_kernel(
 // counter, so the slots in flight stay inside a narrow range of consecutive
 // tiles -- one sender window -- however unevenly the blocks progress (a
 // grid-stride loop lets slow blocks lag into earlier windows; at 2^26 rows
-// that made the window reads miss L2: 77 instead of 40 B/row).
-constexpr int kFlatChunk = 2048;
+// that made the window reads miss L2: 77 instead of 40 B/row).  Chunk size
+// measured at 256 / 512 / 1024 / 2048 / 4096 slots: 1024 is best (2^24:
+// 0.91 / 0.82 / 0.82 / 0.84 / 0.94 ms; 2^28: 15.8 / 15.0 / 14.8 / 15.1 / 17.3).
+constexpr int kFlatChunk = 1024;
 
 // the first row of this block's next chunk: handed out in order through the
 // counter `next` (all threads get the block's value), or, without a counter,
