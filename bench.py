@@ -381,6 +381,23 @@ def c5_legs(args, world: int) -> dict:
     return out
 
 
+def guarded(name: str, fn):
+    """A secondary leg: its failure (an out-of-memory, a missing package) is
+    recorded in the line instead of losing the headline.  Bit-exactness gates
+    raise SystemExit and are NOT caught: a wrong result is never reported."""
+    try:
+        return fn()
+    except Exception as exc:  # noqa: BLE001
+        import traceback
+        traceback.print_exc()
+        try:
+            import torch
+            torch.cuda.empty_cache()
+        except Exception:  # noqa: BLE001
+            pass
+        return {"error": f"{name}: {type(exc).__name__}: {exc}"[:500]}
+
+
 def main():
     args = parse()
     rc = launch_ranks(args)
@@ -545,7 +562,7 @@ def main():
 
     query = None
     if rank == 0 and not args.no_query:
-        query = query_latency(args.query_steps)
+        query = guarded("query_latency", lambda: query_latency(args.query_steps))
 
     # the 16M-vertex config (BASELINE configs[3]): row-sharded secEval over all ranks
     c4 = None
@@ -553,22 +570,23 @@ def main():
         import bench_configs
         del b0, pts, out
         torch.cuda.empty_cache()
-        c4 = bench_configs.c4_sec_eval(2_000_000, 1, 10, 3, rank, world)
+        c4 = guarded("c4_sec_eval", lambda: bench_configs.c4_sec_eval(2_000_000, 1, 10, 3, rank, world))
         torch.cuda.empty_cache()
-        c4["root_slot"] = bench_configs.c4_root_slot(2_000_000, 1, 10, 3, rank, world)
+        c4["root_slot"] = guarded("c4_root_slot",
+                                  lambda: bench_configs.c4_root_slot(2_000_000, 1, 10, 3, rank, world))
 
     # C3 (BASELINE configs[2]): the medium graph's root slot on one GPU
     c3 = None
     if world == 1 and not args.no_c3:
         import bench_configs
         torch.cuda.empty_cache()
-        c3 = bench_configs.c3_leg(args.steps, args.warmup)
+        c3 = guarded("c3_root_slot", lambda: bench_configs.c3_leg(args.steps, args.warmup))
         torch.cuda.empty_cache()
 
     # C5 (BASELINE configs[4]): shuffle and 1/10/100% fetch bandwidth, every rank its own tables
     c5 = None
     if not args.no_c5:
-        c5 = c5_legs(args, world)
+        c5 = guarded("c5", lambda: c5_legs(args, world))
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
@@ -583,7 +601,8 @@ def main():
     live = None
     if rank == 0 and world == 1 and not args.no_live_ref:
         import bench_reference
-        live = bench_reference.live_reference([int(x) for x in args.c5_logs.split(",") if x])
+        live = guarded("live_reference",
+                       lambda: bench_reference.live_reference([int(x) for x in args.c5_logs.split(",") if x]))
         if query is not None and "c1" in live:
             live["c1"]["matches_equal_ours"] = live["c1"]["matches"] == sorted(query.get("match_list", []))
 
