@@ -301,14 +301,16 @@ int ogm_flag_shuffle_trio(int64_t rows, const int32_t* k1, const int32_t* pi12, 
  * (as ogm_shuffle_online_planned_ex with V in source order and Z in slot
  * order) whose final window passes also compute c1f, r3f and the opened
  * column `plain` -- the flag column needs the rows in output order, which
- * those passes walk anyway.  qs as ogm_shuffle_online_planned_slots (may be
- * NULL).  Same results as ogm_shuffle_online_planned_ex +
+ * those passes walk anyway.  qs and run_* as ogm_shuffle_online_planned_slots
+ * (may be NULL).  Same results as ogm_shuffle_online_planned_ex +
  * ogm_flag_shuffle_trio. */
 int ogm_fetch128_online_planned(int64_t rows, const int32_t* const* q2, const int32_t* const* gdst,
-                                const uint16_t* const* srow, const int32_t* const* qs, const uint32_t* a,
-                                const uint32_t* b, const uint32_t* c,
-                                const uint32_t* u_src, const uint32_t* v_src, const uint32_t* w_blind, int w_order,
-                                const uint32_t* z_slot, uint32_t* const* inter, uint32_t* r3, const int32_t* k1,
+                                const uint16_t* const* srow, const int32_t* const* qs,
+                                const uint16_t* const* run_start, const int32_t* const* run_off,
+                                const int64_t* run_nwin, const int64_t* wrows, const uint32_t* a, const uint32_t* b,
+                                const uint32_t* c, const uint32_t* u_src, const uint32_t* v_src,
+                                const uint32_t* w_blind, int w_order, const uint32_t* z_slot, int z_order,
+                                uint32_t* const* inter, uint32_t* r3, const int32_t* k1,
                                 const int32_t* pi12, const int32_t* pi23, const int32_t* k3, const uint32_t* f1,
                                 const uint32_t* f2, const uint32_t* f3, const uint32_t* uf, const uint32_t* vf,
                                 const uint32_t* wf, const uint32_t* zf, const uint32_t* r1f, const uint32_t* r2f,
@@ -391,6 +393,16 @@ int64_t ogm_gather_tile_rows(int64_t pitch_words);
 int64_t ogm_gather_plan_workspace_bytes(int64_t n);
 int ogm_gather_plan(int64_t n, const int32_t* idx, int64_t window_rows, int64_t tile_rows, int32_t* q2,
                     int32_t* gdst, uint16_t* srow, void* workspace, int64_t workspace_bytes, void* stream);
+/* A plan's run table (offline): tile t's slots are grouped by destination
+ * window with the I rows of a (tile, window) run consecutive, so
+ * gdst[s] = off[t*OS + d] + s for global slot s in run d of tile t.
+ * start[t*SS + d] (uint16) = the tile slot where run d begins (an empty run:
+ * where the next begins), start[t*SS + nwin] = the tile's row count; nwin =
+ * ceil(n / window_rows), SS = (nwin + 8) & ~7, OS = (nwin + 3) & ~3
+ * (16-byte per-tile strides for bulk copies), start: ceil(n / tile_rows) * SS
+ * uint16, off: ceil(n / tile_rows) * OS int32.  tile_rows <= 32768. */
+int ogm_gather_plan_runs(int64_t n, int64_t window_rows, int64_t tile_rows, const int32_t* gdst, uint16_t* start,
+                         int32_t* off, void* stream);
 int ogm_gather_planned(int64_t rows, int64_t words, int64_t pitch, int64_t tile_rows, const int32_t* q2,
                        const int32_t* gdst, const uint16_t* srow, const uint32_t* m1, const uint32_t* m2,
                        const uint32_t* m4, const uint32_t* m3, const uint32_t* r_mat, uint32_t* inter, uint32_t* out,
@@ -472,19 +484,35 @@ int ogm_shuffle_online_planned_ex(int64_t rows, const int32_t* const* q2, const 
                                   uint32_t* const* inter, uint32_t* x1, uint32_t* y1, uint32_t* c1, uint32_t* r3,
                                   void* stream);
 
-/* The chained online shuffle with the flat hand-over: qs[0] = x1's window
- * index composed with c1's partition slot order (qs[0][t*4096 + k] =
- * q2[0][t*4096 + srow[2][t*4096 + k]]), qs[1] the same for y1 -> R3 (q2[1],
- * srow[3]).  Each slot then fetches its message row from the sender's window
- * and scatters it as the receiver's partition in one streaming pass (no
- * shared-memory staging).  Blinds: U', V' in source order, W in c1's output
- * (w_order 1) or slot (2) order, Z in slot order.  Same results as
- * ogm_shuffle_online_planned_ex. */
+/* The chained online shuffle with the flat hand-over: each row of the
+ * receiver's partition fetches its message row from the sender's window in
+ * one streaming pass (no shared-memory staging), in one of two orders:
+ *   z_order 3 (I order; the product path): qs[0][p] = q2[0][src2[p]] for
+ *     every I row p of c1's plan, src2[p] = the source row that I row holds
+ *     (the row of slot s = t*4096 + srow[2][s] at p = gdst[2][s]); qs[1]
+ *     the same for y1 -> R3 (q2[1], plan 3).  The pass writes I rows
+ *     sequentially and reads no destination index; chunks are interleaved
+ *     over the receiver's windows (wrows[2], wrows[3] = its window rows) so
+ *     the sender-window reads stay L2-resident.  W (w_order 3) and Z are in
+ *     the same I-row order;
+ *   z_order 2 (slot order): qs[0][t*4096 + k] = q2[0][t*4096 +
+ *     srow[2][t*4096 + k]], the slot scattered through gdst[2]; W (w_order
+ *     2) and Z in slot order.
+ * w_order 1: W in c1's output order, streamed in c1's window pass (no blind
+ * in the hand-over).  U', V' in source order.  run_start / run_off /
+ * run_nwin: the four plans' run tables (ogm_gather_plan_runs; arrays of 4,
+ * all NULL to read gdst instead): the two partition passes then locate each
+ * slot's destination from its tile's table (staged with the tile) instead of
+ * reading 4 B of gdst per row.  Same results as
+ * ogm_shuffle_online_planned_ex.  ABI version 3. */
 int ogm_shuffle_online_planned_slots(int64_t rows, const int32_t* const* q2, const int32_t* const* gdst,
-                                     const uint16_t* const* srow, const int32_t* const* qs, const uint32_t* a,
+                                     const uint16_t* const* srow, const int32_t* const* qs,
+                                     const uint16_t* const* run_start, const int32_t* const* run_off,
+                                     const int64_t* run_nwin, const int64_t* wrows, const uint32_t* a,
                                      const uint32_t* b, const uint32_t* c, const uint32_t* u_src,
                                      const uint32_t* v_src, const uint32_t* w_blind, int w_order,
-                                     const uint32_t* z_slot, uint32_t* const* inter, uint32_t* r3, void* stream);
+                                     const uint32_t* z_slot, int z_order, uint32_t* const* inter, uint32_t* r3,
+                                     void* stream);
 
 /* ---- native trio executor (src/engine.py:352-417 for three co-resident
  * parties) ------------------------------------------------------------------

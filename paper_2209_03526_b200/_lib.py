@@ -74,8 +74,8 @@ SIGNATURES = {
     "ogm_keep_rows": ([_i64, _vp, _int, _vp, _i64, _vp, _i64, _vp, _vp, _vp, _i64, _vp], _int),
     "ogm_split_flag_rows": ([_i64, _vp, _i64, _vp, _vp, _vp], _int),
     "ogm_flag_shuffle_trio": ([_i64] + [_vp] * 19, _int),
-    "ogm_fetch128_online_planned": ([_i64] + [_vp] * 10 + [_int] + [_vp] * 22, _int),
-    "ogm_shuffle_online_planned_slots": ([_i64] + [_vp] * 10 + [_int] + [_vp] * 4, _int),
+    "ogm_fetch128_online_planned": ([_i64] + [_vp] * 14 + [_int, _vp, _int] + [_vp] * 21, _int),
+    "ogm_shuffle_online_planned_slots": ([_i64] + [_vp] * 14 + [_int, _vp, _int] + [_vp] * 3, _int),
     "ogm_shuffle_gather": ([_i64, _i64, _i64, _vp, _vp, _vp, _vp, _vp, _cp, _cp, _u64, _vp, _cp, _cp, _u64,
                             _vp, _cp, _cp, _u64, _vp, _i64, _i64, _vp, _vp], _int),
     "ogm_perm_compose": ([_i64, _vp, _vp, _vp, _vp], _int),
@@ -84,6 +84,7 @@ SIGNATURES = {
     "ogm_gather_tile_rows": ([_i64], _i64),
     "ogm_gather_plan_workspace_bytes": ([_i64], _i64),
     "ogm_gather_plan": ([_i64, _vp, _i64, _i64, _vp, _vp, _vp, _vp, _i64, _vp], _int),
+    "ogm_gather_plan_runs": ([_i64, _i64, _i64, _vp, _vp, _vp, _vp], _int),
     "ogm_gather_planned": ([_i64, _i64, _i64, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _int, _vp], _int),
     "ogm_trio_shuffle_workspace_bytes": ([_i64, _i64], _i64),
     "ogm_trio_shuffle": ([_cp, _cp, _cp, _u64, _i64, _i64, _i64, _int, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _vp], _int),

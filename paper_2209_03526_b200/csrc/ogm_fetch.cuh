@@ -315,13 +315,15 @@ int ogm_flag_shuffle_trio(int64_t rows, const int32_t* k1, const int32_t* pi12, 
 // whose final window passes carry flag phase 2 and the open (FlagTail): one
 // launch sequence, no separate phase-2 flag kernel.  Arguments as
 // ogm_shuffle_online_planned_slots (qs: the composed slot indices, may be
-// null for the staged hand-over) and ogm_flag_shuffle_trio; c1f is scratch
-// when the passes are split (> 256 MB).
+// null for the staged hand-over; run_*: the plans' run tables, or null) and
+// ogm_flag_shuffle_trio; c1f is scratch when the passes are split (> 256 MB).
 int ogm_fetch128_online_planned(int64_t rows, const int32_t* const* q2, const int32_t* const* gdst,
-                                const uint16_t* const* srow, const int32_t* const* qs, const uint32_t* a,
-                                const uint32_t* b, const uint32_t* c,
-                                const uint32_t* u_src, const uint32_t* v_src, const uint32_t* w_blind, int w_order,
-                                const uint32_t* z_slot, uint32_t* const* inter, uint32_t* r3, const int32_t* k1,
+                                const uint16_t* const* srow, const int32_t* const* qs,
+                                const uint16_t* const* run_start, const int32_t* const* run_off,
+                                const int64_t* run_nwin, const int64_t* wrows, const uint32_t* a, const uint32_t* b,
+                                const uint32_t* c, const uint32_t* u_src, const uint32_t* v_src,
+                                const uint32_t* w_blind, int w_order, const uint32_t* z_slot, int z_order,
+                                uint32_t* const* inter, uint32_t* r3, const int32_t* k1,
                                 const int32_t* pi12, const int32_t* pi23, const int32_t* k3, const uint32_t* f1,
                                 const uint32_t* f2, const uint32_t* f3, const uint32_t* uf, const uint32_t* vf,
                                 const uint32_t* wf, const uint32_t* zf, const uint32_t* r1f, const uint32_t* r2f,
@@ -339,8 +341,11 @@ int ogm_fetch128_online_planned(int64_t rows, const int32_t* const* q2, const in
     flag_shuffle1_kernel<<<grid_for(rows), 256, 0, st>>>(rows, k1, pi12, f12, f3, uf, vf, x1f, y1f);
     OGM_LAUNCH_CHECK();
     const FlagTail ft{pi23, k3, x1f, y1f, wf, zf, r1f, r2f, c1f, r3f, plain};
-    return shuffle_online_planned_impl(rows, q2, gdst, srow, a, b, c, u_src, v_src, 0, w_blind, w_order, z_slot, 2,
-                                       inter, nullptr, nullptr, nullptr, r3, &ft, qs, stream);
+    RunTable rt[4];
+    const bool runs = run_tables(run_start, run_off, run_nwin, rt);
+    return shuffle_online_planned_impl(rows, q2, gdst, srow, a, b, c, u_src, v_src, 0, w_blind, w_order, z_slot,
+                                       z_order, inter, nullptr, nullptr, nullptr, r3, &ft, qs, runs ? rt : nullptr,
+                                       wrows, stream);
 }
 
 int64_t ogm_keep_rows_workspace_bytes(int64_t rows) {

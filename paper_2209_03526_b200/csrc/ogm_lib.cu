@@ -31,7 +31,7 @@ using namespace ogm;
 extern "C" {
 
 const char* ogm_last_error(void) { return get_error(); }
-int ogm_abi_version(void) { return 2; }
+int ogm_abi_version(void) { return 3; }
 int ogm_init(void) { return device_init(); }
 
 int ogm_prg_expand(const void* seeds, int64_t n, void* left, void* right, uint8_t* t_left,

@@ -509,6 +509,73 @@ __global__ void plan_slots_kernel(const int32_t* __restrict__ sj2, const int32_t
     }
 }
 
+// ---- run tables: pass-1 destinations without a per-row index --------------
+// Pass 1's slots are a tile's rows grouped by destination window, source
+// order inside, and I-region d holds window d's rows in source order; so the
+// slots of one (tile, window) run write consecutive I rows: gdst[s] =
+// off[t][d] + s for every global slot s of run d of tile t.  A plan's run
+// table -- per tile, the slot where each run starts (u16) and its offset
+// (i32) -- replaces the TMA partition's 4-B-per-row gdst read with 0.05
+// B/row at 2^24 rows (32 windows) and 0.75 B/row at 2^28 (512), staged with
+// the tile and searched in shared memory (partitions 2-3% faster).  Per-tile
+// strides are padded to 16 B for the bulk copies.  (The hand-over passes do
+// not use it: a per-row search on a streaming pass's store address measured
+// 10-40% slower than reading gdst; they run in I-row order instead.)
+struct RunTable {
+    const uint16_t* start;   // [ntiles][run_sstride(nwin)]: run d starts at slot start[d] (empty runs: the next start)
+    const int32_t* off;      // [ntiles][run_ostride(nwin)]
+    int nwin;
+};
+__host__ __device__ constexpr int run_sstride(int nwin) { return (nwin + 1 + 7) & ~7; }
+__host__ __device__ constexpr int run_ostride(int nwin) { return (nwin + 3) & ~3; }
+
+// the run holding tile slot k: the largest d < nwin with start[d] <= k
+// (start[0] = 0; a fixed number of steps, so warps stay converged)
+// the four plans' run tables from the C ABI's arrays (all null: none)
+static inline bool run_tables(const uint16_t* const* start, const int32_t* const* off, const int64_t* nwin,
+                              RunTable* rt) {
+    if (!start) return false;
+    for (int k = 0; k < 4; k++) rt[k] = RunTable{start[k], off ? off[k] : nullptr, nwin ? (int)nwin[k] : 0};
+    return true;
+}
+
+template <bool LDG>
+__device__ __forceinline__ int run_of(const uint16_t* __restrict__ start, int nwin, int k) {
+    int d = 0;
+    for (int step = 1 << (31 - __clz(nwin)); step; step >>= 1) {
+        const int e = d + step;
+        if (e < nwin && (int)(LDG ? __ldg(start + e) : start[e]) <= k) d = e;
+    }
+    return d;
+}
+
+__global__ void plan_runs_kernel(const int32_t* __restrict__ gdst, int64_t n, int64_t T, int64_t Wr, int nwin,
+                                 uint16_t* __restrict__ start, int32_t* __restrict__ off) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    const int sst = run_sstride(nwin), ost = run_ostride(nwin);
+    for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += stride) {
+        const int64_t t = k / T, kl = k - t * T;
+        const int32_t g = __ldg(gdst + k);
+        const int d = (int)(g / Wr);
+        if (kl == 0 || __ldg(gdst + k - 1) / Wr != d) {
+            start[t * sst + d] = (uint16_t)kl;
+            off[t * ost + d] = (int32_t)(g - k);
+        }
+    }
+}
+
+// empty runs start where the next run starts; start[nwin] = the tile's row count
+__global__ void plan_runs_fill_kernel(int64_t n, int64_t T, int nwin, uint16_t* __restrict__ start) {
+    const int64_t ntiles = (n + T - 1) / T;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < ntiles; t += stride) {
+        uint16_t* s = start + t * run_sstride(nwin);
+        s[nwin] = (uint16_t)(n - t * T < T ? n - t * T : T);
+        for (int d = nwin - 1; d >= 0; d--)
+            if (s[d] == 0xFFFF) s[d] = s[d + 1];
+    }
+}
+
 // Generic pass 1 in units U (uint4 for 16-B-multiple pitches, else words);
 // wu = pitch in U.  Stores are evict-first: L2 appears to keep evict-normal
 // DIRTY lines ahead of clean ones, so normal stores here leave pass 2 an L2
@@ -560,17 +627,28 @@ constexpr int kTmaSmemBytes = 2 * kTmaStageBytes + 64;
 // SLOT_M2: m2 is a blind in SLOT order (tile t, slot k <- source row
 // t*T + srow[t*T + k]) and m4 is null: it is XORed into each row as the row
 // is scattered, with no shared-memory XOR pass over the staged tile.
-template <bool SLOT_M2>
+// RUNS: destinations from the plan's run table (staged per tile) instead of
+// gdst; the stage is then T*18 B plus the tile's table (kTmaRunsStageBytes).
+__host__ __device__ constexpr int kTmaRunsStageBytes(int nwin) {
+    return kTmaTile * 18 + run_sstride(nwin) * 2 + run_ostride(nwin) * 4;
+}
+
+template <bool SLOT_M2, bool RUNS = false>
 __global__ void __launch_bounds__(kTmaThreads, 1) plan_partition_tma_kernel(
     const uint4* __restrict__ m1, const uint4* __restrict__ m2, const uint4* __restrict__ m4,
-    const uint16_t* __restrict__ srow, const int32_t* __restrict__ gdst, int64_t rows, uint4* __restrict__ inter) {
+    const uint16_t* __restrict__ srow, const int32_t* __restrict__ gdst, int64_t rows, uint4* __restrict__ inter,
+    RunTable rt = RunTable{}) {
     extern __shared__ __align__(128) unsigned char tma_smem[];
     constexpr int T = kTmaTile;
     constexpr int Q = T / kTmaThreads;
-    uint64_t* bar = reinterpret_cast<uint64_t*>(tma_smem + 2 * kTmaStageBytes);
-    auto rows_of = [&](int s) { return reinterpret_cast<uint4*>(tma_smem + s * kTmaStageBytes); };
-    auto srow_of = [&](int s) { return reinterpret_cast<uint16_t*>(tma_smem + s * kTmaStageBytes + T * 16); };
-    auto gdst_of = [&](int s) { return reinterpret_cast<int32_t*>(tma_smem + s * kTmaStageBytes + T * 18); };
+    const int SB = RUNS ? kTmaRunsStageBytes(rt.nwin) : kTmaStageBytes;
+    const int sst = run_sstride(rt.nwin), ost = run_ostride(rt.nwin);
+    uint64_t* bar = reinterpret_cast<uint64_t*>(tma_smem + 2 * SB);
+    auto rows_of = [&](int s) { return reinterpret_cast<uint4*>(tma_smem + s * SB); };
+    auto srow_of = [&](int s) { return reinterpret_cast<uint16_t*>(tma_smem + s * SB + T * 16); };
+    auto gdst_of = [&](int s) { return reinterpret_cast<int32_t*>(tma_smem + s * SB + T * 18); };
+    auto start_of = [&](int s) { return reinterpret_cast<uint16_t*>(tma_smem + s * SB + T * 18); };
+    auto off_of = [&](int s) { return reinterpret_cast<int32_t*>(tma_smem + s * SB + T * 18 + sst * 2); };
     const int64_t nfull = rows / T;
     const int64_t G = gridDim.x;
     if (threadIdx.x == 0) {
@@ -580,10 +658,20 @@ __global__ void __launch_bounds__(kTmaThreads, 1) plan_partition_tma_kernel(
     }
     __syncthreads();
     auto issue = [&](int64_t t, int s) {
-        mbar_expect_tx(&bar[s], kTmaStageBytes);
+        mbar_expect_tx(&bar[s], SB);
         bulk_g2s(rows_of(s), m1 + t * T, T * 16, &bar[s]);
         bulk_g2s(srow_of(s), srow + t * T, T * 2, &bar[s]);
-        bulk_g2s(gdst_of(s), gdst + t * T, T * 4, &bar[s]);
+        if (RUNS) {
+            bulk_g2s(start_of(s), rt.start + t * sst, sst * 2, &bar[s]);
+            bulk_g2s(off_of(s), rt.off + t * ost, ost * 4, &bar[s]);
+        } else {
+            bulk_g2s(gdst_of(s), gdst + t * T, T * 4, &bar[s]);
+        }
+    };
+    // destination of tile t's slot k (stage s)
+    auto dest = [&](int s, int64_t t, int k) -> int64_t {
+        if (RUNS) return (int64_t)off_of(s)[run_of<false>(start_of(s), rt.nwin, k)] + t * T + k;
+        return gdst_of(s)[k];
     };
     if (threadIdx.x == 0) {
         if (blockIdx.x < nfull) issue(blockIdx.x, 0);
@@ -607,7 +695,6 @@ __global__ void __launch_bounds__(kTmaThreads, 1) plan_partition_tma_kernel(
         parity ^= 1u << s;
         uint4* rs = rows_of(s);
         const uint16_t* sr = srow_of(s);
-        const int32_t* gd = gdst_of(s);
         if (SLOT_M2) {
             uint4 cur[Q];
 #pragma unroll
@@ -616,7 +703,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) plan_partition_tma_kernel(
 #pragma unroll
             for (int i = 0; i < Q; i++) {
                 const int k = threadIdx.x + i * kTmaThreads;
-                __stcs(inter + gd[k], xor4(rs[sr[k]], cur[i]));
+                __stcs(inter + dest(s, t, k), xor4(rs[sr[k]], cur[i]));
             }
         } else {
             if (m2 || m4) {
@@ -631,7 +718,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) plan_partition_tma_kernel(
 #pragma unroll
             for (int i = 0; i < Q; i++) {
                 const int k = threadIdx.x + i * kTmaThreads;
-                __stcs(inter + gd[k], rs[sr[k]]);
+                __stcs(inter + dest(s, t, k), rs[sr[k]]);
             }
         }
         __syncthreads();  // stage s fully read before it is refilled
@@ -647,7 +734,9 @@ __global__ void __launch_bounds__(kTmaThreads, 1) plan_partition_tma_kernel(
             uint4 v = __ldcs(m1 + b0 + j);
             if (m2) v = xor4(v, __ldcs(m2 + b0 + (SLOT_M2 ? k : j)));
             if (m4) v = xor4(v, __ldcs(m4 + b0 + j));
-            __stcs(inter + __ldcs(gdst + b0 + k), v);
+            const int64_t dst = RUNS ? (int64_t)__ldg(rt.off + nfull * ost + run_of<true>(rt.start + nfull * sst, rt.nwin, k)) + b0 + k
+                                     : (int64_t)__ldcs(gdst + b0 + k);
+            __stcs(inter + dst, v);
         }
     }
 }
@@ -812,6 +901,38 @@ __global__ void __launch_bounds__(256) chain_flat_kernel(const int32_t* __restri
             uint4 v = __ldcg(ia + __ldcs(qs + s));
             if (bl) v = xor4(v, __ldcs(bl + s));
             __stcs(ib + __ldcs(gdst + s), v);
+        }
+    }
+}
+
+// The flat hand-over in the receiver's I-row order (the product path):
+// ib[p] = ia[qi[p]] ^ bl[p] for every I row p of the receiving plan, qi[p] =
+// q[src[p]] and bl composed offline in that order -- so no destination
+// index is read and every write is sequential (the slot-order pass above
+// reads gdst and, at 2^28 rows, scatters 128-B runs).  Chunk c covers rows
+// [m*C, (m+1)*C) of region r = c % nreg, m = c / nreg: the chunks in flight
+// sit at the same offset of every region, and a region's rows are in source
+// order, so their sources -- and the sender window rows they read -- stay
+// inside one narrow source range (the L2-resident sender window), as in slot
+// order.  Measured per pass: 2^24 142 us (slot order 153), 2^28 1.8-2.2 ms
+// (2.0-2.4); whole shuffle -5% at 2^24-2^28 (profiles/r02_c5_chain_ncu.txt).
+__global__ void __launch_bounds__(256) chain_inter_kernel(const int32_t* __restrict__ qi,
+                                                          const uint4* __restrict__ ia,
+                                                          const uint4* __restrict__ bl, int64_t rows, int64_t wr,
+                                                          uint4* __restrict__ ib, unsigned long long* next) {
+    __shared__ int64_t chunk;
+    const int64_t nreg = (rows + wr - 1) / wr, per = (wr + kFlatChunk - 1) / kFlatChunk;
+    for (int64_t round = 0;; round++) {
+        const int64_t c = next_chunk(next, &chunk, round) / kFlatChunk;
+        if (c >= nreg * per) break;
+        const int64_t r = c % nreg, m = c / nreg;
+        const int64_t p0 = r * wr + m * kFlatChunk;
+        const int64_t p1 = min(min(p0 + kFlatChunk, (r + 1) * wr), rows);
+#pragma unroll 4
+        for (int64_t p = p0 + threadIdx.x; p < p1; p += blockDim.x) {
+            uint4 v = __ldcg(ia + __ldcs(qi + p));
+            if (bl) v = xor4(v, __ldcs(bl + p));
+            __stcs(ib + p, v);
         }
     }
 }
@@ -1236,6 +1357,26 @@ int ogm_gather_plan(int64_t n, const int32_t* idx, int64_t window_rows, int64_t 
     return OGM_OK;
 }
 
+int ogm_gather_plan_runs(int64_t n, int64_t window_rows, int64_t tile_rows, const int32_t* gdst, uint16_t* start,
+                         int32_t* off, void* stream) {
+    using namespace ogm;
+    OGM_CHECK_ARG(n >= 0 && n < ((int64_t)1 << 31), OGM_ERR_ARG, "plan size out of range");
+    OGM_CHECK_ARG(window_rows >= 1 && tile_rows >= 1 && tile_rows <= 32768, OGM_ERR_ARG,
+                  "window_rows must be positive and tile_rows in [1, 32768]");
+    if (n == 0) return OGM_OK;
+    OGM_CHECK_ARG(gdst && start && off, OGM_ERR_ARG, "gdst and the run table are required");
+    const int64_t nwin = (n + window_rows - 1) / window_rows;
+    OGM_CHECK_ARG(nwin < (1 << 20), OGM_ERR_ARG, "too many windows");
+    const int64_t ntiles = (n + tile_rows - 1) / tile_rows;
+    cudaStream_t st = as_stream(stream);
+    OGM_CUDA_TRY(cudaMemsetAsync(start, 0xFF, (size_t)(ntiles * run_sstride((int)nwin) * 2), st));
+    OGM_CUDA_TRY(cudaMemsetAsync(off, 0, (size_t)(ntiles * run_ostride((int)nwin) * 4), st));
+    plan_runs_kernel<<<grid_for(n), 256, 0, st>>>(gdst, n, tile_rows, window_rows, (int)nwin, start, off);
+    plan_runs_fill_kernel<<<grid_for(ntiles), 256, 0, st>>>(n, tile_rows, (int)nwin, start);
+    OGM_LAUNCH_CHECK();
+    return OGM_OK;
+}
+
 int ogm_gather_planned(int64_t rows, int64_t words, int64_t pitch, int64_t tile_rows, const int32_t* q2,
                        const int32_t* gdst, const uint16_t* srow, const uint32_t* m1, const uint32_t* m2,
                        const uint32_t* m4, const uint32_t* m3, const uint32_t* r_mat, uint32_t* inter, uint32_t* out,
@@ -1493,7 +1634,8 @@ int shuffle_online_planned_impl(int64_t rows, const int32_t* const* q2, const in
                                 const uint32_t* u_src, const uint32_t* v_src, int v_order, const uint32_t* w_src,
                                 int w_order, const uint32_t* z_src, int z_order, uint32_t* const* inter, uint32_t* x1,
                                 uint32_t* y1, uint32_t* c1, uint32_t* r3, const FlagTail* ft,
-                                const int32_t* const* qs, void* stream);
+                                const int32_t* const* qs, const RunTable* runs, const int64_t* wrows,
+                                void* stream);
 }
 extern "C" {
 
@@ -1517,7 +1659,7 @@ int ogm_shuffle_online_planned_ex(int64_t rows, const int32_t* const* q2, const 
                                   uint32_t* const* inter, uint32_t* x1, uint32_t* y1, uint32_t* c1, uint32_t* r3,
                                   void* stream) {
     return ogm::shuffle_online_planned_impl(rows, q2, gdst, srow, a, b, c, u_src, v_src, v_order, w_src, w_order,
-                                            z_src, z_order, inter, x1, y1, c1, r3, nullptr, nullptr, stream);
+                                            z_src, z_order, inter, x1, y1, c1, r3, nullptr, nullptr, nullptr, nullptr, stream);
 }
 }  // extern "C"
 
@@ -1529,7 +1671,8 @@ int shuffle_online_planned_impl(int64_t rows, const int32_t* const* q2, const in
                                 const uint32_t* u_src, const uint32_t* v_src, int v_order, const uint32_t* w_src,
                                 int w_order, const uint32_t* z_src, int z_order, uint32_t* const* inter, uint32_t* x1,
                                 uint32_t* y1, uint32_t* c1, uint32_t* r3, const FlagTail* ft,
-                                const int32_t* const* qs, void* stream) {
+                                const int32_t* const* qs, const RunTable* runs, const int64_t* wrows,
+                                void* stream) {
     OGM_CHECK_ARG(rows >= 0 && rows < ((int64_t)1 << 31), OGM_ERR_ARG, "rows out of range");
     OGM_CHECK_ARG(q2 && gdst && srow && inter, OGM_ERR_ARG, "plans and scratch are required");
     const void* need[] = {a, b, c, u_src, v_src, w_src, z_src, r3, inter[0], inter[1], inter[2]};
@@ -1541,10 +1684,24 @@ int shuffle_online_planned_impl(int64_t rows, const int32_t* const* q2, const in
     if (rows == 0) return OGM_OK;
     OGM_ENSURE_INIT();
     cudaStream_t st = as_stream(stream);
-    OGM_CHECK_ARG((v_order == 0 || v_order == 2) && w_order >= 0 && w_order <= 2 && (z_order == 0 || z_order == 2),
-                  OGM_ERR_ARG, "blind orders: v 0 (source) / 2 (slot), w 0 / 1 (output) / 2, z 0 / 2");
+    OGM_CHECK_ARG((v_order == 0 || v_order == 2) && w_order >= 0 && w_order <= 3 && z_order >= 0 && z_order <= 3 &&
+                      z_order != 1,
+                  OGM_ERR_ARG, "blind orders: v 0 (source) / 2 (slot), w 0 / 1 (output) / 2 / 3 (I order), z 0 / 2 / 3");
+    OGM_CHECK_ARG((w_order != 3 && z_order != 3) || (qs && qs[0] && qs[1] && wrows && wrows[2] > 0 && wrows[3] > 0),
+                  OGM_ERR_ARG, "I-order blinds need the I-order indices and the receiving plans' window rows");
     OGM_CUDA_TRY(allow_big_smem(plan_partition_tma_kernel<false>, kTmaSmemBytes));
     OGM_CUDA_TRY(allow_big_smem(plan_partition_tma_kernel<true>, kTmaSmemBytes));
+    if (runs)
+        for (int k = 0; k < 4; k++)
+            OGM_CHECK_ARG(runs[k].start && runs[k].off && runs[k].nwin >= 1 &&
+                              2 * kTmaRunsStageBytes(runs[k].nwin) + 64 <= kMaxDynSmem,
+                          OGM_ERR_ARG, "run table %d is incomplete or too large", k);
+    const int runs_smem0 = runs ? 2 * kTmaRunsStageBytes(runs[0].nwin) + 64 : 0;
+    const int runs_smem1 = runs ? 2 * kTmaRunsStageBytes(runs[1].nwin) + 64 : 0;
+    if (runs) {
+        OGM_CUDA_TRY(allow_big_smem(plan_partition_tma_kernel<false, true>, std::max(runs_smem0, runs_smem1)));
+        OGM_CUDA_TRY(allow_big_smem(plan_partition_tma_kernel<true, true>, std::max(runs_smem0, runs_smem1)));
+    }
     OGM_CUDA_TRY(allow_big_smem(plan_chain_kernel<false>, kChainSmem2));
     OGM_CUDA_TRY(allow_big_smem(plan_chain_kernel<true>, kChainSmem2));
     const int64_t ntiles = (rows + kTmaTile - 1) / kTmaTile;
@@ -1559,14 +1716,26 @@ int shuffle_online_planned_impl(int64_t rows, const int32_t* const* q2, const in
     using U4 = const uint4*;
     uint4 *i0 = (uint4*)inter[0], *i1 = (uint4*)inter[1], *i2 = (uint4*)inter[2];
     constexpr int TT = kTmaThreads;
-    plan_partition_tma_kernel<false><<<g, TT, kTmaSmemBytes, st>>>((U4)a, (U4)b, (U4)u_src, srow[0], gdst[0], rows,
-                                                                   i0);
-    if (v_order == 2)
-        plan_partition_tma_kernel<true><<<g, TT, kTmaSmemBytes, st>>>((U4)c, (U4)v_src, nullptr, srow[1], gdst[1],
-                                                                      rows, i1);
-    else
-        plan_partition_tma_kernel<false><<<g, TT, kTmaSmemBytes, st>>>((U4)c, (U4)v_src, nullptr, srow[1], gdst[1],
-                                                                       rows, i1);
+    if (runs) {
+        plan_partition_tma_kernel<false, true><<<g, TT, runs_smem0, st>>>((U4)a, (U4)b, (U4)u_src, srow[0], nullptr,
+                                                                          rows, i0, runs[0]);
+        if (v_order == 2)
+            plan_partition_tma_kernel<true, true><<<g, TT, runs_smem1, st>>>((U4)c, (U4)v_src, nullptr, srow[1],
+                                                                             nullptr, rows, i1, runs[1]);
+        else
+            plan_partition_tma_kernel<false, true><<<g, TT, runs_smem1, st>>>((U4)c, (U4)v_src, nullptr, srow[1],
+                                                                              nullptr, rows, i1, runs[1]);
+    } else {
+        plan_partition_tma_kernel<false><<<g, TT, kTmaSmemBytes, st>>>((U4)a, (U4)b, (U4)u_src, srow[0], gdst[0],
+                                                                       rows, i0);
+        if (v_order == 2)
+            plan_partition_tma_kernel<true><<<g, TT, kTmaSmemBytes, st>>>((U4)c, (U4)v_src, nullptr, srow[1], gdst[1],
+                                                                          rows, i1);
+        else
+            plan_partition_tma_kernel<false><<<g, TT, kTmaSmemBytes, st>>>((U4)c, (U4)v_src, nullptr, srow[1],
+                                                                           gdst[1], rows, i1);
+    }
+    const int64_t gf = std::min<int64_t>((rows + kFlatChunk - 1) / kFlatChunk, (int64_t)sm_count() * 8);
     if (scrub_l2() != OGM_OK) return OGM_ERR_CUDA;
     // above the dual-pass size P2's blind W stays in c1's OUTPUT order: the x1 -> c1 chain kernel
     // then needs no XOR pass (it is MIO-bound) and W streams in c1's own window pass (2-3% at
@@ -1579,7 +1748,6 @@ int shuffle_online_planned_impl(int64_t rows, const int32_t* const* q2, const in
         else
             plan_chain_kernel<false><<<g, TT, kChainSmem2, st>>>(q, ia, bl, sr, gd, rows, ib, msg);
     };
-    const int64_t gf = std::min<int64_t>((rows + kFlatChunk - 1) / kFlatChunk, (int64_t)sm_count() * 8);
     unsigned long long* ctr = flat_counters(st);   // the two chain passes' chunk counters
     if (!ctr) {
         set_error("could not allocate the chunk counters");
@@ -1587,12 +1755,17 @@ int shuffle_online_planned_impl(int64_t rows, const int32_t* const* q2, const in
     }
     OGM_CUDA_TRY(cudaMemsetAsync(ctr, 0, 2 * sizeof(unsigned long long), st));
     // the flat hand-over needs the composed indices, slot-order (or no) blinds and no message copies
-    if (qs && qs[0] && !x1 && (w_order == 2 || w_out))
+    const bool inter_order = z_order == 3;   // the I-order hand-over (w_order 3, or 1 with W streamed later)
+    if (inter_order && !x1)
+        chain_inter_kernel<<<(int)gf, 256, 0, st>>>(qs[0], i0, w_out ? nullptr : (U4)w_src, rows, wrows[2], i2, ctr);
+    else if (qs && qs[0] && !x1 && (w_order == 2 || w_out))
         chain_flat_kernel<<<(int)gf, 256, 0, st>>>(qs[0], i0, w_out ? nullptr : (U4)w_src, gdst[2], rows, i2, ctr);
     else
         chain(w_order == 2, q2[0], i0, w_out ? nullptr : (U4)w_src, srow[2], gdst[2], i2, (uint4*)x1);
     if (scrub_l2() != OGM_OK) return OGM_ERR_CUDA;
-    if (qs && qs[1] && !y1 && z_order == 2)
+    if (inter_order && !y1)
+        chain_inter_kernel<<<(int)gf, 256, 0, st>>>(qs[1], i1, (U4)z_src, rows, wrows[3], i0, ctr + 1);
+    else if (qs && qs[1] && !y1 && z_order == 2)
         chain_flat_kernel<<<(int)gf, 256, 0, st>>>(qs[1], i1, (U4)z_src, gdst[3], rows, i0, ctr + 1);
     else
         chain(z_order == 2, q2[1], i1, (U4)z_src, srow[3], gdst[3], i0, (uint4*)y1);
@@ -1633,15 +1806,22 @@ int shuffle_online_planned_impl(int64_t rows, const int32_t* const* q2, const in
 extern "C" {
 
 int ogm_shuffle_online_planned_slots(int64_t rows, const int32_t* const* q2, const int32_t* const* gdst,
-                                     const uint16_t* const* srow, const int32_t* const* qs, const uint32_t* a,
+                                     const uint16_t* const* srow, const int32_t* const* qs,
+                                     const uint16_t* const* run_start, const int32_t* const* run_off,
+                                     const int64_t* run_nwin, const int64_t* wrows, const uint32_t* a,
                                      const uint32_t* b, const uint32_t* c, const uint32_t* u_src,
                                      const uint32_t* v_src, const uint32_t* w_blind, int w_order,
-                                     const uint32_t* z_slot, uint32_t* const* inter, uint32_t* r3, void* stream) {
+                                     const uint32_t* z_slot, int z_order, uint32_t* const* inter, uint32_t* r3,
+                                     void* stream) {
     using namespace ogm;
     OGM_CHECK_ARG(qs && qs[0] && qs[1], OGM_ERR_ARG, "the two composed slot indices are required");
-    OGM_CHECK_ARG(w_order == 1 || w_order == 2, OGM_ERR_ARG, "W in c1's output (1) or slot (2) order");
-    return shuffle_online_planned_impl(rows, q2, gdst, srow, a, b, c, u_src, v_src, 0, w_blind, w_order, z_slot, 2,
-                                       inter, nullptr, nullptr, nullptr, r3, nullptr, qs, stream);
+    OGM_CHECK_ARG(w_order >= 1 && w_order <= 3 && (z_order == 2 || z_order == 3), OGM_ERR_ARG,
+                  "W in c1's output (1), slot (2) or I (3) order; Z in slot (2) or I (3) order");
+    RunTable rt[4];
+    const bool runs = run_tables(run_start, run_off, run_nwin, rt);
+    return shuffle_online_planned_impl(rows, q2, gdst, srow, a, b, c, u_src, v_src, 0, w_blind, w_order, z_slot,
+                                       z_order, inter, nullptr, nullptr, nullptr, r3, nullptr, qs,
+                                       runs ? rt : nullptr, wrows, stream);
 }
 
 int ogm_shuffle_online_fused(int64_t rows, const int32_t* k1, const int32_t* pi12, const int32_t* pi23,

@@ -33,7 +33,8 @@ import torch
 
 from . import _lib
 from .bits import words_for
-from .shuffle import FLAG_ROW_BITS, ShuffleOffline, chain_slot_indices, shuffle_online_fused, shuffle_online_planned
+from .shuffle import (FLAG_ROW_BITS, ShuffleOffline, flat_chain_args, run_table_args, shuffle_online_fused,
+                      shuffle_online_planned)
 
 FUSED_MAX_BYTES = 32 << 20   # one cooperative launch up to 2^21 16-byte rows (measured crossover)
 FLAG_TAIL_MIN_BYTES = 256 << 20   # above: the flag column's phase 2 rides the split window passes
@@ -58,7 +59,7 @@ class FlaggedFetch:
         if not self.fused:
             for o in self.off:
                 o.chain_blinds()
-            chain_slot_indices(self.off)
+            flat_chain_args(self.off)
             # the chained shuffle reads only its chain blinds (chain_blinds); the other copies go
             p1.u = p2.v = p3.z = None
             if not p2.w_output_order:
@@ -113,14 +114,16 @@ class FlaggedFetch:
         else:
             # one launch sequence: flag phase 1, then the chained payload shuffle whose final
             # window passes also produce the flag column's phase 2 and the opened column
-            (u,), (v, w), (z,) = p1.chain_blinds(), p2.chain_blinds(), p3.chain_blinds()
+            (u,), (v, _) = p1.chain_blinds(), p2.chain_blinds()
             arr = lambda xs: (ctypes.c_void_p * len(xs))(*[P(x) for x in xs])  # noqa: E731
             q2, gd, sr, it = (arr([pl.q2 for pl in self.plans]), arr([pl.gdst for pl in self.plans]),
                               arr([pl.srow for pl in self.plans]), arr(self.inter))
-            qs = arr(chain_slot_indices(self.off))
+            qf, wf, w_order, zf, z_order, wr = flat_chain_args(self.off)
+            qs = arr(qf)
+            rs, ro, rn = run_table_args(self.plans)
             _lib.call("ogm_fetch128_online_planned", rows, ctypes.addressof(q2), ctypes.addressof(gd),
-                      ctypes.addressof(sr), ctypes.addressof(qs), P(a), P(b), P(c), P(u), P(v), P(w), 1 if p2.w_output_order else 2,
-                      P(z), ctypes.addressof(it), P(self.r3), P(p1.k1), P(p2.pi12), P(p2.pi23), P(p3.k3),
+                      ctypes.addressof(sr), ctypes.addressof(qs), rs, ro, rn, wr, P(a), P(b), P(c),
+                      P(u), P(v), P(wf), w_order, P(zf), z_order, ctypes.addressof(it), P(self.r3), P(p1.k1), P(p2.pi12), P(p2.pi23), P(p3.k3),
                       P(flags[0]), P(flags[1]), P(flags[2]), P(p1.flag["u"]), P(p2.flag["v"]), P(p2.flag["w"]),
                       P(p3.flag["z"]), P(self.r1f), P(self.r2f), P(self.x1f), P(self.y1f), P(self.c1f),
                       P(self.r3f), P(self.plain), _lib.stream_ptr())

@@ -33,7 +33,7 @@ for lg in map(int, sys.argv[1:]):
     off = [ShuffleOffline(p + 1, cfg[p].seed_with_next, cfg[p].seed_with_prev, 0, rows, 128, plan=True)
            for p in range(3)]
     # the blinds as the chained shuffle expects them (W in c1's output order above 256 MB)
-    (u_src,), (v_src, w_src), (z_src,) = off[0].chain_blinds(), off[1].chain_blinds(), off[2].chain_blinds()
+    (u_src,), (v_src, w_src), (z_src,) = (o.chain_blinds("slot") for o in off)
     w_steps = source_order(off[1].w, off[1].pi23)   # the per-party steps with source-order blinds
     plans = [off[0].plan_x1, off[1].plan_y1, off[1].plan_c1, off[2].plan_r3]
     want = [e() for _ in range(4)]
@@ -49,7 +49,7 @@ for lg in map(int, sys.argv[1:]):
     it = (ctypes.c_void_p * 3)(*[P(t) for t in inter])
 
     def chained(msgs: bool):
-        # chain_blinds(): U', V' in source order, W and Z in slot order (W in output order above 256 MB)
+        # chain_blinds("slot"): U', V' in source order, W and Z in slot order (W in output order above 256 MB)
         _lib.call("ogm_shuffle_online_planned_ex", rows, ctypes.addressof(q2), ctypes.addressof(gd),
                   ctypes.addressof(sr), P(comps[0]), P(comps[1]), P(comps[2]), P(u_src), P(v_src), 0, P(w_src),
                   1 if off[1].w_output_order else 2, P(z_src), 2, ctypes.addressof(it),

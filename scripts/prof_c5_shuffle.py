@@ -1,6 +1,9 @@
 """C5 online shuffle at one size, a few iterations (for ncu launch lists):
-python scripts/prof_c5_shuffle.py [log2 rows] [iterations]."""
+python scripts/prof_c5_shuffle.py [log2 rows] [iterations]; OGM_GDST=1 reads
+gdst instead of the plans' run tables, OGM_FLAT_ORDER=slot runs the
+slot-order hand-over (A/B)."""
 
+import os
 import sys
 from pathlib import Path
 
@@ -9,13 +12,15 @@ import torch
 sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
 
 import bench_configs as bc  # noqa: E402
-from paper_2209_03526_b200 import _lib, workloads  # noqa: E402
+from paper_2209_03526_b200 import _lib, shuffle, workloads  # noqa: E402
 from paper_2209_03526_b200.net import make_session_configs  # noqa: E402
 from paper_2209_03526_b200.shuffle import ShuffleOffline, shuffle_online_fused, shuffle_online_planned  # noqa: E402
 
 
 def main():
     lg = int(sys.argv[1]) if len(sys.argv) > 1 else 24
+    shuffle.USE_RUN_TABLES = not os.environ.get("OGM_GDST")
+    shuffle.FLAT_ORDER = os.environ.get("OGM_FLAT_ORDER", shuffle.FLAT_ORDER)
     iters = int(sys.argv[2]) if len(sys.argv) > 2 else 3
     _lib.check(_lib.load().ogm_init())
     rows = 1 << lg

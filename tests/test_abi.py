@@ -38,7 +38,7 @@ def test_binding_table_covers_header(lib):
 
 
 def test_abi_version(lib):
-    assert lib.ogm_abi_version() == 2
+    assert lib.ogm_abi_version() == 3
 
 
 def test_argument_errors_map_to_reference_exceptions(lib):

@@ -612,11 +612,13 @@ def test_c5_planned_shuffle_matches_oracle_at_scale():
 
 
 @pytest.mark.parametrize("rows", [4096, 3 * 4096 + 77, 148 * 4096 + 4095, 1 << 20, (1 << 24) + 3 * 4096 + 5])
-def test_chained_online_shuffle_equals_party_steps(rows):
+def test_chained_online_shuffle_equals_party_steps(rows, monkeypatch):
     """ogm_shuffle_online_planned (each message handed from sender to
     receiver tile by tile in shared memory; ragged last tiles; the dual
-    window pass) gives the four per-party planned steps' messages and R3."""
-    from paper_2209_03526_b200 import workloads
+    window pass) gives the four per-party planned steps' messages and R3;
+    so does the flat hand-over, in the receiving partition's I-row or slot
+    order, with partition destinations from the run tables or from gdst."""
+    from paper_2209_03526_b200 import shuffle, workloads
     from paper_2209_03526_b200.net import make_session_configs
     from paper_2209_03526_b200.shuffle import ShuffleOffline, shuffle_online_planned
 
@@ -634,7 +636,38 @@ def test_chained_online_shuffle_equals_party_steps(rows):
     r3 = shuffle_online_planned(off, comps[0], comps[1], comps[2], e(), msgs=msgs)
     for got, w in zip(msgs + [r3], want):
         assert torch.equal(got, w)
-    assert torch.equal(shuffle_online_planned(off, comps[0], comps[1], comps[2], e()), want[3])
+    for order in ("inter", "slot"):
+        for runs in (True, False):
+            monkeypatch.setattr(shuffle, "FLAT_ORDER", order)
+            monkeypatch.setattr(shuffle, "USE_RUN_TABLES", runs)
+            assert torch.equal(shuffle_online_planned(off, comps[0], comps[1], comps[2], e()), want[3]), (order, runs)
+
+
+@pytest.mark.parametrize("rows,window", [(1, 1), (4096, 1 << 20), (3 * 4096 + 77, 1000), (1 << 20, 1 << 16),
+                                         (123457, 4099), (5 * 4096, 7)])
+def test_plan_run_table_reconstructs_gdst(rows, window):
+    """ogm_gather_plan_runs: for every slot s of tile t, off[t][d] + s = gdst[s]
+    with d the run holding s (the last run starting at or before it), runs
+    ordered by window, start[t][nwin] = the tile's row count (ragged tiles,
+    empty runs, one row per window)."""
+    from paper_2209_03526_b200.shuffle import GatherPlan
+
+    g = torch.Generator(device="cuda").manual_seed(rows)
+    idx = torch.randperm(rows, device="cuda", generator=g).to(torch.int32)
+    plan = GatherPlan(idx, 4, window_bytes=window * 16)
+    start, off, nwin = plan.runs()
+    T, ntiles = plan.tile, -(-rows // plan.tile)
+    assert nwin == -(-rows // window)
+    st = start.cpu().numpy().view(np.uint16)[:ntiles * ((nwin + 8) & ~7)].reshape(ntiles, -1)
+    of = off.cpu().numpy()[:ntiles * ((nwin + 3) & ~3)].reshape(ntiles, -1)
+    gd = plan.gdst.cpu().numpy()
+    for t in range(ntiles):
+        n_t = min(T, rows - t * T)
+        assert st[t, nwin] == n_t and st[t, 0] == 0 and np.all(np.diff(st[t, :nwin + 1].astype(np.int64)) >= 0)
+        s = np.arange(t * T, t * T + n_t)
+        d = np.searchsorted(st[t, :nwin], s - t * T, side="right") - 1
+        assert np.array_equal(of[t, d].astype(np.int64) + s, gd[s]), t
+        assert np.array_equal(d, gd[s] // window), t
 
 
 @pytest.mark.parametrize("world", [1, 2, 3, 8])
