@@ -296,26 +296,38 @@ int ogm_flag_shuffle_trio(int64_t rows, const int32_t* k1, const int32_t* pi12, 
                           const uint32_t* r1f, const uint32_t* r2f, uint32_t* x1f, uint32_t* y1f, uint32_t* c1f,
                           uint32_t* r3f, uint32_t* plain, void* stream);
 
+/* The flag column of the co-resident trio, each party's step composed with
+ * the next one's (as the payload's flat hand-over composes them: the message
+ * bits x1f / y1f exist only in flight), so two random bit reads per row
+ * instead of four:
+ *   c1f[i] = f12[kc[i]] ^ uwf[i],        kc = k1 o pi23 (kc[i] = k1[pi23[i]]),
+ *                                        uwf[i] = Uf[pi23[i]] ^ Wf[i]
+ *   r3f[i] = f3[kr[i]] ^ vzf[i] ^ c1f[i], kr = pi12 o k3, vzf[i] = Vf[k3[i]] ^ Zf[i]
+ *   plain  = R1f ^ R2f ^ r3f
+ * f12 = f1 ^ f2 (scratch, rows/32 words); c1f may be NULL.  The same columns
+ * as ogm_flag_shuffle_trio. */
+int ogm_flag_open_composed(int64_t rows, const int32_t* kc, const int32_t* kr, const uint32_t* f1,
+                           const uint32_t* f2, const uint32_t* f3, const uint32_t* uwf, const uint32_t* vzf,
+                           const uint32_t* r1f, const uint32_t* r2f, uint32_t* f12, uint32_t* c1f, uint32_t* r3f,
+                           uint32_t* plain, void* stream);
+
 /* The online phase of a flag-split fetch shuffle for >= 2^22 rows in one
- * call: flag phase 1 (x1f, y1f), then the chained planned payload shuffle
- * (as ogm_shuffle_online_planned_ex with V in source order and Z in slot
- * order) whose final window passes also compute c1f, r3f and the opened
- * column `plain` -- the flag column needs the rows in output order, which
- * those passes walk anyway.  qs and run_* as ogm_shuffle_online_planned_slots
- * (may be NULL).  Same results as ogm_shuffle_online_planned_ex +
- * ogm_flag_shuffle_trio. */
+ * call: f12 = f1 ^ f2, then the chained planned payload shuffle (as
+ * ogm_shuffle_online_planned_slots) whose final window passes also compute
+ * the composed flag column of ogm_flag_open_composed (c1f: scratch) and the
+ * opened column -- the flag column needs the rows in output order, which
+ * those passes walk anyway.  Same results as ogm_shuffle_online_planned_slots
+ * + ogm_flag_open_composed. */
 int ogm_fetch128_online_planned(int64_t rows, const int32_t* const* q2, const int32_t* const* gdst,
                                 const uint16_t* const* srow, const int32_t* const* qs,
                                 const uint16_t* const* run_start, const int32_t* const* run_off,
                                 const int64_t* run_nwin, const int64_t* wrows, const uint32_t* a, const uint32_t* b,
                                 const uint32_t* c, const uint32_t* u_src, const uint32_t* v_src,
                                 const uint32_t* w_blind, int w_order, const uint32_t* z_slot, int z_order,
-                                uint32_t* const* inter, uint32_t* r3, const int32_t* k1,
-                                const int32_t* pi12, const int32_t* pi23, const int32_t* k3, const uint32_t* f1,
-                                const uint32_t* f2, const uint32_t* f3, const uint32_t* uf, const uint32_t* vf,
-                                const uint32_t* wf, const uint32_t* zf, const uint32_t* r1f, const uint32_t* r2f,
-                                uint32_t* x1f, uint32_t* y1f, uint32_t* c1f, uint32_t* r3f, uint32_t* plain,
-                                void* stream);
+                                uint32_t* const* inter, uint32_t* r3, const int32_t* kc, const int32_t* kr,
+                                const uint32_t* f1, const uint32_t* f2, const uint32_t* f3, const uint32_t* uwf,
+                                const uint32_t* vzf, const uint32_t* r1f, const uint32_t* r2f, uint32_t* f12,
+                                uint32_t* c1f, uint32_t* r3f, uint32_t* plain, void* stream);
 
 /* ---- storage (src/storage.py) -------------------------------------------- */
 

@@ -310,37 +310,63 @@ int ogm_flag_shuffle_trio(int64_t rows, const int32_t* k1, const int32_t* pi12, 
     return OGM_OK;
 }
 
-// The whole online fetch shuffle of flag-split rows (>= 2^22 rows): flag
-// phase 1 (f1 ^ f2, then x1f / y1f), then the chained planned payload shuffle
-// whose final window passes carry flag phase 2 and the open (FlagTail): one
-// launch sequence, no separate phase-2 flag kernel.  Arguments as
-// ogm_shuffle_online_planned_slots (qs: the composed slot indices, may be
-// null for the staged hand-over; run_*: the plans' run tables, or null) and
-// ogm_flag_shuffle_trio; c1f is scratch when the passes are split (> 256 MB).
+// The flag column of the co-resident trio with each party's step composed
+// with the next one's, as the payload's flat hand-over composes them: the
+// message bits x1f / y1f exist only in flight (each read once, where the
+// receiver's step needs it), so the column costs two random bit reads per
+// row instead of four:
+//   c1f[i] = f12[kc[i]] ^ uwf[i],  kc = k1 o pi23, uwf[i] = Uf[pi23[i]] ^ Wf[i]
+//   r3f[i] = f3[kr[i]] ^ vzf[i] ^ c1f[i],  kr = pi12 o k3, vzf[i] = Vf[k3[i]] ^ Zf[i]
+// (offline compositions; phase 2's kernel computes exactly this given them).
+int ogm_flag_open_composed(int64_t rows, const int32_t* kc, const int32_t* kr, const uint32_t* f1,
+                           const uint32_t* f2, const uint32_t* f3, const uint32_t* uwf, const uint32_t* vzf,
+                           const uint32_t* r1f, const uint32_t* r2f, uint32_t* f12, uint32_t* c1f, uint32_t* r3f,
+                           uint32_t* plain, void* stream) {
+    using namespace ogm;
+    OGM_CHECK_ARG(rows >= 0 && rows < ((int64_t)1 << 31), OGM_ERR_ARG, "rows out of range");
+    if (rows == 0) return OGM_OK;
+    const void* need[] = {kc, kr, f1, f2, f3, uwf, vzf, f12, r3f};
+    for (const void* p : need)
+        OGM_CHECK_ARG(p, OGM_ERR_ARG, "composed indices, flag columns, blinds and f12/r3f scratch are required");
+    OGM_CHECK_ARG(!plain || (r1f && r2f), OGM_ERR_ARG, "the opened column needs R1f and R2f");
+    cudaStream_t st = as_stream(stream);
+    const int64_t nw = (rows + 31) / 32;
+    flag_xor2_kernel<<<grid_for(nw), 256, 0, st>>>(f1, f2, nw, f12);
+    flag_shuffle2_kernel<<<grid_for(rows), 256, 0, st>>>(rows, kc, kr, f12, f3, uwf, vzf, r1f, r2f, c1f, r3f, plain);
+    OGM_LAUNCH_CHECK();
+    return OGM_OK;
+}
+
+// The whole online fetch shuffle of flag-split rows (>= 2^22 rows) in one
+// call: f12 = f1 ^ f2, then the chained planned payload shuffle whose final
+// window passes also compute the flag column -- composed as in
+// ogm_flag_open_composed, so each pass makes one random bit read per row --
+// and the opened column (FlagTail; they walk the rows in output order
+// anyway).  Arguments as ogm_shuffle_online_planned_slots (qs: the composed
+// indices, may be null for the staged hand-over; run_*: the plans' run
+// tables, or null) and ogm_flag_open_composed; c1f is scratch when the
+// passes are split (> 256 MB).
 int ogm_fetch128_online_planned(int64_t rows, const int32_t* const* q2, const int32_t* const* gdst,
                                 const uint16_t* const* srow, const int32_t* const* qs,
                                 const uint16_t* const* run_start, const int32_t* const* run_off,
                                 const int64_t* run_nwin, const int64_t* wrows, const uint32_t* a, const uint32_t* b,
                                 const uint32_t* c, const uint32_t* u_src, const uint32_t* v_src,
                                 const uint32_t* w_blind, int w_order, const uint32_t* z_slot, int z_order,
-                                uint32_t* const* inter, uint32_t* r3, const int32_t* k1,
-                                const int32_t* pi12, const int32_t* pi23, const int32_t* k3, const uint32_t* f1,
-                                const uint32_t* f2, const uint32_t* f3, const uint32_t* uf, const uint32_t* vf,
-                                const uint32_t* wf, const uint32_t* zf, const uint32_t* r1f, const uint32_t* r2f,
-                                uint32_t* x1f, uint32_t* y1f, uint32_t* c1f, uint32_t* r3f, uint32_t* plain,
-                                void* stream) {
+                                uint32_t* const* inter, uint32_t* r3, const int32_t* kc, const int32_t* kr,
+                                const uint32_t* f1, const uint32_t* f2, const uint32_t* f3, const uint32_t* uwf,
+                                const uint32_t* vzf, const uint32_t* r1f, const uint32_t* r2f, uint32_t* f12,
+                                uint32_t* c1f, uint32_t* r3f, uint32_t* plain, void* stream) {
     using namespace ogm;
     OGM_CHECK_ARG(rows >= 0 && rows < ((int64_t)1 << 31), OGM_ERR_ARG, "rows out of range");
     if (rows == 0) return OGM_OK;
-    const void* need[] = {k1, pi12, pi23, k3, f1, f2, f3, uf, vf, wf, zf, r1f, r2f, x1f, y1f, c1f, r3f, plain};
-    for (const void* p : need) OGM_CHECK_ARG(p, OGM_ERR_ARG, "permutations, flag columns and scratch are required");
+    const void* need[] = {kc, kr, f1, f2, f3, uwf, vzf, r1f, r2f, f12, c1f, r3f, plain};
+    for (const void* p : need)
+        OGM_CHECK_ARG(p, OGM_ERR_ARG, "composed indices, flag columns, blinds and scratch are required");
     cudaStream_t st = as_stream(stream);
     const int64_t nw = (rows + 31) / 32;
-    uint32_t* f12 = r3f;   // P1's f1 ^ f2, staged in r3f's words: written only by the last pass
     flag_xor2_kernel<<<grid_for(nw), 256, 0, st>>>(f1, f2, nw, f12);
-    flag_shuffle1_kernel<<<grid_for(rows), 256, 0, st>>>(rows, k1, pi12, f12, f3, uf, vf, x1f, y1f);
     OGM_LAUNCH_CHECK();
-    const FlagTail ft{pi23, k3, x1f, y1f, wf, zf, r1f, r2f, c1f, r3f, plain};
+    const FlagTail ft{kc, kr, f12, f3, uwf, vzf, r1f, r2f, c1f, r3f, plain};
     RunTable rt[4];
     const bool runs = run_tables(run_start, run_off, run_nwin, rt);
     return shuffle_online_planned_impl(rows, q2, gdst, srow, a, b, c, u_src, v_src, 0, w_blind, w_order, z_slot,

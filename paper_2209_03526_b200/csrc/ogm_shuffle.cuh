@@ -938,17 +938,18 @@ __global__ void __launch_bounds__(256) chain_inter_kernel(const int32_t* __restr
 }
 
 // The flag column of a flag-split fetch (csrc/ogm_fetch.cuh) rides along the
-// final window passes: its phase 2 (P2's c1 bits, P3's R3 bits and the opened
-// column) needs the rows in output order, which these passes walk anyway.
-// Each warp owns 32 consecutive output rows, so a bit column word is one
-// ballot.  All pointers null = a plain shuffle.
+// final window passes: composed (ogm_flag_open_composed), it needs the rows
+// in output order -- P2's c1 bits, P3's R3 bits and the opened column --
+// which these passes walk anyway.  Each warp owns 32 consecutive output
+// rows, so a bit column word is one ballot.  All pointers null = a plain
+// shuffle.
 struct FlagTail {
-    const int32_t* pi23;      // c1's permutation
-    const int32_t* k3;        // R3's composed permutation
-    const uint32_t* x1f;      // P1's message bits (phase 1)
-    const uint32_t* y1f;      // P2's message bits (phase 1)
-    const uint32_t* wf;       // W's flag column (output order)
-    const uint32_t* zf;       // Z's flag column (output order)
+    const int32_t* kc;        // c1's bits: f12[kc[i]] ^ uwf[i]  (kc = k1 o pi23)
+    const int32_t* kr;        // R3's bits: f3[kr[i]] ^ vzf[i] ^ c1  (kr = pi12 o k3)
+    const uint32_t* f12;      // P1's f1 ^ f2
+    const uint32_t* f3;       // P2's third component
+    const uint32_t* uwf;      // composed blinds (output order)
+    const uint32_t* vzf;
     const uint32_t* r1f;      // R1, R2 flag columns (for the open)
     const uint32_t* r2f;
     uint32_t* c1f;            // P2's c1 bits (needed between the split passes)
@@ -966,8 +967,8 @@ template <int FLAG>
 __device__ __forceinline__ void flag_tail_word(const FlagTail& ft, int64_t base, int64_t i, bool valid) {
     uint32_t bc = 0, br = 0;
     if (valid) {
-        if (FLAG & 1) bc = tail_bit(ft.x1f, __ldcs(ft.pi23 + i));
-        if (FLAG & 2) br = tail_bit(ft.y1f, __ldcs(ft.k3 + i));
+        if (FLAG & 1) bc = tail_bit(ft.f12, __ldcs(ft.kc + i));
+        if (FLAG & 2) br = tail_bit(ft.f3, __ldcs(ft.kr + i));
     }
     const uint32_t wc = (FLAG & 1) ? __ballot_sync(0xffffffffu, bc) : 0u;
     const uint32_t wr = (FLAG & 2) ? __ballot_sync(0xffffffffu, br) : 0u;
@@ -975,13 +976,13 @@ __device__ __forceinline__ void flag_tail_word(const FlagTail& ft, int64_t base,
         const int64_t w = base >> 5;
         uint32_t c;
         if (FLAG & 1) {
-            c = wc ^ __ldg(ft.wf + w);
+            c = wc ^ __ldg(ft.uwf + w);
             if (ft.c1f) ft.c1f[w] = c;
         } else {
             c = __ldg(ft.c1f + w);
         }
         if (FLAG & 2) {
-            const uint32_t r = wr ^ c ^ __ldg(ft.zf + w);
+            const uint32_t r = wr ^ c ^ __ldg(ft.vzf + w);
             ft.r3f[w] = r;
             if (ft.plain) ft.plain[w] = __ldg(ft.r1f + w) ^ __ldg(ft.r2f + w) ^ r;
         }

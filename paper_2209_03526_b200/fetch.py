@@ -11,16 +11,20 @@ out rows (csrc/ogm_fetch.cuh).  The blinds are drawn in the reference's
 5-word layout and split offline (``ShuffleOffline(flag_split=True)``), so
 the kept records are bit-identical to the reference's.
 
+The flag column is composed across the parties' steps, as the payload's
+flat hand-over composes them: each party's bit gather is folded into the
+next party's (offline kc = k1 o pi23, kr = pi12 o k3 and the matching blind
+columns), so the message bits x1f / y1f exist only in flight and the column
+costs two random bit reads per row instead of four (ogm_flag_open_composed).
+
 Online phase (what the C5 fetch bench times):
   1. up to 2^21 rows: the 16-byte three-party shuffle in one cooperative
-     launch, then the flag column's two bit-gather launches
-     (ogm_flag_shuffle_trio, which also write the opened column);
-     from 2^22 rows: the chained planned payload shuffle, then the same two
-     flag launches; above 256 MB tables ONE launch sequence
-     (ogm_fetch128_online_planned): the flag column's first phase, then the
-     payload shuffle whose split final window passes also compute the flag
-     column's second phase and the opened column (they walk the rows in
-     output order anyway);
+     launch, then the composed flag column in one bit-gather launch (plus
+     f1 ^ f2), which also writes the opened column; from 2^22 rows: the
+     chained planned payload shuffle, then the same flag launches; above
+     256 MB tables ONE call (ogm_fetch128_online_planned): the payload
+     shuffle whose split final window passes also compute the flag column
+     and the opened column (they walk the rows in output order anyway);
   2. keep: hand-written compaction copying the kept payload rows of the
      three new components (ogm_keep_rows).
 """
@@ -33,11 +37,28 @@ import torch
 
 from . import _lib
 from .bits import words_for
-from .shuffle import (FLAG_ROW_BITS, ShuffleOffline, flat_chain_args, run_table_args, shuffle_online_fused,
+from .shuffle import (FLAG_ROW_BITS, ShuffleOffline, compose, flat_chain_args, run_table_args, shuffle_online_fused,
                       shuffle_online_planned)
 
 FUSED_MAX_BYTES = 32 << 20   # one cooperative launch up to 2^21 16-byte rows (measured crossover)
-FLAG_TAIL_MIN_BYTES = 256 << 20   # above: the flag column's phase 2 rides the split window passes
+FLAG_TAIL_MIN_BYTES = 256 << 20   # above: the flag column rides the split window passes
+
+
+def bit_gather(col: torch.Tensor, idx: torch.Tensor, n: int) -> torch.Tensor:
+    """Packed bit column out with bit i = bit idx[i] of ``col`` (little-endian
+    int32 words; clean tail).  Offline only (chunked torch ops)."""
+    nw = words_for(n)
+    out = torch.zeros((max(nw, 1),), dtype=torch.int32, device=col.device)
+    w64 = col.to(torch.int64) & 0xFFFFFFFF
+    shifts = torch.arange(32, device=col.device, dtype=torch.int64)
+    step = 1 << 22
+    for s in range(0, n, step):
+        j = idx[s:min(n, s + step)].to(torch.int64)
+        b = (w64[j >> 5] >> (j & 31)) & 1
+        b = torch.nn.functional.pad(b, (0, (-b.numel()) % 32))
+        v = (b.view(-1, 32) << shifts).sum(1)
+        out[s // 32:s // 32 + v.numel()] = torch.where(v >= 1 << 31, v - (1 << 32), v).to(torch.int32)
+    return out
 
 
 class FlaggedFetch:
@@ -69,15 +90,18 @@ class FlaggedFetch:
         self.r1, self.r2 = p1.out_a, p1.out_b
         self.r1f, self.r2f = p1.flag["out_a"], p1.flag["out_b"]
         nw = words_for(rows)
+        # the composed flag column (offline): c1 bits = f12[kc] ^ uwf, R3 bits = f3[kr] ^ vzf ^ c1 bits
+        self.kc, self.kr = compose(p2.pi23, p1.k1), compose(p3.k3, p2.pi12)
+        self.uwf = bit_gather(p1.flag["u"], p2.pi23, rows) ^ p2.flag["w"]
+        self.vzf = bit_gather(p2.flag["v"], p3.k3, rows) ^ p3.flag["z"]
 
         def vec():
             return torch.empty((max(nw, 1),), dtype=torch.int32, device=self.dev)
 
         self.r3 = torch.empty((rows, 4), dtype=torch.int32, device=self.dev)
-        self.x1f, self.y1f, self.c1f, self.r3f, self.plain = vec(), vec(), vec(), vec(), vec()
+        self.f12, self.c1f, self.r3f, self.plain = vec(), vec(), vec(), vec()
         self.plans = None if self.fused else [p1.plan_x1, p2.plan_y1, p2.plan_c1, p3.plan_r3]
-        # the flag tail rides the final window passes only where they are split (> 256 MB):
-        # measured 1% faster at 2^28, 2% slower folded into the dual pass at 2^24
+        # the flag column rides the final window passes only where they are split (> 256 MB)
         self.flag_tail = not self.fused and (rows * 16 > FLAG_TAIL_MIN_BYTES if flag_tail is None else flag_tail)
         self.inter = ([torch.empty_like(self.r3) for _ in range(3)] if not self.fused
                       else [torch.empty_like(self.r3) for _ in range(2)])
@@ -107,13 +131,12 @@ class FlaggedFetch:
                 shuffle_online_fused(self.off, a, b, c, self.inter[0], self.inter[1], None, self.r3)
             else:
                 shuffle_online_planned(self.off, a, b, c, self.r3, inter=self.inter)
-            _lib.call("ogm_flag_shuffle_trio", rows, P(p1.k1), P(p2.pi12), P(p2.pi23), P(p3.k3), P(flags[0]),
-                      P(flags[1]), P(flags[2]), P(p1.flag["u"]), P(p2.flag["v"]), P(p2.flag["w"]), P(p3.flag["z"]),
-                      P(self.r1f), P(self.r2f), P(self.x1f), P(self.y1f), None, P(self.r3f), P(self.plain),
-                      _lib.stream_ptr())
+            _lib.call("ogm_flag_open_composed", rows, P(self.kc), P(self.kr), P(flags[0]), P(flags[1]),
+                      P(flags[2]), P(self.uwf), P(self.vzf), P(self.r1f), P(self.r2f), P(self.f12), None,
+                      P(self.r3f), P(self.plain), _lib.stream_ptr())
         else:
-            # one launch sequence: flag phase 1, then the chained payload shuffle whose final
-            # window passes also produce the flag column's phase 2 and the opened column
+            # one call: the chained payload shuffle whose final window passes also produce the
+            # composed flag column and the opened column
             (u,), (v, _) = p1.chain_blinds(), p2.chain_blinds()
             arr = lambda xs: (ctypes.c_void_p * len(xs))(*[P(x) for x in xs])  # noqa: E731
             q2, gd, sr, it = (arr([pl.q2 for pl in self.plans]), arr([pl.gdst for pl in self.plans]),
@@ -123,10 +146,10 @@ class FlaggedFetch:
             rs, ro, rn = run_table_args(self.plans)
             _lib.call("ogm_fetch128_online_planned", rows, ctypes.addressof(q2), ctypes.addressof(gd),
                       ctypes.addressof(sr), ctypes.addressof(qs), rs, ro, rn, wr, P(a), P(b), P(c),
-                      P(u), P(v), P(wf), w_order, P(zf), z_order, ctypes.addressof(it), P(self.r3), P(p1.k1), P(p2.pi12), P(p2.pi23), P(p3.k3),
-                      P(flags[0]), P(flags[1]), P(flags[2]), P(p1.flag["u"]), P(p2.flag["v"]), P(p2.flag["w"]),
-                      P(p3.flag["z"]), P(self.r1f), P(self.r2f), P(self.x1f), P(self.y1f), P(self.c1f),
-                      P(self.r3f), P(self.plain), _lib.stream_ptr())
+                      P(u), P(v), P(wf), w_order, P(zf), z_order, ctypes.addressof(it), P(self.r3),
+                      P(self.kc), P(self.kr),
+                      P(flags[0]), P(flags[1]), P(flags[2]), P(self.uwf), P(self.vzf), P(self.r1f), P(self.r2f),
+                      P(self.f12), P(self.c1f), P(self.r3f), P(self.plain), _lib.stream_ptr())
         mats = (ctypes.c_void_p * 3)(P(self.r1), P(self.r2), P(self.r3))
         outs = (ctypes.c_void_p * 3)(*[P(o) for o in self.outs])
         _lib.call("ogm_keep_rows", rows, P(self.plain), 3, ctypes.addressof(mats), 4, ctypes.addressof(outs), 4,

@@ -1,6 +1,8 @@
 """C5 fetch at one size: per-launch device times of the online phase (for
-ncu launch lists) -- python scripts/prof_c5_fetch.py [log2 rows] [p ...]."""
+ncu launch lists) -- python scripts/prof_c5_fetch.py [log2 rows] [p ...];
+OGM_FLAG_TAIL=0/1 forces the flag column's layout (A/B)."""
 
+import os
 import sys
 from pathlib import Path
 
@@ -24,7 +26,8 @@ def main():
     seeds = (cfg[0].seed_with_next, cfg[1].seed_with_next, cfg[2].seed_with_next)
     payload = [workloads.device_random_words(rows * 4, 1, 30 + c).reshape(rows, 4) for c in range(3)]
     f12 = [bc._random_bits(rows, 1, 40), bc._random_bits(rows, 1, 41)]
-    ff = FlaggedFetch(seeds, 0, rows)
+    tail = os.environ.get("OGM_FLAG_TAIL")
+    ff = FlaggedFetch(seeds, 0, rows, flag_tail=None if tail is None else tail == "1")
     for p in ps:
         fp = bc._bernoulli_bits(rows, p, 7)
         flags = [f12[0], f12[1], fp ^ f12[0] ^ f12[1]]

@@ -30,6 +30,23 @@ def _case(g, tag):
     return rows, master, ids, flags
 
 
+@pytest.mark.parametrize("n", [0, 1, 31, 32, 33, 1000, (1 << 22) + 5])
+def test_bit_gather_matches_numpy(n):
+    """fetch.bit_gather (offline composition of the flag blinds): bit i of
+    the output = bit idx[i] of the source column, clean tail."""
+    import torch
+
+    from paper_2209_03526_b200.fetch import bit_gather
+
+    rng = np.random.default_rng(n)
+    src = rng.integers(0, 2, n, dtype=np.uint8)
+    idx = rng.permutation(n).astype(np.int32)
+    col = torch.from_numpy(oracle.pack_bits(src).view(np.int32).copy())
+    got = bit_gather(col, torch.from_numpy(idx), n).numpy().view(np.uint32)
+    want = oracle.pack_bits(src[idx])
+    assert np.array_equal(got[:want.size], want)
+
+
 def test_oracle_fetch_matches_reference(golden):
     g = golden("c5fetch")
     for tag in g["cases"]:
