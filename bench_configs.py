@@ -63,17 +63,20 @@ def events(n):
 # ---------------------------------------------------------------------------
 
 
-def cpu_port_sec_eval(comps, words: int, ind_of, gpu_bits_of, sample: int) -> dict:
+def cpu_port_sec_eval(comps, words: int, ind_of, gpu_bits_of, sample: int, folded: bool = False) -> dict:
     """The CPU path beside a secEval line: the oracle port's masked parity
     (oracle/, C, one core; src/engine.py:76-80) for all 3 parties x 2 passes
     on the first `sample` candidate rows, timed and extrapolated linearly to
-    the full row count.  Its bits are checked against the GPU result."""
+    the full row count.  Its bits are checked against the GPU result (per
+    pass, or -- ``folded`` -- the XOR of the two passes against
+    gpu_bits_of(p, None))."""
     import oracle
 
     rows = comps[0].shape[0]
     sample = min(sample, rows)
     host = [c[:sample, :words].cpu().numpy().view(np.uint32) for c in comps]
     dt, same = 0.0, True
+    acc = {}
     for ps in range(2):
         for p in range(3):
             ia = ind_of(p, ps)[0].cpu().numpy().view(np.uint32)[:words]
@@ -81,6 +84,12 @@ def cpu_port_sec_eval(comps, words: int, ind_of, gpu_bits_of, sample: int) -> di
             t = time.perf_counter()
             bits = oracle.masked_parity(host[p], host[(p + 1) % 3], ia, ib)
             dt += time.perf_counter() - t
+            if folded:
+                acc[p] = bits if ps == 0 else acc[p] ^ bits
+                if ps == 1:
+                    got = oracle.unpack_bits(gpu_bits_of(p, None), rows)[:sample]
+                    same = same and bool(np.array_equal(acc[p], got))
+                continue
             got = oracle.unpack_bits(gpu_bits_of(p, ps), rows)[:sample]
             same = same and bool(np.array_equal(bits, got))
     return {"value": 1e3 * dt * rows / sample, "unit": "ms", "cores": 1, "kind": "port",
@@ -1045,8 +1054,10 @@ def c4_sec_eval(rows: int, seed: int, steps: int, warmup: int, rank: int, world:
     """C4 (BASELINE configs[3]) root-slot secEval, row-sharded over `world`
     ranks (an initialised NCCL group when world > 1): 2M candidates of one
     vertex type (16M vertices / 8 types), Zipf(1.1) attribute over 10^4
-    values, an interval predicate (2 DCF passes) for all three parties, match
-    bits all-gathered.  Strong scaling; device time max over ranks.
+    values, an interval predicate (2 DCF passes, folded into one parity pass
+    over XORed indicators with both zero shares XORed in -- the co-resident
+    trio's secEval, same result shares) for all three parties, match bits
+    all-gathered.  Strong scaling; device time max over ranks.
 
     Shares are drawn by GLOBAL row (workloads.shared_one_hot row0), so every
     world size shares the same table; rank 0 then gates the all-gathered
@@ -1054,7 +1065,7 @@ def c4_sec_eval(rows: int, seed: int, steps: int, warmup: int, rank: int, world:
     rank's shard (regenerated from the same streams)."""
     import torch.distributed as dist
 
-    from paper_2209_03526_b200.sharding import ShardPlan, sharded_sec_eval_trio
+    from paper_2209_03526_b200.sharding import ShardPlan, fold_indicators, sharded_sec_eval_trio
 
     n = 10_000
     plan = ShardPlan(rows, world)
@@ -1075,7 +1086,9 @@ def c4_sec_eval(rows: int, seed: int, steps: int, warmup: int, rank: int, world:
              for q in range(3)] for ps in range(2)]
     cfg = make_session_configs(b"\x44" * 16)
     zk = [(c.zero_key_own, c.zero_key_prev) for c in cfg]
-    step = lambda: sharded_sec_eval_trio(comps, w, plan, rank, inds, zk, [0, 1])  # noqa: E731
+    # the two passes folded into one parity pass (the co-resident trio's secEval, ShardedTrio.sec_eval)
+    folded = fold_indicators(inds)
+    step = lambda: sharded_sec_eval_trio(comps, w, plan, rank, folded, zk, [0, 1], fold=True)  # noqa: E731
     for _ in range(warmup):
         step()
     torch.cuda.synchronize()
@@ -1099,15 +1112,15 @@ def c4_sec_eval(rows: int, seed: int, steps: int, warmup: int, rank: int, world:
 
         zero = {(p_, ps): oracle.zero_share(zk[p_][0], zk[p_][1], ps, rows) for p_ in range(3) for ps in range(2)}
 
-        def gpu_bits(p_, ps):  # undo the re-share blinding: additive bits = message ^ zero share
-            return res[ps][p_].cpu().numpy().view(np.uint32) ^ zero[(p_, ps)]
+        def gpu_bits(p_, ps=None):  # undo the re-share blinding: additive bits = result ^ both zero shares
+            return res[0][p_].cpu().numpy().view(np.uint32) ^ zero[(p_, 0)] ^ zero[(p_, 1)]
 
         if world == 1:
-            cpu = cpu_port_sec_eval(comps, w, lambda p_, ps: inds[ps][p_], gpu_bits, 20000)
+            cpu = cpu_port_sec_eval(comps, w, lambda p_, ps: inds[ps][p_], gpu_bits, 20000, folded=True)
         # N-rank parity gate: 2048 rows from the start of every shard, shares regenerated by global row
         per = 2048
         checked, equal = 0, True
-        full = {(p_, ps): oracle.unpack_bits(gpu_bits(p_, ps), rows) for p_ in range(3) for ps in range(2)}
+        full = {p_: oracle.unpack_bits(gpu_bits(p_), rows) for p_ in range(3)}
         for r in range(world):
             r_lo, r_hi = plan.bounds(r)
             m = min(per, r_hi - r_lo)
@@ -1115,16 +1128,18 @@ def c4_sec_eval(rows: int, seed: int, steps: int, warmup: int, rank: int, world:
                 continue
             sub = torch.from_numpy(vals_all[r_lo:r_lo + m]).cuda()
             sc = [c.cpu().numpy().view(np.uint32) for c in workloads.shared_one_hot(sub, n, seed, 40, row0=r_lo)]
-            for ps in range(2):
-                for p_ in range(3):
+            for p_ in range(3):
+                want = 0
+                for ps in range(2):
                     ia = inds[ps][p_][0].cpu().numpy().view(np.uint32)[:w]
                     ib = inds[ps][p_][1].cpu().numpy().view(np.uint32)[:w]
-                    want = oracle.masked_parity(sc[p_], sc[(p_ + 1) % 3], ia, ib)
-                    equal = equal and bool(np.array_equal(want, full[(p_, ps)][r_lo:r_lo + m]))
+                    want = want ^ oracle.masked_parity(sc[p_], sc[(p_ + 1) % 3], ia, ib)
+                equal = equal and bool(np.array_equal(want, full[p_][r_lo:r_lo + m]))
             checked += m
         gate = {"rows_checked": checked, "shards_checked": world, "equal_to_oracle": equal,
-                "how": "all-gathered re-shared bits ^ zero share == oracle.masked_parity on the first "
-                       f"{per} rows of every rank's shard (shares drawn by global row)"}
+                "how": "all-gathered re-shared bits ^ both passes' zero shares == the XOR of the two passes' "
+                       f"oracle.masked_parity on the first {per} rows of every rank's shard (shares drawn by "
+                       "global row)"}
         if not equal:
             raise SystemExit("C4 sharded secEval differs from the oracle port")
     return {"config": f"C4 root secEval, {rows} candidates (Zipf attr n={n}, w={w}), interval, "

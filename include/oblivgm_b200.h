@@ -165,6 +165,15 @@ int ogm_zero_share_trio_slice2(const uint8_t* k1, const uint8_t* k2, const uint8
                                const uint32_t* const* xor_into1, uint32_t* const* out1,
                                const uint32_t* const* xor_into2, uint32_t* const* out2, void* stream);
 
+/* The two passes of an interval predicate folded (co-resident trio): a
+ * re-share is a zero share XORed in and parity is linear, so the XOR of the
+ * two passes' re-shared parities equals ONE parity over XORed indicators
+ * with both zero shares XORed in.  out = xor_into ^ zs(counter1) ^
+ * zs(counter2) on the slice [w0, w0 + nwords) (xor_into may alias out). */
+int ogm_zero_share_trio_fold2(const uint8_t* k1, const uint8_t* k2, const uint8_t* k3, uint64_t counter1,
+                              uint64_t counter2, int64_t nbits, int64_t w0, int64_t nwords,
+                              const uint32_t* const* xor_into, uint32_t* const* out, void* stream);
+
 /* The matrix re-share of src/engine.py:83-92 for the three parties: the
  * zero share of rows*words*32 bits XORed into xor_into[q], every row's tail
  * (bits >= width of each `words`-word row) masked after the XOR. */

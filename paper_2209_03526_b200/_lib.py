@@ -52,6 +52,7 @@ SIGNATURES = {
     "ogm_zero_share_trio": ([_cp, _cp, _cp, _u64, _i64, _vp, _vp, _vp], _int),
     "ogm_zero_share_trio_rows": ([_cp, _cp, _cp, _u64, _i64, _i64, _i64, _vp, _vp, _vp], _int),
     "ogm_zero_share_trio_slice2": ([_cp, _cp, _cp, _u64, _u64, _i64, _i64, _i64, _vp, _vp, _vp, _vp, _vp], _int),
+    "ogm_zero_share_trio_fold2": ([_cp, _cp, _cp, _u64, _u64, _i64, _i64, _i64, _vp, _vp, _vp], _int),
     "ogm_zero_share_trio_slice": ([_cp, _cp, _cp, _u64, _i64, _i64, _i64, _vp, _vp, _vp], _int),
     "ogm_and_terms": ([_i64, _int, _vp, _vp, _vp, _vp, _vp, _vp], _int),
     "ogm_xor_words": ([_i64, _vp, _vp, _vp, _vp, _vp], _int),

@@ -346,6 +346,7 @@ struct Zs3Args {
     uint32_t* out[2][3];
     uint64_t counter[2];
     int npass;
+    int fold;   // 1: one output, zero share of counter[0] XOR that of counter[1] (npass = 1)
 };
 
 template <class TAB = AesTab>
@@ -369,6 +370,11 @@ __global__ void __launch_bounds__(kAesThreads) zero_share3_kernel(const __grid_c
         uint4 f[3];
 #pragma unroll
         for (int q = 0; q < 3; q++) f[q] = aes128_enc(T, ctr, ParamKey{a.k[q].rk});
+        if (a.fold) {   // the two streams' shares XOR: F(c0) ^ F(c1) per key, then the partner XOR
+            const uint4 ctr2 = ctr_block(label_be, a.counter[1], (uint64_t)(b0 + b));
+#pragma unroll
+            for (int q = 0; q < 3; q++) f[q] = xor4(f[q], aes128_enc(T, ctr2, ParamKey{a.k[q].rk}));
+        }
 #pragma unroll
         for (int q = 0; q < 3; q++) {
             const uint4 z = xor4(f[q], f[(q + 2) % 3]);
@@ -413,7 +419,10 @@ __global__ void __launch_bounds__(96) zero_share3x_kernel(const __grid_constant_
         const int ps = t >= nblk ? 1 : 0;
         const int64_t b = t - ps * nblk;
         uint4 f = make_uint4(0, 0, 0, 0);
-        if (valid) f = aes128_enc(T, ctr_block(label_be, a.counter[ps], (uint64_t)(b0 + b)), ParamKey{a.k[q].rk});
+        if (valid) {
+            f = aes128_enc(T, ctr_block(label_be, a.counter[ps], (uint64_t)(b0 + b)), ParamKey{a.k[q].rk});
+            if (a.fold) f = xor4(f, aes128_enc(T, ctr_block(label_be, a.counter[1], (uint64_t)(b0 + b)), ParamKey{a.k[q].rk}));
+        }
         xch[q * 32 + lane] = f;
         __syncthreads();
         if (valid) {
@@ -1036,6 +1045,8 @@ static int masked_parity_impl(int64_t rows, int64_t words, int64_t pitch, int nc
         // a warp's rows per stage times the (pass, party) count must fit one packed word
         const int rows_per_warp = 32 / (npass * nparty);
         int RT = 32;
+        // stages as large as three fit (smaller stages measured far slower at C4: RT 16 / 8 / 4 =
+        // 1.24 / 1.70 / 2.51 ms -- the per-stage barrier and butterfly amortise over fewer rows)
         while (RT > 1 && ((int64_t)ncomp * RT * pitch * 4 > kParTmaSmemMax / 3 || RT > RGW * rows_per_warp)) RT >>= 1;
         if (RGW > RT) RGW = RT;
         const int64_t stage_bytes = (int64_t)ncomp * RT * pitch * 4;
@@ -1135,7 +1146,8 @@ static int zero_share_trio_impl(const uint8_t* k1, const uint8_t* k2, const uint
                                 int64_t nbits, int64_t w0, int64_t nloc, const uint32_t* const* xor_into,
                                 uint32_t* const* out, void* stream, int64_t row_words = 0,
                                 uint32_t row_tail = 0xffffffffu, int npass = 1, uint64_t counter2 = 0,
-                                const uint32_t* const* xor_into2 = nullptr, uint32_t* const* out2 = nullptr) {
+                                const uint32_t* const* xor_into2 = nullptr, uint32_t* const* out2 = nullptr,
+                                int fold = 0) {
     using namespace ogm;
     OGM_CHECK_ARG(k1 && k2 && k3 && out && (npass == 1 || out2), OGM_ERR_ARG,
                   "zero-share keys and outputs are required");
@@ -1152,6 +1164,7 @@ static int zero_share_trio_impl(const uint8_t* k1, const uint8_t* k2, const uint
     a.k[1] = make_sched(k2);
     a.k[2] = make_sched(k3);
     a.npass = npass;
+    a.fold = fold;
     a.counter[0] = counter;
     a.counter[1] = counter2;
     for (int q = 0; q < 3; q++) {
@@ -1196,6 +1209,13 @@ int ogm_zero_share_trio_slice2(const uint8_t* k1, const uint8_t* k2, const uint8
                                const uint32_t* const* xor_into2, uint32_t* const* out2, void* stream) {
     return zero_share_trio_impl(k1, k2, k3, counter1, nbits, w0, nwords, xor_into1, out1, stream, 0, 0xffffffffu, 2,
                                 counter2, xor_into2, out2);
+}
+
+int ogm_zero_share_trio_fold2(const uint8_t* k1, const uint8_t* k2, const uint8_t* k3, uint64_t counter1,
+                              uint64_t counter2, int64_t nbits, int64_t w0, int64_t nwords,
+                              const uint32_t* const* xor_into, uint32_t* const* out, void* stream) {
+    return zero_share_trio_impl(k1, k2, k3, counter1, nbits, w0, nwords, xor_into, out, stream, 0, 0xffffffffu, 1,
+                                counter2, nullptr, nullptr, 1);
 }
 
 int ogm_zero_share_trio_slice(const uint8_t* k1, const uint8_t* k2, const uint8_t* k3, uint64_t counter,

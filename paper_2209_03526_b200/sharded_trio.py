@@ -92,11 +92,15 @@ class ShardedTrio(Trio):
             return super().sec_eval(group, key_pairs, attr, domain, cache)
         rows6 = self._pass_indicators(key_pairs, domain, cache)
         npass = len(rows6)
+        fold = npass == 2   # one parity pass over the folded indicators (Trio._folded_indicators)
+        if fold:
+            rows6 = [self._folded_indicators(key_pairs, domain, cache)]
         inds = [[(r[2 * q], r[2 * q + 1]) for q in range(3)] for r in rows6]
         comps = group.attrs[attr]
         zk = [(k, None) for k in self.k]
         counters = [self.counter + ps for ps in range(npass)]
-        packed = sec_eval_local_packed(comps, comps[0].shape[1], group.plan, self.rank, inds, zk, counters)
+        packed = sec_eval_local_packed(comps, comps[0].shape[1], group.plan, self.rank, inds, zk, counters,
+                                       fold=fold)
         self.counter += npass
         nvec, wpr = packed.shape
         if self.world == 1:
@@ -104,7 +108,7 @@ class ShardedTrio(Trio):
         else:
             full = assemble_many(self.comm.all_gather(packed).view(self.world, nvec, wpr), group.plan)
         result = None
-        for ps in range(npass):
+        for ps in range(nvec // 3):
             b = full[3 * ps: 3 * ps + 3]
             shared = [b[2].contiguous(), b[0].contiguous(), b[1].contiguous()]   # comp j := blinded_{j-1}
             result = shared if result is None else self.xor(result, shared)

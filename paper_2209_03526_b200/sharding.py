@@ -166,14 +166,35 @@ def all_gather_bits(local: torch.Tensor, plan: ShardPlan, group=None) -> torch.T
     return assemble(as_comm(group).all_gather(pad_slice(local, plan)), plan)
 
 
-def sec_eval_local_packed(comps, words: int, plan: ShardPlan, rank: int, inds, zero_keys, counters) -> torch.Tensor:
+def fold_indicators(inds) -> list:
+    """[pass][party] -> (ind_a, ind_b) of a two-pass predicate folded into ONE
+    pass: per party (a0 ^ a1, b0 ^ b1).  Parity is linear, so one masked
+    parity over the folded indicators is the XOR of the two passes'
+    (sec_eval_local_packed(fold=True))."""
+    def x(a, b):
+        o = torch.empty_like(a)
+        _lib.call("ogm_xor_words", a.numel(), _lib.ptr(a), _lib.ptr(b), None, _lib.ptr(o), _lib.stream_ptr())
+        return o
+    return [[(x(inds[0][q][0], inds[1][q][0]), x(inds[0][q][1], inds[1][q][1])) for q in range(3)]]
+
+
+def sec_eval_local_packed(comps, words: int, plan: ShardPlan, rank: int, inds, zero_keys, counters,
+                          fold: bool = False) -> torch.Tensor:
     """This rank's share of a row-sharded secEval for all three parties: the
     blinded packed bits of its rows for every (pass, party), as one
     zero-padded (3*npass, words_per_rank) buffer ready for ONE all-gather
     (at 8 GPUs the per-call collective latency, not the kernel, bounds the
-    strong scaling).  Row j = pass j // 3, party j % 3."""
+    strong scaling).  Row j = pass j // 3, party j % 3.
+
+    fold=True (a two-pass predicate, co-resident trio): ``inds`` holds the
+    ONE folded pass (fold_indicators) and ``counters`` both passes' zero-share
+    counters; the buffer then holds 3 rows, each the XOR of the two passes'
+    re-shared bits (both zero shares XORed in) -- the same result shares from
+    one parity pass and half the all-gather."""
     if plan.per_rank % 32:
         raise ValueError("secEval shards need row counts that are multiples of 32 (default ShardPlan alignment)")
+    if fold and (len(inds) != 1 or len(counters) != 2):
+        raise ValueError("a folded secEval takes one folded pass of indicators and two counters")
     lo, hi = plan.bounds(rank)
     nloc = hi - lo
     npass = len(inds)
@@ -190,7 +211,11 @@ def sec_eval_local_packed(comps, words: int, plan: ShardPlan, rank: int, inds, z
     adds = [[outs[ps * 3 + q][: w1 - w0] for q in range(3)] for ps in range(npass)]
     k = (zero_keys[0][0], zero_keys[1][0], zero_keys[2][0])
     none3 = A([None, None, None])
-    if w1 > w0 and npass == 2:
+    if w1 > w0 and fold:
+        # both passes' zero shares in one output (F(c0) ^ F(c1) per key)
+        _lib.call("ogm_zero_share_trio_fold2", *k, counters[0], counters[1], plan.rows, w0, w1 - w0, none3,
+                  A(adds[0]), _lib.stream_ptr())
+    elif w1 > w0 and npass == 2:
         # both passes, all three parties: one launch (3 AES per block and pass, not 6)
         _lib.call("ogm_zero_share_trio_slice2", *k, counters[0], counters[1], plan.rows, w0, w1 - w0,
                   none3, A(adds[0]), none3, A(adds[1]), _lib.stream_ptr())
@@ -216,7 +241,7 @@ def assemble_many(gathered: torch.Tensor, plan: ShardPlan) -> list:
 
 
 def sharded_sec_eval_trio(comps, words: int, plan: ShardPlan, rank: int, inds, zero_keys, counters,
-                          group=None) -> list:
+                          group=None, fold: bool = False) -> list:
     """One secEval for all three parties on this rank's row shard.
 
     comps: the three (rows_local, pitch) share components of this shard.
@@ -225,8 +250,9 @@ def sharded_sec_eval_trio(comps, words: int, plan: ShardPlan, rank: int, inds, z
     counters: zero-share counter per pass (identical across parties).
     Returns per pass the three parties' full blinded vectors (all ranks),
     i.e. the re-share messages; component j of the result is blinded_{j-1}.
+    fold: as sec_eval_local_packed (one folded pass, two counters).
     """
-    packed = sec_eval_local_packed(comps, words, plan, rank, inds, zero_keys, counters)
+    packed = sec_eval_local_packed(comps, words, plan, rank, inds, zero_keys, counters, fold=fold)
     nvec, wpr = packed.shape
     if plan.world == 1:
         full = [packed[j][: plan.total_words] for j in range(nvec)]
@@ -494,5 +520,5 @@ class ShardedTrioShuffle:
         return [p1.out_a, p1.out_b, r3]
 
 
-__all__ = ["Comm", "DistComm", "ThreadComm", "as_comm", "ShardPlan", "pad_slice", "assemble", "all_gather_bits", "sharded_sec_eval_trio", "ExchangePlan",
+__all__ = ["Comm", "DistComm", "ThreadComm", "as_comm", "ShardPlan", "pad_slice", "assemble", "all_gather_bits", "sharded_sec_eval_trio", "fold_indicators", "ExchangePlan",
            "exchange_plan", "exchange_gather", "ShardedTrioShuffle", "fss"]

@@ -430,22 +430,48 @@ class Trio:
             inds.append(cache[ck])
         return inds
 
+    def _folded_indicators(self, key_pairs: list, domain: int, cache: dict) -> list:
+        """The six indicator rows of a two-pass (interval) predicate XORed
+        over the passes, cached per key: parity is linear and a re-share is a
+        zero share XORed in, so the XOR of the two passes' re-shared parities
+        (src/engine.py:150-165) is ONE parity over the folded indicators with
+        both zero shares XORed in (reshare2)."""
+        ck = (id(key_pairs[0][0]), "fold")
+        if ck not in cache:
+            p0, p1 = self._pass_indicators(key_pairs, domain, cache)
+            rows = []
+            for a, b in zip(p0, p1):
+                o = torch.empty_like(a)
+                _lib.call("ogm_xor_words", a.numel(), _lib.ptr(a), _lib.ptr(b), None, _lib.ptr(o), _lib.stream_ptr())
+                rows.append(o)
+            cache[ck] = rows
+        return cache[ck]
+
+    def reshare2(self, adds: list, nbits: int) -> list:
+        """Two consecutive re-shares (counters c, c + 1) of values whose XOR
+        is ``adds``, folded: the XOR of reshare(x0) and reshare(x1) for x0 ^
+        x1 = adds (src/rss.py:164-176 twice, comp j := blinded_{j-1})."""
+        outs = [torch.empty_like(a) for a in adds]
+        if nbits:
+            _lib.call("ogm_zero_share_trio_fold2", self.k[0], self.k[1], self.k[2], self.counter, self.counter + 1,
+                      nbits, 0, words_for(nbits), A(adds), A(outs), _lib.stream_ptr())
+        self.counter += 2
+        return [outs[2], outs[0], outs[1]]
+
     def sec_eval(self, group: TrioGroup, key_pairs: list, attr: str, domain: int, cache: dict) -> list:
-        """src/engine.py:139-165 for all parties; both passes from one read."""
+        """src/engine.py:139-165 for all parties in one read of the shares; a
+        two-pass (interval) predicate as ONE parity pass over the folded
+        indicators (_folded_indicators, reshare2) -- the same result shares."""
         inds = self._pass_indicators(key_pairs, domain, cache)
-        npass = len(inds)
+        fold = len(inds) == 2
+        flat = self._folded_indicators(key_pairs, domain, cache) if fold else inds[0]
         comps = group.attrs[attr]
         rows = group.count
         words = comps[0].shape[1]
-        outs = [self._empty(words_for(rows)) for _ in range(3 * npass)]
-        flat = [t for ps in range(npass) for t in inds[ps]]
+        outs = [self._empty(words_for(rows)) for _ in range(3)]
         _lib.call("ogm_masked_parity", rows, words, comps[0].stride(0), 3, A(comps), 3, _lib.int_array([0, 1, 2]),
-                  _lib.int_array([1, 2, 0]), npass, A(flat), A(outs), _lib.stream_ptr())
-        result = None
-        for ps in range(npass):
-            sh = self.reshare(outs[3 * ps:3 * ps + 3], rows)
-            result = sh if result is None else self.xor(result, sh)
-        return result
+                  _lib.int_array([1, 2, 0]), 1, A(flat), A(outs), _lib.stream_ptr())
+        return self.reshare2(outs, rows) if fold else self.reshare(outs, rows)
 
     def combine(self, bits: list, combiner: str, any_mode: str, n: int) -> list:
         """src/engine.py:168-189."""

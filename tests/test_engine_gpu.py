@@ -351,6 +351,36 @@ def test_sharded_sec_eval_slices_equal_unsharded(world):
             assert np.array_equal(host(full[ps * 3 + q]), want), (world, ps, q)
 
 
+@pytest.mark.parametrize("world", [1, 3])
+def test_folded_sec_eval_equals_two_passes(world):
+    """A two-pass predicate folded (fold_indicators + fold=True: one parity
+    pass over XORed indicators, both zero shares XORed in) gives the XOR of
+    the two passes' re-shared vectors -- what ShardedTrio / Trio combine."""
+    from paper_2209_03526_b200.graphs import padded_device_matrix
+    from paper_2209_03526_b200.sharding import (ShardPlan, assemble_many, fold_indicators, sec_eval_local_packed,
+                                                sharded_sec_eval_trio)
+    rows, words, counters = 70_000, 313, [3, 4]
+    rng = np.random.default_rng(40 + world)
+    comps_h = [rng.integers(0, 1 << 32, (rows, words), dtype=np.uint32) for _ in range(3)]
+    inds_h = [[(rng.integers(0, 1 << 32, words, dtype=np.uint32), rng.integers(0, 1 << 32, words, dtype=np.uint32))
+               for _ in range(3)] for _ in range(2)]
+    keys = [bytes([19 + i]) * 16 for i in range(3)]
+    zk = [(keys[0], keys[2]), (keys[1], keys[0]), (keys[2], keys[1])]
+    comps = [padded_device_matrix(c) for c in comps_h]
+    inds = [[(dev(a), dev(b)) for a, b in ps] for ps in inds_h]
+    plan = ShardPlan(rows, world)
+    two = sharded_sec_eval_trio(comps, words, ShardPlan(rows, 1), 0, inds, zk, counters)
+    folded = fold_indicators(inds)
+    if world == 1:
+        got = sharded_sec_eval_trio(comps, words, plan, 0, folded, zk, counters, fold=True)[0]
+    else:
+        packs = [sec_eval_local_packed([c[lo:hi] for c in comps], words, plan, r, folded, zk, counters, fold=True)
+                 for r, (lo, hi) in enumerate(plan.bounds(r) for r in range(world))]
+        got = assemble_many(torch.stack(packs), plan)
+    for q in range(3):
+        assert torch.equal(got[q], two[0][q] ^ two[1][q]), q
+
+
 @pytest.mark.parametrize("rows,width", [(1, 128), (1000, 128), (70_001, 129), (300_000, 45), (50_000, 700)])
 @pytest.mark.parametrize("window_bytes,tile_rows", [(None, None), (64 << 10, 100)])
 def test_planned_gather_equals_direct(rows, width, window_bytes, tile_rows):

@@ -310,6 +310,26 @@ def test_c2_full_size_eval_matches_oracle():
     assert np.array_equal(e0, want)
 
 
+@pytest.mark.parametrize("nbits,w0,nw", [(250_003, 4096, 3717), (100, 0, 4), (33, 0, 2), (64_000_000, 0, 2_000_000)])
+def test_zero_share_trio_fold2_equals_xor_of_two(golden, nbits, w0, nw):
+    """ogm_zero_share_trio_fold2 (the folded two-pass re-share) == the XOR
+    of the two single-counter slices, in place (xor_into aliasing out) too."""
+    g = golden("zero_share")
+    keys = [g["keys"][i].tobytes() for i in range(3)]
+    A = _lib.ptr_array
+    mk = lambda: [torch.empty((nw,), dtype=torch.int32, device="cuda") for _ in range(3)]  # noqa: E731
+    base = [dev_u32(np.arange(nw, dtype=np.uint32) * np.uint32(5 + q)) for q in range(3)]
+    one, two = mk(), mk()
+    _lib.call("ogm_zero_share_trio_slice", *keys, 21, nbits, w0, nw, A(base), A(one), _lib.stream_ptr())
+    _lib.call("ogm_zero_share_trio_slice", *keys, 22, nbits, w0, nw, A(one), A(two), _lib.stream_ptr())
+    got = mk()
+    _lib.call("ogm_zero_share_trio_fold2", *keys, 21, 22, nbits, w0, nw, A(base), A(got), _lib.stream_ptr())
+    inplace = [b.clone() for b in base]
+    _lib.call("ogm_zero_share_trio_fold2", *keys, 21, 22, nbits, w0, nw, A(inplace), A(inplace), _lib.stream_ptr())
+    for q in range(3):
+        assert torch.equal(got[q], two[q]) and torch.equal(inplace[q], two[q]), q
+
+
 def test_zero_share_trio_slice2_equals_two_slices(golden):
     """Both passes' zero-share slices in one launch == two single-counter launches."""
     g = golden("zero_share")
