@@ -139,7 +139,7 @@ __global__ void __launch_bounds__(256) masked_parity_kernel(const ParityArgs p) 
 // with 128-bit loads, and the indicator traffic is paid once per CTA.
 // ---------------------------------------------------------------------------
 template <int NPARTY, int NPASS>
-__global__ void __launch_bounds__(256) masked_parity_v2_kernel(const ParityArgs p, int CW, int64_t tiles_per_block) {
+__global__ void __launch_bounds__(256, 2) masked_parity_v2_kernel(const ParityArgs p, int CW, int64_t tiles_per_block) {
     constexpr int NJ = NPARTY * NPASS;
     constexpr int NCOMP = NPARTY == 1 ? 2 : 3;
     const int lane = threadIdx.x & 31;
@@ -172,7 +172,10 @@ __global__ void __launch_bounds__(256) masked_parity_v2_kernel(const ParityArgs 
         const int nrow = (int)min((int64_t)32, p.rows - rbase);
         // rows in batches of RB: issue all RB x NCOMP 128-bit loads before the
         // first ballot so each lane keeps RB*NCOMP*16 B in flight.
-        constexpr int RB = NPARTY == 1 ? 8 : 4;
+        // (RB divides 32: the row bits of a tile are shifted in per batch; two CTAs per SM.
+        // Measured for the trio's single pass at w = 5691: RB 2 / 4 / 8 = 2.13 / 2.03 / 2.01 ms)
+        constexpr int RB = (NPARTY == 1 || NPASS == 1) ? 8 : 4;
+        static_assert(32 % RB == 0, "a batch of rows must divide the 32-row tile");
         for (int i0 = 0; i0 < nrow; i0 += RB) {
             uint4 cv[RB][NCOMP];
 #pragma unroll

@@ -159,7 +159,8 @@ class ShardedTrio(Trio):
         host, local_idx, first, total = sharded_keep(plain, plan, rank, self.comm)
         opened = BitVector(host[: words_for(plan.rows)], plan.rows)
         self.opened.append((self.label, opened))
-        audit.append(("fetch", opened.to_bits().copy()))
+        bits = opened.to_bits()
+        audit.append(("fetch", bits))
         # this shard's kept rows, sliced into fields, then every shard's kept records in shard order
         k_local = local_idx.numel()
         fields = [(1, group.id_width)]
@@ -167,7 +168,6 @@ class ShardedTrio(Trio):
         for wd in widths:
             fields.append((off, wd))
             off += wd
-        bits = opened.to_bits()
         counts = [int(bits[a:b].sum()) for a, b in (plan.bounds(r) for r in range(self.world))]
         kmax = max(counts) if counts else 0
         got = []

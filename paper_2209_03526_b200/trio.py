@@ -430,6 +430,9 @@ class Trio:
             inds.append(cache[ck])
         return inds
 
+    # a two-pass predicate as one parity pass over folded indicators (sec_eval)
+    FOLD_PASSES = True
+
     def _folded_indicators(self, key_pairs: list, domain: int, cache: dict) -> list:
         """The six indicator rows of a two-pass (interval) predicate XORed
         over the passes, cached per key: parity is linear and a re-share is a
@@ -463,15 +466,25 @@ class Trio:
         two-pass (interval) predicate as ONE parity pass over the folded
         indicators (_folded_indicators, reshare2) -- the same result shares."""
         inds = self._pass_indicators(key_pairs, domain, cache)
-        fold = len(inds) == 2
-        flat = self._folded_indicators(key_pairs, domain, cache) if fold else inds[0]
         comps = group.attrs[attr]
         rows = group.count
         words = comps[0].shape[1]
-        outs = [self._empty(words_for(rows)) for _ in range(3)]
+        if len(inds) == 2 and self.FOLD_PASSES:
+            outs = [self._empty(words_for(rows)) for _ in range(3)]
+            _lib.call("ogm_masked_parity", rows, words, comps[0].stride(0), 3, A(comps), 3, _lib.int_array([0, 1, 2]),
+                      _lib.int_array([1, 2, 0]), 1, A(self._folded_indicators(key_pairs, domain, cache)), A(outs),
+                      _lib.stream_ptr())
+            return self.reshare2(outs, rows)
+        npass = len(inds)
+        outs = [self._empty(words_for(rows)) for _ in range(3 * npass)]
         _lib.call("ogm_masked_parity", rows, words, comps[0].stride(0), 3, A(comps), 3, _lib.int_array([0, 1, 2]),
-                  _lib.int_array([1, 2, 0]), 1, A(flat), A(outs), _lib.stream_ptr())
-        return self.reshare2(outs, rows) if fold else self.reshare(outs, rows)
+                  _lib.int_array([1, 2, 0]), npass, A([t for ps in range(npass) for t in inds[ps]]), A(outs),
+                  _lib.stream_ptr())
+        result = None
+        for ps in range(npass):
+            sh = self.reshare(outs[3 * ps:3 * ps + 3], rows)
+            result = sh if result is None else self.xor(result, sh)
+        return result
 
     def combine(self, bits: list, combiner: str, any_mode: str, n: int) -> list:
         """src/engine.py:168-189."""
@@ -539,7 +552,7 @@ class Trio:
                   _lib.stream_ptr())
         opened = BitVector(host[:nw], rows)
         self.opened.append((self.label, opened))
-        audit.append((phase, opened.to_bits().copy()))
+        audit.append((phase, opened.to_bits()))
         k = int(kept.value)
         return k, [[o[:k] for o in per] for per in outs]
 
@@ -571,10 +584,11 @@ class Trio:
         self.label += 1
         host = ff.plain[: words_for(rows)].cpu().numpy().view(np.uint32)
         opened = BitVector(host, rows)
-        self.opened.append((self.label, opened))
-        audit.append(("fetch", opened.to_bits().copy()))
-        k = ff.kept()
+        k = opened.popcount()   # = the device count of kept rows, without a second synchronisation
+        # the record copies go to the device first; the host bookkeeping below overlaps them
         ids = [o[:k] if 2 * k >= rows else o[:k].clone() for o in ff.outs]
+        self.opened.append((self.label, opened))
+        audit.append(("fetch", opened.to_bits()))   # a fresh array (unpacked from the words)
         return TrioRecords(group.parent_slot, group.parent_record, k, group.id_width, ids, {}, {})
 
     def fetch_multi(self, group: TrioGroup, flags: list, audit: list, online_blinds=None) -> TrioRecords:

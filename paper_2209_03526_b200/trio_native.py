@@ -278,7 +278,7 @@ def match_native(trio, tokens: list, gshares: list, any_mode: str = "or"):
         o = opens[oi]
         bv = BitVector(bits[o.bits_off: o.bits_off + words_for(o.nbits)].copy(), int(o.nbits))
         trio.opened.append((int(o.label), bv))
-        audit.append(("fetch" if o.phase == 0 else "access", bv.to_bits().copy()))
+        audit.append(("fetch" if o.phase == 0 else "access", bv.to_bits()))
     views = [[_RecView(b.parent_slot, b.parent_record) for b, _ in recs] for recs in records]
     result = TrioResult(tokens[0].structure, records, _assemble(slots, views), audit)
     result._keep = (arena, keep)  # the record tensors are views into the arena
