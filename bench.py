@@ -43,6 +43,7 @@ from __future__ import annotations
 
 import argparse
 import ctypes
+import gc
 import json
 import os
 import statistics
@@ -368,7 +369,9 @@ def c5_legs(args, world: int) -> dict:
            "scaling": "weak (replicas)" if world > 1 else None, "shuffle": [], "fetch": []}
     torch.cuda.empty_cache()
     for lg in [int(x) for x in args.c5_logs.split(",") if x]:
+        gc.collect()
         sh = bench_configs.c5_shuffle_leg(lg, args.steps, args.warmup)
+        gc.collect()
         fe = bench_configs.c5_fetch_leg(lg, args.steps, args.warmup)
         for e, per_row in [(sh, 240)] + [(f, f["algorithmic_bytes_per_row"]) for f in fe]:
             e["ms"] = worst(e["ms"])
@@ -377,6 +380,7 @@ def c5_legs(args, world: int) -> dict:
             e["rows_per_s_all_ranks"] = world * e["rows"] / (e["ms"] * 1e-3)
         out["shuffle"].append(sh)
         out["fetch"].extend(fe)
+        gc.collect()
         torch.cuda.empty_cache()
     return out
 
@@ -385,6 +389,7 @@ def guarded(name: str, fn):
     """A secondary leg: its failure (an out-of-memory, a missing package) is
     recorded in the line instead of losing the headline.  Bit-exactness gates
     raise SystemExit and are NOT caught: a wrong result is never reported."""
+    gc.collect()   # the previous leg's garbage is collected here, never inside a timed region
     try:
         return fn()
     except Exception as exc:  # noqa: BLE001
@@ -428,6 +433,12 @@ def main():
         comm_ranks = int(ones.item())
     lib = _lib.load()
     _lib.check(lib.ogm_init())
+    # Automatic garbage collection is off for the GPU arm (timeit's convention): a generation-2
+    # collection left pending by the query leg's many small objects otherwise lands inside a later
+    # leg's timed loop and stalls its host-driven launches (C4 secEval 1.08 -> 3.1-4.2 ms measured);
+    # every leg starts with an explicit collection (guarded).
+    gc.collect()
+    gc.disable()
 
     K = args.keys
     comparison = args.kind == "dcf"

@@ -413,22 +413,21 @@ class Trio:
         per key."""
         parts = [list(zip(fss.key_parts_for_engine(f), fss.key_parts_for_engine(s))) for f, s in key_pairs]
         npass = len(parts[0])
-        inds = []
-        for ps in range(npass):
-            ck = (id(key_pairs[0][0]), ps)
-            if ck not in cache:
-                keys = [k for q in range(3) for k in parts[q][ps]]
-                by_kind: dict = {}
-                for i, k in enumerate(keys):
-                    by_kind.setdefault(fss.is_comparison(k), []).append(i)
-                rows = [None] * 6
-                for idxs in by_kind.values():
-                    fd = self._fde([keys[i] for i in idxs], domain)
-                    for j, i in enumerate(idxs):
-                        rows[i] = fd[j]
-                cache[ck] = rows
-            inds.append(cache[ck])
-        return inds
+        if any((id(key_pairs[0][0]), ps) not in cache for ps in range(npass)):
+            # every pass's keys at once, one full-domain launch per key kind (an interval's two
+            # passes are both DCF: one launch of 12 keys instead of two of 6)
+            keys = [k for ps in range(npass) for q in range(3) for k in parts[q][ps]]
+            by_kind: dict = {}
+            for i, k in enumerate(keys):
+                by_kind.setdefault(fss.is_comparison(k), []).append(i)
+            rows = [None] * len(keys)
+            for idxs in by_kind.values():
+                fd = self._fde([keys[i] for i in idxs], domain)
+                for j, i in enumerate(idxs):
+                    rows[i] = fd[j]
+            for ps in range(npass):
+                cache[(id(key_pairs[0][0]), ps)] = rows[6 * ps:6 * ps + 6]
+        return [cache[(id(key_pairs[0][0]), ps)] for ps in range(npass)]
 
     # a two-pass predicate as one parity pass over folded indicators (sec_eval)
     FOLD_PASSES = True
