@@ -220,13 +220,20 @@ __global__ void __launch_bounds__(256) keep_emit_kernel(const uint32_t* __restri
     const int wi = threadIdx.x / 32;
     const uint32_t below = (1u << lane) - 1u;
     int queued = 0;
+    // one kept row of every matrix: all loads issued before any store (the matrices may not
+    // alias, but the compiler cannot know it)
+    auto copy_row = [&](int64_t pos, int64_t row) {
+        uint4 v[kKeepMaxMats];
+#pragma unroll
+        for (int j = 0; j < kKeepMaxMats; j++)
+            if (j < m.n) v[j] = __ldcs(m.in[j] + row * m.pitch);
+#pragma unroll
+        for (int j = 0; j < kKeepMaxMats; j++)
+            if (j < m.n) __stcs(m.out[j] + pos * m.opitch, v[j]);
+    };
     auto flush = [&]() {
         __syncwarp();
-        for (int e = (int)lane; e < queued; e += 32) {
-            const int64_t pos = q_pos[wi][e];
-            const int64_t row = q_row[wi][e];
-            for (int j = 0; j < m.n; j++) __stcs(m.out[j] + pos * m.opitch, __ldcs(m.in[j] + row * m.pitch));
-        }
+        for (int e = (int)lane; e < queued; e += 32) copy_row(q_pos[wi][e], q_row[wi][e]);
         __syncwarp();
         queued = 0;
     };
@@ -247,6 +254,12 @@ __global__ void __launch_bounds__(256) keep_emit_kernel(const uint32_t* __restri
                 const uint32_t word = __shfl_sync(0xffffffffu, mine, k);
                 if (!word) continue;
                 const int off = __shfl_sync(0xffffffffu, excl, k);
+                if (word == 0xffffffffu) {   // 32 kept rows in a row: straight to their consecutive slots
+                    const int64_t pos = base + off + lane, row = (wb + k) * 32 + lane;
+                    if (out_idx) out_idx[pos] = (int32_t)row;
+                    if (m.n) copy_row(pos, row);
+                    continue;
+                }
                 const int n = __popc(word);
                 if (m.n && queued + n > kKeepQueue) flush();
                 if ((word >> lane) & 1u) {
