@@ -720,12 +720,38 @@ __device__ __forceinline__ int interior_field(const PackArgs& a, int64_t c) {
 // wide rows, NS share sets with 16-B aligned field rows: a CTA walks rows;
 // each thread issues every load of two 128-bit output groups (field words
 // of all sets + the XORed row) before it computes either, so twice the
-// bytes are in flight per warp.  NS = 0: unaligned fields, generic loads.
-template <int NS>
+// bytes are in flight per warp (four measured slower: registers halve the
+// occupancy).  Field words are read through L1 (a lane's second group is its
+// neighbour's first: evict-first loads re-read it from L2/DRAM, 8.6 vs 7.9 ms
+// at C3).  NS = 0: unaligned fields, generic loads.
+// TAB: the per-chunk field, shift and source offset -- the same for every row
+// -- computed once per CTA into a shared-memory table (8 B per 128-bit
+// output chunk, rows up to kPackTabChunks chunks) instead of per chunk and
+// row (the field search and 64-bit offset math made the kernel issue-bound:
+// ~250 warp instructions per chunk at C3).
+constexpr int kPackTabChunks = 6144;   // 48 KB of table: rows up to 98 KB
+
+template <int NS, bool TAB = false>
 __global__ void __launch_bounds__(256) pack_gather_rows_kernel(const PackArgs a) {
     const int64_t ow = (a.owidth + 31) >> 5;
     const int64_t ng = a.opitch >> 2;
     const int bd = blockDim.x;
+    extern __shared__ uint2 pk_tab[];   // TAB: x = (field + 1) | du << 8 | sh << 16, y = source group offset
+    if (TAB) {
+        for (int64_t c = threadIdx.x; c < ng; c += bd) {
+            const int f = interior_field(a, c);
+            uint2 e = make_uint2(0u, 0u);
+            if (f >= 0) {
+                const int64_t s0 = c * 128 - a.foff[f];
+                const int64_t q = s0 >> 5;
+                const int du = (int)(q & 3);
+                e = make_uint2((uint32_t)(f + 1) | ((uint32_t)du << 8) | ((uint32_t)(s0 & 31) << 16),
+                               (uint32_t)(q - du));
+            }
+            pk_tab[c] = e;
+        }
+        __syncthreads();
+    }
     for (int64_t i = blockIdx.x; i < a.rows; i += gridDim.x) {
         const int64_t src = a.idx ? (int64_t)__ldg(a.idx + i) : i;
         uint4* orow = reinterpret_cast<uint4*>(a.out + i * a.opitch);
@@ -747,24 +773,33 @@ __global__ void __launch_bounds__(256) pack_gather_rows_kernel(const PackArgs a)
                 for (int u = 0; u < 2; u++) {
                     const bool valid = cc[u] < ng;
                     rv[u] = (rrow && valid) ? __ldcs(rrow + cc[u]) : make_uint4(0, 0, 0, 0);
-                    const int f = valid ? interior_field(a, cc[u]) : -1;
-                    fu[u] = valid ? f : -2;
+                    int f;
                     int64_t base = 0;
                     shu[u] = du[u] = 0;
-                    if (f >= 0) {
-                        const int64_t s0 = cc[u] * 128 - a.foff[f];
-                        const int64_t q = s0 >> 5;
-                        shu[u] = (int)(s0 & 31);
-                        du[u] = (int)(q & 3);
-                        base = q - du[u];
+                    if (TAB) {
+                        const uint2 e = valid ? pk_tab[cc[u]] : make_uint2(0u, 0u);
+                        f = (int)(e.x & 0xffu) - 1;
+                        du[u] = (int)((e.x >> 8) & 3u);
+                        shu[u] = (int)((e.x >> 16) & 31u);
+                        base = (int64_t)e.y;
+                    } else {
+                        f = valid ? interior_field(a, cc[u]) : -1;
+                        if (f >= 0) {
+                            const int64_t s0 = cc[u] * 128 - a.foff[f];
+                            const int64_t q = s0 >> 5;
+                            shu[u] = (int)(s0 & 31);
+                            du[u] = (int)(q & 3);
+                            base = q - du[u];
+                        }
                     }
+                    fu[u] = valid ? f : -2;
 #pragma unroll
                     for (int s = 0; s < NS; s++) {
                         A[u][s] = B[u][s] = make_uint4(0, 0, 0, 0);
                         if (f >= 0) {
                             const uint4* row = reinterpret_cast<const uint4*>(a.f[s][f] + src * a.fpitch[s][f] + base);
-                            A[u][s] = __ldcs(row);
-                            if (du[u] || shu[u]) B[u][s] = __ldcs(row + 1);
+                            A[u][s] = __ldg(row);
+                            if (du[u] || shu[u]) B[u][s] = __ldg(row + 1);
                         }
                     }
                 }
@@ -1363,9 +1398,16 @@ static int pack_launch(int64_t rows, const int32_t* idx, int nsets, const uint32
     if (wide) {
         int64_t g = rows < (int64_t)sm_count() * 8 ? rows : (int64_t)sm_count() * 8;
         const int ns = vec ? nsets : 0;
-        auto kern = ns == 1 ? pack_gather_rows_kernel<1> : ns == 2 ? pack_gather_rows_kernel<2>
-                  : ns == 3 ? pack_gather_rows_kernel<3> : pack_gather_rows_kernel<0>;
-        kern<<<(int)g, 256, 0, as_stream(stream)>>>(a);
+        const int64_t ng = opitch / 4;
+        if (ns > 0 && ng <= kPackTabChunks) {
+            auto kern = ns == 1 ? pack_gather_rows_kernel<1, true> : ns == 2 ? pack_gather_rows_kernel<2, true>
+                      : pack_gather_rows_kernel<3, true>;
+            kern<<<(int)g, 256, (size_t)(ng * 8), as_stream(stream)>>>(a);
+        } else {
+            auto kern = ns == 1 ? pack_gather_rows_kernel<1> : ns == 2 ? pack_gather_rows_kernel<2>
+                      : ns == 3 ? pack_gather_rows_kernel<3> : pack_gather_rows_kernel<0>;
+            kern<<<(int)g, 256, 0, as_stream(stream)>>>(a);
+        }
     } else {
         pack_gather_kernel<<<grid_for(rows * opitch), 256, 0, as_stream(stream)>>>(a);
     }
