@@ -119,6 +119,39 @@ def test_flagged_fetch_matches_oracle(rows, p, plan, tail):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("rows", [1, 1000, (1 << 20) + 77])
+def test_flag_shuffle_trio_equals_composed(rows):
+    """ogm_flag_shuffle_trio (each party's bit gather on its own, the message
+    bits x1f / y1f / c1f materialised) and ogm_flag_open_composed (the steps
+    composed offline) give the same R3 flag column and opened column; the
+    per-step messages are the composition's intermediate terms."""
+    import torch
+
+    from paper_2209_03526_b200 import _lib
+    from paper_2209_03526_b200.fetch import FlaggedFetch, bit_gather
+
+    seeds = _seeds(bytes([0x6a, rows & 0xFF]) * 8)
+    _, flags, _ = _inputs(rows, 0.3, rows + 1)
+    ff = FlaggedFetch(seeds, 5, rows, plan=False)
+    p1, p2, p3 = ff.off
+    f = [_dev(x) for x in flags]
+    P = _lib.ptr
+    nw = (rows + 31) // 32
+    vec = lambda: torch.zeros((nw,), dtype=torch.int32, device="cuda")  # noqa: E731
+    x1f, y1f, c1f, r3f, plain = vec(), vec(), vec(), vec(), vec()
+    _lib.call("ogm_flag_shuffle_trio", rows, P(p1.k1), P(p2.pi12), P(p2.pi23), P(p3.k3), P(f[0]), P(f[1]), P(f[2]),
+              P(p1.flag["u"]), P(p2.flag["v"]), P(p2.flag["w"]), P(p3.flag["z"]), P(ff.r1f), P(ff.r2f), P(x1f),
+              P(y1f), P(c1f), P(r3f), P(plain), _lib.stream_ptr())
+    f12, c1g, r3g, plain_g = vec(), vec(), vec(), vec()
+    _lib.call("ogm_flag_open_composed", rows, P(ff.kc), P(ff.kr), P(f[0]), P(f[1]), P(f[2]), P(ff.uwf), P(ff.vzf),
+              P(ff.r1f), P(ff.r2f), P(f12), P(c1g), P(r3g), P(plain_g), _lib.stream_ptr())
+    assert torch.equal(r3f, r3g) and torch.equal(plain, plain_g) and torch.equal(c1f, c1g)
+    # the messages: x1f = f12[k1] ^ Uf (P1 -> P2), y1f = f3[pi12] ^ Vf (P2 -> P3)
+    assert torch.equal(x1f, bit_gather(f12, p1.k1, rows) ^ p1.flag["u"])
+    assert torch.equal(y1f, bit_gather(f[2], p2.pi12, rows) ^ p2.flag["v"])
+
+
+@pytest.mark.gpu
 def test_trio_fetch_multi_matches_reference_golden(golden):
     """Trio.fetch_multi (the split path for 128-bit ids) reproduces the live
     reference's records and opened flags at the C5 fetch shape."""
