@@ -441,11 +441,22 @@ class Trio:
         ck = (id(key_pairs[0][0]), "fold")
         if ck not in cache:
             p0, p1 = self._pass_indicators(key_pairs, domain, cache)
-            rows = []
-            for a, b in zip(p0, p1):
-                o = torch.empty_like(a)
-                _lib.call("ogm_xor_words", a.numel(), _lib.ptr(a), _lib.ptr(b), None, _lib.ptr(o), _lib.stream_ptr())
-                rows.append(o)
+            pitch = p0[1].data_ptr() - p0[0].data_ptr()
+            if pitch > 0 and all(r.data_ptr() == p0[0].data_ptr() + i * pitch for i, r in enumerate(p0 + p1)):
+                # both passes' rows are consecutive rows of one full-domain batch: one launch
+                n = 6 * pitch // 4
+                out = torch.empty((n,), dtype=torch.int32, device=self.dev)
+                _lib.call("ogm_xor_words", n, p0[0].data_ptr(), p1[0].data_ptr(), None, _lib.ptr(out),
+                          _lib.stream_ptr())
+                w = p0[0].numel()
+                rows = [out[i * (pitch // 4): i * (pitch // 4) + w] for i in range(6)]
+            else:
+                rows = []
+                for a, b in zip(p0, p1):
+                    o = torch.empty_like(a)
+                    _lib.call("ogm_xor_words", a.numel(), _lib.ptr(a), _lib.ptr(b), None, _lib.ptr(o),
+                              _lib.stream_ptr())
+                    rows.append(o)
             cache[ck] = rows
         return cache[ck]
 
