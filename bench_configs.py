@@ -32,8 +32,8 @@ from paper_2209_03526_b200.engine import CandidateGroup, EngineConfig, open_resu
 from paper_2209_03526_b200.graphs import device_trio, encrypt_graph  # noqa: E402
 from paper_2209_03526_b200.net import local_runtimes, make_session_configs, run_trio  # noqa: E402
 from paper_2209_03526_b200.query import gen_token, load_query  # noqa: E402
-from paper_2209_03526_b200.shuffle import (ShuffleOffline, blind_table, gather, shuffle_online_fused,  # noqa: E402
-                                            shuffle_online_planned)
+from paper_2209_03526_b200.shuffle import (FUSED_MAX_BYTES, ShuffleOffline, blind_table, gather,  # noqa: E402
+                                            shuffle_online_fused, shuffle_online_planned)
 from paper_2209_03526_b200.prf import seeded_permutation_device  # noqa: E402
 from paper_2209_03526_b200 import workloads  # noqa: E402
 from paper_2209_03526_b200.trio import TrioGroup  # noqa: E402
@@ -490,8 +490,8 @@ def run_c5(args):
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         pc = {(s, 0, rows): perms[s] for s in perms}
-        # measured: one cooperative launch wins up to 2^21 rows, the chained planned gathers from 2^22
-        fused = rows * 16 <= (32 << 20)
+        # measured: one cooperative launch wins up to 2^20 rows, the chained planned gathers from 2^21
+        fused = rows * 16 <= FUSED_MAX_BYTES
         off = [ShuffleOffline(p + 1, cfg[p].seed_with_next, cfg[p].seed_with_prev, 0, rows, width, perm_cache=pc,
                               plan=not fused)
                for p in range(3)]
@@ -643,7 +643,7 @@ def _bernoulli_bits(n: int, p: float, seed: int) -> torch.Tensor:
 def c5_shuffle_leg(lg: int, steps: int, warmup: int, seed: int = 1) -> dict:
     """C5 (BASELINE configs[4]): the three-party shuffle of 2^lg rows x 128
     bits, offline material prepared (ShuffleOffline), online phase timed:
-    one cooperative launch up to 2^21 rows, the chained planned gathers above.
+    one cooperative launch up to 2^20 rows, the chained planned gathers above.
     Gate: R1 ^ R2 ^ R3 == the plaintext table under the composed permutation,
     at full size, plus the oracle port's R3 bit for bit on a 2^16-row run."""
     import oracle
@@ -655,7 +655,7 @@ def c5_shuffle_leg(lg: int, steps: int, warmup: int, seed: int = 1) -> dict:
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     pc: dict = {}
-    fused = rows * 16 <= (32 << 20)
+    fused = rows * 16 <= FUSED_MAX_BYTES
     pairs = [(seeds[0], seeds[2]), (seeds[1], seeds[0]), (seeds[2], seeds[1])]
     off = [ShuffleOffline(p + 1, *pairs[p], 0, rows, 128, perm_cache=pc, plan=not fused) for p in range(3)]
     if not fused:

@@ -18,9 +18,9 @@ columns), so the message bits x1f / y1f exist only in flight and the column
 costs two random bit reads per row instead of four (ogm_flag_open_composed).
 
 Online phase (what the C5 fetch bench times):
-  1. up to 2^21 rows: the 16-byte three-party shuffle in one cooperative
+  1. up to 2^20 rows: the 16-byte three-party shuffle in one cooperative
      launch, then the composed flag column in one bit-gather launch (plus
-     f1 ^ f2), which also writes the opened column; from 2^22 rows: the
+     f1 ^ f2), which also writes the opened column; from 2^21 rows: the
      chained planned payload shuffle, then the same flag launches; above
      256 MB tables ONE call (ogm_fetch128_online_planned): the payload
      shuffle whose split final window passes also compute the flag column
@@ -37,10 +37,9 @@ import torch
 
 from . import _lib
 from .bits import words_for
-from .shuffle import (FLAG_ROW_BITS, ShuffleOffline, compose, flat_chain_args, run_table_args, shuffle_online_fused,
-                      shuffle_online_planned)
+from .shuffle import (FLAG_ROW_BITS, FUSED_MAX_BYTES, ShuffleOffline, compose, flat_chain_args, run_table_args,
+                      shuffle_online_fused, shuffle_online_planned)
 
-FUSED_MAX_BYTES = 32 << 20   # one cooperative launch up to 2^21 16-byte rows (measured crossover)
 FLAG_TAIL_MIN_BYTES = 256 << 20   # above: the flag column rides the split window passes
 
 

@@ -1,7 +1,7 @@
 """C5 online shuffle at one size, a few iterations (for ncu launch lists):
 python scripts/prof_c5_shuffle.py [log2 rows] [iterations]; OGM_GDST=1 reads
 gdst instead of the plans' run tables, OGM_FLAT_ORDER=slot runs the
-slot-order hand-over (A/B)."""
+slot-order hand-over, OGM_FUSED=0/1 forces the chained / one-launch path (A/B)."""
 
 import os
 import sys
@@ -14,7 +14,8 @@ sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
 import bench_configs as bc  # noqa: E402
 from paper_2209_03526_b200 import _lib, shuffle, workloads  # noqa: E402
 from paper_2209_03526_b200.net import make_session_configs  # noqa: E402
-from paper_2209_03526_b200.shuffle import ShuffleOffline, shuffle_online_fused, shuffle_online_planned  # noqa: E402
+from paper_2209_03526_b200.shuffle import (FUSED_MAX_BYTES, ShuffleOffline, shuffle_online_fused,  # noqa: E402
+                                           shuffle_online_planned)
 
 
 def main():
@@ -27,7 +28,7 @@ def main():
     cfg = make_session_configs(b"\x77" * 16)
     seeds = (cfg[0].seed_with_next, cfg[1].seed_with_next, cfg[2].seed_with_next)
     comps = [workloads.device_random_words(rows * 4, 1, 20 + c).reshape(rows, 4) for c in range(3)]
-    fused = rows * 16 <= (32 << 20)
+    fused = rows * 16 <= FUSED_MAX_BYTES if not os.environ.get("OGM_FUSED") else os.environ["OGM_FUSED"] == "1"
     pairs = [(seeds[0], seeds[2]), (seeds[1], seeds[0]), (seeds[2], seeds[1])]
     pc = {}
     off = [ShuffleOffline(p + 1, *pairs[p], 0, rows, 128, perm_cache=pc, plan=not fused) for p in range(3)]
