@@ -490,7 +490,7 @@ def run_c5(args):
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         pc = {(s, 0, rows): perms[s] for s in perms}
-        # measured: one cooperative launch wins up to 2^20 rows, the chained planned gathers from 2^21
+        # one cooperative launch up to 2^21 rows (shuffle.FUSED_MAX_BYTES), the chained planned gathers above
         fused = rows * 16 <= FUSED_MAX_BYTES
         off = [ShuffleOffline(p + 1, cfg[p].seed_with_next, cfg[p].seed_with_prev, 0, rows, width, perm_cache=pc,
                               plan=not fused)
@@ -643,7 +643,7 @@ def _bernoulli_bits(n: int, p: float, seed: int) -> torch.Tensor:
 def c5_shuffle_leg(lg: int, steps: int, warmup: int, seed: int = 1) -> dict:
     """C5 (BASELINE configs[4]): the three-party shuffle of 2^lg rows x 128
     bits, offline material prepared (ShuffleOffline), online phase timed:
-    one cooperative launch up to 2^20 rows, the chained planned gathers above.
+    one cooperative launch up to 2^21 rows, the chained planned gathers above.
     Gate: R1 ^ R2 ^ R3 == the plaintext table under the composed permutation,
     at full size, plus the oracle port's R3 bit for bit on a 2^16-row run."""
     import oracle

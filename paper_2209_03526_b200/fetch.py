@@ -18,9 +18,9 @@ columns), so the message bits x1f / y1f exist only in flight and the column
 costs two random bit reads per row instead of four (ogm_flag_open_composed).
 
 Online phase (what the C5 fetch bench times):
-  1. up to 2^20 rows: the 16-byte three-party shuffle in one cooperative
+  1. up to 2^21 rows: the 16-byte three-party shuffle in one cooperative
      launch, then the composed flag column in one bit-gather launch (plus
-     f1 ^ f2), which also writes the opened column; from 2^21 rows: the
+     f1 ^ f2), which also writes the opened column; from 2^22 rows: the
      chained planned payload shuffle, then the same flag launches; above
      256 MB tables ONE call (ogm_fetch128_online_planned): the payload
      shuffle whose split final window passes also compute the flag column
@@ -33,6 +33,7 @@ from __future__ import annotations
 
 import ctypes
 
+import numpy as np
 import torch
 
 from . import _lib
@@ -108,6 +109,11 @@ class FlaggedFetch:
         nb = int(_lib.load().ogm_keep_rows_workspace_bytes(rows))
         self.ws = torch.empty((nb,), dtype=torch.uint8, device=self.dev)
         self.count = torch.zeros((1,), dtype=torch.int64, device=self.dev)
+        # the opened column's and the kept count's host copies (pinned: a pageable copy stages
+        # through a bounce buffer and synchronises on its own)
+        pin = self.dev.type == "cuda"
+        self.plain_host = torch.empty((max(nw, 1),), dtype=torch.int32, pin_memory=pin)
+        self.count_host = torch.zeros((1,), dtype=torch.int64, pin_memory=pin)
 
     def online(self, flags: list, payload: list) -> None:
         """The three parties' online fetch over component flags [f1, f2, f3]
@@ -153,6 +159,15 @@ class FlaggedFetch:
         outs = (ctypes.c_void_p * 3)(*[P(o) for o in self.outs])
         _lib.call("ogm_keep_rows", rows, P(self.plain), 3, ctypes.addressof(mats), 4, ctypes.addressof(outs), 4,
                   None, P(self.count), P(self.ws), self.ws.numel(), _lib.stream_ptr())
+
+    def opened_host(self) -> tuple:
+        """(the opened flag column as uint32 words, the kept count) on the
+        host, both copied in one synchronisation of the current stream."""
+        nw = words_for(self.rows)
+        self.plain_host[:nw].copy_(self.plain[:nw], non_blocking=True)
+        self.count_host.copy_(self.count, non_blocking=True)
+        torch.cuda.current_stream(self.dev).synchronize()
+        return self.plain_host[:nw].numpy().view(np.uint32), int(self.count_host[0])
 
     def components(self) -> list:
         """The shuffled table's new components (R1, R2, R3): payload tables

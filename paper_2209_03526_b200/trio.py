@@ -592,11 +592,11 @@ class Trio:
                    rows2d(c).reshape(rows, -1)[:, :4].contiguous() for c in group.ids]
         ff.online(list(flags), payload)
         self.label += 1
-        host = ff.plain[: words_for(rows)].cpu().numpy().view(np.uint32)
-        opened = BitVector(host, rows)
-        k = opened.popcount()   # = the device count of kept rows, without a second synchronisation
-        # the record copies go to the device first; the host bookkeeping below overlaps them
-        ids = [o[:k] if 2 * k >= rows else o[:k].clone() for o in ff.outs]
+        words, k = ff.opened_host()   # the opened column and the kept count, one synchronisation
+        opened = BitVector(words, rows)   # copies the words
+        # the records are views of the fetch's row-sized outputs unless those would pin more than
+        # 256 MB for few rows (then copied); the host bookkeeping below overlaps the copies
+        ids = [o[:k] if 2 * k >= rows or 3 * rows * 16 <= (256 << 20) else o[:k].clone() for o in ff.outs]
         self.opened.append((self.label, opened))
         audit.append(("fetch", opened.to_bits()))   # a fresh array (unpacked from the words)
         return TrioRecords(group.parent_slot, group.parent_record, k, group.id_width, ids, {}, {})
