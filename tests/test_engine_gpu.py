@@ -729,3 +729,29 @@ def test_sharded_fold_and_keep_slices_on_device(world):
     for a, w_ in zip(acc, want):
         assert torch.equal(a, w_)
     assert kept == np.nonzero(bits)[0].tolist()
+
+
+def test_run_trio_party_threads_nested_and_errors():
+    """run_trio on the long-lived party threads: a run_trio from inside a
+    party (the threads are busy) falls back to fresh threads instead of
+    deadlocking, a party's failure is re-raised, and the threads serve the
+    next call afterwards."""
+    from paper_2209_03526_b200 import net
+
+    cfg = net.make_session_configs(b"\x11" * 16)
+
+    def outer(rt):
+        inner = net.run_trio(lambda r: r.index * 10, net.local_runtimes(net.make_session_configs(b"\x12" * 16)))
+        return rt.index, inner
+
+    res = net.run_trio(outer, net.local_runtimes(cfg))
+    assert [r[0] for r in res] == [1, 2, 3] and all(r[1] == [10, 20, 30] for r in res)
+
+    def bad(rt):
+        if rt.index == 2:
+            raise ValueError("boom")
+        return rt.index
+
+    with pytest.raises(ValueError, match="boom"):
+        net.run_trio(bad, net.local_runtimes(cfg))
+    assert net.run_trio(lambda rt: rt.index, net.local_runtimes(cfg)) == [1, 2, 3]
