@@ -403,7 +403,9 @@ int ogm_perm_invert(int64_t n, const int32_t* perm, int32_t* inv, void* stream);
  *           one contiguous run per output window of window_rows rows;
  *   pass 2: a gather whose random reads stay inside one contiguous window.
  * ogm_gather_plan derives q2, gdst (n int32 each) and srow (n uint16) from
- * idx; ogm_gather_window_rows / ogm_gather_tile_rows give the defaults for a
+ * idx (tile_rows <= 16384: each tile is sorted in shared memory, then the
+ * (tile, window) counts are scanned per window -- no library sort);
+ * ogm_gather_window_rows / ogm_gather_tile_rows give the defaults for a
  * pitch.  m2/m4 are source-order terms XORed in pass 1 (m4: an offline blind
  * already moved to source order), m3/r_mat output-order terms XORed in pass
  * 2 -- pass 2 keeps its window L2-resident only with at most one of them
@@ -411,7 +413,7 @@ int ogm_perm_invert(int64_t n, const int32_t* perm, int32_t* inv, void* stream);
  * Replaces a direct random-row gather step of src/shuffle.py:106-143. */
 int64_t ogm_gather_window_rows(int64_t pitch_words);
 int64_t ogm_gather_tile_rows(int64_t pitch_words);
-int64_t ogm_gather_plan_workspace_bytes(int64_t n);
+int64_t ogm_gather_plan_workspace_bytes(int64_t n, int64_t window_rows, int64_t tile_rows);
 int ogm_gather_plan(int64_t n, const int32_t* idx, int64_t window_rows, int64_t tile_rows, int32_t* q2,
                     int32_t* gdst, uint16_t* srow, void* workspace, int64_t workspace_bytes, void* stream);
 /* A plan's run table (offline): tile t's slots are grouped by destination

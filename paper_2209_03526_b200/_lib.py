@@ -84,7 +84,7 @@ SIGNATURES = {
     "ogm_perm_invert": ([_i64, _vp, _vp, _vp], _int),
     "ogm_gather_window_rows": ([_i64], _i64),
     "ogm_gather_tile_rows": ([_i64], _i64),
-    "ogm_gather_plan_workspace_bytes": ([_i64], _i64),
+    "ogm_gather_plan_workspace_bytes": ([_i64, _i64, _i64], _i64),
     "ogm_gather_plan": ([_i64, _vp, _i64, _i64, _vp, _vp, _vp, _vp, _i64, _vp], _int),
     "ogm_gather_plan_runs": ([_i64, _i64, _i64, _vp, _vp, _vp, _vp], _int),
     "ogm_gather_planned": ([_i64, _i64, _i64, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _int, _vp], _int),

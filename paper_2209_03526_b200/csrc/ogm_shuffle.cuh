@@ -2,7 +2,6 @@
 // secret-shared shuffle (src/shuffle.py:80-144) for sm_100a.
 #pragma once
 
-#include <cub/cub.cuh>
 
 #include "ogm_aes.cuh"
 #include "ogm_common.cuh"
@@ -477,36 +476,122 @@ __global__ void plan_inv_kernel(const int32_t* __restrict__ idx, int64_t n, int3
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) inv[__ldg(idx + i)] = (int32_t)i;
 }
 
-// key[j] = (tile of j) * nwin + (destination window of j); tile_rows = 0 drops the tile part
-__global__ void plan_keys_kernel(const int32_t* __restrict__ inv, int64_t n, int64_t Wr, int64_t T, int64_t nwin,
-                                 int32_t* __restrict__ key, int32_t* __restrict__ val) {
-    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += stride) {
-        const int64_t d = __ldg(inv + j) / Wr;
-        key[j] = (int32_t)(T ? (j / T) * nwin + d : d);
-        val[j] = (int32_t)j;
+// ---- plan construction without a global sort ------------------------------
+// The I-layout is a stable sort of the sources by destination window, and
+// the pass-1 slots a stable sort of each tile's sources by window.  Window d
+// receives exactly Wr sources (idx is a permutation), so source j's I row is
+// P(j) = d*Wr + (its rank among window d's sources) -- a sum over earlier
+// tiles of the (tile, window) counts plus its rank inside its tile.  So: one
+// shared-memory sort per tile (by (window, tile row): the slot order, run
+// starts and counts), a per-window scan of the counts over the tiles, then
+// P, gdst and q2 elementwise.  Hand-written, no library sort.
+constexpr int kPlanSortMax = 16384;   // tile rows sorted in shared memory (64-bit keys, 128 KB)
+
+// one CTA per tile (grid-stride): bitonic sort of key = window << 32 | tile row
+__global__ void __launch_bounds__(1024) plan_tile_sort_kernel(const int32_t* __restrict__ inv, int64_t n, int64_t T,
+                                                              int Tp, int64_t Wr, int64_t nwin,
+                                                              uint16_t* __restrict__ srow,
+                                                              int32_t* __restrict__ rstart,
+                                                              int32_t* __restrict__ rend) {
+    extern __shared__ __align__(16) unsigned long long pk[];
+    const int64_t ntiles = (n + T - 1) / T;
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        const int nt = (int)min(T, n - t * T);
+        for (int e = threadIdx.x; e < Tp; e += blockDim.x)
+            pk[e] = e < nt ? ((unsigned long long)(__ldg(inv + t * T + e) / Wr) << 32) | (unsigned)e : ~0ull;
+        __syncthreads();
+        for (int size = 2; size <= Tp; size <<= 1) {
+            for (int stride = size >> 1; stride > 0; stride >>= 1) {
+                for (int i = threadIdx.x; i < (Tp >> 1); i += blockDim.x) {
+                    const int lo = 2 * i - (i & (stride - 1)), hi = lo + stride;
+                    const unsigned long long a = pk[lo], b = pk[hi];
+                    if ((a > b) == ((lo & size) == 0)) {
+                        pk[lo] = b;
+                        pk[hi] = a;
+                    }
+                }
+                __syncthreads();
+            }
+        }
+        for (int k = threadIdx.x; k < nt; k += blockDim.x) {
+            const unsigned long long key = pk[k];
+            const int64_t d = (int64_t)(key >> 32);
+            srow[t * T + k] = (uint16_t)(key & 0xffffu);
+            if (k == 0 || (pk[k - 1] >> 32) != (unsigned long long)d) rstart[t * nwin + d] = k;
+            if (k == nt - 1 || (pk[k + 1] >> 32) != (unsigned long long)d) rend[t * nwin + d] = k + 1;
+        }
+        __syncthreads();   // the tile's keys are rewritten next
     }
 }
 
-__global__ void plan_pos_kernel(const int32_t* __restrict__ sj, int64_t n, int32_t* __restrict__ P) {
+// per-window scan of the (tile, window) counts over the tiles, in chunks of
+// kPlanScanChunk tiles: chunk sums, then their scan (+ d * Wr), then the
+// chunks' own scans -- leaving base[t][d] = the I row of run (t, d)'s first slot
+constexpr int kPlanScanChunk = 256;
+
+__global__ void plan_chunk_sums_kernel(const int32_t* __restrict__ rstart, const int32_t* __restrict__ rend,
+                                       int64_t ntiles, int64_t nwin, int64_t* __restrict__ csum) {
+    const int64_t nch = (ntiles + kPlanScanChunk - 1) / kPlanScanChunk;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < n; p += stride) P[__ldg(sj + p)] = (int32_t)p;
+    for (int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; x < nch * nwin; x += stride) {
+        const int64_t c = x / nwin, d = x - c * nwin;
+        int64_t s = 0;
+        const int64_t t1 = min(ntiles, (c + 1) * kPlanScanChunk);
+        for (int64_t t = c * kPlanScanChunk; t < t1; t++) s += rend[t * nwin + d] - rstart[t * nwin + d];
+        csum[x] = s;
+    }
+}
+
+__global__ void plan_chunk_scan_kernel(int64_t nch, int64_t nwin, int64_t Wr, int64_t* __restrict__ csum) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t d = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; d < nwin; d += stride) {
+        int64_t run = d * Wr;
+        for (int64_t c = 0; c < nch; c++) {
+            const int64_t v = csum[c * nwin + d];
+            csum[c * nwin + d] = run;
+            run += v;
+        }
+    }
+}
+
+// rend[t][d] becomes base[t][d] (the count is read first)
+__global__ void plan_chunk_bases_kernel(const int32_t* __restrict__ rstart, int32_t* __restrict__ rend,
+                                        int64_t ntiles, int64_t nwin, const int64_t* __restrict__ csum) {
+    const int64_t nch = (ntiles + kPlanScanChunk - 1) / kPlanScanChunk;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; x < nch * nwin; x += stride) {
+        const int64_t c = x / nwin, d = x - c * nwin;
+        int64_t run = csum[x];
+        const int64_t t1 = min(ntiles, (c + 1) * kPlanScanChunk);
+        for (int64_t t = c * kPlanScanChunk; t < t1; t++) {
+            const int64_t cnt = rend[t * nwin + d] - rstart[t * nwin + d];
+            rend[t * nwin + d] = (int32_t)run;
+            run += cnt;
+        }
+    }
+}
+
+// slot s of tile t holds tile row srow[s] (source j); its I row:
+// gdst[s] = base[t][d] + (s's offset in its run); P[j] = gdst[s]
+__global__ void plan_slots_kernel(const int32_t* __restrict__ inv, const uint16_t* __restrict__ srow, int64_t n,
+                                  int64_t T, int64_t Wr, int64_t nwin, const int32_t* __restrict__ rstart,
+                                  const int32_t* __restrict__ base, int32_t* __restrict__ gdst,
+                                  int32_t* __restrict__ P) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; s < n; s += stride) {
+        const int64_t t = s / T, k = s - t * T;
+        const int64_t j = t * T + __ldg(srow + s);
+        const int64_t d = __ldg(inv + j) / Wr;
+        const int32_t g = (int32_t)(__ldg(base + t * nwin + d) + (k - __ldg(rstart + t * nwin + d)));
+        gdst[s] = g;
+        P[j] = g;
+    }
 }
 
 __global__ void plan_q2_kernel(const int32_t* __restrict__ idx, const int32_t* __restrict__ P, int64_t n,
                                int32_t* __restrict__ q2) {
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) q2[i] = __ldg(P + __ldg(idx + i));
-}
-
-__global__ void plan_slots_kernel(const int32_t* __restrict__ sj2, const int32_t* __restrict__ P, int64_t n,
-                                  int64_t T, int32_t* __restrict__ gdst, uint16_t* __restrict__ srow) {
-    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += stride) {
-        const int32_t j = __ldg(sj2 + k);  // same tile as k: the sort key leads with the tile
-        gdst[k] = __ldg(P + j);
-        srow[k] = (uint16_t)(j % T);
-    }
 }
 
 // ---- run tables: pass-1 destinations without a per-row index --------------
@@ -1309,51 +1394,54 @@ int64_t ogm_gather_window_rows(int64_t pitch_words) {
 int64_t ogm_gather_tile_rows(int64_t pitch_words) {
     if (pitch_words <= 0) return 0;
     int64_t r = ogm::kPartSmemBytes / (4 * pitch_words);
-    if (r > 65536) r = 65536;
+    if (r > ogm::kPlanSortMax) r = ogm::kPlanSortMax;
     return r > 0 ? r : 1;
 }
 
-int64_t ogm_gather_plan_workspace_bytes(int64_t n) {
-    size_t temp = 0;
-    cub::DeviceRadixSort::SortPairs(nullptr, temp, (int32_t*)nullptr, (int32_t*)nullptr, (int32_t*)nullptr,
-                                    (int32_t*)nullptr, (int)(n > 0 ? n : 1));
-    return (int64_t)temp + 6 * 4 * n + 1024;
+int64_t ogm_gather_plan_workspace_bytes(int64_t n, int64_t window_rows, int64_t tile_rows) {
+    if (n <= 0 || window_rows < 1 || tile_rows < 1) return 256;
+    const int64_t nwin = (n + window_rows - 1) / window_rows, ntiles = (n + tile_rows - 1) / tile_rows;
+    const int64_t nch = (ntiles + ogm::kPlanScanChunk - 1) / ogm::kPlanScanChunk;
+    // inv, P; the (tile, window) run starts and ends/bases; the chunk sums
+    return 2 * 4 * n + 2 * 4 * ntiles * nwin + 8 * nch * nwin + 1024;
 }
 
 int ogm_gather_plan(int64_t n, const int32_t* idx, int64_t window_rows, int64_t tile_rows, int32_t* q2,
                     int32_t* gdst, uint16_t* srow, void* workspace, int64_t workspace_bytes, void* stream) {
     using namespace ogm;
     OGM_CHECK_ARG(n >= 0 && n < ((int64_t)1 << 31), OGM_ERR_ARG, "plan size out of range");
-    OGM_CHECK_ARG(window_rows >= 1 && tile_rows >= 1 && tile_rows <= 65536, OGM_ERR_ARG,
-                  "window_rows must be positive and tile_rows in [1, 65536]");
-    OGM_CHECK_ARG(workspace_bytes >= ogm_gather_plan_workspace_bytes(n), OGM_ERR_ARG, "plan workspace too small");
+    OGM_CHECK_ARG(window_rows >= 1 && tile_rows >= 1 && tile_rows <= kPlanSortMax, OGM_ERR_ARG,
+                  "window_rows must be positive and tile_rows in [1, %d]", kPlanSortMax);
+    OGM_CHECK_ARG(workspace_bytes >= ogm_gather_plan_workspace_bytes(n, window_rows, tile_rows), OGM_ERR_ARG,
+                  "plan workspace too small");
     if (n == 0) return OGM_OK;
+    OGM_CHECK_ARG(idx && q2 && gdst && srow && workspace, OGM_ERR_ARG, "idx, the plan outputs and workspace are required");
     const int64_t nwin = (n + window_rows - 1) / window_rows;
     const int64_t ntiles = (n + tile_rows - 1) / tile_rows;
-    OGM_CHECK_ARG(ntiles * nwin < ((int64_t)1 << 31), OGM_ERR_ARG, "%lld tiles x %lld windows overflow the sort key",
-                  (long long)ntiles, (long long)nwin);
+    const int64_t nch = (ntiles + kPlanScanChunk - 1) / kPlanScanChunk;
     cudaStream_t st = as_stream(stream);
     int32_t* inv = (int32_t*)workspace;
-    int32_t* key = inv + n;
-    int32_t* val = key + n;
-    int32_t* skey = val + n;
-    int32_t* sval = skey + n;
-    int32_t* P = sval + n;
-    void* temp = (void*)(((uintptr_t)(P + n) + 255) & ~(uintptr_t)255);
-    size_t temp_bytes = (size_t)(workspace_bytes - ((uint8_t*)temp - (uint8_t*)workspace));
-    auto bits_for = [](int64_t m) { int b = 1; while ((m - 1) >> b) b++; return b; };
+    int32_t* P = inv + n;
+    int32_t* rstart = P + n;
+    int32_t* rend = rstart + ntiles * nwin;
+    int64_t* csum = (int64_t*)(((uintptr_t)(rend + ntiles * nwin) + 7) & ~(uintptr_t)7);
     const int g = grid_for(n);
     plan_inv_kernel<<<g, 256, 0, st>>>(idx, n, inv);
-    // I-layout: sources grouped by destination window, source order inside (LSD radix sort is stable)
-    plan_keys_kernel<<<g, 256, 0, st>>>(inv, n, window_rows, 0, nwin, key, val);
-    OGM_CUDA_TRY(cub::DeviceRadixSort::SortPairs(temp, temp_bytes, key, skey, val, sval, (int)n, 0, bits_for(nwin), st));
-    plan_pos_kernel<<<g, 256, 0, st>>>(sval, n, P);
+    OGM_CUDA_TRY(cudaMemsetAsync(rstart, 0, (size_t)(2 * 4 * ntiles * nwin), st));   // empty runs: count 0
+    int Tp = 1;
+    while (Tp < tile_rows) Tp <<= 1;
+    const int smem = Tp * 8;
+    OGM_CUDA_TRY(allow_big_smem(plan_tile_sort_kernel, smem));
+    const int gt = (int)std::min<int64_t>(ntiles, (int64_t)sm_count() * (smem <= (48 << 10) ? 4 : 1));
+    plan_tile_sort_kernel<<<gt, std::min(1024, std::max(32, Tp / 2)), smem, st>>>(inv, n, tile_rows, Tp,
+                                                                                   window_rows, nwin, srow, rstart,
+                                                                                   rend);
+    const int gc = grid_for(nch * nwin);
+    plan_chunk_sums_kernel<<<gc, 256, 0, st>>>(rstart, rend, ntiles, nwin, csum);
+    plan_chunk_scan_kernel<<<grid_for(nwin), 256, 0, st>>>(nch, nwin, window_rows, csum);
+    plan_chunk_bases_kernel<<<gc, 256, 0, st>>>(rstart, rend, ntiles, nwin, csum);
+    plan_slots_kernel<<<g, 256, 0, st>>>(inv, srow, n, tile_rows, window_rows, nwin, rstart, rend, gdst, P);
     plan_q2_kernel<<<g, 256, 0, st>>>(idx, P, n, q2);
-    // pass-1 slots: each tile's rows grouped by destination window, source order inside
-    plan_keys_kernel<<<g, 256, 0, st>>>(inv, n, window_rows, tile_rows, nwin, key, val);
-    OGM_CUDA_TRY(cub::DeviceRadixSort::SortPairs(temp, temp_bytes, key, skey, val, sval, (int)n, 0,
-                                                 bits_for(ntiles * nwin), st));
-    plan_slots_kernel<<<g, 256, 0, st>>>(sval, P, n, tile_rows, gdst, srow);
     OGM_LAUNCH_CHECK();
     return OGM_OK;
 }

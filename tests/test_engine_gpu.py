@@ -755,3 +755,30 @@ def test_run_trio_party_threads_nested_and_errors():
     with pytest.raises(ValueError, match="boom"):
         net.run_trio(bad, net.local_runtimes(cfg))
     assert net.run_trio(lambda rt: rt.index, net.local_runtimes(cfg)) == [1, 2, 3]
+
+
+@pytest.mark.parametrize("n,window,tile", [(1, 1, 1), (100, 7, 16), (5000, 333, 100), (70_001, 4096, 1024),
+                                           (1 << 20, 1 << 17, 4096), ((1 << 20) + 77, 1 << 18, 16384),
+                                           (123457, 1, 4096)])
+def test_gather_plan_matches_stable_sorts(n, window, tile):
+    """ogm_gather_plan (per-tile shared-memory sorts + per-window scans, no
+    library sort) equals its definition: I rows = the sources stably sorted
+    by destination window, slots = each tile's sources stably sorted by
+    window, q2 = the I row of idx[i] (numpy stable argsorts)."""
+    from paper_2209_03526_b200.shuffle import GatherPlan
+
+    g = torch.Generator(device="cuda").manual_seed(n + window)
+    idx = torch.randperm(n, device="cuda", generator=g).to(torch.int32)
+    plan = GatherPlan(idx, 4, window_bytes=window * 16, tile_rows=tile)
+    ih = idx.cpu().numpy().astype(np.int64)
+    inv = np.empty(n, np.int64)
+    inv[ih] = np.arange(n)
+    d = inv // window
+    order = np.argsort(d, kind="stable")            # sources in I order
+    P = np.empty(n, np.int64)
+    P[order] = np.arange(n)
+    t = np.arange(n) // tile
+    slots = np.lexsort((np.arange(n), d, t))       # by tile, then window, then source
+    assert np.array_equal(plan.q2.cpu().numpy(), P[ih])
+    assert np.array_equal(plan.gdst.cpu().numpy(), P[slots])
+    assert np.array_equal(plan.srow.cpu().numpy().view(np.uint16).astype(np.int64), slots % tile)
