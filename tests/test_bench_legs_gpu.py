@@ -44,3 +44,46 @@ def test_c4_root_slot_small(bc, rows):
 def test_c4_sec_eval_gate(bc):
     e = bc.c4_sec_eval(100_000, 1, 1, 1, 0, 1)
     assert e["parity_gate"]["equal_to_oracle"]
+
+
+def _c4_gloo_worker(rank, world, port, out_dir):
+    import json
+    import os
+
+    import torch
+    import torch.distributed as dist
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    torch.cuda.set_device(0)
+    import bench_configs
+    from paper_2209_03526_b200 import _lib
+    _lib.check(_lib.load().ogm_init())
+    sec = bench_configs.c4_sec_eval(200_000, 1, 1, 1, rank, world)
+    slot = bench_configs.c4_root_slot(200_000, 1, 1, 1, rank, world)
+    with open(os.path.join(out_dir, f"r{rank}.json"), "w") as f:
+        json.dump({"sec_gate": (sec.get("parity_gate") or {}).get("equal_to_oracle"), "slot_gate": slot["gate"],
+                   "kept": slot["kept"], "matches": slot["matches"], "n_gpus": sec["n_gpus"]}, f)
+    dist.destroy_process_group()
+
+
+def test_c4_legs_two_gloo_ranks(tmp_path):
+    """bench.py's C4 legs (sharded secEval with its N-rank parity gate, and
+    the sharded root slot) under a 2-rank process group -- the code the
+    driver's multi-GPU bench runs -- over gloo on one GPU (collectives staged
+    through the host; a logic check, not a timing)."""
+    import json
+    import socket
+
+    import torch.multiprocessing as mp
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    mp.spawn(_c4_gloo_worker, args=(2, port, str(tmp_path)), nprocs=2, join=True)
+    r0 = json.loads((tmp_path / "r0.json").read_text())
+    r1 = json.loads((tmp_path / "r1.json").read_text())
+    assert r0["sec_gate"] is True and r0["n_gpus"] == 2
+    for r in (r0, r1):
+        assert all(r["slot_gate"].values()), r
+        assert r["kept"] == r["matches"] == r0["matches"]
