@@ -66,7 +66,7 @@ LOOKUPS = {"dcf": 31 * (160 + 133) + 133, "dpf": 32 * (160 + 133)}
 OPS_PER_LOOKUP = 2
 # dram__bytes_read.sum + dram__bytes_write.sum of one fss_eval_kernel launch at
 # 2^24 DCF keys (profiles/r01_fss_eval_full_ncu.csv): 8,877,741,568 + 5,532,672
-NCU_TRAFFIC = {("dcf", DEFAULT_KEYS): 8877741568 + 5532672}
+NCU_TRAFFIC = {("dcf", DEFAULT_KEYS): 8877250000 + 6400768}   # profiles/r02_fss_eval_ncu.txt (read + write)
 
 
 def parse():
@@ -507,7 +507,7 @@ def main():
     roofline = {"bound": "int_alu", "achieved": achieved / 1e12, "peak": peak.value / 1e12,
                 "unit": "Tops/s", "frac": achieved / peak.value,
                 "traffic": NCU_TRAFFIC.get((args.kind, K)),
-                "traffic_source": "ncu dram__bytes_read+write per launch, profiles/r01_fss_eval_full_ncu.csv",
+                "traffic_source": "ncu --set full dram__bytes_read+write per launch, profiles/r02_fss_eval_ncu.txt",
                 "algorithmic_key_bytes_per_launch": K * (16 + 16 * (BITS - (1 if comparison else 0)) + 12 + 1 + 4),
                 "binding_pipe": "LSU (shared-memory T-table lookups) 93.5% / ALU 83.7% of peak (ncu)",
                 "ops_per_eval": ops_per_eval, "aes_lookups_per_eval": LOOKUPS[args.kind],
