@@ -87,3 +87,29 @@ def test_c4_legs_two_gloo_ranks(tmp_path):
     for r in (r0, r1):
         assert all(r["slot_gate"].values()), r
         assert r["kept"] == r["matches"] == r0["matches"]
+
+
+def test_bench_json_contract_small():
+    """bench.py end to end at a small key count (secondary legs off): one JSON
+    line carrying the contract's keys -- metric, value, ms_per_step, roofline,
+    cpu_baseline, e2e with its byte counts, gpu_launches and clocks."""
+    import json
+    import subprocess
+    import sys
+    from pathlib import Path
+
+    root = Path(__file__).resolve().parent.parent
+    out = subprocess.run([sys.executable, "bench.py", "--keys", "65536", "--steps", "3", "--warmup", "3",
+                          "--no-c3", "--no-c4", "--no-c5", "--no-live-ref", "--no-query", "--cpu-seconds", "0.5"],
+                         cwd=root, capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [ln for ln in out.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better",
+              "dtype", "config", "roofline", "cpu_baseline", "e2e", "gpu_launches", "clocks"):
+        assert k in d, k
+    assert d["n_gpus"] == 1 and d["steps"] == 3 and d["value"] > 0 and d["gpu_launches"] == 3
+    assert 0 < d["roofline"]["frac"] and d["roofline"]["unit"] == "Tops/s"
+    assert d["e2e"]["h2d_bytes_per_step"] > 0 and d["e2e"]["d2h_bytes_per_step"] > 0
+    assert d["cpu_baseline"]["kind"] == "port" and d["cpu_baseline"]["value"] > 0
