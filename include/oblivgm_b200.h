@@ -165,7 +165,8 @@ int ogm_zero_share_trio_slice2(const uint8_t* k1, const uint8_t* k2, const uint8
                                const uint32_t* const* xor_into1, uint32_t* const* out1,
                                const uint32_t* const* xor_into2, uint32_t* const* out2, void* stream);
 
-/* The two passes of an interval predicate folded (co-resident trio): a
+/* The two passes of an interval predicate folded (co-resident trio;
+ * src/engine.py:150-165 with src/rss.py:143-148,164-176): a
  * re-share is a zero share XORed in and parity is linear, so the XOR of the
  * two passes' re-shared parities equals ONE parity over XORed indicators
  * with both zero shares XORed in.  out = xor_into ^ zs(counter1) ^
@@ -305,7 +306,9 @@ int ogm_flag_shuffle_trio(int64_t rows, const int32_t* k1, const int32_t* pi12, 
                           const uint32_t* r1f, const uint32_t* r2f, uint32_t* x1f, uint32_t* y1f, uint32_t* c1f,
                           uint32_t* r3f, uint32_t* plain, void* stream);
 
-/* The flag column of the co-resident trio, each party's step composed with
+/* The flag column of the co-resident trio (src/shuffle.py:106-143 on bit 0
+ * of the fetch rows, then the open of src/engine.py:241-247 /
+ * src/rss.py:184-206), each party's step composed with
  * the next one's (as the payload's flat hand-over composes them: the message
  * bits x1f / y1f exist only in flight), so two random bit reads per row
  * instead of four:
@@ -416,7 +419,8 @@ int64_t ogm_gather_tile_rows(int64_t pitch_words);
 int64_t ogm_gather_plan_workspace_bytes(int64_t n, int64_t window_rows, int64_t tile_rows);
 int ogm_gather_plan(int64_t n, const int32_t* idx, int64_t window_rows, int64_t tile_rows, int32_t* q2,
                     int32_t* gdst, uint16_t* srow, void* workspace, int64_t workspace_bytes, void* stream);
-/* A plan's run table (offline): tile t's slots are grouped by destination
+/* A plan's run table (offline; the planned form of a src/shuffle.py:106-143
+ * gather step): tile t's slots are grouped by destination
  * window with the I rows of a (tile, window) run consecutive, so
  * gdst[s] = off[t*OS + d] + s for global slot s in run d of tile t.
  * start[t*SS + d] (uint16) = the tile slot where run d begins (an empty run:
