@@ -69,6 +69,31 @@ def test_sec_eval_matches_reference(golden, padded):
         assert np.array_equal(rss.reconstruct(res).to_bits(), g[f"{tag}_plain"])
 
 
+@pytest.mark.parametrize("fold", [True, False])
+@pytest.mark.parametrize("padded", [False, True])
+def test_trio_sec_eval_matches_reference(golden, fold, padded, monkeypatch):
+    """Trio.sec_eval (all three parties at once; an interval's two passes
+    folded into one parity pass, or not) returns exactly the reference's
+    per-party output shares: party p holds components (p, p + 1) -- every
+    recorded case, including intervals on the TMA-staged parity path."""
+    from paper_2209_03526_b200.graphs import padded_device_matrix
+    from paper_2209_03526_b200.trio import Trio, TrioGroup
+
+    monkeypatch.setattr(Trio, "FOLD_PASSES", fold)
+    g = golden("engine")
+    for tag in g["ev_cases"]:
+        count, domain = int(g[f"{tag}_count"]), int(g[f"{tag}_domain"])
+        attr = [padded_device_matrix(g[f"{tag}_attr{c}"]) if padded else dev(g[f"{tag}_attr{c}"]) for c in range(3)]
+        ids = [torch.zeros((count, (count + 31) // 32), dtype=torch.int32, device="cuda") for _ in range(3)]
+        group = TrioGroup(None, None, count, count, ids, {"a": attr}, {"a": domain})
+        keys = [(fss.parse_key(g[f"{tag}_key{p}_0"].tobytes()), fss.parse_key(g[f"{tag}_key{p}_1"].tobytes()))
+                for p in range(3)]
+        res = Trio(g[f"{tag}_master"].tobytes()).sec_eval(group, keys, "a", domain, {})
+        for p in range(3):
+            assert np.array_equal(host(res[p]), g[f"{tag}_out{p}_a"]), (tag, p)
+            assert np.array_equal(host(res[(p + 1) % 3]), g[f"{tag}_out{p}_b"]), (tag, p)
+
+
 def test_combine_matches_reference(golden):
     g = golden("engine")
     for tag in g["cb_cases"]:
