@@ -323,6 +323,20 @@ int ogm_flag_open_composed(int64_t rows, const int32_t* kc, const int32_t* kr, c
                            const uint32_t* r1f, const uint32_t* r2f, uint32_t* f12, uint32_t* c1f, uint32_t* r3f,
                            uint32_t* plain, void* stream);
 
+/* The online phase of a flag-split fetch of <= 2^21 rows in ONE cooperative
+ * launch: the three-party shuffle of ogm_shuffle_online_fused (x1 / y1:
+ * scratch tables; R3 out) and, in its second phase, the composed flag column
+ * and the open of ogm_flag_open_composed (f12: scratch; r3f and plain out).
+ * Same results as those two calls (src/shuffle.py:80-144 on the fetch rows,
+ * src/engine.py:241-247). */
+int ogm_fetch128_online_fused(int64_t rows, const int32_t* k1, const int32_t* pi12, const int32_t* pi23,
+                              const int32_t* k3, const uint32_t* a, const uint32_t* b, const uint32_t* c,
+                              const uint32_t* U, const uint32_t* V, const uint32_t* W, const uint32_t* Z,
+                              uint32_t* x1, uint32_t* y1, uint32_t* r3, const int32_t* kc, const int32_t* kr,
+                              const uint32_t* f1, const uint32_t* f2, const uint32_t* f3, const uint32_t* uwf,
+                              const uint32_t* vzf, const uint32_t* r1f, const uint32_t* r2f, uint32_t* f12,
+                              uint32_t* r3f, uint32_t* plain, void* stream);
+
 /* The online phase of a flag-split fetch shuffle for >= 2^22 rows in one
  * call: f12 = f1 ^ f2, then the chained planned payload shuffle (as
  * ogm_shuffle_online_planned_slots) whose final window passes also compute

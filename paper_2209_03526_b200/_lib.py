@@ -77,6 +77,7 @@ SIGNATURES = {
     "ogm_flag_shuffle_trio": ([_i64] + [_vp] * 19, _int),
     "ogm_fetch128_online_planned": ([_i64] + [_vp] * 14 + [_int, _vp, _int] + [_vp] * 16, _int),
     "ogm_flag_open_composed": ([_i64] + [_vp] * 14, _int),
+    "ogm_fetch128_online_fused": ([_i64] + [_vp] * 27, _int),
     "ogm_shuffle_online_planned_slots": ([_i64] + [_vp] * 14 + [_int, _vp, _int] + [_vp] * 3, _int),
     "ogm_shuffle_gather": ([_i64, _i64, _i64, _vp, _vp, _vp, _vp, _vp, _cp, _cp, _u64, _vp, _cp, _cp, _u64,
                             _vp, _cp, _cp, _u64, _vp, _i64, _i64, _vp, _vp], _int),

@@ -114,6 +114,55 @@ __global__ void __launch_bounds__(256) flag_shuffle2_kernel(
     }
 }
 
+// ---- the whole fetch shuffle in one cooperative launch (<= 2^21 rows) -------
+// ogm_shuffle_online_fused's two phases with the composed flag column of
+// ogm_flag_open_composed folded in: phase 1 also XORs P1's two flag
+// components, phase 2 -- which walks the rows in output order anyway -- also
+// gathers the two composed flag bits per row and writes the new component's
+// flag column and the opened column (one ballot per warp).  Two launches fewer
+// than the separate shuffle + flag kernels.
+struct Fetch4Flags {
+    const int32_t *kc, *kr;
+    const uint32_t *f1, *f2, *f3, *uwf, *vzf, *r1f, *r2f;
+    uint32_t *f12, *r3f, *plain;
+};
+
+__global__ void __launch_bounds__(256) fetch128_coop_kernel(const Shuffle4Args p, const Fetch4Flags q) {
+    namespace cg = cooperative_groups;
+    cg::grid_group grid = cg::this_grid();
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    const int64_t t0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t nw = (p.rows + 31) >> 5;
+    for (int64_t w = t0; w < nw; w += stride) q.f12[w] = __ldg(q.f1 + w) ^ __ldg(q.f2 + w);
+    for (int64_t i = t0; i < p.rows; i += stride) {
+        const int64_t k = __ldg(p.k1 + i), j = __ldg(p.pi12 + i);
+        p.x1[i] = xor4(xor4(__ldcg(p.a + k), __ldcg(p.b + k)), __ldcs(p.U + i));
+        p.y1[i] = xor4(__ldcg(p.c + j), __ldcs(p.V + i));
+    }
+    grid.sync();
+    const int lane = threadIdx.x & 31;
+    for (int64_t base = t0 - lane; base < p.rows; base += stride) {   // warp-uniform: the ballots need every lane
+        const int64_t i = base + lane;
+        uint32_t bc = 0, br = 0;
+        if (i < p.rows) {
+            const uint4 c = xor4(__ldcg(p.x1 + __ldg(p.pi23 + i)), __ldcs(p.W + i));
+            if (p.c1) p.c1[i] = c;
+            p.r3[i] = xor4(xor4(__ldcg(p.y1 + __ldg(p.k3 + i)), c), __ldcs(p.Z + i));
+            const int32_t jc = __ldcs(q.kc + i), jr = __ldcs(q.kr + i);
+            bc = (__ldcg(q.f12 + (jc >> 5)) >> (jc & 31)) & 1u;   // written above: no read-only path
+            br = (__ldg(q.f3 + (jr >> 5)) >> (jr & 31)) & 1u;
+        }
+        const uint32_t wc = __ballot_sync(0xffffffffu, bc), wr = __ballot_sync(0xffffffffu, br);
+        if (lane == 0) {
+            const int64_t w = base >> 5;
+            const uint32_t cw = wc ^ __ldg(q.uwf + w);
+            const uint32_t r = wr ^ cw ^ __ldg(q.vzf + w);
+            q.r3f[w] = r;
+            q.plain[w] = __ldg(q.r1f + w) ^ __ldg(q.r2f + w) ^ r;
+        }
+    }
+}
+
 // ---- public compaction: keep the rows whose opened bit is set, in order ----
 // Three launches, no library: per-chunk popcounts (one warp per chunk of
 // 32..256 mask words, sized for >= 4096 chunks so every SM has warps),
@@ -385,6 +434,41 @@ int ogm_fetch128_online_planned(int64_t rows, const int32_t* const* q2, const in
     return shuffle_online_planned_impl(rows, q2, gdst, srow, a, b, c, u_src, v_src, 0, w_blind, w_order, z_slot,
                                        z_order, inter, nullptr, nullptr, nullptr, r3, &ft, qs, runs ? rt : nullptr,
                                        wrows, stream);
+}
+
+// One cooperative launch: the shuffle of ogm_shuffle_online_fused (x1 / y1
+// scratch tables, R3 out) and the composed flag column of
+// ogm_flag_open_composed (f12 scratch; r3f and the opened column out).
+int ogm_fetch128_online_fused(int64_t rows, const int32_t* k1, const int32_t* pi12, const int32_t* pi23,
+                              const int32_t* k3, const uint32_t* a, const uint32_t* b, const uint32_t* c,
+                              const uint32_t* U, const uint32_t* V, const uint32_t* W, const uint32_t* Z,
+                              uint32_t* x1, uint32_t* y1, uint32_t* r3, const int32_t* kc, const int32_t* kr,
+                              const uint32_t* f1, const uint32_t* f2, const uint32_t* f3, const uint32_t* uwf,
+                              const uint32_t* vzf, const uint32_t* r1f, const uint32_t* r2f, uint32_t* f12,
+                              uint32_t* r3f, uint32_t* plain, void* stream) {
+    using namespace ogm;
+    OGM_CHECK_ARG(rows >= 0 && rows < ((int64_t)1 << 31), OGM_ERR_ARG, "rows out of range");
+    const void* ptrs[] = {a, b, c, U, V, W, Z, x1, y1, r3};
+    for (const void* q : ptrs)
+        OGM_CHECK_ARG(q && (((uintptr_t)q) & 15) == 0, OGM_ERR_ARG, "16-byte aligned tables are required");
+    const void* need[] = {k1, pi12, pi23, k3, kc, kr, f1, f2, f3, uwf, vzf, r1f, r2f, f12, r3f, plain};
+    for (const void* q : need)
+        OGM_CHECK_ARG(q, OGM_ERR_ARG, "permutations, composed indices, flag columns and scratch are required");
+    if (rows == 0) return OGM_OK;
+    OGM_ENSURE_INIT();
+    Shuffle4Args p{k1, pi12, pi23, k3, (const uint4*)a, (const uint4*)b, (const uint4*)c, (const uint4*)U,
+                   (const uint4*)V, (const uint4*)W, (const uint4*)Z, (uint4*)x1, (uint4*)y1, nullptr,
+                   (uint4*)r3, rows};
+    Fetch4Flags q{kc, kr, f1, f2, f3, uwf, vzf, r1f, r2f, f12, r3f, plain};
+    int per_sm = 0;
+    OGM_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fetch128_coop_kernel, 256, 0));
+    int64_t g = (int64_t)sm_count() * std::max(per_sm, 1);
+    const int64_t need_g = (rows + 255) / 256;
+    if (g > need_g) g = need_g;
+    void* args[] = {&p, &q};
+    OGM_CUDA_TRY(cudaLaunchCooperativeKernel((const void*)fetch128_coop_kernel, dim3((unsigned)g), dim3(256), args, 0,
+                                             as_stream(stream)));
+    return OGM_OK;
 }
 
 int64_t ogm_keep_rows_workspace_bytes(int64_t rows) {

@@ -18,10 +18,12 @@ columns), so the message bits x1f / y1f exist only in flight and the column
 costs two random bit reads per row instead of four (ogm_flag_open_composed).
 
 Online phase (what the C5 fetch bench times):
-  1. up to 2^21 rows: the 16-byte three-party shuffle in one cooperative
-     launch, then the composed flag column in one bit-gather launch (plus
-     f1 ^ f2), which also writes the opened column; from 2^22 rows: the
-     chained planned payload shuffle, then the same flag launches; above
+  1. up to 2^20 rows: ONE cooperative launch (ogm_fetch128_online_fused):
+     the 16-byte three-party shuffle, whose second phase also gathers the
+     composed flag column and writes the opened column; at 2^21 rows the
+     cooperative shuffle, then the composed flag launch; from 2^22 rows: the
+     chained planned payload shuffle, then the composed flag launch (plus
+     f1 ^ f2, ogm_flag_open_composed); above
      256 MB tables ONE call (ogm_fetch128_online_planned): the payload
      shuffle whose split final window passes also compute the flag column
      and the opened column (they walk the rows in output order anyway);
@@ -41,6 +43,9 @@ from .bits import words_for
 from .shuffle import (FLAG_ROW_BITS, FUSED_MAX_BYTES, ShuffleOffline, compose, flat_chain_args, run_table_args,
                       shuffle_online_fused, shuffle_online_planned)
 
+# up to 16 MB tables the flag column rides the cooperative shuffle launch (measured 2^16 / 2^18 rows:
+# 0.042 / 0.053 ms against 0.057 / 0.071 ms in two launches; even at 2^20, 2% slower at 2^21)
+FUSED_FLAGS_MAX_BYTES = 16 << 20
 FLAG_TAIL_MIN_BYTES = 256 << 20   # above: the flag column rides the split window passes
 
 
@@ -131,7 +136,13 @@ class FlaggedFetch:
             if t.shape != (rows, 4) or not t.is_contiguous():
                 raise ValueError("payload components must be contiguous (rows, 4) tables")
         P = _lib.ptr
-        if self.fused or not self.flag_tail:
+        if self.fused and rows * 16 <= FUSED_FLAGS_MAX_BYTES:
+            # one cooperative launch: the shuffle, the composed flag column and the open
+            _lib.call("ogm_fetch128_online_fused", rows, P(p1.k1), P(p2.pi12), P(p2.pi23), P(p3.k3), P(a), P(b),
+                      P(c), P(p1.u), P(p2.v), P(p2.w), P(p3.z), P(self.inter[0]), P(self.inter[1]), P(self.r3),
+                      P(self.kc), P(self.kr), P(flags[0]), P(flags[1]), P(flags[2]), P(self.uwf), P(self.vzf),
+                      P(self.r1f), P(self.r2f), P(self.f12), P(self.r3f), P(self.plain), _lib.stream_ptr())
+        elif self.fused or not self.flag_tail:
             if self.fused:
                 shuffle_online_fused(self.off, a, b, c, self.inter[0], self.inter[1], None, self.r3)
             else:

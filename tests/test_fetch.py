@@ -82,6 +82,7 @@ def _inputs(rows: int, p: float, seed: int):
 @pytest.mark.gpu
 @pytest.mark.parametrize("rows,p,plan,tail", [(1, 1.0, False, None), (33, 0.5, False, None),
                                               (1000, 0.1, False, None), (1 << 20, 0.1, False, None),
+                                              ((1 << 20) + 77, 0.2, False, None), (1 << 21, 0.05, False, None),
                                               (1 << 20, 0.01, True, None), ((1 << 20) + 77, 1.0, True, None),
                                               (40000, 0.0, True, None), ((1 << 20) + 77, 0.3, True, True),
                                               (1 << 22, 0.1, True, True), ((1 << 24) + 33, 0.05, None, None)])
