@@ -98,6 +98,38 @@ class TrioRecords:
     attr_widths: dict
 
 
+def one_hot_rows(x: np.ndarray, shapes: list) -> list:
+    """Decode reconstructed one-hot rows (src/bits.py hot_index, as
+    src/engine.py:458-500 applies it per record) for many fields at once:
+    ``x`` holds the fields' (rows, words) uint32 matrices back to back, row
+    major, ``shapes`` their shapes.  Per field, a list with the set bit's
+    index per row (None for an all-zero row); a row with more than one bit set
+    raises, naming the first such row's weight (fields in order)."""
+    counts = [int(r) for r, _ in shapes]
+    widths = np.repeat(np.array([int(w) for _, w in shapes], np.int64), counts)
+    nrows = widths.size
+    hot = np.full(nrows, -1, np.int64)
+    pos = np.flatnonzero(widths > 0)              # rows that own words
+    if pos.size and x.size:
+        starts = np.zeros(nrows, np.int64)
+        np.cumsum(widths[:-1], out=starts[1:])
+        st = starts[pos]                          # strictly increasing; the last row ends at x's end
+        weight = np.add.reduceat(np.bitwise_count(x), st, dtype=np.int64)
+        bad = weight > 1
+        if bad.any():
+            raise ValueError(f"expected Hamming weight <= 1, got {int(weight[bad][0])}")
+        nz = np.flatnonzero(x)                    # at most one set word per row
+        r = np.searchsorted(st, nz, side="right") - 1
+        v = x[nz]
+        hot[pos[r]] = (nz - st[r]) * 32 + np.bitwise_count(v - np.uint32(1))
+    flat = hot.tolist()
+    out, o = [], 0
+    for c in counts:
+        out.append([None if h < 0 else h for h in flat[o:o + c]])
+        o += c
+    return out
+
+
 @dataclass
 class TrioResult:
     structure: dict
@@ -109,9 +141,10 @@ class TrioResult:
         """engine.open_results(self.party_results()[:2], schema) -- the same
         (matches, details) -- straight from the record batches: ONE
         device-to-host copy of every batch matrix of the three components, then
-        vectorised XOR and one-hot decoding per batch (src/engine.py:458-500)."""
+        one XOR and one one-hot decoding for every batch at once (one_hot_rows;
+        src/engine.py:458-500)."""
         slots = self.structure["slots"]
-        order, mats = [], []
+        order, mats = [], [[], [], []]
         for s, slot in enumerate(slots):
             names = sorted({p["attr"] for p in slot["preds"]})
             seen = {}
@@ -123,21 +156,14 @@ class TrioResult:
                                                                  for a in names]
                 for name, comps, width in fields:
                     order.append((s, id(batch), name, comps[0].shape))
-                    mats += [c.reshape(-1) for c in comps]
-        host = torch.cat(mats).cpu().numpy().view(np.uint32) if mats else np.zeros(0, np.uint32)
-        plain, off = {}, 0
-        for s, bid, name, shape in order:
-            n = int(np.prod(shape))
-            c = [host[off + q * n: off + (q + 1) * n].reshape(shape) for q in range(3)]
-            off += 3 * n
-            x = c[0] ^ c[1] ^ c[2]
-            weight = np.bitwise_count(x).sum(axis=1) if x.size else np.zeros(shape[0], np.int64)
-            if (weight > 1).any():
-                raise ValueError(f"expected Hamming weight <= 1, got {int(weight[weight > 1][0])}")
-            word = np.argmax(x != 0, axis=1) if x.size else np.zeros(shape[0], np.int64)
-            val = x[np.arange(shape[0]), word] if x.size else np.zeros(shape[0], np.uint32)
-            hot = word * 32 + np.log2(np.maximum(val, 1)).astype(np.int64)
-            plain[(s, bid, name)] = [None if w == 0 else int(h) for w, h in zip(weight, hot)]
+                    for q in range(3):
+                        mats[q].append(comps[q].reshape(-1))
+        # component-major: every field of component 0, then 1, then 2 -- one XOR for all fields
+        host = (torch.cat(mats[0] + mats[1] + mats[2]).cpu().numpy().view(np.uint32) if mats[0]
+                else np.zeros(0, np.uint32))
+        h = host.reshape(3, -1)
+        hots = one_hot_rows(h[0] ^ h[1] ^ h[2], [sh for *_, sh in order])
+        plain = {(s, bid, name): hot for (s, bid, name, _), hot in zip(order, hots)}
         decoded = []
         for s, slot in enumerate(slots):
             ts = schema.types[slot["type"]]

@@ -250,13 +250,16 @@ def match_native(trio, tokens: list, gshares: list, any_mode: str = "or"):
 
     base = arena.data_ptr()
     a32 = arena.view(torch.int32)
+    n32 = a32.numel()
 
     def view(ptr, rows, pitch, width):
         w = words_for(width)
         if rows == 0:
             return torch.zeros((0, w), dtype=torch.int32, device=trio.dev)
         off = (ptr - base) // 4
-        return a32[off: off + rows * pitch].view(rows, pitch)[:, :w]
+        if off < 0 or off + rows * pitch > n32:
+            raise RuntimeError("ogm_trio_match returned a record matrix outside its arena")
+        return torch.as_strided(a32, (rows, w), (pitch, 1), off)   # one op: rows of the pitched matrix
 
     records: list = [[] for _ in slots]
     for bi in range(out.nbatches):

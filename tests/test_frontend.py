@@ -132,3 +132,37 @@ def test_graph_parse_errors_match_reference(reference):
         except GraphFormatError as exc:
             with_mine = str(exc)
         assert with_mine == with_ref, text
+
+
+def test_one_hot_rows_matches_hot_index():
+    """TrioResult.open's batched decoding (trio.one_hot_rows) equals
+    BitVector.hot_index (src/bits.py) row by row: random one-hot and all-zero
+    rows over fields of different widths, empty fields included, and the
+    weight > 1 error names the first offending row's weight."""
+    import pytest
+
+    from paper_2209_03526_b200.bits import BitVector
+    from paper_2209_03526_b200.trio import one_hot_rows
+
+    rng = np.random.default_rng(7)
+    shapes = [(5, 1), (0, 3), (17, 4), (1, 33), (0, 0), (9, 2)]
+    mats = []
+    for rows, w in shapes:
+        m = np.zeros((rows, w), np.uint32)
+        for r in range(rows):
+            if w and rng.random() < 0.8:
+                b = int(rng.integers(0, 32 * w))
+                m[r, b // 32] = np.uint32(1) << np.uint32(b % 32)
+        mats.append(m)
+    x = np.concatenate([m.reshape(-1) for m in mats])
+    got = one_hot_rows(x, shapes)
+    want = [[BitVector(m[r], 32 * m.shape[1]).hot_index() if m.shape[1] else None for r in range(m.shape[0])]
+            for m in mats]
+    assert got == want
+    assert one_hot_rows(np.zeros(0, np.uint32), []) == []
+    bad = [m.copy() for m in mats]
+    bad[2][3] = 0
+    bad[2][3, 0] = 0b1011
+    bad[5][0, 1] = 0b11
+    with pytest.raises(ValueError, match="expected Hamming weight <= 1, got 3"):
+        one_hot_rows(np.concatenate([m.reshape(-1) for m in bad]), shapes)
