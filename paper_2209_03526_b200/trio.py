@@ -188,6 +188,14 @@ class TrioResult:
 
     def party_results(self) -> list:
         """Per-party MatchResultSet views (same layout as engine.sec_match)."""
+        views: dict = {}
+
+        def rows_of(mats):   # every component's row views, one unbind per matrix
+            r = views.get(id(mats))
+            if r is None:
+                r = views[id(mats)] = [m.unbind(0) for m in mats]
+            return r
+
         out = []
         for q in range(3):
             recs = []
@@ -195,7 +203,8 @@ class TrioResult:
                 lst = []
                 for batch, i in slot:
                     def sv(c, width):
-                        return SharedBitVector(q + 1, DBits(c[q][i], width), DBits(c[_nxt(q)][i], width))
+                        r = rows_of(c)
+                        return SharedBitVector(q + 1, DBits(r[q][i], width), DBits(r[_nxt(q)][i], width))
                     lst.append(MatchedRecord(batch.parent_slot, batch.parent_record, sv(batch.ids, batch.id_width),
                                              {a: sv(batch.attrs[a], batch.attr_widths[a]) for a in batch.attrs}))
                 recs.append(lst)
